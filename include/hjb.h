@@ -1,0 +1,250 @@
+/*
+ * hjb.h — C ABI of the B200-native Hamilton-Jacobi reachability solver.
+ *
+ * This is the drop-in boundary for the reference library's solver API
+ * (hjsafe, `proj/include/hjsafe/solver.hpp:45-77`).  Every entry point below
+ * replaces one reference function; the citation is given next to it.  All
+ * signatures use plain C types: pointers, sizes and POD descriptors — no C++
+ * or torch types cross this boundary.
+ *
+ * Conventions
+ *  - Fields are fp64, row-major, last axis fastest (reference
+ *    `proj/src/grid.cpp:27-30`).
+ *  - Functions without a suffix take HOST pointers (the reference's
+ *    `ScalarField` / `IntervalField` storage) and copy to/from the GPU inside
+ *    the call.  Functions with the `_dev` suffix take DEVICE pointers so warm
+ *    and adaptive chains stay resident in HBM.
+ *  - Every call returns an `int` status (hjb_status).  The message of the
+ *    last failure on the calling thread is returned by hjb_last_error().
+ *    HJB_ERR_INVALID_ARGUMENT maps to the reference's std::invalid_argument,
+ *    HJB_ERR_RUNTIME / HJB_ERR_DIVERGED to std::runtime_error
+ *    (`proj/src/solver.cpp:14-17,194-199,279-280,291-295,318-322,367-369`).
+ *  - A context (hjb_context) owns a CUDA stream and device workspaces.  A
+ *    context must not be used by two threads at once; independent contexts
+ *    may run concurrently (the reference's solve is re-entrant,
+ *    `proj/src/sim.cpp:340-363`).
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    call fails with HJB_ERR_CUDA.
+ */
+#ifndef HJB_H_
+#define HJB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HJB_MAX_DIMS 6   /* grid rank supported by the device kernels */
+#define HJB_MAX_STATE 10 /* reference kMaxStateDim, dynamics.hpp:12 */
+#define HJB_MAX_INPUT 3  /* reference kMaxInputDim, dynamics.hpp:13 */
+
+typedef enum hjb_status {
+  HJB_OK = 0,
+  HJB_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  HJB_ERR_RUNTIME = 2,          /* std::runtime_error (e.g. zero flow)     */
+  HJB_ERR_CUDA = 3,             /* no device / CUDA failure                */
+  HJB_ERR_UNSUPPORTED = 4,      /* valid for the reference, not on device  */
+  HJB_ERR_DIVERGED = 5,         /* std::runtime_error "solve: diverging"   */
+  HJB_ERR_NCCL = 6
+} hjb_status;
+
+/* ---------------------------------------------------------------- grid */
+/* GridDim, reference grid.hpp:11-17 (same field order). */
+typedef struct hjb_grid_dim {
+  double min;
+  double max;
+  int64_t n;
+} hjb_grid_dim;
+
+/* Grid, reference grid.hpp:23-48.  spacing = (max-min)/(n-1)
+ * (grid.cpp:24); coord(d,k) = k==n-1 ? max : min + k*spacing
+ * (grid.cpp:33-38). */
+typedef struct hjb_grid {
+  int32_t ndims;
+  int32_t reserved;
+  hjb_grid_dim dims[HJB_MAX_DIMS];
+} hjb_grid;
+
+/* Interval, reference dynamics.hpp:16-19. */
+typedef struct hjb_interval {
+  double lo;
+  double hi;
+} hjb_interval;
+
+/* ------------------------------------------------------------- dynamics */
+/* Control-affine dynamics f(x,u,d) = drift(x) + B u + C d (reference
+ * AffineFlow, dynamics.hpp:24-33) with an additively separable drift:
+ *   drift_i(x) = term0_i(x) + term1_i(x)      (term1 optional)
+ * Each term depends on one coordinate and is evaluated with the reference
+ * model's own expression, so the device consumes identical bits:
+ *   COORD: scale * x[axis]          e.g. x[1], -d1*theta   (dynamics.cpp:139)
+ *   TAN:   scale * tan(x[axis])     g*tan(theta)           (dynamics.cpp:138)
+ *   CONST: scale                    -g, gravity+k_offset   (dynamics.cpp:129,148)
+ *   TABLE: table[k_axis]            user-tabulated f(x_axis), one entry per node
+ * Every model of the reference (dynamics.cpp:126-198) has this form. */
+typedef enum hjb_term_kind {
+  HJB_TERM_NONE = 0,
+  HJB_TERM_COORD = 1,
+  HJB_TERM_TAN = 2,
+  HJB_TERM_CONST = 3,
+  HJB_TERM_TABLE = 4
+} hjb_term_kind;
+
+typedef struct hjb_drift_term {
+  int32_t kind;
+  int32_t axis;
+  double scale;
+  const double* table; /* host pointer, HJB_TERM_TABLE only */
+} hjb_drift_term;
+
+typedef struct hjb_model {
+  int32_t state_dim;
+  int32_t control_dim;
+  int32_t disturbance_dim;
+  int32_t reserved;
+  hjb_drift_term drift[HJB_MAX_STATE][2];
+  double control[HJB_MAX_STATE][HJB_MAX_INPUT];     /* B, row per state */
+  double disturbance[HJB_MAX_STATE][HJB_MAX_INPUT]; /* C, row per state */
+  hjb_interval ubounds[HJB_MAX_INPUT];              /* control_bounds() */
+} hjb_model;
+
+/* IntervalField, reference interval_field.hpp:11-42: per channel [lo,hi]
+ * either constant (IntervalField::constant, interval_field.cpp:16-27) or one
+ * value per node.  Per-node pointers live in the same memory space as the
+ * field pointers of the call (host for plain calls, device for _dev). */
+typedef struct hjb_dbounds {
+  int32_t channels;
+  int32_t per_node;
+  hjb_interval constant[HJB_MAX_INPUT];
+  const double* lo[HJB_MAX_INPUT];
+  const double* hi[HJB_MAX_INPUT];
+} hjb_dbounds;
+
+/* --------------------------------------------------------------- solver */
+typedef enum hjb_scheme { HJB_GODUNOV = 0, HJB_LAX_FRIEDRICHS = 1 } hjb_scheme;
+typedef enum hjb_dissipation { HJB_PER_NODE = 0, HJB_GLOBAL = 1 } hjb_dissipation;
+
+/* SolveConfig, reference solver.hpp:12-25, plus the B200 extensions
+ * (spatial/time order, time horizon, target set). */
+typedef struct hjb_solve_config {
+  double cfl_factor;     /* (0,1], default 0.8 */
+  double tolerance;      /* > 0, default 1e-3 */
+  int64_t max_iters;     /* default 20000 */
+  int32_t scheme;        /* hjb_scheme, default Godunov */
+  int32_t dissipation;   /* hjb_dissipation, default per-node */
+  int32_t spatial_order; /* 1 = reference first order; 2 = ENO2; 3 = ENO3 */
+  int32_t time_order;    /* 1 = forward Euler (reference); 2/3 = TVD-RK */
+  double time_horizon;   /* > 0: also stop once iterations*dt >= horizon */
+  int32_t threads;       /* reference CPU knob; accepted and ignored */
+  int32_t flags;         /* reserved, 0 */
+} hjb_solve_config;
+
+/* SolveResult, reference solver.hpp:27-36.  The value field is written to
+ * the caller's buffer; histories are written to caller buffers of
+ * `history_capacity` entries (may be NULL / 0). */
+typedef struct hjb_solve_result {
+  int64_t iterations;
+  double dt;
+  double wall_seconds;  /* device time of the iteration loop */
+  int32_t converged;
+  int32_t reserved;
+  int64_t nodes_per_sweep;
+  double final_residual;
+  double* residual_history; /* max|dV|/dt per iteration */
+  double* wall_ms_history;  /* cumulative device ms per iteration */
+  int64_t history_capacity;
+} hjb_solve_result;
+
+typedef struct hjb_context hjb_context;
+
+/* ------------------------------------------------------------ lifecycle */
+const char* hjb_version(void);
+const char* hjb_last_error(void);
+void hjb_solve_config_default(hjb_solve_config* cfg);
+int hjb_context_create(int device, hjb_context** out);
+int hjb_context_destroy(hjb_context* ctx);
+int hjb_device_count(int* out);
+
+/* ------------------------------------------------------------ solver API */
+/* cfl_dt, reference solver.hpp:48-49 / solver.cpp:272-282. */
+int hjb_cfl_dt(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+               const hjb_dbounds* dbounds, double cfl_factor, double* dt_out);
+
+/* vi_step, reference solver.hpp:55-57 / solver.cpp:284-308. */
+int hjb_vi_step(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                const hjb_dbounds* dbounds, const double* value, const double* constraint,
+                double dt, const hjb_solve_config* cfg, double* out);
+
+/* solve, reference solver.hpp:63-65 / solver.cpp:310-376. */
+int hjb_solve(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+              const hjb_dbounds* dbounds, const double* init, const double* constraint,
+              const hjb_solve_config* cfg, double* value_out, hjb_solve_result* result);
+
+/* solve_coarse_to_fine, reference solver.hpp:70-74 / solver.cpp:387-425.
+ * warm_init_fine may be NULL (cold coarse stage). */
+int hjb_solve_coarse_to_fine(hjb_context* ctx, const hjb_grid* fine_grid,
+                             const hjb_model* model, const hjb_dbounds* dbounds_fine,
+                             const double* constraint_fine, const hjb_grid* coarse_grid,
+                             const hjb_solve_config* cfg, const double* warm_init_fine,
+                             double* coarse_value_out, hjb_solve_result* coarse_result,
+                             double* fine_value_out, hjb_solve_result* fine_result,
+                             double* wall_seconds);
+
+/* ------------------------------------------------ grid / level-set helpers */
+/* resample (multilinear), reference grid.hpp:108-109 / grid.cpp:215-231. */
+int hjb_resample(hjb_context* ctx, const hjb_grid* src_grid, const double* src,
+                 const hjb_grid* dst_grid, double* dst);
+
+/* max_adjacent_jump, reference grid.hpp:104 / grid.cpp:197-213. */
+int hjb_max_adjacent_jump(hjb_context* ctx, const hjb_grid* grid, const double* field,
+                          double* out);
+
+/* seed_from lambda, reference solver.cpp:404-411:
+ *   dst = max(resample(src) - max_adjacent_jump(src), constraint_dst). */
+int hjb_seed_from(hjb_context* ctx, const hjb_grid* src_grid, const double* src,
+                  const hjb_grid* dst_grid, const double* constraint_dst, double* dst);
+
+/* signed_distance_band, reference levelset.hpp:31 / levelset.cpp:54-66. */
+int hjb_signed_distance_band(hjb_context* ctx, const hjb_grid* grid, int32_t dim, double lo,
+                             double hi, double* out);
+
+/* ------------------------------------------- device-resident (_dev) API */
+int hjb_vi_step_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                    const hjb_dbounds* dbounds, const double* value, const double* constraint,
+                    double dt, const hjb_solve_config* cfg, double* out);
+
+int hjb_solve_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                  const hjb_dbounds* dbounds, const double* init, const double* constraint,
+                  const hjb_solve_config* cfg, double* value_out, hjb_solve_result* result);
+
+int hjb_resample_dev(hjb_context* ctx, const hjb_grid* src_grid, const double* src,
+                     const hjb_grid* dst_grid, double* dst);
+
+int hjb_max_adjacent_jump_dev(hjb_context* ctx, const hjb_grid* grid, const double* field,
+                              double* out);
+
+int hjb_seed_from_dev(hjb_context* ctx, const hjb_grid* src_grid, const double* src,
+                      const hjb_grid* dst_grid, const double* constraint_dst, double* dst);
+
+int hjb_signed_distance_band_dev(hjb_context* ctx, const hjb_grid* grid, int32_t dim,
+                                 double lo, double hi, double* out);
+
+/* Elementwise max/min (field_max/field_min, levelset.cpp:81-95). */
+int hjb_field_max_dev(hjb_context* ctx, int64_t n, const double* a, const double* b,
+                      double* out);
+int hjb_field_min_dev(hjb_context* ctx, int64_t n, const double* a, const double* b,
+                      double* out);
+
+/* Stream of the context (cudaStream_t as void*) and synchronisation. */
+void* hjb_context_stream(hjb_context* ctx);
+int hjb_context_synchronize(hjb_context* ctx);
+
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t hjb_context_launch_count(hjb_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HJB_H_ */

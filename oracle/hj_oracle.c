@@ -1,0 +1,794 @@
+/*
+ * hj_oracle.c — TEST INFRASTRUCTURE ONLY (see hj_oracle.h).
+ *
+ * Plain-C restatement of the reference solver hot path.  Arithmetic follows
+ * the reference expression by expression (same operand order, same
+ * ternaries, the zero-coefficient accumulations of dim_slopes/flow_bounds/
+ * hamiltonian kept), so that built with -ffp-contract=off it is bitwise equal
+ * to the reference compiled the same way.  OpenMP only splits the node loop;
+ * every reduction is a max, so results do not depend on the thread count
+ * (reference parallel.hpp:16-21 determinism contract).
+ */
+#include "hj_oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static __thread char g_err[256];
+static int g_threads = 0;
+
+const char* hjo_last_error(void) { return g_err; }
+void hjo_set_threads(int threads) { g_threads = threads; }
+
+static int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+/* std::max / std::min as libstdc++ defines them (a<b ? b : a, b<a ? b : a) */
+#define STD_MAX(a, b) ((a) < (b) ? (b) : (a))
+#define STD_MIN(a, b) ((b) < (a) ? (b) : (a))
+
+/* ------------------------------------------------------------------ grid */
+typedef struct {
+  int nd;
+  int64_t n[HJB_MAX_DIMS];
+  double min[HJB_MAX_DIMS], max[HJB_MAX_DIMS], spacing[HJB_MAX_DIMS];
+  int64_t stride[HJB_MAX_DIMS];
+  int64_t size;
+} grid_t;
+
+/* Grid::Grid, grid.cpp:10-31 */
+static int grid_init(const hjb_grid* g, grid_t* o) {
+  if (g->ndims < 1) return fail(HJB_ERR_INVALID_ARGUMENT, "Grid: ndims must be >= 1");
+  if (g->ndims > HJB_MAX_DIMS) return fail(HJB_ERR_UNSUPPORTED, "Grid: too many dims");
+  o->nd = g->ndims;
+  o->size = 1;
+  for (int i = 0; i < o->nd; ++i) {
+    const hjb_grid_dim* d = &g->dims[i];
+    if (!(d->min < d->max)) return fail(HJB_ERR_INVALID_ARGUMENT, "Grid: min must be < max");
+    if (d->n < 2) return fail(HJB_ERR_INVALID_ARGUMENT, "Grid: need at least 2 nodes");
+    if (!isfinite(d->min) || !isfinite(d->max))
+      return fail(HJB_ERR_INVALID_ARGUMENT, "Grid: non-finite bounds");
+    o->n[i] = d->n;
+    o->min[i] = d->min;
+    o->max[i] = d->max;
+    o->spacing[i] = (d->max - d->min) / (double)(d->n - 1);
+    o->size *= d->n;
+  }
+  o->stride[o->nd - 1] = 1;
+  for (int i = o->nd - 1; i-- > 0;) o->stride[i] = o->stride[i + 1] * o->n[i + 1];
+  return 0;
+}
+
+static int grid_same(const hjb_grid* a, const hjb_grid* b) {
+  if (a->ndims != b->ndims) return 0;
+  for (int i = 0; i < a->ndims; ++i)
+    if (a->dims[i].min != b->dims[i].min || a->dims[i].max != b->dims[i].max ||
+        a->dims[i].n != b->dims[i].n)
+      return 0;
+  return 1;
+}
+
+/* Grid::coord, grid.cpp:33-38 */
+static inline double coord(const grid_t* g, int d, int64_t k) {
+  if (k == g->n[d] - 1) return g->max[d];
+  return g->min[d] + (double)k * g->spacing[d];
+}
+
+/* Grid::unravel, grid.cpp:52-57 */
+static inline void unravel(const grid_t* g, int64_t lin, int64_t* idx) {
+  for (int i = 0; i < g->nd; ++i) {
+    idx[i] = lin / g->stride[i];
+    lin -= idx[i] * g->stride[i];
+  }
+}
+
+static inline void odometer(const grid_t* g, int64_t* idx) {
+  for (int d = g->nd; d-- > 0;) {
+    if (++idx[d] < g->n[d]) break;
+    idx[d] = 0;
+  }
+}
+
+/* -------------------------------------------------------------- dynamics */
+typedef struct {
+  int n, m, p;
+  double drift[HJB_MAX_STATE];
+  const double (*B)[HJB_MAX_INPUT];
+  const double (*C)[HJB_MAX_INPUT];
+} affine_t;
+
+static int model_check(const hjb_model* m) {
+  if (m->state_dim < 1 || m->state_dim > HJB_MAX_STATE || m->control_dim < 0 ||
+      m->control_dim > HJB_MAX_INPUT || m->disturbance_dim < 0 ||
+      m->disturbance_dim > HJB_MAX_INPUT)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "model: bad dimensions");
+  return 0;
+}
+
+static inline double term_value(const hjb_drift_term* t, const double* x, const int64_t* idx) {
+  switch (t->kind) {
+    case HJB_TERM_COORD: return t->scale * x[t->axis];
+    case HJB_TERM_TAN: return t->scale * tan(x[t->axis]);
+    case HJB_TERM_CONST: return t->scale;
+    case HJB_TERM_TABLE: return idx ? t->table[idx[t->axis]] : NAN;
+    default: return 0.0;
+  }
+}
+
+/* Model::affine (dynamics.cpp:126-198 for the stock models): drift terms,
+ * AffineFlow::reset zero-fills (dynamics.cpp:9-16) so absent rows are 0.0. */
+static inline void model_affine(const hjb_model* m, const double* x, const int64_t* idx,
+                                affine_t* af) {
+  af->n = m->state_dim;
+  af->m = m->control_dim;
+  af->p = m->disturbance_dim;
+  af->B = m->control;
+  af->C = m->disturbance;
+  for (int i = 0; i < af->n; ++i) {
+    const hjb_drift_term* t = m->drift[i];
+    double v = 0.0;
+    if (t[0].kind != HJB_TERM_NONE) {
+      v = term_value(&t[0], x, idx);
+      if (t[1].kind != HJB_TERM_NONE) v = v + term_value(&t[1], x, idx);
+    }
+    af->drift[i] = v;
+  }
+}
+
+/* extremal_inputs + hamiltonian, dynamics.cpp:37-83 */
+static double hamiltonian(const affine_t* f, const double* p, const hjb_interval* ub,
+                          const hjb_interval* db) {
+  double u[HJB_MAX_INPUT], d[HJB_MAX_INPUT];
+  for (int j = 0; j < f->m; ++j) {
+    double coeff = 0.0;
+    for (int i = 0; i < f->n; ++i) coeff += p[i] * f->B[i][j];
+    u[j] = coeff > 0.0 ? ub[j].lo : (coeff < 0.0 ? ub[j].hi : ub[j].lo);
+  }
+  for (int k = 0; k < f->p; ++k) {
+    double coeff = 0.0;
+    for (int i = 0; i < f->n; ++i) coeff += p[i] * f->C[i][k];
+    d[k] = coeff > 0.0 ? db[k].hi : (coeff < 0.0 ? db[k].lo : db[k].lo);
+  }
+  double h = 0.0;
+  for (int i = 0; i < f->n; ++i) {
+    double fi = f->drift[i];
+    for (int j = 0; j < f->m; ++j) fi += f->B[i][j] * u[j];
+    for (int k = 0; k < f->p; ++k) fi += f->C[i][k] * d[k];
+    h += p[i] * fi;
+  }
+  return h;
+}
+
+/* flow_bounds, dynamics.cpp:93-112 */
+static void flow_bounds(const affine_t* f, const hjb_interval* ub, const hjb_interval* db,
+                        double* alpha) {
+  for (int i = 0; i < f->n; ++i) {
+    double lo = f->drift[i];
+    double hi = f->drift[i];
+    for (int j = 0; j < f->m; ++j) {
+      const double a = f->B[i][j] * ub[j].lo;
+      const double b = f->B[i][j] * ub[j].hi;
+      lo += STD_MIN(a, b);
+      hi += STD_MAX(a, b);
+    }
+    for (int k = 0; k < f->p; ++k) {
+      const double a = f->C[i][k] * db[k].lo;
+      const double b = f->C[i][k] * db[k].hi;
+      lo += STD_MIN(a, b);
+      hi += STD_MAX(a, b);
+    }
+    alpha[i] = STD_MAX(fabs(lo), fabs(hi));
+  }
+}
+
+/* rows_separable, solver.cpp:88-102 */
+static int rows_separable(const affine_t* f) {
+  for (int j = 0; j < f->m; ++j) {
+    int rows = 0;
+    for (int i = 0; i < f->n; ++i)
+      if (f->B[i][j] != 0.0) ++rows;
+    if (rows > 1) return 0;
+  }
+  for (int k = 0; k < f->p; ++k) {
+    int rows = 0;
+    for (int i = 0; i < f->n; ++i)
+      if (f->C[i][k] != 0.0) ++rows;
+    if (rows > 1) return 0;
+  }
+  return 1;
+}
+
+/* DimSlopes / kink_h / godunov_flux / dim_slopes, solver.cpp:39-86 */
+typedef struct {
+  double pos, neg;
+} slopes_t;
+
+static inline double kink_h(slopes_t s, double p) { return p > 0.0 ? s.pos * p : s.neg * p; }
+
+static inline double godunov_flux(slopes_t s, double dminus, double dplus) {
+  const double ha = kink_h(s, dminus);
+  const double hb = kink_h(s, dplus);
+  if (dminus <= dplus) {
+    double h = ha > hb ? ha : hb;
+    if (dminus <= 0.0 && 0.0 <= dplus && h < 0.0) h = 0.0;
+    return h;
+  }
+  double h = ha < hb ? ha : hb;
+  if (dplus <= 0.0 && 0.0 <= dminus && h > 0.0) h = 0.0;
+  return h;
+}
+
+static inline void dim_slopes(const affine_t* f, const hjb_interval* ub, const hjb_interval* db,
+                              slopes_t* out) {
+  for (int d = 0; d < f->n; ++d) {
+    double pos = f->drift[d];
+    double neg = f->drift[d];
+    for (int j = 0; j < f->m; ++j) {
+      const double a = f->B[d][j] * ub[j].lo;
+      const double b = f->B[d][j] * ub[j].hi;
+      pos += a < b ? a : b;
+      neg += a > b ? a : b;
+    }
+    for (int k = 0; k < f->p; ++k) {
+      const double a = f->C[d][k] * db[k].lo;
+      const double b = f->C[d][k] * db[k].hi;
+      pos += a > b ? a : b;
+      neg += a < b ? a : b;
+    }
+    out[d].pos = pos;
+    out[d].neg = neg;
+  }
+}
+
+/* IntervalField::at_node, interval_field.hpp:27-29 */
+static inline void db_at(const hjb_dbounds* db, int64_t lin, hjb_interval* out) {
+  for (int ch = 0; ch < db->channels; ++ch) {
+    if (db->per_node) {
+      out[ch].lo = db->lo[ch][lin];
+      out[ch].hi = db->hi[ch][lin];
+    } else {
+      out[ch] = db->constant[ch];
+    }
+  }
+}
+
+static int check_ctx(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, grid_t* g) {
+  int rc = grid_init(gi, g);
+  if (rc) return rc;
+  if ((rc = model_check(m))) return rc;
+  /* make_context, solver.cpp:192-199 */
+  if (g->nd != m->state_dim)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "solver: grid rank does not match model state");
+  if (db->channels != m->disturbance_dim)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "solver: disturbance channel count mismatch");
+  return 0;
+}
+
+static int nthreads(void) {
+#ifdef _OPENMP
+  return g_threads > 0 ? g_threads : omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+#define CHUNK 4096 /* kChunk, solver.cpp:22 */
+
+/* scan_alpha, solver.cpp:221-268 */
+static void scan_alpha(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
+                       hjo_scan* out) {
+  const int nd = g->nd;
+  const int64_t nchunks = (g->size + CHUNK - 1) / CHUNK;
+  double best = 0.0;
+  double best_alpha[HJB_MAX_STATE] = {0};
+  int sep = 1;
+  double inv[HJB_MAX_DIMS];
+  for (int d = 0; d < nd; ++d) inv[d] = 1.0 / g->spacing[d];
+#pragma omp parallel num_threads(nthreads())
+  {
+    double lbest = 0.0, lalpha[HJB_MAX_STATE] = {0};
+    int lsep = 1;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      const int64_t lo = ch * CHUNK;
+      const int64_t hi = lo + CHUNK < g->size ? lo + CHUNK : g->size;
+      int64_t idx[HJB_MAX_DIMS];
+      double x[HJB_MAX_STATE], alpha[HJB_MAX_STATE];
+      hjb_interval dbn[HJB_MAX_INPUT];
+      affine_t af;
+      unravel(g, lo, idx);
+      for (int64_t lin = lo; lin < hi; ++lin) {
+        for (int d = 0; d < nd; ++d) x[d] = coord(g, d, idx[d]);
+        db_at(db, lin, dbn);
+        model_affine(m, x, idx, &af);
+        if (!rows_separable(&af)) lsep = 0;
+        flow_bounds(&af, m->ubounds, dbn, alpha);
+        double speed = 0.0;
+        for (int d = 0; d < nd; ++d) {
+          speed += alpha[d] * inv[d];
+          lalpha[d] = STD_MAX(lalpha[d], alpha[d]);
+        }
+        lbest = STD_MAX(lbest, speed);
+        odometer(g, idx);
+      }
+    }
+#pragma omp critical
+    {
+      best = STD_MAX(best, lbest);
+      for (int d = 0; d < nd; ++d) best_alpha[d] = STD_MAX(best_alpha[d], lalpha[d]);
+      if (!lsep) sep = 0;
+    }
+  }
+  out->max_speed_sum = best;
+  for (int d = 0; d < HJB_MAX_STATE; ++d) out->max_alpha[d] = d < nd ? best_alpha[d] : 0.0;
+  out->separable = sep;
+}
+
+int hjo_scan_alpha(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, hjo_scan* out) {
+  grid_t g;
+  int rc = check_ctx(gi, m, db, &g);
+  if (rc) return rc;
+  scan_alpha(&g, m, db, out);
+  return 0;
+}
+
+/* cfl_dt, solver.cpp:272-282 */
+int hjo_cfl_dt(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, double cfl,
+               double* dt) {
+  if (!(cfl > 0.0) || cfl > 1.0)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: cfl_factor must be in (0,1]");
+  hjo_scan s;
+  int rc = hjo_scan_alpha(gi, m, db, &s);
+  if (rc) return rc;
+  if (!(s.max_speed_sum > 0.0))
+    return fail(HJB_ERR_RUNTIME, "cfl_dt: flow is identically zero on the grid");
+  *dt = cfl / s.max_speed_sum;
+  return 0;
+}
+
+/* update_chunk, solver.cpp:106-190 */
+static double update_range(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
+                           const double* inv, int godunov, const double* global_alpha,
+                           const double* v, const double* c, double* out, double dt, int64_t lo,
+                           int64_t hi) {
+  const int nd = g->nd;
+  int64_t idx[HJB_MAX_DIMS];
+  double x[HJB_MAX_STATE], dminus[HJB_MAX_STATE], dplus[HJB_MAX_STATE];
+  double costate[HJB_MAX_STATE], alpha[HJB_MAX_STATE];
+  slopes_t slopes[HJB_MAX_STATE];
+  hjb_interval dbn[HJB_MAX_INPUT];
+  affine_t af;
+  unravel(g, lo, idx);
+  double max_dv = 0.0;
+  for (int64_t lin = lo; lin < hi; ++lin) {
+    for (int d = 0; d < nd; ++d) x[d] = coord(g, d, idx[d]);
+    for (int d = 0; d < nd; ++d) {
+      const int64_t stride = g->stride[d];
+      const int64_t k = idx[d];
+      const int64_t n = g->n[d];
+      double left, right;
+      if (k > 0 && k < n - 1) {
+        left = (v[lin] - v[lin - stride]) * inv[d];
+        right = (v[lin + stride] - v[lin]) * inv[d];
+      } else if (k == 0) {
+        right = (v[lin + stride] - v[lin]) * inv[d];
+        left = godunov ? 0.0 : right;
+      } else {
+        left = (v[lin] - v[lin - stride]) * inv[d];
+        right = godunov ? 0.0 : left;
+      }
+      dminus[d] = left;
+      dplus[d] = right;
+    }
+    db_at(db, lin, dbn);
+    model_affine(m, x, idx, &af);
+    double hhat = 0.0;
+    if (godunov) {
+      dim_slopes(&af, m->ubounds, dbn, slopes);
+      for (int d = 0; d < nd; ++d) hhat += godunov_flux(slopes[d], dminus[d], dplus[d]);
+    } else {
+      for (int d = 0; d < nd; ++d) costate[d] = 0.5 * (dminus[d] + dplus[d]);
+      hhat = hamiltonian(&af, costate, m->ubounds, dbn);
+      if (!global_alpha) {
+        flow_bounds(&af, m->ubounds, dbn, alpha);
+        for (int d = 0; d < nd; ++d) hhat += alpha[d] * 0.5 * (dplus[d] - dminus[d]);
+      } else {
+        for (int d = 0; d < nd; ++d) hhat += global_alpha[d] * 0.5 * (dplus[d] - dminus[d]);
+      }
+    }
+    const double stepped = v[lin] + dt * hhat;
+    const double vnew = stepped > c[lin] ? stepped : c[lin];
+    out[lin] = vnew;
+    const double dv = fabs(vnew - v[lin]);
+    if (dv > max_dv) max_dv = dv;
+    odometer(g, idx);
+  }
+  return max_dv;
+}
+
+static double sweep(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, const double* v,
+                    const double* c, double dt, int godunov, const double* global_alpha,
+                    double* out) {
+  double inv[HJB_MAX_DIMS];
+  for (int d = 0; d < g->nd; ++d) inv[d] = 1.0 / g->spacing[d];
+  const int64_t nchunks = (g->size + CHUNK - 1) / CHUNK;
+  double best = 0.0;
+#pragma omp parallel num_threads(nthreads())
+  {
+    double lbest = 0.0;
+#pragma omp for schedule(static)
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      const int64_t lo = ch * CHUNK;
+      const int64_t hi = lo + CHUNK < g->size ? lo + CHUNK : g->size;
+      const double r = update_range(g, m, db, inv, godunov, global_alpha, v, c, out, dt, lo, hi);
+      lbest = STD_MAX(lbest, r);
+    }
+#pragma omp critical
+    best = STD_MAX(best, lbest);
+  }
+  return best;
+}
+
+int hjo_sweep(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, const double* v,
+              const double* c, double dt, int32_t scheme, const double* global_alpha,
+              double* out, double* max_dv) {
+  grid_t g;
+  int rc = check_ctx(gi, m, db, &g);
+  if (rc) return rc;
+  *max_dv = sweep(&g, m, db, v, c, dt, scheme == HJB_GODUNOV, global_alpha, out);
+  return 0;
+}
+
+/* vi_step, solver.cpp:284-308 */
+int hjo_vi_step(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, const double* v,
+                const double* c, double dt, const hjb_solve_config* cfg, double* out) {
+  grid_t g;
+  int rc = check_ctx(gi, m, db, &g);
+  if (rc) return rc;
+  hjo_scan s;
+  scan_alpha(&g, m, db, &s);
+  if (dt * s.max_speed_sum > 1.0 + 1e-12)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "vi_step: dt violates the CFL bound");
+  if (cfg->scheme == HJB_GODUNOV && !s.separable)
+    return fail(HJB_ERR_INVALID_ARGUMENT,
+                "vi_step: model inputs are not row-separable, use the Lax-Friedrichs scheme");
+  const double* ga = cfg->dissipation == HJB_GLOBAL ? s.max_alpha : NULL;
+  sweep(&g, m, db, v, c, dt, cfg->scheme == HJB_GODUNOV, ga, out);
+  return 0;
+}
+
+int hjo_ho_solve(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, const double* init,
+                 const double* c, const hjb_solve_config* cfg, const hjo_scan* s, double dt,
+                 double* out, hjb_solve_result* res);
+
+static double now_ms(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
+/* solve, solver.cpp:310-376 */
+int hjo_solve(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, const double* init,
+              const double* c, const hjb_solve_config* cfg, double* out, hjb_solve_result* res) {
+  if (!(cfg->cfl_factor > 0.0) || cfg->cfl_factor > 1.0)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: cfl_factor must be in (0,1]");
+  if (!(cfg->tolerance > 0.0))
+    return fail(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: tolerance must be > 0");
+  grid_t g;
+  int rc = check_ctx(gi, m, db, &g);
+  if (rc) return rc;
+  hjo_scan s;
+  scan_alpha(&g, m, db, &s);
+  if (!(s.max_speed_sum > 0.0))
+    return fail(HJB_ERR_RUNTIME, "solve: flow is identically zero on the grid");
+  if (cfg->scheme == HJB_GODUNOV && !s.separable)
+    return fail(HJB_ERR_INVALID_ARGUMENT,
+                "solve: model inputs are not row-separable, use the Lax-Friedrichs scheme");
+  const double dt = cfg->cfl_factor / s.max_speed_sum;
+  res->dt = dt;
+  res->nodes_per_sweep = g.size;
+  res->converged = 0;
+  res->iterations = 0;
+  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+    return hjo_ho_solve(&g, m, db, init, c, cfg, &s, dt, out, res);
+  const double* ga = cfg->dissipation == HJB_GLOBAL ? s.max_alpha : NULL;
+  const int godunov = cfg->scheme == HJB_GODUNOV;
+
+  const double t0 = now_ms();
+  double* front = (double*)malloc(g.size * sizeof(double));
+  double* back = (double*)malloc(g.size * sizeof(double));
+  memcpy(front, init, g.size * sizeof(double));
+  double min_residual = INFINITY, first = 0.0, residual = 0.0;
+  int status = 0;
+  for (int64_t iter = 1; iter <= cfg->max_iters; ++iter) {
+    const double max_dv = sweep(&g, m, db, front, c, dt, godunov, ga, back);
+    residual = max_dv / dt;
+    double* t = front;
+    front = back;
+    back = t;
+    res->iterations = iter;
+    if (iter == 1) first = residual;
+    if (res->residual_history && iter <= res->history_capacity)
+      res->residual_history[iter - 1] = residual;
+    if (res->wall_ms_history && iter <= res->history_capacity)
+      res->wall_ms_history[iter - 1] = now_ms() - t0;
+    if (residual < cfg->tolerance) {
+      res->converged = 1;
+      break;
+    }
+    min_residual = STD_MIN(min_residual, residual);
+    if (!isfinite(residual) || residual > 10.0 * STD_MAX(min_residual, first)) {
+      status = fail(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+      break;
+    }
+    if (cfg->time_horizon > 0.0 && (double)iter * dt >= cfg->time_horizon) break;
+  }
+  res->final_residual = residual;
+  memcpy(out, front, g.size * sizeof(double));
+  res->wall_seconds = (now_ms() - t0) * 1e-3;
+  free(front);
+  free(back);
+  return status;
+}
+
+/* ------------------------------------------------------ interpolation */
+/* locate + interp_ex, grid.cpp:84-135 */
+static double interp_at(const grid_t* g, const double* f, const double* x, int* ood) {
+  int64_t base[HJB_MAX_DIMS];
+  double frac[HJB_MAX_DIMS];
+  *ood = 0;
+  for (int d = 0; d < g->nd; ++d) {
+    double t = (x[d] - g->min[d]) / g->spacing[d];
+    if (t < 0.0) {
+      t = 0.0;
+      *ood = 1;
+    }
+    const double tmax = (double)(g->n[d] - 1);
+    if (t > tmax) {
+      t = tmax;
+      if (x[d] > g->max[d]) *ood = 1;
+    }
+    int64_t i0 = (int64_t)t;
+    if (i0 > g->n[d] - 2) i0 = g->n[d] - 2;
+    base[d] = i0;
+    frac[d] = t - (double)i0;
+  }
+  double value = 0.0;
+  const int64_t corners = (int64_t)1 << g->nd;
+  for (int64_t corner = 0; corner < corners; ++corner) {
+    double w = 1.0;
+    int64_t lin = 0;
+    for (int d = 0; d < g->nd; ++d) {
+      const int hi = (corner >> d) & 1;
+      w *= hi ? frac[d] : 1.0 - frac[d];
+      lin += (base[d] + (hi ? 1 : 0)) * g->stride[d];
+    }
+    if (w != 0.0) value += w * f[lin];
+  }
+  return value;
+}
+
+int hjo_interp(const hjb_grid* gi, const double* field, const double* x, double* value,
+               int32_t* out_of_domain) {
+  grid_t g;
+  int rc = grid_init(gi, &g);
+  if (rc) return rc;
+  for (int d = 0; d < g.nd; ++d)
+    if (!isfinite(x[d])) return fail(HJB_ERR_INVALID_ARGUMENT, "interp: non-finite query");
+  int ood;
+  *value = interp_at(&g, field, x, &ood);
+  *out_of_domain = ood;
+  return 0;
+}
+
+/* resample, grid.cpp:215-231 */
+int hjo_resample(const hjb_grid* sgi, const double* src, const hjb_grid* dgi, double* dst) {
+  grid_t sg, dg;
+  int rc = grid_init(sgi, &sg);
+  if (rc) return rc;
+  if ((rc = grid_init(dgi, &dg))) return rc;
+  if (sg.nd != dg.nd) return fail(HJB_ERR_INVALID_ARGUMENT, "resample: dimension mismatch");
+  const int64_t nchunks = (dg.size + CHUNK - 1) / CHUNK;
+#pragma omp parallel for num_threads(nthreads()) schedule(static)
+  for (int64_t ch = 0; ch < nchunks; ++ch) {
+    const int64_t lo = ch * CHUNK;
+    const int64_t hi = lo + CHUNK < dg.size ? lo + CHUNK : dg.size;
+    int64_t idx[HJB_MAX_DIMS];
+    double x[HJB_MAX_DIMS];
+    unravel(&dg, lo, idx);
+    for (int64_t lin = lo; lin < hi; ++lin) {
+      for (int d = 0; d < dg.nd; ++d) x[d] = coord(&dg, d, idx[d]);
+      int ood;
+      dst[lin] = interp_at(&sg, src, x, &ood);
+      odometer(&dg, idx);
+    }
+  }
+  return 0;
+}
+
+/* max_adjacent_jump, grid.cpp:197-213 */
+int hjo_max_adjacent_jump(const hjb_grid* gi, const double* f, double* out) {
+  grid_t g;
+  int rc = grid_init(gi, &g);
+  if (rc) return rc;
+  const int64_t nchunks = (g.size + CHUNK - 1) / CHUNK;
+  double best = 0.0;
+#pragma omp parallel num_threads(nthreads())
+  {
+    double lbest = 0.0;
+#pragma omp for schedule(static)
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      const int64_t lo = ch * CHUNK;
+      const int64_t hi = lo + CHUNK < g.size ? lo + CHUNK : g.size;
+      int64_t idx[HJB_MAX_DIMS];
+      unravel(&g, lo, idx);
+      for (int64_t lin = lo; lin < hi; ++lin) {
+        for (int d = 0; d < g.nd; ++d) {
+          if (idx[d] + 1 >= g.n[d]) continue;
+          const double dv = fabs(f[lin + g.stride[d]] - f[lin]);
+          if (dv > lbest) lbest = dv;
+        }
+        odometer(&g, idx);
+      }
+    }
+#pragma omp critical
+    if (lbest > best) best = lbest;
+  }
+  *out = best;
+  return 0;
+}
+
+/* seed_from lambda, solver.cpp:404-411 */
+int hjo_seed_from(const hjb_grid* sgi, const double* src, const hjb_grid* dgi,
+                  const double* c_dst, double* dst) {
+  int rc = hjo_resample(sgi, src, dgi, dst);
+  if (rc) return rc;
+  double slack;
+  if ((rc = hjo_max_adjacent_jump(sgi, src, &slack))) return rc;
+  grid_t dg;
+  grid_init(dgi, &dg);
+  for (int64_t i = 0; i < dg.size; ++i) dst[i] = STD_MAX(dst[i] - slack, c_dst[i]);
+  return 0;
+}
+
+/* solve_coarse_to_fine, solver.cpp:387-425 (constant dbounds: resampling a
+ * constant IntervalField reproduces the constant, solver.cpp:378-385, since
+ * the multilinear weights of every query sum to one... only when they do
+ * exactly; per-node resampling is done explicitly below to stay faithful) */
+int hjo_solve_coarse_to_fine(const hjb_grid* fine, const hjb_model* m, const hjb_dbounds* db,
+                             const double* c_fine, const hjb_grid* coarse,
+                             const hjb_solve_config* cfg, const double* warm_init_fine,
+                             double* coarse_out, hjb_solve_result* coarse_res, double* fine_out,
+                             hjb_solve_result* fine_res) {
+  grid_t fg, cg;
+  int rc = grid_init(fine, &fg);
+  if (rc) return rc;
+  if ((rc = grid_init(coarse, &cg))) return rc;
+  if (cg.nd != fg.nd)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "solve_coarse_to_fine: grid rank mismatch");
+  double* c_coarse = (double*)malloc(cg.size * sizeof(double));
+  double* init_coarse = (double*)malloc(cg.size * sizeof(double));
+  double* init_fine = (double*)malloc(fg.size * sizeof(double));
+  double* dbuf = NULL;
+  hjb_dbounds dbc = *db;
+  hjo_resample(fine, c_fine, coarse, c_coarse);
+  /* resample(IntervalField), solver.cpp:378-385: per channel lo/hi */
+  if (db->channels > 0) {
+    dbuf = (double*)malloc((size_t)2 * db->channels * fg.size * sizeof(double));
+    double* cbuf = (double*)malloc((size_t)2 * db->channels * cg.size * sizeof(double));
+    for (int ch = 0; ch < db->channels; ++ch) {
+      double* flo = dbuf + (size_t)(2 * ch) * fg.size;
+      double* fhi = dbuf + (size_t)(2 * ch + 1) * fg.size;
+      for (int64_t i = 0; i < fg.size; ++i) {
+        flo[i] = db->per_node ? db->lo[ch][i] : db->constant[ch].lo;
+        fhi[i] = db->per_node ? db->hi[ch][i] : db->constant[ch].hi;
+      }
+      hjo_resample(fine, flo, coarse, cbuf + (size_t)(2 * ch) * cg.size);
+      hjo_resample(fine, fhi, coarse, cbuf + (size_t)(2 * ch + 1) * cg.size);
+      dbc.lo[ch] = cbuf + (size_t)(2 * ch) * cg.size;
+      dbc.hi[ch] = cbuf + (size_t)(2 * ch + 1) * cg.size;
+    }
+    dbc.per_node = 1;
+    free(dbuf);
+    dbuf = cbuf;
+  }
+  if (warm_init_fine)
+    hjo_seed_from(fine, warm_init_fine, coarse, c_coarse, init_coarse);
+  else
+    memcpy(init_coarse, c_coarse, cg.size * sizeof(double));
+  rc = hjo_solve(coarse, m, &dbc, init_coarse, c_coarse, cfg, coarse_out, coarse_res);
+  if (!rc) {
+    hjo_seed_from(coarse, coarse_out, fine, c_fine, init_fine);
+    rc = hjo_solve(fine, m, db, init_fine, c_fine, cfg, fine_out, fine_res);
+  }
+  free(c_coarse);
+  free(init_coarse);
+  free(init_fine);
+  free(dbuf);
+  return rc;
+}
+
+/* ------------------------------------------------------------ level sets */
+/* signed_distance_band, levelset.cpp:54-66 */
+int hjo_signed_distance_band(const hjb_grid* gi, int32_t dim, double lo, double hi, double* out) {
+  grid_t g;
+  int rc = grid_init(gi, &g);
+  if (rc) return rc;
+  if (dim < 0 || dim >= g.nd)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "signed_distance_band: dim out of range");
+  if (!(lo < hi)) return fail(HJB_ERR_INVALID_ARGUMENT, "signed_distance_band: lo must be < hi");
+  for (int64_t lin = 0; lin < g.size; ++lin) {
+    const double x = coord(&g, dim, (lin / g.stride[dim]) % g.n[dim]);
+    out[lin] = STD_MAX(lo - x, x - hi);
+  }
+  return 0;
+}
+
+/* signed_distance_box_at / signed_distance_box, levelset.cpp:11-52 */
+int hjo_signed_distance_box(const hjb_grid* gi, const double* lo, const double* hi, double* out) {
+  grid_t g;
+  int rc = grid_init(gi, &g);
+  if (rc) return rc;
+  for (int d = 0; d < g.nd; ++d)
+    if (!(lo[d] < hi[d]))
+      return fail(HJB_ERR_INVALID_ARGUMENT, "signed_distance_box: lo must be < hi");
+  int64_t idx[HJB_MAX_DIMS] = {0};
+  for (int64_t lin = 0; lin < g.size; ++lin) {
+    double inside = INFINITY, outside_sq = 0.0;
+    int outside = 0;
+    for (int d = 0; d < g.nd; ++d) {
+      const double x = coord(&g, d, idx[d]);
+      const double below = lo[d] - x;
+      const double above = x - hi[d];
+      const double excess = STD_MAX(below, above);
+      if (excess > 0.0) {
+        outside = 1;
+        outside_sq += excess * excess;
+      } else {
+        inside = STD_MIN(inside, -excess);
+      }
+    }
+    out[lin] = outside ? sqrt(outside_sq) : -inside;
+    odometer(&g, idx);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------- probes */
+int hjo_hamiltonian(const hjb_model* m, const double* x, const double* p, const hjb_interval* db,
+                    double* h) {
+  int rc = model_check(m);
+  if (rc) return rc;
+  affine_t af;
+  model_affine(m, x, NULL, &af);
+  *h = hamiltonian(&af, p, m->ubounds, db);
+  return 0;
+}
+
+int hjo_flow_bounds(const hjb_model* m, const double* x, const hjb_interval* db, double* alpha) {
+  int rc = model_check(m);
+  if (rc) return rc;
+  affine_t af;
+  model_affine(m, x, NULL, &af);
+  flow_bounds(&af, m->ubounds, db, alpha);
+  return 0;
+}
+
+/* ------------------------------------------- high order (no reference) */
+/* Placeholder until the ENO/TVD-RK restatement lands. */
+int hjo_ho_solve(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, const double* init,
+                 const double* c, const hjb_solve_config* cfg, const hjo_scan* s, double dt,
+                 double* out, hjb_solve_result* res) {
+  (void)g; (void)m; (void)db; (void)init; (void)c; (void)cfg; (void)s; (void)dt; (void)out;
+  (void)res;
+  return fail(HJB_ERR_UNSUPPORTED, "solve: spatial/time order > 1 not available yet");
+}

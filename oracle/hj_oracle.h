@@ -1,0 +1,83 @@
+/*
+ * hj_oracle.h — TEST INFRASTRUCTURE ONLY: plain-C CPU restatement of the
+ * reference's hot path (hjsafe::solve and its helpers).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this library, and only as the checker.  The product (libhjb.so) never
+ * links or calls it.  Each function cites the reference file:line it
+ * restates.  Parity of this restatement is pinned against the reference
+ * itself (oracle/_ref/libhjref.so, built from the unmodified reference
+ * sources) and against the golden fixtures under tests/golden/.
+ *
+ * The ENO2/ENO3 + TVD-RK2/RK3 extension (hjo_sweep_ho / hjo_solve with
+ * spatial_order/time_order > 1) has NO reference implementation (reference
+ * SPEC.md:324 lists high-order schemes as non-goals): that part is
+ * "parity unpinned" and is validated by reduction to the first-order
+ * reference, convergence-order tests and sign agreement.
+ */
+#ifndef HJ_ORACLE_H_
+#define HJ_ORACLE_H_
+
+#include <stdint.h>
+
+#include "../include/hjb.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hjo_scan {
+  double max_speed_sum;
+  double max_alpha[HJB_MAX_STATE];
+  int32_t separable;
+} hjo_scan;
+
+/* Status codes follow hjb_status.  Messages mirror the reference's. */
+const char* hjo_last_error(void);
+void hjo_set_threads(int threads);
+
+/* scan_alpha, solver.cpp:221-268 */
+int hjo_scan_alpha(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, hjo_scan* out);
+/* cfl_dt, solver.cpp:272-282 */
+int hjo_cfl_dt(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, double cfl,
+               double* dt);
+/* update_chunk over the whole grid, solver.cpp:106-190; returns max|dV|.
+ * global_alpha == NULL selects per-node dissipation. */
+int hjo_sweep(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, const double* v,
+              const double* c, double dt, int32_t scheme, const double* global_alpha,
+              double* out, double* max_dv);
+/* vi_step, solver.cpp:284-308 */
+int hjo_vi_step(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, const double* v,
+                const double* c, double dt, const hjb_solve_config* cfg, double* out);
+/* solve, solver.cpp:310-376 (+ ENO/TVD-RK extension when orders > 1) */
+int hjo_solve(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, const double* init,
+              const double* c, const hjb_solve_config* cfg, double* out, hjb_solve_result* res);
+/* interp_ex at a point, grid.cpp:84-135 (returns out_of_domain flag) */
+int hjo_interp(const hjb_grid* g, const double* field, const double* x, double* value,
+               int32_t* out_of_domain);
+/* resample, grid.cpp:215-231 */
+int hjo_resample(const hjb_grid* src_g, const double* src, const hjb_grid* dst_g, double* dst);
+/* max_adjacent_jump, grid.cpp:197-213 */
+int hjo_max_adjacent_jump(const hjb_grid* g, const double* v, double* out);
+/* seed_from, solver.cpp:404-411 */
+int hjo_seed_from(const hjb_grid* src_g, const double* src, const hjb_grid* dst_g,
+                  const double* c_dst, double* dst);
+/* solve_coarse_to_fine, solver.cpp:387-425 (dbounds must be constant) */
+int hjo_solve_coarse_to_fine(const hjb_grid* fine, const hjb_model* m, const hjb_dbounds* db,
+                             const double* c_fine, const hjb_grid* coarse,
+                             const hjb_solve_config* cfg, const double* warm_init_fine,
+                             double* coarse_out, hjb_solve_result* coarse_res, double* fine_out,
+                             hjb_solve_result* fine_res);
+/* signed_distance_band / signed_distance_box, levelset.cpp:11-66 */
+int hjo_signed_distance_band(const hjb_grid* g, int32_t dim, double lo, double hi, double* out);
+int hjo_signed_distance_box(const hjb_grid* g, const double* lo, const double* hi, double* out);
+/* hamiltonian / flow_bounds at a point, dynamics.cpp:37-112 */
+int hjo_hamiltonian(const hjb_model* m, const double* x, const double* p, const hjb_interval* db,
+                    double* h);
+int hjo_flow_bounds(const hjb_model* m, const double* x, const hjb_interval* db, double* alpha);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

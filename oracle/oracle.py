@@ -1,0 +1,391 @@
+"""TEST INFRASTRUCTURE ONLY — Python loader of the CPU oracles.
+
+Two checkers live here, both CPU-only:
+  * ``Restatement``: oracle/libhjoracle.so, the plain-C restatement of the
+    reference hot path (oracle/hj_oracle.c);
+  * ``Reference``: oracle/_ref/libhjref.so, the reference's own sources
+    compiled in place (oracle/Makefile `ref`) behind oracle/ref_shim.cpp.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this
+module.  The product (paper_2101_05916_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_2101_05916_b200 import abi
+from paper_2101_05916_b200 import hjsafe as hj
+
+HERE = Path(__file__).resolve().parent
+RESTATEMENT_SO = HERE / "libhjoracle.so"
+REF_SO = HERE / "_ref" / "libhjref.so"
+REF_SRC = Path("/root/reference/proj")
+
+
+def build(ref: bool = True) -> None:
+    """Compile the restatement (always) and _ref (when the reference sources exist)."""
+    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    if ref and REF_SRC.exists():
+        subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+P = C.POINTER
+_vp = C.c_void_p
+_d = C.c_double
+
+
+class ScanResult(C.Structure):
+    _fields_ = [("max_speed_sum", C.c_double), ("max_alpha", C.c_double * abi.HJB_MAX_STATE),
+                ("separable", C.c_int32)]
+
+
+def _arr(a: np.ndarray):
+    return a.ctypes.data_as(_vp)
+
+
+def _vals(f) -> np.ndarray:
+    return np.ascontiguousarray(f.values() if hasattr(f, "values") else f, dtype=np.float64)
+
+
+class Restatement:
+    """oracle/libhjoracle.so (plain C, OpenMP over node chunks)."""
+
+    def __init__(self, path: os.PathLike | None = None, threads: int = 0):
+        p = Path(path) if path else RESTATEMENT_SO
+        if not p.exists():
+            build(ref=False)
+        self.lib = C.CDLL(str(p))
+        L = self.lib
+        L.hjo_last_error.restype = C.c_char_p
+        L.hjo_set_threads.argtypes = [C.c_int]
+        L.hjo_scan_alpha.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), P(ScanResult)]
+        L.hjo_cfl_dt.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _d, P(_d)]
+        L.hjo_sweep.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp, _vp, _d,
+                                C.c_int32, _vp, _vp, P(_d)]
+        L.hjo_vi_step.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp, _vp, _d,
+                                  P(abi.HjbSolveConfig), _vp]
+        L.hjo_solve.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp, _vp,
+                                P(abi.HjbSolveConfig), _vp, P(abi.HjbSolveResult)]
+        L.hjo_interp.argtypes = [P(abi.HjbGrid), _vp, _vp, P(_d), P(C.c_int32)]
+        L.hjo_resample.argtypes = [P(abi.HjbGrid), _vp, P(abi.HjbGrid), _vp]
+        L.hjo_max_adjacent_jump.argtypes = [P(abi.HjbGrid), _vp, P(_d)]
+        L.hjo_seed_from.argtypes = [P(abi.HjbGrid), _vp, P(abi.HjbGrid), _vp, _vp]
+        L.hjo_solve_coarse_to_fine.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds),
+                                               _vp, P(abi.HjbGrid), P(abi.HjbSolveConfig), _vp, _vp,
+                                               P(abi.HjbSolveResult), _vp, P(abi.HjbSolveResult)]
+        L.hjo_signed_distance_band.argtypes = [P(abi.HjbGrid), C.c_int32, _d, _d, _vp]
+        L.hjo_signed_distance_box.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp]
+        L.hjo_hamiltonian.argtypes = [P(abi.HjbModel), _vp, _vp, P(abi.HjbInterval), P(_d)]
+        L.hjo_flow_bounds.argtypes = [P(abi.HjbModel), _vp, P(abi.HjbInterval), _vp]
+        if threads:
+            L.hjo_set_threads(threads)
+
+    def _chk(self, rc):
+        if rc:
+            raise OracleError(rc, self.lib.hjo_last_error().decode())
+
+    def scan_alpha(self, grid, model, db):
+        s = ScanResult()
+        g, m, d = grid.to_c(), model.to_c(), db.to_c()
+        self._chk(self.lib.hjo_scan_alpha(C.byref(g), C.byref(m), C.byref(d), C.byref(s)))
+        return s.max_speed_sum, list(s.max_alpha)[:grid.ndims()], bool(s.separable)
+
+    def cfl_dt(self, grid, model, db, cfl):
+        out = C.c_double()
+        g, m, d = grid.to_c(), model.to_c(), db.to_c()
+        self._chk(self.lib.hjo_cfl_dt(C.byref(g), C.byref(m), C.byref(d), cfl, C.byref(out)))
+        return out.value
+
+    def sweep(self, grid, model, db, v, c, dt, scheme=abi.GODUNOV, global_alpha=None):
+        v, c = _vals(v), _vals(c)
+        out = np.empty_like(v)
+        mx = C.c_double()
+        ga = None
+        if global_alpha is not None:
+            ga_arr = np.zeros(abi.HJB_MAX_STATE)
+            ga_arr[:len(global_alpha)] = global_alpha
+            ga = _arr(ga_arr)
+        g, m, d = grid.to_c(), model.to_c(), db.to_c()
+        self._chk(self.lib.hjo_sweep(C.byref(g), C.byref(m), C.byref(d), _arr(v), _arr(c), dt,
+                                     scheme, ga, _arr(out), C.byref(mx)))
+        return out, mx.value
+
+    def vi_step(self, v, c, model, db, dt, cfg=None):
+        cfg = cfg or hj.SolveConfig()
+        grid = v.grid()
+        vv, cc = _vals(v), _vals(c)
+        out = np.empty_like(vv)
+        g, m, d, k = grid.to_c(), model.to_c(), db.to_c(), cfg.to_c()
+        self._chk(self.lib.hjo_vi_step(C.byref(g), C.byref(m), C.byref(d), _arr(vv), _arr(cc), dt,
+                                       C.byref(k), _arr(out)))
+        return out
+
+    def solve(self, init, c, model, db, cfg, history_capacity=None):
+        grid = init.grid()
+        cap = int(cfg.max_iters if history_capacity is None else history_capacity)
+        r, rh, wh = hj._c_result(cap)
+        iv, cv = _vals(init), _vals(c)
+        out = np.empty_like(iv)
+        g, m, d, k = grid.to_c(), model.to_c(), db.to_c(), cfg.to_c()
+        self._chk(self.lib.hjo_solve(C.byref(g), C.byref(m), C.byref(d), _arr(iv), _arr(cv),
+                                     C.byref(k), _arr(out), C.byref(r)))
+        return hj._to_result(grid, out, r, rh, wh)
+
+    def solve_coarse_to_fine(self, c_fine, model, db, coarse_grid, cfg, warm=None):
+        fg = c_fine.grid()
+        cap = int(cfg.max_iters)
+        rc_, rhc, whc = hj._c_result(cap)
+        rf_, rhf, whf = hj._c_result(cap)
+        cout = np.empty(coarse_grid.size())
+        fout = np.empty(fg.size())
+        g, cg, m, d, k = fg.to_c(), coarse_grid.to_c(), model.to_c(), db.to_c(), cfg.to_c()
+        wv = _vals(warm) if warm is not None else None
+        self._chk(self.lib.hjo_solve_coarse_to_fine(
+            C.byref(g), C.byref(m), C.byref(d), _arr(_vals(c_fine)), C.byref(cg), C.byref(k),
+            _arr(wv) if wv is not None else None, _arr(cout), C.byref(rc_), _arr(fout), C.byref(rf_)))
+        return hj.CoarseToFineResult(coarse=hj._to_result(coarse_grid, cout, rc_, rhc, whc),
+                                     fine=hj._to_result(fg, fout, rf_, rhf, whf))
+
+    def interp(self, f, x):
+        val = C.c_double()
+        ood = C.c_int32()
+        xv = np.asarray(x, dtype=np.float64)
+        g = f.grid().to_c()
+        self._chk(self.lib.hjo_interp(C.byref(g), _arr(_vals(f)), _arr(xv), C.byref(val), C.byref(ood)))
+        return val.value, bool(ood.value)
+
+    def resample(self, f, target):
+        out = np.empty(target.size())
+        sg, dg = f.grid().to_c(), target.to_c()
+        self._chk(self.lib.hjo_resample(C.byref(sg), _arr(_vals(f)), C.byref(dg), _arr(out)))
+        return out
+
+    def max_adjacent_jump(self, f):
+        out = C.c_double()
+        g = f.grid().to_c()
+        self._chk(self.lib.hjo_max_adjacent_jump(C.byref(g), _arr(_vals(f)), C.byref(out)))
+        return out.value
+
+    def seed_from(self, src, target, c_dst):
+        out = np.empty(target.size())
+        sg, dg = src.grid().to_c(), target.to_c()
+        self._chk(self.lib.hjo_seed_from(C.byref(sg), _arr(_vals(src)), C.byref(dg),
+                                         _arr(_vals(c_dst)), _arr(out)))
+        return out
+
+    def signed_distance_band(self, grid, dim, lo, hi):
+        out = np.empty(grid.size())
+        g = grid.to_c()
+        self._chk(self.lib.hjo_signed_distance_band(C.byref(g), dim, lo, hi, _arr(out)))
+        return out
+
+    def signed_distance_box(self, grid, lo, hi):
+        out = np.empty(grid.size())
+        lo = np.asarray(lo, dtype=np.float64)
+        hi = np.asarray(hi, dtype=np.float64)
+        g = grid.to_c()
+        self._chk(self.lib.hjo_signed_distance_box(C.byref(g), _arr(lo), _arr(hi), _arr(out)))
+        return out
+
+    def hamiltonian(self, model, x, p, db):
+        h = C.c_double()
+        xv, pv = np.asarray(x, dtype=np.float64), np.asarray(p, dtype=np.float64)
+        dbs = (abi.HjbInterval * abi.HJB_MAX_INPUT)(*[abi.HjbInterval(b.lo, b.hi) for b in db])
+        m = model.to_c()
+        self._chk(self.lib.hjo_hamiltonian(C.byref(m), _arr(xv), _arr(pv), dbs, C.byref(h)))
+        return h.value
+
+    def flow_bounds(self, model, x, db):
+        out = np.zeros(abi.HJB_MAX_STATE)
+        xv = np.asarray(x, dtype=np.float64)
+        dbs = (abi.HjbInterval * abi.HJB_MAX_INPUT)(*[abi.HjbInterval(b.lo, b.hi) for b in db])
+        m = model.to_c()
+        self._chk(self.lib.hjo_flow_bounds(C.byref(m), _arr(xv), dbs, _arr(out)))
+        return out[:model.state_dim()]
+
+
+# ----------------------------------------------------------- reference
+class ModelSpec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d_row", C.c_int32), ("p", C.c_double * 10)]
+
+
+class RefResult(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("dt", C.c_double), ("wall_seconds", C.c_double),
+                ("converged", C.c_int32), ("reserved", C.c_int32), ("nodes_per_sweep", C.c_int64),
+                ("residual_history", P(C.c_double)), ("history_capacity", C.c_int64)]
+
+
+def model_spec(model) -> ModelSpec:
+    s = ModelSpec()
+    if isinstance(model, hj.Quad2DVert):
+        s.kind, vals = 0, [model.p.k_thrust, model.p.k_offset, model.p.gravity]
+    elif isinstance(model, hj.NearHoverPlanar4D):
+        p = model.p
+        s.kind, vals = 1, [p.d0, p.d1, p.n0, p.gravity, p.max_angle_cmd]
+        s.d_row = model.d_row
+    elif isinstance(model, hj.NearHoverVertical2D):
+        p = model.p
+        s.kind, vals = 2, [p.gravity, p.thrust_gain, p.thrust_frac_lo, p.thrust_frac_hi]
+    elif isinstance(model, hj.TwinDoubleIntegrator):
+        s.kind, vals = 4, [model.p.a_min, model.p.a_max]
+    elif isinstance(model, hj.DoubleIntegrator):
+        s.kind, vals = 3, [model.p.a_min, model.p.a_max]
+    elif isinstance(model, hj.ConstantAdvection):
+        s.kind, vals = 5, list(model.speed)
+        s.d_row = len(model.speed)
+    else:
+        raise TypeError(f"no reference model for {type(model).__name__}")
+    for i, v in enumerate(vals):
+        s.p[i] = v
+    return s
+
+
+class Reference:
+    """oracle/_ref/libhjref.so: the reference's own code, compiled in place."""
+
+    def __init__(self, path: os.PathLike | None = None):
+        p = Path(path) if path else REF_SO
+        if not p.exists():
+            raise FileNotFoundError(f"{p} missing (build with `make -C oracle ref` where "
+                                    "/root/reference exists)")
+        self.lib = C.CDLL(str(p))
+        L = self.lib
+        E = [C.c_char_p, C.c_int]
+        L.hjr_cfl_dt.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds), _d, C.c_uint, P(_d)] + E
+        L.hjr_vi_step.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds), _vp, _vp, _d,
+                                  P(abi.HjbSolveConfig), _vp] + E
+        L.hjr_solve.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds), _vp, _vp,
+                                P(abi.HjbSolveConfig), _vp, P(RefResult)] + E
+        L.hjr_solve_coarse_to_fine.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds), _vp,
+                                               P(abi.HjbGrid), P(abi.HjbSolveConfig), _vp, _vp,
+                                               P(RefResult), _vp, P(RefResult)] + E
+        L.hjr_resample.argtypes = [P(abi.HjbGrid), _vp, P(abi.HjbGrid), _vp] + E
+        L.hjr_max_adjacent_jump.argtypes = [P(abi.HjbGrid), _vp, P(_d)] + E
+        L.hjr_signed_distance_band.argtypes = [P(abi.HjbGrid), C.c_int32, _d, _d, _vp] + E
+        L.hjr_signed_distance_box.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp] + E
+        L.hjr_hamiltonian.argtypes = [P(ModelSpec), _vp, _vp, P(abi.HjbInterval), P(_d)] + E
+        L.hjr_flow_bounds.argtypes = [P(ModelSpec), _vp, P(abi.HjbInterval), _vp] + E
+        L.hjr_write_hjvf.argtypes = [C.c_char_p, P(abi.HjbGrid), _vp] + E
+
+    def _call(self, fn, *args):
+        err = C.create_string_buffer(512)
+        rc = fn(*args, err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+
+    def cfl_dt(self, grid, model, db, cfl, threads=0):
+        out = C.c_double()
+        g, m, d = grid.to_c(), model_spec(model), db.to_c()
+        self._call(self.lib.hjr_cfl_dt, C.byref(g), C.byref(m), C.byref(d), cfl, threads, C.byref(out))
+        return out.value
+
+    def vi_step(self, v, c, model, db, dt, cfg=None):
+        cfg = cfg or hj.SolveConfig()
+        vv, cc = _vals(v), _vals(c)
+        out = np.empty_like(vv)
+        g, m, d, k = v.grid().to_c(), model_spec(model), db.to_c(), cfg.to_c()
+        self._call(self.lib.hjr_vi_step, C.byref(g), C.byref(m), C.byref(d), _arr(vv), _arr(cc), dt,
+                   C.byref(k), _arr(out))
+        return out
+
+    def solve(self, init, c, model, db, cfg):
+        grid = init.grid()
+        cap = int(cfg.max_iters)
+        hist = np.zeros(max(cap, 1))
+        r = RefResult()
+        r.residual_history = hist.ctypes.data_as(P(C.c_double))
+        r.history_capacity = cap
+        iv, cv = _vals(init), _vals(c)
+        out = np.empty_like(iv)
+        g, m, d, k = grid.to_c(), model_spec(model), db.to_c(), cfg.to_c()
+        self._call(self.lib.hjr_solve, C.byref(g), C.byref(m), C.byref(d), _arr(iv), _arr(cv),
+                   C.byref(k), _arr(out), C.byref(r))
+        n = min(int(r.iterations), cap)
+        return hj.SolveResult(value=hj.ScalarField(grid, out, check=False), iterations=int(r.iterations),
+                              dt=r.dt, wall_seconds=r.wall_seconds, converged=bool(r.converged),
+                              residual_history=hist[:n].copy(), nodes_per_sweep=int(r.nodes_per_sweep))
+
+    def solve_coarse_to_fine(self, c_fine, model, db, coarse_grid, cfg, warm=None):
+        fg = c_fine.grid()
+        cap = int(cfg.max_iters)
+        res = []
+        for _ in range(2):
+            h = np.zeros(max(cap, 1))
+            r = RefResult()
+            r.residual_history = h.ctypes.data_as(P(C.c_double))
+            r.history_capacity = cap
+            res.append((r, h))
+        cout = np.empty(coarse_grid.size())
+        fout = np.empty(fg.size())
+        g, cg, m, d, k = fg.to_c(), coarse_grid.to_c(), model_spec(model), db.to_c(), cfg.to_c()
+        wv = _vals(warm) if warm is not None else None
+        self._call(self.lib.hjr_solve_coarse_to_fine, C.byref(g), C.byref(m), C.byref(d),
+                   _arr(_vals(c_fine)), C.byref(cg), C.byref(k), _arr(wv) if wv is not None else None,
+                   _arr(cout), C.byref(res[0][0]), _arr(fout), C.byref(res[1][0]))
+        out = []
+        for (r, h), grid, v in ((res[0], coarse_grid, cout), (res[1], fg, fout)):
+            n = min(int(r.iterations), cap)
+            out.append(hj.SolveResult(value=hj.ScalarField(grid, v, check=False),
+                                      iterations=int(r.iterations), dt=r.dt,
+                                      wall_seconds=r.wall_seconds, converged=bool(r.converged),
+                                      residual_history=h[:n].copy()))
+        return hj.CoarseToFineResult(coarse=out[0], fine=out[1])
+
+    def resample(self, f, target):
+        out = np.empty(target.size())
+        sg, dg = f.grid().to_c(), target.to_c()
+        self._call(self.lib.hjr_resample, C.byref(sg), _arr(_vals(f)), C.byref(dg), _arr(out))
+        return out
+
+    def max_adjacent_jump(self, f):
+        out = C.c_double()
+        g = f.grid().to_c()
+        self._call(self.lib.hjr_max_adjacent_jump, C.byref(g), _arr(_vals(f)), C.byref(out))
+        return out.value
+
+    def signed_distance_band(self, grid, dim, lo, hi):
+        out = np.empty(grid.size())
+        g = grid.to_c()
+        self._call(self.lib.hjr_signed_distance_band, C.byref(g), dim, lo, hi, _arr(out))
+        return out
+
+    def signed_distance_box(self, grid, lo, hi):
+        out = np.empty(grid.size())
+        g = grid.to_c()
+        self._call(self.lib.hjr_signed_distance_box, C.byref(g), _arr(np.asarray(lo, float)),
+                   _arr(np.asarray(hi, float)), _arr(out))
+        return out
+
+    def hamiltonian(self, model, x, p, db):
+        h = C.c_double()
+        dbs = (abi.HjbInterval * abi.HJB_MAX_INPUT)(*[abi.HjbInterval(b.lo, b.hi) for b in db])
+        m = model_spec(model)
+        self._call(self.lib.hjr_hamiltonian, C.byref(m), _arr(np.asarray(x, float)),
+                   _arr(np.asarray(p, float)), dbs, C.byref(h))
+        return h.value
+
+    def flow_bounds(self, model, x, db):
+        out = np.zeros(abi.HJB_MAX_STATE)
+        dbs = (abi.HjbInterval * abi.HJB_MAX_INPUT)(*[abi.HjbInterval(b.lo, b.hi) for b in db])
+        m = model_spec(model)
+        self._call(self.lib.hjr_flow_bounds, C.byref(m), _arr(np.asarray(x, float)), dbs, _arr(out))
+        return out[:model.state_dim()]
+
+    def write_hjvf(self, path, f):
+        g = f.grid().to_c()
+        self._call(self.lib.hjr_write_hjvf, str(path).encode(), C.byref(g), _arr(_vals(f)))
+
+
+def reference_available() -> bool:
+    return REF_SO.exists()

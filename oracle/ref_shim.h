@@ -1,0 +1,97 @@
+/*
+ * ref_shim.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * extern "C" harness over the UNMODIFIED reference sources
+ * (/root/reference/proj/src/{grid,hjvf,levelset,dynamics,interval_field,
+ * solver}.cpp), compiled by oracle/Makefile into oracle/_ref/libhjref.so.
+ * It is the parity anchor for the C restatement (oracle/hj_oracle.c) and the
+ * CPU arm of bench.py.  The product path never links or loads it.
+ */
+#ifndef HJ_REF_SHIM_H_
+#define HJ_REF_SHIM_H_
+
+#include <stdint.h>
+
+#include "../include/hjb.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum hjr_model_kind {
+  HJR_QUAD2D_VERT = 0,    /* Quad2DVert           dynamics.hpp:102-125 */
+  HJR_PLANAR4D = 1,       /* NearHoverPlanar4D    dynamics.hpp:133-162 */
+  HJR_VERTICAL2D = 2,     /* NearHoverVertical2D  dynamics.hpp:170-197 */
+  HJR_DOUBLE_INT = 3,     /* DoubleIntegrator     dynamics.hpp:201-223 */
+  HJR_TWIN_DI = 4,        /* TwinDoubleIntegrator dynamics.hpp:227-244 */
+  HJR_ADVECTION = 5,      /* ConstantAdvection, test_solver.cpp:14-29  */
+  HJR_NEAR_HOVER_10D = 6  /* NearHover10D         dynamics.hpp:250-271 */
+};
+
+/* Model by kind + parameters.
+ *  QUAD2D_VERT: p = {k_thrust, k_offset, gravity}
+ *  PLANAR4D:    p = {d0, d1, n0, gravity, max_angle_cmd}; d_row = 1 is the
+ *               stock reference class, d_row = 0 the BASELINE variant (wind
+ *               on the position row) as a harness-side DynamicsModel
+ *               subclass, exactly like the reference's own test models.
+ *  VERTICAL2D:  p = {gravity, thrust_gain, frac_lo, frac_hi}
+ *  DOUBLE_INT / TWIN_DI: p = {a_min, a_max}
+ *  ADVECTION:   d_row = number of dims, p = speeds
+ *  NEAR_HOVER_10D: p = {planar d0,d1,n0,g,max_angle, vertical g,kT,lo,hi} */
+typedef struct hjr_model_spec {
+  int32_t kind;
+  int32_t d_row;
+  double p[10];
+} hjr_model_spec;
+
+typedef struct hjr_result {
+  int64_t iterations;
+  double dt;
+  double wall_seconds;
+  int32_t converged;
+  int32_t reserved;
+  int64_t nodes_per_sweep;
+  double* residual_history;
+  int64_t history_capacity;
+} hjr_result;
+
+/* All return 0 on success, 1 std::invalid_argument, 2 std::runtime_error,
+ * 3 other; the message is copied into err (if non-NULL). */
+int hjr_cfl_dt(const hjb_grid* g, const hjr_model_spec* m, const hjb_dbounds* db, double cfl,
+               unsigned threads, double* dt, char* err, int errlen);
+int hjr_vi_step(const hjb_grid* g, const hjr_model_spec* m, const hjb_dbounds* db,
+                const double* v, const double* c, double dt, const hjb_solve_config* cfg,
+                double* out, char* err, int errlen);
+int hjr_solve(const hjb_grid* g, const hjr_model_spec* m, const hjb_dbounds* db,
+              const double* init, const double* c, const hjb_solve_config* cfg, double* out,
+              hjr_result* res, char* err, int errlen);
+int hjr_solve_coarse_to_fine(const hjb_grid* fine, const hjr_model_spec* m,
+                             const hjb_dbounds* db_fine, const double* c_fine,
+                             const hjb_grid* coarse, const hjb_solve_config* cfg,
+                             const double* warm_init_fine, double* coarse_out,
+                             hjr_result* coarse_res, double* fine_out, hjr_result* fine_res,
+                             char* err, int errlen);
+int hjr_resample(const hjb_grid* src_g, const double* src, const hjb_grid* dst_g, double* dst,
+                 char* err, int errlen);
+int hjr_max_adjacent_jump(const hjb_grid* g, const double* v, double* out, char* err,
+                          int errlen);
+int hjr_signed_distance_band(const hjb_grid* g, int32_t dim, double lo, double hi, double* out,
+                             char* err, int errlen);
+int hjr_signed_distance_box(const hjb_grid* g, const double* lo, const double* hi, double* out,
+                            char* err, int errlen);
+/* dynamics probes (test_dynamics.cpp restatements) */
+int hjr_hamiltonian(const hjr_model_spec* m, const double* x, const double* p,
+                    const hjb_interval* db, double* h, char* err, int errlen);
+int hjr_flow_bounds(const hjr_model_spec* m, const double* x, const hjb_interval* db,
+                    double* alpha, char* err, int errlen);
+int hjr_affine(const hjr_model_spec* m, const double* x, double* drift, double* control,
+               double* disturbance, hjb_interval* ubounds, int32_t* dims, char* err,
+               int errlen);
+/* HJVF I/O (hjvf.cpp:46-95) for golden files */
+int hjr_write_hjvf(const char* path, const hjb_grid* g, const double* v, char* err, int errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

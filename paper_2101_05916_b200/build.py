@@ -1,0 +1,60 @@
+"""In-tree build of libhjb.so (the product) with nvcc for sm_100a.
+
+The library is a plain shared object (static cudart, no torch dependency);
+Python reaches it through ctypes (abi.py), C/C++ callers link it directly.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "libhjb.so"
+
+SOURCES = ["hjb_capi.cu", "hjb_kernels.cu", "hjb_ho.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [
+    "-O3", "-lineinfo", "-std=c++17",
+    # bitwise parity with the reference: no a*b+c contraction, IEEE div/sqrt
+    "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
+    "-Xcompiler", "-fPIC,-O3,-ffp-contract=off,-fno-fast-math",
+    "-Xptxas", "-v", "--threads", "0",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (Path(cand).exists() or cand == "nvcc"):
+            return cand
+    return "nvcc"
+
+
+def needs_build() -> bool:
+    if not OUT.exists():
+        return True
+    mtime = OUT.stat().st_mtime
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "hjb.h"]
+    return any(p.stat().st_mtime > mtime for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return OUT
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-shared", "-o", str(OUT),
+           *[str(CSRC / s) for s in SOURCES], "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    log = proc.stdout + proc.stderr
+    (PKG / "build.log").write_text(" ".join(cmd) + "\n" + log)
+    if proc.returncode != 0:
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc failed ({proc.returncode}); see {PKG / 'build.log'}")
+    if verbose:
+        sys.stderr.write(log)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,967 @@
+// hjb_capi.cu — host side of the C ABI declared in include/hjb.h.
+//
+// Validation mirrors the reference's exceptions one for one (solver.cpp,
+// grid.cpp); model descriptors become per-axis tables computed on the host
+// with the reference model's own expressions (std::tan, unary minus first,
+// Grid::coord endpoint rule) so the device consumes identical bits.  The
+// iteration loop of solve() runs on the device: a CUDA graph whose WHILE
+// conditional node repeats a body of sweeps until the last CTA of a sweep
+// clears the condition (converged / diverged / max_iters / horizon).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hjb.h"
+#include "hjb_common.cuh"
+#include "hjb_ho.cuh"
+#include "hjb_kernels.cuh"
+
+using namespace hjb;
+
+thread_local std::string hjb::g_err;
+
+namespace {
+
+// ----------------------------------------------------------------- grid
+// Grid::Grid validation, grid.cpp:10-31
+int make_grid(const hjb_grid* gi, DevGrid& g) {
+  if (!gi) return set_err(HJB_ERR_INVALID_ARGUMENT, "grid: null");
+  if (gi->ndims < 1) return set_err(HJB_ERR_INVALID_ARGUMENT, "Grid: ndims must be >= 1");
+  if (gi->ndims > kMaxDims)
+    return set_err(HJB_ERR_UNSUPPORTED, "Grid: device kernels support up to 6 dims");
+  std::memset(&g, 0, sizeof g);
+  g.nd = gi->ndims;
+  uint64_t size = 1;
+  for (int i = 0; i < g.nd; ++i) {
+    const hjb_grid_dim& d = gi->dims[i];
+    if (!(d.min < d.max))
+      return set_err(HJB_ERR_INVALID_ARGUMENT, "Grid: min must be < max in dim " + std::to_string(i));
+    if (d.n < 2)
+      return set_err(HJB_ERR_INVALID_ARGUMENT,
+                     "Grid: need at least 2 nodes in dim " + std::to_string(i));
+    if (!std::isfinite(d.min) || !std::isfinite(d.max))
+      return set_err(HJB_ERR_INVALID_ARGUMENT, "Grid: non-finite bounds in dim " + std::to_string(i));
+    g.n[i] = static_cast<uint32_t>(d.n);
+    g.min[i] = d.min;
+    g.max[i] = d.max;
+    g.spacing[i] = (d.max - d.min) / static_cast<double>(d.n - 1);
+    g.inv_spacing[i] = 1.0 / g.spacing[i];  // solver.cpp:208-209
+    size *= static_cast<uint64_t>(d.n);
+    if (size >= (1ull << 31))
+      return set_err(HJB_ERR_UNSUPPORTED, "Grid: more than 2^31 nodes per device");
+  }
+  g.size = static_cast<uint32_t>(size);
+  g.stride[g.nd - 1] = 1;
+  for (int i = g.nd - 1; i-- > 0;) g.stride[i] = g.stride[i + 1] * g.n[i + 1];
+  for (int i = 0; i < g.nd; ++i) g.divs[i].init(g.n[i]);
+  return HJB_OK;
+}
+
+// Grid::coord, grid.cpp:33-38
+inline double coord(const DevGrid& g, int d, uint32_t k) {
+  if (k == g.n[d] - 1) return g.max[d];
+  return g.min[d] + static_cast<double>(k) * g.spacing[d];
+}
+
+bool same_grid(const hjb_grid* a, const hjb_grid* b) {
+  if (a->ndims != b->ndims) return false;
+  for (int i = 0; i < a->ndims; ++i)
+    if (a->dims[i].min != b->dims[i].min || a->dims[i].max != b->dims[i].max ||
+        a->dims[i].n != b->dims[i].n)
+      return false;
+  return true;
+}
+
+// ---------------------------------------------------------------- model
+double term_at(const hjb_drift_term& t, double x, uint32_t k) {
+  switch (t.kind) {
+    case HJB_TERM_COORD: return t.scale * x;
+    case HJB_TERM_TAN: return t.scale * std::tan(x);
+    case HJB_TERM_CONST: return t.scale;
+    case HJB_TERM_TABLE: return t.table[k];
+    default: return 0.0;
+  }
+}
+
+struct HostModel {
+  DevModel dm;
+  std::vector<double> tab;
+  bool separable = true;
+};
+
+int check_term(const hjb_drift_term& t, const DevGrid& g) {
+  if (t.kind < HJB_TERM_NONE || t.kind > HJB_TERM_TABLE)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "model: unknown drift term kind");
+  if (t.kind == HJB_TERM_COORD || t.kind == HJB_TERM_TAN || t.kind == HJB_TERM_TABLE) {
+    if (t.axis < 0 || t.axis >= g.nd)
+      return set_err(HJB_ERR_INVALID_ARGUMENT, "model: drift term axis out of range");
+    if (t.kind == HJB_TERM_TABLE && !t.table)
+      return set_err(HJB_ERR_INVALID_ARGUMENT, "model: table term without table");
+  }
+  return HJB_OK;
+}
+
+// make_context checks (solver.cpp:192-199) and the device descriptor.
+int make_model(const hjb_model* mi, const hjb_dbounds* db, const DevGrid& g, HostModel& hm) {
+  if (!mi || !db) return set_err(HJB_ERR_INVALID_ARGUMENT, "model/dbounds: null");
+  if (mi->state_dim < 1 || mi->state_dim > kMaxState || mi->control_dim < 0 ||
+      mi->control_dim > kMaxInput || mi->disturbance_dim < 0 || mi->disturbance_dim > kMaxInput)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "model: bad dimensions");
+  if (db->channels < 0 || db->channels > kMaxInput)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "dbounds: bad channel count");
+  if (g.nd != mi->state_dim)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solver: grid rank does not match model state");
+  if (db->channels != mi->disturbance_dim)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solver: disturbance channel count mismatch");
+  if (!db->per_node)
+    for (int c = 0; c < db->channels; ++c)
+      if (!(db->constant[c].lo <= db->constant[c].hi))
+        return set_err(HJB_ERR_INVALID_ARGUMENT, "IntervalField: lo > hi");
+
+  DevModel& m = hm.dm;
+  std::memset(&m, 0, sizeof m);
+  m.n = mi->state_dim;
+  m.m = mi->control_dim;
+  m.p = mi->disturbance_dim;
+  m.per_node = db->per_node ? 1 : 0;
+  for (int j = 0; j < m.m; ++j) {
+    m.ulo[j] = mi->ubounds[j].lo;
+    m.uhi[j] = mi->ubounds[j].hi;
+  }
+  for (int k = 0; k < m.p; ++k) {
+    m.dlo[k] = db->constant[k].lo;
+    m.dhi[k] = db->constant[k].hi;
+  }
+  // rows_separable (solver.cpp:88-102); B and C do not depend on x.
+  for (int j = 0; j < m.m; ++j) {
+    int rows = 0;
+    for (int i = 0; i < m.n; ++i)
+      if (mi->control[i][j] != 0.0) {
+        m.u_rows[j][m.u_nrow[j]] = i;
+        m.u_coef[j][m.u_nrow[j]] = mi->control[i][j];
+        ++m.u_nrow[j];
+        ++rows;
+      }
+    if (rows > 1) hm.separable = false;
+  }
+  for (int k = 0; k < m.p; ++k) {
+    int rows = 0;
+    for (int i = 0; i < m.n; ++i)
+      if (mi->disturbance[i][k] != 0.0) {
+        m.d_rows[k][m.d_nrow[k]] = i;
+        m.d_coef[k][m.d_nrow[k]] = mi->disturbance[i][k];
+        ++m.d_nrow[k];
+        ++rows;
+      }
+    if (rows > 1) hm.separable = false;
+  }
+
+  std::vector<double>& tab = hm.tab;
+  tab.clear();
+  for (int i = 0; i < m.n; ++i) {
+    const hjb_drift_term* t = mi->drift[i];
+    int rc;
+    if ((rc = check_term(t[0], g)) || (rc = check_term(t[1], g))) return rc;
+    if (t[0].kind == HJB_TERM_NONE && t[1].kind != HJB_TERM_NONE)
+      return set_err(HJB_ERR_INVALID_ARGUMENT, "model: drift term1 without term0");
+    DevRow& r = m.row[i];
+    r.axis_a = r.axis_b = -1;
+    r.off_a = r.off_b = r.off_pos = r.off_neg = r.off_alpha = -1;
+    const bool c0 = t[0].kind == HJB_TERM_NONE || t[0].kind == HJB_TERM_CONST;
+    const bool c1 = t[1].kind == HJB_TERM_NONE || t[1].kind == HJB_TERM_CONST;
+    // drift evaluated the reference way: term0 (+ term1)
+    auto drift_of = [&](uint32_t ka, uint32_t kb) {
+      if (t[0].kind == HJB_TERM_NONE) return 0.0;
+      double v = term_at(t[0], c0 ? 0.0 : coord(g, t[0].axis, ka), ka);
+      if (t[1].kind != HJB_TERM_NONE) v = v + term_at(t[1], c1 ? 0.0 : coord(g, t[1].axis, kb), kb);
+      return v;
+    };
+    if (c0 && c1) {
+      r.constant_drift = 1;
+      r.drift_const = drift_of(0, 0);
+    } else if (!c0 && !c1) {
+      r.axis_a = t[0].axis;
+      r.axis_b = t[1].axis;
+      r.off_a = static_cast<int>(tab.size());
+      for (uint32_t k = 0; k < g.n[r.axis_a]; ++k)
+        tab.push_back(term_at(t[0], coord(g, r.axis_a, k), k));
+      r.off_b = static_cast<int>(tab.size());
+      for (uint32_t k = 0; k < g.n[r.axis_b]; ++k)
+        tab.push_back(term_at(t[1], coord(g, r.axis_b, k), k));
+    } else {
+      // one coordinate term, possibly plus a constant: fully tabulated drift
+      const int ax = c0 ? t[1].axis : t[0].axis;
+      r.axis_a = ax;
+      r.off_a = static_cast<int>(tab.size());
+      for (uint32_t k = 0; k < g.n[ax]; ++k) tab.push_back(drift_of(k, k));
+    }
+    // non-zero control / disturbance terms of the row, reference order
+    for (int j = 0; j < m.m; ++j) {
+      const double B = mi->control[i][j];
+      if (B == 0.0) continue;
+      const double a = B * mi->ubounds[j].lo;
+      const double b = B * mi->ubounds[j].hi;
+      r.uch[r.n_uadd] = j;
+      r.ucoef[r.n_uadd] = B;
+      r.uadd_pos[r.n_uadd] = a < b ? a : b;   // dim_slopes: control minimizes
+      r.uadd_neg[r.n_uadd] = a > b ? a : b;
+      r.ulo_term[r.n_uadd] = b < a ? b : a;   // flow_bounds: std::min
+      r.uhi_term[r.n_uadd] = a < b ? b : a;   // std::max
+      ++r.n_uadd;
+    }
+    for (int k = 0; k < m.p; ++k) {
+      const double Cc = mi->disturbance[i][k];
+      if (Cc == 0.0) continue;
+      r.dch[r.n_dterm] = k;
+      r.dcoef[r.n_dterm] = Cc;
+      ++r.n_dterm;
+    }
+    // Folded Godunov slope and LF alpha tables for rows whose drift depends
+    // on at most one axis, when the disturbance bounds are constant:
+    // dim_slopes / flow_bounds with ALL terms, exactly as the reference.
+    if (!db->per_node && r.axis_b < 0) {
+      const uint32_t len = r.axis_a >= 0 ? g.n[r.axis_a] : 1;
+      std::vector<double> pos(len), neg(len), alpha(len);
+      for (uint32_t k = 0; k < len; ++k) {
+        const double dr = r.constant_drift ? r.drift_const : tab[r.off_a + k];
+        double ps = dr, ng = dr, lo = dr, hi = dr;
+        for (int j = 0; j < m.m; ++j) {
+          const double a = mi->control[i][j] * mi->ubounds[j].lo;
+          const double b = mi->control[i][j] * mi->ubounds[j].hi;
+          ps += a < b ? a : b;
+          ng += a > b ? a : b;
+          lo += b < a ? b : a;
+          hi += a < b ? b : a;
+        }
+        for (int kk = 0; kk < m.p; ++kk) {
+          const double a = mi->disturbance[i][kk] * db->constant[kk].lo;
+          const double b = mi->disturbance[i][kk] * db->constant[kk].hi;
+          ps += a > b ? a : b;
+          ng += a < b ? a : b;
+          lo += b < a ? b : a;
+          hi += a < b ? b : a;
+        }
+        pos[k] = ps;
+        neg[k] = ng;
+        const double al = std::fabs(lo), ah = std::fabs(hi);
+        alpha[k] = al < ah ? ah : al;
+      }
+      r.folded = 1;
+      r.off_pos = static_cast<int>(tab.size());
+      tab.insert(tab.end(), pos.begin(), pos.end());
+      r.off_neg = static_cast<int>(tab.size());
+      tab.insert(tab.end(), neg.begin(), neg.end());
+      r.off_alpha = static_cast<int>(tab.size());
+      tab.insert(tab.end(), alpha.begin(), alpha.end());
+    }
+  }
+  if (tab.empty()) tab.push_back(0.0);
+  return HJB_OK;
+}
+
+// SolveConfig::validate, solver.cpp:13-18
+int validate_cfg(const hjb_solve_config* cfg) {
+  if (!cfg) return set_err(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: null");
+  if (!(cfg->cfl_factor > 0.0) || cfg->cfl_factor > 1.0)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: cfl_factor must be in (0,1]");
+  if (!(cfg->tolerance > 0.0))
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: tolerance must be > 0");
+  if (cfg->max_iters < 0) return set_err(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: max_iters < 0");
+  if (cfg->spatial_order < 1 || cfg->spatial_order > 3 || cfg->time_order < 1 ||
+      cfg->time_order > 3)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: spatial/time order must be 1..3");
+  return HJB_OK;
+}
+
+int upload_model(hjb_context* ctx, HostModel& hm) {
+  CUDA_TRY(ctx->tables.ensure(hm.tab.size() * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(ctx->tables.p, hm.tab.data(), hm.tab.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  hm.dm.tab = ctx->tables.d();
+  return HJB_OK;
+}
+
+struct Scan {
+  double max_speed_sum = 0.0;
+  double max_alpha[kMaxDims] = {0};
+};
+
+// scan_alpha on the device (K1) — solver.cpp:221-268
+int run_scan(hjb_context* ctx, const DevGrid& g, const DevModel& m, Scan& out) {
+  CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
+  CUDA_TRY(cudaMemsetAsync(ctx->scratch.p, 0, (1 + kMaxDims) * sizeof(double), ctx->stream));
+  CUDA_TRY(launch_scan(g, m, ctx->scratch.d(), ctx->stream));
+  ++ctx->launches;
+  double h[1 + kMaxDims];
+  CUDA_TRY(cudaMemcpyAsync(h, ctx->scratch.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  out.max_speed_sum = h[0];
+  for (int d = 0; d < kMaxDims; ++d) out.max_alpha[d] = d < g.nd ? h[1 + d] : 0.0;
+  return HJB_OK;
+}
+
+StepArgs base_args(const DevGrid& g, const DevModel& m, const double* c, double dt,
+                   int scheme, const Scan& s) {
+  StepArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.g = g;
+  a.m = m;
+  a.c = c;
+  a.dt = dt;
+  a.scheme = scheme;
+  for (int d = 0; d < kMaxDims; ++d) a.galpha[d] = s.max_alpha[d];
+  return a;
+}
+
+int scheme_of(const hjb_solve_config* cfg) {
+  if (cfg->scheme == HJB_GODUNOV) return kGodunov;
+  return cfg->dissipation == HJB_GLOBAL ? kLfGlobal : kLfPerNode;
+}
+
+// Loop driver: WHILE-conditional CUDA graph, or (HJB_LOOP=poll) chunks of
+// sweeps with a host poll of the device `done` flag.
+int run_loop(hjb_context* ctx, const StepArgs& proto, int body) {
+  const char* mode = std::getenv("HJB_LOOP");
+  const bool poll = mode && std::strcmp(mode, "poll") == 0;
+  if (!poll) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle handle;
+    CUDA_TRY(cudaGraphCreate(&graph, 0));
+    int rc = HJB_OK;
+    do {
+      cudaError_t e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("conditional handle: ") + cudaGetErrorString(e)); break; }
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = handle;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("conditional node: ") + cudaGetErrorString(e)); break; }
+      cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+      StepArgs a = proto;
+      a.loop = 1;
+      a.handle = handle;
+      a.use_handle = 1;
+      e = cudaStreamBeginCaptureToGraph(ctx->stream, bodyg, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e)); break; }
+      cudaError_t le = cudaSuccess;
+      for (int i = 0; i < body && le == cudaSuccess; ++i) le = launch_step(a, ctx->stream);
+      cudaGraph_t captured = nullptr;
+      e = cudaStreamEndCapture(ctx->stream, &captured);
+      if (le != cudaSuccess || e != cudaSuccess) {
+        rc = set_err(HJB_ERR_CUDA, std::string("capture body: ") +
+                                       cudaGetErrorString(le != cudaSuccess ? le : e));
+        break;
+      }
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(e)); break; }
+      e = cudaGraphLaunch(exec, ctx->stream);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e)); break; }
+      e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("loop: ") + cudaGetErrorString(e)); break; }
+    } while (0);
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    return rc;
+  }
+  StepArgs a = proto;
+  a.loop = 1;
+  a.use_handle = 0;
+  for (;;) {
+    for (int i = 0; i < body; ++i) CUDA_TRY(launch_step(a, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->st_host->done) break;
+  }
+  return HJB_OK;
+}
+
+}  // namespace
+
+// Device-resident solve: every pointer is device memory.  Shared by the
+// host-pointer entry point (which stages through the context buffers).
+static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
+                      const hjb_dbounds* db, const double* init, const double* c,
+                      const hjb_solve_config* cfg, double* value_out, hjb_solve_result* res) {
+  int rc;
+  if ((rc = validate_cfg(cfg))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  HostModel hm;
+  if ((rc = make_model(mi, db, g, hm))) return rc;
+  if ((rc = upload_model(ctx, hm))) return rc;
+  if (db->per_node)
+    for (int ch = 0; ch < db->channels; ++ch) {
+      hm.dm.db_lo[ch] = db->lo[ch];
+      hm.dm.db_hi[ch] = db->hi[ch];
+    }
+  Scan s;
+  if ((rc = run_scan(ctx, g, hm.dm, s))) return rc;
+  if (!(s.max_speed_sum > 0.0))
+    return set_err(HJB_ERR_RUNTIME, "solve: flow is identically zero on the grid");
+  if (cfg->scheme == HJB_GODUNOV && !hm.separable)
+    return set_err(HJB_ERR_INVALID_ARGUMENT,
+                   "solve: model inputs are not row-separable, use the Lax-Friedrichs scheme");
+  const double dt = cfg->cfl_factor / s.max_speed_sum;
+  const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
+
+  hjb_solve_result local;
+  std::memset(&local, 0, sizeof local);
+  if (!res) res = &local;
+  res->dt = dt;
+  res->nodes_per_sweep = g.size;
+  res->converged = 0;
+  res->iterations = 0;
+  res->final_residual = 0.0;
+
+  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+    return ho_solve(ctx, g, hm.dm, init, c, cfg, dt, s.max_alpha, value_out, res);
+
+  CUDA_TRY(ctx->v0.ensure(bytes));
+  CUDA_TRY(ctx->v1.ensure(bytes));
+  CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (cfg->max_iters == 0) {
+    if (value_out != init)
+      CUDA_TRY(cudaMemcpyAsync(value_out, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return HJB_OK;
+  }
+  const long long cap =
+      std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
+  CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
+  CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
+  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
+                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
+                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
+  ++ctx->launches;
+  StepArgs a = base_args(g, hm.dm, c, dt, scheme_of(cfg), s);
+  a.st = ctx->st;
+  a.buf0 = ctx->v0.d();
+  a.buf1 = ctx->v1.d();
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, ctx->stream));
+  const int body = 8;
+  rc = run_loop(ctx, a, body);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const LoopState& st = *ctx->st_host;
+  ctx->launches += st.iter + body;  // sweeps run (+ early-exit tail of the body)
+  res->iterations = st.iter;
+  res->converged = st.converged;
+  res->final_residual = st.last_residual;
+  res->wall_seconds = ms * 1e-3;
+  const long long nh = std::min<long long>(st.iter, res->history_capacity);
+  if (nh > 0 && res->residual_history)
+    CUDA_TRY(cudaMemcpyAsync(res->residual_history, ctx->hist.p, nh * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  if (nh > 0 && res->wall_ms_history)
+    CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  const double* final_buf = (st.iter & 1) ? ctx->v1.d() : ctx->v0.d();
+  CUDA_TRY(cudaMemcpyAsync(value_out, final_buf, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (st.status == HJB_ERR_DIVERGED)
+    return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+  return HJB_OK;
+}
+
+namespace {
+
+// Stage host fields into device buffers owned by the context.
+struct Staged {
+  DevBuf init, c, out, db;
+};
+
+int stage_dbounds(hjb_context* ctx, const hjb_dbounds* db, size_t n, DevBuf& buf,
+                  hjb_dbounds& out) {
+  out = *db;
+  if (!db->per_node || db->channels == 0) return HJB_OK;
+  const size_t bytes = n * sizeof(double);
+  CUDA_TRY(buf.ensure(2 * db->channels * bytes));
+  for (int ch = 0; ch < db->channels; ++ch) {
+    if (!db->lo[ch] || !db->hi[ch]) return set_err(HJB_ERR_INVALID_ARGUMENT, "dbounds: null field");
+    double* lo = buf.d() + (2 * ch) * n;
+    double* hi = buf.d() + (2 * ch + 1) * n;
+    CUDA_TRY(cudaMemcpyAsync(lo, db->lo[ch], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(hi, db->hi[ch], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    out.lo[ch] = lo;
+    out.hi[ch] = hi;
+  }
+  return HJB_OK;
+}
+
+size_t grid_size(const hjb_grid* gi) {
+  size_t n = 1;
+  for (int i = 0; i < gi->ndims; ++i) n *= static_cast<size_t>(gi->dims[i].n);
+  return n;
+}
+
+int check_ctx(hjb_context* ctx) {
+  if (!ctx) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: null");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return HJB_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* hjb_version(void) { return "hjb 0.1 (sm_100a)"; }
+
+const char* hjb_last_error(void) { return g_err.c_str(); }
+
+void hjb_solve_config_default(hjb_solve_config* cfg) {
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->cfl_factor = 0.8;  // solver.hpp:13-15
+  cfg->tolerance = 1e-3;
+  cfg->max_iters = 20000;
+  cfg->scheme = HJB_GODUNOV;
+  cfg->dissipation = HJB_PER_NODE;
+  cfg->spatial_order = 1;
+  cfg->time_order = 1;
+  cfg->time_horizon = 0.0;
+}
+
+int hjb_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return set_err(HJB_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *out = n;
+  return HJB_OK;
+}
+
+int hjb_context_create(int device, hjb_context** out) {
+  if (!out) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: null out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return set_err(HJB_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= n) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: bad device");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return set_err(HJB_ERR_CUDA, "hjb kernels are built for sm_100a (B200); device is sm_" +
+                                     std::to_string(prop.major) + std::to_string(prop.minor));
+  hjb_context* ctx = new hjb_context();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->st, sizeof(LoopState)) != cudaSuccess ||
+      cudaMallocHost(&ctx->st_host, sizeof(LoopState)) != cudaSuccess) {
+    delete ctx;
+    return set_err(HJB_ERR_CUDA, "context: allocation failed");
+  }
+  *out = ctx;
+  return HJB_OK;
+}
+
+int hjb_context_destroy(hjb_context* ctx) {
+  if (!ctx) return HJB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->st) cudaFree(ctx->st);
+  if (ctx->st_host) cudaFreeHost(ctx->st_host);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return HJB_OK;
+}
+
+void* hjb_context_stream(hjb_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int hjb_context_synchronize(hjb_context* ctx) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int64_t hjb_context_launch_count(hjb_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int hjb_cfl_dt(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const hjb_dbounds* db,
+               double cfl_factor, double* dt_out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  if (!(cfl_factor > 0.0) || cfl_factor > 1.0)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: cfl_factor must be in (0,1]");
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  HostModel hm;
+  if ((rc = make_model(mi, db, g, hm))) return rc;
+  if ((rc = upload_model(ctx, hm))) return rc;
+  DevBuf dbb;
+  hjb_dbounds dbs;
+  if ((rc = stage_dbounds(ctx, db, g.size, dbb, dbs))) return rc;
+  for (int ch = 0; ch < db->channels; ++ch) {
+    hm.dm.db_lo[ch] = dbs.lo[ch];
+    hm.dm.db_hi[ch] = dbs.hi[ch];
+  }
+  Scan s;
+  if ((rc = run_scan(ctx, g, hm.dm, s))) return rc;
+  if (!(s.max_speed_sum > 0.0))
+    return set_err(HJB_ERR_RUNTIME, "cfl_dt: flow is identically zero on the grid");
+  *dt_out = cfl_factor / s.max_speed_sum;
+  return HJB_OK;
+}
+
+// vi_step on device pointers (solver.cpp:284-308)
+int hjb_vi_step_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
+                    const hjb_dbounds* db, const double* value, const double* constraint,
+                    double dt, const hjb_solve_config* cfg, double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  hjb_solve_config dflt;
+  if (!cfg) {
+    hjb_solve_config_default(&dflt);
+    cfg = &dflt;
+  }
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  HostModel hm;
+  if ((rc = make_model(mi, db, g, hm))) return rc;
+  if ((rc = upload_model(ctx, hm))) return rc;
+  for (int ch = 0; db->per_node && ch < db->channels; ++ch) {
+    hm.dm.db_lo[ch] = db->lo[ch];
+    hm.dm.db_hi[ch] = db->hi[ch];
+  }
+  Scan s;
+  if ((rc = run_scan(ctx, g, hm.dm, s))) return rc;
+  if (dt * s.max_speed_sum > 1.0 + 1e-12)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "vi_step: dt violates the CFL bound");
+  if (cfg->scheme == HJB_GODUNOV && !hm.separable)
+    return set_err(HJB_ERR_INVALID_ARGUMENT,
+                   "vi_step: model inputs are not row-separable, use the Lax-Friedrichs scheme");
+  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+    return ho_vi_step(ctx, g, hm.dm, value, constraint, cfg, dt, s.max_alpha, out);
+  StepArgs a = base_args(g, hm.dm, constraint, dt, scheme_of(cfg), s);
+  a.st = ctx->st;
+  a.loop = 0;
+  a.src = value;
+  a.dst = out;
+  if (value == out) {
+    // out may alias value: sweep into a scratch buffer first
+    CUDA_TRY(ctx->v1.ensure(static_cast<size_t>(g.size) * sizeof(double)));
+    a.dst = ctx->v1.d();
+  }
+  CUDA_TRY(launch_step(a, ctx->stream));
+  ++ctx->launches;
+  if (a.dst != out)
+    CUDA_TRY(cudaMemcpyAsync(out, a.dst, g.size * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_vi_step(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const hjb_dbounds* db,
+                const double* value, const double* constraint, double dt,
+                const hjb_solve_config* cfg, double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
+  Staged sb;
+  CUDA_TRY(sb.init.ensure(bytes));
+  CUDA_TRY(sb.c.ensure(bytes));
+  CUDA_TRY(sb.out.ensure(bytes));
+  CUDA_TRY(cudaMemcpyAsync(sb.init.p, value, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(sb.c.p, constraint, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  hjb_dbounds dbs;
+  if ((rc = stage_dbounds(ctx, db, g.size, sb.db, dbs))) return rc;
+  if ((rc = hjb_vi_step_dev(ctx, gi, mi, &dbs, sb.init.d(), sb.c.d(), dt, cfg, sb.out.d())))
+    return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, sb.out.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_solve_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
+                  const hjb_dbounds* db, const double* init, const double* constraint,
+                  const hjb_solve_config* cfg, double* value_out, hjb_solve_result* res) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  return solve_impl(ctx, gi, mi, db, init, constraint, cfg, value_out, res);
+}
+
+int hjb_solve(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const hjb_dbounds* db,
+              const double* init, const double* constraint, const hjb_solve_config* cfg,
+              double* value_out, hjb_solve_result* res) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  if ((rc = validate_cfg(cfg))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
+  CUDA_TRY(ctx->xbuf.ensure(bytes));
+  CUDA_TRY(ctx->cbuf.ensure(bytes));
+  CUDA_TRY(cudaMemcpyAsync(ctx->xbuf.p, init, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->cbuf.p, constraint, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  hjb_dbounds dbs;
+  if ((rc = stage_dbounds(ctx, db, g.size, ctx->dbbuf, dbs))) return rc;
+  rc = solve_impl(ctx, gi, mi, &dbs, ctx->xbuf.d(), ctx->cbuf.d(), cfg, ctx->xbuf.d(), res);
+  if (rc && rc != HJB_ERR_DIVERGED) return rc;
+  const int status = rc;
+  const std::string msg = g_err;
+  CUDA_TRY(cudaMemcpyAsync(value_out, ctx->xbuf.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (status) return set_err(status, msg);
+  return HJB_OK;
+}
+
+int hjb_resample_dev(hjb_context* ctx, const hjb_grid* sgi, const double* src,
+                     const hjb_grid* dgi, double* dst) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid sg, dg;
+  if ((rc = make_grid(sgi, sg)) || (rc = make_grid(dgi, dg))) return rc;
+  if (sg.nd != dg.nd) return set_err(HJB_ERR_INVALID_ARGUMENT, "resample: dimension mismatch");
+  CUDA_TRY(launch_resample(sg, src, dg, dst, nullptr, nullptr, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_max_adjacent_jump_dev(hjb_context* ctx, const hjb_grid* gi, const double* field,
+                              double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
+  double* slot = ctx->scratch.d() + 16;
+  CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(double), ctx->stream));
+  CUDA_TRY(launch_max_adjacent_jump(g, field, slot, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaMemcpyAsync(out, slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_seed_from_dev(hjb_context* ctx, const hjb_grid* sgi, const double* src,
+                      const hjb_grid* dgi, const double* constraint_dst, double* dst) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid sg, dg;
+  if ((rc = make_grid(sgi, sg)) || (rc = make_grid(dgi, dg))) return rc;
+  if (sg.nd != dg.nd) return set_err(HJB_ERR_INVALID_ARGUMENT, "resample: dimension mismatch");
+  CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
+  double* slot = ctx->scratch.d() + 17;
+  CUDA_TRY(cudaMemsetAsync(slot, 0, sizeof(double), ctx->stream));
+  CUDA_TRY(launch_max_adjacent_jump(sg, src, slot, ctx->stream));
+  CUDA_TRY(launch_resample(sg, src, dg, dst, slot, constraint_dst, ctx->stream));
+  ctx->launches += 2;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_signed_distance_band_dev(hjb_context* ctx, const hjb_grid* gi, int32_t dim, double lo,
+                                 double hi, double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  if (dim < 0 || dim >= g.nd)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "signed_distance_band: dim out of range");
+  if (!(lo < hi)) return set_err(HJB_ERR_INVALID_ARGUMENT, "signed_distance_band: lo must be < hi");
+  CUDA_TRY(launch_band(g, dim, lo, hi, out, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_field_max_dev(hjb_context* ctx, int64_t n, const double* a, const double* b,
+                      double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  CUDA_TRY(launch_field_op(n, a, b, out, 1, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_field_min_dev(hjb_context* ctx, int64_t n, const double* a, const double* b,
+                      double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  CUDA_TRY(launch_field_op(n, a, b, out, 0, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+// --------------------------------------------------- host-pointer helpers
+int hjb_resample(hjb_context* ctx, const hjb_grid* sgi, const double* src, const hjb_grid* dgi,
+                 double* dst) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid sg, dg;
+  if ((rc = make_grid(sgi, sg)) || (rc = make_grid(dgi, dg))) return rc;
+  DevBuf s, d;
+  CUDA_TRY(s.ensure(sg.size * sizeof(double)));
+  CUDA_TRY(d.ensure(dg.size * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(s.p, src, sg.size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  if ((rc = hjb_resample_dev(ctx, sgi, s.d(), dgi, d.d()))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dst, d.p, dg.size * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_max_adjacent_jump(hjb_context* ctx, const hjb_grid* gi, const double* field,
+                          double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  DevBuf s;
+  CUDA_TRY(s.ensure(g.size * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(s.p, field, g.size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  return hjb_max_adjacent_jump_dev(ctx, gi, s.d(), out);
+}
+
+int hjb_seed_from(hjb_context* ctx, const hjb_grid* sgi, const double* src, const hjb_grid* dgi,
+                  const double* constraint_dst, double* dst) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid sg, dg;
+  if ((rc = make_grid(sgi, sg)) || (rc = make_grid(dgi, dg))) return rc;
+  DevBuf s, c, d;
+  CUDA_TRY(s.ensure(sg.size * sizeof(double)));
+  CUDA_TRY(c.ensure(dg.size * sizeof(double)));
+  CUDA_TRY(d.ensure(dg.size * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(s.p, src, sg.size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(c.p, constraint_dst, dg.size * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  if ((rc = hjb_seed_from_dev(ctx, sgi, s.d(), dgi, c.d(), d.d()))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dst, d.p, dg.size * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_signed_distance_band(hjb_context* ctx, const hjb_grid* gi, int32_t dim, double lo,
+                             double hi, double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid g;
+  if ((rc = make_grid(gi, g))) return rc;
+  DevBuf d;
+  CUDA_TRY(d.ensure(g.size * sizeof(double)));
+  if ((rc = hjb_signed_distance_band_dev(ctx, gi, dim, lo, hi, d.d()))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, d.p, g.size * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+// solve_coarse_to_fine, solver.cpp:387-425, entirely on the device:
+// restriction of c and the disturbance bounds, seeding, both solves.
+int hjb_solve_coarse_to_fine(hjb_context* ctx, const hjb_grid* fgi, const hjb_model* mi,
+                             const hjb_dbounds* db, const double* c_fine,
+                             const hjb_grid* cgi, const hjb_solve_config* cfg,
+                             const double* warm_init_fine, double* coarse_out,
+                             hjb_solve_result* coarse_res, double* fine_out,
+                             hjb_solve_result* fine_res, double* wall_seconds) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  DevGrid fg, cg;
+  if ((rc = make_grid(fgi, fg)) || (rc = make_grid(cgi, cg))) return rc;
+  if (cg.nd != fg.nd)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_coarse_to_fine: grid rank mismatch");
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, ctx->stream));
+  const size_t fb = fg.size * sizeof(double), cb = cg.size * sizeof(double);
+  DevBuf dcf, dcc, dinit_c, dinit_f, dout_c, dout_f, dwarm, ddbf, ddbc;
+  CUDA_TRY(dcf.ensure(fb));
+  CUDA_TRY(dcc.ensure(cb));
+  CUDA_TRY(dinit_c.ensure(cb));
+  CUDA_TRY(dinit_f.ensure(fb));
+  CUDA_TRY(dout_c.ensure(cb));
+  CUDA_TRY(dout_f.ensure(fb));
+  CUDA_TRY(cudaMemcpyAsync(dcf.p, c_fine, fb, cudaMemcpyHostToDevice, ctx->stream));
+  // c_coarse = resample(c_fine, coarse) (solver.cpp:396)
+  CUDA_TRY(launch_resample(fg, dcf.d(), cg, dcc.d(), nullptr, nullptr, ctx->stream));
+  // db_coarse = resample(db_fine, coarse) (solver.cpp:397, 378-385)
+  hjb_dbounds dbf = *db, dbc = *db;
+  const int nch = db->channels;
+  if (nch > 0) {
+    CUDA_TRY(ddbf.ensure(2 * nch * fb));
+    CUDA_TRY(ddbc.ensure(2 * nch * cb));
+    for (int ch = 0; ch < nch; ++ch) {
+      for (int s = 0; s < 2; ++s) {
+        double* f = ddbf.d() + (2 * ch + s) * fg.size;
+        double* cc = ddbc.d() + (2 * ch + s) * cg.size;
+        if (db->per_node) {
+          CUDA_TRY(cudaMemcpyAsync(f, s ? db->hi[ch] : db->lo[ch], fb, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+        } else {
+          std::vector<double> tmp(fg.size, s ? db->constant[ch].hi : db->constant[ch].lo);
+          CUDA_TRY(cudaMemcpyAsync(f, tmp.data(), fb, cudaMemcpyHostToDevice, ctx->stream));
+          CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        }
+        CUDA_TRY(launch_resample(fg, f, cg, cc, nullptr, nullptr, ctx->stream));
+        if (s) {
+          dbf.hi[ch] = f;
+          dbc.hi[ch] = cc;
+        } else {
+          dbf.lo[ch] = f;
+          dbc.lo[ch] = cc;
+        }
+      }
+    }
+    dbc.per_node = 1;
+    if (db->per_node) dbf.per_node = 1; else dbf = *db;
+  }
+  // init_coarse = warm ? seed_from(warm, coarse, c_coarse) : c_coarse
+  if (warm_init_fine) {
+    CUDA_TRY(dwarm.ensure(fb));
+    CUDA_TRY(cudaMemcpyAsync(dwarm.p, warm_init_fine, fb, cudaMemcpyHostToDevice, ctx->stream));
+    if ((rc = hjb_seed_from_dev(ctx, fgi, dwarm.d(), cgi, dcc.d(), dinit_c.d()))) return rc;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(dinit_c.p, dcc.p, cb, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if ((rc = solve_impl(ctx, cgi, mi, &dbc, dinit_c.d(), dcc.d(), cfg, dout_c.d(), coarse_res)))
+    return rc;
+  if ((rc = hjb_seed_from_dev(ctx, cgi, dout_c.d(), fgi, dcf.d(), dinit_f.d()))) return rc;
+  if ((rc = solve_impl(ctx, fgi, mi, &dbf, dinit_f.d(), dcf.d(), cfg, dout_f.d(), fine_res)))
+    return rc;
+  CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(coarse_out, dout_c.p, cb, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(fine_out, dout_f.p, fb, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (wall_seconds) *wall_seconds = ms * 1e-3;
+  return HJB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,548 @@
+// hjb_kernels.cu — generic-rank sm_100a kernels of the HJ reachability solver.
+//
+// Bitwise contract: every expression below reproduces the reference's
+// (proj/src/solver.cpp, dynamics.cpp, grid.cpp, levelset.cpp) operand order;
+// built with -fmad=false no multiply-add is contracted.  Terms the reference
+// accumulates with a zero coefficient (0*lo, 0*u) are skipped: adding +-0
+// never changes a value, only possibly the sign of an exact zero, and the
+// parity contract compares fields with IEEE ==.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hjb_kernels.cuh"
+
+namespace hjb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int ND>
+__device__ __forceinline__ void unravel(const DevGrid& g, uint32_t lin, uint32_t* idx) {
+#pragma unroll
+  for (int d = ND - 1; d >= 0; --d) {
+    const uint32_t q = g.divs[d].quo(lin);
+    idx[d] = lin - q * g.n[d];
+    lin = q;
+  }
+}
+
+// max over non-negative doubles through their IEEE bit patterns (which order
+// like the values); NaN never enters: callers only fold values with `>`.
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v) {
+  __shared__ unsigned long long part[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max_u64(v);
+  if (lane == 0) part[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? part[lane] : 0ull;
+    v = warp_max_u64(v);
+  }
+  return v;  // valid in thread 0
+}
+
+// Epilogue of one sweep: residual, histories, convergence and divergence
+// tests of solver.cpp:347-369, executed by the last CTA to finish.
+__device__ void finish_sweep(const StepArgs& a, double local_max) {
+  LoopState* st = a.st;
+  const unsigned long long b = block_max_u64(__double_as_longlong(local_max));
+  if (threadIdx.x != 0) return;
+  if (b) atomicMax(&st->maxdv_bits, b);
+  if (!a.loop) return;
+  __threadfence();
+  const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
+  if (ticket != gridDim.x * gridDim.y - 1) return;
+  __threadfence();
+  const unsigned long long bits = atomicAdd(&st->maxdv_bits, 0ull);
+  const double max_dv = __longlong_as_double(bits);
+  const double residual = max_dv / st->dt;
+  const long long iter = st->iter + 1;
+  st->iter = iter;
+  if (iter - 1 < st->history_cap) {
+    if (st->history) st->history[iter - 1] = residual;
+    if (st->wall_history)
+      st->wall_history[iter - 1] = (double)(globaltimer_ns() - st->t0_ns) * 1e-6;
+  }
+  st->last_residual = residual;
+  bool stop = false;
+  if (residual < st->tol) {
+    st->converged = 1;
+    stop = true;
+  } else {
+    if (iter == 1) st->first_residual = residual;
+    const double mr0 = st->min_residual;
+    const double mr = residual < mr0 ? residual : mr0;  // std::min(min_residual, residual)
+    st->min_residual = mr;
+    const double first = st->first_residual;
+    const double base = mr < first ? first : mr;  // std::max(min_residual, front)
+    if (!isfinite(residual) || residual > 10.0 * base) {
+      st->status = HJB_ERR_DIVERGED;
+      stop = true;
+    }
+  }
+  if (iter >= st->max_iters) stop = true;
+  if (st->horizon > 0.0 && (double)iter * st->dt >= st->horizon) stop = true;
+  st->maxdv_bits = 0ull;
+  st->blocks_done = 0u;
+  if (stop) {
+    st->done = 1;
+    if (a.use_handle) cudaGraphSetConditional(a.handle, 0u);
+  }
+  __threadfence();
+}
+
+// drift_i(x) of the separable affine model (AffineFlow::drift, model
+// affine() of dynamics.cpp:126-198 evaluated through host-built tables).
+template <int ND>
+__device__ __forceinline__ double row_drift(const DevModel& m, const DevRow& r,
+                                            const uint32_t* idx) {
+  if (r.constant_drift) return r.drift_const;
+  double v = __ldg(m.tab + r.off_a + idx[r.axis_a]);
+  if (r.axis_b >= 0) v = v + __ldg(m.tab + r.off_b + idx[r.axis_b]);
+  return v;
+}
+
+template <bool PERNODE>
+__device__ __forceinline__ void dist_bounds(const DevModel& m, int ch, uint32_t lin, double& lo,
+                                            double& hi) {
+  if (PERNODE) {
+    lo = __ldg(m.db_lo[ch] + lin);
+    hi = __ldg(m.db_hi[ch] + lin);
+  } else {
+    lo = m.dlo[ch];
+    hi = m.dhi[ch];
+  }
+}
+
+// dim_slopes for one row (solver.cpp:67-86)
+template <int ND, bool PERNODE>
+__device__ __forceinline__ void row_slopes(const DevModel& m, const DevRow& r,
+                                           const uint32_t* idx, uint32_t lin, double& pos,
+                                           double& neg) {
+  if (!PERNODE && r.folded) {
+    const uint32_t k = r.axis_a >= 0 ? idx[r.axis_a] : 0u;
+    pos = __ldg(m.tab + r.off_pos + k);
+    neg = __ldg(m.tab + r.off_neg + k);
+    return;
+  }
+  const double dr = row_drift<ND>(m, r, idx);
+  pos = dr;
+  neg = dr;
+  for (int t = 0; t < r.n_uadd; ++t) {
+    pos += r.uadd_pos[t];
+    neg += r.uadd_neg[t];
+  }
+  for (int t = 0; t < r.n_dterm; ++t) {
+    double lo, hi;
+    dist_bounds<PERNODE>(m, r.dch[t], lin, lo, hi);
+    const double a = r.dcoef[t] * lo;
+    const double b = r.dcoef[t] * hi;
+    pos += a > b ? a : b;
+    neg += a < b ? a : b;
+  }
+}
+
+// godunov_flux (solver.cpp:44-63)
+__device__ __forceinline__ double godunov_flux(double pos, double neg, double dminus,
+                                               double dplus) {
+  const double ha = dminus > 0.0 ? pos * dminus : neg * dminus;
+  const double hb = dplus > 0.0 ? pos * dplus : neg * dplus;
+  if (dminus <= dplus) {
+    double h = ha > hb ? ha : hb;
+    if (dminus <= 0.0 && 0.0 <= dplus && h < 0.0) h = 0.0;
+    return h;
+  }
+  double h = ha < hb ? ha : hb;
+  if (dplus <= 0.0 && 0.0 <= dminus && h > 0.0) h = 0.0;
+  return h;
+}
+
+// flow_bounds alpha for one row (dynamics.cpp:93-112)
+template <int ND, bool PERNODE>
+__device__ __forceinline__ double row_alpha(const DevModel& m, const DevRow& r,
+                                            const uint32_t* idx, uint32_t lin) {
+  if (!PERNODE && r.off_alpha >= 0) {
+    const uint32_t k = r.axis_a >= 0 ? idx[r.axis_a] : 0u;
+    return __ldg(m.tab + r.off_alpha + k);
+  }
+  const double dr = row_drift<ND>(m, r, idx);
+  double lo = dr, hi = dr;
+  for (int t = 0; t < r.n_uadd; ++t) {
+    lo += r.ulo_term[t];
+    hi += r.uhi_term[t];
+  }
+  for (int t = 0; t < r.n_dterm; ++t) {
+    double dlo, dhi;
+    dist_bounds<PERNODE>(m, r.dch[t], lin, dlo, dhi);
+    const double a = r.dcoef[t] * dlo;
+    const double b = r.dcoef[t] * dhi;
+    lo += b < a ? b : a;  // std::min
+    hi += a < b ? b : a;  // std::max
+  }
+  const double al = fabs(lo), ah = fabs(hi);
+  return al < ah ? ah : al;
+}
+
+// extremal_inputs + hamiltonian (dynamics.cpp:37-83)
+template <int ND, bool PERNODE>
+__device__ __forceinline__ double lf_hamiltonian(const DevModel& m, const double* p,
+                                                 const uint32_t* idx, uint32_t lin) {
+  double u[kMaxInput], d[kMaxInput];
+  for (int j = 0; j < m.m; ++j) {
+    double coeff = 0.0;
+    for (int t = 0; t < m.u_nrow[j]; ++t) coeff += p[m.u_rows[j][t]] * m.u_coef[j][t];
+    u[j] = coeff > 0.0 ? m.ulo[j] : (coeff < 0.0 ? m.uhi[j] : m.ulo[j]);
+  }
+  for (int k = 0; k < m.p; ++k) {
+    double coeff = 0.0;
+    for (int t = 0; t < m.d_nrow[k]; ++t) coeff += p[m.d_rows[k][t]] * m.d_coef[k][t];
+    double lo, hi;
+    dist_bounds<PERNODE>(m, k, lin, lo, hi);
+    d[k] = coeff > 0.0 ? hi : (coeff < 0.0 ? lo : lo);
+  }
+  double h = 0.0;
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    const DevRow& r = m.row[i];
+    double fi = row_drift<ND>(m, r, idx);
+    for (int t = 0; t < r.n_uadd; ++t) fi += r.ucoef[t] * u[r.uch[t]];
+    for (int t = 0; t < r.n_dterm; ++t) fi += r.dcoef[t] * d[r.dch[t]];
+    h += p[i] * fi;
+  }
+  return h;
+}
+
+// K2/K3: update_chunk (solver.cpp:106-190) for one node per thread.
+template <int ND, int SCHEME, bool PERNODE>
+__global__ void __launch_bounds__(kThreads) k_step(const __grid_constant__ StepArgs a) {
+  const double* src;
+  double* dst;
+  if (a.loop) {
+    if (*(volatile int*)&a.st->done) return;
+    const long long it = a.st->iter;
+    src = (it & 1) ? a.buf1 : a.buf0;
+    dst = (it & 1) ? a.buf0 : a.buf1;
+  } else {
+    src = a.src;
+    dst = a.dst;
+  }
+  const DevGrid& g = a.g;
+  const uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x;
+  double local = 0.0;
+  if (lin < g.size) {
+    uint32_t idx[ND];
+    unravel<ND>(g, lin, idx);
+    const double v = src[lin];
+    double dm[ND], dp[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const uint32_t s = g.stride[d];
+      const uint32_t k = idx[d];
+      const double inv = g.inv_spacing[d];
+      double left, right;
+      if (k > 0 && k < g.n[d] - 1) {
+        left = (v - src[lin - s]) * inv;
+        right = (src[lin + s] - v) * inv;
+      } else if (k == 0) {
+        right = (src[lin + s] - v) * inv;
+        left = SCHEME == kGodunov ? 0.0 : right;
+      } else {
+        left = (v - src[lin - s]) * inv;
+        right = SCHEME == kGodunov ? 0.0 : left;
+      }
+      dm[d] = left;
+      dp[d] = right;
+    }
+    double hhat = 0.0;
+    if (SCHEME == kGodunov) {
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        double pos, neg;
+        row_slopes<ND, PERNODE>(a.m, a.m.row[d], idx, lin, pos, neg);
+        hhat += godunov_flux(pos, neg, dm[d], dp[d]);
+      }
+    } else {
+      double p[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) p[d] = 0.5 * (dm[d] + dp[d]);
+      hhat = lf_hamiltonian<ND, PERNODE>(a.m, p, idx, lin);
+      if (SCHEME == kLfPerNode) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const double al = row_alpha<ND, PERNODE>(a.m, a.m.row[d], idx, lin);
+          hhat += al * 0.5 * (dp[d] - dm[d]);
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) hhat += a.galpha[d] * 0.5 * (dp[d] - dm[d]);
+      }
+    }
+    const double stepped = v + a.dt * hhat;
+    const double cc = a.c[lin];
+    const double vnew = stepped > cc ? stepped : cc;
+    dst[lin] = vnew;
+    const double dv = fabs(vnew - v);
+    if (dv > local) local = dv;
+  }
+  finish_sweep(a, local);
+}
+
+// K1: scan_alpha (solver.cpp:221-268)
+template <int ND, bool PERNODE>
+__global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ DevGrid g,
+                                                   const __grid_constant__ DevModel m,
+                                                   double* out) {
+  const uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x;
+  double speed_max = 0.0;
+  double amax[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) amax[d] = 0.0;
+  if (lin < g.size) {
+    uint32_t idx[ND];
+    unravel<ND>(g, lin, idx);
+    double speed = 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const double al = row_alpha<ND, PERNODE>(m, m.row[d], idx, lin);
+      speed += al * g.inv_spacing[d];
+      amax[d] = al;
+    }
+    speed_max = speed;
+  }
+  unsigned long long b = block_max_u64(__double_as_longlong(speed_max));
+  if (threadIdx.x == 0 && b) atomicMax((unsigned long long*)out, b);
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    __syncthreads();
+    b = block_max_u64(__double_as_longlong(amax[d]));
+    if (threadIdx.x == 0 && b) atomicMax((unsigned long long*)(out + 1 + d), b);
+  }
+}
+
+__global__ void k_loop_init(LoopState* st, long long max_iters, double dt, double tol,
+                            double horizon, long long history_cap, double* history,
+                            double* wall_history) {
+  st->maxdv_bits = 0ull;
+  st->blocks_done = 0u;
+  st->done = 0;
+  st->status = 0;
+  st->converged = 0;
+  st->iter = 0;
+  st->max_iters = max_iters;
+  st->history_cap = history_cap;
+  st->dt = dt;
+  st->tol = tol;
+  st->horizon = horizon;
+  st->min_residual = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  st->first_residual = 0.0;
+  st->last_residual = 0.0;
+  st->history = history;
+  st->wall_history = wall_history;
+  st->t0_ns = globaltimer_ns();
+}
+
+// K4: resample (grid.cpp:84-135 locate/interp_ex, 215-231) with the optional
+// seed clamp of solver.cpp:404-411.
+template <int ND>
+__global__ void __launch_bounds__(kThreads)
+    k_resample(const __grid_constant__ DevGrid sg, const double* __restrict__ src,
+               const __grid_constant__ DevGrid dg, double* __restrict__ dst,
+               const double* slack, const double* __restrict__ c) {
+  const uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lin >= dg.size) return;
+  uint32_t idx[ND];
+  unravel<ND>(dg, lin, idx);
+  uint32_t base[ND];
+  double frac[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    const double x = idx[d] == dg.n[d] - 1 ? dg.max[d] : dg.min[d] + (double)idx[d] * dg.spacing[d];
+    double t = (x - sg.min[d]) / sg.spacing[d];
+    if (t < 0.0) t = 0.0;
+    const double tmax = (double)(sg.n[d] - 1);
+    if (t > tmax) t = tmax;
+    uint32_t i0 = (uint32_t)t;
+    if (i0 > sg.n[d] - 2) i0 = sg.n[d] - 2;
+    base[d] = i0;
+    frac[d] = t - (double)i0;
+  }
+  double value = 0.0;
+  constexpr int corners = 1 << ND;
+#pragma unroll 4
+  for (int corner = 0; corner < corners; ++corner) {
+    double w = 1.0;
+    uint32_t l = 0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const bool hi = (corner >> d) & 1;
+      w *= hi ? frac[d] : 1.0 - frac[d];
+      l += (base[d] + (hi ? 1u : 0u)) * sg.stride[d];
+    }
+    if (w != 0.0) value += w * src[l];
+  }
+  if (c) {
+    const double a = value - *slack;
+    const double b = c[lin];
+    value = a < b ? b : a;  // std::max(init - slack, constraint)
+  }
+  dst[lin] = value;
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kThreads)
+    k_max_jump(const __grid_constant__ DevGrid g, const double* __restrict__ f, double* out) {
+  const uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x;
+  double jump = 0.0;
+  if (lin < g.size) {
+    uint32_t idx[ND];
+    unravel<ND>(g, lin, idx);
+    const double v = f[lin];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      if (idx[d] + 1 >= g.n[d]) continue;
+      const double dv = fabs(f[lin + g.stride[d]] - v);
+      if (dv > jump) jump = dv;
+    }
+  }
+  const unsigned long long b = block_max_u64(__double_as_longlong(jump));
+  if (threadIdx.x == 0 && b) atomicMax((unsigned long long*)out, b);
+}
+
+template <int ND>
+__global__ void k_band(const __grid_constant__ DevGrid g, int dim, double lo, double hi,
+                       double* out) {
+  const uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lin >= g.size) return;
+  uint32_t idx[ND];
+  unravel<ND>(g, lin, idx);
+  const uint32_t k = idx[dim];
+  const double x = k == g.n[dim] - 1 ? g.max[dim] : g.min[dim] + (double)k * g.spacing[dim];
+  const double a = lo - x, b = x - hi;
+  out[lin] = a < b ? b : a;  // std::max(lo - x, x - hi)
+}
+
+__global__ void k_field_op(long long n, const double* __restrict__ a,
+                           const double* __restrict__ b, double* __restrict__ out, int is_max) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    out[i] = is_max ? (x < y ? y : x) : (y < x ? y : x);
+  }
+}
+
+inline dim3 blocks_for(uint32_t n) { return dim3((n + kThreads - 1) / kThreads); }
+
+template <int ND>
+cudaError_t step_nd(const StepArgs& a, cudaStream_t s) {
+  const dim3 grid = blocks_for(a.g.size);
+  const bool pn = a.m.per_node != 0;
+  switch (a.scheme) {
+    case kGodunov:
+      if (pn) k_step<ND, kGodunov, true><<<grid, kThreads, 0, s>>>(a);
+      else k_step<ND, kGodunov, false><<<grid, kThreads, 0, s>>>(a);
+      break;
+    case kLfPerNode:
+      if (pn) k_step<ND, kLfPerNode, true><<<grid, kThreads, 0, s>>>(a);
+      else k_step<ND, kLfPerNode, false><<<grid, kThreads, 0, s>>>(a);
+      break;
+    default:
+      if (pn) k_step<ND, kLfGlobal, true><<<grid, kThreads, 0, s>>>(a);
+      else k_step<ND, kLfGlobal, false><<<grid, kThreads, 0, s>>>(a);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+#define HJB_DISPATCH_ND(nd, CALL) \
+  switch (nd) {                    \
+    case 1: CALL(1); break;        \
+    case 2: CALL(2); break;        \
+    case 3: CALL(3); break;        \
+    case 4: CALL(4); break;        \
+    case 5: CALL(5); break;        \
+    case 6: CALL(6); break;        \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_step(const StepArgs& a, cudaStream_t s) {
+#define CALL(N) return step_nd<N>(a, s)
+  HJB_DISPATCH_ND(a.g.nd, CALL)
+#undef CALL
+  return cudaSuccess;
+}
+
+cudaError_t launch_scan(const DevGrid& g, const DevModel& m, double* out, cudaStream_t s) {
+  const dim3 grid = blocks_for(g.size);
+#define CALL(N)                                                    \
+  if (m.per_node) k_scan<N, true><<<grid, kThreads, 0, s>>>(g, m, out); \
+  else k_scan<N, false><<<grid, kThreads, 0, s>>>(g, m, out)
+  HJB_DISPATCH_ND(g.nd, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loop_init(LoopState* st, long long max_iters, double dt, double tol,
+                             double horizon, long long history_cap, double* history,
+                             double* wall_history, cudaStream_t s) {
+  k_loop_init<<<1, 1, 0, s>>>(st, max_iters, dt, tol, horizon, history_cap, history,
+                              wall_history);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resample(const DevGrid& sg, const double* src, const DevGrid& dg,
+                            double* dst, const double* slack, const double* c,
+                            cudaStream_t s) {
+  const dim3 grid = blocks_for(dg.size);
+#define CALL(N) k_resample<N><<<grid, kThreads, 0, s>>>(sg, src, dg, dst, slack, c)
+  HJB_DISPATCH_ND(dg.nd, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_adjacent_jump(const DevGrid& g, const double* f, double* out,
+                                     cudaStream_t s) {
+  const dim3 grid = blocks_for(g.size);
+#define CALL(N) k_max_jump<N><<<grid, kThreads, 0, s>>>(g, f, out)
+  HJB_DISPATCH_ND(g.nd, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band(const DevGrid& g, int dim, double lo, double hi, double* out,
+                        cudaStream_t s) {
+  const dim3 grid = blocks_for(g.size);
+#define CALL(N) k_band<N><<<grid, kThreads, 0, s>>>(g, dim, lo, hi, out)
+  HJB_DISPATCH_ND(g.nd, CALL)
+#undef CALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_field_op(long long n, const double* a, const double* b, double* out,
+                            int is_max, cudaStream_t s) {
+  const int blocks = (int)((n + kThreads - 1) / kThreads < 148 * 16 ? (n + kThreads - 1) / kThreads
+                                                                     : 148 * 16);
+  if (n <= 0) return cudaSuccess;
+  k_field_op<<<blocks, kThreads, 0, s>>>(n, a, b, out, is_max);
+  return cudaGetLastError();
+}
+
+}  // namespace hjb

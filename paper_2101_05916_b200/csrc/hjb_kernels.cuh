@@ -1,0 +1,58 @@
+// hjb_kernels.cuh — launch interface of the sm_100a kernels (hjb_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "hjb_device.cuh"
+
+namespace hjb {
+
+enum Scheme { kGodunov = 0, kLfPerNode = 1, kLfGlobal = 2 };
+
+// Arguments of one VI sweep (solver.cpp:106-190 over the whole grid).
+struct StepArgs {
+  DevGrid g;
+  DevModel m;
+  const double* c;   // constraint
+  double* buf0;      // loop mode: front/back double buffer, parity = st->iter
+  double* buf1;
+  const double* src; // single-step mode
+  double* dst;
+  LoopState* st;
+  double dt;
+  double galpha[kMaxDims];
+  int scheme;
+  int loop;          // 1: read parity/done from st and run the epilogue
+  cudaGraphConditionalHandle handle;
+  int use_handle;
+};
+
+// K1: alpha scan (solver.cpp:221-268).  out[0] = max_nodes sum_d alpha_d/dx_d,
+// out[1+d] = max_nodes alpha_d.  out must be zeroed by the caller.
+cudaError_t launch_scan(const DevGrid& g, const DevModel& m, double* out, cudaStream_t s);
+
+// K2/K3: one Euler sweep with the VI clamp and the max|dV| reduction.
+cudaError_t launch_step(const StepArgs& a, cudaStream_t s);
+
+// Loop state initialisation (records the start timestamp on the device).
+cudaError_t launch_loop_init(LoopState* st, long long max_iters, double dt, double tol,
+                             double horizon, long long history_cap, double* history,
+                             double* wall_history, cudaStream_t s);
+
+// K4: multilinear resample (grid.cpp:84-135,215-231); optional seed clamp
+// out = max(resampled - *slack, c) when c != nullptr (solver.cpp:404-411).
+cudaError_t launch_resample(const DevGrid& src_g, const double* src, const DevGrid& dst_g,
+                            double* dst, const double* slack, const double* c,
+                            cudaStream_t s);
+
+// max_adjacent_jump (grid.cpp:197-213) into *out (zeroed by the caller).
+cudaError_t launch_max_adjacent_jump(const DevGrid& g, const double* f, double* out,
+                                     cudaStream_t s);
+
+// K5: signed_distance_band / field_max / field_min (levelset.cpp:54-95).
+cudaError_t launch_band(const DevGrid& g, int dim, double lo, double hi, double* out,
+                        cudaStream_t s);
+cudaError_t launch_field_op(long long n, const double* a, const double* b, double* out,
+                            int is_max, cudaStream_t s);
+
+}  // namespace hjb

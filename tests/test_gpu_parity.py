@@ -1,0 +1,128 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bitwise (IEEE ==) values, identical iteration counts and residual histories,
+on the same seeded inputs (BASELINE.json north_star: |dV| <= 1e-9, identical
+signs, identical iteration count — bitwise equality implies all three).
+"""
+import numpy as np
+import pytest
+
+from paper_2101_05916_b200 import configs
+from paper_2101_05916_b200 import hjsafe as hj
+
+from cases import (band_np, per_node_case, quad_setup, same, solve_cases, with_iters,
+                   workload_case)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case,iters", solve_cases(), ids=lambda x: getattr(x, "name", str(x)))
+def test_solve_matches_oracle(gpu_ctx, oracle, case, iters):
+    case = with_iters(case, iters)
+    init, c = case.init_field(), case.c_field()
+    want = oracle.solve(init, c, case.model, case.db, case.cfg)
+    got = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
+    assert got.dt == want.dt
+    assert got.iterations == want.iterations
+    assert got.converged == want.converged
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+def test_config1_converges_like_reference(gpu_ctx):
+    case = workload_case(configs.config1())
+    r = hj.solve(case.init_field(), case.c_field(), case.model, case.db, case.cfg, ctx=gpu_ctx)
+    assert r.converged and r.iterations == 146
+    assert int(np.sum(r.value.values() <= 0)) == 4544
+
+
+@pytest.mark.parametrize("n,iters", [(21, 200), (51, 10)])
+def test_config2_k_iterations(gpu_ctx, oracle, n, iters):
+    case = with_iters(workload_case(configs.config2(n)), iters)
+    init, c = case.init_field(), case.c_field()
+    want = oracle.solve(init, c, case.model, case.db, case.cfg)
+    got = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations == iters
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+@pytest.mark.parametrize("scheme,diss", [(hj.GODUNOV, hj.PER_NODE), (hj.LAX_FRIEDRICHS, hj.PER_NODE),
+                                         (hj.LAX_FRIEDRICHS, hj.GLOBAL)])
+def test_vi_step_matches_oracle(gpu_ctx, oracle, scheme, diss):
+    for case in (quad_setup(31), per_node_case(17), workload_case(configs.config2(9))):
+        case.cfg.scheme = scheme
+        case.cfg.dissipation = diss
+        rng = np.random.default_rng(5)
+        v = hj.ScalarField(case.grid, case.c + 0.3 * rng.random(case.grid.size()))
+        dt = oracle.cfl_dt(case.grid, case.model, case.db, 0.8)
+        assert hj.cfl_dt(case.grid, case.model, case.db, 0.8, ctx=gpu_ctx) == dt
+        want = oracle.vi_step(v, case.c_field(), case.model, case.db, dt, case.cfg)
+        got = hj.vi_step(v, case.c_field(), case.model, case.db, dt, case.cfg, ctx=gpu_ctx)
+        assert same(got.values(), want), case.name
+
+
+def test_errors_match_reference(gpu_ctx):
+    m = hj.ConstantAdvection([0.0])
+    g = hj.Grid([(0.0, 1.0, 11)])
+    db = hj.IntervalField.constant(g, [])
+    with pytest.raises(hj.SolverRuntimeError):
+        hj.cfl_dt(g, m, db, 0.8, ctx=gpu_ctx)
+    m = hj.ConstantAdvection([1.0])
+    dt = hj.cfl_dt(g, m, db, 0.8, ctx=gpu_ctx)
+    v = hj.ScalarField(g, g.coords(0))
+    c = hj.ScalarField(g, fill=-100.0)
+    with pytest.raises(hj.InvalidArgument):
+        hj.vi_step(v, c, m, db, 10 * dt, ctx=gpu_ctx)
+    with pytest.raises(hj.InvalidArgument):
+        hj.solve(v, c, m, db, hj.SolveConfig(cfl_factor=1.5), ctx=gpu_ctx)
+    with pytest.raises(hj.InvalidArgument):
+        hj.solve(v, c, m, db, hj.SolveConfig(tolerance=0.0), ctx=gpu_ctx)
+    q = quad_setup(11)
+    with pytest.raises(hj.InvalidArgument):  # rank mismatch
+        hj.solve(v, c, q.model, hj.IntervalField.constant(g, [hj.Interval(-1, 1)]), ctx=gpu_ctx)
+
+
+def test_resample_seed_jump_match_oracle(gpu_ctx, oracle):
+    rng = np.random.default_rng(11)
+    src_g, dst_g = configs.planar_grid(7), configs.planar_grid(13)
+    f = hj.ScalarField(src_g, rng.standard_normal(src_g.size()))
+    assert same(hj.resample(f, dst_g, ctx=gpu_ctx).values(), oracle.resample(f, dst_g))
+    assert hj.max_adjacent_jump(f, ctx=gpu_ctx) == oracle.max_adjacent_jump(f)
+    c = hj.ScalarField(dst_g, band_np(dst_g, 0, -4.0, 4.0))
+    assert same(hj.seed_from(f, dst_g, c, ctx=gpu_ctx).values(), oracle.seed_from(f, dst_g, c))
+    g = configs.planar_grid(9)
+    assert same(hj.signed_distance_band(g, 0, -4.0, 4.0, ctx=gpu_ctx).values(),
+                oracle.signed_distance_band(g, 0, -4.0, 4.0))
+
+
+def test_coarse_to_fine_matches_oracle(gpu_ctx, oracle):
+    case = quad_setup(41)
+    coarse = hj.Grid([(0.0, 3.2, 21), (-5.0, 5.0, 21)])
+    want = oracle.solve_coarse_to_fine(case.c_field(), case.model, case.db, coarse, case.cfg)
+    got = hj.solve_coarse_to_fine(case.c_field(), case.model, case.db, coarse, case.cfg, ctx=gpu_ctx)
+    for x, y in ((got.coarse, want.coarse), (got.fine, want.fine)):
+        assert x.iterations == y.iterations
+        assert same(x.value.values(), y.value.values())
+    warm = got.fine.value
+    case2 = quad_setup(41, dbar=0.4)
+    want = oracle.solve_coarse_to_fine(case2.c_field(), case2.model, case2.db, coarse, case2.cfg, warm)
+    got = hj.solve_coarse_to_fine(case2.c_field(), case2.model, case2.db, coarse, case2.cfg, warm,
+                                  ctx=gpu_ctx)
+    assert got.fine.iterations == want.fine.iterations
+    assert same(got.fine.value.values(), want.fine.value.values())
+
+
+def test_determinism_and_invariants_101(gpu_ctx):
+    """Size-independent properties at the config-3 size (101^4): two runs are
+    bitwise identical, V >= c exactly, cold evolution is non-decreasing."""
+    w = configs.config3(101, max_iters=3)
+    case = workload_case(w)
+    init, c = case.init_field(), case.c_field()
+    r1 = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
+    r2 = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
+    assert same(r1.value.values(), r2.value.values())
+    assert same(r1.residual_history, r2.residual_history)
+    v = r1.value.values()
+    assert np.all(v >= case.c)
+    assert np.all(v >= init.values() - 1e-12)
