@@ -14,11 +14,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
 #include "../../include/hjb.h"
 #include "hjb_common.cuh"
+#include "hjb_fast4d.cuh"
 #include "hjb_ho.cuh"
 #include "hjb_kernels.cuh"
 
@@ -324,9 +326,12 @@ int scheme_of(const hjb_solve_config* cfg) {
   return cfg->dissipation == HJB_GLOBAL ? kLfGlobal : kLfPerNode;
 }
 
-// Loop driver: WHILE-conditional CUDA graph, or (HJB_LOOP=poll) chunks of
-// sweeps with a host poll of the device `done` flag.
-int run_loop(hjb_context* ctx, const StepArgs& proto, int body) {
+// Loop driver: WHILE-conditional CUDA graph whose body is `body` sweeps, or
+// (HJB_LOOP=poll) chunks of sweeps with a host poll of the device `done`
+// flag.  `launch(stream, handle, use_handle)` enqueues one sweep in loop mode.
+using SweepLauncher = std::function<cudaError_t(cudaStream_t, cudaGraphConditionalHandle, int)>;
+
+int run_loop(hjb_context* ctx, const SweepLauncher& launch, int body) {
   const char* mode = std::getenv("HJB_LOOP");
   const bool poll = mode && std::strcmp(mode, "poll") == 0;
   if (!poll) {
@@ -347,15 +352,11 @@ int run_loop(hjb_context* ctx, const StepArgs& proto, int body) {
       e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
       if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("conditional node: ") + cudaGetErrorString(e)); break; }
       cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
-      StepArgs a = proto;
-      a.loop = 1;
-      a.handle = handle;
-      a.use_handle = 1;
       e = cudaStreamBeginCaptureToGraph(ctx->stream, bodyg, nullptr, nullptr, 0,
                                         cudaStreamCaptureModeThreadLocal);
       if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e)); break; }
       cudaError_t le = cudaSuccess;
-      for (int i = 0; i < body && le == cudaSuccess; ++i) le = launch_step(a, ctx->stream);
+      for (int i = 0; i < body && le == cudaSuccess; ++i) le = launch(ctx->stream, handle, 1);
       cudaGraph_t captured = nullptr;
       e = cudaStreamEndCapture(ctx->stream, &captured);
       if (le != cudaSuccess || e != cudaSuccess) {
@@ -374,17 +375,26 @@ int run_loop(hjb_context* ctx, const StepArgs& proto, int body) {
     cudaGraphDestroy(graph);
     return rc;
   }
-  StepArgs a = proto;
-  a.loop = 1;
-  a.use_handle = 0;
+  cudaGraphConditionalHandle none = 0;
   for (;;) {
-    for (int i = 0; i < body; ++i) CUDA_TRY(launch_step(a, ctx->stream));
+    for (int i = 0; i < body; ++i) CUDA_TRY(launch(ctx->stream, none, 0));
     CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
                              ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (ctx->st_host->done) break;
   }
   return HJB_OK;
+}
+
+int sm_count(int device) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms > 0 ? sms : 148;
+}
+
+bool fast_enabled() {
+  const char* e = std::getenv("HJB_FAST");
+  return !(e && std::strcmp(e, "0") == 0);
 }
 
 }  // namespace
@@ -428,9 +438,6 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   if (cfg->spatial_order > 1 || cfg->time_order > 1)
     return ho_solve(ctx, g, hm.dm, init, c, cfg, dt, s.max_alpha, value_out, res);
 
-  CUDA_TRY(ctx->v0.ensure(bytes));
-  CUDA_TRY(ctx->v1.ensure(bytes));
-  CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   if (cfg->max_iters == 0) {
     if (value_out != init)
       CUDA_TRY(cudaMemcpyAsync(value_out, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -441,20 +448,65 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
       std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
   CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
   CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
+  CUDA_TRY(ctx->v0.ensure(bytes));
+  CUDA_TRY(ctx->v1.ensure(bytes));
+  CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
                             cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
                             ctx->hist.d(), ctx->whist.d(), ctx->stream));
   ++ctx->launches;
+  const int shape = fast_enabled() ? fast4d_shape(g, hm.dm, scheme_of(cfg)) : -1;
   StepArgs a = base_args(g, hm.dm, c, dt, scheme_of(cfg), s);
   a.st = ctx->st;
   a.buf0 = ctx->v0.d();
   a.buf1 = ctx->v1.d();
+  Fast4dArgs f;
+  std::memset(&f, 0, sizeof f);
+  uint64_t rows = 0;
+  if (shape >= 0) {
+    // padded internal layout (even contiguous extent) for the 4D fast path
+    fast4d_config(g, sm_count(ctx->device), f);
+    rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
+    const size_t pbytes = rows * f.n3p * sizeof(double);
+    CUDA_TRY(ctx->v2.ensure(pbytes));
+    CUDA_TRY(ctx->v3.ensure(pbytes));
+    CUDA_TRY(ctx->pcbuf.ensure(pbytes));
+    CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
+    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
+    ctx->launches += 2;
+    f.tab = hm.dm.tab;
+    for (int d = 0; d < 4; ++d) {
+      f.off_pos[d] = hm.dm.row[d].off_pos;
+      f.off_neg[d] = hm.dm.row[d].off_neg;
+      f.off_a[d] = hm.dm.row[d].off_a;
+      f.off_b[d] = hm.dm.row[d].off_b;
+    }
+    f.c = ctx->pcbuf.d();
+    f.buf0 = ctx->v2.d();
+    f.buf1 = ctx->v3.d();
+    f.st = ctx->st;
+    f.dt = dt;
+    f.loop = 1;
+  }
+  SweepLauncher launch = [&](cudaStream_t st, cudaGraphConditionalHandle h, int use) {
+    if (shape >= 0) {
+      Fast4dArgs x = f;
+      x.handle = h;
+      x.use_handle = use;
+      return launch_fast4d(x, shape, st);
+    }
+    StepArgs x = a;
+    x.loop = 1;
+    x.handle = h;
+    x.use_handle = use;
+    return launch_step(x, st);
+  };
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   CUDA_TRY(cudaEventRecord(e0, ctx->stream));
   const int body = 8;
-  rc = run_loop(ctx, a, body);
+  rc = run_loop(ctx, launch, body);
   if (rc) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -481,8 +533,14 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   if (nh > 0 && res->wall_ms_history)
     CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
-  const double* final_buf = (st.iter & 1) ? ctx->v1.d() : ctx->v0.d();
-  CUDA_TRY(cudaMemcpyAsync(value_out, final_buf, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (shape >= 0) {
+    const double* final_buf = (st.iter & 1) ? ctx->v3.d() : ctx->v2.d();
+    CUDA_TRY(launch_unpad4(final_buf, value_out, rows, g.n[3], f.n3p, ctx->stream));
+    ++ctx->launches;
+  } else {
+    const double* final_buf = (st.iter & 1) ? ctx->v1.d() : ctx->v0.d();
+    CUDA_TRY(cudaMemcpyAsync(value_out, final_buf, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (st.status == HJB_ERR_DIVERGED)
     return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");

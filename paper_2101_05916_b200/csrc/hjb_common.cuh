@@ -54,7 +54,7 @@ struct hjb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
-  hjb::DevBuf v0, v1, v2, v3, cbuf, dbbuf, tables, scratch, hist, whist, xbuf;
+  hjb::DevBuf v0, v1, v2, v3, cbuf, pcbuf, dbbuf, tables, scratch, hist, whist, xbuf;
   hjb::LoopState* st = nullptr;
   hjb::LoopState* st_host = nullptr;  // pinned mirror
   long long launches = 0;

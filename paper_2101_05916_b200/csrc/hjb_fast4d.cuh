@@ -1,0 +1,41 @@
+// hjb_fast4d.cuh — launch interface of the specialised 4D sweep (hjb_fast4d.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hjb_device.cuh"
+
+namespace hjb {
+
+struct Fast4dArgs {
+  uint32_t n[4];
+  uint32_t n3p;  // padded contiguous extent (even)
+  double inv[4];
+  uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads;
+  const double* tab;
+  int off_pos[4], off_neg[4], off_a[4], off_b[4];
+  const double* c;  // padded constraint
+  double* buf0;
+  double* buf1;
+  const double* src;
+  double* dst;
+  LoopState* st;
+  double dt;
+  int loop;
+  cudaGraphConditionalHandle handle;
+  int use_handle;
+};
+
+// Model shape id for the fast path, or -1 when the generic kernel must run
+// (rank != 4, LF scheme, per-node bounds, rows depending on x0, ...).
+int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
+void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
+cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
+cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,
+                        cudaStream_t s);
+cudaError_t launch_unpad4(const double* in, double* out, uint64_t rows, uint32_t n3,
+                          uint32_t n3p, cudaStream_t s);
+
+}  // namespace hjb

@@ -244,9 +244,9 @@ __global__ void __launch_bounds__(kThreads) k_step(const __grid_constant__ StepA
     dst = a.dst;
   }
   const DevGrid& g = a.g;
-  const uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x;
   double local = 0.0;
-  if (lin < g.size) {
+  for (uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x; lin < g.size;
+       lin += gridDim.x * blockDim.x) {
     uint32_t idx[ND];
     unravel<ND>(g, lin, idx);
     const double v = src[lin];
@@ -449,9 +449,24 @@ __global__ void k_field_op(long long n, const double* __restrict__ a,
 
 inline dim3 blocks_for(uint32_t n) { return dim3((n + kThreads - 1) / kThreads); }
 
+// Persistent-style grid: a few CTAs per SM stride over the nodes, so the
+// per-sweep epilogue sees ~10^3 CTA arrivals instead of one per 256 nodes.
+inline dim3 step_blocks(uint32_t n) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint32_t want = (n + kThreads - 1) / kThreads;
+  const uint32_t cap = static_cast<uint32_t>(sms) * 8u;
+  return dim3(want < cap ? want : cap);
+}
+
 template <int ND>
 cudaError_t step_nd(const StepArgs& a, cudaStream_t s) {
-  const dim3 grid = blocks_for(a.g.size);
+  const dim3 grid = step_blocks(a.g.size);
   const bool pn = a.m.per_node != 0;
   switch (a.scheme) {
     case kGodunov:
