@@ -484,6 +484,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     f.c = ctx->pcbuf.d();
     f.buf0 = ctx->v2.d();
     f.buf1 = ctx->v3.d();
+    CUDA_TRY(fast4d_make_maps(f, f.buf0, f.buf1, f.c));
     f.st = ctx->st;
     f.dt = dt;
     f.loop = 1;

@@ -21,9 +21,12 @@
 //    the selection logic (solver.cpp:52-63) is restated with sign-bit tests
 //    (every case where a sign test could differ from the reference's `> 0`
 //    involves an exact zero operand, where both candidate results are +-0).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+
+#include <cudaTypedefs.h>
 
 #include "hjb_fast4d.cuh"
 
@@ -96,127 +99,261 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
   return a > b ? a : b;
 }
 
+// ---- mbarrier / bulk-copy primitives (PTX ISA 8.x, sm_90+; TMA engine) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 4D TMA tile load (tensor map in kernel-parameter space), OOB -> zeros
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int c0, int c1,
+                                          int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+
+// One CTA = a T1 x T2 tile of (i1, i2) rows (full contiguous rows of n3p),
+// marching i0 over [c0, c1).  One elected thread streams each V plane
+// (tile + 1-row halo in i1 and i2, out-of-range rows zero-filled by the TMA
+// unit) and each c plane (tile) into shared-memory rings with a single 4D
+// tensor copy each; full/empty mbarriers pipeline the planes, so no
+// block-wide barrier is needed inside the march.  Every thread owns one
+// 2-cell pencil.
 template <class S>
-__global__ void __launch_bounds__(512, 1) k_fast4d(const __grid_constant__ Fast4dArgs a) {
+__global__ void __launch_bounds__(448, 2) k_fast4d(const __grid_constant__ Fast4dArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const double* src;
   double* dst;
+  const CUtensorMap* vmap;
   if (a.loop) {
     if (*(volatile int*)&a.st->done) return;
     const long long it = a.st->iter;
     src = (it & 1) ? a.buf1 : a.buf0;
     dst = (it & 1) ? a.buf0 : a.buf1;
+    vmap = (it & 1) ? &a.map1 : &a.map0;
   } else {
     src = a.src;
     dst = a.dst;
+    vmap = &a.map0;
   }
+  (void)src;
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3];
   const uint32_t n3p = a.n3p;
   const uint32_t J = n3p >> 1;
+  const uint32_t T1 = a.T1, T2 = a.T2;
+  const uint32_t W2 = T2 + 2;
+  const uint32_t RC = T1 * T2;        // c rows per slot
+  constexpr uint32_t SV = 4;          // V ring
+  constexpr uint32_t SC = 2;          // c ring
+  double* vring = reinterpret_cast<double*>(smem_raw);
+  double* cring = reinterpret_cast<double*>(smem_raw + SV * a.vslot_bytes);
+  uint64_t* full_v = reinterpret_cast<uint64_t*>(smem_raw + SV * a.vslot_bytes + SC * a.cslot_bytes);
+  uint64_t* empty_v = full_v + SV;
+  uint64_t* full_c = empty_v + SV;
+  uint64_t* empty_c = full_c + SC;
+  const uint32_t vslot = a.vslot_bytes / 8, cslot = a.cslot_bytes / 8;  // in doubles
 
-  // block -> (tile_i1, tile_i2, i0 chunk)
   uint32_t b = blockIdx.x;
   const uint32_t chunk = b % a.nchunks;
   b /= a.nchunks;
   const uint32_t t2 = b % a.tiles2;
   const uint32_t t1 = b / a.tiles2;
+  const uint32_t base1 = t1 * T1, base2 = t2 * T2;
+  const uint32_t c0 = chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, n0);
+  const uint64_t s2 = n3p;
+  const uint64_t s1 = static_cast<uint64_t>(n2) * n3p;
+  const uint64_t s0 = static_cast<uint64_t>(n1) * s1;
+  const uint32_t nwarps = blockDim.x >> 5;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = threadIdx.x == 0;
+
+  if (producer) {
+    for (uint32_t k = 0; k < SV; ++k) {
+      mbar_init(full_v + k, 1);
+      mbar_init(empty_v + k, nwarps);
+    }
+    for (uint32_t k = 0; k < SC; ++k) {
+      mbar_init(full_c + k, 1);
+      mbar_init(empty_c + k, nwarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer state (thread 0 only): per-slot parity bits of the empty barriers
+  uint32_t pv = 0, pc = 0;
+  const uint32_t last_v = (c1 < n0) ? c1 : n0 - 1;  // last V plane this chunk reads
+  auto issue_v = [&](uint32_t p) {
+    const uint32_t sl = p % SV;
+    mbar_wait(empty_v + sl, ((pv >> sl) & 1u) ^ 1u);
+    pv ^= 1u << sl;
+    mbar_arrive_expect_tx(full_v + sl, a.vbox_bytes);
+    tma_load4(vring + sl * vslot, vmap, 0, (int)base2 - 1, (int)base1 - 1, (int)p, full_v + sl);
+  };
+  auto issue_c = [&](uint32_t p) {
+    const uint32_t sl = p % SC;
+    mbar_wait(empty_c + sl, ((pc >> sl) & 1u) ^ 1u);
+    pc ^= 1u << sl;
+    mbar_arrive_expect_tx(full_c + sl, a.cbox_bytes);
+    tma_load4(cring + sl * cslot, &a.mapc, 0, (int)base2, (int)base1, (int)p, full_c + sl);
+  };
+
+  const uint32_t pfirst = c0 > 0 ? c0 - 1 : 0;
+  if (producer) {
+    for (uint32_t p = pfirst; p <= c0 + 1 && p <= last_v; ++p) issue_v(p);
+    issue_c(c0);
+  }
+  uint32_t fv = 0, fc = 0;  // consumer parity bits of the full barriers
+
   const uint32_t t = threadIdx.x;
   const uint32_t r = t / J;
   const uint32_t j = t - r * J;
-  const uint32_t r1 = r / a.T2;
-  const uint32_t r2 = r - r1 * a.T2;
-  const uint32_t i1 = t1 * a.T1 + r1;
-  const uint32_t i2 = t2 * a.T2 + r2;
-  const bool active = r < a.T1 * a.T2 && i1 < n1 && i2 < n2;
-  unsigned long long mbits = 0ull;
+  const uint32_t r1 = r / T2;
+  const uint32_t r2 = r - r1 * T2;
+  const uint32_t i1 = base1 + r1;
+  const uint32_t i2 = base2 + r2;
+  const bool active = r < RC && i1 < n1 && i2 < n2;
+  const uint32_t i3 = 2 * j;
+  const bool has1 = i3 + 1 < n3;
+  const bool has_r = i3 + 2 < n3;
+  const bool has_l = i3 > 0;
+  const bool m1 = i1 > 0, p1 = i1 + 1 < n1;
+  const bool m2 = i2 > 0, p2 = i2 + 1 < n2;
+  const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
+  const uint32_t own = ((r1 + 1) * W2 + (r2 + 1)) * n3p + i3;  // pencil offset in a V slot
+  const uint32_t cown = r * n3p + i3;                          // pencil offset in a c slot
+  double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3;
 
-  if (active) {
-    const uint32_t i3 = 2 * j;
-    const bool has1 = i3 + 1 < n3;          // second pencil cell is real
-    const bool has_r = i3 + 2 < n3;         // right neighbour exists
-    const bool has_l = i3 > 0;
-    const bool m1 = i1 > 0, p1 = i1 + 1 < n1;
-    const bool m2 = i2 > 0, p2 = i2 + 1 < n2;
-    const uint64_t s2 = n3p;
-    const uint64_t s1 = static_cast<uint64_t>(n2) * n3p;
-    const uint64_t s0 = static_cast<uint64_t>(n1) * s1;
-    const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
-
-    // loop-invariant Godunov slopes (rows never depend on x0 in this path)
-    double pos[4][2], neg[4][2];
+  double pos[4][2], neg[4][2];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
+  for (int d = 0; d < 4; ++d) {
+    // rows that do not depend on x3 hold one slope pair for the whole pencil
+    constexpr int dummy = 0;
+    (void)dummy;
+    const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const uint32_t ka = pick<S>(S::A(d), i1, i2, i3 + c);
-        if (S::B(d) < 0) {
-          pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
-          neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
-        } else {
-          const uint32_t kb = pick<S>(S::B(d), i1, i2, i3 + c);
-          const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
-          pos[d][c] = dr;
-          neg[d][c] = dr;
-        }
+    for (int c = 0; c < 2; ++c) {
+      if (c == 1 && !per_cell) {
+        pos[d][1] = pos[d][0];
+        neg[d][1] = neg[d][0];
+        continue;
+      }
+      const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+      if (S::B(d) < 0) {
+        pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+        neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+      } else {
+        const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+        const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+        pos[d][c] = dr;
+        neg[d][c] = dr;
       }
     }
+  }
 
-    const uint32_t c0 = chunk * a.L;
-    const uint32_t c1 = min(c0 + a.L, n0);
-    const uint64_t rowoff = (static_cast<uint64_t>(i1) * n2 + i2) * n3p + i3;
-    const double* vp = src + rowoff;  // pencil at plane 0
-    double* op = dst + rowoff;
-    const double* cp = a.c + rowoff;
+  auto wait_v = [&](uint32_t p) {
+    const uint32_t sl = p % SV;
+    mbar_wait(full_v + sl, (fv >> sl) & 1u);
+    fv ^= 1u << sl;
+  };
+  auto release_v = [&](uint32_t p) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_v + (p % SV));
+  };
 
-    double2 vprev = make_double2(0.0, 0.0);
-    double2 vcur = ldg2(vp + c0 * s0);
-    double2 vnext = make_double2(0.0, 0.0);
-    double2 vnn = make_double2(0.0, 0.0);
-    if (c0 > 0) vprev = ldg2(vp + (c0 - 1) * s0);
-    if (c0 + 1 < n0) vnext = ldg2(vp + (c0 + 1) * s0);
-    double2 ccur = ldg2_stream(cp + c0 * s0);
-    // axis-0 D- of the first step
-    double dm0a = 0.0, dm0b = 0.0;
-    if (c0 > 0) {
-      dm0a = (vcur.x - vprev.x) * inv0;
-      dm0b = (vcur.y - vprev.y) * inv0;
+  // prologue planes c0-1, c0
+  for (uint32_t p = pfirst; p <= c0; ++p) wait_v(p);
+  double2 vprev = make_double2(0.0, 0.0), vcur = make_double2(0.0, 0.0);
+  if (active) {
+    if (c0 > 0) vprev = lds2(vring + ((c0 - 1) % SV) * vslot + own);
+    vcur = lds2(vring + (c0 % SV) * vslot + own);
+  }
+  if (c0 > 0) release_v(c0 - 1);
+  double dm0a = 0.0, dm0b = 0.0;
+  if (c0 > 0) {
+    dm0a = (vcur.x - vprev.x) * inv0;
+    dm0b = (vcur.y - vprev.y) * inv0;
+  }
+  unsigned long long mbits = 0ull;
+
+  for (uint32_t i0 = c0; i0 < c1; ++i0) {
+    if (producer) {
+      if (i0 + 2 <= last_v) issue_v(i0 + 2);
+      if (i0 + 1 < c1) issue_c(i0 + 1);
     }
-    for (uint32_t i0 = c0; i0 < c1; ++i0) {
-      const uint64_t pl = static_cast<uint64_t>(i0) * s0;
-      // prefetch V[i0+2] and c[i0+1]
-      if (i0 + 2 < n0) vnn = ldg2(vp + pl + 2 * s0);
-      double2 cnext = make_double2(0.0, 0.0);
-      if (i0 + 1 < c1) cnext = ldg2_stream(cp + pl + s0);
-      // in-plane neighbours at plane i0
-      const double* q = vp + pl;
-      double2 a1m = m1 ? ldg2(q - s1) : vcur;
-      double2 a1p = p1 ? ldg2(q + s1) : vcur;
-      double2 a2m = m2 ? ldg2(q - s2) : vcur;
-      double2 a2p = p2 ? ldg2(q + s2) : vcur;
-      const double vl = has_l ? __ldg(q - 1) : 0.0;
-      const double vr = has_r ? __ldg(q + 2) : 0.0;
+    if (i0 + 1 < n0) wait_v(i0 + 1);
+    {
+      const uint32_t sl = i0 % SC;
+      mbar_wait(full_c + sl, (fc >> sl) & 1u);
+      fc ^= 1u << sl;
+    }
+    if (active) {
+      const double* cur = vring + (i0 % SV) * vslot + own;
+      double2 vnext = vcur;
+      if (i0 + 1 < n0) vnext = lds2(vring + ((i0 + 1) % SV) * vslot + own);
+      const double2 cc = lds2(cring + (i0 % SC) * cslot + cown);
+      const double2 a1m = lds2(cur - W2 * n3p);
+      const double2 a1p = lds2(cur + W2 * n3p);
+      const double2 a2m = lds2(cur - n3p);
+      const double2 a2p = lds2(cur + n3p);
+      const double vl = has_l ? cur[-1] : 0.0;
+      const double vr = has_r ? cur[2] : 0.0;
 
-      // axis 0: D+ (shared with the next step's D-)
       double dp0a = 0.0, dp0b = 0.0;
       if (i0 + 1 < n0) {
         dp0a = (vnext.x - vcur.x) * inv0;
         dp0b = (vnext.y - vcur.y) * inv0;
       }
-      // axis 1
       const double dm1a = m1 ? (vcur.x - a1m.x) * inv1 : 0.0;
       const double dm1b = m1 ? (vcur.y - a1m.y) * inv1 : 0.0;
       const double dp1a = p1 ? (a1p.x - vcur.x) * inv1 : 0.0;
       const double dp1b = p1 ? (a1p.y - vcur.y) * inv1 : 0.0;
-      // axis 2
       const double dm2a = m2 ? (vcur.x - a2m.x) * inv2 : 0.0;
       const double dm2b = m2 ? (vcur.y - a2m.y) * inv2 : 0.0;
       const double dp2a = p2 ? (a2p.x - vcur.x) * inv2 : 0.0;
       const double dp2b = p2 ? (a2p.y - vcur.y) * inv2 : 0.0;
-      // axis 3: faces (l|x), (x|y), (y|r)
       const double f3m = has_l ? (vcur.x - vl) * inv3 : 0.0;
       const double f3c = has1 ? (vcur.y - vcur.x) * inv3 : 0.0;
       const double f3p = has_r ? (vr - vcur.y) * inv3 : 0.0;
 
-      // Hhat = sum_d flux_d, in d order (hhat starts at 0.0: 0.0 + h0 == h0 in value)
       double ha_ = flux(pos[0][0], neg[0][0], dm0a, dp0a);
       ha_ += flux(pos[1][0], neg[1][0], dm1a, dp1a);
       ha_ += flux(pos[2][0], neg[2][0], dm2a, dp2a);
@@ -229,9 +366,9 @@ __global__ void __launch_bounds__(512, 1) k_fast4d(const __grid_constant__ Fast4
       const double sa = vcur.x + a.dt * ha_;
       const double sb = vcur.y + a.dt * hb_;
       double2 o;
-      o.x = sa > ccur.x ? sa : ccur.x;
-      o.y = sb > ccur.y ? sb : ccur.y;
-      *reinterpret_cast<double2*>(op + pl) = o;
+      o.x = sa > cc.x ? sa : cc.x;
+      o.y = sb > cc.y ? sb : cc.y;
+      *reinterpret_cast<double2*>(op + static_cast<uint64_t>(i0) * s0) = o;
       const double dva = fabs(o.x - vcur.x);
       const double dvb = fabs(o.y - vcur.y);
       // NaN never wins (reference: `if (dv > max_dv)`); its bit pattern would
@@ -243,26 +380,26 @@ __global__ void __launch_bounds__(512, 1) k_fast4d(const __grid_constant__ Fast4
       if (!has1) bb = 0ull;
       mbits = umax64(mbits, umax64(ba, bb));
 
-      // rotate the queue
       dm0a = dp0a;
       dm0b = dp0b;
       vprev = vcur;
       vcur = vnext;
-      vnext = vnn;
-      ccur = cnext;
     }
-    (void)vprev;
+    // plane i0 (V) and c plane i0 are no longer read by this warp
+    release_v(i0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_c + (i0 % SC));
   }
+  (void)vprev;
 
   // CTA max -> global, last CTA runs the sweep epilogue (solver.cpp:347-369)
   __shared__ unsigned long long part[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane == 0) part[warp] = mbits;
   __syncthreads();
   if (warp != 0) return;
-  mbits = lane < (int)(blockDim.x >> 5) ? part[lane] : 0ull;
+  mbits = lane < (blockDim.x >> 5) ? part[lane] : 0ull;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
@@ -337,7 +474,7 @@ __global__ void k_unpad4(const double* __restrict__ in, double* __restrict__ out
 
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   if (g.nd != 4 || scheme != 0 || m.per_node) return -1;
-  if ((g.n[3] + 1) / 2 > 512) return -1;
+  if (g.n[3] + (g.n[3] & 1u) > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   for (int d = 0; d < 4; ++d) {
     const DevRow& r = m.row[d];
@@ -364,6 +501,14 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   return -1;
 }
 
+static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 128 * 128); }
+
+static size_t fast4d_smem(uint32_t T1, uint32_t T2, uint32_t n3p) {
+  const size_t rv = (T1 + 2) * (T2 + 2), rc = T1 * T2;
+  return 4 * (size_t)round128(rv * n3p * sizeof(double)) +
+         2 * (size_t)round128(rc * n3p * sizeof(double)) + 12 * sizeof(uint64_t);
+}
+
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   for (int d = 0; d < 4; ++d) {
     a.n[d] = g.n[d];
@@ -371,20 +516,30 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   }
   a.n3p = g.n[3] + (g.n[3] & 1u);
   const uint32_t J = a.n3p / 2;
-  // rows per CTA so that a CTA has ~256-512 threads
-  uint32_t R = 512 / J;
+  // rows per CTA: <= 448 threads, shared-memory rings small enough for 2 CTAs/SM
+  uint32_t R = 448 / J;
   if (R < 1) R = 1;
-  uint32_t T2 = 1;
-  while (T2 * T2 < R) ++T2;
-  if (T2 > g.n[2]) T2 = g.n[2];
-  uint32_t T1 = R / T2;
-  if (T1 < 1) T1 = 1;
-  if (T1 > g.n[1]) T1 = g.n[1];
+  uint32_t T1 = 1, T2 = 1;
+  for (;;) {
+    T2 = 1;
+    while (T2 * T2 < R) ++T2;
+    if (T2 > g.n[2]) T2 = g.n[2];
+    T1 = R / T2;
+    if (T1 < 1) T1 = 1;
+    if (T1 > g.n[1]) T1 = g.n[1];
+    if (fast4d_smem(T1, T2, a.n3p) <= 110 * 1024 || R == 1) break;
+    --R;
+  }
   a.T1 = T1;
   a.T2 = T2;
   a.tiles1 = (g.n[1] + T1 - 1) / T1;
   a.tiles2 = (g.n[2] + T2 - 1) / T2;
   a.threads = ((T1 * T2 * J + 31) / 32) * 32;
+  a.smem = static_cast<uint32_t>(fast4d_smem(T1, T2, a.n3p));
+  a.vbox_bytes = (T1 + 2) * (T2 + 2) * a.n3p * 8u;
+  a.cbox_bytes = T1 * T2 * a.n3p * 8u;
+  a.vslot_bytes = round128(a.vbox_bytes);
+  a.cslot_bytes = round128(a.cbox_bytes);
   const uint32_t tiles = a.tiles1 * a.tiles2;
   const uint32_t want = static_cast<uint32_t>(sms) * 4;  // ~2 CTAs/SM x 2 waves
   uint32_t nch = (want + tiles - 1) / tiles;
@@ -397,11 +552,46 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
 }
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_fast4d<ShapePlanar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(k_fast4d<ShapeTwin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr_set = true;
+  }
   if (shape == 0)
-    k_fast4d<ShapePlanar><<<a.blocks, a.threads, 0, s>>>(a);
+    k_fast4d<ShapePlanar><<<a.blocks, a.threads, a.smem, s>>>(a);
   else
-    k_fast4d<ShapeTwin><<<a.blocks, a.threads, 0, s>>>(a);
+    k_fast4d<ShapeTwin><<<a.blocks, a.threads, a.smem, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const double* c) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[4] = {a.n3p, a.n[2], a.n[1], a.n[0]};
+  const cuuint64_t strides[3] = {(cuuint64_t)a.n3p * 8, (cuuint64_t)a.n3p * a.n[2] * 8,
+                                 (cuuint64_t)a.n3p * a.n[2] * a.n[1] * 8};
+  const cuuint32_t vbox[4] = {a.n3p, a.T2 + 2, a.T1 + 2, 1};
+  const cuuint32_t cbox[4] = {a.n3p, a.T2, a.T1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMap* maps[3] = {&a.map0, &a.map1, &a.mapc};
+  const void* ptrs[3] = {buf0, buf1, c};
+  for (int k = 0; k < 3; ++k) {
+    CUresult r = encode(maps[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(ptrs[k]),
+                        dims, strides, k < 2 ? vbox : cbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,

@@ -1,6 +1,7 @@
 // hjb_fast4d.cuh — launch interface of the specialised 4D sweep (hjb_fast4d.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -10,10 +11,14 @@
 namespace hjb {
 
 struct Fast4dArgs {
+  CUtensorMap map0;  // V buffer 0 (padded), box = tile + halo rows
+  CUtensorMap map1;  // V buffer 1
+  CUtensorMap mapc;  // constraint (padded), box = tile rows
+  uint32_t vslot_bytes, cslot_bytes, vbox_bytes, cbox_bytes;
   uint32_t n[4];
   uint32_t n3p;  // padded contiguous extent (even)
   double inv[4];
-  uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads;
+  uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads, smem;
   const double* tab;
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
   const double* c;  // padded constraint
@@ -33,6 +38,9 @@ struct Fast4dArgs {
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
+// Encode the three TMA tensor maps for the padded buffers (driver entry point
+// fetched through the runtime; no libcuda link dependency).
+cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const double* c);
 cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,
                         cudaStream_t s);
 cudaError_t launch_unpad4(const double* in, double* out, uint64_t rows, uint32_t n3,
