@@ -68,13 +68,23 @@ __device__ __forceinline__ double flux(double pos, double neg, double dm, double
   return h;
 }
 
-struct ShapePlanar {  // NearHoverPlanar4D rows: x1 | tan(x2) | x2 + x3 | x2
+// Row structure of the model, fixed at compile time: axis of the slope
+// table (A), optional second drift axis (B, pos == neg then), and whether
+// the row is always linear (pos == neg everywhere: no inputs on the row).
+struct ShapePlanarD0 {  // BASELINE planar 4D, wind on row 0: rows x1 | tan x2 | x2 + x3 | x2
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : 2; }
   __host__ __device__ static constexpr int B(int d) { return d == 2 ? 3 : -1; }
+  __host__ __device__ static constexpr bool LIN(int d) { return d == 1 || d == 2; }
+};
+struct ShapePlanarD1 {  // stock NearHoverPlanar4D, wind on row 1
+  __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : 2; }
+  __host__ __device__ static constexpr int B(int d) { return d == 2 ? 3 : -1; }
+  __host__ __device__ static constexpr bool LIN(int d) { return d == 0 || d == 2; }
 };
 struct ShapeTwin {  // TwinDoubleIntegrator rows: x1 | const | x3 | const
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr int B(int) { return -1; }
+  __host__ __device__ static constexpr bool LIN(int d) { return d == 0 || d == 2; }
 };
 
 template <class S>
@@ -86,78 +96,96 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-__device__ __forceinline__ double2 ldg2_stream(const double* p) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
                                                      unsigned long long b) {
   return a > b ? a : b;
 }
 
-// ---- mbarrier / bulk-copy primitives (PTX ISA 8.x, sm_90+; TMA engine) ----
+// Loop-invariant classification of a one-kink Hamiltonian row
+// (H(p) = pos*p for p > 0, neg*p otherwise):
+//   LIN  pos == neg         flux = s * (s >= 0 ? dp : dm)
+//   INC  pos, neg >= 0      H non-decreasing: flux = H(dp) (== reference hb)
+//   DEC  pos, neg <= 0      H non-increasing: flux = H(dm) (== reference ha)
+//   GEN  otherwise          full Godunov selection (flux() above)
+// In every case the value equals the reference's godunov_flux
+// (solver.cpp:52-63): for monotone H the reference's max/min selects hb
+// (INC) or ha (DEC), or an equal value, and its zero clamps cannot fire.
+enum : int { kLin = 0, kInc = 1, kDec = 2, kGen = 3 };
+
+__device__ __forceinline__ int classify(double pos, double neg) {
+  if (pos == neg) return kLin;
+  if (sign_clear(pos) && sign_clear(neg)) return kInc;
+  if (!sign_clear(pos) && !sign_clear(neg)) return kDec;
+  return kGen;
+}
+
+__device__ __forceinline__ double flux_mode(int mode, double pos, double neg, double dm,
+                                            double dp) {
+  if (mode == kInc) return (sign_clear(dp) ? pos : neg) * dp;
+  if (mode == kDec) return (sign_clear(dm) ? pos : neg) * dm;
+  return flux(pos, neg, dm, dp);  // kLin never reaches here; kGen
+}
+
+__device__ __forceinline__ double flux_lin(double s, bool s_nonneg, double dm, double dp) {
+  return s * (s_nonneg ? dp : dm);
+}
+
+// ---- mbarrier / bulk-tensor primitives (PTX ISA 8.x; TMA engine) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 // 4D TMA tile load (tensor map in kernel-parameter space), OOB -> zeros
-__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int c0, int c1,
-                                          int c2, int c3, uint64_t* bar) {
+__device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                          int c2, int c3, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-      "r"(smem_u32(bar))
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
-
-__device__ __forceinline__ double2 lds2(const double* p) {
-  return *reinterpret_cast<const double2*>(p);
+__device__ __forceinline__ double2 lds2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double lds1(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
 }
 
+constexpr int kRing = 4;  // planes in flight per ring (prefetch distance kRing - 1)
+
 // One CTA = a T1 x T2 tile of (i1, i2) rows (full contiguous rows of n3p),
-// marching i0 over [c0, c1).  One elected thread streams each V plane
-// (tile + 1-row halo in i1 and i2, out-of-range rows zero-filled by the TMA
-// unit) and each c plane (tile) into shared-memory rings with a single 4D
-// tensor copy each; full/empty mbarriers pipeline the planes, so no
-// block-wide barrier is needed inside the march.  Every thread owns one
-// 2-cell pencil.
+// marching i0 over [c0, c1).  A dedicated producer warp streams each V plane
+// (tile + 1-row halo in i1 and i2; out-of-range rows are zero-filled by the
+// TMA unit and never read) and each c plane (tile) into shared-memory rings
+// with one 4D tensor copy each; full/empty mbarriers pipeline the planes.
+// Consumer threads own one 2-cell pencil each.  The march is unrolled by the
+// ring depth so ring slots and barrier parities are compile-time constants.
 template <class S>
-__global__ void __launch_bounds__(448, 2) k_fast4d(const __grid_constant__ Fast4dArgs a) {
+__global__ void __launch_bounds__(640, 1) k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const double* src;
   double* dst;
@@ -173,22 +201,17 @@ __global__ void __launch_bounds__(448, 2) k_fast4d(const __grid_constant__ Fast4
     dst = a.dst;
     vmap = &a.map0;
   }
-  (void)src;
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3];
   const uint32_t n3p = a.n3p;
   const uint32_t J = n3p >> 1;
   const uint32_t T1 = a.T1, T2 = a.T2;
   const uint32_t W2 = T2 + 2;
-  const uint32_t RC = T1 * T2;        // c rows per slot
-  constexpr uint32_t SV = 4;          // V ring
-  constexpr uint32_t SC = 2;          // c ring
-  double* vring = reinterpret_cast<double*>(smem_raw);
-  double* cring = reinterpret_cast<double*>(smem_raw + SV * a.vslot_bytes);
-  uint64_t* full_v = reinterpret_cast<uint64_t*>(smem_raw + SV * a.vslot_bytes + SC * a.cslot_bytes);
-  uint64_t* empty_v = full_v + SV;
-  uint64_t* full_c = empty_v + SV;
-  uint64_t* empty_c = full_c + SC;
-  const uint32_t vslot = a.vslot_bytes / 8, cslot = a.cslot_bytes / 8;  // in doubles
+  const uint32_t smem0 = smem_u32(smem_raw);
+  const uint32_t vring = smem0;
+  const uint32_t cring = smem0 + kRing * a.vslot_bytes;
+  const uint32_t bars = cring + kRing * a.cslot_bytes;  // full_v[4] empty_v[4] full_c[4] empty_c[4]
+  uint64_t* bar_ptr = reinterpret_cast<uint64_t*>(smem_raw + kRing * a.vslot_bytes +
+                                                  kRing * a.cslot_bytes);
 
   uint32_t b = blockIdx.x;
   const uint32_t chunk = b % a.nchunks;
@@ -201,196 +224,208 @@ __global__ void __launch_bounds__(448, 2) k_fast4d(const __grid_constant__ Fast4
   const uint64_t s2 = n3p;
   const uint64_t s1 = static_cast<uint64_t>(n2) * n3p;
   const uint64_t s0 = static_cast<uint64_t>(n1) * s1;
-  const uint32_t nwarps = blockDim.x >> 5;
+  const uint32_t ncons = a.consumers;  // consumer threads (multiple of 32)
+  const uint32_t nwarps_c = ncons >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool producer = threadIdx.x == 0;
 
-  if (producer) {
-    for (uint32_t k = 0; k < SV; ++k) {
-      mbar_init(full_v + k, 1);
-      mbar_init(empty_v + k, nwarps);
-    }
-    for (uint32_t k = 0; k < SC; ++k) {
-      mbar_init(full_c + k, 1);
-      mbar_init(empty_c + k, nwarps);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kRing; ++k) {
+      mbar_init(bar_ptr + k, 1);
+      mbar_init(bar_ptr + kRing + k, nwarps_c);
+      mbar_init(bar_ptr + 2 * kRing + k, 1);
+      mbar_init(bar_ptr + 3 * kRing + k, nwarps_c);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
-  // producer state (thread 0 only): per-slot parity bits of the empty barriers
-  uint32_t pv = 0, pc = 0;
   const uint32_t last_v = (c1 < n0) ? c1 : n0 - 1;  // last V plane this chunk reads
-  auto issue_v = [&](uint32_t p) {
-    const uint32_t sl = p % SV;
-    mbar_wait(empty_v + sl, ((pv >> sl) & 1u) ^ 1u);
-    pv ^= 1u << sl;
-    mbar_arrive_expect_tx(full_v + sl, a.vbox_bytes);
-    tma_load4(vring + sl * vslot, vmap, 0, (int)base2 - 1, (int)base1 - 1, (int)p, full_v + sl);
-  };
-  auto issue_c = [&](uint32_t p) {
-    const uint32_t sl = p % SC;
-    mbar_wait(empty_c + sl, ((pc >> sl) & 1u) ^ 1u);
-    pc ^= 1u << sl;
-    mbar_arrive_expect_tx(full_c + sl, a.cbox_bytes);
-    tma_load4(cring + sl * cslot, &a.mapc, 0, (int)base2, (int)base1, (int)p, full_c + sl);
-  };
-
-  const uint32_t pfirst = c0 > 0 ? c0 - 1 : 0;
-  if (producer) {
-    for (uint32_t p = pfirst; p <= c0 + 1 && p <= last_v; ++p) issue_v(p);
-    issue_c(c0);
-  }
-  uint32_t fv = 0, fc = 0;  // consumer parity bits of the full barriers
-
-  const uint32_t t = threadIdx.x;
-  const uint32_t r = t / J;
-  const uint32_t j = t - r * J;
-  const uint32_t r1 = r / T2;
-  const uint32_t r2 = r - r1 * T2;
-  const uint32_t i1 = base1 + r1;
-  const uint32_t i2 = base2 + r2;
-  const bool active = r < RC && i1 < n1 && i2 < n2;
-  const uint32_t i3 = 2 * j;
-  const bool has1 = i3 + 1 < n3;
-  const bool has_r = i3 + 2 < n3;
-  const bool has_l = i3 > 0;
-  const bool m1 = i1 > 0, p1 = i1 + 1 < n1;
-  const bool m2 = i2 > 0, p2 = i2 + 1 < n2;
-  const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
-  const uint32_t own = ((r1 + 1) * W2 + (r2 + 1)) * n3p + i3;  // pencil offset in a V slot
-  const uint32_t cown = r * n3p + i3;                          // pencil offset in a c slot
-  double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3;
-
-  double pos[4][2], neg[4][2];
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    // rows that do not depend on x3 hold one slope pair for the whole pencil
-    constexpr int dummy = 0;
-    (void)dummy;
-    const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      if (c == 1 && !per_cell) {
-        pos[d][1] = pos[d][0];
-        neg[d][1] = neg[d][0];
-        continue;
-      }
-      const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-      if (S::B(d) < 0) {
-        pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
-        neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
-      } else {
-        const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-        const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
-        pos[d][c] = dr;
-        neg[d][c] = dr;
-      }
-    }
-  }
-
-  auto wait_v = [&](uint32_t p) {
-    const uint32_t sl = p % SV;
-    mbar_wait(full_v + sl, (fv >> sl) & 1u);
-    fv ^= 1u << sl;
-  };
-  auto release_v = [&](uint32_t p) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_v + (p % SV));
-  };
-
-  // prologue planes c0-1, c0
-  for (uint32_t p = pfirst; p <= c0; ++p) wait_v(p);
-  double2 vprev = make_double2(0.0, 0.0), vcur = make_double2(0.0, 0.0);
-  if (active) {
-    if (c0 > 0) vprev = lds2(vring + ((c0 - 1) % SV) * vslot + own);
-    vcur = lds2(vring + (c0 % SV) * vslot + own);
-  }
-  if (c0 > 0) release_v(c0 - 1);
-  double dm0a = 0.0, dm0b = 0.0;
-  if (c0 > 0) {
-    dm0a = (vcur.x - vprev.x) * inv0;
-    dm0b = (vcur.y - vprev.y) * inv0;
-  }
   unsigned long long mbits = 0ull;
 
-  for (uint32_t i0 = c0; i0 < c1; ++i0) {
-    if (producer) {
-      if (i0 + 2 <= last_v) issue_v(i0 + 2);
-      if (i0 + 1 < c1) issue_c(i0 + 1);
-    }
-    if (i0 + 1 < n0) wait_v(i0 + 1);
-    {
-      const uint32_t sl = i0 % SC;
-      mbar_wait(full_c + sl, (fc >> sl) & 1u);
-      fc ^= 1u << sl;
-    }
-    if (active) {
-      const double* cur = vring + (i0 % SV) * vslot + own;
-      double2 vnext = vcur;
-      if (i0 + 1 < n0) vnext = lds2(vring + ((i0 + 1) % SV) * vslot + own);
-      const double2 cc = lds2(cring + (i0 % SC) * cslot + cown);
-      const double2 a1m = lds2(cur - W2 * n3p);
-      const double2 a1p = lds2(cur + W2 * n3p);
-      const double2 a2m = lds2(cur - n3p);
-      const double2 a2p = lds2(cur + n3p);
-      const double vl = has_l ? cur[-1] : 0.0;
-      const double vr = has_r ? cur[2] : 0.0;
-
-      double dp0a = 0.0, dp0b = 0.0;
-      if (i0 + 1 < n0) {
-        dp0a = (vnext.x - vcur.x) * inv0;
-        dp0b = (vnext.y - vcur.y) * inv0;
+  if (threadIdx.x >= ncons) {
+    // ---------------- producer warp ----------------
+    if (lane == 0) {
+      for (uint32_t q = 0;; ++q) {
+        const uint32_t pv = c0 + q, pc = c0 + q;
+        const bool dv = pv <= last_v, dc = pc < c1;
+        if (!dv && !dc) break;
+        const uint32_t sl = q % kRing, use = q / kRing;
+        if (dv) {
+          mbar_wait(bars + (kRing + sl) * 8, (use & 1u) ^ 1u);
+          mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes);
+          tma_load4(vring + sl * a.vslot_bytes, vmap, 0, (int)base2 - 1, (int)base1 - 1, (int)pv,
+                    bars + sl * 8);
+        }
+        if (dc) {
+          mbar_wait(bars + (3 * kRing + sl) * 8, (use & 1u) ^ 1u);
+          mbar_arrive_expect_tx(bars + (2 * kRing + sl) * 8, a.cbox_bytes);
+          tma_load4(cring + sl * a.cslot_bytes, &a.mapc, 0, (int)base2, (int)base1, (int)pc,
+                    bars + (2 * kRing + sl) * 8);
+        }
       }
-      const double dm1a = m1 ? (vcur.x - a1m.x) * inv1 : 0.0;
-      const double dm1b = m1 ? (vcur.y - a1m.y) * inv1 : 0.0;
-      const double dp1a = p1 ? (a1p.x - vcur.x) * inv1 : 0.0;
-      const double dp1b = p1 ? (a1p.y - vcur.y) * inv1 : 0.0;
-      const double dm2a = m2 ? (vcur.x - a2m.x) * inv2 : 0.0;
-      const double dm2b = m2 ? (vcur.y - a2m.y) * inv2 : 0.0;
-      const double dp2a = p2 ? (a2p.x - vcur.x) * inv2 : 0.0;
-      const double dp2b = p2 ? (a2p.y - vcur.y) * inv2 : 0.0;
-      const double f3m = has_l ? (vcur.x - vl) * inv3 : 0.0;
-      const double f3c = has1 ? (vcur.y - vcur.x) * inv3 : 0.0;
-      const double f3p = has_r ? (vr - vcur.y) * inv3 : 0.0;
-
-      double ha_ = flux(pos[0][0], neg[0][0], dm0a, dp0a);
-      ha_ += flux(pos[1][0], neg[1][0], dm1a, dp1a);
-      ha_ += flux(pos[2][0], neg[2][0], dm2a, dp2a);
-      ha_ += flux(pos[3][0], neg[3][0], f3m, f3c);
-      double hb_ = flux(pos[0][1], neg[0][1], dm0b, dp0b);
-      hb_ += flux(pos[1][1], neg[1][1], dm1b, dp1b);
-      hb_ += flux(pos[2][1], neg[2][1], dm2b, dp2b);
-      hb_ += flux(pos[3][1], neg[3][1], f3c, f3p);
-
-      const double sa = vcur.x + a.dt * ha_;
-      const double sb = vcur.y + a.dt * hb_;
-      double2 o;
-      o.x = sa > cc.x ? sa : cc.x;
-      o.y = sb > cc.y ? sb : cc.y;
-      *reinterpret_cast<double2*>(op + static_cast<uint64_t>(i0) * s0) = o;
-      const double dva = fabs(o.x - vcur.x);
-      const double dvb = fabs(o.y - vcur.y);
-      // NaN never wins (reference: `if (dv > max_dv)`); its bit pattern would
-      // order above +inf, so it is filtered explicitly
-      const unsigned long long ba =
-          dva == dva ? (unsigned long long)__double_as_longlong(dva) : 0ull;
-      unsigned long long bb =
-          dvb == dvb ? (unsigned long long)__double_as_longlong(dvb) : 0ull;
-      if (!has1) bb = 0ull;
-      mbits = umax64(mbits, umax64(ba, bb));
-
-      dm0a = dp0a;
-      dm0b = dp0b;
-      vprev = vcur;
-      vcur = vnext;
     }
-    // plane i0 (V) and c plane i0 are no longer read by this warp
-    release_v(i0);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_c + (i0 % SC));
+  } else {
+    // ---------------- consumer warps ----------------
+    const uint32_t t = threadIdx.x;
+    const uint32_t r = t / J;
+    const uint32_t j = t - r * J;
+    const uint32_t r1 = r / T2;
+    const uint32_t r2 = r - r1 * T2;
+    const uint32_t i1 = base1 + r1;
+    const uint32_t i2 = base2 + r2;
+    const bool active = r < T1 * T2 && i1 < n1 && i2 < n2;
+    const uint32_t i3 = 2 * j;
+    const bool has1 = i3 + 1 < n3;
+    const bool has_r = i3 + 2 < n3;
+    const bool has_l = i3 > 0;
+    const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
+    // shared-memory byte offsets inside a V slot: own pencil and neighbours;
+    // a missing neighbour (grid edge) is aliased to the pencil itself so its
+    // difference is exactly (x - x) * inv = +0, the reference's ghost value
+    const uint32_t rowb = n3p * 8u;
+    const uint32_t own = (((r1 + 1) * W2 + (r2 + 1)) * n3p + i3) * 8u;
+    const uint32_t o1m = (i1 > 0) ? own - W2 * rowb : own;
+    const uint32_t o1p = (i1 + 1 < n1) ? own + W2 * rowb : own;
+    const uint32_t o2m = (i2 > 0) ? own - rowb : own;
+    const uint32_t o2p = (i2 + 1 < n2) ? own + rowb : own;
+    const uint32_t ol = has_l ? own - 8u : own;       // left of cell a (self if none)
+    const uint32_t orr = has_r ? own + 16u : own + 8u;  // right of cell b (self if none)
+    const uint32_t cown = (r * n3p + i3) * 8u;
+
+    // loop-invariant slopes and their classification
+    double pos[4][2], neg[4][2];
+    int mode[4][2];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c == 1 && !per_cell) {
+          pos[d][1] = pos[d][0];
+          neg[d][1] = neg[d][0];
+          mode[d][1] = mode[d][0];
+          continue;
+        }
+        const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+        if (S::B(d) < 0) {
+          pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+          neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+        } else {
+          const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+          const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+          pos[d][c] = dr;
+          neg[d][c] = dr;
+        }
+        mode[d][c] = classify(pos[d][c], neg[d][c]);
+      }
+    }
+    bool snn[4][2];  // sign of the linear slope (LIN rows)
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) snn[d][c] = sign_clear(pos[d][c]);
+
+    double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
+                 static_cast<uint64_t>(c0) * s0;
+    // prologue: own pencil of plane c0-1 straight from global (once per chunk)
+    double2 vprev = make_double2(0.0, 0.0);
+    if (active && c0 > 0)
+      vprev = ldg2(src + static_cast<uint64_t>(c0 - 1) * s0 + static_cast<uint64_t>(i1) * s1 +
+                   static_cast<uint64_t>(i2) * s2 + i3);
+    mbar_wait(bars + 0, 0u);  // plane c0 in slot 0, first use
+    double2 vcur = make_double2(0.0, 0.0);
+    if (active) vcur = lds2(vring + own);
+    if (c0 == 0) vprev = vcur;  // D- at the i0 = 0 edge: (x - x) * inv = +0
+    double dm0a = (vcur.x - vprev.x) * inv0;
+    double dm0b = (vcur.y - vprev.y) * inv0;
+
+    for (uint32_t rb = c0; rb < c1; rb += kRing) {
+      const uint32_t round = (rb - c0) / kRing;
+#pragma unroll
+      for (int k = 0; k < kRing; ++k) {
+        const uint32_t i0 = rb + k;
+        if (i0 >= c1) break;
+        const uint32_t slot_cur = vring + k * a.vslot_bytes;
+        const int kn = (k + 1) % kRing;
+        const uint32_t use_n = (k + 1 == kRing) ? round + 1 : round;
+        double2 vnext = vcur;
+        if (i0 + 1 < n0) {
+          mbar_wait(bars + kn * 8, use_n & 1u);
+          if (active) vnext = lds2(vring + kn * a.vslot_bytes + own);
+        }
+        mbar_wait(bars + (2 * kRing + k) * 8, round & 1u);
+        if (active) {
+          const double2 cc = lds2(cring + k * a.cslot_bytes + cown);
+          const double2 a1m = lds2(slot_cur + o1m);
+          const double2 a1p = lds2(slot_cur + o1p);
+          const double2 a2m = lds2(slot_cur + o2m);
+          const double2 a2p = lds2(slot_cur + o2p);
+          const double vl = lds1(slot_cur + ol);
+          const double vr = lds1(slot_cur + orr);
+          const double vy = has1 ? vcur.y : vcur.x;  // pad cell: zero face
+
+          const double dp0a = (vnext.x - vcur.x) * inv0;
+          const double dp0b = (vnext.y - vcur.y) * inv0;
+          const double dm1a = (vcur.x - a1m.x) * inv1;
+          const double dm1b = (vcur.y - a1m.y) * inv1;
+          const double dp1a = (a1p.x - vcur.x) * inv1;
+          const double dp1b = (a1p.y - vcur.y) * inv1;
+          const double dm2a = (vcur.x - a2m.x) * inv2;
+          const double dm2b = (vcur.y - a2m.y) * inv2;
+          const double dp2a = (a2p.x - vcur.x) * inv2;
+          const double dp2b = (a2p.y - vcur.y) * inv2;
+          const double f3m = (vcur.x - vl) * inv3;
+          const double f3c = (vy - vcur.x) * inv3;
+          const double f3p = (vr - vcur.y) * inv3;
+
+          const double dmv[4][2] = {{dm0a, dm0b}, {dm1a, dm1b}, {dm2a, dm2b}, {f3m, f3c}};
+          const double dpv[4][2] = {{dp0a, dp0b}, {dp1a, dp1b}, {dp2a, dp2b}, {f3c, f3p}};
+          double hh[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            double h = 0.0;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+              double f;
+              if (S::LIN(d)) {
+                f = flux_lin(pos[d][c], snn[d][c], dmv[d][c], dpv[d][c]);
+              } else if (mode[d][c] == kLin) {
+                f = flux_lin(pos[d][c], snn[d][c], dmv[d][c], dpv[d][c]);
+              } else {
+                f = flux_mode(mode[d][c], pos[d][c], neg[d][c], dmv[d][c], dpv[d][c]);
+              }
+              h = d == 0 ? f : h + f;  // reference: hhat = 0.0; hhat += f (0.0 + f == f)
+            }
+            hh[c] = h;
+          }
+          const double sa = vcur.x + a.dt * hh[0];
+          const double sb = vcur.y + a.dt * hh[1];
+          double2 o;
+          o.x = sa > cc.x ? sa : cc.x;
+          o.y = sb > cc.y ? sb : cc.y;
+          *reinterpret_cast<double2*>(op) = o;
+          const double dva = fabs(o.x - vcur.x);
+          const double dvb = fabs(o.y - vcur.y);
+          // NaN never wins (reference: `if (dv > max_dv)`); its bit pattern
+          // would order above +inf, so it is filtered explicitly
+          const unsigned long long ba =
+              dva == dva ? (unsigned long long)__double_as_longlong(dva) : 0ull;
+          unsigned long long bb =
+              (dvb == dvb && has1) ? (unsigned long long)__double_as_longlong(dvb) : 0ull;
+          mbits = umax64(mbits, umax64(ba, bb));
+          dm0a = dp0a;
+          dm0b = dp0b;
+        }
+        op += s0;
+        vcur = vnext;
+        // plane i0 (V) and c plane i0 are no longer read by this warp
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bars + (kRing + k) * 8);
+          mbar_arrive(bars + (3 * kRing + k) * 8);
+        }
+      }
+    }
   }
-  (void)vprev;
 
   // CTA max -> global, last CTA runs the sweep epilogue (solver.cpp:347-369)
   __shared__ unsigned long long part[32];
@@ -475,7 +510,9 @@ __global__ void k_unpad4(const double* __restrict__ in, double* __restrict__ out
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   if (g.nd != 4 || scheme != 0 || m.per_node) return -1;
   if (g.n[3] + (g.n[3] & 1u) > 256) return -1;  // TMA box extent limit
+  if ((g.n[3] + 1) / 2 > 608) return -1;
   int A[4], B[4];
+  bool lin[4];
   for (int d = 0; d < 4; ++d) {
     const DevRow& r = m.row[d];
     if (r.folded) {
@@ -488,16 +525,20 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
       return -1;
     }
     if (A[d] == 0 || B[d] == 0) return -1;
+    lin[d] = r.n_uadd == 0 && r.n_dterm == 0;
   }
-  auto match = [&](const int* a, const int* b) {
+  auto match = [&](const int* a, const int* b, const bool* l) {
     for (int d = 0; d < 4; ++d)
-      if (a[d] != A[d] || b[d] != B[d]) return false;
+      if (a[d] != A[d] || b[d] != B[d] || (l[d] && !lin[d])) return false;
     return true;
   };
   static const int pa[4] = {1, 2, 2, 2}, pb[4] = {-1, -1, 3, -1};
+  static const bool l0[4] = {false, true, true, false}, l1[4] = {true, false, true, false};
   static const int ta[4] = {1, -1, 3, -1}, tb[4] = {-1, -1, -1, -1};
-  if (match(pa, pb)) return 0;
-  if (match(ta, tb)) return 1;
+  static const bool lt[4] = {true, false, true, false};
+  if (match(pa, pb, l0)) return 0;
+  if (match(pa, pb, l1)) return 1;
+  if (match(ta, tb, lt)) return 2;
   return -1;
 }
 
@@ -505,8 +546,8 @@ static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 12
 
 static size_t fast4d_smem(uint32_t T1, uint32_t T2, uint32_t n3p) {
   const size_t rv = (T1 + 2) * (T2 + 2), rc = T1 * T2;
-  return 4 * (size_t)round128(rv * n3p * sizeof(double)) +
-         2 * (size_t)round128(rc * n3p * sizeof(double)) + 12 * sizeof(uint64_t);
+  return kRing * (size_t)round128(rv * n3p * sizeof(double)) +
+         kRing * (size_t)round128(rc * n3p * sizeof(double)) + 4 * kRing * sizeof(uint64_t);
 }
 
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
@@ -516,32 +557,35 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   }
   a.n3p = g.n[3] + (g.n[3] & 1u);
   const uint32_t J = a.n3p / 2;
-  // rows per CTA: <= 448 threads, shared-memory rings small enough for 2 CTAs/SM
-  uint32_t R = 448 / J;
-  if (R < 1) R = 1;
-  uint32_t T1 = 1, T2 = 1;
-  for (;;) {
-    T2 = 1;
-    while (T2 * T2 < R) ++T2;
-    if (T2 > g.n[2]) T2 = g.n[2];
-    T1 = R / T2;
-    if (T1 < 1) T1 = 1;
-    if (T1 > g.n[1]) T1 = g.n[1];
-    if (fast4d_smem(T1, T2, a.n3p) <= 110 * 1024 || R == 1) break;
-    --R;
+  // tile of (i1, i2) rows: <= 608 consumer threads (+1 producer warp), rings within one SM's
+  // shared memory, smallest halo/tile ratio
+  uint32_t bestT1 = 1, bestT2 = 1;
+  double best = 1e30;
+  for (uint32_t T1 = 1; T1 <= g.n[1] && T1 * J <= 608; ++T1) {
+    for (uint32_t T2 = 1; T2 <= g.n[2] && T1 * T2 * J <= 608; ++T2) {
+      if (fast4d_smem(T1, T2, a.n3p) > 200 * 1024) continue;
+      const double ratio = double((T1 + 2) * (T2 + 2)) / double(T1 * T2);
+      const double score = ratio - 1e-3 * T1 * T2;
+      if (score < best) {
+        best = score;
+        bestT1 = T1;
+        bestT2 = T2;
+      }
+    }
   }
-  a.T1 = T1;
-  a.T2 = T2;
-  a.tiles1 = (g.n[1] + T1 - 1) / T1;
-  a.tiles2 = (g.n[2] + T2 - 1) / T2;
-  a.threads = ((T1 * T2 * J + 31) / 32) * 32;
-  a.smem = static_cast<uint32_t>(fast4d_smem(T1, T2, a.n3p));
-  a.vbox_bytes = (T1 + 2) * (T2 + 2) * a.n3p * 8u;
-  a.cbox_bytes = T1 * T2 * a.n3p * 8u;
+  a.T1 = bestT1;
+  a.T2 = bestT2;
+  a.tiles1 = (g.n[1] + a.T1 - 1) / a.T1;
+  a.tiles2 = (g.n[2] + a.T2 - 1) / a.T2;
+  a.consumers = ((a.T1 * a.T2 * J + 31) / 32) * 32;
+  a.threads = a.consumers + 32;
+  a.smem = static_cast<uint32_t>(fast4d_smem(a.T1, a.T2, a.n3p));
+  a.vbox_bytes = (a.T1 + 2) * (a.T2 + 2) * a.n3p * 8u;
+  a.cbox_bytes = a.T1 * a.T2 * a.n3p * 8u;
   a.vslot_bytes = round128(a.vbox_bytes);
   a.cslot_bytes = round128(a.cbox_bytes);
   const uint32_t tiles = a.tiles1 * a.tiles2;
-  const uint32_t want = static_cast<uint32_t>(sms) * 4;  // ~2 CTAs/SM x 2 waves
+  const uint32_t want = static_cast<uint32_t>(sms) * 3;  // 1 CTA/SM, ~3 waves
   uint32_t nch = (want + tiles - 1) / tiles;
   if (nch < 1) nch = 1;
   uint32_t L = (g.n[0] + nch - 1) / nch;
@@ -554,14 +598,18 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_fast4d<ShapePlanar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fast4d<ShapePlanarD0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(k_fast4d<ShapePlanarD1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     cudaFuncSetAttribute(k_fast4d<ShapeTwin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_set = true;
   }
   if (shape == 0)
-    k_fast4d<ShapePlanar><<<a.blocks, a.threads, a.smem, s>>>(a);
+    k_fast4d<ShapePlanarD0><<<a.blocks, a.threads, a.smem, s>>>(a);
+  else if (shape == 1)
+    k_fast4d<ShapePlanarD1><<<a.blocks, a.threads, a.smem, s>>>(a);
   else
     k_fast4d<ShapeTwin><<<a.blocks, a.threads, a.smem, s>>>(a);
   return cudaGetLastError();
