@@ -465,6 +465,8 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   uint64_t rows = 0;
   if (shape >= 0) {
     // padded internal layout (even contiguous extent) for the 4D fast path
+    const char* kc = std::getenv("HJB_KCELLS");
+    f.kcells = (kc && std::atoi(kc) == 4) ? 4u : 2u;
     fast4d_config(g, sm_count(ctx->device), f);
     rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
     const size_t pbytes = rows * f.n3p * sizeof(double);

@@ -177,15 +177,53 @@ __device__ __forceinline__ double lds1(uint32_t addr) {
 
 constexpr int kRing = 4;  // planes in flight per ring (prefetch distance kRing - 1)
 
+template <int K>
+__device__ __forceinline__ void lds_cells(uint32_t addr, double* v) {
+#pragma unroll
+  for (int c = 0; c < K; c += 2) {
+    const double2 x = lds2(addr + 8u * c);
+    v[c] = x.x;
+    v[c + 1] = x.y;
+  }
+}
+
+// reference kink_h (solver.cpp:44-46): s = p > 0 ? pos : neg; s * p.  The
+// sign-bit test differs from `p > 0` only for p == +0, where both products
+// are +-0 (see file header).
+__device__ __forceinline__ double kink(double pos, double neg, double p) {
+  return (sign_clear(p) ? pos : neg) * p;
+}
+
+// Godunov selection (solver.cpp:52-63) given the two kink products, branch
+// free.  pos_nn / neg_nn: sign_clear(pos), sign_clear(neg) (loop invariant).
+//  same-signed gradients  -> upwind end: hb if the active slope is >= 0
+//  dm <= 0 < dp (rarefaction) -> max(ha, hb), clamped below at 0
+//  dp <= 0 < dm (shock)       -> min(ha, hb), clamped above at 0
+__device__ __forceinline__ double godunov_select(double ha, double hb, double dm, double dp,
+                                                 bool pos_nn, bool neg_nn) {
+  const bool km = sign_clear(dm), kp = sign_clear(dp);
+  const bool gt = ha > hb;
+  const bool same = km == kp;
+  const bool s_nn = km ? pos_nn : neg_nn;
+  const bool pick_a = same ? !s_nn : (gt != km);
+  double h = pick_a ? ha : hb;
+  const bool zero = !same && (sign_clear(h) == km);
+  return zero ? 0.0 : h;
+}
+
 // One CTA = a T1 x T2 tile of (i1, i2) rows (full contiguous rows of n3p),
 // marching i0 over [c0, c1).  A dedicated producer warp streams each V plane
 // (tile + 1-row halo in i1 and i2; out-of-range rows are zero-filled by the
 // TMA unit and never read) and each c plane (tile) into shared-memory rings
 // with one 4D tensor copy each; full/empty mbarriers pipeline the planes.
-// Consumer threads own one 2-cell pencil each.  The march is unrolled by the
-// ring depth so ring slots and barrier parities are compile-time constants.
-template <class S>
-__global__ void __launch_bounds__(640, 1) k_fast4d(const __grid_constant__ Fast4dArgs a) {
+// Consumer threads own kK consecutive cells of one row.  The march is
+// unrolled by the ring depth so ring slots and barrier parities are
+// compile-time constants.  Kink products of faces shared by two cells are
+// formed once: along the march (carried to the next plane) and inside the
+// pencil when the row's slopes do not vary along the contiguous axis.
+template <class S, int kK>
+__global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
+    k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const double* src;
   double* dst;
@@ -203,7 +241,7 @@ __global__ void __launch_bounds__(640, 1) k_fast4d(const __grid_constant__ Fast4
   }
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3];
   const uint32_t n3p = a.n3p;
-  const uint32_t J = n3p >> 1;
+  const uint32_t J = n3p / kK;
   const uint32_t T1 = a.T1, T2 = a.T2;
   const uint32_t W2 = T2 + 2;
   const uint32_t smem0 = smem_u32(smem_raw);
@@ -266,16 +304,21 @@ __global__ void __launch_bounds__(640, 1) k_fast4d(const __grid_constant__ Fast4
   } else {
     // ---------------- consumer warps ----------------
     const uint32_t t = threadIdx.x;
-    const uint32_t r = t / J;
-    const uint32_t j = t - r * J;
+    const uint32_t rr = t / J;
+    const uint32_t j = t - rr * J;
+    const bool in_tile = rr < T1 * T2;  // threads rounding the CTA up to a warp multiple
+    const uint32_t r = in_tile ? rr : 0u;
     const uint32_t r1 = r / T2;
     const uint32_t r2 = r - r1 * T2;
     const uint32_t i1 = base1 + r1;
     const uint32_t i2 = base2 + r2;
-    const bool active = r < T1 * T2 && i1 < n1 && i2 < n2;
-    const uint32_t i3 = 2 * j;
-    const bool has1 = i3 + 1 < n3;
-    const bool has_r = i3 + 2 < n3;
+    const bool active = in_tile && i1 < n1 && i2 < n2;
+    const uint32_t i3 = kK * j;
+    // valid cells of the pencil (the padded tail of a row holds pad cells)
+    bool valid[kK];
+#pragma unroll
+    for (int c = 0; c < kK; ++c) valid[c] = active && (i3 + c < n3);
+    const bool has_r = i3 + kK < n3;
     const bool has_l = i3 > 0;
     const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
     // shared-memory byte offsets inside a V slot: own pencil and neighbours;
@@ -287,56 +330,65 @@ __global__ void __launch_bounds__(640, 1) k_fast4d(const __grid_constant__ Fast4
     const uint32_t o1p = (i1 + 1 < n1) ? own + W2 * rowb : own;
     const uint32_t o2m = (i2 > 0) ? own - rowb : own;
     const uint32_t o2p = (i2 + 1 < n2) ? own + rowb : own;
-    const uint32_t ol = has_l ? own - 8u : own;       // left of cell a (self if none)
-    const uint32_t orr = has_r ? own + 16u : own + 8u;  // right of cell b (self if none)
+    const uint32_t ol = has_l ? own - 8u : own;
+    const uint32_t orr = has_r ? own + 8u * kK : own + 8u * (kK - 1);
     const uint32_t cown = (r * n3p + i3) * 8u;
 
-    // loop-invariant slopes and their classification
-    double pos[4][2], neg[4][2];
-    int mode[4][2];
+    // loop-invariant slopes (row d, cell c); rows that do not vary along x3
+    // hold one pair for the whole pencil
+    double pos[4][kK], neg[4][kK];
+    bool pnn[4][kK], nnn[4][kK];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        if (c == 1 && !per_cell) {
-          pos[d][1] = pos[d][0];
-          neg[d][1] = neg[d][0];
-          mode[d][1] = mode[d][0];
-          continue;
-        }
-        const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-        if (S::B(d) < 0) {
-          pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
-          neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+      for (int c = 0; c < kK; ++c) {
+        if (c > 0 && !per_cell) {
+          pos[d][c] = pos[d][0];
+          neg[d][c] = neg[d][0];
         } else {
-          const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-          const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
-          pos[d][c] = dr;
-          neg[d][c] = dr;
+          const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+          if (S::B(d) < 0) {
+            pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+            neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+          } else {
+            const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+            const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+            pos[d][c] = dr;
+            neg[d][c] = dr;
+          }
         }
-        mode[d][c] = classify(pos[d][c], neg[d][c]);
+        pnn[d][c] = sign_clear(pos[d][c]);
+        nnn[d][c] = sign_clear(neg[d][c]);
       }
     }
-    bool snn[4][2];  // sign of the linear slope (LIN rows)
-#pragma unroll
-    for (int d = 0; d < 4; ++d)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) snn[d][c] = sign_clear(pos[d][c]);
 
     double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
                  static_cast<uint64_t>(c0) * s0;
     // prologue: own pencil of plane c0-1 straight from global (once per chunk)
-    double2 vprev = make_double2(0.0, 0.0);
-    if (active && c0 > 0)
-      vprev = ldg2(src + static_cast<uint64_t>(c0 - 1) * s0 + static_cast<uint64_t>(i1) * s1 +
-                   static_cast<uint64_t>(i2) * s2 + i3);
+    double v[kK], vp[kK];
     mbar_wait(bars + 0, 0u);  // plane c0 in slot 0, first use
-    double2 vcur = make_double2(0.0, 0.0);
-    if (active) vcur = lds2(vring + own);
-    if (c0 == 0) vprev = vcur;  // D- at the i0 = 0 edge: (x - x) * inv = +0
-    double dm0a = (vcur.x - vprev.x) * inv0;
-    double dm0b = (vcur.y - vprev.y) * inv0;
+    lds_cells<kK>(vring + own, v);
+    if (active && c0 > 0) {
+      const double* g = src + static_cast<uint64_t>(c0 - 1) * s0 + static_cast<uint64_t>(i1) * s1 +
+                        static_cast<uint64_t>(i2) * s2 + i3;
+#pragma unroll
+      for (int c = 0; c < kK; c += 2) {
+        const double2 x = ldg2(g + c);
+        vp[c] = x.x;
+        vp[c + 1] = x.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < kK; ++c) vp[c] = v[c];  // D- at the i0 = 0 edge: +0
+    }
+    // axis-0 carry: D- and its kink product of the first plane
+    double dm0[kK], ka0[kK];
+#pragma unroll
+    for (int c = 0; c < kK; ++c) {
+      dm0[c] = (v[c] - vp[c]) * inv0;
+      ka0[c] = kink(pos[0][c], neg[0][c], dm0[c]);
+    }
 
     for (uint32_t rb = c0; rb < c1; rb += kRing) {
       const uint32_t round = (rb - c0) / kRing;
@@ -347,76 +399,106 @@ __global__ void __launch_bounds__(640, 1) k_fast4d(const __grid_constant__ Fast4
         const uint32_t slot_cur = vring + k * a.vslot_bytes;
         const int kn = (k + 1) % kRing;
         const uint32_t use_n = (k + 1 == kRing) ? round + 1 : round;
-        double2 vnext = vcur;
+        double vn[kK];
         if (i0 + 1 < n0) {
           mbar_wait(bars + kn * 8, use_n & 1u);
-          if (active) vnext = lds2(vring + kn * a.vslot_bytes + own);
+          lds_cells<kK>(vring + kn * a.vslot_bytes + own, vn);
+        } else {
+#pragma unroll
+          for (int c = 0; c < kK; ++c) vn[c] = v[c];  // D+ at the i0 = n0-1 edge: +0
         }
         mbar_wait(bars + (2 * kRing + k) * 8, round & 1u);
-        if (active) {
-          const double2 cc = lds2(cring + k * a.cslot_bytes + cown);
-          const double2 a1m = lds2(slot_cur + o1m);
-          const double2 a1p = lds2(slot_cur + o1p);
-          const double2 a2m = lds2(slot_cur + o2m);
-          const double2 a2p = lds2(slot_cur + o2p);
-          const double vl = lds1(slot_cur + ol);
-          const double vr = lds1(slot_cur + orr);
-          const double vy = has1 ? vcur.y : vcur.x;  // pad cell: zero face
+        double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
+        lds_cells<kK>(cring + k * a.cslot_bytes + cown, cc);
+        lds_cells<kK>(slot_cur + o1m, n1m);
+        lds_cells<kK>(slot_cur + o1p, n1p);
+        lds_cells<kK>(slot_cur + o2m, n2m);
+        lds_cells<kK>(slot_cur + o2p, n2p);
+        const double vl = lds1(slot_cur + ol);
+        const double vr = lds1(slot_cur + orr);
 
-          const double dp0a = (vnext.x - vcur.x) * inv0;
-          const double dp0b = (vnext.y - vcur.y) * inv0;
-          const double dm1a = (vcur.x - a1m.x) * inv1;
-          const double dm1b = (vcur.y - a1m.y) * inv1;
-          const double dp1a = (a1p.x - vcur.x) * inv1;
-          const double dp1b = (a1p.y - vcur.y) * inv1;
-          const double dm2a = (vcur.x - a2m.x) * inv2;
-          const double dm2b = (vcur.y - a2m.y) * inv2;
-          const double dp2a = (a2p.x - vcur.x) * inv2;
-          const double dp2b = (a2p.y - vcur.y) * inv2;
-          const double f3m = (vcur.x - vl) * inv3;
-          const double f3c = (vy - vcur.x) * inv3;
-          const double f3p = (vr - vcur.y) * inv3;
-
-          const double dmv[4][2] = {{dm0a, dm0b}, {dm1a, dm1b}, {dm2a, dm2b}, {f3m, f3c}};
-          const double dpv[4][2] = {{dp0a, dp0b}, {dp1a, dp1b}, {dp2a, dp2b}, {f3c, f3p}};
-          double hh[2];
+        // axis-3 faces of the pencil: f3[c] is D- of cell c, f3[c+1] its D+;
+        // faces past the last real cell are the reference's zero ghost
+        double f3[kK + 1];
+        f3[0] = (v[0] - vl) * inv3;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            double h = 0.0;
+        for (int c = 1; c < kK; ++c) {
+          const double f = (v[c] - v[c - 1]) * inv3;
+          f3[c] = valid[c] ? f : 0.0;
+        }
+        f3[kK] = (vr - v[kK - 1]) * inv3;
+        constexpr bool row3_shared = !(S::A(3) == 3 || S::B(3) == 3);
+        double k3a[kK + 1], k3b[kK + 1];  // kink products of faces, as D+ (a) / D- (b) users
+        if (row3_shared && !S::LIN(3)) {
 #pragma unroll
-            for (int d = 0; d < 4; ++d) {
-              double f;
-              if (S::LIN(d)) {
-                f = flux_lin(pos[d][c], snn[d][c], dmv[d][c], dpv[d][c]);
-              } else if (mode[d][c] == kLin) {
-                f = flux_lin(pos[d][c], snn[d][c], dmv[d][c], dpv[d][c]);
-              } else {
-                f = flux_mode(mode[d][c], pos[d][c], neg[d][c], dmv[d][c], dpv[d][c]);
-              }
-              h = d == 0 ? f : h + f;  // reference: hhat = 0.0; hhat += f (0.0 + f == f)
-            }
-            hh[c] = h;
+          for (int c = 0; c <= kK; ++c) {
+            k3a[c] = kink(pos[3][0], neg[3][0], f3[c]);
+            k3b[c] = k3a[c];
           }
-          const double sa = vcur.x + a.dt * hh[0];
-          const double sb = vcur.y + a.dt * hh[1];
-          double2 o;
-          o.x = sa > cc.x ? sa : cc.x;
-          o.y = sb > cc.y ? sb : cc.y;
-          *reinterpret_cast<double2*>(op) = o;
-          const double dva = fabs(o.x - vcur.x);
-          const double dvb = fabs(o.y - vcur.y);
-          // NaN never wins (reference: `if (dv > max_dv)`); its bit pattern
-          // would order above +inf, so it is filtered explicitly
-          const unsigned long long ba =
-              dva == dva ? (unsigned long long)__double_as_longlong(dva) : 0ull;
-          unsigned long long bb =
-              (dvb == dvb && has1) ? (unsigned long long)__double_as_longlong(dvb) : 0ull;
-          mbits = umax64(mbits, umax64(ba, bb));
-          dm0a = dp0a;
-          dm0b = dp0b;
+        }
+        double out[kK];
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          // axis 0
+          const double dp0 = (vn[c] - v[c]) * inv0;
+          double h0;
+          const double kb0 = kink(pos[0][c], neg[0][c], dp0);
+          if (S::LIN(0)) {
+            h0 = pnn[0][c] ? kb0 : ka0[c];
+          } else {
+            h0 = godunov_select(ka0[c], kb0, dm0[c], dp0, pnn[0][c], nnn[0][c]);
+          }
+          dm0[c] = dp0;
+          ka0[c] = kb0;
+          // axis 1
+          const double dm1 = (v[c] - n1m[c]) * inv1;
+          const double dp1 = (n1p[c] - v[c]) * inv1;
+          double h1;
+          if (S::LIN(1)) {
+            h1 = pos[1][c] * (pnn[1][c] ? dp1 : dm1);
+          } else {
+            h1 = godunov_select(kink(pos[1][c], neg[1][c], dm1), kink(pos[1][c], neg[1][c], dp1),
+                                dm1, dp1, pnn[1][c], nnn[1][c]);
+          }
+          // axis 2
+          const double dm2 = (v[c] - n2m[c]) * inv2;
+          const double dp2 = (n2p[c] - v[c]) * inv2;
+          double h2;
+          if (S::LIN(2)) {
+            h2 = pos[2][c] * (pnn[2][c] ? dp2 : dm2);
+          } else {
+            h2 = godunov_select(kink(pos[2][c], neg[2][c], dm2), kink(pos[2][c], neg[2][c], dp2),
+                                dm2, dp2, pnn[2][c], nnn[2][c]);
+          }
+          // axis 3
+          double h3;
+          if (S::LIN(3)) {
+            h3 = pos[3][c] * (pnn[3][c] ? f3[c + 1] : f3[c]);
+          } else if (row3_shared) {
+            h3 = godunov_select(k3a[c], k3b[c + 1], f3[c], f3[c + 1], pnn[3][c], nnn[3][c]);
+          } else {
+            h3 = godunov_select(kink(pos[3][c], neg[3][c], f3[c]),
+                                kink(pos[3][c], neg[3][c], f3[c + 1]), f3[c], f3[c + 1],
+                                pnn[3][c], nnn[3][c]);
+          }
+          // hhat = 0.0 + h0 + h1 + h2 + h3 (0.0 + h0 == h0 in value)
+          const double hh = ((h0 + h1) + h2) + h3;
+          const double st = v[c] + a.dt * hh;
+          out[c] = st > cc[c] ? st : cc[c];
+          // |dV| bits: clear the sign (== std::abs); NaN (above +inf) never
+          // wins, as in the reference's `if (dv > max_dv)` (solver.cpp:181-182)
+          const unsigned long long ib =
+              (unsigned long long)__double_as_longlong(out[c] - v[c]) & 0x7fffffffffffffffull;
+          if (valid[c] && ib <= 0x7ff0000000000000ull) mbits = umax64(mbits, ib);
+        }
+        if (active) {
+#pragma unroll
+          for (int c = 0; c < kK; c += 2)
+            *reinterpret_cast<double2*>(op + c) = make_double2(out[c], out[c + 1]);
         }
         op += s0;
-        vcur = vnext;
+#pragma unroll
+        for (int c = 0; c < kK; ++c) v[c] = vn[c];
         // plane i0 (V) and c plane i0 are no longer read by this warp
         __syncwarp();
         if (lane == 0) {
@@ -509,8 +591,7 @@ __global__ void k_unpad4(const double* __restrict__ in, double* __restrict__ out
 
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   if (g.nd != 4 || scheme != 0 || m.per_node) return -1;
-  if (g.n[3] + (g.n[3] & 1u) > 256) return -1;  // TMA box extent limit
-  if ((g.n[3] + 1) / 2 > 608) return -1;
+  if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   bool lin[4];
   for (int d = 0; d < 4; ++d) {
@@ -555,14 +636,16 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
     a.n[d] = g.n[d];
     a.inv[d] = g.inv_spacing[d];
   }
-  a.n3p = g.n[3] + (g.n[3] & 1u);
-  const uint32_t J = a.n3p / 2;
-  // tile of (i1, i2) rows: <= 608 consumer threads (+1 producer warp), rings within one SM's
+  const uint32_t kK = a.kcells;
+  a.n3p = (g.n[3] + kK - 1) / kK * kK;
+  const uint32_t J = a.n3p / kK;
+  // tile of (i1, i2) rows: <= 352 consumer threads (+1 producer warp), rings within one SM's
   // shared memory, smallest halo/tile ratio
   uint32_t bestT1 = 1, bestT2 = 1;
   double best = 1e30;
-  for (uint32_t T1 = 1; T1 <= g.n[1] && T1 * J <= 608; ++T1) {
-    for (uint32_t T2 = 1; T2 <= g.n[2] && T1 * T2 * J <= 608; ++T2) {
+  const uint32_t maxc = kK == 2 ? 608 : 352;
+  for (uint32_t T1 = 1; T1 <= g.n[1] && T1 * J <= maxc; ++T1) {
+    for (uint32_t T2 = 1; T2 <= g.n[2] && T1 * T2 * J <= maxc; ++T2) {
       if (fast4d_smem(T1, T2, a.n3p) > 200 * 1024) continue;
       const double ratio = double((T1 + 2) * (T2 + 2)) / double(T1 * T2);
       const double score = ratio - 1e-3 * T1 * T2;
@@ -584,34 +667,51 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.cbox_bytes = a.T1 * a.T2 * a.n3p * 8u;
   a.vslot_bytes = round128(a.vbox_bytes);
   a.cslot_bytes = round128(a.cbox_bytes);
+  // one resident CTA per SM.  Split the axis-0 march into nch chunks to
+  // balance waves; every chunk pays a ring prologue (~3 plane-steps), so
+  // minimise waves * (chunk length + 3).
   const uint32_t tiles = a.tiles1 * a.tiles2;
-  const uint32_t want = static_cast<uint32_t>(sms) * 3;  // 1 CTA/SM, ~3 waves
-  uint32_t nch = (want + tiles - 1) / tiles;
-  if (nch < 1) nch = 1;
+  uint32_t nch = 1;
+  double best_cost = 1e30;
+  for (uint32_t k = 1; k <= 16 && k <= g.n[0]; ++k) {
+    const uint32_t waves = (tiles * k + sms - 1) / sms;
+    const double cost = double(waves) * (double((g.n[0] + k - 1) / k) + 3.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      nch = k;
+    }
+  }
   uint32_t L = (g.n[0] + nch - 1) / nch;
-  if (L < 4) L = 4;
   a.L = L;
   a.nchunks = (g.n[0] + L - 1) / L;
   a.blocks = tiles * a.nchunks;
 }
 
-cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
+template <class S, int K>
+static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_fast4d<ShapePlanarD0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    cudaFuncSetAttribute(k_fast4d<ShapePlanarD1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    cudaFuncSetAttribute(k_fast4d<ShapeTwin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    cudaFuncSetAttribute(k_fast4d<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  if (shape == 0)
-    k_fast4d<ShapePlanarD0><<<a.blocks, a.threads, a.smem, s>>>(a);
-  else if (shape == 1)
-    k_fast4d<ShapePlanarD1><<<a.blocks, a.threads, a.smem, s>>>(a);
+  k_fast4d<S, K><<<a.blocks, a.threads, a.smem, s>>>(a);
+}
+
+template <class S>
+static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.kcells == 4)
+    launch_one<S, 4>(a, s);
   else
-    k_fast4d<ShapeTwin><<<a.blocks, a.threads, a.smem, s>>>(a);
+    launch_one<S, 2>(a, s);
+}
+
+cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
+  if (shape == 0)
+    launch_shape<ShapePlanarD0>(a, s);
+  else if (shape == 1)
+    launch_shape<ShapePlanarD1>(a, s);
+  else
+    launch_shape<ShapeTwin>(a, s);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@ struct Fast4dArgs {
   uint32_t n[4];
   uint32_t n3p;  // padded contiguous extent (even)
   double inv[4];
+  uint32_t kcells;  // cells per thread along the contiguous axis (2 or 4)
   uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads, consumers, smem;
   const double* tab;
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
