@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
   const uint32_t smem0 = smem_u32(smem_raw);
   const uint32_t vring = smem0;
   const uint32_t cring = smem0 + kRing * a.vslot_bytes;
-  const uint32_t bars = cring + kRing * a.cslot_bytes;  // full_v[4] empty_v[4] full_c[4] empty_c[4]
+  const uint32_t bars = cring + kRing * a.cslot_bytes;  // full_v empty_v full_c empty_c [kRing] each
   uint64_t* bar_ptr = reinterpret_cast<uint64_t*>(smem_raw + kRing * a.vslot_bytes +
                                                   kRing * a.cslot_bytes);
 
