@@ -38,6 +38,7 @@ extern "C" {
 #define HJB_MAX_DIMS 6   /* grid rank supported by the device kernels */
 #define HJB_MAX_STATE 10 /* reference kMaxStateDim, dynamics.hpp:12 */
 #define HJB_MAX_INPUT 3  /* reference kMaxInputDim, dynamics.hpp:13 */
+#define HJB_MAX_LEVELS 8 /* hjb_solve_multilevel */
 
 typedef enum hjb_status {
   HJB_OK = 0,
@@ -190,6 +191,31 @@ int hjb_solve_coarse_to_fine(hjb_context* ctx, const hjb_grid* fine_grid,
                              double* coarse_value_out, hjb_solve_result* coarse_result,
                              double* fine_value_out, hjb_solve_result* fine_result,
                              double* wall_seconds);
+
+/* Multi-level adaptive solve, the N-level generalisation of
+ * solve_coarse_to_fine (reference solver.cpp:387-425; with nlevels == 2 it is
+ * that function exactly).  grids[0..nlevels-1] run coarse to fine; the last
+ * is the fine grid of c_fine / dbounds_fine.  For every coarser level l:
+ * c_l = resample(c_fine, grid_l), db_l = resample(db_fine, grid_l)
+ * (solver.cpp:396-397); level 0 starts from c_0, or from
+ * seed_from(warm_init_fine, grid_0, c_0) when warm_init_fine != NULL
+ * (solver.cpp:413-414); level l > 0 starts from
+ * seed_from(V*_{l-1}, grid_l, c_l) (solver.cpp:404-411,419-420).  A level
+ * that does not converge still seeds the next (the reference has no
+ * converged-check between stages).  values_out[l] (may be NULL) receives V*_l,
+ * results[l] its SolveResult. */
+int hjb_solve_multilevel(hjb_context* ctx, int32_t nlevels, const hjb_grid* grids,
+                         const hjb_model* model, const hjb_dbounds* dbounds_fine,
+                         const double* c_fine, const hjb_solve_config* cfg,
+                         const double* warm_init_fine, double* const* values_out,
+                         hjb_solve_result* results, double* wall_seconds);
+/* Same with device pointers (c_fine, warm_init_fine, values_out[l] and the
+ * per-node bounds of dbounds_fine). */
+int hjb_solve_multilevel_dev(hjb_context* ctx, int32_t nlevels, const hjb_grid* grids,
+                             const hjb_model* model, const hjb_dbounds* dbounds_fine,
+                             const double* c_fine, const hjb_solve_config* cfg,
+                             const double* warm_init_fine, double* const* values_out,
+                             hjb_solve_result* results, double* wall_seconds);
 
 /* ------------------------------------------------ grid / level-set helpers */
 /* resample (multilinear), reference grid.hpp:108-109 / grid.cpp:215-231. */

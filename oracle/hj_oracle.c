@@ -717,6 +717,77 @@ int hjo_solve_coarse_to_fine(const hjb_grid* fine, const hjb_model* m, const hjb
   return rc;
 }
 
+int hjo_solve_multilevel(int32_t nl, const hjb_grid* grids, const hjb_model* m,
+                         const hjb_dbounds* db, const double* c_fine, const hjb_solve_config* cfg,
+                         const double* warm, double* const* values_out,
+                         hjb_solve_result* results) {
+  if (nl < 1 || nl > HJB_MAX_LEVELS)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "solve_multilevel: 1..8 levels");
+  grid_t g[HJB_MAX_LEVELS];
+  int rc;
+  for (int l = 0; l < nl; ++l)
+    if ((rc = grid_init(&grids[l], &g[l]))) return rc;
+  for (int l = 0; l < nl; ++l)
+    if (g[l].nd != g[nl - 1].nd)
+      return fail(HJB_ERR_INVALID_ARGUMENT, "solve_coarse_to_fine: grid rank mismatch");
+  const int F = nl - 1;
+  const int64_t nf = g[F].size;
+  double* fine_db = NULL;  /* fine-level bounds as fields, for resampling */
+  if (db->channels > 0 && nl > 1) {
+    fine_db = (double*)malloc((size_t)2 * db->channels * nf * sizeof(double));
+    for (int ch = 0; ch < db->channels; ++ch)
+      for (int64_t i = 0; i < nf; ++i) {
+        fine_db[(2 * ch) * nf + i] = db->per_node ? db->lo[ch][i] : db->constant[ch].lo;
+        fine_db[(2 * ch + 1) * nf + i] = db->per_node ? db->hi[ch][i] : db->constant[ch].hi;
+      }
+  }
+  double* own[HJB_MAX_LEVELS] = {0};
+  double* cl[HJB_MAX_LEVELS] = {0};
+  double* dbl[HJB_MAX_LEVELS] = {0};
+  double* init = NULL;
+  rc = 0;
+  for (int l = 0; l < nl && !rc; ++l) {
+    const int64_t n = g[l].size;
+    double* out = (values_out && values_out[l]) ? values_out[l]
+                                                : (own[l] = (double*)malloc(n * sizeof(double)));
+    hjb_dbounds dbx = *db;
+    const double* c = c_fine;
+    if (l < F) {
+      cl[l] = (double*)malloc(n * sizeof(double));
+      hjo_resample(&grids[F], c_fine, &grids[l], cl[l]);
+      c = cl[l];
+      if (db->channels > 0) {
+        dbl[l] = (double*)malloc((size_t)2 * db->channels * n * sizeof(double));
+        for (int ch = 0; ch < db->channels; ++ch) {
+          hjo_resample(&grids[F], fine_db + (2 * ch) * nf, &grids[l], dbl[l] + (2 * ch) * n);
+          hjo_resample(&grids[F], fine_db + (2 * ch + 1) * nf, &grids[l], dbl[l] + (2 * ch + 1) * n);
+          dbx.lo[ch] = dbl[l] + (2 * ch) * n;
+          dbx.hi[ch] = dbl[l] + (2 * ch + 1) * n;
+        }
+        dbx.per_node = 1;
+      }
+    }
+    free(init);
+    init = (double*)malloc(n * sizeof(double));
+    if (l == 0) {
+      if (warm) hjo_seed_from(&grids[F], warm, &grids[0], c, init);
+      else memcpy(init, c, n * sizeof(double));
+    } else {
+      const double* prev = (values_out && values_out[l - 1]) ? values_out[l - 1] : own[l - 1];
+      hjo_seed_from(&grids[l - 1], prev, &grids[l], c, init);
+    }
+    rc = hjo_solve(&grids[l], m, &dbx, init, c, cfg, out, &results[l]);
+  }
+  free(init);
+  free(fine_db);
+  for (int l = 0; l < nl; ++l) {
+    free(own[l]);
+    free(cl[l]);
+    free(dbl[l]);
+  }
+  return rc;
+}
+
 /* ------------------------------------------------------------ level sets */
 /* signed_distance_band, levelset.cpp:54-66 */
 int hjo_signed_distance_band(const hjb_grid* gi, int32_t dim, double lo, double hi, double* out) {

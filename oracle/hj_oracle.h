@@ -68,6 +68,14 @@ int hjo_solve_coarse_to_fine(const hjb_grid* fine, const hjb_model* m, const hjb
                              const hjb_solve_config* cfg, const double* warm_init_fine,
                              double* coarse_out, hjb_solve_result* coarse_res, double* fine_out,
                              hjb_solve_result* fine_res);
+/* N-level chain generalising solve_coarse_to_fine (solver.cpp:387-425),
+ * composed from resample + max_adjacent_jump + clamp + solve (the reference's
+ * seed_from is a private lambda, solver.cpp:404-411).  values_out[l] may be
+ * NULL. */
+int hjo_solve_multilevel(int32_t nlevels, const hjb_grid* grids, const hjb_model* m,
+                         const hjb_dbounds* db, const double* c_fine, const hjb_solve_config* cfg,
+                         const double* warm_init_fine, double* const* values_out,
+                         hjb_solve_result* results);
 /* signed_distance_band / signed_distance_box, levelset.cpp:11-66 */
 int hjo_signed_distance_band(const hjb_grid* g, int32_t dim, double lo, double hi, double* out);
 int hjo_signed_distance_box(const hjb_grid* g, const double* lo, const double* hi, double* out);

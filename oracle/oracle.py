@@ -84,6 +84,9 @@ class Restatement:
         L.hjo_solve_coarse_to_fine.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds),
                                                _vp, P(abi.HjbGrid), P(abi.HjbSolveConfig), _vp, _vp,
                                                P(abi.HjbSolveResult), _vp, P(abi.HjbSolveResult)]
+        L.hjo_solve_multilevel.argtypes = [C.c_int32, P(abi.HjbGrid), P(abi.HjbModel),
+                                           P(abi.HjbDbounds), _vp, P(abi.HjbSolveConfig), _vp,
+                                           P(_vp), P(abi.HjbSolveResult)]
         L.hjo_signed_distance_band.argtypes = [P(abi.HjbGrid), C.c_int32, _d, _d, _vp]
         L.hjo_signed_distance_box.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp]
         L.hjo_hamiltonian.argtypes = [P(abi.HjbModel), _vp, _vp, P(abi.HjbInterval), P(_d)]
@@ -156,6 +159,26 @@ class Restatement:
             _arr(wv) if wv is not None else None, _arr(cout), C.byref(rc_), _arr(fout), C.byref(rf_)))
         return hj.CoarseToFineResult(coarse=hj._to_result(coarse_grid, cout, rc_, rhc, whc),
                                      fine=hj._to_result(fg, fout, rf_, rhf, whf))
+
+    def solve_multilevel(self, c_fine, model, db, coarse_grids, cfg, warm=None):
+        grids = list(coarse_grids) + [c_fine.grid()]
+        nl = len(grids)
+        cg = (abi.HjbGrid * nl)(*[g.to_c() for g in grids])
+        res = (abi.HjbSolveResult * nl)()
+        keep = []
+        for l in range(nl):
+            r, rh, wh = hj._c_result(int(cfg.max_iters))
+            res[l] = r
+            keep.append((rh, wh))
+        outs = [np.empty(g.size()) for g in grids]
+        optr = (C.c_void_p * nl)(*[o.ctypes.data for o in outs])
+        m, d, k = model.to_c(), db.to_c(), cfg.to_c()
+        wv = _vals(warm) if warm is not None else None
+        self._chk(self.lib.hjo_solve_multilevel(nl, cg, C.byref(m), C.byref(d), _arr(_vals(c_fine)),
+                                                C.byref(k), _arr(wv) if wv is not None else None,
+                                                optr, res))
+        return hj.MultiLevelResult([hj._to_result(grids[l], outs[l], res[l], *keep[l])
+                                    for l in range(nl)])
 
     def interp(self, f, x):
         val = C.c_double()

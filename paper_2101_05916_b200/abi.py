@@ -14,6 +14,7 @@ from pathlib import Path
 HJB_MAX_DIMS = 6
 HJB_MAX_STATE = 10
 HJB_MAX_INPUT = 3
+HJB_MAX_LEVELS = 8
 
 HJB_OK = 0
 HJB_ERR_INVALID_ARGUMENT = 1
@@ -109,6 +110,10 @@ SIGNATURES = [
     ("hjb_solve_coarse_to_fine", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp,
                                       P(HjbGrid), P(HjbSolveConfig), _vp, _vp,
                                       P(HjbSolveResult), _vp, P(HjbSolveResult), _dp]),
+    ("hjb_solve_multilevel", _i, [_vp, C.c_int32, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp,
+                                  P(HjbSolveConfig), _vp, P(_vp), P(HjbSolveResult), _dp]),
+    ("hjb_solve_multilevel_dev", _i, [_vp, C.c_int32, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp,
+                                      P(HjbSolveConfig), _vp, P(_vp), P(HjbSolveResult), _dp]),
     ("hjb_resample", _i, [_vp, P(HjbGrid), _vp, P(HjbGrid), _vp]),
     ("hjb_max_adjacent_jump", _i, [_vp, P(HjbGrid), _vp, _dp]),
     ("hjb_seed_from", _i, [_vp, P(HjbGrid), _vp, P(HjbGrid), _vp, _vp]),

@@ -401,13 +401,51 @@ bool fast_enabled() {
 
 // Device-resident solve: every pointer is device memory.  Shared by the
 // host-pointer entry point (which stages through the context buffers).
+// A per-node IntervalField whose every node holds the same interval is the
+// constant field (identical values at every node); collapsing it keeps the
+// folded-slope fast path (e.g. a resampled constant field of a coarse level).
+static int collapse_dbounds(hjb_context* ctx, const DevGrid& g, const hjb_dbounds* db,
+                            hjb_dbounds& out) {
+  out = *db;
+  if (!db->per_node || db->channels == 0) return HJB_OK;
+  CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
+  unsigned int* flags = reinterpret_cast<unsigned int*>(ctx->scratch.d() + 32);
+  CUDA_TRY(cudaMemsetAsync(flags, 0, 2 * kMaxInput * sizeof(unsigned int), ctx->stream));
+  double firsts[2 * kMaxInput];
+  for (int ch = 0; ch < db->channels; ++ch) {
+    CUDA_TRY(launch_not_constant(db->lo[ch], g.size, flags + 2 * ch, ctx->stream));
+    CUDA_TRY(launch_not_constant(db->hi[ch], g.size, flags + 2 * ch + 1, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(firsts + 2 * ch, db->lo[ch], sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(firsts + 2 * ch + 1, db->hi[ch], sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->launches += 2;
+  }
+  unsigned int hflags[2 * kMaxInput];
+  CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < 2 * db->channels; ++k)
+    if (hflags[k]) return HJB_OK;
+  for (int ch = 0; ch < db->channels; ++ch) {
+    if (!(firsts[2 * ch] <= firsts[2 * ch + 1])) return HJB_OK;  // let validation see lo > hi
+    out.constant[ch].lo = firsts[2 * ch];
+    out.constant[ch].hi = firsts[2 * ch + 1];
+  }
+  out.per_node = 0;
+  return HJB_OK;
+}
+
 static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
-                      const hjb_dbounds* db, const double* init, const double* c,
+                      const hjb_dbounds* db_in, const double* init, const double* c,
                       const hjb_solve_config* cfg, double* value_out, hjb_solve_result* res) {
   int rc;
   if ((rc = validate_cfg(cfg))) return rc;
   DevGrid g;
   if ((rc = make_grid(gi, g))) return rc;
+  hjb_dbounds dbc;
+  if (!db_in) return set_err(HJB_ERR_INVALID_ARGUMENT, "model/dbounds: null");
+  if ((rc = collapse_dbounds(ctx, g, db_in, dbc))) return rc;
+  const hjb_dbounds* db = &dbc;
   HostModel hm;
   if ((rc = make_model(mi, db, g, hm))) return rc;
   if ((rc = upload_model(ctx, hm))) return rc;
@@ -940,82 +978,103 @@ int hjb_signed_distance_band(hjb_context* ctx, const hjb_grid* gi, int32_t dim, 
   return HJB_OK;
 }
 
-// solve_coarse_to_fine, solver.cpp:387-425, entirely on the device:
-// restriction of c and the disturbance bounds, seeding, both solves.
-int hjb_solve_coarse_to_fine(hjb_context* ctx, const hjb_grid* fgi, const hjb_model* mi,
-                             const hjb_dbounds* db, const double* c_fine,
-                             const hjb_grid* cgi, const hjb_solve_config* cfg,
-                             const double* warm_init_fine, double* coarse_out,
-                             hjb_solve_result* coarse_res, double* fine_out,
-                             hjb_solve_result* fine_res, double* wall_seconds) {
+// N-level adaptive solve (solve_coarse_to_fine generalised), device pointers.
+static int multilevel_impl(hjb_context* ctx, int nl, const hjb_grid* grids, const hjb_model* mi,
+                           const hjb_dbounds* db, const double* c_fine, const hjb_solve_config* cfg,
+                           const double* warm, double* const* values_out,
+                           hjb_solve_result* results, double* wall_seconds) {
   int rc;
-  if ((rc = check_ctx(ctx))) return rc;
-  DevGrid fg, cg;
-  if ((rc = make_grid(fgi, fg)) || (rc = make_grid(cgi, cg))) return rc;
-  if (cg.nd != fg.nd)
-    return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_coarse_to_fine: grid rank mismatch");
+  if (nl < 1 || nl > HJB_MAX_LEVELS)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_multilevel: 1..8 levels");
+  if ((rc = validate_cfg(cfg))) return rc;
+  DevGrid g[HJB_MAX_LEVELS];
+  for (int l = 0; l < nl; ++l)
+    if ((rc = make_grid(&grids[l], g[l]))) return rc;
+  for (int l = 0; l < nl; ++l)
+    if (g[l].nd != g[nl - 1].nd)
+      return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_coarse_to_fine: grid rank mismatch");
+  const int F = nl - 1;
+  const int nch = db->channels;
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   CUDA_TRY(cudaEventRecord(e0, ctx->stream));
-  const size_t fb = fg.size * sizeof(double), cb = cg.size * sizeof(double);
-  DevBuf dcf, dcc, dinit_c, dinit_f, dout_c, dout_f, dwarm, ddbf, ddbc;
-  CUDA_TRY(dcf.ensure(fb));
-  CUDA_TRY(dcc.ensure(cb));
-  CUDA_TRY(dinit_c.ensure(cb));
-  CUDA_TRY(dinit_f.ensure(fb));
-  CUDA_TRY(dout_c.ensure(cb));
-  CUDA_TRY(dout_f.ensure(fb));
-  CUDA_TRY(cudaMemcpyAsync(dcf.p, c_fine, fb, cudaMemcpyHostToDevice, ctx->stream));
-  // c_coarse = resample(c_fine, coarse) (solver.cpp:396)
-  CUDA_TRY(launch_resample(fg, dcf.d(), cg, dcc.d(), nullptr, nullptr, ctx->stream));
-  // db_coarse = resample(db_fine, coarse) (solver.cpp:397, 378-385)
-  hjb_dbounds dbf = *db, dbc = *db;
-  const int nch = db->channels;
-  if (nch > 0) {
-    CUDA_TRY(ddbf.ensure(2 * nch * fb));
-    CUDA_TRY(ddbc.ensure(2 * nch * cb));
-    for (int ch = 0; ch < nch; ++ch) {
-      for (int s = 0; s < 2; ++s) {
-        double* f = ddbf.d() + (2 * ch + s) * fg.size;
-        double* cc = ddbc.d() + (2 * ch + s) * cg.size;
-        if (db->per_node) {
-          CUDA_TRY(cudaMemcpyAsync(f, s ? db->hi[ch] : db->lo[ch], fb, cudaMemcpyHostToDevice,
-                                   ctx->stream));
-        } else {
-          std::vector<double> tmp(fg.size, s ? db->constant[ch].hi : db->constant[ch].lo);
-          CUDA_TRY(cudaMemcpyAsync(f, tmp.data(), fb, cudaMemcpyHostToDevice, ctx->stream));
-          CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        }
-        CUDA_TRY(launch_resample(fg, f, cg, cc, nullptr, nullptr, ctx->stream));
-        if (s) {
-          dbf.hi[ch] = f;
-          dbc.hi[ch] = cc;
-        } else {
-          dbf.lo[ch] = f;
-          dbc.lo[ch] = cc;
-        }
+  DevBuf cl[HJB_MAX_LEVELS], dbl[HJB_MAX_LEVELS], init[HJB_MAX_LEVELS], out[HJB_MAX_LEVELS];
+  DevBuf dbf_const;
+  // the fine level's bounds as device fields (a constant field is expanded
+  // only to be resampled onto the coarse grids, solver.cpp:378-385)
+  const double* dbf_lo[HJB_MAX_INPUT] = {nullptr, nullptr, nullptr};
+  const double* dbf_hi[HJB_MAX_INPUT] = {nullptr, nullptr, nullptr};
+  if (nch > 0 && nl > 1) {
+    if (db->per_node) {
+      for (int ch = 0; ch < nch; ++ch) {
+        dbf_lo[ch] = db->lo[ch];
+        dbf_hi[ch] = db->hi[ch];
+      }
+    } else {
+      const size_t fb = static_cast<size_t>(g[F].size) * sizeof(double);
+      CUDA_TRY(dbf_const.ensure(2 * nch * fb));
+      for (int ch = 0; ch < nch; ++ch) {
+        double* lo = dbf_const.d() + (2 * ch) * static_cast<size_t>(g[F].size);
+        double* hi = dbf_const.d() + (2 * ch + 1) * static_cast<size_t>(g[F].size);
+        CUDA_TRY(launch_fill(lo, g[F].size, db->constant[ch].lo, ctx->stream));
+        CUDA_TRY(launch_fill(hi, g[F].size, db->constant[ch].hi, ctx->stream));
+        dbf_lo[ch] = lo;
+        dbf_hi[ch] = hi;
       }
     }
-    dbc.per_node = 1;
-    if (db->per_node) dbf.per_node = 1; else dbf = *db;
   }
-  // init_coarse = warm ? seed_from(warm, coarse, c_coarse) : c_coarse
-  if (warm_init_fine) {
-    CUDA_TRY(dwarm.ensure(fb));
-    CUDA_TRY(cudaMemcpyAsync(dwarm.p, warm_init_fine, fb, cudaMemcpyHostToDevice, ctx->stream));
-    if ((rc = hjb_seed_from_dev(ctx, fgi, dwarm.d(), cgi, dcc.d(), dinit_c.d()))) return rc;
-  } else {
-    CUDA_TRY(cudaMemcpyAsync(dinit_c.p, dcc.p, cb, cudaMemcpyDeviceToDevice, ctx->stream));
+  double* level_out[HJB_MAX_LEVELS];
+  for (int l = 0; l < nl; ++l) {
+    const size_t b = static_cast<size_t>(g[l].size) * sizeof(double);
+    CUDA_TRY(out[l].ensure(b));
+    level_out[l] = (values_out && values_out[l]) ? values_out[l] : out[l].d();
+    CUDA_TRY(init[l].ensure(b));
   }
-  if ((rc = solve_impl(ctx, cgi, mi, &dbc, dinit_c.d(), dcc.d(), cfg, dout_c.d(), coarse_res)))
-    return rc;
-  if ((rc = hjb_seed_from_dev(ctx, cgi, dout_c.d(), fgi, dcf.d(), dinit_f.d()))) return rc;
-  if ((rc = solve_impl(ctx, fgi, mi, &dbf, dinit_f.d(), dcf.d(), cfg, dout_f.d(), fine_res)))
-    return rc;
+  const double* c_l[HJB_MAX_LEVELS];
+  hjb_dbounds db_l[HJB_MAX_LEVELS];
+  for (int l = 0; l < F; ++l) {
+    const size_t b = static_cast<size_t>(g[l].size) * sizeof(double);
+    CUDA_TRY(cl[l].ensure(b));
+    CUDA_TRY(launch_resample(g[F], c_fine, g[l], cl[l].d(), nullptr, nullptr, ctx->stream));
+    c_l[l] = cl[l].d();
+    db_l[l] = *db;
+    if (nch > 0) {
+      CUDA_TRY(dbl[l].ensure(2 * nch * b));
+      for (int ch = 0; ch < nch; ++ch) {
+        double* lo = dbl[l].d() + (2 * ch) * static_cast<size_t>(g[l].size);
+        double* hi = dbl[l].d() + (2 * ch + 1) * static_cast<size_t>(g[l].size);
+        CUDA_TRY(launch_resample(g[F], dbf_lo[ch], g[l], lo, nullptr, nullptr, ctx->stream));
+        CUDA_TRY(launch_resample(g[F], dbf_hi[ch], g[l], hi, nullptr, nullptr, ctx->stream));
+        db_l[l].lo[ch] = lo;
+        db_l[l].hi[ch] = hi;
+      }
+      db_l[l].per_node = 1;
+    }
+    ctx->launches += 1 + 2 * nch;
+  }
+  c_l[F] = c_fine;
+  db_l[F] = *db;
+  for (int l = 0; l < nl; ++l) {
+    const double* init_l;
+    if (l == 0) {
+      if (warm) {
+        if ((rc = hjb_seed_from_dev(ctx, &grids[F], warm, &grids[0], c_l[0], init[0].d()))) return rc;
+        init_l = init[0].d();
+      } else {
+        init_l = c_l[0];
+      }
+    } else {
+      if ((rc = hjb_seed_from_dev(ctx, &grids[l - 1], level_out[l - 1], &grids[l], c_l[l],
+                                  init[l].d())))
+        return rc;
+      init_l = init[l].d();
+    }
+    hjb_solve_result* res = results ? &results[l] : nullptr;
+    if ((rc = solve_impl(ctx, &grids[l], mi, &db_l[l], init_l, c_l[l], cfg, level_out[l], res)))
+      return rc;
+  }
   CUDA_TRY(cudaEventRecord(e1, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(coarse_out, dout_c.p, cb, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(fine_out, dout_f.p, fb, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -1023,6 +1082,75 @@ int hjb_solve_coarse_to_fine(hjb_context* ctx, const hjb_grid* fgi, const hjb_mo
   cudaEventDestroy(e1);
   if (wall_seconds) *wall_seconds = ms * 1e-3;
   return HJB_OK;
+}
+
+int hjb_solve_multilevel_dev(hjb_context* ctx, int32_t nl, const hjb_grid* grids,
+                             const hjb_model* mi, const hjb_dbounds* db, const double* c_fine,
+                             const hjb_solve_config* cfg, const double* warm,
+                             double* const* values_out, hjb_solve_result* results,
+                             double* wall_seconds) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  return multilevel_impl(ctx, nl, grids, mi, db, c_fine, cfg, warm, values_out, results,
+                         wall_seconds);
+}
+
+int hjb_solve_multilevel(hjb_context* ctx, int32_t nl, const hjb_grid* grids, const hjb_model* mi,
+                         const hjb_dbounds* db, const double* c_fine, const hjb_solve_config* cfg,
+                         const double* warm, double* const* values_out,
+                         hjb_solve_result* results, double* wall_seconds) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  if (nl < 1 || nl > HJB_MAX_LEVELS)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_multilevel: 1..8 levels");
+  DevGrid g[HJB_MAX_LEVELS];
+  for (int l = 0; l < nl; ++l)
+    if ((rc = make_grid(&grids[l], g[l]))) return rc;
+  const size_t fb = static_cast<size_t>(g[nl - 1].size) * sizeof(double);
+  DevBuf dc, dw, dout[HJB_MAX_LEVELS], ddb;
+  CUDA_TRY(dc.ensure(fb));
+  CUDA_TRY(cudaMemcpyAsync(dc.p, c_fine, fb, cudaMemcpyHostToDevice, ctx->stream));
+  if (warm) {
+    CUDA_TRY(dw.ensure(fb));
+    CUDA_TRY(cudaMemcpyAsync(dw.p, warm, fb, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  hjb_dbounds dbs;
+  if ((rc = stage_dbounds(ctx, db, g[nl - 1].size, ddb, dbs))) return rc;
+  double* outs[HJB_MAX_LEVELS];
+  for (int l = 0; l < nl; ++l) {
+    CUDA_TRY(dout[l].ensure(static_cast<size_t>(g[l].size) * sizeof(double)));
+    outs[l] = dout[l].d();
+  }
+  if ((rc = multilevel_impl(ctx, nl, grids, mi, &dbs, dc.d(), cfg, warm ? dw.d() : nullptr, outs,
+                            results, wall_seconds)))
+    return rc;
+  for (int l = 0; l < nl; ++l)
+    if (values_out && values_out[l])
+      CUDA_TRY(cudaMemcpyAsync(values_out[l], outs[l], static_cast<size_t>(g[l].size) * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+// solve_coarse_to_fine, solver.cpp:387-425: the two-level case of the above.
+int hjb_solve_coarse_to_fine(hjb_context* ctx, const hjb_grid* fgi, const hjb_model* mi,
+                             const hjb_dbounds* db, const double* c_fine,
+                             const hjb_grid* cgi, const hjb_solve_config* cfg,
+                             const double* warm_init_fine, double* coarse_out,
+                             hjb_solve_result* coarse_res, double* fine_out,
+                             hjb_solve_result* fine_res, double* wall_seconds) {
+  if (!fgi || !cgi) return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_coarse_to_fine: null grid");
+  hjb_grid grids[2] = {*cgi, *fgi};
+  double* outs[2] = {coarse_out, fine_out};
+  hjb_solve_result res[2];
+  std::memset(res, 0, sizeof res);
+  if (coarse_res) res[0] = *coarse_res;
+  if (fine_res) res[1] = *fine_res;
+  const int rc = hjb_solve_multilevel(ctx, 2, grids, mi, db, c_fine, cfg, warm_init_fine, outs, res,
+                                      wall_seconds);
+  if (coarse_res) *coarse_res = res[0];
+  if (fine_res) *fine_res = res[1];
+  return rc;
 }
 
 }  // extern "C"

@@ -447,6 +447,19 @@ __global__ void k_field_op(long long n, const double* __restrict__ a,
   }
 }
 
+__global__ void k_fill(double* out, uint32_t n, double value) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = value;
+}
+
+__global__ void k_not_constant(const double* __restrict__ f, uint32_t n, unsigned int* flag) {
+  const unsigned long long first = __double_as_longlong(f[0]);
+  bool diff = false;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    diff |= (unsigned long long)__double_as_longlong(f[i]) != first;
+  if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
 inline dim3 blocks_for(uint32_t n) { return dim3((n + kThreads - 1) / kThreads); }
 
 // Persistent-style grid: a few CTAs per SM stride over the nodes, so the
@@ -548,6 +561,20 @@ cudaError_t launch_band(const DevGrid& g, int dim, double lo, double hi, double*
 #define CALL(N) k_band<N><<<grid, kThreads, 0, s>>>(g, dim, lo, hi, out)
   HJB_DISPATCH_ND(g.nd, CALL)
 #undef CALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(double* out, uint32_t n, double value, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const uint32_t b = (n + kThreads - 1) / kThreads;
+  k_fill<<<b < 148 * 16 ? b : 148 * 16, kThreads, 0, s>>>(out, n, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_not_constant(const double* f, uint32_t n, unsigned int* flag, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const uint32_t b = (n + kThreads - 1) / kThreads;
+  k_not_constant<<<b < 148 * 8 ? b : 148 * 8, kThreads, 0, s>>>(f, n, flag);
   return cudaGetLastError();
 }
 

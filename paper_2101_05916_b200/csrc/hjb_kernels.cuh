@@ -55,4 +55,9 @@ cudaError_t launch_band(const DevGrid& g, int dim, double lo, double hi, double*
 cudaError_t launch_field_op(long long n, const double* a, const double* b, double* out,
                             int is_max, cudaStream_t s);
 
+// fill n doubles with a value
+cudaError_t launch_fill(double* out, uint32_t n, double value, cudaStream_t s);
+// *flag |= 1 if any of f[0..n) differs bitwise from f[0] (flag zeroed by caller)
+cudaError_t launch_not_constant(const double* f, uint32_t n, unsigned int* flag, cudaStream_t s);
+
 }  // namespace hjb

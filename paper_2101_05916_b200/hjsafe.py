@@ -879,6 +879,49 @@ def solve_coarse_to_fine(constraint_fine: ScalarField, model: DynamicsModel,
                               fine=_to_result(fg, fout, rf_, rhf, whf), wall_seconds=wall.value)
 
 
+@dataclass
+class MultiLevelResult:
+    levels: list  # SolveResult per level, coarse to fine
+    wall_seconds: float = 0.0
+
+
+def solve_multilevel(constraint_fine: ScalarField, model: DynamicsModel,
+                     dbounds_fine: IntervalField, coarse_grids: Sequence[Grid],
+                     cfg: SolveConfig | None = None,
+                     warm_init_fine: ScalarField | None = None,
+                     ctx: Context | None = None) -> MultiLevelResult:
+    """N-level adaptive solve (coarse grids listed coarse to fine, then the fine
+    grid of constraint_fine), generalising solve_coarse_to_fine
+    (solver.cpp:387-425); device-resident end to end."""
+    cfg = cfg or SolveConfig()
+    cfg.validate()
+    grids = list(coarse_grids) + [constraint_fine.grid()]
+    for g in grids:
+        if g.ndims() != constraint_fine.grid().ndims():
+            raise InvalidArgument("solve_coarse_to_fine: grid rank mismatch")
+    lib = abi.load()
+    nl = len(grids)
+    cg = (abi.HjbGrid * nl)(*[g.to_c() for g in grids])
+    res = (abi.HjbSolveResult * nl)()
+    keep = []
+    for l in range(nl):
+        rh = np.zeros(int(cfg.max_iters))
+        wh = np.zeros(int(cfg.max_iters))
+        keep.append((rh, wh))
+        res[l].residual_history = rh.ctypes.data_as(C.POINTER(C.c_double))
+        res[l].wall_ms_history = wh.ctypes.data_as(C.POINTER(C.c_double))
+        res[l].history_capacity = int(cfg.max_iters)
+    outs = [np.empty(g.size()) for g in grids]
+    optr = (C.c_void_p * nl)(*[o.ctypes.data for o in outs])
+    wall = C.c_double()
+    m, d, c = model.to_c(), dbounds_fine.to_c(), cfg.to_c()
+    warm = warm_init_fine.ptr() if warm_init_fine is not None else None
+    _check(lib.hjb_solve_multilevel(_ctx(ctx), nl, cg, C.byref(m), C.byref(d), constraint_fine.ptr(),
+                                    C.byref(c), warm, optr, res, C.byref(wall)))
+    return MultiLevelResult([_to_result(grids[l], outs[l], res[l], *keep[l]) for l in range(nl)],
+                            wall.value)
+
+
 def resample(f, target: Grid, ctx: Context | None = None):
     """grid.hpp:108-109 (ScalarField) and solver.hpp:77 (IntervalField)."""
     if isinstance(f, IntervalField):

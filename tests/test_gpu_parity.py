@@ -10,7 +10,7 @@ import pytest
 from paper_2101_05916_b200 import configs
 from paper_2101_05916_b200 import hjsafe as hj
 
-from cases import (band_np, per_node_case, quad_setup, same, solve_cases, with_iters,
+from cases import (band_np, fmax_np, per_node_case, quad_setup, same, solve_cases, with_iters,
                    workload_case)
 
 pytestmark = pytest.mark.gpu
@@ -154,3 +154,19 @@ def test_fast4d_matches_generic_kernel(gpu_ctx, monkeypatch):
     gen = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
     assert same(fast.value.values(), gen.value.values())
     assert same(fast.residual_history, gen.residual_history)
+
+
+def test_multilevel_three_levels_matches_oracle(gpu_ctx, oracle):
+    """Config-5 style 3-level chain (obstacles, wind 0.6) at reduced size:
+    7^4 -> 13^4 -> 25^4, bitwise per level."""
+    ws = configs.config5(levels=(7, 13, 25), tol=5e-3)
+    fine = ws[-1]
+    c = hj.ScalarField(fine.grid, fine.constraint(band_np, fmax_np))
+    cfg = hj.SolveConfig(tolerance=5e-3, max_iters=300)
+    want = oracle.solve_multilevel(c, fine.model, fine.dbounds(), [w.grid for w in ws[:-1]], cfg)
+    got = hj.solve_multilevel(c, fine.model, fine.dbounds(), [w.grid for w in ws[:-1]], cfg,
+                              ctx=gpu_ctx)
+    for x, y in zip(got.levels, want.levels):
+        assert x.iterations == y.iterations
+        assert same(x.residual_history, y.residual_history)
+        assert same(x.value.values(), y.value.values())

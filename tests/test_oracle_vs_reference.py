@@ -162,3 +162,14 @@ def test_hamiltonian_and_flow_bounds_probes(oracle, ref):
     assert a[1] == pytest.approx(10.1) and a[0] == pytest.approx(2.0)
     a = oracle.flow_bounds(hj.NearHoverPlanar4D("x"), [0, 0, 0, 0], db)
     assert a[3] == pytest.approx(10.0 * 0.2443)
+
+
+def test_multilevel_two_levels_is_coarse_to_fine(oracle, ref):
+    """hjo_solve_multilevel with 2 levels == the reference's solve_coarse_to_fine."""
+    q = quad_setup(41)
+    coarse = hj.Grid([(0.0, 3.2, 21), (-5.0, 5.0, 21)])
+    a = oracle.solve_multilevel(q.c_field(), q.model, q.db, [coarse], q.cfg)
+    b = ref.solve_coarse_to_fine(q.c_field(), q.model, q.db, coarse, q.cfg)
+    for x, y in zip(a.levels, (b.coarse, b.fine)):
+        assert x.iterations == y.iterations
+        assert same(x.value.values(), y.value.values())
