@@ -289,6 +289,12 @@ def run_hjb(args):
     e2e_rate = world * args.iters * cells / e2e_s
 
     peak, peak_src = measured_peak()
+    traffic = None
+    tp = ROOT / "profiles" / "round1_traffic.json"
+    if tp.exists():
+        t = json.loads(tp.read_text()).get(str(args.n))
+        if t:
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
     sweep = statistics.mean(sweep_s)
     achieved = BYTES_PER_CELL * cells / sweep / 1e9
     line = {
@@ -304,7 +310,8 @@ def run_hjb(args):
                    "l2": f"working set {3 * cells * 8 / 1e6:.0f} MB (V front/back + c) vs 126 MB L2; "
                          "no explicit flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "profiles/round1_traffic.json (ncu --set full, one launch)",
                      "kernel": "k_fast4d sweep (TMA plane ring; avg device time per sweep incl. launch gaps)",
                      "bytes_per_cell": BYTES_PER_CELL, "peak_source": peak_src,
                      "sweep_us": sweep * 1e6},
