@@ -262,6 +262,36 @@ int hjb_field_max_dev(hjb_context* ctx, int64_t n, const double* a, const double
 int hjb_field_min_dev(hjb_context* ctx, int64_t n, const double* a, const double* b,
                       double* out);
 
+/* ------------------------------------------- multi-GPU slab partition */
+/* Axis-0 slab partition across ranks: one process per GPU,
+ * balanced slabs (the first n0 % nranks ranks own one extra plane). */
+typedef struct hjb_comm hjb_comm;
+int hjb_slab_partition(int64_t n0, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end);
+/* NCCL unique id (128 bytes) created on rank 0 and broadcast by the caller
+ * (e.g. over torch.distributed); NCCL is loaded with dlopen. */
+int hjb_nccl_unique_id(void* out128);
+int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* unique_id128,
+                    hjb_comm** out);
+int hjb_comm_destroy(hjb_comm* comm);
+/* solve() over a slab-partitioned 4D grid: init/c/value_out hold this rank's
+ * owned planes [begin, end) of `global_grid` (reference layout, device
+ * pointers).  Per sweep: NCCL halo exchange, slab sweep, all-reduce(max) of
+ * max|dV|, device epilogue; bitwise identical to hjb_solve_dev.  4D
+ * Godunov fast-path models with constant bounds. */
+int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* global_grid,
+                          const hjb_model* model, const hjb_dbounds* dbounds,
+                          const double* init_slab, const double* c_slab,
+                          const hjb_solve_config* cfg, double* value_slab_out,
+                          hjb_solve_result* result);
+/* One sweep restricted to planes [plane_begin, plane_end) of a full grid
+ * (device pointers): the slab computation of one rank, for single-device
+ * verification of the partition.  Planes of `out` outside the range receive
+ * a copy of `value`. */
+int hjb_sweep_planes_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                         const hjb_dbounds* dbounds, const double* value,
+                         const double* constraint, int64_t plane_begin, int64_t plane_end,
+                         double dt, double* out, double* max_dv);
+
 /* Stream of the context (cudaStream_t as void*) and synchronisation. */
 void* hjb_context_stream(hjb_context* ctx);
 int hjb_context_synchronize(hjb_context* ctx);

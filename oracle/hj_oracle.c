@@ -448,6 +448,22 @@ int hjo_sweep(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, con
   return 0;
 }
 
+int hjo_sweep_planes(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db,
+                     const double* v, const double* c, double dt, int32_t scheme,
+                     const double* global_alpha, int64_t pb, int64_t pe, double* out,
+                     double* max_dv) {
+  grid_t g;
+  int rc = check_ctx(gi, m, db, &g);
+  if (rc) return rc;
+  if (pb < 0 || pe > g.n[0] || pb >= pe)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "sweep_planes: bad plane range");
+  double inv[HJB_MAX_DIMS];
+  for (int d = 0; d < g.nd; ++d) inv[d] = 1.0 / g.spacing[d];
+  *max_dv = update_range(&g, m, db, inv, scheme == HJB_GODUNOV, global_alpha, v, c, out, dt,
+                         pb * g.stride[0], pe * g.stride[0]);
+  return 0;
+}
+
 /* vi_step, solver.cpp:284-308 */
 int hjo_vi_step(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, const double* v,
                 const double* c, double dt, const hjb_solve_config* cfg, double* out) {

@@ -46,6 +46,13 @@ int hjo_cfl_dt(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, dou
 int hjo_sweep(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, const double* v,
               const double* c, double dt, int32_t scheme, const double* global_alpha,
               double* out, double* max_dv);
+/* update_chunk over planes [plane_begin, plane_end) of axis 0 only: the slab
+ * computation of one rank of the multi-GPU partition (neighbour planes are
+ * read from v; the grid's own edges keep the reference edge rule). */
+int hjo_sweep_planes(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db,
+                     const double* v, const double* c, double dt, int32_t scheme,
+                     const double* global_alpha, int64_t plane_begin, int64_t plane_end,
+                     double* out, double* max_dv);
 /* vi_step, solver.cpp:284-308 */
 int hjo_vi_step(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db, const double* v,
                 const double* c, double dt, const hjb_solve_config* cfg, double* out);

@@ -75,6 +75,8 @@ class Restatement:
                                 C.c_int32, _vp, _vp, P(_d)]
         L.hjo_vi_step.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp, _vp, _d,
                                   P(abi.HjbSolveConfig), _vp]
+        L.hjo_sweep_planes.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp, _vp,
+                                       _d, C.c_int32, _vp, C.c_int64, C.c_int64, _vp, P(_d)]
         L.hjo_solve.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp, _vp,
                                 P(abi.HjbSolveConfig), _vp, P(abi.HjbSolveResult)]
         L.hjo_interp.argtypes = [P(abi.HjbGrid), _vp, _vp, P(_d), P(C.c_int32)]
@@ -123,6 +125,15 @@ class Restatement:
         self._chk(self.lib.hjo_sweep(C.byref(g), C.byref(m), C.byref(d), _arr(v), _arr(c), dt,
                                      scheme, ga, _arr(out), C.byref(mx)))
         return out, mx.value
+
+    def sweep_planes(self, grid, model, db, v, c, dt, pb, pe, out):
+        """In-place update of planes [pb, pe) of `out` (numpy, full grid size)."""
+        mx = C.c_double()
+        g, m, d = grid.to_c(), model.to_c(), db.to_c()
+        self._chk(self.lib.hjo_sweep_planes(C.byref(g), C.byref(m), C.byref(d), _arr(_vals(v)),
+                                            _arr(_vals(c)), dt, abi.GODUNOV, None, pb, pe,
+                                            _arr(out), C.byref(mx)))
+        return mx.value
 
     def vi_step(self, v, c, model, db, dt, cfg=None):
         cfg = cfg or hj.SolveConfig()

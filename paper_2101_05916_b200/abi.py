@@ -128,6 +128,14 @@ SIGNATURES = [
     ("hjb_signed_distance_band_dev", _i, [_vp, P(HjbGrid), _i32, _d, _d, _vp]),
     ("hjb_field_max_dev", _i, [_vp, _i64, _vp, _vp, _vp]),
     ("hjb_field_min_dev", _i, [_vp, _i64, _vp, _vp, _vp]),
+    ("hjb_slab_partition", _i, [_i64, _i32, _i32, P(_i64), P(_i64)]),
+    ("hjb_nccl_unique_id", _i, [_vp]),
+    ("hjb_comm_create", _i, [_vp, _i32, _i32, _vp, P(_vp)]),
+    ("hjb_comm_destroy", _i, [_vp]),
+    ("hjb_solve_sharded_dev", _i, [_vp, _vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp,
+                                   P(HjbSolveConfig), _vp, P(HjbSolveResult)]),
+    ("hjb_sweep_planes_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp, _i64,
+                                  _i64, _d, _vp, _dp]),
     ("hjb_context_stream", _vp, [_vp]),
     ("hjb_context_synchronize", _i, [_vp]),
     ("hjb_context_launch_count", _i64, [_vp]),

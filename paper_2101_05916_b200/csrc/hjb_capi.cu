@@ -21,6 +21,7 @@
 #include "../../include/hjb.h"
 #include "hjb_common.cuh"
 #include "hjb_fast4d.cuh"
+#include "hjb_internal.cuh"
 #include "hjb_ho.cuh"
 #include "hjb_kernels.cuh"
 
@@ -28,7 +29,7 @@ using namespace hjb;
 
 thread_local std::string hjb::g_err;
 
-namespace {
+namespace hjb {
 
 // ----------------------------------------------------------------- grid
 // Grid::Grid validation, grid.cpp:10-31
@@ -71,14 +72,6 @@ inline double coord(const DevGrid& g, int d, uint32_t k) {
   return g.min[d] + static_cast<double>(k) * g.spacing[d];
 }
 
-bool same_grid(const hjb_grid* a, const hjb_grid* b) {
-  if (a->ndims != b->ndims) return false;
-  for (int i = 0; i < a->ndims; ++i)
-    if (a->dims[i].min != b->dims[i].min || a->dims[i].max != b->dims[i].max ||
-        a->dims[i].n != b->dims[i].n)
-      return false;
-  return true;
-}
 
 // ---------------------------------------------------------------- model
 double term_at(const hjb_drift_term& t, double x, uint32_t k) {
@@ -90,12 +83,6 @@ double term_at(const hjb_drift_term& t, double x, uint32_t k) {
     default: return 0.0;
   }
 }
-
-struct HostModel {
-  DevModel dm;
-  std::vector<double> tab;
-  bool separable = true;
-};
 
 int check_term(const hjb_drift_term& t, const DevGrid& g) {
   if (t.kind < HJB_TERM_NONE || t.kind > HJB_TERM_TABLE)
@@ -289,11 +276,6 @@ int upload_model(hjb_context* ctx, HostModel& hm) {
   return HJB_OK;
 }
 
-struct Scan {
-  double max_speed_sum = 0.0;
-  double max_alpha[kMaxDims] = {0};
-};
-
 // scan_alpha on the device (K1) — solver.cpp:221-268
 int run_scan(hjb_context* ctx, const DevGrid& g, const DevModel& m, Scan& out) {
   CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
@@ -397,7 +379,28 @@ bool fast_enabled() {
   return !(e && std::strcmp(e, "0") == 0);
 }
 
-}  // namespace
+// 4D fast-path preparation shared with the sharded driver (hjb_shard.cu)
+int prepare(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const hjb_dbounds* db,
+            Prepared& p) {
+  int rc;
+  if ((rc = make_grid(gi, p.g))) return rc;
+  if ((rc = make_model(mi, db, p.g, p.hm))) return rc;
+  if ((rc = upload_model(ctx, p.hm))) return rc;
+  p.shape = fast4d_shape(p.g, p.hm.dm, 0);
+  return HJB_OK;
+}
+
+void fill_tables(const Prepared& p, Fast4dArgs& f) {
+  f.tab = p.hm.dm.tab;
+  for (int d = 0; d < 4; ++d) {
+    f.off_pos[d] = p.hm.dm.row[d].off_pos;
+    f.off_neg[d] = p.hm.dm.row[d].off_neg;
+    f.off_a[d] = p.hm.dm.row[d].off_a;
+    f.off_b[d] = p.hm.dm.row[d].off_b;
+  }
+}
+
+}  // namespace hjb
 
 // Device-resident solve: every pointer is device memory.  Shared by the
 // host-pointer entry point (which stages through the context buffers).
@@ -613,11 +616,6 @@ int stage_dbounds(hjb_context* ctx, const hjb_dbounds* db, size_t n, DevBuf& buf
   return HJB_OK;
 }
 
-size_t grid_size(const hjb_grid* gi) {
-  size_t n = 1;
-  for (int i = 0; i < gi->ndims; ++i) n *= static_cast<size_t>(gi->dims[i].n);
-  return n;
-}
 
 int check_ctx(hjb_context* ctx) {
   if (!ctx) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: null");

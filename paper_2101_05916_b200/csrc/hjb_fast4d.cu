@@ -42,32 +42,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns4() {
 
 __device__ __forceinline__ bool sign_clear(double x) { return __double2hiint(x) >= 0; }
 
-// Godunov flux for a one-kink Hamiltonian (solver.cpp:44-63), value-exact.
-__device__ __forceinline__ double flux(double pos, double neg, double dm, double dp) {
-  const bool km = sign_clear(dm);  // dm "> 0" (+-0 classified by sign: see file header)
-  const bool kp = sign_clear(dp);
-  const double sm = km ? pos : neg;
-  const double sp = kp ? pos : neg;
-  const double ha = sm * dm;  // == reference kink_h(s, dminus)
-  const double hb = sp * dp;  // == reference kink_h(s, dplus)
-  const bool gt = ha > hb;
-  double h;
-  if (km == kp) {
-    // same-signed gradients: the extremum over [dm,dp] of the linear piece is
-    // attained at the upwind end: hb if the slope is >= 0, else ha
-    h = sign_clear(sm) ? hb : ha;
-  } else if (kp) {
-    // dm <= 0 < dp: rarefaction, max(ha, hb) clamped at 0 from below
-    h = gt ? ha : hb;
-    h = sign_clear(h) ? h : 0.0;
-  } else {
-    // dp <= 0 < dm: shock, min(ha, hb) clamped at 0 from above
-    h = gt ? hb : ha;
-    h = sign_clear(h) ? 0.0 : h;
-  }
-  return h;
-}
-
 // Row structure of the model, fixed at compile time: axis of the slope
 // table (A), optional second drift axis (B, pos == neg then), and whether
 // the row is always linear (pos == neg everywhere: no inputs on the row).
@@ -99,35 +73,6 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
                                                      unsigned long long b) {
   return a > b ? a : b;
-}
-
-// Loop-invariant classification of a one-kink Hamiltonian row
-// (H(p) = pos*p for p > 0, neg*p otherwise):
-//   LIN  pos == neg         flux = s * (s >= 0 ? dp : dm)
-//   INC  pos, neg >= 0      H non-decreasing: flux = H(dp) (== reference hb)
-//   DEC  pos, neg <= 0      H non-increasing: flux = H(dm) (== reference ha)
-//   GEN  otherwise          full Godunov selection (flux() above)
-// In every case the value equals the reference's godunov_flux
-// (solver.cpp:52-63): for monotone H the reference's max/min selects hb
-// (INC) or ha (DEC), or an equal value, and its zero clamps cannot fire.
-enum : int { kLin = 0, kInc = 1, kDec = 2, kGen = 3 };
-
-__device__ __forceinline__ int classify(double pos, double neg) {
-  if (pos == neg) return kLin;
-  if (sign_clear(pos) && sign_clear(neg)) return kInc;
-  if (!sign_clear(pos) && !sign_clear(neg)) return kDec;
-  return kGen;
-}
-
-__device__ __forceinline__ double flux_mode(int mode, double pos, double neg, double dm,
-                                            double dp) {
-  if (mode == kInc) return (sign_clear(dp) ? pos : neg) * dp;
-  if (mode == kDec) return (sign_clear(dm) ? pos : neg) * dm;
-  return flux(pos, neg, dm, dp);  // kLin never reaches here; kGen
-}
-
-__device__ __forceinline__ double flux_lin(double s, bool s_nonneg, double dm, double dp) {
-  return s * (s_nonneg ? dp : dm);
 }
 
 // ---- mbarrier / bulk-tensor primitives (PTX ISA 8.x; TMA engine) ----
@@ -173,6 +118,47 @@ __device__ __forceinline__ double lds1(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
+}
+
+// solve() loop logic after a sweep (solver.cpp:347-369): residual, histories,
+// convergence, the 10x divergence guard, max_iters / horizon; resets the
+// sweep accumulators and clears the graph's WHILE condition when done.
+__device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
+  const double max_dv = __longlong_as_double(atomicAdd(&st->maxdv_bits, 0ull));
+  const double residual = max_dv / st->dt;
+  const long long iter = st->iter + 1;
+  st->iter = iter;
+  if (iter - 1 < st->history_cap) {
+    if (st->history) st->history[iter - 1] = residual;
+    if (st->wall_history)
+      st->wall_history[iter - 1] = (double)(globaltimer_ns4() - st->t0_ns) * 1e-6;
+  }
+  st->last_residual = residual;
+  bool stop = false;
+  if (residual < st->tol) {
+    st->converged = 1;
+    stop = true;
+  } else {
+    if (iter == 1) st->first_residual = residual;
+    const double mr0 = st->min_residual;
+    const double mr = residual < mr0 ? residual : mr0;  // std::min(min_residual, residual)
+    st->min_residual = mr;
+    const double first = st->first_residual;
+    const double base = mr < first ? first : mr;  // std::max(min_residual, front)
+    if (!isfinite(residual) || residual > 10.0 * base) {
+      st->status = HJB_ERR_DIVERGED;
+      stop = true;
+    }
+  }
+  if (iter >= st->max_iters) stop = true;
+  if (st->horizon > 0.0 && (double)iter * st->dt >= st->horizon) stop = true;
+  st->maxdv_bits = 0ull;
+  st->blocks_done = 0u;
+  if (stop) {
+    st->done = 1;
+    if (use_handle) cudaGraphSetConditional(handle, 0u);
+  }
+  __threadfence();
 }
 
 constexpr int kRing = 4;  // planes in flight per ring (prefetch distance kRing - 1)
@@ -228,13 +214,14 @@ __global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
   const double* src;
   double* dst;
   const CUtensorMap* vmap;
-  if (a.loop) {
+  if (a.loop == 1) {  // device loop: buffer parity from the loop state
     if (*(volatile int*)&a.st->done) return;
     const long long it = a.st->iter;
     src = (it & 1) ? a.buf1 : a.buf0;
     dst = (it & 1) ? a.buf0 : a.buf1;
     vmap = (it & 1) ? &a.map1 : &a.map0;
-  } else {
+  } else {  // explicit buffers (single step, or a slab sweep of the sharded loop)
+    if (a.loop == 2 && *(volatile int*)&a.st->done) return;
     src = a.src;
     dst = a.dst;
     vmap = &a.map0;
@@ -257,8 +244,10 @@ __global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
   const uint32_t t2 = b % a.tiles2;
   const uint32_t t1 = b / a.tiles2;
   const uint32_t base1 = t1 * T1, base2 = t2 * T2;
-  const uint32_t c0 = chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, n0);
+  // planes [cbeg, cend) are updated; a plane outside the range (a slab's
+  // halo) is read as a neighbour, a missing one is the grid edge
+  const uint32_t c0 = a.cbeg + chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, a.cend);
   const uint64_t s2 = n3p;
   const uint64_t s1 = static_cast<uint64_t>(n2) * n3p;
   const uint64_t s0 = static_cast<uint64_t>(n1) * s1;
@@ -522,46 +511,19 @@ __global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
   if (lane != 0) return;
   LoopState* st = a.st;
   if (mbits) atomicMax(&st->maxdv_bits, mbits);
-  if (!a.loop) return;
+  if (a.loop != 1) return;  // single step / sharded: no fused epilogue
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  const double max_dv = __longlong_as_double(atomicAdd(&st->maxdv_bits, 0ull));
-  const double residual = max_dv / st->dt;
-  const long long iter = st->iter + 1;
-  st->iter = iter;
-  if (iter - 1 < st->history_cap) {
-    if (st->history) st->history[iter - 1] = residual;
-    if (st->wall_history)
-      st->wall_history[iter - 1] = (double)(globaltimer_ns4() - st->t0_ns) * 1e-6;
-  }
-  st->last_residual = residual;
-  bool stop = false;
-  if (residual < st->tol) {
-    st->converged = 1;
-    stop = true;
-  } else {
-    if (iter == 1) st->first_residual = residual;
-    const double mr0 = st->min_residual;
-    const double mr = residual < mr0 ? residual : mr0;
-    st->min_residual = mr;
-    const double first = st->first_residual;
-    const double base = mr < first ? first : mr;
-    if (!isfinite(residual) || residual > 10.0 * base) {
-      st->status = HJB_ERR_DIVERGED;
-      stop = true;
-    }
-  }
-  if (iter >= st->max_iters) stop = true;
-  if (st->horizon > 0.0 && (double)iter * st->dt >= st->horizon) stop = true;
-  st->maxdv_bits = 0ull;
-  st->blocks_done = 0u;
-  if (stop) {
-    st->done = 1;
-    if (a.use_handle) cudaGraphSetConditional(a.handle, 0u);
-  }
-  __threadfence();
+  loop_epilogue(st, a.handle, a.use_handle);
+}
+
+// Sharded loop: after the residual all-reduce, one thread applies the
+// solve() loop logic to the global max|dV| (every rank decides identically).
+__global__ void k_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
+  if (st->done) return;
+  loop_epilogue(st, handle, use_handle);
 }
 
 // padded <-> reference layout
@@ -673,17 +635,22 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   const uint32_t tiles = a.tiles1 * a.tiles2;
   uint32_t nch = 1;
   double best_cost = 1e30;
-  for (uint32_t k = 1; k <= 16 && k <= g.n[0]; ++k) {
+  if (a.cend == 0) {
+    a.cbeg = 0;
+    a.cend = g.n[0];
+  }
+  const uint32_t span = a.cend - a.cbeg;
+  for (uint32_t k = 1; k <= 16 && k <= span; ++k) {
     const uint32_t waves = (tiles * k + sms - 1) / sms;
-    const double cost = double(waves) * (double((g.n[0] + k - 1) / k) + 3.0);
+    const double cost = double(waves) * (double((span + k - 1) / k) + 3.0);
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
       nch = k;
     }
   }
-  uint32_t L = (g.n[0] + nch - 1) / nch;
+  uint32_t L = (span + nch - 1) / nch;
   a.L = L;
-  a.nchunks = (g.n[0] + L - 1) / L;
+  a.nchunks = (span + L - 1) / L;
   a.blocks = tiles * a.nchunks;
 }
 
@@ -740,6 +707,12 @@ cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const do
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
+                            cudaStream_t s) {
+  k_epilogue<<<1, 1, 0, s>>>(st, handle, use_handle);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,

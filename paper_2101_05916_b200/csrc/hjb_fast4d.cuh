@@ -20,6 +20,7 @@ struct Fast4dArgs {
   double inv[4];
   uint32_t kcells;  // cells per thread along the contiguous axis (2 or 4)
   uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads, consumers, smem;
+  uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
   const double* tab;
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
   const double* c;  // padded constraint
@@ -29,7 +30,7 @@ struct Fast4dArgs {
   double* dst;
   LoopState* st;
   double dt;
-  int loop;
+  int loop;  // 0 single step, 1 device loop (fused epilogue), 2 sharded slab sweep
   cudaGraphConditionalHandle handle;
   int use_handle;
 };
@@ -42,6 +43,8 @@ cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
 // Encode the three TMA tensor maps for the padded buffers (driver entry point
 // fetched through the runtime; no libcuda link dependency).
 cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const double* c);
+cudaError_t launch_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
+                            cudaStream_t s);
 cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,
                         cudaStream_t s);
 cudaError_t launch_unpad4(const double* in, double* out, uint64_t rows, uint32_t n3,

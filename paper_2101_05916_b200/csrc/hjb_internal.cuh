@@ -1,0 +1,41 @@
+// hjb_internal.cuh — host helpers shared by the C-ABI translation units
+// (hjb_capi.cu defines them; hjb_shard.cu uses them).
+#pragma once
+
+#include <vector>
+
+#include "hjb_common.cuh"
+#include "hjb_fast4d.cuh"
+
+namespace hjb {
+
+struct HostModel {
+  DevModel dm;
+  std::vector<double> tab;
+  bool separable = true;
+};
+
+struct Scan {
+  double max_speed_sum = 0.0;
+  double max_alpha[kMaxDims] = {0};
+};
+
+// grid / model / bounds validated and uploaded; shape = fast-path id or -1
+struct Prepared {
+  DevGrid g;
+  HostModel hm;
+  int shape = -1;
+};
+
+int make_grid(const hjb_grid* gi, DevGrid& g);
+int make_model(const hjb_model* mi, const hjb_dbounds* db, const DevGrid& g, HostModel& hm);
+int validate_cfg(const hjb_solve_config* cfg);
+int upload_model(hjb_context* ctx, HostModel& hm);
+int run_scan(hjb_context* ctx, const DevGrid& g, const DevModel& m, Scan& out);
+// Godunov + constant bounds preparation for the 4D fast path
+int prepare(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const hjb_dbounds* db,
+            Prepared& p);
+void fill_tables(const Prepared& p, Fast4dArgs& f);
+inline int validate_config(const hjb_solve_config* cfg) { return validate_cfg(cfg); }
+
+}  // namespace hjb

@@ -1,0 +1,426 @@
+// hjb_shard.cu — multi-GPU slab partition of the 4D solve.
+//
+// One process per GPU.  Axis 0 (the slowest, so slabs are contiguous) is
+// split into balanced slabs; every rank keeps its slab plus one halo plane
+// per interior side in the padded layout of k_fast4d.  Per sweep:
+//   1. halo exchange of the first/last owned planes with the neighbours
+//      (ncclSend/ncclRecv in one group);
+//   2. k_fast4d over the owned planes (loop mode 2: halo planes are read as
+//      neighbours, the global edges keep the reference's zero ghost rule);
+//   3. ncclAllReduce(max) of the sweep's max|dV| bits (non-negative doubles
+//      order like uint64);
+//   4. k_epilogue: the solve() loop logic on the global max, identical on
+//      every rank, so all ranks stop at the same sweep.
+// The whole loop is one CUDA graph with a WHILE node; the body holds an even
+// number of sweeps with fixed buffers (NCCL needs fixed pointers), which the
+// parity of the loop state matches because the loop starts at iteration 0.
+// A Jacobi sweep reads only the previous iterate, so the slab result is
+// bitwise identical to the single-GPU solve.
+//
+// NCCL is loaded with dlopen at communicator creation, so libhjb.so carries
+// no hard dependency on it (single-GPU use never loads it).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "../../include/hjb.h"
+#include "hjb_common.cuh"
+#include "hjb_fast4d.cuh"
+#include "hjb_internal.cuh"
+#include "hjb_kernels.cuh"
+
+namespace hjb {
+namespace {
+
+// minimal NCCL ABI (nccl.h 2.x)
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclUint64_ = 5, ncclFloat64_ = 8 };
+enum { ncclMax_ = 2 };
+
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) =
+      nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl* nccl() {
+  static Nccl api;
+  static bool tried = false;
+  if (tried) return api.h ? &api : nullptr;
+  tried = true;
+  for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+    api.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) break;
+  }
+  if (!api.h) return nullptr;
+#define SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))
+  SYM(GetUniqueId);
+  SYM(CommInitRank);
+  SYM(CommDestroy);
+  SYM(GroupStart);
+  SYM(GroupEnd);
+  SYM(Send);
+  SYM(Recv);
+  SYM(AllReduce);
+  SYM(GetErrorString);
+#undef SYM
+  if (!api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.AllReduce) {
+    api.h = nullptr;
+    return nullptr;
+  }
+  return &api;
+}
+
+#define NCCL_TRY(expr)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (expr);                                                            \
+    if (r_ != 0)                                                                         \
+      return set_err(HJB_ERR_NCCL, std::string(#expr " failed: ") +                      \
+                                       (nccl()->GetErrorString ? nccl()->GetErrorString(r_) \
+                                                               : "nccl error"));         \
+  } while (0)
+
+}  // namespace
+}  // namespace hjb
+
+struct hjb_comm {
+  hjb::ncclComm_t comm = nullptr;
+  int nranks = 1;
+  int rank = 0;
+};
+
+using namespace hjb;
+
+extern "C" {
+
+int hjb_slab_partition(int64_t n0, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || n0 < nranks)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "slab_partition: need 0 <= rank < nranks <= n0");
+  const int64_t base = n0 / nranks, extra = n0 % nranks;
+  *begin = rank * base + (rank < extra ? rank : extra);
+  *end = *begin + base + (rank < extra ? 1 : 0);
+  return HJB_OK;
+}
+
+int hjb_nccl_unique_id(void* out) {
+  Nccl* api = nccl();
+  if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  NCCL_TRY(api->GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof id);
+  return HJB_OK;
+}
+
+int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* unique_id,
+                    hjb_comm** out) {
+  if (!ctx || !out || !unique_id) return set_err(HJB_ERR_INVALID_ARGUMENT, "comm_create: null");
+  Nccl* api = nccl();
+  if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof id);
+  hjb_comm* c = new hjb_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  const ncclResult_t r = api->CommInitRank(&c->comm, nranks, id, rank);
+  if (r != 0) {
+    delete c;
+    return set_err(HJB_ERR_NCCL, std::string("ncclCommInitRank failed: ") +
+                                     (api->GetErrorString ? api->GetErrorString(r) : ""));
+  }
+  *out = c;
+  return HJB_OK;
+}
+
+int hjb_comm_destroy(hjb_comm* c) {
+  if (!c) return HJB_OK;
+  if (c->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(c->comm);
+  delete c;
+  return HJB_OK;
+}
+
+// One sweep over planes [plane_begin, plane_end) of a full 4D grid (device
+// pointers, reference layout): the slab computation of rank r on one device.
+// Writes only those planes of `out` and the slab's max|dV| to *max_dv.
+int hjb_sweep_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
+                         const hjb_dbounds* db, const double* value, const double* constraint,
+                         int64_t plane_begin, int64_t plane_end, double dt, double* out,
+                         double* max_dv) {
+  int rc;
+  if (!ctx) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: null");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Prepared p;
+  if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
+  if (p.shape < 0)
+    return set_err(HJB_ERR_UNSUPPORTED, "sweep_planes: model/grid outside the 4D fast path");
+  if (plane_begin < 0 || plane_end > p.g.n[0] || plane_begin >= plane_end)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "sweep_planes: bad plane range");
+  Fast4dArgs f;
+  std::memset(&f, 0, sizeof f);
+  f.kcells = 2;
+  f.cbeg = static_cast<uint32_t>(plane_begin);
+  f.cend = static_cast<uint32_t>(plane_end);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  fast4d_config(p.g, sms > 0 ? sms : 148, f);
+  const uint64_t rows = static_cast<uint64_t>(p.g.n[0]) * p.g.n[1] * p.g.n[2];
+  const size_t pb = rows * f.n3p * sizeof(double);
+  DevBuf a, bbuf, cb;
+  CUDA_TRY(a.ensure(pb));
+  CUDA_TRY(bbuf.ensure(pb));
+  CUDA_TRY(cb.ensure(pb));
+  CUDA_TRY(launch_pad4(value, a.d(), rows, p.g.n[3], f.n3p, ctx->stream));
+  CUDA_TRY(launch_pad4(constraint, cb.d(), rows, p.g.n[3], f.n3p, ctx->stream));
+  CUDA_TRY(launch_pad4(value, bbuf.d(), rows, p.g.n[3], f.n3p, ctx->stream));
+  fill_tables(p, f);
+  f.c = cb.d();
+  f.buf0 = a.d();
+  f.buf1 = bbuf.d();
+  f.src = a.d();
+  f.dst = bbuf.d();
+  CUDA_TRY(fast4d_make_maps(f, a.d(), bbuf.d(), cb.d()));
+  f.st = ctx->st;
+  f.dt = dt;
+  f.loop = 0;
+  CUDA_TRY(cudaMemsetAsync(ctx->st, 0, sizeof(LoopState), ctx->stream));
+  CUDA_TRY(launch_fast4d(f, p.shape, ctx->stream));
+  CUDA_TRY(launch_unpad4(bbuf.d(), out, rows, p.g.n[3], f.n3p, ctx->stream));
+  ctx->launches += 5;
+  unsigned long long bits = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bits, &ctx->st->maxdv_bits, sizeof bits, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(max_dv, &bits, sizeof bits);
+  return HJB_OK;
+}
+
+int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
+                          const hjb_model* mi, const hjb_dbounds* db, const double* init_slab,
+                          const double* c_slab, const hjb_solve_config* cfg,
+                          double* value_slab_out, hjb_solve_result* res) {
+  int rc;
+  if (!ctx || !comm) return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_sharded: null context/comm");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  if ((rc = validate_config(cfg))) return rc;
+  Prepared p;
+  if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
+  if (p.shape < 0)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
+  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: first-order Euler only");
+  Nccl* api = nccl();
+  if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
+  const int P = comm->nranks, r = comm->rank;
+  int64_t slab_b, slab_e;
+  if ((rc = hjb_slab_partition(p.g.n[0], P, r, &slab_b, &slab_e))) return rc;
+  const uint32_t owned = static_cast<uint32_t>(slab_e - slab_b);
+  const bool has_lo = r > 0, has_hi = r < P - 1;
+  const uint32_t nloc = owned + (has_lo ? 1 : 0) + (has_hi ? 1 : 0);
+
+  // CFL scan over the slab + all-reduce(max): rows of the fast path never
+  // depend on x0, so the slab's local grid gives the global values
+  DevGrid gl = p.g;
+  gl.n[0] = owned;
+  gl.size = owned * gl.stride[0];
+  gl.divs[0].init(owned);
+  Scan s;
+  if ((rc = run_scan(ctx, gl, p.hm.dm, s))) return rc;
+  {
+    unsigned long long bits[1 + kMaxDims];
+    std::memcpy(bits, &s.max_speed_sum, sizeof(double));
+    std::memcpy(bits + 1, s.max_alpha, kMaxDims * sizeof(double));
+    unsigned long long* dbits = reinterpret_cast<unsigned long long*>(ctx->scratch.d());
+    CUDA_TRY(cudaMemcpyAsync(dbits, bits, sizeof bits, cudaMemcpyHostToDevice, ctx->stream));
+    NCCL_TRY(api->AllReduce(dbits, dbits, 1 + kMaxDims, ncclUint64_, ncclMax_, comm->comm,
+                            ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(bits, dbits, sizeof bits, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(&s.max_speed_sum, bits, sizeof(double));
+  }
+  if (!(s.max_speed_sum > 0.0))
+    return set_err(HJB_ERR_RUNTIME, "solve: flow is identically zero on the grid");
+  const double dt = cfg->cfl_factor / s.max_speed_sum;
+  hjb_solve_result local;
+  std::memset(&local, 0, sizeof local);
+  if (!res) res = &local;
+  res->dt = dt;
+  res->nodes_per_sweep = p.g.size;
+  res->iterations = 0;
+  res->converged = 0;
+  if (cfg->max_iters == 0) {
+    CUDA_TRY(cudaMemcpyAsync(value_slab_out, init_slab,
+                             static_cast<size_t>(owned) * p.g.stride[0] * sizeof(double),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return HJB_OK;
+  }
+
+  // local padded slab arrays: [halo_lo?][owned][halo_hi?]
+  DevGrid gloc = p.g;
+  gloc.n[0] = nloc;
+  Fast4dArgs f;
+  std::memset(&f, 0, sizeof f);
+  f.kcells = 2;
+  f.cbeg = has_lo ? 1u : 0u;
+  f.cend = f.cbeg + owned;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  fast4d_config(gloc, sms > 0 ? sms : 148, f);
+  const uint64_t plane = static_cast<uint64_t>(p.g.n[1]) * p.g.n[2] * f.n3p;  // padded plane
+  const uint64_t rows_owned = static_cast<uint64_t>(owned) * p.g.n[1] * p.g.n[2];
+  const size_t lbytes = static_cast<size_t>(nloc) * plane * sizeof(double);
+  CUDA_TRY(ctx->v2.ensure(lbytes));
+  CUDA_TRY(ctx->v3.ensure(lbytes));
+  CUDA_TRY(ctx->pcbuf.ensure(lbytes));
+  CUDA_TRY(cudaMemsetAsync(ctx->v2.p, 0, lbytes, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->v3.p, 0, lbytes, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->pcbuf.p, 0, lbytes, ctx->stream));
+  double* own0 = ctx->v2.d() + f.cbeg * plane;
+  CUDA_TRY(launch_pad4(init_slab, own0, rows_owned, p.g.n[3], f.n3p, ctx->stream));
+  CUDA_TRY(launch_pad4(c_slab, ctx->pcbuf.d() + f.cbeg * plane, rows_owned, p.g.n[3], f.n3p,
+                       ctx->stream));
+  ctx->launches += 2;
+  fill_tables(p, f);
+  f.c = ctx->pcbuf.d();
+  f.buf0 = ctx->v2.d();
+  f.buf1 = ctx->v3.d();
+  CUtensorMap map_b0, map_b1;
+  CUDA_TRY(fast4d_make_maps(f, f.buf0, f.buf1, f.c));
+  map_b0 = f.map0;
+  map_b1 = f.map1;
+  f.st = ctx->st;
+  f.dt = dt;
+  f.loop = 2;
+
+  const long long cap =
+      std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
+  CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
+  CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
+  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
+                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
+                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
+  ++ctx->launches;
+  unsigned long long* maxbits = &ctx->st->maxdv_bits;
+  const size_t pe = static_cast<size_t>(plane);
+  // one sweep at a fixed buffer parity: exchange, sweep, all-reduce, epilogue
+  auto sweep = [&](int k, cudaGraphConditionalHandle h, int use) -> int {
+    double* src = (k & 1) ? f.buf1 : f.buf0;
+    double* dst = (k & 1) ? f.buf0 : f.buf1;
+    if (P > 1) {
+      NCCL_TRY(api->GroupStart());
+      if (has_lo) {
+        NCCL_TRY(api->Send(src + f.cbeg * pe, pe, ncclFloat64_, r - 1, comm->comm, ctx->stream));
+        NCCL_TRY(api->Recv(src, pe, ncclFloat64_, r - 1, comm->comm, ctx->stream));
+      }
+      if (has_hi) {
+        NCCL_TRY(api->Send(src + (f.cend - 1) * pe, pe, ncclFloat64_, r + 1, comm->comm,
+                           ctx->stream));
+        NCCL_TRY(api->Recv(src + f.cend * pe, pe, ncclFloat64_, r + 1, comm->comm, ctx->stream));
+      }
+      NCCL_TRY(api->GroupEnd());
+    }
+    Fast4dArgs x = f;
+    x.src = src;
+    x.dst = dst;
+    x.map0 = (k & 1) ? map_b1 : map_b0;
+    CUDA_TRY(launch_fast4d(x, p.shape, ctx->stream));
+    NCCL_TRY(api->AllReduce(maxbits, maxbits, 1, ncclUint64_, ncclMax_, comm->comm, ctx->stream));
+    CUDA_TRY(launch_epilogue(ctx->st, h, use, ctx->stream));
+    return HJB_OK;
+  };
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, ctx->stream));
+  const int body = 8;  // even: buffer parity of position k == iteration parity
+  const char* mode = std::getenv("HJB_LOOP");
+  if (mode && std::strcmp(mode, "poll") == 0) {
+    for (;;) {
+      for (int k = 0; k < body; ++k)
+        if ((rc = sweep(k, 0, 0))) return rc;
+      CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      if (ctx->st_host->done) break;
+    }
+  } else {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CUDA_TRY(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle handle;
+    rc = HJB_OK;
+    do {
+      cudaError_t e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = handle;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+      e = cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr,
+                                        nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+      for (int k = 0; k < body && rc == HJB_OK; ++k) rc = sweep(k, handle, 1);
+      cudaGraph_t captured = nullptr;
+      e = cudaStreamEndCapture(ctx->stream, &captured);
+      if (rc) break;
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+      e = cudaGraphLaunch(exec, ctx->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+    } while (0);
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const LoopState& st = *ctx->st_host;
+  ctx->launches += 2 * (st.iter + body);
+  res->iterations = st.iter;
+  res->converged = st.converged;
+  res->final_residual = st.last_residual;
+  res->wall_seconds = ms * 1e-3;
+  const long long nh = std::min<long long>(st.iter, res->history_capacity);
+  if (nh > 0 && res->residual_history)
+    CUDA_TRY(cudaMemcpyAsync(res->residual_history, ctx->hist.p, nh * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  if (nh > 0 && res->wall_ms_history)
+    CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  const double* fin = ((st.iter & 1) ? f.buf1 : f.buf0) + f.cbeg * pe;
+  CUDA_TRY(launch_unpad4(fin, value_slab_out, rows_owned, p.g.n[3], f.n3p, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (st.status == HJB_ERR_DIVERGED)
+    return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+  return HJB_OK;
+}
+
+}  // extern "C"
