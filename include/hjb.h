@@ -138,8 +138,12 @@ typedef struct hjb_solve_config {
   int32_t time_order;    /* 1 = forward Euler (reference); 2/3 = TVD-RK */
   double time_horizon;   /* > 0: also stop once iterations*dt >= horizon */
   int32_t threads;       /* reference CPU knob; accepted and ignored */
-  int32_t flags;         /* reserved, 0 */
+  int32_t flags;         /* HJB_FLAG_* (0 by default) */
 } hjb_solve_config;
+
+/* run the ENO/TVD-RK stage machinery even for order 1 / Euler (verification:
+ * it must reproduce the reference update bit for bit) */
+#define HJB_FLAG_FORCE_HO 1
 
 /* SolveResult, reference solver.hpp:27-36.  The value field is written to
  * the caller's buffer; histories are written to caller buffers of

@@ -514,7 +514,7 @@ int hjo_solve(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, con
   res->nodes_per_sweep = g.size;
   res->converged = 0;
   res->iterations = 0;
-  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+  if (cfg->spatial_order > 1 || cfg->time_order > 1 || (cfg->flags & HJB_FLAG_FORCE_HO))
     return hjo_ho_solve(&g, m, db, init, c, cfg, &s, dt, out, res);
   const double* ga = cfg->dissipation == HJB_GLOBAL ? s.max_alpha : NULL;
   const int godunov = cfg->scheme == HJB_GODUNOV;
@@ -871,11 +871,204 @@ int hjo_flow_bounds(const hjb_model* m, const double* x, const hjb_interval* db,
 }
 
 /* ------------------------------------------- high order (no reference) */
-/* Placeholder until the ENO/TVD-RK restatement lands. */
+/* ENO2/ENO3 spatial derivatives + TVD-RK2/RK3 (Shu-Osher) time stepping.
+ * PARITY UNPINNED: the reference has no high-order scheme.
+ * Definitions (shared bit for bit with the device kernel k_ho_stage):
+ *  a(j) = (V[j+1] - V[j]) * inv_dx              (j = left node of the face)
+ *  ghost faces (j < 0 or j > n-2): Godunov 0.0 (the reference's zero ghost
+ *    difference, solver.cpp:141-147); LF the nearest interior face (the
+ *    reference's replicated one-sided difference)
+ *  d2(j) = a(j) - a(j-1);  d3(j) = d2(j+1) - d2(j);  minabs(x,y) = |x|<=|y| ? x : y
+ *  ENO1: D- = a(k-1), D+ = a(k)
+ *  ENO2: D- = a(k-1) + 0.5*minabs(d2(k-1), d2(k))
+ *        D+ = a(k)  + (-0.5)*minabs(d2(k), d2(k+1))
+ *  ENO3 (Osher & Fedkiw, Level Set Methods, sec. 3.3, base K = k-1 for D-,
+ *        K = k for D+): pick c2 = minabs(d2(K), d2(K+1)) with ks = K-1 when
+ *        d2(K) wins else K; c3 = minabs(d3(ks), d3(ks+1));
+ *        D = (a(K) + s2*c2) + w(k-ks)*c3, s2 = +0.5 (D-) / -0.5 (D+),
+ *        w(0) = w(2) = 1/3, w(1) = -1/6
+ *  The numerical Hamiltonian is the reference's (Godunov or LF) applied to
+ *  (D-, D+).  Stages: s = Vs + dt*Hhat(Vs); Euler/first stage V1 = max(c, s);
+ *  RK2 final max(c, 0.5*V + 0.5*s); RK3 second max(c, 0.75*V + 0.25*s),
+ *  final max(c, (1/3)*V + (2/3)*s): the VI clamp after every stage.
+ *  Residual = max|V_{n+1} - V_n| / dt.  ENO1 + Euler reproduces the
+ *  reference update bit for bit (tested). */
+
+static const double kThird = 1.0 / 3.0;
+static const double kTwoThirds = 2.0 / 3.0;
+static const double kSixthNeg = -1.0 / 6.0;
+
+static inline double minabs(double x, double y) { return fabs(x) <= fabs(y) ? x : y; }
+
+/* face difference a(j) along axis d for the node at linear index lin whose
+ * axis-d index is k */
+static inline double face(const double* v, int64_t lin, int64_t stride, int64_t k, int64_t n,
+                          int64_t j, double inv, int godunov) {
+  if (j < 0 || j > n - 2) {
+    if (godunov || n < 2) return 0.0;
+    j = j < 0 ? 0 : n - 2;
+  }
+  const double* p = v + lin + (j - k) * stride;
+  return (p[stride] - p[0]) * inv;
+}
+
+static inline void eno_pair(const double* v, int64_t lin, int64_t stride, int64_t k, int64_t n,
+                            double inv, int godunov, int order, double* dm, double* dp) {
+  if (order <= 1) {
+    *dm = face(v, lin, stride, k, n, k - 1, inv, godunov);
+    *dp = face(v, lin, stride, k, n, k, inv, godunov);
+    return;
+  }
+  double a[6]; /* a(k-3) .. a(k+2) */
+  for (int t = 0; t < 6; ++t) a[t] = face(v, lin, stride, k, n, k - 3 + t, inv, godunov);
+#define A(j) a[(j) - (k - 3)]
+#define D2(j) (A(j) - A((j) - 1))
+  if (order == 2) {
+    *dm = A(k - 1) + 0.5 * minabs(D2(k - 1), D2(k));
+    *dp = A(k) + -0.5 * minabs(D2(k), D2(k + 1));
+  } else {
+    for (int side = 0; side < 2; ++side) {
+      const int64_t K = side == 0 ? k - 1 : k;
+      const double x = D2(K), y = D2(K + 1);
+      const int left = fabs(x) <= fabs(y);
+      const double c2 = left ? x : y;
+      const int64_t ks = left ? K - 1 : K;
+      const double c3 = minabs(D2(ks + 1) - D2(ks), D2(ks + 2) - D2(ks + 1));
+      const int64_t mm = k - ks;
+      const double w = mm == 1 ? kSixthNeg : kThird;
+      const double s2 = side == 0 ? 0.5 : -0.5;
+      const double d = (A(K) + s2 * c2) + w * c3;
+      if (side == 0) *dm = d; else *dp = d;
+    }
+  }
+#undef D2
+#undef A
+}
+
+/* one RK stage over the whole grid; kind: 0 V1 = max(c, s), 1 RK2 final,
+ * 2 RK3 second, 3 RK3 final.  Returns max|out - vn| (meaningful for the
+ * final stage). */
+static double ho_stage(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
+                       const double* inv, int godunov, const double* global_alpha, int order,
+                       const double* vs, const double* vn, const double* c, double dt, int kind,
+                       double* out) {
+  const int nd = g->nd;
+  const int64_t nchunks = (g->size + CHUNK - 1) / CHUNK;
+  double best = 0.0;
+#pragma omp parallel num_threads(nthreads())
+  {
+    double lbest = 0.0;
+#pragma omp for schedule(static)
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      const int64_t lo = ch * CHUNK;
+      const int64_t hi = lo + CHUNK < g->size ? lo + CHUNK : g->size;
+      int64_t idx[HJB_MAX_DIMS];
+      double x[HJB_MAX_STATE], dminus[HJB_MAX_STATE], dplus[HJB_MAX_STATE];
+      double costate[HJB_MAX_STATE], alpha[HJB_MAX_STATE];
+      slopes_t slopes[HJB_MAX_STATE];
+      hjb_interval dbn[HJB_MAX_INPUT];
+      affine_t af;
+      unravel(g, lo, idx);
+      for (int64_t lin = lo; lin < hi; ++lin) {
+        for (int d = 0; d < nd; ++d) x[d] = coord(g, d, idx[d]);
+        for (int d = 0; d < nd; ++d)
+          eno_pair(vs, lin, g->stride[d], idx[d], g->n[d], inv[d], godunov, order, &dminus[d],
+                   &dplus[d]);
+        db_at(db, lin, dbn);
+        model_affine(m, x, idx, &af);
+        double hhat = 0.0;
+        if (godunov) {
+          dim_slopes(&af, m->ubounds, dbn, slopes);
+          for (int d = 0; d < nd; ++d) hhat += godunov_flux(slopes[d], dminus[d], dplus[d]);
+        } else {
+          for (int d = 0; d < nd; ++d) costate[d] = 0.5 * (dminus[d] + dplus[d]);
+          hhat = hamiltonian(&af, costate, m->ubounds, dbn);
+          if (!global_alpha) {
+            flow_bounds(&af, m->ubounds, dbn, alpha);
+            for (int d = 0; d < nd; ++d) hhat += alpha[d] * 0.5 * (dplus[d] - dminus[d]);
+          } else {
+            for (int d = 0; d < nd; ++d) hhat += global_alpha[d] * 0.5 * (dplus[d] - dminus[d]);
+          }
+        }
+        const double st = vs[lin] + dt * hhat;
+        double val;
+        switch (kind) {
+          case 1: val = 0.5 * vn[lin] + 0.5 * st; break;
+          case 2: val = 0.75 * vn[lin] + 0.25 * st; break;
+          case 3: val = kThird * vn[lin] + kTwoThirds * st; break;
+          default: val = st; break;
+        }
+        const double cl = val > c[lin] ? val : c[lin];
+        out[lin] = cl;
+        const double dv = fabs(cl - vn[lin]);
+        if (dv > lbest) lbest = dv;
+        odometer(g, idx);
+      }
+    }
+#pragma omp critical
+    if (lbest > best) best = lbest;
+  }
+  return best;
+}
+
 int hjo_ho_solve(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, const double* init,
                  const double* c, const hjb_solve_config* cfg, const hjo_scan* s, double dt,
                  double* out, hjb_solve_result* res) {
-  (void)g; (void)m; (void)db; (void)init; (void)c; (void)cfg; (void)s; (void)dt; (void)out;
-  (void)res;
-  return fail(HJB_ERR_UNSUPPORTED, "solve: spatial/time order > 1 not available yet");
+  const int order = cfg->spatial_order < 1 ? 1 : cfg->spatial_order;
+  const int rk = cfg->time_order < 1 ? 1 : cfg->time_order;
+  if (order > 3 || rk > 3) return fail(HJB_ERR_INVALID_ARGUMENT, "SolveConfig: order must be 1..3");
+  const double* ga = cfg->dissipation == HJB_GLOBAL ? s->max_alpha : NULL;
+  const int godunov = cfg->scheme == HJB_GODUNOV;
+  double inv[HJB_MAX_DIMS];
+  for (int d = 0; d < g->nd; ++d) inv[d] = 1.0 / g->spacing[d];
+  const size_t bytes = g->size * sizeof(double);
+  double* front = (double*)malloc(bytes);
+  double* back = (double*)malloc(bytes);
+  double* s1 = (double*)malloc(bytes);
+  double* s2 = (double*)malloc(bytes);
+  memcpy(front, init, bytes);
+  const double t0 = now_ms();
+  double min_residual = INFINITY, first = 0.0, residual = 0.0;
+  int status = 0;
+  for (int64_t iter = 1; iter <= cfg->max_iters; ++iter) {
+    double max_dv;
+    if (rk == 1) {
+      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, dt, 0, back);
+    } else if (rk == 2) {
+      ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, dt, 0, s1);
+      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, s1, front, c, dt, 1, back);
+    } else {
+      ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, dt, 0, s1);
+      ho_stage(g, m, db, inv, godunov, ga, order, s1, front, c, dt, 2, s2);
+      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, s2, front, c, dt, 3, back);
+    }
+    residual = max_dv / dt;
+    double* t = front;
+    front = back;
+    back = t;
+    res->iterations = iter;
+    if (iter == 1) first = residual;
+    if (res->residual_history && iter <= res->history_capacity)
+      res->residual_history[iter - 1] = residual;
+    if (res->wall_ms_history && iter <= res->history_capacity)
+      res->wall_ms_history[iter - 1] = now_ms() - t0;
+    if (residual < cfg->tolerance) {
+      res->converged = 1;
+      break;
+    }
+    min_residual = STD_MIN(min_residual, residual);
+    if (!isfinite(residual) || residual > 10.0 * STD_MAX(min_residual, first)) {
+      status = fail(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+      break;
+    }
+    if (cfg->time_horizon > 0.0 && (double)iter * dt >= cfg->time_horizon) break;
+  }
+  res->final_residual = residual;
+  memcpy(out, front, bytes);
+  res->wall_seconds = (now_ms() - t0) * 1e-3;
+  free(front);
+  free(back);
+  free(s1);
+  free(s2);
+  return status;
 }

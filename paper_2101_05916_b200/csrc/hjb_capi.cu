@@ -311,7 +311,6 @@ int scheme_of(const hjb_solve_config* cfg) {
 // Loop driver: WHILE-conditional CUDA graph whose body is `body` sweeps, or
 // (HJB_LOOP=poll) chunks of sweeps with a host poll of the device `done`
 // flag.  `launch(stream, handle, use_handle)` enqueues one sweep in loop mode.
-using SweepLauncher = std::function<cudaError_t(cudaStream_t, cudaGraphConditionalHandle, int)>;
 
 int run_loop(hjb_context* ctx, const SweepLauncher& launch, int body) {
   const char* mode = std::getenv("HJB_LOOP");
@@ -476,7 +475,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   res->iterations = 0;
   res->final_residual = 0.0;
 
-  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+  if (cfg->spatial_order > 1 || cfg->time_order > 1 || (cfg->flags & HJB_FLAG_FORCE_HO))
     return ho_solve(ctx, g, hm.dm, init, c, cfg, dt, s.max_alpha, value_out, res);
 
   if (cfg->max_iters == 0) {
@@ -756,7 +755,7 @@ int hjb_vi_step_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   if (cfg->scheme == HJB_GODUNOV && !hm.separable)
     return set_err(HJB_ERR_INVALID_ARGUMENT,
                    "vi_step: model inputs are not row-separable, use the Lax-Friedrichs scheme");
-  if (cfg->spatial_order > 1 || cfg->time_order > 1)
+  if (cfg->spatial_order > 1 || cfg->time_order > 1 || (cfg->flags & HJB_FLAG_FORCE_HO))
     return ho_vi_step(ctx, g, hm.dm, value, constraint, cfg, dt, s.max_alpha, out);
   StepArgs a = base_args(g, hm.dm, constraint, dt, scheme_of(cfg), s);
   a.st = ctx->st;

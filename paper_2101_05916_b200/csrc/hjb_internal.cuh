@@ -2,6 +2,7 @@
 // (hjb_capi.cu defines them; hjb_shard.cu uses them).
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "hjb_common.cuh"
@@ -36,6 +37,11 @@ int run_scan(hjb_context* ctx, const DevGrid& g, const DevModel& m, Scan& out);
 int prepare(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const hjb_dbounds* db,
             Prepared& p);
 void fill_tables(const Prepared& p, Fast4dArgs& f);
+// Device iteration loop: WHILE-conditional CUDA graph (or HJB_LOOP=poll);
+// `launch(stream, handle, use_handle)` enqueues one loop-mode sweep.
+using SweepLauncher = std::function<cudaError_t(cudaStream_t, cudaGraphConditionalHandle, int)>;
+int run_loop(hjb_context* ctx, const SweepLauncher& launch, int body);
+int sm_count(int device);
 inline int validate_config(const hjb_solve_config* cfg) { return validate_cfg(cfg); }
 
 }  // namespace hjb

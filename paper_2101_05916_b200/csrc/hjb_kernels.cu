@@ -304,6 +304,135 @@ __global__ void __launch_bounds__(kThreads) k_step(const __grid_constant__ StepA
   finish_sweep(a, local);
 }
 
+// ---------------------------------------------------------------- K6
+// ENO2/ENO3 + TVD-RK stages.  No reference; the definitions are
+// the repo's CPU restatement's (oracle/hj_oracle.c, "high order" section),
+// reproduced operation for operation.
+constexpr double kThird = 1.0 / 3.0;
+constexpr double kTwoThirds = 2.0 / 3.0;
+constexpr double kSixthNeg = -1.0 / 6.0;
+
+__device__ __forceinline__ double minabs(double x, double y) { return fabs(x) <= fabs(y) ? x : y; }
+
+// face difference a(j) = (V[j+1] - V[j]) * inv along one axis; ghost faces:
+// Godunov 0.0, LF the nearest interior face
+template <bool GODUNOV>
+__device__ __forceinline__ double face(const double* __restrict__ v, uint32_t lin, uint32_t stride,
+                                       int k, int n, int j, double inv) {
+  if (j < 0 || j > n - 2) {
+    if (GODUNOV) return 0.0;
+    j = j < 0 ? 0 : n - 2;
+  }
+  const double* p = v + lin + (long long)(j - k) * (long long)stride;
+  return (p[stride] - p[0]) * inv;
+}
+
+template <bool GODUNOV>
+__device__ __forceinline__ void eno_pair(const double* __restrict__ v, uint32_t lin,
+                                         uint32_t stride, int k, int n, double inv, int ORDER,
+                                         double& dm, double& dp) {
+  if (ORDER <= 1) {
+    dm = face<GODUNOV>(v, lin, stride, k, n, k - 1, inv);
+    dp = face<GODUNOV>(v, lin, stride, k, n, k, inv);
+    return;
+  }
+  double a[6];  // a(k-3) .. a(k+2)
+#pragma unroll
+  for (int t = 0; t < 6; ++t) a[t] = face<GODUNOV>(v, lin, stride, k, n, k - 3 + t, inv);
+  // index helpers relative to k: A(j) = a[j - k + 3], D2(j) = A(j) - A(j-1)
+#define A_(o) a[(o) + 3]
+#define D2_(o) (A_(o) - A_((o)-1))
+  if (ORDER == 2) {
+    dm = A_(-1) + 0.5 * minabs(D2_(-1), D2_(0));
+    dp = A_(0) + -0.5 * minabs(D2_(0), D2_(1));
+  } else {
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int K = side == 0 ? -1 : 0;  // relative to k
+      const double x = D2_(K), y = D2_(K + 1);
+      const bool left = fabs(x) <= fabs(y);
+      const double c2 = left ? x : y;
+      const int ks = left ? K - 1 : K;
+      double d3l, d3r;  // d3(ks), d3(ks+1)
+      if (left) {
+        d3l = D2_(K) - D2_(K - 1);
+        d3r = D2_(K + 1) - D2_(K);
+      } else {
+        d3l = D2_(K + 1) - D2_(K);
+        d3r = D2_(K + 2) - D2_(K + 1);
+      }
+      const double c3 = minabs(d3l, d3r);
+      const int mm = -ks;  // k - ks
+      const double w = mm == 1 ? kSixthNeg : kThird;
+      const double s2 = side == 0 ? 0.5 : -0.5;
+      const double d = (A_(K) + s2 * c2) + w * c3;
+      if (side == 0) dm = d; else dp = d;
+    }
+  }
+#undef D2_
+#undef A_
+}
+
+template <int ND, int SCHEME, bool PERNODE>
+__global__ void __launch_bounds__(kThreads) k_ho_stage(const __grid_constant__ StepArgs a) {
+  if (a.loop && *(volatile int*)&a.st->done) return;
+  const long long it = a.loop ? a.st->iter : 0;
+  const double* vn = a.loop ? ((it & 1) ? a.buf1 : a.buf0) : a.src;
+  double* outp = a.loop ? ((it & 1) ? a.buf0 : a.buf1) : a.dst;
+  const double* vs = a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2);
+  double* dst = a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2);
+  const DevGrid& g = a.g;
+  double local = 0.0;
+  for (uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x; lin < g.size;
+       lin += gridDim.x * blockDim.x) {
+    uint32_t idx[ND];
+    unravel<ND>(g, lin, idx);
+    double dm[ND], dp[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d)
+      eno_pair<SCHEME == kGodunov>(vs, lin, g.stride[d], (int)idx[d], (int)g.n[d],
+                                   g.inv_spacing[d], a.order, dm[d], dp[d]);
+    double hhat = 0.0;
+    if (SCHEME == kGodunov) {
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        double pos, neg;
+        row_slopes<ND, PERNODE>(a.m, a.m.row[d], idx, lin, pos, neg);
+        hhat += godunov_flux(pos, neg, dm[d], dp[d]);
+      }
+    } else {
+      double p[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) p[d] = 0.5 * (dm[d] + dp[d]);
+      hhat = lf_hamiltonian<ND, PERNODE>(a.m, p, idx, lin);
+      if (SCHEME == kLfPerNode) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const double al = row_alpha<ND, PERNODE>(a.m, a.m.row[d], idx, lin);
+          hhat += al * 0.5 * (dp[d] - dm[d]);
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) hhat += a.galpha[d] * 0.5 * (dp[d] - dm[d]);
+      }
+    }
+    const double st = vs[lin] + a.dt * hhat;
+    double val;
+    switch (a.kind) {
+      case 1: val = 0.5 * vn[lin] + 0.5 * st; break;
+      case 2: val = 0.75 * vn[lin] + 0.25 * st; break;
+      case 3: val = kThird * vn[lin] + kTwoThirds * st; break;
+      default: val = st; break;
+    }
+    const double cc = a.c[lin];
+    const double cl = val > cc ? val : cc;
+    dst[lin] = cl;
+    const double dv = fabs(cl - vn[lin]);
+    if (dv > local) local = dv;
+  }
+  if (a.final_stage) finish_sweep(a, local);
+}
+
 // K1: scan_alpha (solver.cpp:221-268)
 template <int ND, bool PERNODE>
 __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ DevGrid g,
@@ -516,6 +645,37 @@ cudaError_t launch_step(const StepArgs& a, cudaStream_t s) {
   HJB_DISPATCH_ND(a.g.nd, CALL)
 #undef CALL
   return cudaSuccess;
+}
+
+template <int ND>
+cudaError_t ho_nd(const StepArgs& a, cudaStream_t s) {
+  const dim3 grid = step_blocks(a.g.size);
+  const bool pn = a.m.per_node != 0;
+  switch (a.scheme) {
+    case kGodunov:
+      if (pn) k_ho_stage<ND, kGodunov, true><<<grid, kThreads, 0, s>>>(a);
+      else k_ho_stage<ND, kGodunov, false><<<grid, kThreads, 0, s>>>(a);
+      break;
+    case kLfPerNode:
+      if (pn) k_ho_stage<ND, kLfPerNode, true><<<grid, kThreads, 0, s>>>(a);
+      else k_ho_stage<ND, kLfPerNode, false><<<grid, kThreads, 0, s>>>(a);
+      break;
+    default:
+      if (pn) k_ho_stage<ND, kLfGlobal, true><<<grid, kThreads, 0, s>>>(a);
+      else k_ho_stage<ND, kLfGlobal, false><<<grid, kThreads, 0, s>>>(a);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ho_stage(const StepArgs& a, cudaStream_t s) {
+  switch (a.g.nd) {
+    case 1: return ho_nd<1>(a, s);
+    case 2: return ho_nd<2>(a, s);
+    case 3: return ho_nd<3>(a, s);
+    case 4: return ho_nd<4>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_scan(const DevGrid& g, const DevModel& m, double* out, cudaStream_t s) {

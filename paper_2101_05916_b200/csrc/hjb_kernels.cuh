@@ -25,7 +25,18 @@ struct StepArgs {
   int loop;          // 1: read parity/done from st and run the epilogue
   cudaGraphConditionalHandle handle;
   int use_handle;
+  // high-order stages (k_ho_stage): buffers and roles
+  double* stage1;
+  double* stage2;
+  int src_sel;      // 0: V_n (parity / src), 1: stage1, 2: stage2
+  int dst_sel;      // 0: V_{n+1} (parity / dst), 1: stage1, 2: stage2
+  int kind;         // 0 first stage, 1 RK2 final, 2 RK3 second, 3 RK3 final
+  int final_stage;  // run the max|dV| reduction / loop epilogue
+  int order;        // ENO order 1..3
 };
+
+// K6: one ENO/TVD-RK stage (generic rank; see hjb_kernels.cu).
+cudaError_t launch_ho_stage(const StepArgs& a, cudaStream_t s);
 
 // K1: alpha scan (solver.cpp:221-268).  out[0] = max_nodes sum_d alpha_d/dx_d,
 // out[1+d] = max_nodes alpha_d.  out must be zeroed by the caller.

@@ -738,6 +738,7 @@ class SolveConfig:
     spatial_order: int = 1
     time_order: int = 1
     time_horizon: float = 0.0
+    flags: int = 0  # HJB_FLAG_FORCE_HO = 1: ENO/RK machinery at order 1 (verification)
 
     def validate(self):
         if not (self.cfl_factor > 0.0) or self.cfl_factor > 1.0:
@@ -756,6 +757,7 @@ class SolveConfig:
         c.time_order = self.time_order
         c.time_horizon = self.time_horizon
         c.threads = self.threads
+        c.flags = self.flags
         return c
 
 
