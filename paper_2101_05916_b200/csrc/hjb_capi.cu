@@ -549,7 +549,20 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   CUDA_TRY(cudaEventCreate(&e1));
   CUDA_TRY(cudaEventRecord(e0, ctx->stream));
   const int body = 8;
-  rc = run_loop(ctx, launch, body);
+  // small 2D grids: the whole loop in one cluster launch (V in DSMEM)
+  const char* s2d = std::getenv("HJB_SMALL2D");
+  const bool small2d = shape < 0 && g.nd == 2 && !(s2d && std::strcmp(s2d, "0") == 0) &&
+                       small2d_smem(g, nullptr, nullptr) <= 200 * 1024;
+  if (small2d) {
+    StepArgs x = a;
+    x.src = ctx->v0.d();
+    x.dst = value_out;
+    cudaError_t e = launch_small2d(x, ctx->stream);
+    rc = e == cudaSuccess ? HJB_OK
+                          : set_err(HJB_ERR_CUDA, std::string("small2d: ") + cudaGetErrorString(e));
+  } else {
+    rc = run_loop(ctx, launch, body);
+  }
   if (rc) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -564,7 +577,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   const LoopState& st = *ctx->st_host;
-  ctx->launches += st.iter + body;  // sweeps run (+ early-exit tail of the body)
+  ctx->launches += small2d ? 1 : st.iter + body;  // sweeps (+ early-exit tail of the body)
   res->iterations = st.iter;
   res->converged = st.converged;
   res->final_residual = st.last_residual;
@@ -580,7 +593,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     const double* final_buf = (st.iter & 1) ? ctx->v3.d() : ctx->v2.d();
     CUDA_TRY(launch_unpad4(final_buf, value_out, rows, g.n[3], f.n3p, ctx->stream));
     ++ctx->launches;
-  } else {
+  } else if (!small2d) {
     const double* final_buf = (st.iter & 1) ? ctx->v1.d() : ctx->v0.d();
     CUDA_TRY(cudaMemcpyAsync(value_out, final_buf, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   }

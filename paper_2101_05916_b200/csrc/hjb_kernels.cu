@@ -589,6 +589,197 @@ __global__ void k_not_constant(const double* __restrict__ f, uint32_t n, unsigne
   if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
+// ------------------------------------------------------ small 2D grids
+// The whole solve() loop of a small 2D grid (config 1: 101^2) in ONE launch:
+// a thread-block cluster of up to 16 CTAs, each owning a band of axis-0 rows
+// of V (double-buffered) and c in shared memory; rows of the neighbouring
+// bands are read through distributed shared memory.  Per sweep: update, CTA
+// max, every CTA publishes its max into rank 0's slots (double-buffered by
+// sweep parity), one cluster barrier, then every CTA reduces the slots and
+// applies the solve() loop logic (solver.cpp:347-369) redundantly (identical
+// inputs, identical decisions); CTA 0 writes the histories.
+struct Small2dArgs {
+  StepArgs s;        // grid/model/c/dt/scheme/galpha; s.src = init, s.dst = out
+  uint32_t rows;     // axis-0 rows per CTA (last CTA may own fewer)
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctas() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ const double* map_rank(const double* p, uint32_t rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const double*>(out);
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
+template <int SCHEME, bool PERNODE>
+__global__ void __launch_bounds__(512, 1) k_small2d(const __grid_constant__ Small2dArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const StepArgs& p = a.s;
+  const DevGrid& g = p.g;
+  const uint32_t n0 = g.n[0], n1 = g.n[1];
+  const uint32_t R = a.rows;
+  const uint32_t me = cluster_ctarank(), nct = cluster_nctas();
+  const uint32_t r0 = me * R;
+  const uint32_t r1 = min(r0 + R, n0);
+  const uint32_t own = r1 > r0 ? (r1 - r0) * n1 : 0;
+  double* buf[2] = {sm, sm + R * n1};
+  double* cl = sm + 2 * R * n1;
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(sm + 3 * R * n1);  // [2][16]
+  __shared__ unsigned long long part[32];
+  __shared__ int s_done;
+  for (uint32_t t = threadIdx.x; t < own; t += blockDim.x) {
+    buf[0][t] = p.src[r0 * n1 + t];
+    cl[t] = p.c[r0 * n1 + t];
+  }
+  const double inv0 = g.inv_spacing[0], inv1 = g.inv_spacing[1];
+  // loop state (identical in every CTA)
+  long long iter = 0;
+  double min_res = __longlong_as_double(0x7ff0000000000000ll), first = 0.0, residual = 0.0;
+  int converged = 0, status = 0;
+  cluster_sync_all();
+  const double* remote_prev[2];
+  const double* remote_next[2];
+  for (int b = 0; b < 2; ++b) {
+    remote_prev[b] = me > 0 ? map_rank(buf[b], me - 1) : nullptr;
+    remote_next[b] = me + 1 < nct ? map_rank(buf[b], me + 1) : nullptr;
+  }
+  unsigned long long* slots0 = const_cast<unsigned long long*>(
+      reinterpret_cast<const unsigned long long*>(map_rank(reinterpret_cast<const double*>(slots), 0)));
+  const unsigned long long t0 = globaltimer_ns();
+  for (;;) {
+    const int cb = static_cast<int>(iter & 1);
+    const double* cur = buf[cb];
+    double* nxt = buf[cb ^ 1];
+    double local = 0.0;
+    for (uint32_t t = threadIdx.x; t < own; t += blockDim.x) {
+      const uint32_t lr = t / n1, k1 = t - lr * n1;
+      const uint32_t k0 = r0 + lr;
+      uint32_t idx[2] = {k0, k1};
+      const uint32_t lin = k0 * n1 + k1;
+      const double v = cur[t];
+      // axis-0 neighbours: local rows or the neighbouring bands (DSMEM)
+      double vm0 = 0.0, vp0 = 0.0;
+      if (k0 > 0) vm0 = lr > 0 ? cur[t - n1] : remote_prev[cb][(R - 1) * n1 + k1];
+      if (k0 + 1 < n0) vp0 = lr + 1 < r1 - r0 ? cur[t + n1] : remote_next[cb][k1];
+      double dm[2], dp[2];
+      // solver.cpp:134-151
+      if (k0 > 0 && k0 < n0 - 1) {
+        dm[0] = (v - vm0) * inv0;
+        dp[0] = (vp0 - v) * inv0;
+      } else if (k0 == 0) {
+        dp[0] = (vp0 - v) * inv0;
+        dm[0] = SCHEME == kGodunov ? 0.0 : dp[0];
+      } else {
+        dm[0] = (v - vm0) * inv0;
+        dp[0] = SCHEME == kGodunov ? 0.0 : dm[0];
+      }
+      if (k1 > 0 && k1 < n1 - 1) {
+        dm[1] = (v - cur[t - 1]) * inv1;
+        dp[1] = (cur[t + 1] - v) * inv1;
+      } else if (k1 == 0) {
+        dp[1] = (cur[t + 1] - v) * inv1;
+        dm[1] = SCHEME == kGodunov ? 0.0 : dp[1];
+      } else {
+        dm[1] = (v - cur[t - 1]) * inv1;
+        dp[1] = SCHEME == kGodunov ? 0.0 : dm[1];
+      }
+      double hhat = 0.0;
+      if (SCHEME == kGodunov) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          double pos, neg;
+          row_slopes<2, PERNODE>(p.m, p.m.row[d], idx, lin, pos, neg);
+          hhat += godunov_flux(pos, neg, dm[d], dp[d]);
+        }
+      } else {
+        double q[2] = {0.5 * (dm[0] + dp[0]), 0.5 * (dm[1] + dp[1])};
+        hhat = lf_hamiltonian<2, PERNODE>(p.m, q, idx, lin);
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const double al = SCHEME == kLfPerNode ? row_alpha<2, PERNODE>(p.m, p.m.row[d], idx, lin)
+                                                 : p.galpha[d];
+          hhat += al * 0.5 * (dp[d] - dm[d]);
+        }
+      }
+      const double stepped = v + p.dt * hhat;
+      const double cc = cl[t];
+      const double vnew = stepped > cc ? stepped : cc;
+      nxt[t] = vnew;
+      const double dv = fabs(vnew - v);
+      if (dv > local) local = dv;
+    }
+    // CTA max -> slot of rank 0
+    unsigned long long bm = warp_max_u64(__double_as_longlong(local));
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = bm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) m = part[w] > m ? part[w] : m;
+      slots0[cb * 16 + me] = m;
+    }
+    cluster_sync_all();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (uint32_t r = 0; r < nct; ++r) {
+        const unsigned long long x = slots0[cb * 16 + r];
+        m = x > m ? x : m;
+      }
+      residual = __longlong_as_double(m) / p.dt;
+      ++iter;
+      LoopState* st = p.st;
+      if (me == 0 && iter - 1 < st->history_cap) {
+        if (st->history) st->history[iter - 1] = residual;
+        if (st->wall_history)
+          st->wall_history[iter - 1] = (double)(globaltimer_ns() - t0) * 1e-6;
+      }
+      bool stop = false;
+      if (residual < p.st->tol) {
+        converged = 1;
+        stop = true;
+      } else {
+        if (iter == 1) first = residual;
+        min_res = residual < min_res ? residual : min_res;
+        const double base = min_res < first ? first : min_res;
+        if (!isfinite(residual) || residual > 10.0 * base) {
+          status = HJB_ERR_DIVERGED;
+          stop = true;
+        }
+      }
+      if (iter >= p.st->max_iters) stop = true;
+      if (p.st->horizon > 0.0 && (double)iter * p.dt >= p.st->horizon) stop = true;
+      s_done = stop ? 1 : 0;
+    }
+    __syncthreads();
+    // every thread tracks iter identically (thread 0's value broadcast)
+    if (threadIdx.x != 0) ++iter;
+    if (s_done) break;
+  }
+  // write the final iterate (buffer parity of iter) and the loop state
+  const double* fin = buf[iter & 1];
+  for (uint32_t t = threadIdx.x; t < own; t += blockDim.x) p.dst[r0 * n1 + t] = fin[t];
+  if (me == 0 && threadIdx.x == 0) {
+    LoopState* st = p.st;
+    st->iter = iter;
+    st->converged = converged;
+    st->status = status;
+    st->last_residual = residual;
+    st->done = 1;
+  }
+  cluster_sync_all();  // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
 inline dim3 blocks_for(uint32_t n) { return dim3((n + kThreads - 1) / kThreads); }
 
 // Persistent-style grid: a few CTAs per SM stride over the nodes, so the
@@ -736,6 +927,47 @@ cudaError_t launch_not_constant(const double* f, uint32_t n, unsigned int* flag,
   const uint32_t b = (n + kThreads - 1) / kThreads;
   k_not_constant<<<b < 148 * 8 ? b : 148 * 8, kThreads, 0, s>>>(f, n, flag);
   return cudaGetLastError();
+}
+
+size_t small2d_smem(const DevGrid& g, uint32_t* rows_out, uint32_t* ctas_out) {
+  if (g.nd != 2) return 0;
+  const uint32_t R = (g.n[0] + 15) / 16;
+  const uint32_t nct = (g.n[0] + R - 1) / R;
+  if (rows_out) *rows_out = R;
+  if (ctas_out) *ctas_out = nct;
+  return (3ull * R * g.n[1]) * sizeof(double) + 32 * sizeof(unsigned long long);
+}
+
+cudaError_t launch_small2d(const StepArgs& s, cudaStream_t stream) {
+  uint32_t R = 0, nct = 0;
+  const size_t smem = small2d_smem(s.g, &R, &nct);
+  Small2dArgs a;
+  a.s = s;
+  a.rows = R;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nct);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = nct;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto go = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+  };
+  const bool pn = s.m.per_node != 0;
+  switch (s.scheme) {
+    case kGodunov: return pn ? go(k_small2d<kGodunov, true>) : go(k_small2d<kGodunov, false>);
+    case kLfPerNode:
+      return pn ? go(k_small2d<kLfPerNode, true>) : go(k_small2d<kLfPerNode, false>);
+    default: return pn ? go(k_small2d<kLfGlobal, true>) : go(k_small2d<kLfGlobal, false>);
+  }
 }
 
 cudaError_t launch_field_op(long long n, const double* a, const double* b, double* out,

@@ -35,6 +35,13 @@ struct StepArgs {
   int order;        // ENO order 1..3
 };
 
+// Whole solve() loop of a small 2D grid in one cluster launch (<= 16 CTAs,
+// V in distributed shared memory).  s.src = init, s.dst = out (device),
+// s.st = loop state initialised by launch_loop_init.  small2d_smem returns
+// the per-CTA shared memory (0 when the grid is not 2D).
+size_t small2d_smem(const DevGrid& g, uint32_t* rows, uint32_t* ctas);
+cudaError_t launch_small2d(const StepArgs& s, cudaStream_t stream);
+
 // K6: one ENO/TVD-RK stage (generic rank; see hjb_kernels.cu).
 cudaError_t launch_ho_stage(const StepArgs& a, cudaStream_t s);
 
