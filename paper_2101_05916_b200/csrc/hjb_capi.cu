@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -403,6 +405,108 @@ void fill_tables(const Prepared& p, Fast4dArgs& f) {
 
 // Device-resident solve: every pointer is device memory.  Shared by the
 // host-pointer entry point (which stages through the context buffers).
+// Kernel-variant choice for the 4D fast path: (cells per thread, CTA thread
+// bound) in {(2,640), (2,448), (4,384)}.  Wave quantisation and register
+// pressure make the best variant grid dependent, so the first solve of a
+// grid shape times 3 sweeps of each variant (HJB_AUTOTUNE=0 disables, which
+// keeps (2,640); HJB_KCELLS / HJB_MAXT force one) and caches the winner.
+struct F4Key {
+  uint32_t n[4];
+  int shape;
+  bool operator<(const F4Key& o) const {
+    for (int d = 0; d < 4; ++d)
+      if (n[d] != o.n[d]) return n[d] < o.n[d];
+    return shape < o.shape;
+  }
+};
+
+static int fast4d_prepare_buffers(hjb_context* ctx, const DevGrid& g, Fast4dArgs& f) {
+  const uint64_t rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
+  const size_t pbytes = rows * ((g.n[3] + 3) / 4 * 4) * sizeof(double);
+  CUDA_TRY(ctx->v2.ensure(pbytes));
+  CUDA_TRY(ctx->v3.ensure(pbytes));
+  CUDA_TRY(ctx->pcbuf.ensure(pbytes));
+  (void)f;
+  return HJB_OK;
+}
+
+int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* init,
+                  const double* c, Fast4dArgs& f) {
+  static std::mutex mu;
+  static std::map<F4Key, std::pair<uint32_t, uint32_t>> cache;
+  int rc;
+  if ((rc = fast4d_prepare_buffers(ctx, g, f))) return rc;
+  const int sms = sm_count(ctx->device);
+  auto configure = [&](uint32_t k, uint32_t t) {
+    f.kcells = k;
+    f.maxthreads = t;
+    f.cbeg = f.cend = 0;
+    fast4d_config(g, sms, f);
+  };
+  const char* kc = std::getenv("HJB_KCELLS");
+  const char* mt = std::getenv("HJB_MAXT");
+  if (kc || mt) {
+    const uint32_t k = (kc && std::atoi(kc) == 4) ? 4u : 2u;
+    configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 640u));
+    return HJB_OK;
+  }
+  const F4Key key{{g.n[0], g.n[1], g.n[2], g.n[3]}, shape};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      configure(it->second.first, it->second.second);
+      return HJB_OK;
+    }
+  }
+  const char* at = std::getenv("HJB_AUTOTUNE");
+  if ((at && std::strcmp(at, "0") == 0) || g.size < (1u << 20)) {
+    configure(2, 640);
+    return HJB_OK;
+  }
+  const uint32_t cands[3][2] = {{2, 640}, {2, 448}, {4, 384}};
+  float best = 1e30f;
+  uint32_t bk = 2, bt = 640;
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const uint64_t rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
+  for (const auto& cd : cands) {
+    configure(cd[0], cd[1]);
+    CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
+    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
+    Fast4dArgs x = f;
+    x.c = ctx->pcbuf.d();
+    x.buf0 = ctx->v2.d();
+    x.src = ctx->v2.d();
+    x.buf1 = ctx->v3.d();
+    x.dst = ctx->v3.d();
+    x.loop = 0;
+    CUDA_TRY(fast4d_make_maps(x, x.buf0, x.buf1, x.c));
+    CUDA_TRY(launch_fast4d(x, shape, ctx->stream));  // warm-up
+    CUDA_TRY(cudaEventRecord(e0, ctx->stream));
+    for (int r = 0; r < 3; ++r) CUDA_TRY(launch_fast4d(x, shape, ctx->stream));
+    CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ctx->launches += 6;
+    if (ms < best) {
+      best = ms;
+      bk = cd[0];
+      bt = cd[1];
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = {bk, bt};
+  }
+  configure(bk, bt);
+  return HJB_OK;
+}
+
 // A per-node IntervalField whose every node holds the same interval is the
 // constant field (identical values at every node); collapsing it keeps the
 // folded-slope fast path (e.g. a resampled constant field of a coarse level).
@@ -504,18 +608,8 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   std::memset(&f, 0, sizeof f);
   uint64_t rows = 0;
   if (shape >= 0) {
-    // padded internal layout (even contiguous extent) for the 4D fast path
-    const char* kc = std::getenv("HJB_KCELLS");
-    f.kcells = (kc && std::atoi(kc) == 4) ? 4u : 2u;
-    fast4d_config(g, sm_count(ctx->device), f);
-    rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
-    const size_t pbytes = rows * f.n3p * sizeof(double);
-    CUDA_TRY(ctx->v2.ensure(pbytes));
-    CUDA_TRY(ctx->v3.ensure(pbytes));
-    CUDA_TRY(ctx->pcbuf.ensure(pbytes));
-    CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
-    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
-    ctx->launches += 2;
+    // padded internal layout for the 4D fast path; kernel variant chosen by
+    // the autotuner (cached per grid shape)
     f.tab = hm.dm.tab;
     for (int d = 0; d < 4; ++d) {
       f.off_pos[d] = hm.dm.row[d].off_pos;
@@ -523,6 +617,13 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
       f.off_a[d] = hm.dm.row[d].off_a;
       f.off_b[d] = hm.dm.row[d].off_b;
     }
+    f.st = ctx->st;
+    f.dt = dt;
+    if ((rc = fast4d_choose(ctx, g, shape, init, c, f))) return rc;
+    rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
+    CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
+    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
+    ctx->launches += 2;
     f.c = ctx->pcbuf.d();
     f.buf0 = ctx->v2.d();
     f.buf1 = ctx->v3.d();

@@ -100,6 +100,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Consumer-side wait without a compiler memory barrier: every shared-memory
+// read of the consumers is itself an `asm volatile` (lds1/lds2), so volatile
+// ordering keeps them after the wait, while independent arithmetic of the
+// previous plane may still be scheduled across it (more ILP per warp).
+__device__ __forceinline__ void mbar_wait_nc(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITNC_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITNC_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity));
+}
 // 4D TMA tile load (tensor map in kernel-parameter space), OOB -> zeros
 __device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                           int c2, int c3, uint32_t bar) {
@@ -207,8 +221,8 @@ __device__ __forceinline__ double godunov_select(double ha, double hb, double dm
 // compile-time constants.  Kink products of faces shared by two cells are
 // formed once: along the march (carried to the next plane) and inside the
 // pencil when the row's slopes do not vary along the contiguous axis.
-template <class S, int kK>
-__global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
+template <class S, int kK, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const double* src;
@@ -390,13 +404,13 @@ __global__ void __launch_bounds__(kK == 2 ? 640 : 384, 1)
         const uint32_t use_n = (k + 1 == kRing) ? round + 1 : round;
         double vn[kK];
         if (i0 + 1 < n0) {
-          mbar_wait(bars + kn * 8, use_n & 1u);
+          mbar_wait_nc(bars + kn * 8, use_n & 1u);
           lds_cells<kK>(vring + kn * a.vslot_bytes + own, vn);
         } else {
 #pragma unroll
           for (int c = 0; c < kK; ++c) vn[c] = v[c];  // D+ at the i0 = n0-1 edge: +0
         }
-        mbar_wait(bars + (2 * kRing + k) * 8, round & 1u);
+        mbar_wait_nc(bars + (2 * kRing + k) * 8, round & 1u);
         double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
         lds_cells<kK>(cring + k * a.cslot_bytes + cown, cc);
         lds_cells<kK>(slot_cur + o1m, n1m);
@@ -605,7 +619,7 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   // shared memory, smallest halo/tile ratio
   uint32_t bestT1 = 1, bestT2 = 1;
   double best = 1e30;
-  const uint32_t maxc = kK == 2 ? 608 : 352;
+  const uint32_t maxc = a.maxthreads - 32;  // consumers; one producer warp
   for (uint32_t T1 = 1; T1 <= g.n[1] && T1 * J <= maxc; ++T1) {
     for (uint32_t T2 = 1; T2 <= g.n[2] && T1 * T2 * J <= maxc; ++T2) {
       if (fast4d_smem(T1, T2, a.n3p) > 200 * 1024) continue;
@@ -654,22 +668,27 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.blocks = tiles * a.nchunks;
 }
 
-template <class S, int K>
+template <class S, int K, int MAXT>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_fast4d<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_fast4d<S, K, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr_set = true;
   }
-  k_fast4d<S, K><<<a.blocks, a.threads, a.smem, s>>>(a);
+  k_fast4d<S, K, MAXT><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
+// kernel variants (cells per thread, CTA thread bound): the tile search and
+// the autotuner pick among them per grid
 template <class S>
 static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
   if (a.kcells == 4)
-    launch_one<S, 4>(a, s);
+    launch_one<S, 4, 384>(a, s);
+  else if (a.maxthreads == 448)
+    launch_one<S, 2, 448>(a, s);
   else
-    launch_one<S, 2>(a, s);
+    launch_one<S, 2, 640>(a, s);
 }
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {

@@ -18,7 +18,8 @@ struct Fast4dArgs {
   uint32_t n[4];
   uint32_t n3p;  // padded contiguous extent (even)
   double inv[4];
-  uint32_t kcells;  // cells per thread along the contiguous axis (2 or 4)
+  uint32_t kcells;      // cells per thread along the contiguous axis (2 or 4)
+  uint32_t maxthreads;  // CTA thread bound of the variant: (2, 640), (2, 448), (4, 384)
   uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads, consumers, smem;
   uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
   const double* tab;
