@@ -175,7 +175,7 @@ __device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, 
   __threadfence();
 }
 
-constexpr int kRing = 4;  // planes in flight per ring (prefetch distance kRing - 1)
+constexpr int kRing = 6;  // planes in flight per ring (prefetch distance kRing - 1)
 
 template <int K>
 __device__ __forceinline__ void lds_cells(uint32_t addr, double* v) {
@@ -442,6 +442,11 @@ __global__ void __launch_bounds__(MAXT, 1)
         double out[kK];
 #pragma unroll
         for (int c = 0; c < kK; ++c) {
+          if (a.debug_nocompute) {  // data-movement-only diagnostic (HJB_DEBUG_NOCOMPUTE)
+            out[c] = (v[c] + 1.0) + cc[c] * 0.0;
+            if (valid[c]) mbits = umax64(mbits, 0x3ff0000000000000ull);  // |dV| = 1
+            continue;
+          }
           // axis 0
           const double dp0 = (vn[c] - v[c]) * inv0;
           double h0;
