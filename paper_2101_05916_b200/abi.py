@@ -31,7 +31,7 @@ PER_NODE, GLOBAL = 0, 1
 PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 HEADER = REPO_DIR / "include" / "hjb.h"
-LIB_PATH = PKG_DIR / "libhjb.so"
+LIB_PATH = Path(os.environ["HJB_LIB"]) if os.environ.get("HJB_LIB") else PKG_DIR / "libhjb.so"
 
 
 class GridDim(C.Structure):

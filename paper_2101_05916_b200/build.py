@@ -40,21 +40,34 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path = OUT,
+          defines: tuple = ()) -> Path:
+    """Compile the library.  ``out``/``defines`` build an experiment variant
+    (e.g. _variants/libhjb_x.so with -DFOO=1) that abi.py loads when HJB_LIB
+    names it; the product is OUT with no extra defines."""
+    if out == OUT and not defines and not force and not needs_build():
         return OUT
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-shared", "-o", str(OUT),
+    out.parent.mkdir(parents=True, exist_ok=True)
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", str(out),
            *[str(CSRC / s) for s in SOURCES], "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     log = proc.stdout + proc.stderr
-    (PKG / "build.log").write_text(" ".join(cmd) + "\n" + log)
+    (PKG / ("build.log" if out == OUT else f"build_{out.stem}.log")).write_text(
+        " ".join(cmd) + "\n" + log)
     if proc.returncode != 0:
         sys.stderr.write(log)
         raise RuntimeError(f"nvcc failed ({proc.returncode}); see {PKG / 'build.log'}")
     if verbose:
         sys.stderr.write(log)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python build.py [--force] [--variant NAME -DX=1 ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        defs = tuple(a[2:] for a in args if a.startswith("-D"))
+        print(build(out=PKG / "_variants" / f"libhjb_{name}.so", defines=defs))
+    else:
+        build(force="--force" in args, verbose=True)

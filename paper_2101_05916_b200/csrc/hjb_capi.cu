@@ -620,7 +620,6 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     f.st = ctx->st;
     f.dt = dt;
     if ((rc = fast4d_choose(ctx, g, shape, init, c, f))) return rc;
-    f.debug_nocompute = std::getenv("HJB_DEBUG_NOCOMPUTE") ? 1 : 0;
     rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
     CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
     CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));

@@ -177,6 +177,11 @@ __device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, 
 
 constexpr int kRing = 6;  // planes in flight per ring (prefetch distance kRing - 1)
 
+// |x| as IEEE bits (std::abs clears the sign bit)
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+
 template <int K>
 __device__ __forceinline__ void lds_cells(uint32_t addr, double* v) {
 #pragma unroll
@@ -195,19 +200,20 @@ __device__ __forceinline__ double kink(double pos, double neg, double p) {
 }
 
 // Godunov selection (solver.cpp:52-63) given the two kink products, branch
-// free.  pos_nn / neg_nn: sign_clear(pos), sign_clear(neg) (loop invariant).
-//  same-signed gradients  -> upwind end: hb if the active slope is >= 0
+// free, on sign bits only (no loop-invariant flags live in the march):
+//  same-signed gradients  -> upwind end: hb if the active slope is >= 0; the
+//                            slope's sign is sign(ha) ^ sign(dm) (IEEE product
+//                            sign rule)
 //  dm <= 0 < dp (rarefaction) -> max(ha, hb), clamped below at 0
 //  dp <= 0 < dm (shock)       -> min(ha, hb), clamped above at 0
-__device__ __forceinline__ double godunov_select(double ha, double hb, double dm, double dp,
-                                                 bool pos_nn, bool neg_nn) {
-  const bool km = sign_clear(dm), kp = sign_clear(dp);
-  const bool gt = ha > hb;
-  const bool same = km == kp;
-  const bool s_nn = km ? pos_nn : neg_nn;
-  const bool pick_a = same ? !s_nn : (gt != km);
-  double h = pick_a ? ha : hb;
-  const bool zero = !same && (sign_clear(h) == km);
+__device__ __forceinline__ double godunov_select(double ha, double hb, double dm, double dp) {
+  const int xm = __double2hiint(dm), xp = __double2hiint(dp);
+  const bool same = (xm ^ xp) >= 0;
+  const bool slope_neg = (__double2hiint(ha) ^ xm) < 0;
+  const bool km = xm >= 0;
+  const bool pick_a = (same && slope_neg) || (!same && ((ha > hb) != km));
+  const double h = pick_a ? ha : hb;
+  const bool zero = !same && ((__double2hiint(h) ^ xm) >= 0);
   return zero ? 0.0 : h;
 }
 
@@ -340,7 +346,6 @@ __global__ void __launch_bounds__(MAXT, 1)
     // loop-invariant slopes (row d, cell c); rows that do not vary along x3
     // hold one pair for the whole pencil
     double pos[4][kK], neg[4][kK];
-    bool pnn[4][kK], nnn[4][kK];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
@@ -361,9 +366,33 @@ __global__ void __launch_bounds__(MAXT, 1)
             neg[d][c] = dr;
           }
         }
-        pnn[d][c] = sign_clear(pos[d][c]);
-        nnn[d][c] = sign_clear(neg[d][c]);
       }
+    }
+    // Linear rows (pos == neg == s: no input on the row): the Godunov flux of
+    // H(p) = s p is s * D+ for s >= 0 and s * D- otherwise (solver.cpp:52-63),
+    // and s * D- = s * ((v - vm) * inv) = |s| * ((vm - v) * inv) exactly (IEEE
+    // negation is exact and rounding symmetric; only the sign of a zero
+    // differs).  An off-march linear row therefore reads one neighbour, the
+    // upwind one: h = |s| * ((v_up - v) * inv).
+    bool up[4][kK];   // s >= 0 (sign bit clear)
+    double as[4][kK];  // |s|
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        up[d][c] = sign_clear(pos[d][c]);
+        as[d][c] = __longlong_as_double(__double_as_longlong(pos[d][c]) & 0x7fffffffffffffffll);
+      }
+    }
+    constexpr bool pc1 = S::A(1) == 3 || S::B(1) == 3;
+    constexpr bool pc2 = S::A(2) == 3 || S::B(2) == 3;
+    // upwind neighbour offsets of linear rows 1, 2 (per cell when the slope
+    // varies along x3, else one for the pencil)
+    uint32_t o1u[kK], o2u[kK];
+#pragma unroll
+    for (int c = 0; c < kK; ++c) {
+      o1u[c] = (up[1][c] ? o1p : o1m) + 8u * c;
+      o2u[c] = (up[2][c] ? o2p : o2m) + 8u * c;
     }
 
     double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
@@ -390,7 +419,7 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
     for (int c = 0; c < kK; ++c) {
       dm0[c] = (v[c] - vp[c]) * inv0;
-      ka0[c] = kink(pos[0][c], neg[0][c], dm0[c]);
+      ka0[c] = S::LIN(0) ? 0.0 : kink(pos[0][c], neg[0][c], dm0[c]);
     }
 
     for (uint32_t rb = c0; rb < c1; rb += kRing) {
@@ -413,10 +442,28 @@ __global__ void __launch_bounds__(MAXT, 1)
         mbar_wait_nc(bars + (2 * kRing + k) * 8, round & 1u);
         double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
         lds_cells<kK>(cring + k * a.cslot_bytes + cown, cc);
-        lds_cells<kK>(slot_cur + o1m, n1m);
-        lds_cells<kK>(slot_cur + o1p, n1p);
-        lds_cells<kK>(slot_cur + o2m, n2m);
-        lds_cells<kK>(slot_cur + o2p, n2p);
+        if (S::LIN(1)) {  // upwind neighbour only (n1p holds it)
+          if (pc1) {
+#pragma unroll
+            for (int c = 0; c < kK; ++c) n1p[c] = lds1(slot_cur + o1u[c]);
+          } else {
+            lds_cells<kK>(slot_cur + o1u[0], n1p);
+          }
+        } else {
+          lds_cells<kK>(slot_cur + o1m, n1m);
+          lds_cells<kK>(slot_cur + o1p, n1p);
+        }
+        if (S::LIN(2)) {
+          if (pc2) {
+#pragma unroll
+            for (int c = 0; c < kK; ++c) n2p[c] = lds1(slot_cur + o2u[c]);
+          } else {
+            lds_cells<kK>(slot_cur + o2u[0], n2p);
+          }
+        } else {
+          lds_cells<kK>(slot_cur + o2m, n2m);
+          lds_cells<kK>(slot_cur + o2p, n2p);
+        }
         const double vl = lds1(slot_cur + ol);
         const double vr = lds1(slot_cur + orr);
 
@@ -442,62 +489,56 @@ __global__ void __launch_bounds__(MAXT, 1)
         double out[kK];
 #pragma unroll
         for (int c = 0; c < kK; ++c) {
-          if (a.debug_nocompute) {  // data-movement-only diagnostic (HJB_DEBUG_NOCOMPUTE)
-            out[c] = (v[c] + 1.0) + cc[c] * 0.0;
-            if (valid[c]) mbits = umax64(mbits, 0x3ff0000000000000ull);  // |dV| = 1
-            continue;
-          }
-          // axis 0
+          // axis 0 (D- carried from the previous plane)
           const double dp0 = (vn[c] - v[c]) * inv0;
           double h0;
-          const double kb0 = kink(pos[0][c], neg[0][c], dp0);
           if (S::LIN(0)) {
-            h0 = pnn[0][c] ? kb0 : ka0[c];
+            h0 = pos[0][c] * (up[0][c] ? dp0 : dm0[c]);
           } else {
-            h0 = godunov_select(ka0[c], kb0, dm0[c], dp0, pnn[0][c], nnn[0][c]);
+            const double kb0 = kink(pos[0][c], neg[0][c], dp0);
+            h0 = godunov_select(ka0[c], kb0, dm0[c], dp0);
+            ka0[c] = kb0;
           }
           dm0[c] = dp0;
-          ka0[c] = kb0;
           // axis 1
-          const double dm1 = (v[c] - n1m[c]) * inv1;
-          const double dp1 = (n1p[c] - v[c]) * inv1;
           double h1;
           if (S::LIN(1)) {
-            h1 = pos[1][c] * (pnn[1][c] ? dp1 : dm1);
+            h1 = as[1][c] * ((n1p[c] - v[c]) * inv1);
           } else {
+            const double dm1 = (v[c] - n1m[c]) * inv1;
+            const double dp1 = (n1p[c] - v[c]) * inv1;
             h1 = godunov_select(kink(pos[1][c], neg[1][c], dm1), kink(pos[1][c], neg[1][c], dp1),
-                                dm1, dp1, pnn[1][c], nnn[1][c]);
+                                dm1, dp1);
           }
           // axis 2
-          const double dm2 = (v[c] - n2m[c]) * inv2;
-          const double dp2 = (n2p[c] - v[c]) * inv2;
           double h2;
           if (S::LIN(2)) {
-            h2 = pos[2][c] * (pnn[2][c] ? dp2 : dm2);
+            h2 = as[2][c] * ((n2p[c] - v[c]) * inv2);
           } else {
+            const double dm2 = (v[c] - n2m[c]) * inv2;
+            const double dp2 = (n2p[c] - v[c]) * inv2;
             h2 = godunov_select(kink(pos[2][c], neg[2][c], dm2), kink(pos[2][c], neg[2][c], dp2),
-                                dm2, dp2, pnn[2][c], nnn[2][c]);
+                                dm2, dp2);
           }
           // axis 3
           double h3;
           if (S::LIN(3)) {
-            h3 = pos[3][c] * (pnn[3][c] ? f3[c + 1] : f3[c]);
+            h3 = pos[3][c] * (up[3][c] ? f3[c + 1] : f3[c]);
           } else if (row3_shared) {
-            h3 = godunov_select(k3a[c], k3b[c + 1], f3[c], f3[c + 1], pnn[3][c], nnn[3][c]);
+            h3 = godunov_select(k3a[c], k3b[c + 1], f3[c], f3[c + 1]);
           } else {
             h3 = godunov_select(kink(pos[3][c], neg[3][c], f3[c]),
-                                kink(pos[3][c], neg[3][c], f3[c + 1]), f3[c], f3[c + 1],
-                                pnn[3][c], nnn[3][c]);
+                                kink(pos[3][c], neg[3][c], f3[c + 1]), f3[c], f3[c + 1]);
           }
           // hhat = 0.0 + h0 + h1 + h2 + h3 (0.0 + h0 == h0 in value)
           const double hh = ((h0 + h1) + h2) + h3;
           const double st = v[c] + a.dt * hh;
           out[c] = st > cc[c] ? st : cc[c];
-          // |dV| bits: clear the sign (== std::abs); NaN (above +inf) never
-          // wins, as in the reference's `if (dv > max_dv)` (solver.cpp:181-182)
-          const unsigned long long ib =
-              (unsigned long long)__double_as_longlong(out[c] - v[c]) & 0x7fffffffffffffffull;
-          if (valid[c] && ib <= 0x7ff0000000000000ull) mbits = umax64(mbits, ib);
+          // |dV| bits: clear the sign (== std::abs).  The unsigned max of the
+          // bits orders non-negative doubles; a NaN (above +inf) is filtered
+          // after the march (rare path below)
+          const unsigned long long ib = abs_bits(out[c] - v[c]);
+          if (valid[c]) mbits = umax64(mbits, ib);
         }
         if (active) {
 #pragma unroll
@@ -512,6 +553,22 @@ __global__ void __launch_bounds__(MAXT, 1)
         if (lane == 0) {
           mbar_arrive(bars + (kRing + k) * 8);
           mbar_arrive(bars + (3 * kRing + k) * 8);
+        }
+      }
+    }
+    if (mbits > 0x7ff0000000000000ull) {
+      // a NaN |dV| won the unfiltered max: redo this pencil's max from global
+      // memory with the reference's filter (a NaN never passes
+      // `if (dv > max_dv)`, solver.cpp:181-182).  Cold path.
+      mbits = 0ull;
+      const uint64_t rowo = static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3;
+      for (uint32_t i0 = c0; i0 < c1; ++i0) {
+        const uint64_t o = static_cast<uint64_t>(i0) * s0 + rowo;
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          if (!valid[c]) continue;
+          const unsigned long long ib = abs_bits(dst[o + c] - src[o + c]);
+          if (ib <= 0x7ff0000000000000ull) mbits = umax64(mbits, ib);
         }
       }
     }

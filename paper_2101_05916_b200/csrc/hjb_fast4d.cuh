@@ -34,7 +34,6 @@ struct Fast4dArgs {
   int loop;  // 0 single step, 1 device loop (fused epilogue), 2 sharded slab sweep
   cudaGraphConditionalHandle handle;
   int use_handle;
-  int debug_nocompute;  // diagnostic: skip the Hamiltonian (copy V), pipeline timing only
 };
 
 // Model shape id for the fast path, or -1 when the generic kernel must run

@@ -170,3 +170,24 @@ def test_multilevel_three_levels_matches_oracle(gpu_ctx, oracle):
         assert x.iterations == y.iterations
         assert same(x.residual_history, y.residual_history)
         assert same(x.value.values(), y.value.values())
+
+
+@pytest.mark.parametrize("fast", ["1", "0"])
+def test_nan_cell_never_wins_the_residual(gpu_ctx, monkeypatch, fast):
+    """A NaN in V (possible only through unchecked inputs) is skipped by the
+    max|dV| reduction as by the reference's `if (dv > max_dv)`
+    (solver.cpp:181-182); the fast kernel takes its rescan path here.  The
+    NaN node itself is clamped to c (std::max(c, NaN) == c)."""
+    monkeypatch.setenv("HJB_FAST", fast)
+    case = with_iters(workload_case(configs.config2(13)), 1)
+    rng = np.random.default_rng(11)
+    v0 = case.c + 0.25 * rng.random(case.grid.size())
+    k = case.grid.linear_index((6, 6, 6, 6))
+    v0[k] = np.nan
+    init = hj.ScalarField(case.grid, v0, check=False)
+    r = hj.solve(init, case.c_field(), case.model, case.db, case.cfg, ctx=gpu_ctx)
+    out = r.value.values()
+    assert out[k] == case.c[k]
+    dv = np.abs(out - v0)
+    want = dv[np.isfinite(dv)].max() / r.dt
+    assert r.iterations == 1 and r.residual_history[0] == want
