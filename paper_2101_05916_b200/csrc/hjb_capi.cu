@@ -406,10 +406,10 @@ void fill_tables(const Prepared& p, Fast4dArgs& f) {
 // Device-resident solve: every pointer is device memory.  Shared by the
 // host-pointer entry point (which stages through the context buffers).
 // Kernel-variant choice for the 4D fast path: (cells per thread, CTA thread
-// bound) in {(2,640), (2,448), (4,384)}.  Wave quantisation and register
+// bound) in {(2,576), (2,448), (4,384)}.  Wave quantisation and register
 // pressure make the best variant grid dependent, so the first solve of a
 // grid shape times 3 sweeps of each variant (HJB_AUTOTUNE=0 disables, which
-// keeps (2,640); HJB_KCELLS / HJB_MAXT force one) and caches the winner.
+// keeps (2,576); HJB_KCELLS / HJB_MAXT force one) and caches the winner.
 struct F4Key {
   uint32_t n[4];
   int shape;
@@ -447,7 +447,7 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
   const char* mt = std::getenv("HJB_MAXT");
   if (kc || mt) {
     const uint32_t k = (kc && std::atoi(kc) == 4) ? 4u : 2u;
-    configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 640u));
+    configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 576u));
     return HJB_OK;
   }
   const F4Key key{{g.n[0], g.n[1], g.n[2], g.n[3]}, shape};
@@ -461,12 +461,13 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
   }
   const char* at = std::getenv("HJB_AUTOTUNE");
   if ((at && std::strcmp(at, "0") == 0) || g.size < (1u << 20)) {
-    configure(2, 640);
+    configure(2, 576);
     return HJB_OK;
   }
-  const uint32_t cands[3][2] = {{2, 640}, {2, 448}, {4, 384}};
+  const uint32_t cands[3][2] = {{2, 576}, {2, 448}, {4, 384}};
+  CUDA_TRY(cudaMemsetAsync(ctx->st, 0, sizeof(LoopState), ctx->stream));  // fresh counters
   float best = 1e30f;
-  uint32_t bk = 2, bt = 640;
+  uint32_t bk = 2, bt = 576;
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
@@ -595,10 +596,6 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   CUDA_TRY(ctx->v0.ensure(bytes));
   CUDA_TRY(ctx->v1.ensure(bytes));
   CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
-  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
-                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
-                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
-  ++ctx->launches;
   const int shape = fast_enabled() ? fast4d_shape(g, hm.dm, scheme_of(cfg)) : -1;
   StepArgs a = base_args(g, hm.dm, c, dt, scheme_of(cfg), s);
   a.st = ctx->st;
@@ -632,6 +629,11 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     f.dt = dt;
     f.loop = 1;
   }
+  // loop state after the autotuner (its timing sweeps use the same state)
+  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
+                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
+                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
+  ++ctx->launches;
   SweepLauncher launch = [&](cudaStream_t st, cudaGraphConditionalHandle h, int use) {
     if (shape >= 0) {
       Fast4dArgs x = f;

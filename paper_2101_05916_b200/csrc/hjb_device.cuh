@@ -103,6 +103,7 @@ struct DevModel {
 struct LoopState {
   unsigned long long maxdv_bits;  // running max |dV| of the current sweep
   unsigned int blocks_done;
+  unsigned int work_next;  // dynamic work-item counter of the persistent 4D sweep
   int done;
   int status;  // 0 ok, HJB_ERR_DIVERGED
   int converged;

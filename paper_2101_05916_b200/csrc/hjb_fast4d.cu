@@ -24,7 +24,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include <cudaTypedefs.h>
 
@@ -64,10 +66,6 @@ struct ShapeTwin {  // TwinDoubleIntegrator rows: x1 | const | x3 | const
 template <class S>
 __device__ __forceinline__ uint32_t pick(int axis, uint32_t i1, uint32_t i2, uint32_t i3) {
   return axis == 1 ? i1 : axis == 2 ? i2 : axis == 3 ? i3 : 0u;
-}
-
-__device__ __forceinline__ double2 ldg2(const double* p) {
-  return __ldg(reinterpret_cast<const double2*>(p));
 }
 
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
@@ -168,6 +166,7 @@ __device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, 
   if (st->horizon > 0.0 && (double)iter * st->dt >= st->horizon) stop = true;
   st->maxdv_bits = 0ull;
   st->blocks_done = 0u;
+  st->work_next = 0u;
   if (stop) {
     st->done = 1;
     if (use_handle) cudaGraphSetConditional(handle, 0u);
@@ -176,11 +175,6 @@ __device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, 
 }
 
 constexpr int kRing = 6;  // planes in flight per ring (prefetch distance kRing - 1)
-
-// |x| as IEEE bits (std::abs clears the sign bit)
-__device__ __forceinline__ unsigned long long abs_bits(double x) {
-  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
-}
 
 template <int K>
 __device__ __forceinline__ void lds_cells(uint32_t addr, double* v) {
@@ -192,41 +186,140 @@ __device__ __forceinline__ void lds_cells(uint32_t addr, double* v) {
   }
 }
 
+#ifndef HJB_SLOPE_IMAD
+#define HJB_SLOPE_IMAD 0  // 1: slope pick on the integer multiply pipe (71^4 faster, 51^4 and 101^4 slower)
+#endif
+
+// A slope pair (for p >= 0, for p < 0) selected by the sign bit s of p as
+// base + s * diff on each 32-bit word (integer multiply-add pipe, no
+// predicate): s = 0 -> base, s = 1 -> base + (other - base) = other.
+struct SlopePair {
+  uint32_t blo, bhi, dlo, dhi;
+};
+__device__ __forceinline__ SlopePair make_pair(double for_pos, double for_neg) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(for_pos);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(for_neg);
+  SlopePair q;
+  q.blo = (uint32_t)a;
+  q.bhi = (uint32_t)(a >> 32);
+  q.dlo = (uint32_t)b - (uint32_t)a;
+  q.dhi = (uint32_t)(b >> 32) - (uint32_t)(a >> 32);
+  return q;
+}
+__device__ __forceinline__ uint32_t sign_bit(double p) {
+#if HJB_SLOPE_IMAD
+  return __umulhi((uint32_t)__double2hiint(p), 2u);  // (hi >> 31) on the multiply pipe
+#else
+  return (uint32_t)__double2hiint(p) >> 31;
+#endif
+}
 // reference kink_h (solver.cpp:44-46): s = p > 0 ? pos : neg; s * p.  The
 // sign-bit test differs from `p > 0` only for p == +0, where both products
 // are +-0 (see file header).
-__device__ __forceinline__ double kink(double pos, double neg, double p) {
-  return (sign_clear(p) ? pos : neg) * p;
+__device__ __forceinline__ double pair_kink(const SlopePair& q, double p, uint32_t s) {
+#if HJB_SLOPE_IMAD
+  const double sl = __hiloint2double((int)(q.bhi + s * q.dhi), (int)(q.blo + s * q.dlo));
+#else
+  const double a = __hiloint2double((int)q.bhi, (int)q.blo);
+  const double b = __hiloint2double((int)(q.bhi + q.dhi), (int)(q.blo + q.dlo));
+  const double sl = s ? b : a;
+#endif
+  return sl * p;
 }
 
-// Godunov selection (solver.cpp:52-63) given the two kink products, branch
-// free, on sign bits only (no loop-invariant flags live in the march):
-//  same-signed gradients  -> upwind end: hb if the active slope is >= 0; the
-//                            slope's sign is sign(ha) ^ sign(dm) (IEEE product
-//                            sign rule)
-//  dm <= 0 < dp (rarefaction) -> max(ha, hb), clamped below at 0
-//  dp <= 0 < dm (shock)       -> min(ha, hb), clamped above at 0
-__device__ __forceinline__ double godunov_select(double ha, double hb, double dm, double dp) {
-  const int xm = __double2hiint(dm), xp = __double2hiint(dp);
-  const bool same = (xm ^ xp) >= 0;
-  const bool slope_neg = (__double2hiint(ha) ^ xm) < 0;
-  const bool km = xm >= 0;
-  const bool pick_a = (same && slope_neg) || (!same && ((ha > hb) != km));
-  const double h = pick_a ? ha : hb;
-  const bool zero = !same && ((__double2hiint(h) ^ xm) >= 0);
-  return zero ? 0.0 : h;
+// Godunov flux of a non-linear row (pos != neg) rewritten per slope shape,
+// with the shape fixed per row and thread (loop invariant).  With
+// P(x) = pos * max(x, 0) and N(x) = neg * min(x, 0) (each the reference's
+// kink product kink_h(x) on its half line, +-0 on the other):
+//   INC  pos, neg >= 0 (H non-decreasing)  -> kink_h(D+)
+//   DEC  pos, neg <  0 (H non-increasing)  -> kink_h(D-)
+//   V    neg < 0 <= pos (convex, min 0)    -> max(N(D-), P(D+))
+//   Lam  pos < 0 <= neg (concave, max 0)   -> min(P(D-), N(D+))
+// Each equals the value solver.cpp:52-63 returns in every sign case of
+// (D-, D+) (only the sign of a zero result can differ).  All four are
+// A = L(D-) and B = R(D+) with per-shape slope pairs L, R and a pick rule
+// (A, B, max or min).  A face shared by two cells yields its L product for
+// the cell above and its R product for the cell below.
+//
+// The pick runs on the FP64 pipe: A is taken iff fma(A, m, ca) > B * m with
+// (m, ca) = (1, 0) max (V), (-1, 0) min (Lam), (0, 0) always B (INC: +-0 >
+// +-0 is false), (0, 1) always A (DEC).  A * +-1 + 0 and B * +-1 are exact.
+struct RowShape {
+  SlopePair L, R;
+  double m, ca;
+};
+__device__ __forceinline__ RowShape row_shape(double pos, double neg) {
+  const bool pn = sign_clear(pos), nn = sign_clear(neg);
+  RowShape r;
+  double lp = 0.0, ln = 0.0, rp = 0.0, rn = 0.0;
+  r.ca = 0.0;
+  if (pn && nn) {          // INC: B = kink_h(D+)
+    rp = pos;
+    rn = neg;
+    r.m = 0.0;
+  } else if (!pn && !nn) {  // DEC: A = kink_h(D-)
+    lp = pos;
+    ln = neg;
+    r.m = 0.0;
+    r.ca = 1.0;
+  } else if (pn) {          // V: A = N(D-), B = P(D+), max
+    ln = neg;
+    rp = pos;
+    r.m = 1.0;
+  } else {                  // Lam: A = P(D-), B = N(D+), min
+    lp = pos;
+    rn = neg;
+    r.m = -1.0;
+  }
+  r.L = make_pair(lp, ln);
+  r.R = make_pair(rp, rn);
+  return r;
+}
+__device__ __forceinline__ double shape_pick(const RowShape& r, double a, double b) {
+  return __fma_rn(a, r.m, r.ca) > b * r.m ? a : b;
 }
 
-// One CTA = a T1 x T2 tile of (i1, i2) rows (full contiguous rows of n3p),
-// marching i0 over [c0, c1).  A dedicated producer warp streams each V plane
+// Work item w of a sweep: a T1 x T2 tile of (i1, i2) rows and a chunk of
+// axis-0 planes.  Full tiles come first and edge (partial) tiles last, so
+// the dynamic schedule hands out the long items first.
+__device__ __forceinline__ void item_tile(const Fast4dArgs& a, uint32_t w, uint32_t& t1,
+                                          uint32_t& t2, uint32_t& chunk) {
+  chunk = w % a.nchunks;
+  const uint32_t u = w / a.nchunks;
+  const uint32_t f1 = a.n[1] / a.T1, f2 = a.n[2] / a.T2;  // full tiles per axis
+  const uint32_t nf = f1 * f2;
+  if (u < nf) {
+    t1 = u / f2;
+    t2 = u - t1 * f2;
+    return;
+  }
+  uint32_t e = u - nf;
+  if (a.tiles2 > f2) {  // partial last tile column, full rows
+    if (e < f1) {
+      t1 = e;
+      t2 = a.tiles2 - 1;
+      return;
+    }
+    e -= f1;
+  }
+  t1 = a.tiles1 - 1;  // partial last tile row
+  t2 = e;
+}
+
+constexpr uint32_t kEndItem = 0xffffffffu;
+
+// Persistent sweep: one CTA per SM pulls work items (tile x plane chunk)
+// until the sweep is done; per item it marches i0 over [c0, c1).  A
+// dedicated producer thread streams, per item, the V planes c0-1 .. c1
 // (tile + 1-row halo in i1 and i2; out-of-range rows are zero-filled by the
-// TMA unit and never read) and each c plane (tile) into shared-memory rings
-// with one 4D tensor copy each; full/empty mbarriers pipeline the planes.
-// Consumer threads own kK consecutive cells of one row.  The march is
-// unrolled by the ring depth so ring slots and barrier parities are
-// compile-time constants.  Kink products of faces shared by two cells are
-// formed once: along the march (carried to the next plane) and inside the
-// pencil when the row's slopes do not vary along the contiguous axis.
+// TMA unit and never read) and the c planes c0 .. c1-1 into one ring of
+// kRing slots with one 4D tensor copy each, full/empty mbarriers per slot,
+// and the item id in a per-slot header.  The ring runs continuously across
+// items, so the next item's planes stream in while the current one is
+// finishing.  Consumer threads own kK consecutive cells of one row.  Kink
+// products of faces shared by two cells are formed once: along the march
+// (carried to the next plane) and inside the pencil when the row's slopes do
+// not vary along the contiguous axis.
 template <class S, int kK, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
@@ -246,6 +339,7 @@ __global__ void __launch_bounds__(MAXT, 1)
     dst = a.dst;
     vmap = &a.map0;
   }
+  (void)src;
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3];
   const uint32_t n3p = a.n3p;
   const uint32_t J = n3p / kK;
@@ -254,60 +348,70 @@ __global__ void __launch_bounds__(MAXT, 1)
   const uint32_t smem0 = smem_u32(smem_raw);
   const uint32_t vring = smem0;
   const uint32_t cring = smem0 + kRing * a.vslot_bytes;
-  const uint32_t bars = cring + kRing * a.cslot_bytes;  // full_v empty_v full_c empty_c [kRing] each
+  const uint32_t bars = cring + kRing * a.cslot_bytes;  // full[kRing], empty[kRing]
   uint64_t* bar_ptr = reinterpret_cast<uint64_t*>(smem_raw + kRing * a.vslot_bytes +
                                                   kRing * a.cslot_bytes);
-
-  uint32_t b = blockIdx.x;
-  const uint32_t chunk = b % a.nchunks;
-  b /= a.nchunks;
-  const uint32_t t2 = b % a.tiles2;
-  const uint32_t t1 = b / a.tiles2;
-  const uint32_t base1 = t1 * T1, base2 = t2 * T2;
-  // planes [cbeg, cend) are updated; a plane outside the range (a slab's
-  // halo) is read as a neighbour, a missing one is the grid edge
-  const uint32_t c0 = a.cbeg + chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, a.cend);
+  __shared__ uint2 hdr[kRing];  // per-slot item header: (tile index, chunk)
+  const uint32_t hdr0 = smem_u32(hdr);
   const uint64_t s2 = n3p;
   const uint64_t s1 = static_cast<uint64_t>(n2) * n3p;
   const uint64_t s0 = static_cast<uint64_t>(n1) * s1;
   const uint32_t ncons = a.consumers;  // consumer threads (multiple of 32)
   const uint32_t nwarps_c = ncons >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nitems = a.items;
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < kRing; ++k) {
       mbar_init(bar_ptr + k, 1);
       mbar_init(bar_ptr + kRing + k, nwarps_c);
-      mbar_init(bar_ptr + 2 * kRing + k, 1);
-      mbar_init(bar_ptr + 3 * kRing + k, nwarps_c);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t last_v = (c1 < n0) ? c1 : n0 - 1;  // last V plane this chunk reads
   unsigned long long mbits = 0ull;
 
   if (threadIdx.x >= ncons) {
-    // ---------------- producer warp ----------------
+    // ---------------- producer thread ----------------
     if (lane == 0) {
-      for (uint32_t q = 0;; ++q) {
-        const uint32_t pv = c0 + q, pc = c0 + q;
-        const bool dv = pv <= last_v, dc = pc < c1;
-        if (!dv && !dc) break;
-        const uint32_t sl = q % kRing, use = q / kRing;
-        if (dv) {
+      uint32_t pos = 0;  // ring position (slot = pos % kRing, use = pos / kRing)
+      uint32_t w = blockIdx.x;
+      for (;;) {
+        // next item id fetched ahead (its latency hides behind this item)
+        uint32_t wn = kEndItem;
+        if (w < nitems) wn = gridDim.x + atomicAdd(&a.st->work_next, 1u);
+        if (w >= nitems) {
+          const uint32_t sl = pos % kRing, use = pos / kRing;
           mbar_wait(bars + (kRing + sl) * 8, (use & 1u) ^ 1u);
-          mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes);
-          tma_load4(vring + sl * a.vslot_bytes, vmap, 0, (int)base2 - 1, (int)base1 - 1, (int)pv,
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hdr0 + sl * 8), "r"(kEndItem),
+                       "r"(0u)
+                       : "memory");
+          mbar_arrive(bars + sl * 8);
+          break;
+        }
+        uint32_t t1, t2, chunk;
+        item_tile(a, w, t1, t2, chunk);
+        const uint32_t c0 = a.cbeg + chunk * a.L;
+        const uint32_t c1 = min(c0 + a.L, a.cend);
+        const uint32_t pbeg = c0 > 0 ? c0 - 1 : 0;
+        const uint32_t pend = c1 < n0 ? c1 : n0 - 1;
+        const int base1 = (int)(t1 * T1), base2 = (int)(t2 * T2);
+        for (uint32_t p = pbeg; p <= pend; ++p, ++pos) {
+          const uint32_t sl = pos % kRing, use = pos / kRing;
+          mbar_wait(bars + (kRing + sl) * 8, (use & 1u) ^ 1u);
+          if (p == pbeg)
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hdr0 + sl * 8),
+                         "r"(t1 * a.tiles2 + t2), "r"(chunk)
+                         : "memory");
+          const bool has_c = p >= c0 && p < c1;
+          mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes + (has_c ? a.cbox_bytes : 0u));
+          tma_load4(vring + sl * a.vslot_bytes, vmap, 0, base2 - 1, base1 - 1, (int)p,
                     bars + sl * 8);
+          if (has_c)
+            tma_load4(cring + sl * a.cslot_bytes, &a.mapc, 0, base2, base1, (int)p,
+                      bars + sl * 8);
         }
-        if (dc) {
-          mbar_wait(bars + (3 * kRing + sl) * 8, (use & 1u) ^ 1u);
-          mbar_arrive_expect_tx(bars + (2 * kRing + sl) * 8, a.cbox_bytes);
-          tma_load4(cring + sl * a.cslot_bytes, &a.mapc, 0, (int)base2, (int)base1, (int)pc,
-                    bars + (2 * kRing + sl) * 8);
-        }
+        w = wn;
       }
     }
   } else {
@@ -319,129 +423,153 @@ __global__ void __launch_bounds__(MAXT, 1)
     const uint32_t r = in_tile ? rr : 0u;
     const uint32_t r1 = r / T2;
     const uint32_t r2 = r - r1 * T2;
-    const uint32_t i1 = base1 + r1;
-    const uint32_t i2 = base2 + r2;
-    const bool active = in_tile && i1 < n1 && i2 < n2;
     const uint32_t i3 = kK * j;
-    // valid cells of the pencil (the padded tail of a row holds pad cells)
-    bool valid[kK];
-#pragma unroll
-    for (int c = 0; c < kK; ++c) valid[c] = active && (i3 + c < n3);
     const bool has_r = i3 + kK < n3;
     const bool has_l = i3 > 0;
     const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
-    // shared-memory byte offsets inside a V slot: own pencil and neighbours;
-    // a missing neighbour (grid edge) is aliased to the pencil itself so its
-    // difference is exactly (x - x) * inv = +0, the reference's ghost value
+    double inv3m[kK];  // inv3 for a face into a real cell, 0.0 into a pad cell
+#pragma unroll
+    for (int c = 0; c < kK; ++c) inv3m[c] = (i3 + c < n3) ? inv3 : 0.0;
     const uint32_t rowb = n3p * 8u;
     const uint32_t own = (((r1 + 1) * W2 + (r2 + 1)) * n3p + i3) * 8u;
-    const uint32_t o1m = (i1 > 0) ? own - W2 * rowb : own;
-    const uint32_t o1p = (i1 + 1 < n1) ? own + W2 * rowb : own;
-    const uint32_t o2m = (i2 > 0) ? own - rowb : own;
-    const uint32_t o2p = (i2 + 1 < n2) ? own + rowb : own;
     const uint32_t ol = has_l ? own - 8u : own;
     const uint32_t orr = has_r ? own + 8u * kK : own + 8u * (kK - 1);
     const uint32_t cown = (r * n3p + i3) * 8u;
+    double mdv = 0.0;
+    uint32_t pos = 0;  // ring position of the item's first plane
 
-    // loop-invariant slopes (row d, cell c); rows that do not vary along x3
-    // hold one pair for the whole pencil
-    double pos[4][kK], neg[4][kK];
+    for (;;) {
+      uint32_t sl = pos % kRing, ph = (pos / kRing) & 1u;
+      mbar_wait(bars + sl * 8, ph);
+      uint32_t tix, chunk;
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tix), "=r"(chunk) : "r"(hdr0 + sl * 8));
+      if (tix == kEndItem) break;
+      const uint32_t t1 = tix / a.tiles2, t2 = tix - t1 * a.tiles2;
+      const uint32_t c0 = a.cbeg + chunk * a.L;
+      const uint32_t c1 = min(c0 + a.L, a.cend);
+      const uint32_t pend = c1 < n0 ? c1 : n0 - 1;
+      const uint32_t i1 = t1 * T1 + r1;
+      const uint32_t i2 = t2 * T2 + r2;
+      const bool active = in_tile && i1 < n1 && i2 < n2;
+      // valid cells of the pencil (the padded tail of a row holds pad cells)
+      bool valid[kK];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-      const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+      for (int c = 0; c < kK; ++c) valid[c] = active && (i3 + c < n3);
+      // shared-memory byte offsets inside a V slot: own pencil and neighbours;
+      // a missing neighbour (grid edge) is aliased to the pencil itself so its
+      // difference is exactly (x - x) * inv = +0, the reference's ghost value
+      const uint32_t o1m = (i1 > 0) ? own - W2 * rowb : own;
+      const uint32_t o1p = (i1 + 1 < n1) ? own + W2 * rowb : own;
+      const uint32_t o2m = (i2 > 0) ? own - rowb : own;
+      const uint32_t o2p = (i2 + 1 < n2) ? own + rowb : own;
+
+      // loop-invariant slopes (row d, cell c); rows that do not vary along x3
+      // hold one pair for the whole pencil
+      double pos_[4][kK], neg_[4][kK];
 #pragma unroll
-      for (int c = 0; c < kK; ++c) {
-        if (c > 0 && !per_cell) {
-          pos[d][c] = pos[d][0];
-          neg[d][c] = neg[d][0];
-        } else {
-          const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-          if (S::B(d) < 0) {
-            pos[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
-            neg[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+      for (int d = 0; d < 4; ++d) {
+        const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          if (c > 0 && !per_cell) {
+            pos_[d][c] = pos_[d][0];
+            neg_[d][c] = neg_[d][0];
           } else {
-            const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-            const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
-            pos[d][c] = dr;
-            neg[d][c] = dr;
+            const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+            if (S::B(d) < 0) {
+              pos_[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+              neg_[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+            } else {
+              const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+              const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+              pos_[d][c] = dr;
+              neg_[d][c] = dr;
+            }
           }
         }
       }
-    }
-    // Linear rows (pos == neg == s: no input on the row): the Godunov flux of
-    // H(p) = s p is s * D+ for s >= 0 and s * D- otherwise (solver.cpp:52-63),
-    // and s * D- = s * ((v - vm) * inv) = |s| * ((vm - v) * inv) exactly (IEEE
-    // negation is exact and rounding symmetric; only the sign of a zero
-    // differs).  An off-march linear row therefore reads one neighbour, the
-    // upwind one: h = |s| * ((v_up - v) * inv).
-    bool up[4][kK];   // s >= 0 (sign bit clear)
-    double as[4][kK];  // |s|
+      // Linear rows (pos == neg == s: no input on the row): the Godunov flux
+      // of H(p) = s p is s * D+ for s >= 0 and s * D- otherwise
+      // (solver.cpp:52-63), and s * D- = s * ((v - vm) * inv) =
+      // |s| * ((vm - v) * inv) exactly (IEEE negation is exact and rounding
+      // symmetric; only the sign of a zero differs).  An off-march linear row
+      // therefore reads one neighbour, the upwind one:
+      // h = |s| * ((v_up - v) * inv).
+      bool up[4][kK];    // s >= 0 (sign bit clear)
+      double as[4][kK];  // |s|
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
+      for (int d = 0; d < 4; ++d) {
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          up[d][c] = sign_clear(pos_[d][c]);
+          as[d][c] =
+              __longlong_as_double(__double_as_longlong(pos_[d][c]) & 0x7fffffffffffffffll);
+        }
+      }
+      // slope shapes of the non-linear rows
+      RowShape shp[4][kK];
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          if (S::LIN(d)) continue;
+          shp[d][c] = (c > 0 && !per_cell) ? shp[d][0] : row_shape(pos_[d][c], neg_[d][c]);
+        }
+      }
+      constexpr bool pc1 = S::A(1) == 3 || S::B(1) == 3;
+      constexpr bool pc2 = S::A(2) == 3 || S::B(2) == 3;
+      // upwind neighbour offsets of linear rows 1, 2 (per cell when the slope
+      // varies along x3, else one for the pencil)
+      uint32_t o1u[kK], o2u[kK];
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
-        up[d][c] = sign_clear(pos[d][c]);
-        as[d][c] = __longlong_as_double(__double_as_longlong(pos[d][c]) & 0x7fffffffffffffffll);
+        o1u[c] = (up[1][c] ? o1p : o1m) + 8u * c;
+        o2u[c] = (up[2][c] ? o2p : o2m) + 8u * c;
       }
-    }
-    constexpr bool pc1 = S::A(1) == 3 || S::B(1) == 3;
-    constexpr bool pc2 = S::A(2) == 3 || S::B(2) == 3;
-    // upwind neighbour offsets of linear rows 1, 2 (per cell when the slope
-    // varies along x3, else one for the pencil)
-    uint32_t o1u[kK], o2u[kK];
-#pragma unroll
-    for (int c = 0; c < kK; ++c) {
-      o1u[c] = (up[1][c] ? o1p : o1m) + 8u * c;
-      o2u[c] = (up[2][c] ? o2p : o2m) + 8u * c;
-    }
 
-    double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
-                 static_cast<uint64_t>(c0) * s0;
-    // prologue: own pencil of plane c0-1 straight from global (once per chunk)
-    double v[kK], vp[kK];
-    mbar_wait(bars + 0, 0u);  // plane c0 in slot 0, first use
-    lds_cells<kK>(vring + own, v);
-    if (active && c0 > 0) {
-      const double* g = src + static_cast<uint64_t>(c0 - 1) * s0 + static_cast<uint64_t>(i1) * s1 +
-                        static_cast<uint64_t>(i2) * s2 + i3;
+      double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
+                   static_cast<uint64_t>(c0) * s0;
+      // prologue: V plane c0-1 (first slot of the item when c0 > 0) and c0
+      double v[kK], vp[kK];
+      if (c0 > 0) {
+        lds_cells<kK>(vring + sl * a.vslot_bytes + own, vp);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bars + (kRing + sl) * 8);
+        ++pos;
+        sl = pos % kRing;
+        ph = (pos / kRing) & 1u;
+        mbar_wait(bars + sl * 8, ph);
+        lds_cells<kK>(vring + sl * a.vslot_bytes + own, v);
+      } else {
+        lds_cells<kK>(vring + sl * a.vslot_bytes + own, v);
 #pragma unroll
-      for (int c = 0; c < kK; c += 2) {
-        const double2 x = ldg2(g + c);
-        vp[c] = x.x;
-        vp[c + 1] = x.y;
+        for (int c = 0; c < kK; ++c) vp[c] = v[c];  // D- at the i0 = 0 edge: +0
       }
-    } else {
+      // axis-0 carry: D- and its L product of the first plane
+      double dm0[kK], ka0[kK];
 #pragma unroll
-      for (int c = 0; c < kK; ++c) vp[c] = v[c];  // D- at the i0 = 0 edge: +0
-    }
-    // axis-0 carry: D- and its kink product of the first plane
-    double dm0[kK], ka0[kK];
-#pragma unroll
-    for (int c = 0; c < kK; ++c) {
-      dm0[c] = (v[c] - vp[c]) * inv0;
-      ka0[c] = S::LIN(0) ? 0.0 : kink(pos[0][c], neg[0][c], dm0[c]);
-    }
+      for (int c = 0; c < kK; ++c) {
+        dm0[c] = (v[c] - vp[c]) * inv0;
+        ka0[c] = S::LIN(0) ? 0.0 : pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
+      }
 
-    for (uint32_t rb = c0; rb < c1; rb += kRing) {
-      const uint32_t round = (rb - c0) / kRing;
-#pragma unroll
-      for (int k = 0; k < kRing; ++k) {
-        const uint32_t i0 = rb + k;
-        if (i0 >= c1) break;
-        const uint32_t slot_cur = vring + k * a.vslot_bytes;
-        const int kn = (k + 1) % kRing;
-        const uint32_t use_n = (k + 1 == kRing) ? round + 1 : round;
+      for (uint32_t i0 = c0; i0 < c1; ++i0) {
+        const uint32_t slot_cur = vring + sl * a.vslot_bytes;
+        const uint32_t csl = cring + sl * a.cslot_bytes;
+        const uint32_t bar_cur = bars + sl * 8;
+        const uint32_t sn = sl + 1 == kRing ? 0u : sl + 1;
+        const uint32_t pn = sn == 0 ? ph ^ 1u : ph;
         double vn[kK];
         if (i0 + 1 < n0) {
-          mbar_wait_nc(bars + kn * 8, use_n & 1u);
-          lds_cells<kK>(vring + kn * a.vslot_bytes + own, vn);
+          mbar_wait_nc(bars + sn * 8, pn);
+          lds_cells<kK>(vring + sn * a.vslot_bytes + own, vn);
         } else {
 #pragma unroll
           for (int c = 0; c < kK; ++c) vn[c] = v[c];  // D+ at the i0 = n0-1 edge: +0
         }
-        mbar_wait_nc(bars + (2 * kRing + k) * 8, round & 1u);
         double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
-        lds_cells<kK>(cring + k * a.cslot_bytes + cown, cc);
+        lds_cells<kK>(csl + cown, cc);
         if (S::LIN(1)) {  // upwind neighbour only (n1p holds it)
           if (pc1) {
 #pragma unroll
@@ -469,21 +597,22 @@ __global__ void __launch_bounds__(MAXT, 1)
 
         // axis-3 faces of the pencil: f3[c] is D- of cell c, f3[c+1] its D+;
         // faces past the last real cell are the reference's zero ghost
+        // (a pad cell's difference times 0.0: +-0, pad values are finite)
         double f3[kK + 1];
         f3[0] = (v[0] - vl) * inv3;
 #pragma unroll
-        for (int c = 1; c < kK; ++c) {
-          const double f = (v[c] - v[c - 1]) * inv3;
-          f3[c] = valid[c] ? f : 0.0;
-        }
+        for (int c = 1; c < kK; ++c) f3[c] = (v[c] - v[c - 1]) * inv3m[c];
         f3[kK] = (vr - v[kK - 1]) * inv3;
         constexpr bool row3_shared = !(S::A(3) == 3 || S::B(3) == 3);
-        double k3a[kK + 1], k3b[kK + 1];  // kink products of faces, as D+ (a) / D- (b) users
+        // row 3: each face's L product (cell above uses it as A) and R
+        // product (cell below uses it as B)
+        double k3a[kK + 1], k3b[kK + 1];
         if (row3_shared && !S::LIN(3)) {
 #pragma unroll
           for (int c = 0; c <= kK; ++c) {
-            k3a[c] = kink(pos[3][0], neg[3][0], f3[c]);
-            k3b[c] = k3a[c];
+            const uint32_t sb = sign_bit(f3[c]);
+            if (c < kK) k3a[c] = pair_kink(shp[3][0].L, f3[c], sb);
+            if (c > 0) k3b[c] = pair_kink(shp[3][0].R, f3[c], sb);
           }
         }
         double out[kK];
@@ -493,11 +622,11 @@ __global__ void __launch_bounds__(MAXT, 1)
           const double dp0 = (vn[c] - v[c]) * inv0;
           double h0;
           if (S::LIN(0)) {
-            h0 = pos[0][c] * (up[0][c] ? dp0 : dm0[c]);
+            h0 = pos_[0][c] * (up[0][c] ? dp0 : dm0[c]);
           } else {
-            const double kb0 = kink(pos[0][c], neg[0][c], dp0);
-            h0 = godunov_select(ka0[c], kb0, dm0[c], dp0);
-            ka0[c] = kb0;
+            const uint32_t sb = sign_bit(dp0);
+            h0 = shape_pick(shp[0][c], ka0[c], pair_kink(shp[0][c].R, dp0, sb));
+            ka0[c] = pair_kink(shp[0][c].L, dp0, sb);
           }
           dm0[c] = dp0;
           // axis 1
@@ -507,8 +636,8 @@ __global__ void __launch_bounds__(MAXT, 1)
           } else {
             const double dm1 = (v[c] - n1m[c]) * inv1;
             const double dp1 = (n1p[c] - v[c]) * inv1;
-            h1 = godunov_select(kink(pos[1][c], neg[1][c], dm1), kink(pos[1][c], neg[1][c], dp1),
-                                dm1, dp1);
+            h1 = shape_pick(shp[1][c], pair_kink(shp[1][c].L, dm1, sign_bit(dm1)),
+                            pair_kink(shp[1][c].R, dp1, sign_bit(dp1)));
           }
           // axis 2
           double h2;
@@ -517,28 +646,27 @@ __global__ void __launch_bounds__(MAXT, 1)
           } else {
             const double dm2 = (v[c] - n2m[c]) * inv2;
             const double dp2 = (n2p[c] - v[c]) * inv2;
-            h2 = godunov_select(kink(pos[2][c], neg[2][c], dm2), kink(pos[2][c], neg[2][c], dp2),
-                                dm2, dp2);
+            h2 = shape_pick(shp[2][c], pair_kink(shp[2][c].L, dm2, sign_bit(dm2)),
+                            pair_kink(shp[2][c].R, dp2, sign_bit(dp2)));
           }
           // axis 3
           double h3;
           if (S::LIN(3)) {
-            h3 = pos[3][c] * (up[3][c] ? f3[c + 1] : f3[c]);
+            h3 = pos_[3][c] * (up[3][c] ? f3[c + 1] : f3[c]);
           } else if (row3_shared) {
-            h3 = godunov_select(k3a[c], k3b[c + 1], f3[c], f3[c + 1]);
+            h3 = shape_pick(shp[3][0], k3a[c], k3b[c + 1]);
           } else {
-            h3 = godunov_select(kink(pos[3][c], neg[3][c], f3[c]),
-                                kink(pos[3][c], neg[3][c], f3[c + 1]), f3[c], f3[c + 1]);
+            h3 = shape_pick(shp[3][c], pair_kink(shp[3][c].L, f3[c], sign_bit(f3[c])),
+                            pair_kink(shp[3][c].R, f3[c + 1], sign_bit(f3[c + 1])));
           }
           // hhat = 0.0 + h0 + h1 + h2 + h3 (0.0 + h0 == h0 in value)
           const double hh = ((h0 + h1) + h2) + h3;
           const double st = v[c] + a.dt * hh;
           out[c] = st > cc[c] ? st : cc[c];
-          // |dV| bits: clear the sign (== std::abs).  The unsigned max of the
-          // bits orders non-negative doubles; a NaN (above +inf) is filtered
-          // after the march (rare path below)
-          const unsigned long long ib = abs_bits(out[c] - v[c]);
-          if (valid[c]) mbits = umax64(mbits, ib);
+          // max |dV| as the reference keeps it: `if (dv > max_dv)`
+          // (solver.cpp:181-182), so a NaN never wins
+          const double dv = fabs(out[c] - v[c]);
+          if (valid[c] && dv > mdv) mdv = dv;
         }
         if (active) {
 #pragma unroll
@@ -548,33 +676,24 @@ __global__ void __launch_bounds__(MAXT, 1)
         op += s0;
 #pragma unroll
         for (int c = 0; c < kK; ++c) v[c] = vn[c];
-        // plane i0 (V) and c plane i0 are no longer read by this warp
+        // V plane i0 and c plane i0 are no longer read by this warp
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(bars + (kRing + k) * 8);
-          mbar_arrive(bars + (3 * kRing + k) * 8);
-        }
+        if (lane == 0) mbar_arrive(bar_cur + kRing * 8);
+        sl = sn;
+        ph = pn;
+        ++pos;
+      }
+      if (pend == c1) {  // trailing V plane c1 (read as D+ only): release it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bars + (kRing + sl) * 8);
+        ++pos;
       }
     }
-    if (mbits > 0x7ff0000000000000ull) {
-      // a NaN |dV| won the unfiltered max: redo this pencil's max from global
-      // memory with the reference's filter (a NaN never passes
-      // `if (dv > max_dv)`, solver.cpp:181-182).  Cold path.
-      mbits = 0ull;
-      const uint64_t rowo = static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3;
-      for (uint32_t i0 = c0; i0 < c1; ++i0) {
-        const uint64_t o = static_cast<uint64_t>(i0) * s0 + rowo;
-#pragma unroll
-        for (int c = 0; c < kK; ++c) {
-          if (!valid[c]) continue;
-          const unsigned long long ib = abs_bits(dst[o + c] - src[o + c]);
-          if (ib <= 0x7ff0000000000000ull) mbits = umax64(mbits, ib);
-        }
-      }
-    }
+    mbits = (unsigned long long)__double_as_longlong(mdv);
   }
 
-  // CTA max -> global, last CTA runs the sweep epilogue (solver.cpp:347-369)
+  // CTA max -> global; the last CTA resets the work counter and, in the
+  // device loop, runs the sweep epilogue (solver.cpp:347-369)
   __shared__ unsigned long long part[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
@@ -587,12 +706,17 @@ __global__ void __launch_bounds__(MAXT, 1)
   if (lane != 0) return;
   LoopState* st = a.st;
   if (mbits) atomicMax(&st->maxdv_bits, mbits);
-  if (a.loop != 1) return;  // single step / sharded: no fused epilogue
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  loop_epilogue(st, a.handle, a.use_handle);
+  if (a.loop == 1) {
+    loop_epilogue(st, a.handle, a.use_handle);
+  } else {  // single step / sharded slab: the caller consumes maxdv_bits
+    st->blocks_done = 0u;
+    st->work_next = 0u;
+    __threadfence();
+  }
 }
 
 // Sharded loop: after the residual all-reduce, one thread applies the
@@ -666,7 +790,7 @@ static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 12
 static size_t fast4d_smem(uint32_t T1, uint32_t T2, uint32_t n3p) {
   const size_t rv = (T1 + 2) * (T2 + 2), rc = T1 * T2;
   return kRing * (size_t)round128(rv * n3p * sizeof(double)) +
-         kRing * (size_t)round128(rc * n3p * sizeof(double)) + 4 * kRing * sizeof(uint64_t);
+         kRing * (size_t)round128(rc * n3p * sizeof(double)) + 2 * kRing * sizeof(uint64_t);
 }
 
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
@@ -705,29 +829,26 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.cbox_bytes = a.T1 * a.T2 * a.n3p * 8u;
   a.vslot_bytes = round128(a.vbox_bytes);
   a.cslot_bytes = round128(a.cbox_bytes);
-  // one resident CTA per SM.  Split the axis-0 march into nch chunks to
-  // balance waves; every chunk pays a ring prologue (~3 plane-steps), so
-  // minimise waves * (chunk length + 3).
+  // persistent grid: one resident CTA per SM pulling items (tile x chunk of
+  // planes) off a counter.  Chunks of the axis-0 march give the schedule
+  // enough items to balance (~4 per CTA) when tiles are few; each chunk
+  // costs one extra V plane at each end, so chunks stay >= 8 planes.
   const uint32_t tiles = a.tiles1 * a.tiles2;
-  uint32_t nch = 1;
-  double best_cost = 1e30;
   if (a.cend == 0) {
     a.cbeg = 0;
     a.cend = g.n[0];
   }
   const uint32_t span = a.cend - a.cbeg;
-  for (uint32_t k = 1; k <= 16 && k <= span; ++k) {
-    const uint32_t waves = (tiles * k + sms - 1) / sms;
-    const double cost = double(waves) * (double((span + k - 1) / k) + 3.0);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      nch = k;
-    }
-  }
-  uint32_t L = (span + nch - 1) / nch;
+  uint32_t nch = 1;
+  if (tiles < 3u * sms) nch = std::min<uint32_t>((4u * sms + tiles - 1) / tiles,
+                                                 std::max<uint32_t>(1u, span / 8u));
+  if (const char* e = std::getenv("HJB_NCH")) nch = std::max(1, std::atoi(e));
+  nch = std::min(nch, span);
+  const uint32_t L = (span + nch - 1) / nch;
   a.L = L;
   a.nchunks = (span + L - 1) / L;
-  a.blocks = tiles * a.nchunks;
+  a.items = tiles * a.nchunks;
+  a.blocks = std::min<uint32_t>(a.items, static_cast<uint32_t>(sms));
 }
 
 template <class S, int K, int MAXT>
@@ -750,7 +871,7 @@ static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
   else if (a.maxthreads == 448)
     launch_one<S, 2, 448>(a, s);
   else
-    launch_one<S, 2, 640>(a, s);
+    launch_one<S, 2, 576>(a, s);
 }
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {

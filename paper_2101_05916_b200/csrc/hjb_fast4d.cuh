@@ -19,8 +19,8 @@ struct Fast4dArgs {
   uint32_t n3p;  // padded contiguous extent (even)
   double inv[4];
   uint32_t kcells;      // cells per thread along the contiguous axis (2 or 4)
-  uint32_t maxthreads;  // CTA thread bound of the variant: (2, 640), (2, 448), (4, 384)
-  uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads, consumers, smem;
+  uint32_t maxthreads;  // CTA thread bound of the variant: (2, 576), (2, 448), (4, 384)
+  uint32_t T1, T2, tiles1, tiles2, L, nchunks, items, blocks, threads, consumers, smem;
   uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
   const double* tab;
   int off_pos[4], off_neg[4], off_a[4], off_b[4];

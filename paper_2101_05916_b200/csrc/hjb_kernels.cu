@@ -101,6 +101,7 @@ __device__ void finish_sweep(const StepArgs& a, double local_max) {
   if (st->horizon > 0.0 && (double)iter * st->dt >= st->horizon) stop = true;
   st->maxdv_bits = 0ull;
   st->blocks_done = 0u;
+  st->work_next = 0u;
   if (stop) {
     st->done = 1;
     if (a.use_handle) cudaGraphSetConditional(a.handle, 0u);
@@ -470,6 +471,7 @@ __global__ void k_loop_init(LoopState* st, long long max_iters, double dt, doubl
                             double* wall_history) {
   st->maxdv_bits = 0ull;
   st->blocks_done = 0u;
+  st->work_next = 0u;
   st->done = 0;
   st->status = 0;
   st->converged = 0;

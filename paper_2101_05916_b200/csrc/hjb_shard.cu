@@ -173,7 +173,7 @@ int hjb_sweep_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* 
   Fast4dArgs f;
   std::memset(&f, 0, sizeof f);
   f.kcells = 2;
-  f.maxthreads = 640;
+  f.maxthreads = 576;
   f.cbeg = static_cast<uint32_t>(plane_begin);
   f.cend = static_cast<uint32_t>(plane_end);
   int sms = 0;
@@ -277,7 +277,7 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   Fast4dArgs f;
   std::memset(&f, 0, sizeof f);
   f.kcells = 2;
-  f.maxthreads = 640;
+  f.maxthreads = 576;
   f.cbeg = has_lo ? 1u : 0u;
   f.cend = f.cbeg + owned;
   int sms = 0;
