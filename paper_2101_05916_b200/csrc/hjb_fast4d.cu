@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include <cudaTypedefs.h>
 
@@ -368,6 +369,14 @@ __global__ void __launch_bounds__(MAXT, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // slope tables -> shared memory once per CTA (per-item slope loads are
+  // then shared-memory hits)
+  const double* tabs = a.tab;
+  if (a.tab_staged) {
+    double* t = reinterpret_cast<double*>(smem_raw + a.tab_off);
+    for (uint32_t k = threadIdx.x; k < a.tab_len; k += blockDim.x) t[k] = __ldg(a.tab + k);
+    tabs = t;
+  }
   __syncthreads();
   unsigned long long mbits = 0ull;
 
@@ -477,11 +486,11 @@ __global__ void __launch_bounds__(MAXT, 1)
           } else {
             const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
             if (S::B(d) < 0) {
-              pos_[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
-              neg_[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+              pos_[d][c] = tabs[a.off_pos[d] + ka];
+              neg_[d][c] = tabs[a.off_neg[d] + ka];
             } else {
               const uint32_t kb = active ? pick<S>(S::B(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-              const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+              const double dr = tabs[a.off_a[d] + ka] + tabs[a.off_b[d] + kb];
               pos_[d][c] = dr;
               neg_[d][c] = dr;
             }
@@ -787,10 +796,11 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
 
 static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 128 * 128); }
 
-static size_t fast4d_smem(uint32_t T1, uint32_t T2, uint32_t n3p) {
+static size_t fast4d_smem(uint32_t T1, uint32_t T2, uint32_t n3p, uint32_t tab_len) {
   const size_t rv = (T1 + 2) * (T2 + 2), rc = T1 * T2;
   return kRing * (size_t)round128(rv * n3p * sizeof(double)) +
-         kRing * (size_t)round128(rc * n3p * sizeof(double)) + 2 * kRing * sizeof(uint64_t);
+         kRing * (size_t)round128(rc * n3p * sizeof(double)) + 2 * kRing * sizeof(uint64_t) +
+         (size_t)tab_len * sizeof(double);
 }
 
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
@@ -806,9 +816,10 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   uint32_t bestT1 = 1, bestT2 = 1;
   double best = 1e30;
   const uint32_t maxc = a.maxthreads - 32;  // consumers; one producer warp
+  const uint32_t tab_small = a.tab_len <= 4096u ? a.tab_len : 0u;  // staged tables (<= 32 KB)
   for (uint32_t T1 = 1; T1 <= g.n[1] && T1 * J <= maxc; ++T1) {
     for (uint32_t T2 = 1; T2 <= g.n[2] && T1 * T2 * J <= maxc; ++T2) {
-      if (fast4d_smem(T1, T2, a.n3p) > 200 * 1024) continue;
+      if (fast4d_smem(T1, T2, a.n3p, tab_small) > 200 * 1024) continue;
       const double ratio = double((T1 + 2) * (T2 + 2)) / double(T1 * T2);
       const double score = ratio - 1e-3 * T1 * T2;
       if (score < best) {
@@ -824,24 +835,32 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.tiles2 = (g.n[2] + a.T2 - 1) / a.T2;
   a.consumers = ((a.T1 * a.T2 * J + 31) / 32) * 32;
   a.threads = a.consumers + 32;
-  a.smem = static_cast<uint32_t>(fast4d_smem(a.T1, a.T2, a.n3p));
+  a.smem = static_cast<uint32_t>(fast4d_smem(a.T1, a.T2, a.n3p, tab_small));
+  a.tab_off = static_cast<uint32_t>(fast4d_smem(a.T1, a.T2, a.n3p, 0));
+  a.tab_staged = tab_small > 0 ? 1 : 0;
+  if (a.smem > 200 * 1024) {  // tables too large to stage: read them from global memory
+    a.tab_staged = 0;
+    a.smem = a.tab_off;
+  }
   a.vbox_bytes = (a.T1 + 2) * (a.T2 + 2) * a.n3p * 8u;
   a.cbox_bytes = a.T1 * a.T2 * a.n3p * 8u;
   a.vslot_bytes = round128(a.vbox_bytes);
   a.cslot_bytes = round128(a.cbox_bytes);
   // persistent grid: one resident CTA per SM pulling items (tile x chunk of
   // planes) off a counter.  Chunks of the axis-0 march give the schedule
-  // enough items to balance (~4 per CTA) when tiles are few; each chunk
-  // costs one extra V plane at each end, so chunks stay >= 8 planes.
+  // more items to balance when tiles are few; each chunk costs an extra V
+  // plane at each end and a per-item set-up, so chunks stay long.
   const uint32_t tiles = a.tiles1 * a.tiles2;
   if (a.cend == 0) {
     a.cbeg = 0;
     a.cend = g.n[0];
   }
   const uint32_t span = a.cend - a.cbeg;
+  // measured (B200): 51^4 and 71^4 best at 2 chunks, 101^4 at 1
   uint32_t nch = 1;
-  if (tiles < 3u * sms) nch = std::min<uint32_t>((4u * sms + tiles - 1) / tiles,
-                                                 std::max<uint32_t>(1u, span / 8u));
+  if (tiles < 3u * sms)
+    nch = std::min<uint32_t>(std::max<uint32_t>(2u, (2u * sms + tiles - 1) / tiles),
+                             std::max<uint32_t>(1u, span / 8u));
   if (const char* e = std::getenv("HJB_NCH")) nch = std::max(1, std::atoi(e));
   nch = std::min(nch, span);
   const uint32_t L = (span + nch - 1) / nch;
@@ -859,7 +878,25 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
                          200 * 1024);
     attr_set = true;
   }
-  k_fast4d<S, K, MAXT><<<a.blocks, a.threads, a.smem, s>>>(a);
+  if (a.l2_bytes == 0) {
+    k_fast4d<S, K, MAXT><<<a.blocks, a.threads, a.smem, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.blocks);
+  cfg.blockDim = dim3(a.threads);
+  cfg.dynamicSmemBytes = a.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(a.l2_base);
+  at[0].val.accessPolicyWindow.num_bytes = a.l2_bytes;
+  at[0].val.accessPolicyWindow.hitRatio = a.l2_hit;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
@@ -882,6 +919,33 @@ cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   else
     launch_shape<ShapeTwin>(a, s);
   return cudaGetLastError();
+}
+
+bool l2_pin(int device, Fast4dArgs& a, const void* base, size_t bytes) {
+  a.l2_base = nullptr;
+  a.l2_bytes = 0;
+  a.l2_hit = 0.f;
+  const char* e = std::getenv("HJB_L2PIN");  // opt-in: measured slower at 51^4
+  if (!(e && std::strcmp(e, "1") == 0)) return false;
+  int maxp = 0, maxw = 0;
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device);
+  if (maxp <= 0 || maxw <= 0 || bytes > (size_t)maxp || bytes > (size_t)maxw) return false;
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  a.l2_base = base;
+  a.l2_bytes = bytes;
+  a.l2_hit = 1.f;
+  return true;
+}
+
+void l2_release(Fast4dArgs& a) {
+  if (a.l2_bytes == 0) return;
+  cudaCtxResetPersistingL2Cache();
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  a.l2_bytes = 0;
 }
 
 cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const double* c) {

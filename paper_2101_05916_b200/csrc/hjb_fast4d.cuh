@@ -22,7 +22,10 @@ struct Fast4dArgs {
   uint32_t maxthreads;  // CTA thread bound of the variant: (2, 576), (2, 448), (4, 384)
   uint32_t T1, T2, tiles1, tiles2, L, nchunks, items, blocks, threads, consumers, smem;
   uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
-  const double* tab;
+  const double* tab;    // slope tables (staged into shared memory per CTA)
+  uint32_t tab_len;     // doubles in tab
+  uint32_t tab_off;     // shared-memory byte offset of the staged copy
+  int tab_staged;       // 1: tables staged in shared memory, 0: read from global
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
   const double* c;  // padded constraint
   double* buf0;
@@ -34,6 +37,11 @@ struct Fast4dArgs {
   int loop;  // 0 single step, 1 device loop (fused epilogue), 2 sharded slab sweep
   cudaGraphConditionalHandle handle;
   int use_handle;
+  // L2 residency of the constraint (read every sweep, never written): an
+  // access-policy window attached to each launch; l2_bytes == 0 disables
+  const void* l2_base;
+  size_t l2_bytes;
+  float l2_hit;
 };
 
 // Model shape id for the fast path, or -1 when the generic kernel must run
@@ -44,6 +52,11 @@ cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
 // Encode the three TMA tensor maps for the padded buffers (driver entry point
 // fetched through the runtime; no libcuda link dependency).
 cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const double* c);
+// Persisting-L2 carve-out for the constraint of a solve: sets the device
+// limit and fills a.l2_*; l2_release() undoes it.  No-op (returns false)
+// when the constraint does not fit the carve-out or HJB_L2PIN=0.
+bool l2_pin(int device, Fast4dArgs& a, const void* base, size_t bytes);
+void l2_release(Fast4dArgs& a);
 cudaError_t launch_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
                             cudaStream_t s);
 cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,

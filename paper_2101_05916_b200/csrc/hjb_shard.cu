@@ -178,6 +178,7 @@ int hjb_sweep_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* 
   f.cend = static_cast<uint32_t>(plane_end);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  f.tab_len = static_cast<uint32_t>(p.hm.tab.size());
   fast4d_config(p.g, sms > 0 ? sms : 148, f);
   const uint64_t rows = static_cast<uint64_t>(p.g.n[0]) * p.g.n[1] * p.g.n[2];
   const size_t pb = rows * f.n3p * sizeof(double);
@@ -282,6 +283,7 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   f.cend = f.cbeg + owned;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  f.tab_len = static_cast<uint32_t>(p.hm.tab.size());
   fast4d_config(gloc, sms > 0 ? sms : 148, f);
   const uint64_t plane = static_cast<uint64_t>(p.g.n[1]) * p.g.n[2] * f.n3p;  // padded plane
   const uint64_t rows_owned = static_cast<uint64_t>(owned) * p.g.n[1] * p.g.n[2];
