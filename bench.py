@@ -275,16 +275,24 @@ def run_hjb(args):
         ms = float(t.item())
     value = world * args.steps * args.iters * cells / (ms * 1e-3)
 
-    # e2e: reference-facing ABI with host buffers (H2D init + c, D2H V*)
-    c_host = hj.ScalarField(grid, c_t.cpu().numpy(), check=False)
-    init_host = hj.ScalarField(grid, c_host.values().copy(), check=False)
+    # e2e: reference-facing ABI with host buffers (H2D init + c, D2H V*),
+    # page-locked host arrays as a serving caller would keep them
+    c_pin = torch.empty(cells, dtype=torch.float64, pin_memory=True)
+    c_pin.copy_(c_t)
+    i_pin = torch.empty(cells, dtype=torch.float64, pin_memory=True)
+    i_pin.copy_(c_t)
+    o_pin = torch.empty(cells, dtype=torch.float64, pin_memory=True)
+    c_host = hj.ScalarField(grid, c_pin.numpy(), check=False)
+    init_host = hj.ScalarField(grid, i_pin.numpy(), check=False)
+    out_host = o_pin.numpy()
     for _ in range(max(1, args.warmup // 2)):
-        hj.solve(init_host, c_host, model, db, cfg, ctx=ctx, history_capacity=0)
+        hj.solve(init_host, c_host, model, db, cfg, ctx=ctx, history_capacity=0, out=out_host)
     e2e_steps = max(2, min(args.steps, 5))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res = hj.solve(init_host, c_host, model, db, cfg, ctx=ctx, history_capacity=0)
+        res = hj.solve(init_host, c_host, model, db, cfg, ctx=ctx, history_capacity=0,
+                       out=out_host)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_rate = world * args.iters * cells / e2e_s
 
@@ -316,7 +324,8 @@ def run_hjb(args):
                      "bytes_per_cell": BYTES_PER_CELL, "peak_source": peak_src,
                      "sweep_us": sweep * 1e6},
         "e2e": {"value": e2e_rate, "unit": UNIT, "h2d_bytes_per_step": 2 * cells * 8,
-                "d2h_bytes_per_step": cells * 8, "ms_per_step": e2e_s * 1e3},
+                "d2h_bytes_per_step": cells * 8, "ms_per_step": e2e_s * 1e3,
+                "path": "hjsafe.solve -> hjb_solve (C ABI), page-locked host init/c/out"},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
         "final_residual": res.final_residual,

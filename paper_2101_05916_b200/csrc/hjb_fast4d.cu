@@ -816,7 +816,10 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   uint32_t bestT1 = 1, bestT2 = 1;
   double best = 1e30;
   const uint32_t maxc = a.maxthreads - 32;  // consumers; one producer warp
-  const uint32_t tab_small = a.tab_len <= 4096u ? a.tab_len : 0u;  // staged tables (<= 32 KB)
+  // staged slope tables (<= 32 KB; HJB_TAB_GLOBAL=1 forces global reads)
+  const char* tg = std::getenv("HJB_TAB_GLOBAL");
+  const bool stage = a.tab_len <= 4096u && !(tg && std::strcmp(tg, "1") == 0);
+  const uint32_t tab_small = stage ? a.tab_len : 0u;
   for (uint32_t T1 = 1; T1 <= g.n[1] && T1 * J <= maxc; ++T1) {
     for (uint32_t T2 = 1; T2 <= g.n[2] && T1 * T2 * J <= maxc; ++T2) {
       if (fast4d_smem(T1, T2, a.n3p, tab_small) > 200 * 1024) continue;

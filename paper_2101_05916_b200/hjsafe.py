@@ -835,8 +835,12 @@ def vi_step(value: ScalarField, constraint: ScalarField, model: DynamicsModel,
 
 def solve(init: ScalarField, constraint: ScalarField, model: DynamicsModel,
           dbounds: IntervalField, cfg: SolveConfig | None = None,
-          ctx: Context | None = None, history_capacity: int | None = None) -> SolveResult:
-    """solver.hpp:63-65: iterate vi_step to a fixed point on the GPU."""
+          ctx: Context | None = None, history_capacity: int | None = None,
+          out: np.ndarray | None = None) -> SolveResult:
+    """solver.hpp:63-65: iterate vi_step to a fixed point on the GPU.
+
+    ``out`` (optional, float64, grid size, C-contiguous) receives V*; pass a
+    page-locked array to make the device->host copy a direct DMA."""
     cfg = cfg or SolveConfig()
     cfg.validate()
     if not (init.grid() == constraint.grid()):
@@ -846,7 +850,12 @@ def solve(init: ScalarField, constraint: ScalarField, model: DynamicsModel,
     lib = abi.load()
     cap = int(cfg.max_iters if history_capacity is None else history_capacity)
     r, rh, wh = _c_result(cap)
-    out = np.empty(init.size(), dtype=np.float64)
+    if out is None:
+        out = np.empty(init.size(), dtype=np.float64)
+    elif (out.dtype != np.float64 or out.size != init.size() or not out.flags.c_contiguous
+          or not out.flags.writeable):
+        raise InvalidArgument("solve: out must be a writeable C-contiguous float64 array of grid size")
+    out = out.reshape(-1)
     g, m, d, c = init.grid().to_c(), model.to_c(), dbounds.to_c(), cfg.to_c()
     _check(lib.hjb_solve(_ctx(ctx), C.byref(g), C.byref(m), C.byref(d), init.ptr(),
                          constraint.ptr(), C.byref(c), out.ctypes.data_as(C.c_void_p), C.byref(r)))

@@ -191,3 +191,39 @@ def test_nan_cell_never_wins_the_residual(gpu_ctx, monkeypatch, fast):
     dv = np.abs(out - v0)
     want = dv[np.isfinite(dv)].max() / r.dt
     assert r.iterations == 1 and r.residual_history[0] == want
+
+
+@pytest.mark.parametrize("nch,tab_global", [("1", "0"), ("3", "0"), ("7", "1"), ("13", "0")])
+def test_fast4d_item_schedule_and_tables(gpu_ctx, oracle, monkeypatch, nch, tab_global):
+    """The persistent kernel's work items (tile x chunk of planes, dynamic
+    schedule) and both slope-table paths (shared-memory staged / global)
+    give the oracle's bits; chunk counts that do not divide the axis."""
+    monkeypatch.setenv("HJB_NCH", nch)
+    monkeypatch.setenv("HJB_TAB_GLOBAL", tab_global)
+    g = hj.Grid([(-5.0, 5.0, 29), (-2.0, 2.0, 13), (-0.35, 0.35, 11), (-1.5, 1.5, 9)])
+    model = configs.planar_model()
+    db = hj.IntervalField.constant(g, [hj.Interval(-0.7, 0.3)])
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=25)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+@pytest.mark.parametrize("wind", [(0.0, 0.0), (-3.0, -2.5), (2.5, 3.0), (-0.2, 0.9)])
+def test_fast4d_slope_shapes(gpu_ctx, oracle, wind):
+    """Disturbance intervals that make the wind row non-decreasing,
+    non-increasing, V-shaped or linear over the whole grid (every Godunov
+    shape branch of the fast kernel) against the oracle."""
+    g = hj.Grid([(-5.0, 5.0, 15), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 11)])
+    model = configs.planar_model()
+    db = hj.IntervalField.constant(g, [hj.Interval(*wind)])
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    cfg = hj.SolveConfig(tolerance=1e-5, max_iters=30)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
