@@ -3,24 +3,24 @@
 // Same arithmetic as the reference's update_chunk (solver.cpp:106-190,
 // Godunov branch) on every node, organised for HBM streaming:
 //
-//  * internal padded layout [n0][n1][n2][n3p], n3p = n3 rounded up to even,
-//    so every thread's 2-cell pencil along the contiguous axis is one aligned
-//    16-byte vector (LDG.128 / STG.128);
-//  * each thread owns one pencil at fixed (i1, i2) and MARCHES along axis 0
-//    with a register queue V[i0-1], V[i0], V[i0+1], V[i0+2] (prefetch
-//    distance 2), so every V element is streamed from HBM once per sweep;
-//    the axis-0 face difference D+ of step i0 is reused as D- of step i0+1,
-//    and the shared axis-3 face inside the pencil is computed once;
-//  * in-plane neighbours (axes 1-3) come from L1/L2: CTAs cover T1 x T2
-//    tiles of (i1, i2) rows and march in near-lockstep, so halo rows are
-//    L2 hits;
-//  * Godunov slopes of rows that do not depend on x0 are loop invariant and
-//    live in registers for the whole march;
-//  * the Godunov flux is evaluated in a branch-free, value-exact form: the
-//    two products the reference forms (ha, hb) are computed identically and
-//    the selection logic (solver.cpp:52-63) is restated with sign-bit tests
-//    (every case where a sign test could differ from the reference's `> 0`
-//    involves an exact zero operand, where both candidate results are +-0).
+//  * internal padded layout [n0][n1][n2][n3p], n3p = n3 rounded up to the
+//    per-thread cell count, so every thread's pencil along the contiguous
+//    axis is aligned 16-byte vectors and a TMA tensor map describes a tile;
+//  * persistent CTAs (one per SM) pull work items (tile of (i1, i2) rows x a
+//    chunk of axis-0 planes) off a device counter; a producer thread streams
+//    each item's V planes (tile + 1-row halo) and c planes with 4D bulk
+//    tensor copies into a shared-memory ring (full/empty mbarriers), so every
+//    V element is read from HBM about once per sweep and halo rows are L2 hits;
+//  * consumer threads march their pencil along axis 0: the face difference
+//    D+ of plane i0 is D- of plane i0+1, faces shared inside the pencil are
+//    computed once;
+//  * Godunov slopes never depend on x0 in this path: they are loop invariant
+//    per item, read from shared-memory copies of the host-built tables and
+//    classified once (linear row / slope shape, see RowShape);
+//  * every rewrite of the flux is value-exact: candidate products are formed
+//    exactly as the reference forms them and only the selection logic is
+//    restated (cases where a sign-bit test differs from the reference's
+//    `> 0` involve an exact zero operand, where the candidates are +-0).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
