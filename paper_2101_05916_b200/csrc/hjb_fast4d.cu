@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -830,6 +831,14 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
         bestT1 = T1;
         bestT2 = T2;
       }
+    }
+  }
+  if (const char* e = std::getenv("HJB_TILE")) {  // experiment override "T1xT2"
+    unsigned x = 0, y = 0;
+    if (std::sscanf(e, "%ux%u", &x, &y) == 2 && x > 0 && y > 0 && x * y * J <= maxc &&
+        fast4d_smem(x, y, a.n3p, tab_small) <= 200 * 1024) {
+      bestT1 = x;
+      bestT2 = y;
     }
   }
   a.T1 = bestT1;
