@@ -176,7 +176,10 @@ __device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, 
   __threadfence();
 }
 
-constexpr int kRing = 6;  // planes in flight per ring (prefetch distance kRing - 1)
+#ifndef HJB_RING
+#define HJB_RING 6
+#endif
+constexpr int kRing = HJB_RING;  // planes in flight per ring (prefetch distance kRing - 1)
 
 template <int K>
 __device__ __forceinline__ void lds_cells(uint32_t addr, double* v) {
