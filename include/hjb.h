@@ -296,6 +296,75 @@ int hjb_sweep_planes_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model
                          const double* constraint, int64_t plane_begin, int64_t plane_end,
                          double dt, double* out, double* max_dv);
 
+/* ------------------------------------------- safety-filter queries */
+/* SafetyFilter queries (reference safety.hpp:35-107 / safety.cpp:86-127),
+ * batched: nq states x[q*nd .. q*nd+nd-1] (nd = grid rank = model state
+ * dim) against a value function V on `grid` and the disturbance bounds
+ * `dbounds` (constant, or per node on the same grid).
+ *  HJB_FILTER_OPTIMAL: SafetyFilter::optimal_control (safety.cpp:86-106):
+ *    value = interp_ex(V, x) (grid.cpp:113-131), costate = the multilinear
+ *    interpolation of central node gradients (safety.cpp:14-49 with
+ *    gradient_at, grid.cpp:141-163), bounds = IntervalField::at (multilinear
+ *    per channel, interval_field.cpp:29-31), control / worst disturbance /
+ *    degenerate by extremal_inputs (dynamics.cpp:37-63); override = 1,
+ *    band = 0.
+ *  HJB_FILTER_FILTER: SafetyFilter::filter (safety.cpp:108-127): eta =
+ *    max(eta_floor, 0.5 * max_cell_jump(V, x)) (grid.cpp:177-195); when
+ *    !out_of_domain and value <= -lambda - eta the performance control
+ *    u_perf[q*m ..] passes through (override 0, worst disturbance and
+ *    flags 0), otherwise the optimal_control decision; band = eta.
+ * A non-finite query is HJB_ERR_INVALID_ARGUMENT ("interp: non-finite
+ * query", grid.cpp:95) and no output is defined. */
+typedef enum hjb_filter_mode { HJB_FILTER_OPTIMAL = 0, HJB_FILTER_FILTER = 1 } hjb_filter_mode;
+
+typedef struct hjb_filter_config {
+  int32_t mode;      /* hjb_filter_mode */
+  int32_t reserved;
+  double eta_floor;  /* SafetyFilter::Config::eta_floor, default 1e-5 */
+  double lambda;     /* contraction level of the filter state */
+} hjb_filter_config;
+
+#define HJB_FILTER_OVERRIDE 1   /* FilterDecision::override_active */
+#define HJB_FILTER_DEGENERATE 2 /* FilterDecision::degenerate */
+#define HJB_FILTER_OOD 4        /* FilterDecision::out_of_domain */
+
+/* Output arrays (any may be NULL): value[nq], band[nq],
+ * control[nq][control_dim], worst_disturbance[nq][disturbance_dim],
+ * flags[nq] (HJB_FILTER_* bits).  FilterDecision, safety.hpp:14-22. */
+typedef struct hjb_filter_out {
+  double* value;
+  double* band;
+  double* control;
+  double* worst_disturbance;
+  uint8_t* flags;
+} hjb_filter_out;
+
+/* Host pointers (V, per-node bounds, x, u_perf and the outputs). */
+int hjb_filter_batch(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                     const hjb_dbounds* dbounds, const double* value, int64_t nq,
+                     const double* x, const double* u_perf, const hjb_filter_config* cfg,
+                     const hjb_filter_out* out);
+/* Device pointers for everything (a value function kept resident in HBM). */
+int hjb_filter_batch_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                         const hjb_dbounds* dbounds, const double* value, int64_t nq,
+                         const double* x, const double* u_perf, const hjb_filter_config* cfg,
+                         const hjb_filter_out* out);
+
+/* interp_ex batched (reference grid.cpp:113-131): value[q] and
+ * out_of_domain[q] (may be NULL) of `field` at x[q*nd ..]; device pointers.
+ * A non-finite query is HJB_ERR_INVALID_ARGUMENT. */
+int hjb_interp_batch_dev(hjb_context* ctx, const hjb_grid* grid, const double* field,
+                         int64_t nq, const double* x, double* value, uint8_t* out_of_domain);
+
+/* ---------------------------------------------- device memory helpers */
+/* For FFI callers of the _dev entry points (no CUDA runtime of their own):
+ * device allocations and copies ordered on the context's stream. */
+int hjb_malloc_dev(hjb_context* ctx, uint64_t bytes, void** out);
+int hjb_free_dev(hjb_context* ctx, void* ptr);
+int hjb_copy_h2d(hjb_context* ctx, void* dst_dev, const void* src_host, uint64_t bytes);
+int hjb_copy_d2h(hjb_context* ctx, void* dst_host, const void* src_dev, uint64_t bytes);
+int hjb_copy_d2d(hjb_context* ctx, void* dst_dev, const void* src_dev, uint64_t bytes);
+
 /* Stream of the context (cudaStream_t as void*) and synchronisation. */
 void* hjb_context_stream(hjb_context* ctx);
 int hjb_context_synchronize(hjb_context* ctx);

@@ -606,6 +606,166 @@ int hjo_interp(const hjb_grid* gi, const double* field, const double* x, double*
   return 0;
 }
 
+/* ------------------------------------------------ safety-filter queries */
+/* locate, grid.cpp:90-111 (base / frac only) */
+static void locate_cell(const grid_t* g, const double* x, int64_t* base, double* frac, int* ood) {
+  *ood = 0;
+  for (int d = 0; d < g->nd; ++d) {
+    double t = (x[d] - g->min[d]) / g->spacing[d];
+    if (t < 0.0) {
+      t = 0.0;
+      *ood = 1;
+    }
+    const double tmax = (double)(g->n[d] - 1);
+    if (t > tmax) {
+      t = tmax;
+      if (x[d] > g->max[d]) *ood = 1;
+    }
+    int64_t i0 = (int64_t)t;
+    if (i0 > g->n[d] - 2) i0 = g->n[d] - 2;
+    base[d] = i0;
+    frac[d] = t - (double)i0;
+  }
+}
+
+/* max_cell_jump, grid.cpp:177-195 */
+static double max_cell_jump_at(const grid_t* g, const double* f, const int64_t* base) {
+  double jump = 0.0;
+  const int64_t corners = (int64_t)1 << g->nd;
+  for (int64_t corner = 0; corner < corners; ++corner) {
+    int64_t lin = 0;
+    for (int d = 0; d < g->nd; ++d) lin += (base[d] + ((corner >> d) & 1)) * g->stride[d];
+    for (int d = 0; d < g->nd; ++d) {
+      if ((corner >> d) & 1) continue;
+      const double dv = fabs(f[lin + g->stride[d]] - f[lin]);
+      if (dv > jump) jump = dv;
+    }
+  }
+  return jump;
+}
+
+/* gradient_at, grid.cpp:141-163 */
+static void gradient_at(const grid_t* g, const double* f, int64_t lin, int d, double* left,
+                        double* right) {
+  const int64_t n = g->n[d];
+  const int64_t stride = g->stride[d];
+  const int64_t k = (lin / stride) % n;
+  const double inv_dx = 1.0 / g->spacing[d];
+  if (k > 0 && k < n - 1) {
+    *left = (f[lin] - f[lin - stride]) * inv_dx;
+    *right = (f[lin + stride] - f[lin]) * inv_dx;
+  } else if (k == 0) {
+    *right = (f[lin + stride] - f[lin]) * inv_dx;
+    *left = *right;
+  } else {
+    *left = (f[lin] - f[lin - stride]) * inv_dx;
+    *right = *left;
+  }
+}
+
+/* SafetyFilter::optimal_control / filter, safety.cpp:86-127, with
+ * interpolated_costate (safety.cpp:14-49), IntervalField::at
+ * (interval_field.cpp:29-31) and extremal_inputs (dynamics.cpp:37-63). */
+int hjo_filter_batch(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db,
+                     const double* value, int64_t nq, const double* x, const double* u_perf,
+                     const hjb_filter_config* cfg, const hjb_filter_out* out) {
+  grid_t g;
+  int rc = grid_init(gi, &g);
+  if (rc) return rc;
+  if (m->state_dim != g.nd)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "SafetyFilter: grid rank does not match model");
+  if (db->channels != m->disturbance_dim)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "filter: disturbance channel count mismatch");
+  for (int64_t q = 0; q < nq; ++q)
+    for (int d = 0; d < g.nd; ++d)
+      if (!isfinite(x[q * g.nd + d])) return fail(HJB_ERR_INVALID_ARGUMENT, "interp: non-finite query");
+  const int n = m->state_dim, nu = m->control_dim, np = m->disturbance_dim;
+  for (int64_t q = 0; q < nq; ++q) {
+    const double* xq = x + q * n;
+    int64_t base[HJB_MAX_DIMS];
+    double frac[HJB_MAX_DIMS];
+    int ood;
+    locate_cell(&g, xq, base, frac, &ood);
+    const double v = interp_at(&g, value, xq, &ood);
+    double band = 0.0;
+    if (cfg->mode == HJB_FILTER_FILTER) {
+      const double eta = STD_MAX(cfg->eta_floor, 0.5 * max_cell_jump_at(&g, value, base));
+      band = eta;
+      if (!ood && v <= -cfg->lambda - eta) {
+        if (out->value) out->value[q] = v;
+        if (out->band) out->band[q] = eta;
+        if (out->control)
+          for (int j = 0; j < nu; ++j) out->control[q * nu + j] = u_perf[q * nu + j];
+        if (out->worst_disturbance)
+          for (int k = 0; k < np; ++k) out->worst_disturbance[q * np + k] = 0.0;
+        if (out->flags) out->flags[q] = 0;
+        continue;
+      }
+    }
+    /* interpolated_costate: std::clamp locate == locate's base/frac */
+    double costate[HJB_MAX_STATE] = {0};
+    double dlo[HJB_MAX_INPUT] = {0}, dhi[HJB_MAX_INPUT] = {0};
+    const int64_t corners = (int64_t)1 << g.nd;
+    for (int64_t corner = 0; corner < corners; ++corner) {
+      double w = 1.0;
+      int64_t lin = 0;
+      for (int d = 0; d < g.nd; ++d) {
+        const int hi = (corner >> d) & 1;
+        w *= hi ? frac[d] : 1.0 - frac[d];
+        lin += (base[d] + (hi ? 1 : 0)) * g.stride[d];
+      }
+      if (w == 0.0) continue;
+      for (int d = 0; d < g.nd; ++d) {
+        double left, right;
+        gradient_at(&g, value, lin, d, &left, &right);
+        costate[d] += w * 0.5 * (left + right);
+      }
+    }
+    /* IntervalField::at: interp of each lo / hi field (skips w == 0) */
+    for (int k = 0; k < np; ++k) {
+      double lo = 0.0, hi = 0.0;
+      for (int64_t corner = 0; corner < corners; ++corner) {
+        double w = 1.0;
+        int64_t lin = 0;
+        for (int d = 0; d < g.nd; ++d) {
+          const int b = (corner >> d) & 1;
+          w *= b ? frac[d] : 1.0 - frac[d];
+          lin += (base[d] + (b ? 1 : 0)) * g.stride[d];
+        }
+        if (w == 0.0) continue;
+        lo += w * (db->per_node ? db->lo[k][lin] : db->constant[k].lo);
+        hi += w * (db->per_node ? db->hi[k][lin] : db->constant[k].hi);
+      }
+      dlo[k] = lo;
+      dhi[k] = hi;
+    }
+    /* extremal_inputs */
+    int any_active = 0;
+    for (int j = 0; j < nu; ++j) {
+      double coeff = 0.0;
+      for (int i = 0; i < n; ++i) coeff += costate[i] * m->control[i][j];
+      const double u = coeff > 0.0 ? m->ubounds[j].lo
+                                   : (coeff < 0.0 ? m->ubounds[j].hi : m->ubounds[j].lo);
+      if (coeff != 0.0) any_active = 1;
+      if (out->control) out->control[q * nu + j] = u;
+    }
+    for (int k = 0; k < np; ++k) {
+      double coeff = 0.0;
+      for (int i = 0; i < n; ++i) coeff += costate[i] * m->disturbance[i][k];
+      const double dk = coeff > 0.0 ? dhi[k] : (coeff < 0.0 ? dlo[k] : dlo[k]);
+      if (coeff != 0.0) any_active = 1;
+      if (out->worst_disturbance) out->worst_disturbance[q * np + k] = dk;
+    }
+    const int degenerate = !any_active && (nu + np) > 0;
+    if (out->value) out->value[q] = v;
+    if (out->band) out->band[q] = band;
+    if (out->flags)
+      out->flags[q] = (uint8_t)(HJB_FILTER_OVERRIDE | (degenerate ? HJB_FILTER_DEGENERATE : 0) |
+                                (ood ? HJB_FILTER_OOD : 0));
+  }
+  return 0;
+}
+
 /* resample, grid.cpp:215-231 */
 int hjo_resample(const hjb_grid* sgi, const double* src, const hjb_grid* dgi, double* dst) {
   grid_t sg, dg;

@@ -91,6 +91,11 @@ int hjo_hamiltonian(const hjb_model* m, const double* x, const double* p, const 
                     double* h);
 int hjo_flow_bounds(const hjb_model* m, const double* x, const hjb_interval* db, double* alpha);
 
+/* SafetyFilter::optimal_control / filter batched (safety.cpp:86-127) */
+int hjo_filter_batch(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db,
+                     const double* value, int64_t nq, const double* x, const double* u_perf,
+                     const hjb_filter_config* cfg, const hjb_filter_out* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,9 @@ class Restatement:
         L.hjo_signed_distance_box.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp]
         L.hjo_hamiltonian.argtypes = [P(abi.HjbModel), _vp, _vp, P(abi.HjbInterval), P(_d)]
         L.hjo_flow_bounds.argtypes = [P(abi.HjbModel), _vp, P(abi.HjbInterval), _vp]
+        L.hjo_filter_batch.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp,
+                                       C.c_int64, _vp, _vp, P(abi.HjbFilterConfig),
+                                       P(abi.HjbFilterOut)]
         if threads:
             L.hjo_set_threads(threads)
 
@@ -250,6 +253,34 @@ class Restatement:
 
 
 # ----------------------------------------------------------- reference
+def _filter_out(nq, m, p):
+    arrs = dict(value=np.empty(nq), band=np.empty(nq), control=np.empty((nq, m)),
+                worst_disturbance=np.empty((nq, p)), flags=np.empty(nq, dtype=np.uint8))
+    out = abi.HjbFilterOut(*(arrs[k].ctypes.data for k in
+                             ("value", "band", "control", "worst_disturbance", "flags")))
+    return arrs, out
+
+
+def _restatement_filter_batch(self, v, model, db, x, u_perf=None, mode=abi.FILTER_OPTIMAL,
+                              eta_floor=1e-5, lam=0.0):
+    """hjo_filter_batch: SafetyFilter::optimal_control / filter restated."""
+    grid = v.grid()
+    X = np.ascontiguousarray(np.asarray(x, dtype=np.float64)).reshape(-1, grid.ndims())
+    nq, m, p = X.shape[0], model.control_dim(), model.disturbance_dim()
+    U = (np.ascontiguousarray(np.asarray(u_perf, dtype=np.float64)).reshape(nq, m)
+         if u_perf is not None else np.zeros((nq, m)))
+    arrs, out = _filter_out(nq, m, p)
+    cfg = abi.HjbFilterConfig(mode, 0, eta_floor, lam)
+    g, mm, d = grid.to_c(), model.to_c(), db.to_c()
+    vv = _vals(v)
+    self._chk(self.lib.hjo_filter_batch(C.byref(g), C.byref(mm), C.byref(d), _arr(vv), nq,
+                                        _arr(X), _arr(U), C.byref(cfg), C.byref(out)))
+    return arrs
+
+
+Restatement.filter_batch = _restatement_filter_batch
+
+
 class ModelSpec(C.Structure):
     _fields_ = [("kind", C.c_int32), ("d_row", C.c_int32), ("p", C.c_double * 10)]
 
@@ -311,6 +342,13 @@ class Reference:
         L.hjr_hamiltonian.argtypes = [P(ModelSpec), _vp, _vp, P(abi.HjbInterval), P(_d)] + E
         L.hjr_flow_bounds.argtypes = [P(ModelSpec), _vp, P(abi.HjbInterval), _vp] + E
         L.hjr_write_hjvf.argtypes = [C.c_char_p, P(abi.HjbGrid), _vp] + E
+        L.hjr_filter_batch.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds), _vp,
+                                       C.c_int64, _vp, _vp, C.c_int32, _d, C.c_int64, _vp, P(_d),
+                                       P(C.c_int32), P(abi.HjbFilterOut)] + E
+        L.hjr_decomposition_batch.argtypes = [C.c_int32, _vp, _vp, _vp, _vp, _vp, C.c_int32,
+                                              C.c_int32, C.c_int32, _d, C.c_int64, _vp,
+                                              C.c_int64, _vp, _vp, P(_d), P(C.c_int32), _vp, _vp,
+                                              _vp, _vp, _vp] + E
 
     def _call(self, fn, *args):
         err = C.create_string_buffer(512)
@@ -419,6 +457,58 @@ class Reference:
     def write_hjvf(self, path, f):
         g = f.grid().to_c()
         self._call(self.lib.hjr_write_hjvf, str(path).encode(), C.byref(g), _arr(_vals(f)))
+
+
+def _reference_filter_batch(self, v, model, db, x, u_perf=None, mode=abi.FILTER_OPTIMAL,
+                            eta_floor=1e-5, violations=()):
+    """The reference's own SafetyFilter: contract(violations) then per-query
+    filter / optimal_control.  Returns (arrays, lambda, emergency)."""
+    grid = v.grid()
+    nd = grid.ndims()
+    X = np.ascontiguousarray(np.asarray(x, dtype=np.float64)).reshape(-1, nd)
+    nq, m, p = X.shape[0], model.control_dim(), model.disturbance_dim()
+    U = (np.ascontiguousarray(np.asarray(u_perf, dtype=np.float64)).reshape(nq, m)
+         if u_perf is not None else np.zeros((nq, m)))
+    Vx = np.ascontiguousarray(np.asarray(violations, dtype=np.float64)).reshape(-1, nd)
+    arrs, out = _filter_out(nq, m, p)
+    lam, em = C.c_double(), C.c_int32()
+    g, mm, d = grid.to_c(), model_spec(model), db.to_c()
+    vv = _vals(v)
+    self._call(self.lib.hjr_filter_batch, C.byref(g), C.byref(mm), C.byref(d), _arr(vv), nq,
+               _arr(X), _arr(U), mode, eta_floor, Vx.shape[0], _arr(Vx), C.byref(lam),
+               C.byref(em), C.byref(out))
+    return arrs, lam.value, bool(em.value)
+
+
+def _reference_decomposition_batch(self, subs, values, dbounds, full_dims, x, u_perf,
+                                   eta_floor=1e-5, violations=()):
+    """The reference's Decomposition over SafetyFilters (subs: hjsafe
+    Subsystem list, values: converged ScalarFields, dbounds: IntervalFields)."""
+    n, m, p = full_dims
+    k = len(subs)
+    grids = (abi.HjbGrid * k)(*[v.grid().to_c() for v in values])
+    specs = (ModelSpec * k)(*[model_spec(s.model) for s in subs])
+    dbs = (abi.HjbDbounds * k)(*[d.to_c() for d in dbounds])
+    vals = [np.ascontiguousarray(_vals(v)) for v in values]
+    vptr = (C.c_void_p * k)(*[a.ctypes.data for a in vals])
+    maps = np.array([i for s in subs for i in (list(s.state_map) + list(s.control_map)
+                                                 + list(s.disturbance_map))], dtype=np.int32)
+    X = np.ascontiguousarray(np.asarray(x, dtype=np.float64)).reshape(-1, n)
+    nq = X.shape[0]
+    U = np.ascontiguousarray(np.asarray(u_perf, dtype=np.float64)).reshape(nq, m)
+    Vx = np.ascontiguousarray(np.asarray(violations, dtype=np.float64)).reshape(-1, n)
+    cv, val, band = np.empty(nq), np.empty(nq), np.empty(nq)
+    ctl, flg = np.empty((nq, m)), np.empty(nq, dtype=np.uint8)
+    lam, em = C.c_double(), C.c_int32()
+    self._call(self.lib.hjr_decomposition_batch, k, grids, specs, dbs, vptr, _arr(maps), n, m, p,
+               eta_floor, Vx.shape[0], _arr(Vx), nq, _arr(X), _arr(U), C.byref(lam), C.byref(em),
+               _arr(cv), _arr(val), _arr(band), _arr(ctl), _arr(flg))
+    return dict(combined_value=cv, value=val, band=band, control=ctl, flags=flg), lam.value, \
+        bool(em.value)
+
+
+Reference.filter_batch = _reference_filter_batch
+Reference.decomposition_batch = _reference_decomposition_batch
 
 
 def reference_available() -> bool:

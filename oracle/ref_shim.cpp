@@ -15,11 +15,13 @@
 #include <string>
 #include <vector>
 
+#include "hjsafe/decomposition.hpp"
 #include "hjsafe/dynamics.hpp"
 #include "hjsafe/grid.hpp"
 #include "hjsafe/hjvf.hpp"
 #include "hjsafe/interval_field.hpp"
 #include "hjsafe/levelset.hpp"
+#include "hjsafe/safety.hpp"
 #include "hjsafe/solver.hpp"
 
 using namespace hjsafe;
@@ -349,6 +351,114 @@ int hjr_affine(const hjr_model_spec* m, const double* x, double* drift, double* 
     }
     auto ub = model->control_bounds();
     for (std::size_t j = 0; j < ub.size(); ++j) ubounds[j] = {ub[j].lo, ub[j].hi};
+  });
+}
+
+int hjr_filter_batch(const hjb_grid* g, const hjr_model_spec* m, const hjb_dbounds* db,
+                     const double* value, int64_t nq, const double* x, const double* u_perf,
+                     int32_t mode, double eta_floor, int64_t nviol, const double* viol_x,
+                     double* lambda_out, int32_t* emergency_out, const hjb_filter_out* out,
+                     char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Grid grid = make_grid(g);
+    std::shared_ptr<const DynamicsModel> model(make(m).release());
+    SolveResult solved{make_field(grid, value)};
+    solved.converged = true;
+    SafetyFilter::Config cfg;
+    cfg.eta_floor = eta_floor;
+    SafetyFilter filter(model, solved, make_db(grid, db), cfg);
+    const std::size_t nd = grid.ndims();
+    if (nviol > 0) {
+      std::vector<Violation> vs;
+      for (int64_t i = 0; i < nviol; ++i) {
+        Violation v;
+        v.x.assign(viol_x + i * nd, viol_x + (i + 1) * nd);
+        vs.push_back(std::move(v));
+      }
+      filter.contract(vs);
+    }
+    if (lambda_out) *lambda_out = filter.lambda();
+    if (emergency_out) *emergency_out = filter.emergency() ? 1 : 0;
+    const std::size_t nu = model->control_dim(), np = model->disturbance_dim();
+    for (int64_t q = 0; q < nq; ++q) {
+      std::span<const double> xq(x + q * nd, nd);
+      const FilterDecision d =
+          mode == HJB_FILTER_FILTER
+              ? filter.filter(xq, std::span<const double>(u_perf + q * nu, nu))
+              : filter.optimal_control(xq);
+      if (out->value) out->value[q] = d.value;
+      if (out->band) out->band[q] = d.band;
+      if (out->control)
+        for (std::size_t j = 0; j < nu; ++j) out->control[q * nu + j] = d.control[j];
+      if (out->worst_disturbance)
+        for (std::size_t k = 0; k < np; ++k)
+          out->worst_disturbance[q * np + k] =
+              k < d.worst_disturbance.size() ? d.worst_disturbance[k] : 0.0;
+      if (out->flags)
+        out->flags[q] = static_cast<uint8_t>((d.override_active ? HJB_FILTER_OVERRIDE : 0) |
+                                             (d.degenerate ? HJB_FILTER_DEGENERATE : 0) |
+                                             (d.out_of_domain ? HJB_FILTER_OOD : 0));
+    }
+  });
+}
+
+int hjr_decomposition_batch(int32_t nsub, const hjb_grid* grids, const hjr_model_spec* models,
+                            const hjb_dbounds* dbs, const double* const* values,
+                            const int32_t* maps, int32_t full_n, int32_t full_m, int32_t full_p,
+                            double eta_floor, int64_t nviol, const double* viol_x, int64_t nq,
+                            const double* x, const double* u_perf, double* lambda_out,
+                            int32_t* emergency_out, double* cv_out, double* value_out,
+                            double* band_out, double* control_out, uint8_t* flags_out, char* err,
+                            int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Subsystem> subs;
+    std::vector<std::shared_ptr<SafetyFilter>> filters;
+    const int32_t* mp = maps;
+    for (int32_t i = 0; i < nsub; ++i) {
+      std::shared_ptr<const DynamicsModel> model(make(&models[i]).release());
+      Subsystem s;
+      s.name = model->name();
+      s.model = model;
+      s.state_map.assign(mp, mp + model->state_dim());
+      mp += model->state_dim();
+      s.control_map.assign(mp, mp + model->control_dim());
+      mp += model->control_dim();
+      s.disturbance_map.assign(mp, mp + model->disturbance_dim());
+      mp += model->disturbance_dim();
+      Grid grid = make_grid(&grids[i]);
+      SolveResult solved{make_field(grid, values[i])};
+      solved.converged = true;
+      SafetyFilter::Config cfg;
+      cfg.eta_floor = eta_floor;
+      filters.push_back(std::make_shared<SafetyFilter>(model, solved, make_db(grid, &dbs[i]), cfg));
+      subs.push_back(std::move(s));
+    }
+    Decomposition dec(std::move(subs), full_n, full_m, full_p);
+    dec.attach(filters);
+    if (nviol > 0) {
+      std::vector<Violation> vs;
+      for (int64_t i = 0; i < nviol; ++i) {
+        Violation v;
+        v.x.assign(viol_x + i * full_n, viol_x + (i + 1) * full_n);
+        vs.push_back(std::move(v));
+      }
+      dec.contract(vs);
+    }
+    if (lambda_out) *lambda_out = dec.lambda();
+    if (emergency_out) *emergency_out = dec.emergency() ? 1 : 0;
+    for (int64_t q = 0; q < nq; ++q) {
+      std::span<const double> xq(x + q * full_n, full_n);
+      if (cv_out) cv_out[q] = dec.combined_value(xq);
+      const CombinedDecision d =
+          dec.combined_control(xq, std::span<const double>(u_perf + q * full_m, full_m));
+      if (value_out) value_out[q] = d.value;
+      if (band_out) band_out[q] = d.band;
+      if (control_out)
+        for (int32_t j = 0; j < full_m; ++j) control_out[q * full_m + j] = d.control[j];
+      if (flags_out)
+        flags_out[q] = static_cast<uint8_t>((d.override_active ? HJB_FILTER_OVERRIDE : 0) |
+                                            (d.out_of_domain ? HJB_FILTER_OOD : 0));
+    }
   });
 }
 

@@ -3,7 +3,7 @@
  *
  * extern "C" harness over the UNMODIFIED reference sources
  * (/root/reference/proj/src/{grid,hjvf,levelset,dynamics,interval_field,
- * solver}.cpp), compiled by oracle/Makefile into oracle/_ref/libhjref.so.
+ * solver,safety,decomposition}.cpp), compiled by oracle/Makefile into oracle/_ref/libhjref.so.
  * It is the parity anchor for the C restatement (oracle/hj_oracle.c) and the
  * CPU arm of bench.py.  The product path never links or loads it.
  */
@@ -88,6 +88,29 @@ int hjr_affine(const hjr_model_spec* m, const double* x, double* drift, double* 
                double* disturbance, hjb_interval* ubounds, int32_t* dims, char* err,
                int errlen);
 /* HJVF I/O (hjvf.cpp:46-95) for golden files */
+/* SafetyFilter (safety.hpp:35-107) around V with Config::eta_floor; after
+ * contract(violations) (viol_x: nviol states), answers nq queries with
+ * filter (mode HJB_FILTER_FILTER, u_perf per query) or optimal_control;
+ * reports the filter's lambda and emergency flag. */
+int hjr_filter_batch(const hjb_grid* g, const hjr_model_spec* m, const hjb_dbounds* db,
+                     const double* value, int64_t nq, const double* x, const double* u_perf,
+                     int32_t mode, double eta_floor, int64_t nviol, const double* viol_x,
+                     double* lambda_out, int32_t* emergency_out, const hjb_filter_out* out,
+                     char* err, int errlen);
+/* Decomposition (decomposition.hpp:33-80) of nsub subsystems, each with its
+ * grid, model, bounds and converged V (values[i]); maps holds, per
+ * subsystem, state_map, control_map and disturbance_map back to back.
+ * After contract(violations) (viol_x: nviol full states), answers nq full
+ * queries: combined_value -> cv_out, combined_control -> value / band /
+ * control / flags (HJB_FILTER_OVERRIDE | HJB_FILTER_OOD). */
+int hjr_decomposition_batch(int32_t nsub, const hjb_grid* grids, const hjr_model_spec* models,
+                            const hjb_dbounds* dbs, const double* const* values,
+                            const int32_t* maps, int32_t full_n, int32_t full_m, int32_t full_p,
+                            double eta_floor, int64_t nviol, const double* viol_x, int64_t nq,
+                            const double* x, const double* u_perf, double* lambda_out,
+                            int32_t* emergency_out, double* cv_out, double* value_out,
+                            double* band_out, double* control_out, uint8_t* flags_out, char* err,
+                            int errlen);
 int hjr_write_hjvf(const char* path, const hjb_grid* g, const double* v, char* err, int errlen);
 
 #ifdef __cplusplus

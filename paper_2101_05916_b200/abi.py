@@ -86,6 +86,19 @@ class HjbSolveResult(C.Structure):
                 ("history_capacity", C.c_int64)]
 
 
+class HjbFilterConfig(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("reserved", C.c_int32), ("eta_floor", C.c_double),
+                ("lambda_", C.c_double)]
+
+
+class HjbFilterOut(C.Structure):
+    _fields_ = [("value", C.c_void_p), ("band", C.c_void_p), ("control", C.c_void_p),
+                ("worst_disturbance", C.c_void_p), ("flags", C.c_void_p)]
+
+
+FILTER_OPTIMAL, FILTER_FILTER = 0, 1
+FILTER_OVERRIDE, FILTER_DEGENERATE, FILTER_OOD = 1, 2, 4
+
 P = C.POINTER
 _d = C.c_double
 _dp = P(C.c_double)
@@ -136,6 +149,16 @@ SIGNATURES = [
                                    P(HjbSolveConfig), _vp, P(HjbSolveResult)]),
     ("hjb_sweep_planes_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp, _i64,
                                   _i64, _d, _vp, _dp]),
+    ("hjb_filter_batch", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _i64, _vp, _vp,
+                              P(HjbFilterConfig), P(HjbFilterOut)]),
+    ("hjb_filter_batch_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _i64, _vp,
+                                  _vp, P(HjbFilterConfig), P(HjbFilterOut)]),
+    ("hjb_interp_batch_dev", _i, [_vp, P(HjbGrid), _vp, _i64, _vp, _vp, _vp]),
+    ("hjb_malloc_dev", _i, [_vp, C.c_uint64, P(_vp)]),
+    ("hjb_free_dev", _i, [_vp, _vp]),
+    ("hjb_copy_h2d", _i, [_vp, _vp, _vp, C.c_uint64]),
+    ("hjb_copy_d2h", _i, [_vp, _vp, _vp, C.c_uint64]),
+    ("hjb_copy_d2d", _i, [_vp, _vp, _vp, C.c_uint64]),
     ("hjb_context_stream", _vp, [_vp]),
     ("hjb_context_synchronize", _i, [_vp]),
     ("hjb_context_launch_count", _i64, [_vp]),

@@ -712,13 +712,9 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   return HJB_OK;
 }
 
-namespace {
+namespace hjb {
 
 // Stage host fields into device buffers owned by the context.
-struct Staged {
-  DevBuf init, c, out, db;
-};
-
 int stage_dbounds(hjb_context* ctx, const hjb_dbounds* db, size_t n, DevBuf& buf,
                   hjb_dbounds& out) {
   out = *db;
@@ -743,6 +739,14 @@ int check_ctx(hjb_context* ctx) {
   CUDA_TRY(cudaSetDevice(ctx->device));
   return HJB_OK;
 }
+
+}  // namespace hjb
+
+namespace {
+
+struct Staged {
+  DevBuf init, c, out, db;
+};
 
 }  // namespace
 

@@ -42,6 +42,10 @@ void fill_tables(const Prepared& p, Fast4dArgs& f);
 using SweepLauncher = std::function<cudaError_t(cudaStream_t, cudaGraphConditionalHandle, int)>;
 int run_loop(hjb_context* ctx, const SweepLauncher& launch, int body);
 int sm_count(int device);
+// host per-node bounds -> context device buffer (constant bounds pass through)
+int stage_dbounds(hjb_context* ctx, const hjb_dbounds* db, size_t n, DevBuf& buf,
+                  hjb_dbounds& out);
+int check_ctx(hjb_context* ctx);
 inline int validate_config(const hjb_solve_config* cfg) { return validate_cfg(cfg); }
 
 }  // namespace hjb

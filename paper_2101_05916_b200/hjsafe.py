@@ -1031,3 +1031,9 @@ def field_max_dev(n: int, a_ptr: int, b_ptr: int, out_ptr: int, ctx: Context | N
     lib = abi.load()
     _check(lib.hjb_field_max_dev(_ctx(ctx), int(n), C.c_void_p(a_ptr), C.c_void_p(b_ptr),
                                  C.c_void_p(out_ptr)))
+
+
+# SafetyFilter / Decomposition (safety.hpp, decomposition.hpp) live in
+# safety.py; re-exported here so the reference's names resolve from hjsafe.
+from .safety import (CombinedDecision, Decomposition, FilterDecision, SafetyFilter,  # noqa: E402
+                     Subsystem, Violation, project, scatter)
