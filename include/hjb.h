@@ -356,6 +356,12 @@ int hjb_filter_batch_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model
 int hjb_interp_batch_dev(hjb_context* ctx, const hjb_grid* grid, const double* field,
                          int64_t nq, const double* x, double* value, uint8_t* out_of_domain);
 
+/* min / max over a device field (either output may be NULL): the
+ * SafetyFilter's min V* (safety.cpp:60, std::min_element) without a host
+ * round trip.  Values are compared as IEEE doubles (NaN-free input). */
+int hjb_field_reduce_dev(hjb_context* ctx, int64_t n, const double* field, double* min_out,
+                         double* max_out);
+
 /* ---------------------------------------------- device memory helpers */
 /* For FFI callers of the _dev entry points (no CUDA runtime of their own):
  * device allocations and copies ordered on the context's stream. */

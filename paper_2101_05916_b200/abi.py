@@ -154,6 +154,7 @@ SIGNATURES = [
     ("hjb_filter_batch_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _i64, _vp,
                                   _vp, P(HjbFilterConfig), P(HjbFilterOut)]),
     ("hjb_interp_batch_dev", _i, [_vp, P(HjbGrid), _vp, _i64, _vp, _vp, _vp]),
+    ("hjb_field_reduce_dev", _i, [_vp, _i64, _vp, _dp, _dp]),
     ("hjb_malloc_dev", _i, [_vp, C.c_uint64, P(_vp)]),
     ("hjb_free_dev", _i, [_vp, _vp]),
     ("hjb_copy_h2d", _i, [_vp, _vp, _vp, C.c_uint64]),

@@ -17,6 +17,7 @@
 // warp covers 32 independent queries.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -257,6 +258,44 @@ void launch_interp_nd(const DevGrid& g, const double* f, long long nq, const dou
   k_interp<ND><<<(unsigned)((nq + 127) / 128), 128, 0, s>>>(g, f, nq, x, value, ood, err);
 }
 
+// order-preserving unsigned key of a double (total order, -0 < +0)
+__device__ __forceinline__ unsigned long long okey(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double unkey(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double d;
+  std::memcpy(&d, &b, sizeof d);
+  return d;
+#endif
+}
+
+__global__ void __launch_bounds__(256)
+    k_reduce(const double* __restrict__ f, long long n, unsigned long long* keys) {
+  unsigned long long mn = ~0ull, mx = 0ull;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = okey(__ldg(f + i));
+    mn = k < mn ? k : mn;
+    mx = k > mx ? k : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(keys, mn);
+    atomicMax(keys + 1, mx);
+  }
+}
+
 template <int ND>
 void launch_nd(const FilterArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)((a.nq + 127) / 128);
@@ -456,6 +495,29 @@ int hjb_interp_batch_dev(hjb_context* ctx, const hjb_grid* grid, const double* f
   CUDA_TRY(cudaMemcpyAsync(&e, err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (e) return set_err(HJB_ERR_INVALID_ARGUMENT, "interp: non-finite query");
+  return HJB_OK;
+}
+
+int hjb_field_reduce_dev(hjb_context* ctx, int64_t n, const double* field, double* min_out,
+                         double* max_out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  if (n <= 0 || !field) return set_err(HJB_ERR_INVALID_ARGUMENT, "reduce: empty field");
+  CUDA_TRY(ctx->scratch.ensure(64));
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(ctx->scratch.p);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  CUDA_TRY(cudaMemcpyAsync(keys, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  const int sms = sm_count(ctx->device);
+  const long long want = (n + 255) / 256;
+  const unsigned blocks = (unsigned)std::min<long long>(want, 4LL * sms);
+  k_reduce<<<blocks, 256, 0, ctx->stream>>>(field, n, keys);
+  CUDA_TRY(cudaGetLastError());
+  ++ctx->launches;
+  unsigned long long out[2];
+  CUDA_TRY(cudaMemcpyAsync(out, keys, sizeof out, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (min_out) *min_out = unkey(out[0]);
+  if (max_out) *max_out = unkey(out[1]);
   return HJB_OK;
 }
 

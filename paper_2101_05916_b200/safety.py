@@ -25,7 +25,7 @@ from . import hjsafe as hj
 
 __all__ = ["FilterDecision", "Violation", "FilterBatch", "SafetyFilter", "Subsystem",
            "CombinedDecision", "CombinedBatch", "Decomposition", "project", "scatter",
-           "DeviceBuffer", "interp_batch"]
+           "DeviceBuffer", "DeviceSolve", "interp_batch"]
 
 
 # ------------------------------------------------------------- device memory
@@ -162,6 +162,10 @@ class FilterBatch:
                               value=float(self.value[q]), band=float(self.band[q]))
 
 
+def _grid_of(solved) -> hj.Grid:
+    return solved.grid if isinstance(solved, DeviceSolve) else solved.value.grid()
+
+
 def _std_max(a, b):
     """std::max(a, b) = (a < b) ? b : a, elementwise."""
     return np.where(np.asarray(a) < np.asarray(b), b, a)
@@ -170,8 +174,10 @@ def _std_max(a, b):
 # ---------------------------------------------------------------- filter
 @dataclass
 class _State:
-    """SafetyFilter::State, safety.hpp:75-82, with V* resident on the device."""
-    value: hj.ScalarField
+    """SafetyFilter::State, safety.hpp:75-82, with V* resident on the device
+    (the host copy `value` is filled on demand for a device-adopted V*)."""
+    grid: hj.Grid
+    value: hj.ScalarField | None
     dbounds: hj.IntervalField
     dev_value: DeviceBuffer
     dev_db: list
@@ -179,6 +185,26 @@ class _State:
     min_value: float
     lam: float = 0.0
     emergency: bool = False
+
+
+@dataclass
+class DeviceSolve:
+    """A solve whose V* stayed in HBM (hjb_solve_dev): the metadata of
+    SolveResult (solver.hpp:27-36) plus the device buffer of V*."""
+    grid: hj.Grid
+    value: DeviceBuffer
+    iterations: int = 0
+    dt: float = 0.0
+    wall_seconds: float = 0.0
+    converged: bool = False
+    final_residual: float = 0.0
+
+    def to_host(self) -> hj.SolveResult:
+        v = self.value.download(np.empty(self.grid.size()))
+        return hj.SolveResult(value=hj.ScalarField(self.grid, v, check=False),
+                              iterations=self.iterations, dt=self.dt,
+                              wall_seconds=self.wall_seconds, converged=self.converged,
+                              final_residual=self.final_residual)
 
 
 class SafetyFilter:
@@ -198,7 +224,7 @@ class SafetyFilter:
                  ctx: hj.Context | None = None):
         if model is None:
             raise hj.InvalidArgument("SafetyFilter: null model")
-        if solved.value.grid().ndims() != model.state_dim():
+        if _grid_of(solved).ndims() != model.state_dim():
             raise hj.InvalidArgument("SafetyFilter: grid rank does not match model")
         self._model = model
         self._cfg = cfg or SafetyFilter.Config()
@@ -208,23 +234,31 @@ class SafetyFilter:
         self._state = self._make_state(solved, dbounds)
 
     # safety.cpp:53-66
-    def _make_state(self, solved: hj.SolveResult, dbounds: hj.IntervalField) -> _State:
+    def _make_state(self, solved, dbounds: hj.IntervalField) -> _State:
         if not solved.converged:
             raise hj.InvalidArgument("SafetyFilter: value function is not converged")
         dbounds.validate()
-        v = solved.value
-        dev = DeviceBuffer(self._ctx, v.size() * 8)
-        dev.upload(v.values())
+        if isinstance(solved, DeviceSolve):  # V* already in HBM: no host round trip
+            grid, v, dev = solved.grid, None, solved.value
+            mn = C.c_double()
+            hj._check(abi.load().hjb_field_reduce_dev(self._ctx.handle, grid.size(), dev.ptr,
+                                                      C.byref(mn), None))
+            mn = mn.value
+        else:
+            v = solved.value
+            grid = v.grid()
+            dev = DeviceBuffer(self._ctx, v.size() * 8)
+            dev.upload(v.values())
+            mn = float(np.min(v.values()))
         dev_db = []
         if not dbounds.is_constant():
             for ch in range(dbounds.channels()):
-                lo = DeviceBuffer(self._ctx, v.size() * 8)
+                lo = DeviceBuffer(self._ctx, grid.size() * 8)
                 lo.upload(dbounds.lo(ch).values())
-                hi = DeviceBuffer(self._ctx, v.size() * 8)
+                hi = DeviceBuffer(self._ctx, grid.size() * 8)
                 hi.upload(dbounds.hi(ch).values())
                 dev_db.append((lo, hi))
-        mn = float(np.min(v.values()))
-        return _State(value=v, dbounds=dbounds, dev_value=dev, dev_db=dev_db,
+        return _State(grid=grid, value=v, dbounds=dbounds, dev_value=dev, dev_db=dev_db,
                       eta_floor=self._cfg.eta_floor, min_value=mn, lam=0.0,
                       emergency=mn >= 0.0)
 
@@ -264,7 +298,7 @@ class SafetyFilter:
         dflg = ws.get("flg", nq)
         out = abi.HjbFilterOut(dval.ptr, dband.ptr, dctl.ptr, dwst.ptr, dflg.ptr)
         cfg = abi.HjbFilterConfig(mode, 0, s.eta_floor, s.lam)
-        g, mm, d = s.value.grid().to_c(), self._model.to_c(), self._dbounds_c(s)
+        g, mm, d = s.grid.to_c(), self._model.to_c(), self._dbounds_c(s)
         hj._check(abi.load().hjb_filter_batch_dev(self._ctx.handle, C.byref(g), C.byref(mm),
                                                   C.byref(d), s.dev_value.ptr, nq, dx.ptr, du_ptr,
                                                   C.byref(cfg), C.byref(out)))
@@ -277,7 +311,7 @@ class SafetyFilter:
     def filter_batch(self, x, u_perf) -> FilterBatch:
         """SafetyFilter::filter (safety.cpp:108-127) for every row of x."""
         s = self._snapshot()
-        X = _queries(x, s.value.grid().ndims())
+        X = _queries(x, s.grid.ndims())
         m = self._model.control_dim()
         U = np.ascontiguousarray(np.asarray(u_perf, dtype=np.float64)).reshape(X.shape[0], -1) \
             if m > 0 else np.zeros((X.shape[0], 0))
@@ -288,7 +322,7 @@ class SafetyFilter:
     def optimal_control_batch(self, x) -> FilterBatch:
         """SafetyFilter::optimal_control (safety.cpp:86-106) for every row of x."""
         s = self._snapshot()
-        return self._run(s, _queries(x, s.value.grid().ndims()), None, abi.FILTER_OPTIMAL)
+        return self._run(s, _queries(x, s.grid.ndims()), None, abi.FILTER_OPTIMAL)
 
     def filter(self, x: Sequence[float], u_perf: Sequence[float]) -> FilterDecision:
         if len(u_perf) != self._model.control_dim():
@@ -300,7 +334,7 @@ class SafetyFilter:
 
     def value_at_batch(self, x) -> np.ndarray:
         s = self._snapshot()
-        v, _ = interp_batch(s.value.grid(), s.dev_value.ptr, x, self._ctx, self._ws)
+        v, _ = interp_batch(s.grid, s.dev_value.ptr, x, self._ctx, self._ws)
         return v
 
     def value_at(self, x: Sequence[float]) -> float:
@@ -315,7 +349,7 @@ class SafetyFilter:
         if s.dbounds.is_constant():
             key = f"const_db_{channel}"
             if key not in self._ws.bufs:
-                n = s.value.size()
+                n = s.grid.size()
                 lo = DeviceBuffer(self._ctx, n * 8)
                 lo.upload(s.dbounds.lo(channel).values())
                 hi = DeviceBuffer(self._ctx, n * 8)
@@ -325,7 +359,7 @@ class SafetyFilter:
             lo_ptr, hi_ptr = self._ws.bufs[key].ptr, self._ws.bufs[key + "_hi"].ptr
         else:
             lo_ptr, hi_ptr = s.dev_db[channel][0].ptr, s.dev_db[channel][1].ptr
-        g = s.value.grid()
+        g = s.grid
         lo, _ = interp_batch(g, lo_ptr, [list(x)], self._ctx)
         hi, _ = interp_batch(g, hi_ptr, [list(x)], self._ctx)
         return hj.Interval(float(lo[0]), float(hi[0]))
@@ -338,7 +372,7 @@ class SafetyFilter:
             s = self._state
             if not violations:
                 return s.lam
-            v, _ = interp_batch(s.value.grid(), s.dev_value.ptr, [list(x.x) for x in violations],
+            v, _ = interp_batch(s.grid, s.dev_value.ptr, [list(x.x) for x in violations],
                                 self._ctx, self._ws)
             deepest = -math.inf
             for val in v:
@@ -354,14 +388,14 @@ class SafetyFilter:
                     emergency = True
                     break
             lam = s.lam if lam < s.lam else lam  # std::max(lambda, state.lambda)
-            self._state = _State(value=s.value, dbounds=s.dbounds, dev_value=s.dev_value,
+            self._state = _State(grid=s.grid, value=s.value, dbounds=s.dbounds, dev_value=s.dev_value,
                                  dev_db=s.dev_db, eta_floor=s.eta_floor, min_value=s.min_value,
                                  lam=lam, emergency=s.emergency or emergency)
             return lam
 
     def adopt(self, solved: hj.SolveResult, dbounds: hj.IntervalField):
         """safety.cpp:155-161: install a new converged V* and bounds, reset lambda."""
-        if solved.value.grid().ndims() != self._model.state_dim():
+        if _grid_of(solved).ndims() != self._model.state_dim():
             raise hj.InvalidArgument("adopt: grid rank does not match model")
         nxt = self._make_state(solved, dbounds)
         with self._lock:
@@ -379,7 +413,18 @@ class SafetyFilter:
         return self._snapshot().dbounds
 
     def value_snapshot(self) -> hj.ScalarField:
-        return self._snapshot().value
+        s = self._snapshot()
+        if s.value is None:  # device-adopted V*: copy out once
+            v = s.dev_value.download(np.empty(s.grid.size()))
+            s.value = hj.ScalarField(s.grid, v, check=False)
+        return s.value
+
+    def value_device(self) -> DeviceBuffer:
+        """V* of the current state, resident in HBM (warm-start source)."""
+        return self._snapshot().dev_value
+
+    def grid(self) -> hj.Grid:
+        return self._snapshot().grid
 
     def model(self) -> hj.DynamicsModel:
         return self._model
@@ -593,8 +638,47 @@ class Decomposition:
         with self._lock:
             return self._emergency
 
-    def adopt(self, solved: Sequence[hj.SolveResult], dbounds: Sequence[hj.IntervalField]):
-        """decomposition.cpp:172-182."""
+    def warm_update(self, constraints: Sequence[DeviceBuffer], dbounds: Sequence[hj.IntervalField],
+                    cfg: hj.SolveConfig, contexts: Sequence[hj.Context] | None = None
+                    ) -> list:
+        """The solve half of the reference's background update job
+        (sim.cpp:339-363, "warm subsystem solves, one thread each"): every
+        subsystem re-solves from its filter's current V* under new bounds,
+        concurrently, with V* never leaving HBM.  `constraints[i]` is the
+        subsystem's constraint on the device.  Returns DeviceSolve results
+        for adopt()."""
+        if len(constraints) != len(self._subs) or len(dbounds) != len(self._subs):
+            raise hj.InvalidArgument("warm_update: one constraint and bound field per subsystem")
+        self._need_filters()
+        ctxs = list(contexts) if contexts else [hj.Context(0) for _ in self._subs]
+        out: list = [None] * len(self._subs)
+        errors: list = [None] * len(self._subs)
+
+        def job(i):
+            try:
+                f, s = self._filters[i], self._subs[i]
+                g = f.grid()
+                dst = DeviceBuffer(ctxs[i], g.size() * 8)
+                r = hj.solve_dev(g, s.model, dbounds[i], f.value_device().ptr, constraints[i].ptr,
+                                 dst.ptr, cfg, ctx=ctxs[i])
+                out[i] = DeviceSolve(grid=g, value=dst, iterations=r.iterations, dt=r.dt,
+                                     wall_seconds=r.wall_seconds, converged=r.converged,
+                                     final_residual=r.final_residual)
+            except Exception as e:  # reported like the reference's job->error
+                errors[i] = e
+
+        threads = [threading.Thread(target=job, args=(i,)) for i in range(len(self._subs))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for e in errors:
+            if e is not None:
+                raise e
+        return out
+
+    def adopt(self, solved: Sequence, dbounds: Sequence[hj.IntervalField]):
+        """decomposition.cpp:172-182 (host SolveResults or device DeviceSolves)."""
         if len(solved) != len(self._subs) or len(dbounds) != len(self._subs):
             raise hj.InvalidArgument("adopt: one result per subsystem")
         with self._lock:

@@ -130,3 +130,46 @@ def test_filter_errors(gpu_ctx, oracle):
         f.filter(list(X[0]), [0.0, 1.0])
     with pytest.raises(hj.InvalidArgument, match="rank mismatch"):
         f.value_at([0.0, 1.0])
+
+
+def test_device_resident_warm_update(gpu_ctx, oracle):
+    """The online update loop (sim.cpp:339-363) with V* never leaving HBM:
+    warm solves from every filter's device V* under new bounds, adopted
+    straight from the device, answer exactly like the host path (warm solve
+    of the host V*, adopt of the host result) and like the restatement."""
+    from paper_2101_05916_b200 import configs
+    subs, _, _, dims, X, U = decomposition_10d(n4=9, n2=21)
+    cfg = hj.SolveConfig(tolerance=5e-3, max_iters=40000)
+    from cases import band_np
+    ws = []
+    for s in subs:
+        g = {4: configs.planar_grid(9), 2: configs.vertical_grid(21)}[s.model.state_dim()]
+        c = band_np(g, 0, 0.0, 3.0) if s.model.state_dim() == 2 else band_np(g, 0, -4.0, 4.0)
+        ws.append((g, hj.ScalarField(g, c)))
+    b0 = [hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)]) for g, _ in ws]
+    b1 = [hj.IntervalField.constant(g, [hj.Interval(-0.8, 0.8)]) for g, _ in ws]
+    cold = [hj.solve(c, c, s.model, b, cfg, ctx=gpu_ctx) for s, (g, c), b in zip(subs, ws, b0)]
+    assert all(r.converged for r in cold)
+    dec = hj.Decomposition(subs, *dims)
+    dec.attach([hj.SafetyFilter(s.model, r, b, ctx=gpu_ctx) for s, r, b in zip(subs, cold, b0)])
+    cdev = []
+    for g, c in ws:
+        buf = safety.DeviceBuffer(gpu_ctx, g.size() * 8)
+        buf.upload(c.values())
+        cdev.append(buf)
+    upd = dec.warm_update(cdev, b1, cfg)
+    host = [hj.solve(r.value, c, s.model, b, cfg, ctx=gpu_ctx)
+            for s, r, (g, c), b in zip(subs, cold, ws, b1)]
+    want = [oracle.solve(r.value, c, s.model, b, cfg) for s, r, (g, c), b in zip(subs, cold, ws, b1)]
+    for u, h, w in zip(upd, host, want):
+        assert u.iterations == h.iterations == w.iterations and u.converged
+        assert same(u.to_host().value.values(), h.value.values())
+        assert same(h.value.values(), w.value.values())
+    dec.adopt(upd, b1)
+    ref_dec = hj.Decomposition(subs, *dims)
+    ref_dec.attach([hj.SafetyFilter(s.model, h, b, ctx=gpu_ctx) for s, h, b in zip(subs, host, b1)])
+    a, b = dec.combined_control_batch(X, U), ref_dec.combined_control_batch(X, U)
+    assert same(a.value, b.value) and same(a.control, b.control) and same(a.band, b.band)
+    for i in range(dec.count()):
+        assert dec.filter(i).min_value() == float(np.min(host[i].value.values()))
+        assert same(dec.filter(i).value_snapshot().values(), host[i].value.values())
