@@ -633,6 +633,8 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     // the constraint is read every sweep and never written: keep it in a
     // persisting L2 carve-out when it fits
     l2_pin(ctx->device, f, f.c, rows * f.n3p * sizeof(double));
+    const char* pd = std::getenv("HJB_PDL");
+    f.pdl = (pd && std::strcmp(pd, "0") == 0) ? 0 : 1;
   }
   // loop state after the autotuner (its timing sweeps use the same state)
   CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,

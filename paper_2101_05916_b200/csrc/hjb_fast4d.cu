@@ -329,22 +329,6 @@ template <class S, int kK, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const double* src;
-  double* dst;
-  const CUtensorMap* vmap;
-  if (a.loop == 1) {  // device loop: buffer parity from the loop state
-    if (*(volatile int*)&a.st->done) return;
-    const long long it = a.st->iter;
-    src = (it & 1) ? a.buf1 : a.buf0;
-    dst = (it & 1) ? a.buf0 : a.buf1;
-    vmap = (it & 1) ? &a.map1 : &a.map0;
-  } else {  // explicit buffers (single step, or a slab sweep of the sharded loop)
-    if (a.loop == 2 && *(volatile int*)&a.st->done) return;
-    src = a.src;
-    dst = a.dst;
-    vmap = &a.map0;
-  }
-  (void)src;
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3];
   const uint32_t n3p = a.n3p;
   const uint32_t J = n3p / kK;
@@ -382,6 +366,22 @@ __global__ void __launch_bounds__(MAXT, 1)
     tabs = t;
   }
   __syncthreads();
+  // everything above is independent of the previous sweep: under
+  // programmatic dependent launch it overlaps that sweep's tail; the loop
+  // state and V are read only after the dependency resolves
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  double* dst;
+  const CUtensorMap* vmap;
+  if (a.loop == 1) {  // device loop: buffer parity from the loop state
+    if (*(volatile int*)&a.st->done) return;
+    const long long it = a.st->iter;
+    dst = (it & 1) ? a.buf0 : a.buf1;
+    vmap = (it & 1) ? &a.map1 : &a.map0;
+  } else {  // explicit buffers (single step, or a slab sweep of the sharded loop)
+    if (a.loop == 2 && *(volatile int*)&a.st->done) return;
+    dst = a.dst;
+    vmap = &a.map0;
+  }
   unsigned long long mbits = 0ull;
 
   if (threadIdx.x >= ncons) {
@@ -705,6 +705,8 @@ __global__ void __launch_bounds__(MAXT, 1)
     mbits = (unsigned long long)__double_as_longlong(mdv);
   }
 
+  // this CTA's planes are done: the next sweep may start its set-up
+  if (a.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // CTA max -> global; the last CTA resets the work counter and, in the
   // device loop, runs the sweep epilogue (solver.cpp:347-369)
   __shared__ unsigned long long part[32];
@@ -893,7 +895,7 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
                          200 * 1024);
     attr_set = true;
   }
-  if (a.l2_bytes == 0) {
+  if (a.l2_bytes == 0 && !a.pdl) {
     k_fast4d<S, K, MAXT><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
   }
@@ -902,15 +904,24 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   cfg.blockDim = dim3(a.threads);
   cfg.dynamicSmemBytes = a.smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-  at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(a.l2_base);
-  at[0].val.accessPolicyWindow.num_bytes = a.l2_bytes;
-  at[0].val.accessPolicyWindow.hitRatio = a.l2_hit;
-  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (a.l2_bytes) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(a.l2_base);
+    at[na].val.accessPolicyWindow.num_bytes = a.l2_bytes;
+    at[na].val.accessPolicyWindow.hitRatio = a.l2_hit;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  if (a.pdl) {  // sweep i+1's set-up overlaps sweep i's tail
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT>, a);
 }
 

@@ -42,6 +42,9 @@ struct Fast4dArgs {
   const void* l2_base;
   size_t l2_bytes;
   float l2_hit;
+  // programmatic dependent launch (device loop): the kernel waits on
+  // griddepcontrol before touching the loop state or V
+  int pdl;
 };
 
 // Model shape id for the fast path, or -1 when the generic kernel must run
