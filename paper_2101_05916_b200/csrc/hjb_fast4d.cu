@@ -734,6 +734,301 @@ __global__ void __launch_bounds__(MAXT, 1)
   }
 }
 
+// ---------------------------------------------------------------- k_ho4d
+// One ENO (order 1..3) + TVD-RK stage of the 4D fast-path models: the same
+// arithmetic as k_ho_stage / the CPU restatement (oracle/hj_oracle.c, high
+// order section), organised for a 4D grid.  Each thread owns a 2-cell pencil
+// along the contiguous axis and marches axis 0 with a register window of the
+// pencil's V (planes i0-R .. i0+R, R = order) and its axis-0 face
+// differences, so every V element of the stage input is loaded once from
+// HBM along the march; axis-3 faces are formed once per pencil; the axis-1
+// and axis-2 neighbour pencils come from L1/L2 (CTAs cover tiles of rows).
+constexpr double kHoThird = 1.0 / 3.0;
+constexpr double kHoTwoThirds = 2.0 / 3.0;
+constexpr double kHoSixthNeg = -1.0 / 6.0;
+
+__device__ __forceinline__ double minabs_d(double x, double y) {
+  return fabs(x) <= fabs(y) ? x : y;
+}
+
+// ENO derivative pair of one cell from its 2R face differences
+// A[t] = a(k - R + t) (eno_pair in hjb_kernels.cu, hj_oracle.c)
+template <int R>
+__device__ __forceinline__ void eno_faces(const double* A, double& dm, double& dp) {
+  if (R == 1) {
+    dm = A[0];
+    dp = A[1];
+  } else if (R == 2) {
+    const double d2m1 = A[1] - A[0], d20 = A[2] - A[1], d21 = A[3] - A[2];
+    dm = A[1] + 0.5 * minabs_d(d2m1, d20);
+    dp = A[2] + -0.5 * minabs_d(d20, d21);
+  } else {
+    const double d2m2 = A[1] - A[0], d2m1 = A[2] - A[1], d20 = A[3] - A[2], d21 = A[4] - A[3],
+                 d22 = A[5] - A[4];
+    const double t1 = d2m1 - d2m2, t2 = d20 - d2m1, t3 = d21 - d20, t4 = d22 - d21;
+    {
+      const bool left = fabs(d2m1) <= fabs(d20);
+      const double c2 = left ? d2m1 : d20;
+      const double c3 = left ? minabs_d(t1, t2) : minabs_d(t2, t3);
+      const double w = left ? kHoThird : kHoSixthNeg;
+      dm = (A[2] + 0.5 * c2) + w * c3;
+    }
+    {
+      const bool left = fabs(d20) <= fabs(d21);
+      const double c2 = left ? d20 : d21;
+      const double c3 = left ? minabs_d(t2, t3) : minabs_d(t3, t4);
+      const double w = left ? kHoSixthNeg : kHoThird;
+      dp = (A[3] + -0.5 * c2) + w * c3;
+    }
+  }
+}
+
+__host__ __device__ constexpr int ho4d_maxthreads(int r) { return r >= 3 ? 384 : 512; }
+
+template <class S, int R>
+__global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_constant__ Ho4dArgs a) {
+  constexpr int kK = 2;
+  LoopState* st = a.st;
+  if (*(volatile int*)&st->done) return;
+  const long long it = st->iter;
+  const double* vn = (it & 1) ? a.buf1 : a.buf0;
+  double* outp = (it & 1) ? a.buf0 : a.buf1;
+  const double* __restrict__ vs = a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2);
+  double* dst = a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2);
+  const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
+  const uint32_t J = n3p / kK;
+  uint32_t b = blockIdx.x;
+  const uint32_t chunk = b % a.nchunks;
+  b /= a.nchunks;
+  const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
+  const uint32_t t = threadIdx.x;
+  const uint32_t rr = t / J, j = t - rr * J;
+  const bool in_tile = rr < a.T1 * a.T2;
+  const uint32_t r = in_tile ? rr : 0u;
+  const uint32_t r1 = r / a.T2, r2 = r - r1 * a.T2;
+  const uint32_t i1 = t1 * a.T1 + r1, i2 = t2 * a.T2 + r2, i3 = kK * j;
+  const bool active = in_tile && i1 < n1 && i2 < n2;
+  const uint32_t ci1 = active ? i1 : 0u, ci2 = active ? i2 : 0u;  // clamped for addressing
+  const uint64_t s2 = n3p, s1 = (uint64_t)n2 * n3p, s0 = (uint64_t)n1 * s1;
+  const uint64_t rowo = (uint64_t)ci1 * s1 + (uint64_t)ci2 * s2 + i3;
+  const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
+  const uint32_t c0 = chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, n0);
+
+  // slopes and shapes of the rows (as k_fast4d)
+  double pos_[4][kK], neg_[4][kK];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+    for (int c = 0; c < kK; ++c) {
+      if (c > 0 && !per_cell) {
+        pos_[d][c] = pos_[d][0];
+        neg_[d][c] = neg_[d][0];
+      } else {
+        const uint32_t ka = pick<S>(S::A(d), ci1, ci2, min(i3 + c, n3 - 1));
+        if (S::B(d) < 0) {
+          pos_[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+          neg_[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+        } else {
+          const uint32_t kb = pick<S>(S::B(d), ci1, ci2, min(i3 + c, n3 - 1));
+          const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+          pos_[d][c] = dr;
+          neg_[d][c] = dr;
+        }
+      }
+    }
+  }
+  RowShape shp[4][kK];
+  bool up[4][kK];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+    for (int c = 0; c < kK; ++c) {
+      up[d][c] = sign_clear(pos_[d][c]);
+      if (S::LIN(d)) continue;
+      shp[d][c] = (c > 0 && !per_cell) ? shp[d][0] : row_shape(pos_[d][c], neg_[d][c]);
+    }
+  }
+
+  // axis-0 window: own pencil at planes i0-R .. i0+R and faces a0(i0-R ..
+  // i0+R-1); planes outside the grid only feed ghost faces (0.0)
+  double vw[2 * R + 1][kK], fw[2 * R][kK];
+  auto load_plane = [&](int p, double* out) {
+    if (p >= 0 && p < (int)n0) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(vs + (uint64_t)p * s0 + rowo));
+      out[0] = x.x;
+      out[1] = x.y;
+    } else {
+      out[0] = 0.0;
+      out[1] = 0.0;
+    }
+  };
+#pragma unroll
+  for (int q = 0; q <= 2 * R; ++q) load_plane((int)c0 - R + q, vw[q]);
+#pragma unroll
+  for (int q = 0; q < 2 * R; ++q) {
+    const int f = (int)c0 - R + q;  // face index
+    const bool ok = f >= 0 && f <= (int)n0 - 2;
+#pragma unroll
+    for (int c = 0; c < kK; ++c) fw[q][c] = ok ? (vw[q + 1][c] - vw[q][c]) * inv0 : 0.0;
+  }
+
+  double mdv = 0.0;
+  for (uint32_t i0 = c0; i0 < c1; ++i0) {
+    const uint64_t po = (uint64_t)i0 * s0;
+    double dmv[4][kK], dpv[4][kK];
+    // axis 0
+#pragma unroll
+    for (int c = 0; c < kK; ++c) {
+      double A[2 * R];
+#pragma unroll
+      for (int q = 0; q < 2 * R; ++q) A[q] = fw[q][c];
+      eno_faces<R>(A, dmv[0][c], dpv[0][c]);
+    }
+    // axis 3: values i3-R .. i3+kK-1+R of this row, faces a3(i3-R .. i3+kK-1+R-1)
+    {
+      constexpr int NV = kK + 2 * R;
+      double rv[NV];
+      const double* rowp = vs + po + (uint64_t)ci1 * s1 + (uint64_t)ci2 * s2;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const int k = (int)i3 - R + q;
+        if (q >= R && q < R + kK) {
+          rv[q] = vw[R][q - R];
+        } else {
+          rv[q] = (k >= 0 && k < (int)n3p) ? __ldg(rowp + k) : 0.0;
+        }
+      }
+      double f3[NV - 1];
+#pragma unroll
+      for (int q = 0; q < NV - 1; ++q) {
+        const int f = (int)i3 - R + q;
+        f3[q] = (f >= 0 && f <= (int)n3 - 2) ? (rv[q + 1] - rv[q]) * inv3 : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
+    }
+    // axes 1 and 2: neighbour pencils of this plane
+#pragma unroll
+    for (int ax = 1; ax <= 2; ++ax) {
+      const uint32_t ii = ax == 1 ? ci1 : ci2;
+      const uint32_t nn = ax == 1 ? n1 : n2;
+      const uint64_t sx = ax == 1 ? s1 : s2;
+      const double inv = ax == 1 ? inv1 : inv2;
+      double nv[2 * R + 1][kK];
+#pragma unroll
+      for (int q = 0; q <= 2 * R; ++q) {
+        const int k = (int)ii - R + q;
+        if (q == R) {
+          nv[q][0] = vw[R][0];
+          nv[q][1] = vw[R][1];
+        } else if (k >= 0 && k < (int)nn) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(
+              vs + po + rowo + (int64_t)(q - R) * (int64_t)sx));
+          nv[q][0] = x.x;
+          nv[q][1] = x.y;
+        } else {
+          nv[q][0] = 0.0;
+          nv[q][1] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        double A[2 * R];
+#pragma unroll
+        for (int q = 0; q < 2 * R; ++q) {
+          const int f = (int)ii - R + q;
+          A[q] = (f >= 0 && f <= (int)nn - 2) ? (nv[q + 1][c] - nv[q][c]) * inv : 0.0;
+        }
+        eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
+      }
+    }
+    // numerical Hamiltonian (godunov_flux per axis, summed in axis order),
+    // Euler step, RK combination, VI clamp
+    const double2 cc2 = __ldg(reinterpret_cast<const double2*>(a.c + po + rowo));
+    double vnv[kK];
+    if (a.kind != 0 || a.final_stage) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(vn + po + rowo));
+      vnv[0] = x.x;
+      vnv[1] = x.y;
+    } else {
+      vnv[0] = vw[R][0];
+      vnv[1] = vw[R][1];
+    }
+    double out[kK];
+#pragma unroll
+    for (int c = 0; c < kK; ++c) {
+      double h[4];
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        if (S::LIN(d)) {
+          h[d] = pos_[d][c] * (up[d][c] ? dpv[d][c] : dmv[d][c]);
+        } else {
+          const double ka = pair_kink(shp[d][c].L, dmv[d][c], sign_bit(dmv[d][c]));
+          const double kb = pair_kink(shp[d][c].R, dpv[d][c], sign_bit(dpv[d][c]));
+          h[d] = shape_pick(shp[d][c], ka, kb);
+        }
+      }
+      const double hh = ((h[0] + h[1]) + h[2]) + h[3];
+      const double stv = vw[R][c] + a.dt * hh;
+      double val;
+      switch (a.kind) {
+        case 1: val = 0.5 * vnv[c] + 0.5 * stv; break;
+        case 2: val = 0.75 * vnv[c] + 0.25 * stv; break;
+        case 3: val = kHoThird * vnv[c] + kHoTwoThirds * stv; break;
+        default: val = stv; break;
+      }
+      const double ccv = c == 0 ? cc2.x : cc2.y;
+      out[c] = val > ccv ? val : ccv;
+      const double dv = fabs(out[c] - vnv[c]);
+      if (active && i3 + c < n3 && dv > mdv) mdv = dv;
+    }
+    if (active)
+      *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[1]);
+    // slide the axis-0 window
+#pragma unroll
+    for (int q = 0; q < 2 * R; ++q) {
+      vw[q][0] = vw[q + 1][0];
+      vw[q][1] = vw[q + 1][1];
+    }
+    load_plane((int)i0 + R + 1, vw[2 * R]);
+#pragma unroll
+    for (int q = 0; q < 2 * R - 1; ++q) {
+      fw[q][0] = fw[q + 1][0];
+      fw[q][1] = fw[q + 1][1];
+    }
+    {
+      const int f = (int)i0 + R;
+      const bool ok = f <= (int)n0 - 2;
+#pragma unroll
+      for (int c = 0; c < kK; ++c)
+        fw[2 * R - 1][c] = ok ? (vw[2 * R][c] - vw[2 * R - 1][c]) * inv0 : 0.0;
+    }
+  }
+  if (!a.final_stage) return;
+  // max|V_{n+1} - V_n| -> loop state; the last CTA runs the solve() epilogue
+  unsigned long long mbits = (unsigned long long)__double_as_longlong(mdv);
+  __shared__ unsigned long long part[32];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+  if (lane == 0) part[warp] = mbits;
+  __syncthreads();
+  if (warp != 0) return;
+  mbits = lane < (blockDim.x >> 5) ? part[lane] : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+  if (lane != 0) return;
+  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  __threadfence();
+  const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  loop_epilogue(st, a.handle, a.use_handle);
+}
+
 // Sharded loop: after the residual all-reduce, one thread applies the
 // solve() loop logic to the global max|dV| (every rank decides identically).
 __global__ void k_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
@@ -945,6 +1240,57 @@ cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   else
     launch_shape<ShapeTwin>(a, s);
   return cudaGetLastError();
+}
+
+void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
+  for (int d = 0; d < 4; ++d) {
+    a.n[d] = g.n[d];
+    a.inv[d] = g.inv_spacing[d];
+  }
+  a.n3p = (g.n[3] + 1) / 2 * 2;
+  const uint32_t J = a.n3p / 2;
+  const uint32_t maxt = (uint32_t)ho4d_maxthreads(a.order);
+  // tile of (i1, i2) rows: most rows within the thread bound (neighbour rows
+  // are shared through L1), squarish
+  uint32_t bt1 = 1, bt2 = 1, best = 0;
+  for (uint32_t t1 = 1; t1 <= g.n[1] && t1 * J <= maxt; ++t1)
+    for (uint32_t t2 = 1; t2 <= g.n[2] && t1 * t2 * J <= maxt; ++t2) {
+      const uint32_t score = t1 * t2 * 64 - (t1 > t2 ? t1 - t2 : t2 - t1);
+      if (score > best) {
+        best = score;
+        bt1 = t1;
+        bt2 = t2;
+      }
+    }
+  a.T1 = bt1;
+  a.T2 = bt2;
+  a.tiles1 = (g.n[1] + bt1 - 1) / bt1;
+  a.tiles2 = (g.n[2] + bt2 - 1) / bt2;
+  a.threads = ((bt1 * bt2 * J + 31) / 32) * 32;
+  const uint32_t tiles = a.tiles1 * a.tiles2;
+  uint32_t nch = 1;
+  while (tiles * nch < 2u * sms && g.n[0] / (nch + 1) >= 8) ++nch;
+  a.L = (g.n[0] + nch - 1) / nch;
+  a.nchunks = (g.n[0] + a.L - 1) / a.L;
+  a.blocks = tiles * a.nchunks;
+}
+
+namespace {
+template <class S>
+cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
+  switch (a.order) {
+    case 1: k_ho4d<S, 1><<<a.blocks, a.threads, 0, s>>>(a); break;
+    case 2: k_ho4d<S, 2><<<a.blocks, a.threads, 0, s>>>(a); break;
+    default: k_ho4d<S, 3><<<a.blocks, a.threads, 0, s>>>(a); break;
+  }
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s) {
+  if (shape == 0) return ho4d_shape<ShapePlanarD0>(a, s);
+  if (shape == 1) return ho4d_shape<ShapePlanarD1>(a, s);
+  return ho4d_shape<ShapeTwin>(a, s);
 }
 
 bool l2_pin(int device, Fast4dArgs& a, const void* base, size_t bytes) {

@@ -47,6 +47,30 @@ struct Fast4dArgs {
   int pdl;
 };
 
+// One ENO/TVD-RK stage over a padded 4D grid (k_ho4d, hjb_fast4d.cu): the
+// 4D Godunov fast-path models with constant bounds.  Buffers use the padded
+// layout of Fast4dArgs; roles follow StepArgs (src_sel / dst_sel / kind).
+struct Ho4dArgs {
+  uint32_t n[4];
+  uint32_t n3p;
+  double inv[4];
+  uint32_t T1, T2, tiles1, tiles2, L, nchunks, blocks, threads;
+  const double* tab;
+  int off_pos[4], off_neg[4], off_a[4], off_b[4];
+  const double* c;
+  double* buf0;  // V_n ping-pong (parity = st->iter)
+  double* buf1;
+  double* stage1;
+  double* stage2;
+  int src_sel, dst_sel, kind, final_stage, order;
+  LoopState* st;
+  double dt;
+  cudaGraphConditionalHandle handle;
+  int use_handle;
+};
+void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
+cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s);
+
 // Model shape id for the fast path, or -1 when the generic kernel must run
 // (rank != 4, LF scheme, per-node bounds, rows depending on x0, ...).
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);

@@ -10,6 +10,9 @@
 // solve() epilogue (residual = max|V_{n+1} - V_n| / dt).
 #include <cstring>
 
+#include <cstdlib>
+
+#include "hjb_fast4d.cuh"
 #include "hjb_ho.cuh"
 #include "hjb_internal.cuh"
 #include "hjb_kernels.cuh"
@@ -65,11 +68,24 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
              double* out, hjb_solve_result* res) {
   if (g.nd > 4) return set_err(HJB_ERR_UNSUPPORTED, "solve: high-order schemes up to rank 4");
   const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
-  CUDA_TRY(ctx->v0.ensure(bytes));
-  CUDA_TRY(ctx->v1.ensure(bytes));
-  CUDA_TRY(ctx->v2.ensure(bytes));
-  CUDA_TRY(ctx->v3.ensure(bytes));
-  CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  // 4D fast-path models (Godunov, constant bounds): padded layout + k_ho4d
+  const char* fe = std::getenv("HJB_FAST");
+  const int shape = (fe && std::strcmp(fe, "0") == 0) ? -1 : fast4d_shape(g, m, scheme_id(cfg));
+  const uint64_t rows4 = g.nd == 4 ? static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2] : 0;
+  const uint32_t n3p = g.nd == 4 ? (g.n[3] + 1) / 2 * 2 : 0;
+  const size_t pbytes = shape >= 0 ? rows4 * n3p * sizeof(double) : bytes;
+  CUDA_TRY(ctx->v0.ensure(pbytes));
+  CUDA_TRY(ctx->v1.ensure(pbytes));
+  CUDA_TRY(ctx->v2.ensure(pbytes));
+  CUDA_TRY(ctx->v3.ensure(pbytes));
+  if (shape >= 0) {
+    CUDA_TRY(ctx->pcbuf.ensure(pbytes));
+    CUDA_TRY(launch_pad4(init, ctx->v0.d(), rows4, g.n[3], n3p, ctx->stream));
+    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows4, g.n[3], n3p, ctx->stream));
+    ctx->launches += 2;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   if (cfg->max_iters == 0) {
     if (out != init)
       CUDA_TRY(cudaMemcpyAsync(out, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -93,9 +109,41 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   a.loop = 1;
   Stage st[3];
   const int ns = stages_of(cfg->time_order, st);
+  Ho4dArgs h4;
+  std::memset(&h4, 0, sizeof h4);
+  if (shape >= 0) {
+    h4.order = a.order > 3 ? 3 : a.order;
+    ho4d_config(g, sm_count(ctx->device), h4);
+    h4.tab = m.tab;
+    for (int d = 0; d < 4; ++d) {
+      h4.off_pos[d] = m.row[d].off_pos;
+      h4.off_neg[d] = m.row[d].off_neg;
+      h4.off_a[d] = m.row[d].off_a;
+      h4.off_b[d] = m.row[d].off_b;
+    }
+    h4.c = ctx->pcbuf.d();
+    h4.buf0 = ctx->v0.d();
+    h4.buf1 = ctx->v1.d();
+    h4.stage1 = ctx->v2.d();
+    h4.stage2 = ctx->v3.d();
+    h4.st = ctx->st;
+    h4.dt = dt;
+  }
   // one loop "sweep" = one full RK step (all of its stages)
   SweepLauncher launch = [&](cudaStream_t s, cudaGraphConditionalHandle h, int use) {
     for (int k = 0; k < ns; ++k) {
+      if (shape >= 0) {
+        Ho4dArgs x = h4;
+        x.src_sel = st[k].src;
+        x.dst_sel = st[k].dst;
+        x.kind = st[k].kind;
+        x.final_stage = k == ns - 1;
+        x.handle = h;
+        x.use_handle = use;
+        const cudaError_t e = launch_ho4d(x, shape, s);
+        if (e != cudaSuccess) return e;
+        continue;
+      }
       StepArgs x = a;
       x.src_sel = st[k].src;
       x.dst_sel = st[k].dst;
@@ -141,7 +189,12 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
     CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
   const double* fin = (ls.iter & 1) ? ctx->v1.d() : ctx->v0.d();
-  CUDA_TRY(cudaMemcpyAsync(out, fin, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (shape >= 0) {
+    CUDA_TRY(launch_unpad4(fin, out, rows4, g.n[3], n3p, ctx->stream));
+    ++ctx->launches;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(out, fin, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (ls.status == HJB_ERR_DIVERGED)
     return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
