@@ -1029,6 +1029,284 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   loop_epilogue(st, a.handle, a.use_handle);
 }
 
+// TMA-staged variant: a producer thread streams each plane's V box (tile +
+// R-row halo in i1 and i2, full rows) into a shared-memory ring; consumers
+// read the axis-1/2/3 neighbours from shared memory and only their own
+// pencil (c, V_n, the axis-0 window's next plane) from global memory.
+template <class S, int R>
+__global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_constant__ Ho4dArgs a) {
+  constexpr int kK = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  LoopState* st = a.st;
+  if (*(volatile int*)&st->done) return;
+  const long long it = st->iter;
+  const double* vn = (it & 1) ? a.buf1 : a.buf0;
+  double* outp = (it & 1) ? a.buf0 : a.buf1;
+  const double* __restrict__ vs = a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2);
+  const int msel = a.src_sel == 0 ? (int)(it & 1) : (a.src_sel == 1 ? 2 : 3);
+  double* dst = a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2);
+  const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
+  const uint32_t J = n3p / kK;
+  uint32_t b = blockIdx.x;
+  const uint32_t chunk = b % a.nchunks;
+  b /= a.nchunks;
+  const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
+  const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2;
+  const uint32_t c0 = chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, n0);
+  const uint32_t ncons = a.threads - 32;
+  const uint32_t nwarps_c = ncons >> 5;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ring = a.ring;
+  const uint32_t smem0 = smem_u32(smem_raw);
+  const uint32_t bars = smem0 + ring * a.vslot_bytes;  // full[ring], empty[ring]
+  uint64_t* bar_ptr = reinterpret_cast<uint64_t*>(smem_raw + ring * a.vslot_bytes);
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < ring; ++k) {
+      mbar_init(bar_ptr + k, 1);
+      mbar_init(bar_ptr + ring + k, nwarps_c);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double mdv = 0.0;
+  if (threadIdx.x >= ncons) {
+    if (lane == 0) {
+      for (uint32_t q = 0; c0 + q < c1; ++q) {
+        const uint32_t sl = q % ring, use = q / ring;
+        mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
+        mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes);
+        tma_load4(smem0 + sl * a.vslot_bytes, &a.mapv[msel], 0, (int)base2 - R, (int)base1 - R,
+                  (int)(c0 + q), bars + sl * 8);
+      }
+    }
+  } else {
+    const uint32_t t = threadIdx.x;
+    const uint32_t rr = t / J, j = t - rr * J;
+    const bool in_tile = rr < a.T1 * a.T2;
+    const uint32_t r = in_tile ? rr : 0u;
+    const uint32_t r1 = r / a.T2, r2 = r - r1 * a.T2;
+    const uint32_t i1 = base1 + r1, i2 = base2 + r2, i3 = kK * j;
+    const bool active = in_tile && i1 < n1 && i2 < n2;
+    const uint32_t ci1 = active ? i1 : 0u, ci2 = active ? i2 : 0u;
+    const uint64_t s2 = n3p, s1 = (uint64_t)n2 * n3p, s0 = (uint64_t)n1 * s1;
+    const uint64_t rowo = (uint64_t)ci1 * s1 + (uint64_t)ci2 * s2 + i3;
+    const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
+    const uint32_t W2 = a.T2 + 2 * R;
+    const uint32_t rowb = n3p * 8u;
+    const uint32_t own = (((r1 + R) * W2 + (r2 + R)) * n3p + i3) * 8u;
+
+    double pos_[4][kK], neg_[4][kK];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        if (c > 0 && !per_cell) {
+          pos_[d][c] = pos_[d][0];
+          neg_[d][c] = neg_[d][0];
+        } else {
+          const uint32_t ka = pick<S>(S::A(d), ci1, ci2, min(i3 + c, n3 - 1));
+          if (S::B(d) < 0) {
+            pos_[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+            neg_[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+          } else {
+            const uint32_t kb = pick<S>(S::B(d), ci1, ci2, min(i3 + c, n3 - 1));
+            const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+            pos_[d][c] = dr;
+            neg_[d][c] = dr;
+          }
+        }
+      }
+    }
+    RowShape shp[4][kK];
+    bool up[4][kK];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        up[d][c] = sign_clear(pos_[d][c]);
+        if (S::LIN(d)) continue;
+        shp[d][c] = (c > 0 && !per_cell) ? shp[d][0] : row_shape(pos_[d][c], neg_[d][c]);
+      }
+    }
+    // ghost-face masks of axes 1 and 2 are loop invariant
+    bool ok1[2 * R], ok2[2 * R];
+#pragma unroll
+    for (int q = 0; q < 2 * R; ++q) {
+      const int f1 = (int)ci1 - R + q, f2 = (int)ci2 - R + q;
+      ok1[q] = f1 >= 0 && f1 <= (int)n1 - 2;
+      ok2[q] = f2 >= 0 && f2 <= (int)n2 - 2;
+    }
+
+    double vw[2 * R + 1][kK], fw[2 * R][kK];
+    auto load_plane = [&](int p, double* o) {
+      if (p >= 0 && p < (int)n0) {
+        const double2 x = __ldg(reinterpret_cast<const double2*>(vs + (uint64_t)p * s0 + rowo));
+        o[0] = x.x;
+        o[1] = x.y;
+      } else {
+        o[0] = 0.0;
+        o[1] = 0.0;
+      }
+    };
+#pragma unroll
+    for (int q = 0; q <= 2 * R; ++q) load_plane((int)c0 - R + q, vw[q]);
+#pragma unroll
+    for (int q = 0; q < 2 * R; ++q) {
+      const int f = (int)c0 - R + q;
+      const bool ok = f >= 0 && f <= (int)n0 - 2;
+#pragma unroll
+      for (int c = 0; c < kK; ++c) fw[q][c] = ok ? (vw[q + 1][c] - vw[q][c]) * inv0 : 0.0;
+    }
+
+    uint32_t sl = 0, ph = 0;
+    for (uint32_t i0 = c0; i0 < c1; ++i0) {
+      const uint64_t po = (uint64_t)i0 * s0;
+      // own-pencil global loads first (latency behind the shared-memory math)
+      double vnext[kK];
+      load_plane((int)i0 + R + 1, vnext);
+      const double2 cc2 = __ldg(reinterpret_cast<const double2*>(a.c + po + rowo));
+      double2 vn2 = make_double2(vw[R][0], vw[R][1]);
+      if (a.kind != 0 || a.final_stage)
+        vn2 = __ldg(reinterpret_cast<const double2*>(vn + po + rowo));
+      const uint32_t slot = smem0 + sl * a.vslot_bytes;
+      mbar_wait(bars + sl * 8, ph);
+      double dmv[4][kK], dpv[4][kK];
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        double A[2 * R];
+#pragma unroll
+        for (int q = 0; q < 2 * R; ++q) A[q] = fw[q][c];
+        eno_faces<R>(A, dmv[0][c], dpv[0][c]);
+      }
+      {  // axis 3 from this row in shared memory
+        constexpr int NV = kK + 2 * R;
+        double rv[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const int k = (int)i3 - R + q;
+          if (q >= R && q < R + kK) {
+            rv[q] = vw[R][q - R];
+          } else {
+            rv[q] = (k >= 0 && k < (int)n3p) ? lds1(slot + own + (int)(q - R) * 8) : 0.0;
+          }
+        }
+        double f3[NV - 1];
+#pragma unroll
+        for (int q = 0; q < NV - 1; ++q) {
+          const int f = (int)i3 - R + q;
+          f3[q] = (f >= 0 && f <= (int)n3 - 2) ? (rv[q + 1] - rv[q]) * inv3 : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
+      }
+#pragma unroll
+      for (int ax = 1; ax <= 2; ++ax) {
+        const int step = ax == 1 ? (int)(W2 * rowb) : (int)rowb;
+        const double inv = ax == 1 ? inv1 : inv2;
+        double nv[2 * R + 1][kK];
+#pragma unroll
+        for (int q = 0; q <= 2 * R; ++q) {
+          if (q == R) {
+            nv[q][0] = vw[R][0];
+            nv[q][1] = vw[R][1];
+          } else {
+            const double2 x = lds2(slot + own + (q - R) * step);
+            nv[q][0] = x.x;
+            nv[q][1] = x.y;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          double A[2 * R];
+#pragma unroll
+          for (int q = 0; q < 2 * R; ++q) {
+            const bool ok = ax == 1 ? ok1[q] : ok2[q];
+            A[q] = ok ? (nv[q + 1][c] - nv[q][c]) * inv : 0.0;
+          }
+          eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
+        }
+      }
+      // the V box of this plane is no longer read by this warp
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bars + (ring + sl) * 8);
+      if (++sl == ring) {
+        sl = 0;
+        ph ^= 1u;
+      }
+      double out[kK];
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        double h[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          if (S::LIN(d)) {
+            h[d] = pos_[d][c] * (up[d][c] ? dpv[d][c] : dmv[d][c]);
+          } else {
+            const double ka = pair_kink(shp[d][c].L, dmv[d][c], sign_bit(dmv[d][c]));
+            const double kb = pair_kink(shp[d][c].R, dpv[d][c], sign_bit(dpv[d][c]));
+            h[d] = shape_pick(shp[d][c], ka, kb);
+          }
+        }
+        const double hh = ((h[0] + h[1]) + h[2]) + h[3];
+        const double stv = vw[R][c] + a.dt * hh;
+        const double vnc = c == 0 ? vn2.x : vn2.y;
+        double val;
+        switch (a.kind) {
+          case 1: val = 0.5 * vnc + 0.5 * stv; break;
+          case 2: val = 0.75 * vnc + 0.25 * stv; break;
+          case 3: val = kHoThird * vnc + kHoTwoThirds * stv; break;
+          default: val = stv; break;
+        }
+        const double ccv = c == 0 ? cc2.x : cc2.y;
+        out[c] = val > ccv ? val : ccv;
+        const double dv = fabs(out[c] - vnc);
+        if (active && i3 + c < n3 && dv > mdv) mdv = dv;
+      }
+      if (active) *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[1]);
+#pragma unroll
+      for (int q = 0; q < 2 * R; ++q) {
+        vw[q][0] = vw[q + 1][0];
+        vw[q][1] = vw[q + 1][1];
+      }
+      vw[2 * R][0] = vnext[0];
+      vw[2 * R][1] = vnext[1];
+#pragma unroll
+      for (int q = 0; q < 2 * R - 1; ++q) {
+        fw[q][0] = fw[q + 1][0];
+        fw[q][1] = fw[q + 1][1];
+      }
+      {
+        const int f = (int)i0 + R;
+        const bool ok = f <= (int)n0 - 2;
+#pragma unroll
+        for (int c = 0; c < kK; ++c)
+          fw[2 * R - 1][c] = ok ? (vw[2 * R][c] - vw[2 * R - 1][c]) * inv0 : 0.0;
+      }
+    }
+  }
+  if (!a.final_stage) return;
+  unsigned long long mbits = (unsigned long long)__double_as_longlong(mdv);
+  __shared__ unsigned long long part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+  if (lane == 0) part[warp] = mbits;
+  __syncthreads();
+  if (warp != 0) return;
+  mbits = lane < (blockDim.x >> 5) ? part[lane] : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+  if (lane != 0) return;
+  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  __threadfence();
+  const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  loop_epilogue(st, a.handle, a.use_handle);
+}
+
 // Sharded loop: after the residual all-reduce, one thread applies the
 // solve() loop logic to the global max|dV| (every rank decides identically).
 __global__ void k_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
@@ -1267,6 +1545,43 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   a.tiles1 = (g.n[1] + bt1 - 1) / bt1;
   a.tiles2 = (g.n[2] + bt2 - 1) / bt2;
   a.threads = ((bt1 * bt2 * J + 31) / 32) * 32;
+  // TMA variant: ring of V boxes (tile + R halo rows in i1, i2), one
+  // producer warp; the largest tile (most consumer rows, then the smallest
+  // halo ratio) whose 3-deep (else 2-deep) ring fits 200 KB
+  a.tma = 0;
+  {
+    const uint32_t R = (uint32_t)a.order;
+    const uint32_t maxc = maxt - 32;
+    uint32_t bt1 = 0, bt2 = 0, bring = 0;
+    double bscore = -1.0;
+    for (uint32_t ring = 3; ring >= 2 && bt1 == 0; --ring)
+      for (uint32_t t1 = 1; t1 <= g.n[1] && t1 * J <= maxc; ++t1)
+        for (uint32_t t2 = 1; t2 <= g.n[2] && t1 * t2 * J <= maxc; ++t2) {
+          const size_t vb = (size_t)(t1 + 2 * R) * (t2 + 2 * R) * a.n3p * 8;
+          const size_t slot = (vb + 127) / 128 * 128;
+          if (ring * slot + 2 * ring * 8 > 200 * 1024) continue;
+          const double score = t1 * t2 * 1000.0 - double((t1 + 2 * R) * (t2 + 2 * R)) / (t1 * t2);
+          if (score > bscore) {
+            bscore = score;
+            bt1 = t1;
+            bt2 = t2;
+            bring = ring;
+          }
+        }
+    const char* e = std::getenv("HJB_HO_TMA");
+    if (bt1 && a.n3p <= 256 && !(e && std::strcmp(e, "0") == 0)) {
+      a.tma = 1;
+      a.T1 = bt1;
+      a.T2 = bt2;
+      a.tiles1 = (g.n[1] + bt1 - 1) / bt1;
+      a.tiles2 = (g.n[2] + bt2 - 1) / bt2;
+      a.threads = ((bt1 * bt2 * J + 31) / 32) * 32 + 32;
+      a.ring = bring;
+      a.vbox_bytes = (bt1 + 2 * R) * (bt2 + 2 * R) * a.n3p * 8;
+      a.vslot_bytes = (a.vbox_bytes + 127) / 128 * 128;
+      a.smem = bring * a.vslot_bytes + 2 * bring * 8;
+    }
+  }
   const uint32_t tiles = a.tiles1 * a.tiles2;
   uint32_t nch = 1;
   while (tiles * nch < 2u * sms && g.n[0] / (nch + 1) >= 8) ++nch;
@@ -1276,8 +1591,26 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
 }
 
 namespace {
+template <class S, int R>
+void ho4t_launch(const Ho4dArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ho4t<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_ho4t<S, R><<<a.blocks, a.threads, a.smem, s>>>(a);
+}
+
 template <class S>
 cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
+  if (a.tma) {
+    switch (a.order) {
+      case 1: ho4t_launch<S, 1>(a, s); break;
+      case 2: ho4t_launch<S, 2>(a, s); break;
+      default: ho4t_launch<S, 3>(a, s); break;
+    }
+    return cudaGetLastError();
+  }
   switch (a.order) {
     case 1: k_ho4d<S, 1><<<a.blocks, a.threads, 0, s>>>(a); break;
     case 2: k_ho4d<S, 2><<<a.blocks, a.threads, 0, s>>>(a); break;
@@ -1286,6 +1619,32 @@ cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 }  // namespace
+
+cudaError_t ho4d_make_maps(Ho4dArgs& a) {
+  if (!a.tma) return cudaSuccess;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const uint32_t R = (uint32_t)a.order;
+  const cuuint64_t dims[4] = {a.n3p, a.n[2], a.n[1], a.n[0]};
+  const cuuint64_t strides[3] = {(cuuint64_t)a.n3p * 8, (cuuint64_t)a.n3p * a.n[2] * 8,
+                                 (cuuint64_t)a.n3p * a.n[2] * a.n[1] * 8};
+  const cuuint32_t box[4] = {a.n3p, a.T2 + 2 * R, a.T1 + 2 * R, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  double* ptrs[4] = {a.buf0, a.buf1, a.stage1, a.stage2};
+  for (int k = 0; k < 4; ++k) {
+    CUresult r = encode(&a.mapv[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ptrs[k], dims, strides,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
 
 cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s) {
   if (shape == 0) return ho4d_shape<ShapePlanarD0>(a, s);

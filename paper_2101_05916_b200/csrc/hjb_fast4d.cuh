@@ -67,8 +67,16 @@ struct Ho4dArgs {
   double dt;
   cudaGraphConditionalHandle handle;
   int use_handle;
+  // TMA-staged variant (k_ho4t): tensor maps of the four possible stage
+  // inputs (buf0, buf1, stage1, stage2) with a box of tile + R-row halo in
+  // i1 and i2, the shared-memory ring of those boxes, its depth
+  CUtensorMap mapv[4];
+  uint32_t vbox_bytes, vslot_bytes, ring, smem, tma;
 };
 void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
+// fill mapv[] for the current buffers (k_ho4t); returns cudaErrorNotSupported
+// when the driver entry point is unavailable
+cudaError_t ho4d_make_maps(Ho4dArgs& a);
 cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s);
 
 // Model shape id for the fast path, or -1 when the generic kernel must run
