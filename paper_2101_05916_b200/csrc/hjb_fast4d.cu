@@ -783,7 +783,7 @@ __device__ __forceinline__ void eno_faces(const double* A, double& dm, double& d
   }
 }
 
-__host__ __device__ constexpr int ho4d_maxthreads(int r) { return r >= 3 ? 384 : 512; }
+__host__ __device__ constexpr int ho4d_maxthreads(int r) { return r >= 3 ? 352 : 512; }
 
 template <class S, int R>
 __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_constant__ Ho4dArgs a) {
@@ -1161,16 +1161,31 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
       for (int c = 0; c < kK; ++c) fw[q][c] = ok ? (vw[q + 1][c] - vw[q][c]) * inv0 : 0.0;
     }
 
+    // own-pencil global loads run one plane ahead (register FIFO): c, V_n
+    // and the axis-0 window's next plane of step i0 are issued in step i0-1
+    const bool need_vn = a.kind != 0 || a.final_stage;
+    auto load_own = [&](uint32_t p, double2& cc, double2& vv, double* nx) {
+      if (p < c1) {
+        const uint64_t o = (uint64_t)p * s0 + rowo;
+        cc = __ldg(reinterpret_cast<const double2*>(a.c + o));
+        if (need_vn) vv = __ldg(reinterpret_cast<const double2*>(vn + o));
+      }
+      load_plane((int)p + R + 1, nx);
+    };
+    // (ENO3: the FIFO hides the loads behind a whole step; lower orders
+    // load at the step start, which costs fewer registers)
+    constexpr bool kAhead = R >= 3;
+    double2 cc_n = make_double2(0.0, 0.0), vn_n = make_double2(0.0, 0.0);
+    double vnext_n[kK] = {0.0, 0.0};
+    if (kAhead) load_own(c0, cc_n, vn_n, vnext_n);
     uint32_t sl = 0, ph = 0;
     for (uint32_t i0 = c0; i0 < c1; ++i0) {
       const uint64_t po = (uint64_t)i0 * s0;
-      // own-pencil global loads first (latency behind the shared-memory math)
-      double vnext[kK];
-      load_plane((int)i0 + R + 1, vnext);
-      const double2 cc2 = __ldg(reinterpret_cast<const double2*>(a.c + po + rowo));
-      double2 vn2 = make_double2(vw[R][0], vw[R][1]);
-      if (a.kind != 0 || a.final_stage)
-        vn2 = __ldg(reinterpret_cast<const double2*>(vn + po + rowo));
+      if (!kAhead) load_own(i0, cc_n, vn_n, vnext_n);
+      const double2 cc2 = cc_n;
+      const double2 vn2 = need_vn ? vn_n : make_double2(vw[R][0], vw[R][1]);
+      double vnext[kK] = {vnext_n[0], vnext_n[1]};
+      if (kAhead) load_own(i0 + 1, cc_n, vn_n, vnext_n);
       const uint32_t slot = smem0 + sl * a.vslot_bytes;
       mbar_wait(bars + sl * 8, ph);
       double dmv[4][kK], dpv[4][kK];
