@@ -1046,12 +1046,15 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
   const int msel = a.src_sel == 0 ? (int)(it & 1) : (a.src_sel == 1 ? 2 : 3);
   double* dst = a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2);
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
-  const uint32_t J = n3p / kK;
+  const uint32_t J = a.T3 / kK;  // pencil threads per tile row
+  const uint32_t B3 = a.T3 + 2 * a.H3;  // box row width (cells)
   uint32_t b = blockIdx.x;
   const uint32_t chunk = b % a.nchunks;
   b /= a.nchunks;
+  const uint32_t seg = b % a.segs;
+  b /= a.segs;
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
-  const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2;
+  const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2, base3 = seg * a.T3;
   const uint32_t c0 = chunk * a.L;
   const uint32_t c1 = min(c0 + a.L, n0);
   const uint32_t ncons = a.threads - 32;
@@ -1076,8 +1079,8 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
         const uint32_t sl = q % ring, use = q / ring;
         mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
         mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes);
-        tma_load4(smem0 + sl * a.vslot_bytes, &a.mapv[msel], 0, (int)base2 - R, (int)base1 - R,
-                  (int)(c0 + q), bars + sl * 8);
+        tma_load4(smem0 + sl * a.vslot_bytes, &a.mapv[msel], (int)base3 - (int)a.H3,
+                  (int)base2 - R, (int)base1 - R, (int)(c0 + q), bars + sl * 8);
       }
     }
   } else {
@@ -1086,15 +1089,17 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
     const bool in_tile = rr < a.T1 * a.T2;
     const uint32_t r = in_tile ? rr : 0u;
     const uint32_t r1 = r / a.T2, r2 = r - r1 * a.T2;
-    const uint32_t i1 = base1 + r1, i2 = base2 + r2, i3 = kK * j;
-    const bool active = in_tile && i1 < n1 && i2 < n2;
+    const uint32_t i1 = base1 + r1, i2 = base2 + r2;
+    const uint32_t i3u = base3 + kK * j;
+    const bool active = in_tile && i1 < n1 && i2 < n2 && i3u < n3p;
+    const uint32_t i3 = i3u < n3p ? i3u : n3p - kK;  // clamped for addressing
     const uint32_t ci1 = active ? i1 : 0u, ci2 = active ? i2 : 0u;
     const uint64_t s2 = n3p, s1 = (uint64_t)n2 * n3p, s0 = (uint64_t)n1 * s1;
     const uint64_t rowo = (uint64_t)ci1 * s1 + (uint64_t)ci2 * s2 + i3;
     const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
     const uint32_t W2 = a.T2 + 2 * R;
-    const uint32_t rowb = n3p * 8u;
-    const uint32_t own = (((r1 + R) * W2 + (r2 + R)) * n3p + i3) * 8u;
+    const uint32_t rowb = B3 * 8u;
+    const uint32_t own = (((r1 + R) * W2 + (r2 + R)) * B3 + (i3 - base3 + a.H3)) * 8u;
 
     double pos_[4][kK], neg_[4][kK];
 #pragma unroll
@@ -1567,37 +1572,67 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   {
     const uint32_t R = (uint32_t)a.order;
     const uint32_t maxc = maxt - 32;
-    uint32_t bt1 = 0, bt2 = 0, bring = 0;
-    double bscore = -1.0;
-    for (uint32_t ring = 3; ring >= 2 && bt1 == 0; --ring)
-      for (uint32_t t1 = 1; t1 <= g.n[1] && t1 * J <= maxc; ++t1)
-        for (uint32_t t2 = 1; t2 <= g.n[2] && t1 * t2 * J <= maxc; ++t2) {
-          const size_t vb = (size_t)(t1 + 2 * R) * (t2 + 2 * R) * a.n3p * 8;
+    // tiles cover T1 x T2 rows x a T3-cell segment of axis 3; the box adds
+    // R rows in i1, i2 and H3 = R rounded up to even cells on each side of
+    // the segment (16-byte aligned pencils).  Minimise the grid traffic:
+    // box cells read per useful cell, including the waste of partial tiles.
+    const uint32_t H3 = (R + 1) / 2 * 2;
+    uint32_t bt1 = 0, bt2 = 0, bt3 = 0, bring = 0;
+    double bcost = 1e30;
+    const uint32_t want_ring = 4;
+    const char* ft3 = std::getenv("HJB_HO_T3");  // experiment override of the segment width
+    const uint32_t only_t3 = ft3 ? (uint32_t)std::atoi(ft3) : 0u;
+    // segment width: full rows up to 64 cells, else 24..40 (measured on
+    // 51^4 / 71^4 / 101^4: narrower segments lose coalescing, wider tiles
+    // lose rows)
+    const uint32_t t3lo = a.n3p <= 64 ? a.n3p : 24u, t3hi = a.n3p <= 64 ? a.n3p : 40u;
+    for (uint32_t t3 = 8; t3 <= a.n3p; t3 += 2) {
+      if (only_t3 ? t3 != only_t3 : (t3 < t3lo || t3 > t3hi)) continue;
+      const uint32_t B3 = t3 + 2 * H3;
+      if (B3 > 256) break;
+      const uint32_t jj = t3 / 2, segs = (a.n3p + t3 - 1) / t3;
+      for (uint32_t t1 = 1; t1 <= g.n[1] && t1 * jj <= maxc; ++t1)
+        for (uint32_t t2 = 1; t2 <= g.n[2] && t1 * t2 * jj <= maxc; ++t2) {
+          if (t1 * t2 * jj < maxc / 2) continue;  // keep the CTA at least half full
+          const size_t vb = (size_t)(t1 + 2 * R) * (t2 + 2 * R) * B3 * 8;
           const size_t slot = (vb + 127) / 128 * 128;
-          if (ring * slot + 2 * ring * 8 > 200 * 1024) continue;
-          const double score = t1 * t2 * 1000.0 - double((t1 + 2 * R) * (t2 + 2 * R)) / (t1 * t2);
-          if (score > bscore) {
-            bscore = score;
+          uint32_t ring = want_ring;
+          while (ring >= 2 && ring * slot + 2 * ring * 8 > 200 * 1024) --ring;
+          if (ring < 2) continue;
+          const double useful = double(g.n[1]) * g.n[2] * a.n3p;
+          const double boxes = double((g.n[1] + t1 - 1) / t1) * ((g.n[2] + t2 - 1) / t2) * segs;
+          const double cost = boxes * double(vb / 8) / useful + (ring < 3 ? 0.5 : 0.0);
+          if (cost < bcost) {
+            bcost = cost;
             bt1 = t1;
             bt2 = t2;
+            bt3 = t3;
             bring = ring;
           }
         }
+    }
     const char* e = std::getenv("HJB_HO_TMA");
-    if (bt1 && a.n3p <= 256 && !(e && std::strcmp(e, "0") == 0)) {
+    if (bt1 && !(e && std::strcmp(e, "0") == 0)) {
       a.tma = 1;
       a.T1 = bt1;
       a.T2 = bt2;
+      a.T3 = bt3;
+      a.H3 = H3;
+      a.segs = (a.n3p + bt3 - 1) / bt3;
       a.tiles1 = (g.n[1] + bt1 - 1) / bt1;
       a.tiles2 = (g.n[2] + bt2 - 1) / bt2;
-      a.threads = ((bt1 * bt2 * J + 31) / 32) * 32 + 32;
+      a.threads = ((bt1 * bt2 * (bt3 / 2) + 31) / 32) * 32 + 32;
       a.ring = bring;
-      a.vbox_bytes = (bt1 + 2 * R) * (bt2 + 2 * R) * a.n3p * 8;
+      a.vbox_bytes = (bt1 + 2 * R) * (bt2 + 2 * R) * (bt3 + 2 * H3) * 8;
       a.vslot_bytes = (a.vbox_bytes + 127) / 128 * 128;
       a.smem = bring * a.vslot_bytes + 2 * bring * 8;
+      if (std::getenv("HJB_HO_VERBOSE"))
+        std::fprintf(stderr, "ho4t R=%u tile %ux%ux%u (box %ux%ux%u) ring %u threads %u smem %u\n",
+                     R, bt1, bt2, bt3, bt1 + 2 * R, bt2 + 2 * R, bt3 + 2 * H3, bring, a.threads,
+                     a.smem);
     }
   }
-  const uint32_t tiles = a.tiles1 * a.tiles2;
+  const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
   uint32_t nch = 1;
   while (tiles * nch < 2u * sms && g.n[0] / (nch + 1) >= 8) ++nch;
   a.L = (g.n[0] + nch - 1) / nch;
@@ -1649,7 +1684,7 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a) {
   const cuuint64_t dims[4] = {a.n3p, a.n[2], a.n[1], a.n[0]};
   const cuuint64_t strides[3] = {(cuuint64_t)a.n3p * 8, (cuuint64_t)a.n3p * a.n[2] * 8,
                                  (cuuint64_t)a.n3p * a.n[2] * a.n[1] * 8};
-  const cuuint32_t box[4] = {a.n3p, a.T2 + 2 * R, a.T1 + 2 * R, 1};
+  const cuuint32_t box[4] = {a.T3 + 2 * a.H3, a.T2 + 2 * R, a.T1 + 2 * R, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   double* ptrs[4] = {a.buf0, a.buf1, a.stage1, a.stage2};
   for (int k = 0; k < 4; ++k) {

@@ -72,6 +72,7 @@ struct Ho4dArgs {
   // i1 and i2, the shared-memory ring of those boxes, its depth
   CUtensorMap mapv[4];
   uint32_t vbox_bytes, vslot_bytes, ring, smem, tma;
+  uint32_t T3, H3, segs;  // axis-3 segment per tile (even), its box halo (even >= R), segments per row
 };
 void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
 // fill mapv[] for the current buffers (k_ho4t); returns cudaErrorNotSupported
