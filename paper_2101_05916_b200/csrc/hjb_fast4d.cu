@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include <cudaTypedefs.h>
 
@@ -751,18 +752,41 @@ __device__ __forceinline__ double minabs_d(double x, double y) {
   return fabs(x) <= fabs(y) ? x : y;
 }
 
-// ENO derivative pair of one cell from its 2R face differences
-// A[t] = a(k - R + t) (eno_pair in hjb_kernels.cu, hj_oracle.c)
+// ENO selection of one cell from its 2R face differences A[t] = a(k-R+t),
+// their second differences d2[t] = A[t+1] - A[t] and third differences
+// t3[t] = d2[t+1] - d2[t] (eno_pair in hjb_kernels.cu, hj_oracle.c; the
+// D2 / D3 operands are the same subtractions, shared between neighbours)
 template <int R>
-__device__ __forceinline__ void eno_faces(const double* A, double& dm, double& dp) {
+__device__ __forceinline__ void eno_sel(const double* A, const double* d2, const double* t3,
+                                        double& dm, double& dp) {
   if (R == 1) {
     dm = A[0];
     dp = A[1];
   } else if (R == 2) {
-    const double d2m1 = A[1] - A[0], d20 = A[2] - A[1], d21 = A[3] - A[2];
-    dm = A[1] + 0.5 * minabs_d(d2m1, d20);
-    dp = A[2] + -0.5 * minabs_d(d20, d21);
+    dm = A[1] + 0.5 * minabs_d(d2[0], d2[1]);
+    dp = A[2] + -0.5 * minabs_d(d2[1], d2[2]);
   } else {
+    // d2[0..4] = D2(-2..2), t3[0..3] = D2(-1)-D2(-2) .. D2(2)-D2(1)
+    {
+      const bool left = fabs(d2[1]) <= fabs(d2[2]);
+      const double c2 = left ? d2[1] : d2[2];
+      const double c3 = left ? minabs_d(t3[0], t3[1]) : minabs_d(t3[1], t3[2]);
+      const double w = left ? kHoThird : kHoSixthNeg;
+      dm = (A[2] + 0.5 * c2) + w * c3;
+    }
+    {
+      const bool left = fabs(d2[2]) <= fabs(d2[3]);
+      const double c2 = left ? d2[2] : d2[3];
+      const double c3 = left ? minabs_d(t3[1], t3[2]) : minabs_d(t3[2], t3[3]);
+      const double w = left ? kHoSixthNeg : kHoThird;
+      dp = (A[3] + -0.5 * c2) + w * c3;
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void eno_faces(const double* A, double& dm, double& dp) {
+  if (R == 3) {  // named scalars: the register-tight ENO3 kernel allocates them best
     const double d2m2 = A[1] - A[0], d2m1 = A[2] - A[1], d20 = A[3] - A[2], d21 = A[4] - A[3],
                  d22 = A[5] - A[4];
     const double t1 = d2m1 - d2m2, t2 = d20 - d2m1, t3 = d21 - d20, t4 = d22 - d21;
@@ -780,7 +804,27 @@ __device__ __forceinline__ void eno_faces(const double* A, double& dm, double& d
       const double w = left ? kHoSixthNeg : kHoThird;
       dp = (A[3] + -0.5 * c2) + w * c3;
     }
+    return;
   }
+  double d2[2 * R > 1 ? 2 * R - 1 : 1], t3[2 * R > 2 ? 2 * R - 2 : 1];
+#pragma unroll
+  for (int q = 0; q < 2 * R - 1; ++q) d2[q] = A[q + 1] - A[q];
+#pragma unroll
+  for (int q = 0; q < 2 * R - 2; ++q) t3[q] = d2[q + 1] - d2[q];
+  eno_sel<R>(A, d2, t3, dm, dp);
+}
+
+// both cells of a 2-cell pencil from the 2R+1 faces of the pencil
+// (f[t] = a(k0-R+t)); second / third differences formed once
+template <int R>
+__device__ __forceinline__ void eno_pencil(const double* f, double* dm, double* dp) {
+  double d2[2 * R], t3[2 * R > 1 ? 2 * R - 1 : 1];
+#pragma unroll
+  for (int q = 0; q < 2 * R; ++q) d2[q] = f[q + 1] - f[q];
+#pragma unroll
+  for (int q = 0; q < 2 * R - 1; ++q) t3[q] = d2[q + 1] - d2[q];
+  eno_sel<R>(f, d2, t3, dm[0], dp[0]);
+  eno_sel<R>(f + 1, d2 + 1, t3 + 1, dm[1], dp[1]);
 }
 
 __host__ __device__ constexpr int ho4d_maxthreads(int r) { return r >= 3 ? 352 : 512; }
@@ -1144,6 +1188,13 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
       ok1[q] = f1 >= 0 && f1 <= (int)n1 - 2;
       ok2[q] = f2 >= 0 && f2 <= (int)n2 - 2;
     }
+    bool interior = false;
+    if constexpr (R <= 2) {
+      bool own_in = (int)i3 >= R && (int)i3 + kK - 1 + R <= (int)n3 - 1;
+#pragma unroll
+      for (int q = 0; q < 2 * R; ++q) own_in = own_in && ok1[q] && ok2[q];
+      interior = __all_sync(0xffffffffu, own_in);
+    }
 
     double vw[2 * R + 1][kK], fw[2 * R][kK];
     auto load_plane = [&](int p, double* o) {
@@ -1201,52 +1252,127 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
         for (int q = 0; q < 2 * R; ++q) A[q] = fw[q][c];
         eno_faces<R>(A, dmv[0][c], dpv[0][c]);
       }
-      {  // axis 3 from this row in shared memory
-        constexpr int NV = kK + 2 * R;
-        double rv[NV];
+      // axes 3, 1, 2 from this plane's box in shared memory; warps whose
+      // faces are all inside the grid skip the ghost-face selects
+      auto inplane = [&](auto interior) {
+        constexpr bool kIn = decltype(interior)::value;
+        {  // axis 3: the pencil's row
+          constexpr int NV = kK + 2 * R;
+          double rv[NV];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const int k = (int)i3 - R + q;
-          if (q >= R && q < R + kK) {
-            rv[q] = vw[R][q - R];
+          for (int q = 0; q < NV; ++q) {
+            const int k = (int)i3 - R + q;
+            if (q >= R && q < R + kK) {
+              rv[q] = vw[R][q - R];
+            } else if (kIn) {
+              rv[q] = lds1(slot + own + (int)(q - R) * 8);
+            } else {
+              rv[q] = (k >= 0 && k < (int)n3p) ? lds1(slot + own + (int)(q - R) * 8) : 0.0;
+            }
+          }
+          double f3[NV - 1];
+#pragma unroll
+          for (int q = 0; q < NV - 1; ++q) {
+            const int f = (int)i3 - R + q;
+            const double d = (rv[q + 1] - rv[q]) * inv3;
+            f3[q] = (kIn || (f >= 0 && f <= (int)n3 - 2)) ? d : 0.0;
+          }
+          if (R >= 3) {  // per cell: fewer live registers at the ENO3 register cap
+#pragma unroll
+            for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
           } else {
-            rv[q] = (k >= 0 && k < (int)n3p) ? lds1(slot + own + (int)(q - R) * 8) : 0.0;
-          }
-        }
-        double f3[NV - 1];
+            double dm3[kK], dp3[kK];
+            eno_pencil<R>(f3, dm3, dp3);
 #pragma unroll
-        for (int q = 0; q < NV - 1; ++q) {
-          const int f = (int)i3 - R + q;
-          f3[q] = (f >= 0 && f <= (int)n3 - 2) ? (rv[q + 1] - rv[q]) * inv3 : 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
-      }
-#pragma unroll
-      for (int ax = 1; ax <= 2; ++ax) {
-        const int step = ax == 1 ? (int)(W2 * rowb) : (int)rowb;
-        const double inv = ax == 1 ? inv1 : inv2;
-        double nv[2 * R + 1][kK];
-#pragma unroll
-        for (int q = 0; q <= 2 * R; ++q) {
-          if (q == R) {
-            nv[q][0] = vw[R][0];
-            nv[q][1] = vw[R][1];
-          } else {
-            const double2 x = lds2(slot + own + (q - R) * step);
-            nv[q][0] = x.x;
-            nv[q][1] = x.y;
+            for (int c = 0; c < kK; ++c) {
+              dmv[3][c] = dm3[c];
+              dpv[3][c] = dp3[c];
+            }
           }
         }
 #pragma unroll
-        for (int c = 0; c < kK; ++c) {
-          double A[2 * R];
+        for (int ax = 1; ax <= 2; ++ax) {
+          const int step = ax == 1 ? (int)(W2 * rowb) : (int)rowb;
+          const double inv = ax == 1 ? inv1 : inv2;
+          double nv[2 * R + 1][kK];
 #pragma unroll
-          for (int q = 0; q < 2 * R; ++q) {
-            const bool ok = ax == 1 ? ok1[q] : ok2[q];
-            A[q] = ok ? (nv[q + 1][c] - nv[q][c]) * inv : 0.0;
+          for (int q = 0; q <= 2 * R; ++q) {
+            if (q == R) {
+              nv[q][0] = vw[R][0];
+              nv[q][1] = vw[R][1];
+            } else {
+              const double2 x = lds2(slot + own + (q - R) * step);
+              nv[q][0] = x.x;
+              nv[q][1] = x.y;
+            }
           }
-          eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            double A[2 * R];
+#pragma unroll
+            for (int q = 0; q < 2 * R; ++q) {
+              const bool ok = kIn || (ax == 1 ? ok1[q] : ok2[q]);
+              const double d = (nv[q + 1][c] - nv[q][c]) * inv;
+              A[q] = ok ? d : 0.0;
+            }
+            eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
+          }
+        }
+      };
+      // (ENO3: the duplicated body costs more than the selects it saves)
+      if constexpr (R <= 2) {
+        if (interior)
+          inplane(std::true_type{});
+        else
+          inplane(std::false_type{});
+      } else {
+        {  // axis 3 from this row in shared memory
+          constexpr int NV = kK + 2 * R;
+          double rv[NV];
+  #pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            const int k = (int)i3 - R + q;
+            if (q >= R && q < R + kK) {
+              rv[q] = vw[R][q - R];
+            } else {
+              rv[q] = (k >= 0 && k < (int)n3p) ? lds1(slot + own + (int)(q - R) * 8) : 0.0;
+            }
+          }
+          double f3[NV - 1];
+  #pragma unroll
+          for (int q = 0; q < NV - 1; ++q) {
+            const int f = (int)i3 - R + q;
+            f3[q] = (f >= 0 && f <= (int)n3 - 2) ? (rv[q + 1] - rv[q]) * inv3 : 0.0;
+          }
+  #pragma unroll
+          for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
+        }
+  #pragma unroll
+        for (int ax = 1; ax <= 2; ++ax) {
+          const int step = ax == 1 ? (int)(W2 * rowb) : (int)rowb;
+          const double inv = ax == 1 ? inv1 : inv2;
+          double nv[2 * R + 1][kK];
+  #pragma unroll
+          for (int q = 0; q <= 2 * R; ++q) {
+            if (q == R) {
+              nv[q][0] = vw[R][0];
+              nv[q][1] = vw[R][1];
+            } else {
+              const double2 x = lds2(slot + own + (q - R) * step);
+              nv[q][0] = x.x;
+              nv[q][1] = x.y;
+            }
+          }
+  #pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            double A[2 * R];
+  #pragma unroll
+            for (int q = 0; q < 2 * R; ++q) {
+              const bool ok = ax == 1 ? ok1[q] : ok2[q];
+              A[q] = ok ? (nv[q + 1][c] - nv[q][c]) * inv : 0.0;
+            }
+            eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
+          }
         }
       }
       // the V box of this plane is no longer read by this warp
