@@ -1077,9 +1077,35 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
 // R-row halo in i1 and i2, full rows) into a shared-memory ring; consumers
 // read the axis-1/2/3 neighbours from shared memory and only their own
 // pencil (c, V_n, the axis-0 window's next plane) from global memory.
-template <class S, int R>
-__global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_constant__ Ho4dArgs a) {
-  constexpr int kK = 2;
+template <int KC>
+__device__ __forceinline__ void ldg_k(const double* p, double* o) {
+  if (KC == 2) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = x.x;
+    o[1] = x.y;
+  } else {
+    o[0] = __ldg(p);
+  }
+}
+template <int KC>
+__device__ __forceinline__ void lds_k(uint32_t addr, double* o) {
+  if (KC == 2) {
+    const double2 x = lds2(addr);
+    o[0] = x.x;
+    o[1] = x.y;
+  } else {
+    o[0] = lds1(addr);
+  }
+}
+
+__host__ __device__ constexpr int ho4t_maxthreads(int r, int kc) {
+  return kc == 1 ? 512 : ho4d_maxthreads(r);
+}
+
+template <class S, int R, int KC>
+__global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
+    k_ho4t(const __grid_constant__ Ho4dArgs a) {
+  constexpr int kK = KC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
   if (*(volatile int*)&st->done) return;
@@ -1199,12 +1225,10 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
     double vw[2 * R + 1][kK], fw[2 * R][kK];
     auto load_plane = [&](int p, double* o) {
       if (p >= 0 && p < (int)n0) {
-        const double2 x = __ldg(reinterpret_cast<const double2*>(vs + (uint64_t)p * s0 + rowo));
-        o[0] = x.x;
-        o[1] = x.y;
+        ldg_k<kK>(vs + (uint64_t)p * s0 + rowo, o);
       } else {
-        o[0] = 0.0;
-        o[1] = 0.0;
+#pragma unroll
+        for (int c = 0; c < kK; ++c) o[c] = 0.0;
       }
     };
 #pragma unroll
@@ -1220,27 +1244,32 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
     // own-pencil global loads run one plane ahead (register FIFO): c, V_n
     // and the axis-0 window's next plane of step i0 are issued in step i0-1
     const bool need_vn = a.kind != 0 || a.final_stage;
-    auto load_own = [&](uint32_t p, double2& cc, double2& vv, double* nx) {
+    auto load_own = [&](uint32_t p, double* cc, double* vv, double* nx) {
       if (p < c1) {
         const uint64_t o = (uint64_t)p * s0 + rowo;
-        cc = __ldg(reinterpret_cast<const double2*>(a.c + o));
-        if (need_vn) vv = __ldg(reinterpret_cast<const double2*>(vn + o));
+        ldg_k<kK>(a.c + o, cc);
+        if (need_vn) ldg_k<kK>(vn + o, vv);
       }
       load_plane((int)p + R + 1, nx);
     };
     // (ENO3: the FIFO hides the loads behind a whole step; lower orders
     // load at the step start, which costs fewer registers)
     constexpr bool kAhead = R >= 3;
-    double2 cc_n = make_double2(0.0, 0.0), vn_n = make_double2(0.0, 0.0);
-    double vnext_n[kK] = {0.0, 0.0};
+    double cc_n[kK], vn_n[kK], vnext_n[kK];
+#pragma unroll
+    for (int c = 0; c < kK; ++c) cc_n[c] = vn_n[c] = vnext_n[c] = 0.0;
     if (kAhead) load_own(c0, cc_n, vn_n, vnext_n);
     uint32_t sl = 0, ph = 0;
     for (uint32_t i0 = c0; i0 < c1; ++i0) {
       const uint64_t po = (uint64_t)i0 * s0;
       if (!kAhead) load_own(i0, cc_n, vn_n, vnext_n);
-      const double2 cc2 = cc_n;
-      const double2 vn2 = need_vn ? vn_n : make_double2(vw[R][0], vw[R][1]);
-      double vnext[kK] = {vnext_n[0], vnext_n[1]};
+      double ccv[kK], vnv[kK], vnext[kK];
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        ccv[c] = cc_n[c];
+        vnv[c] = need_vn ? vn_n[c] : vw[R][c];
+        vnext[c] = vnext_n[c];
+      }
       if (kAhead) load_own(i0 + 1, cc_n, vn_n, vnext_n);
       const uint32_t slot = smem0 + sl * a.vslot_bytes;
       mbar_wait(bars + sl * 8, ph);
@@ -1277,7 +1306,7 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
             const double d = (rv[q + 1] - rv[q]) * inv3;
             f3[q] = (kIn || (f >= 0 && f <= (int)n3 - 2)) ? d : 0.0;
           }
-          if (R >= 3) {  // per cell: fewer live registers at the ENO3 register cap
+          if (R >= 3 || kK != 2) {  // per cell: fewer live registers at the ENO3 register cap
 #pragma unroll
             for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
           } else {
@@ -1298,12 +1327,10 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
 #pragma unroll
           for (int q = 0; q <= 2 * R; ++q) {
             if (q == R) {
-              nv[q][0] = vw[R][0];
-              nv[q][1] = vw[R][1];
+#pragma unroll
+              for (int c = 0; c < kK; ++c) nv[q][c] = vw[R][c];
             } else {
-              const double2 x = lds2(slot + own + (q - R) * step);
-              nv[q][0] = x.x;
-              nv[q][1] = x.y;
+              lds_k<kK>(slot + own + (q - R) * step, nv[q]);
             }
           }
 #pragma unroll
@@ -1355,12 +1382,10 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
   #pragma unroll
           for (int q = 0; q <= 2 * R; ++q) {
             if (q == R) {
-              nv[q][0] = vw[R][0];
-              nv[q][1] = vw[R][1];
+#pragma unroll
+              for (int c = 0; c < kK; ++c) nv[q][c] = vw[R][c];
             } else {
-              const double2 x = lds2(slot + own + (q - R) * step);
-              nv[q][0] = x.x;
-              nv[q][1] = x.y;
+              lds_k<kK>(slot + own + (q - R) * step, nv[q]);
             }
           }
   #pragma unroll
@@ -1398,7 +1423,7 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
         }
         const double hh = ((h[0] + h[1]) + h[2]) + h[3];
         const double stv = vw[R][c] + a.dt * hh;
-        const double vnc = c == 0 ? vn2.x : vn2.y;
+        const double vnc = vnv[c];
         double val;
         switch (a.kind) {
           case 1: val = 0.5 * vnc + 0.5 * stv; break;
@@ -1406,24 +1431,26 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4t(const __grid_consta
           case 3: val = kHoThird * vnc + kHoTwoThirds * stv; break;
           default: val = stv; break;
         }
-        const double ccv = c == 0 ? cc2.x : cc2.y;
-        out[c] = val > ccv ? val : ccv;
+        out[c] = val > ccv[c] ? val : ccv[c];
         const double dv = fabs(out[c] - vnc);
         if (active && i3 + c < n3 && dv > mdv) mdv = dv;
       }
-      if (active) *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[1]);
-#pragma unroll
-      for (int q = 0; q < 2 * R; ++q) {
-        vw[q][0] = vw[q + 1][0];
-        vw[q][1] = vw[q + 1][1];
+      if (active) {
+        if (kK == 2)
+          *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[kK - 1]);
+        else
+          dst[po + rowo] = out[0];
       }
-      vw[2 * R][0] = vnext[0];
-      vw[2 * R][1] = vnext[1];
 #pragma unroll
-      for (int q = 0; q < 2 * R - 1; ++q) {
-        fw[q][0] = fw[q + 1][0];
-        fw[q][1] = fw[q + 1][1];
-      }
+      for (int q = 0; q < 2 * R; ++q)
+#pragma unroll
+        for (int c = 0; c < kK; ++c) vw[q][c] = vw[q + 1][c];
+#pragma unroll
+      for (int c = 0; c < kK; ++c) vw[2 * R][c] = vnext[c];
+#pragma unroll
+      for (int q = 0; q < 2 * R - 1; ++q)
+#pragma unroll
+        for (int c = 0; c < kK; ++c) fw[q][c] = fw[q + 1][c];
       {
         const int f = (int)i0 + R;
         const bool ok = f <= (int)n0 - 2;
@@ -1697,7 +1724,9 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   a.tma = 0;
   {
     const uint32_t R = (uint32_t)a.order;
-    const uint32_t maxc = maxt - 32;
+    const char* ek = std::getenv("HJB_HO_KC");
+    a.kc = (ek && std::atoi(ek) == 1) ? 1u : 2u;
+    const uint32_t maxc = (uint32_t)ho4t_maxthreads(a.order, (int)a.kc) - 32;
     // tiles cover T1 x T2 rows x a T3-cell segment of axis 3; the box adds
     // R rows in i1, i2 and H3 = R rounded up to even cells on each side of
     // the segment (16-byte aligned pencils).  Minimise the grid traffic:
@@ -1716,7 +1745,7 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
       if (only_t3 ? t3 != only_t3 : (t3 < t3lo || t3 > t3hi)) continue;
       const uint32_t B3 = t3 + 2 * H3;
       if (B3 > 256) break;
-      const uint32_t jj = t3 / 2, segs = (a.n3p + t3 - 1) / t3;
+      const uint32_t jj = t3 / a.kc, segs = (a.n3p + t3 - 1) / t3;
       for (uint32_t t1 = 1; t1 <= g.n[1] && t1 * jj <= maxc; ++t1)
         for (uint32_t t2 = 1; t2 <= g.n[2] && t1 * t2 * jj <= maxc; ++t2) {
           if (t1 * t2 * jj < maxc / 2) continue;  // keep the CTA at least half full
@@ -1747,15 +1776,15 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
       a.segs = (a.n3p + bt3 - 1) / bt3;
       a.tiles1 = (g.n[1] + bt1 - 1) / bt1;
       a.tiles2 = (g.n[2] + bt2 - 1) / bt2;
-      a.threads = ((bt1 * bt2 * (bt3 / 2) + 31) / 32) * 32 + 32;
+      a.threads = ((bt1 * bt2 * (bt3 / a.kc) + 31) / 32) * 32 + 32;
       a.ring = bring;
       a.vbox_bytes = (bt1 + 2 * R) * (bt2 + 2 * R) * (bt3 + 2 * H3) * 8;
       a.vslot_bytes = (a.vbox_bytes + 127) / 128 * 128;
       a.smem = bring * a.vslot_bytes + 2 * bring * 8;
       if (std::getenv("HJB_HO_VERBOSE"))
-        std::fprintf(stderr, "ho4t R=%u tile %ux%ux%u (box %ux%ux%u) ring %u threads %u smem %u\n",
-                     R, bt1, bt2, bt3, bt1 + 2 * R, bt2 + 2 * R, bt3 + 2 * H3, bring, a.threads,
-                     a.smem);
+        std::fprintf(stderr, "ho4t R=%u kc=%u tile %ux%ux%u (box %ux%ux%u) ring %u threads %u smem %u\n",
+                     R, a.kc, bt1, bt2, bt3, bt1 + 2 * R, bt2 + 2 * R, bt3 + 2 * H3, bring,
+                     a.threads, a.smem);
     }
   }
   const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
@@ -1767,14 +1796,23 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
 }
 
 namespace {
-template <class S, int R>
-void ho4t_launch(const Ho4dArgs& a, cudaStream_t s) {
+template <class S, int R, int KC>
+void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ho4t<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_ho4t<S, R, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr = true;
   }
-  k_ho4t<S, R><<<a.blocks, a.threads, a.smem, s>>>(a);
+  k_ho4t<S, R, KC><<<a.blocks, a.threads, a.smem, s>>>(a);
+}
+
+template <class S, int R>
+void ho4t_launch(const Ho4dArgs& a, cudaStream_t s) {
+  if (a.kc == 1)
+    ho4t_launch_k<S, R, 1>(a, s);
+  else
+    ho4t_launch_k<S, R, 2>(a, s);
 }
 
 template <class S>

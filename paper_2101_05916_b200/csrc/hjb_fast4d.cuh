@@ -73,6 +73,7 @@ struct Ho4dArgs {
   CUtensorMap mapv[4];
   uint32_t vbox_bytes, vslot_bytes, ring, smem, tma;
   uint32_t T3, H3, segs;  // axis-3 segment per tile (even), its box halo (even >= R), segments per row
+  uint32_t kc;            // cells per thread along axis 3 (1 or 2)
 };
 void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
 // fill mapv[] for the current buffers (k_ho4t); returns cudaErrorNotSupported
