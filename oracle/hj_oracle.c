@@ -1108,20 +1108,21 @@ static inline void eno_pair(const double* v, int64_t lin, int64_t stride, int64_
 /* one RK stage over the whole grid; kind: 0 V1 = max(c, s), 1 RK2 final,
  * 2 RK3 second, 3 RK3 final.  Returns max|out - vn| (meaningful for the
  * final stage). */
-static double ho_stage(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
-                       const double* inv, int godunov, const double* global_alpha, int order,
-                       const double* vs, const double* vn, const double* c, double dt, int kind,
-                       double* out) {
+/* nodes [begin, end) of one stage */
+static double ho_stage_range(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
+                             const double* inv, int godunov, const double* global_alpha,
+                             int order, const double* vs, const double* vn, const double* c,
+                             double dt, int kind, double* out, int64_t begin, int64_t end) {
   const int nd = g->nd;
-  const int64_t nchunks = (g->size + CHUNK - 1) / CHUNK;
+  const int64_t nchunks = (end - begin + CHUNK - 1) / CHUNK;
   double best = 0.0;
 #pragma omp parallel num_threads(nthreads())
   {
     double lbest = 0.0;
 #pragma omp for schedule(static)
     for (int64_t ch = 0; ch < nchunks; ++ch) {
-      const int64_t lo = ch * CHUNK;
-      const int64_t hi = lo + CHUNK < g->size ? lo + CHUNK : g->size;
+      const int64_t lo = begin + ch * CHUNK;
+      const int64_t hi = lo + CHUNK < end ? lo + CHUNK : end;
       int64_t idx[HJB_MAX_DIMS];
       double x[HJB_MAX_STATE], dminus[HJB_MAX_STATE], dplus[HJB_MAX_STATE];
       double costate[HJB_MAX_STATE], alpha[HJB_MAX_STATE];
@@ -1169,6 +1170,32 @@ static double ho_stage(const grid_t* g, const hjb_model* m, const hjb_dbounds* d
     if (lbest > best) best = lbest;
   }
   return best;
+}
+
+static double ho_stage(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
+                       const double* inv, int godunov, const double* global_alpha, int order,
+                       const double* vs, const double* vn, const double* c, double dt, int kind,
+                       double* out) {
+  return ho_stage_range(g, m, db, inv, godunov, global_alpha, order, vs, vn, c, dt, kind, out, 0,
+                        g->size);
+}
+
+/* one ENO/TVD-RK stage restricted to axis-0 planes [pb, pe) of the full grid
+ * (the slab computation of one rank of the sharded solve) */
+int hjo_ho_stage_planes(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db,
+                        const double* vs, const double* vn, const double* c, double dt,
+                        int32_t order, int32_t kind, int64_t pb, int64_t pe, double* out,
+                        double* max_dv) {
+  grid_t g;
+  int rc = check_ctx(gi, m, db, &g);
+  if (rc) return rc;
+  if (pb < 0 || pe > g.n[0] || pb >= pe)
+    return fail(HJB_ERR_INVALID_ARGUMENT, "ho_stage_planes: bad plane range");
+  double inv[HJB_MAX_DIMS];
+  for (int d = 0; d < g.nd; ++d) inv[d] = 1.0 / g.spacing[d];
+  *max_dv = ho_stage_range(&g, m, db, inv, 1, NULL, order, vs, vn, c, dt, kind, out,
+                           pb * g.stride[0], pe * g.stride[0]);
+  return 0;
 }
 
 int hjo_ho_solve(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, const double* init,

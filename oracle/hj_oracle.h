@@ -91,6 +91,14 @@ int hjo_hamiltonian(const hjb_model* m, const double* x, const double* p, const 
                     double* h);
 int hjo_flow_bounds(const hjb_model* m, const double* x, const hjb_interval* db, double* alpha);
 
+/* one Godunov ENO/TVD-RK stage on axis-0 planes [pb, pe) (high-order
+ * extension, parity unpinned; kind: 0 Euler/first stage, 1 RK2 final,
+ * 2 RK3 second, 3 RK3 final) */
+int hjo_ho_stage_planes(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db,
+                        const double* vs, const double* vn, const double* c, double dt,
+                        int32_t order, int32_t kind, int64_t pb, int64_t pe, double* out,
+                        double* max_dv);
+
 /* SafetyFilter::optimal_control / filter batched (safety.cpp:86-127) */
 int hjo_filter_batch(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* db,
                      const double* value, int64_t nq, const double* x, const double* u_perf,

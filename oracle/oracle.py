@@ -93,6 +93,9 @@ class Restatement:
         L.hjo_signed_distance_box.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp]
         L.hjo_hamiltonian.argtypes = [P(abi.HjbModel), _vp, _vp, P(abi.HjbInterval), P(_d)]
         L.hjo_flow_bounds.argtypes = [P(abi.HjbModel), _vp, P(abi.HjbInterval), _vp]
+        L.hjo_ho_stage_planes.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds),
+                                          _vp, _vp, _vp, _d, C.c_int32, C.c_int32, C.c_int64,
+                                          C.c_int64, _vp, P(_d)]
         L.hjo_filter_batch.argtypes = [P(abi.HjbGrid), P(abi.HjbModel), P(abi.HjbDbounds), _vp,
                                        C.c_int64, _vp, _vp, P(abi.HjbFilterConfig),
                                        P(abi.HjbFilterOut)]
@@ -136,6 +139,16 @@ class Restatement:
         self._chk(self.lib.hjo_sweep_planes(C.byref(g), C.byref(m), C.byref(d), _arr(_vals(v)),
                                             _arr(_vals(c)), dt, abi.GODUNOV, None, pb, pe,
                                             _arr(out), C.byref(mx)))
+        return mx.value
+
+    def ho_stage_planes(self, grid, model, db, vs, vn, c, dt, order, kind, pb, pe, out):
+        """One Godunov ENO/TVD-RK stage on planes [pb, pe) of `out` (numpy,
+        full grid size); returns max|out - vn| over those planes."""
+        mx = C.c_double()
+        g, m, d = grid.to_c(), model.to_c(), db.to_c()
+        self._chk(self.lib.hjo_ho_stage_planes(C.byref(g), C.byref(m), C.byref(d), _arr(vs),
+                                               _arr(vn), _arr(_vals(c)), dt, order, kind, pb, pe,
+                                               _arr(out), C.byref(mx)))
         return mx.value
 
     def vi_step(self, v, c, model, db, dt, cfg=None):
