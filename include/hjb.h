@@ -371,6 +371,19 @@ int hjb_copy_h2d(hjb_context* ctx, void* dst_dev, const void* src_host, uint64_t
 int hjb_copy_d2h(hjb_context* ctx, void* dst_host, const void* src_dev, uint64_t bytes);
 int hjb_copy_d2d(hjb_context* ctx, void* dst_dev, const void* src_dev, uint64_t bytes);
 
+/* One Godunov ENO/TVD-RK stage (order 1..3; kind 0 Euler / first stage,
+ * 1 RK2 final, 2 RK3 second, 3 RK3 final) restricted to axis-0 planes
+ * [plane_begin, plane_end) of a full grid (device pointers): the per-stage
+ * slab computation of the sharded high-order solve, for single-device
+ * verification.  Planes of `out` outside the range receive a copy of
+ * `stage_in`; max_dv = max |out - value_n| over the range.  4D fast-path
+ * models. */
+int hjb_ho_stage_planes_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
+                            const hjb_dbounds* dbounds, const double* stage_in,
+                            const double* value_n, const double* constraint, double dt,
+                            int32_t order, int32_t kind, int64_t plane_begin, int64_t plane_end,
+                            double* out, double* max_dv);
+
 /* Stream of the context (cudaStream_t as void*) and synchronisation. */
 void* hjb_context_stream(hjb_context* ctx);
 int hjb_context_synchronize(hjb_context* ctx);

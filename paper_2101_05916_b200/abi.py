@@ -160,6 +160,8 @@ SIGNATURES = [
     ("hjb_copy_h2d", _i, [_vp, _vp, _vp, C.c_uint64]),
     ("hjb_copy_d2h", _i, [_vp, _vp, _vp, C.c_uint64]),
     ("hjb_copy_d2d", _i, [_vp, _vp, _vp, C.c_uint64]),
+    ("hjb_ho_stage_planes_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp, _vp,
+                                     _d, _i32, _i32, _i64, _i64, _vp, _dp]),
     ("hjb_context_stream", _vp, [_vp]),
     ("hjb_context_synchronize", _i, [_vp]),
     ("hjb_context_launch_count", _i64, [_vp]),

@@ -833,12 +833,14 @@ template <class S, int R>
 __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_constant__ Ho4dArgs a) {
   constexpr int kK = 2;
   LoopState* st = a.st;
-  if (*(volatile int*)&st->done) return;
-  const long long it = st->iter;
-  const double* vn = (it & 1) ? a.buf1 : a.buf0;
+  if (a.loop != 0 && *(volatile int*)&st->done) return;
+  const long long it = a.loop != 0 ? st->iter : 0;
+  const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
-  const double* __restrict__ vs = a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2);
-  double* dst = a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2);
+  const double* __restrict__ vs =
+      a.loop == 0 ? a.xsrc : (a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2));
+  double* dst =
+      a.loop == 0 ? a.xdst : (a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2));
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
   const uint32_t J = n3p / kK;
   uint32_t b = blockIdx.x;
@@ -856,8 +858,8 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   const uint64_t s2 = n3p, s1 = (uint64_t)n2 * n3p, s0 = (uint64_t)n1 * s1;
   const uint64_t rowo = (uint64_t)ci1 * s1 + (uint64_t)ci2 * s2 + i3;
   const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
-  const uint32_t c0 = chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, n0);
+  const uint32_t c0 = a.cbeg + chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, a.cend);
 
   // slopes and shapes of the rows (as k_fast4d)
   double pos_[4][kK], neg_[4][kK];
@@ -1066,6 +1068,7 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
   if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (a.loop != 1) return;  // sharded slab / single stage: the caller reduces
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
   if (ticket != gridDim.x - 1) return;
@@ -1108,13 +1111,15 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   constexpr int kK = KC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
-  if (*(volatile int*)&st->done) return;
-  const long long it = st->iter;
-  const double* vn = (it & 1) ? a.buf1 : a.buf0;
+  if (a.loop != 0 && *(volatile int*)&st->done) return;
+  const long long it = a.loop != 0 ? st->iter : 0;
+  const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
-  const double* __restrict__ vs = a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2);
-  const int msel = a.src_sel == 0 ? (int)(it & 1) : (a.src_sel == 1 ? 2 : 3);
-  double* dst = a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2);
+  const double* __restrict__ vs =
+      a.loop == 0 ? a.xsrc : (a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2));
+  const int msel = a.loop == 0 ? 0 : (a.src_sel == 0 ? (int)(it & 1) : (a.src_sel == 1 ? 2 : 3));
+  double* dst =
+      a.loop == 0 ? a.xdst : (a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2));
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
   const uint32_t J = a.T3 / kK;  // pencil threads per tile row
   const uint32_t B3 = a.T3 + 2 * a.H3;  // box row width (cells)
@@ -1125,8 +1130,8 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   b /= a.segs;
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
   const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2, base3 = seg * a.T3;
-  const uint32_t c0 = chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, n0);
+  const uint32_t c0 = a.cbeg + chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, a.cend);
   const uint32_t ncons = a.threads - 32;
   const uint32_t nwarps_c = ncons >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1473,6 +1478,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
   if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (a.loop != 1) return;  // sharded slab / single stage: the caller reduces
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
   if (ticket != gridDim.x - 1) return;
@@ -1788,10 +1794,15 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
     }
   }
   const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
+  if (a.cend == 0) {
+    a.cbeg = 0;
+    a.cend = g.n[0];
+  }
+  const uint32_t span = a.cend - a.cbeg;
   uint32_t nch = 1;
-  while (tiles * nch < 2u * sms && g.n[0] / (nch + 1) >= 8) ++nch;
-  a.L = (g.n[0] + nch - 1) / nch;
-  a.nchunks = (g.n[0] + a.L - 1) / a.L;
+  while (tiles * nch < 2u * sms && span / (nch + 1) >= 8) ++nch;
+  a.L = (span + nch - 1) / nch;
+  a.nchunks = (span + a.L - 1) / a.L;
   a.blocks = tiles * a.nchunks;
 }
 
@@ -1851,7 +1862,9 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a) {
   const cuuint32_t box[4] = {a.T3 + 2 * a.H3, a.T2 + 2 * R, a.T1 + 2 * R, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   double* ptrs[4] = {a.buf0, a.buf1, a.stage1, a.stage2};
+  if (a.loop == 0) ptrs[0] = const_cast<double*>(a.xsrc);  // single stage: the explicit input
   for (int k = 0; k < 4; ++k) {
+    if (!ptrs[k]) continue;
     CUresult r = encode(&a.mapv[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ptrs[k], dims, strides,
                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -63,6 +63,14 @@ struct Ho4dArgs {
   double* stage1;
   double* stage2;
   int src_sel, dst_sel, kind, final_stage, order;
+  // 1: solve loop (buffer parity from st, fused epilogue on the final stage);
+  // 2: sharded slab (parity from st, the caller all-reduces and runs the
+  //    epilogue); 0: one stage on explicit buffers (xsrc, xvn -> xdst)
+  int loop;
+  uint32_t cbeg, cend;  // planes updated (0, 0 = all)
+  const double* xsrc;
+  const double* xvn;
+  double* xdst;
   LoopState* st;
   double dt;
   cudaGraphConditionalHandle handle;

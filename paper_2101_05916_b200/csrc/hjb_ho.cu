@@ -128,6 +128,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
     h4.stage2 = ctx->v3.d();
     h4.st = ctx->st;
     h4.dt = dt;
+    h4.loop = 1;
     CUDA_TRY(ho4d_make_maps(h4));
   }
   // one loop "sweep" = one full RK step (all of its stages)

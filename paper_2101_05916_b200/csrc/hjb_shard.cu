@@ -23,6 +23,8 @@
 #include <dlfcn.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <functional>
 #include <cstring>
 #include <string>
 
@@ -105,6 +107,218 @@ struct hjb_comm {
 };
 
 using namespace hjb;
+
+namespace hjb {
+namespace {
+
+// WHILE-conditional graph whose body is `body` calls of iter(k, handle, 1)
+// (k = position in the body), or the host-polled loop under HJB_LOOP=poll.
+int run_sharded_loop(hjb_context* ctx, int body,
+                     const std::function<int(int, cudaGraphConditionalHandle, int)>& iter) {
+  int rc = HJB_OK;
+  const char* mode = std::getenv("HJB_LOOP");
+  if (mode && std::strcmp(mode, "poll") == 0) {
+    for (;;) {
+      for (int k = 0; k < body; ++k)
+        if ((rc = iter(k, 0, 0))) return rc;
+      CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      if (ctx->st_host->done) break;
+    }
+    return HJB_OK;
+  }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  CUDA_TRY(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle handle;
+  do {
+    cudaError_t e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+    if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+    e = cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr,
+                                      nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+    for (int k = 0; k < body && rc == HJB_OK; ++k) rc = iter(k, handle, 1);
+    cudaGraph_t captured = nullptr;
+    e = cudaStreamEndCapture(ctx->stream, &captured);
+    if (rc) break;
+    if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+    e = cudaGraphLaunch(exec, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
+  } while (0);
+  if (exec) cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  return rc;
+}
+
+// stage table of a TVD-RK step: (input, output, kind); buffers 0 = V_n
+// (parity), 1 = stage1, 2 = stage2
+struct HoStage {
+  int src, dst, kind;
+};
+int ho_stages(int rk, HoStage* st) {
+  if (rk <= 1) {
+    st[0] = {0, 0, 0};
+    return 1;
+  }
+  if (rk == 2) {
+    st[0] = {0, 1, 0};
+    st[1] = {1, 0, 1};
+    return 2;
+  }
+  st[0] = {0, 1, 0};
+  st[1] = {1, 2, 2};
+  st[2] = {2, 0, 3};
+  return 3;
+}
+
+// ENO/TVD-RK slab solve: halo of R = order planes per interior side,
+// exchanged before every stage, k_ho4t/k_ho4d over the owned
+// planes, all-reduce(max) + epilogue after the last stage of a step.
+int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared& p,
+                     const hjb_solve_config* cfg, double dt, uint32_t owned, bool has_lo,
+                     bool has_hi, const double* init_slab, const double* c_slab,
+                     double* value_slab_out, hjb_solve_result* res) {
+  const int r = comm->rank;
+  const uint32_t R = cfg->spatial_order < 1 ? 1u : (uint32_t)cfg->spatial_order;
+  if ((has_lo || has_hi) && owned < R)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: slab thinner than the ENO halo");
+  const uint32_t nloc = owned + (has_lo ? R : 0) + (has_hi ? R : 0);
+  DevGrid gloc = p.g;
+  gloc.n[0] = nloc;
+  Ho4dArgs h;
+  std::memset(&h, 0, sizeof h);
+  h.order = (int)(R > 3 ? 3 : R);
+  h.cbeg = has_lo ? R : 0u;
+  h.cend = h.cbeg + owned;
+  ho4d_config(gloc, sm_count(ctx->device), h);
+  const uint64_t plane = static_cast<uint64_t>(p.g.n[1]) * p.g.n[2] * h.n3p;
+  const uint64_t rows_owned = static_cast<uint64_t>(owned) * p.g.n[1] * p.g.n[2];
+  const size_t lbytes = static_cast<size_t>(nloc) * plane * sizeof(double);
+  DevBuf* bufs[4] = {&ctx->v0, &ctx->v1, &ctx->v2, &ctx->v3};
+  for (DevBuf* b : bufs) {
+    CUDA_TRY(b->ensure(lbytes));
+    CUDA_TRY(cudaMemsetAsync(b->p, 0, lbytes, ctx->stream));
+  }
+  CUDA_TRY(ctx->pcbuf.ensure(lbytes));
+  CUDA_TRY(cudaMemsetAsync(ctx->pcbuf.p, 0, lbytes, ctx->stream));
+  CUDA_TRY(launch_pad4(init_slab, ctx->v0.d() + h.cbeg * plane, rows_owned, p.g.n[3], h.n3p,
+                       ctx->stream));
+  CUDA_TRY(launch_pad4(c_slab, ctx->pcbuf.d() + h.cbeg * plane, rows_owned, p.g.n[3], h.n3p,
+                       ctx->stream));
+  ctx->launches += 2;
+  h.tab = p.hm.dm.tab;
+  for (int d = 0; d < 4; ++d) {
+    h.off_pos[d] = p.hm.dm.row[d].off_pos;
+    h.off_neg[d] = p.hm.dm.row[d].off_neg;
+    h.off_a[d] = p.hm.dm.row[d].off_a;
+    h.off_b[d] = p.hm.dm.row[d].off_b;
+  }
+  h.c = ctx->pcbuf.d();
+  h.buf0 = ctx->v0.d();
+  h.buf1 = ctx->v1.d();
+  h.stage1 = ctx->v2.d();
+  h.stage2 = ctx->v3.d();
+  h.st = ctx->st;
+  h.dt = dt;
+  h.loop = 2;
+  CUDA_TRY(ho4d_make_maps(h));
+  const long long cap =
+      std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
+  CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
+  CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
+  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
+                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
+                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
+  ++ctx->launches;
+  HoStage stages[3];
+  const int ns = ho_stages(cfg->time_order, stages);
+  unsigned long long* maxbits = &ctx->st->maxdv_bits;
+  const size_t pe = static_cast<size_t>(plane);
+  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
+    for (int q = 0; q < ns; ++q) {
+      double* src = stages[q].src == 0 ? ((k & 1) ? h.buf1 : h.buf0)
+                                       : (stages[q].src == 1 ? h.stage1 : h.stage2);
+      if (comm->nranks > 1) {
+        NCCL_TRY(api->GroupStart());
+        if (has_lo) {
+          NCCL_TRY(api->Send(src + h.cbeg * pe, R * pe, ncclFloat64_, r - 1, comm->comm,
+                             ctx->stream));
+          NCCL_TRY(api->Recv(src + (h.cbeg - R) * pe, R * pe, ncclFloat64_, r - 1, comm->comm,
+                             ctx->stream));
+        }
+        if (has_hi) {
+          NCCL_TRY(api->Send(src + (h.cend - R) * pe, R * pe, ncclFloat64_, r + 1, comm->comm,
+                             ctx->stream));
+          NCCL_TRY(api->Recv(src + h.cend * pe, R * pe, ncclFloat64_, r + 1, comm->comm,
+                             ctx->stream));
+        }
+        NCCL_TRY(api->GroupEnd());
+      }
+      Ho4dArgs x = h;
+      x.src_sel = stages[q].src;
+      x.dst_sel = stages[q].dst;
+      x.kind = stages[q].kind;
+      x.final_stage = q == ns - 1;
+      CUDA_TRY(launch_ho4d(x, p.shape, ctx->stream));
+    }
+    NCCL_TRY(api->AllReduce(maxbits, maxbits, 1, ncclUint64_, ncclMax_, comm->comm, ctx->stream));
+    CUDA_TRY(launch_epilogue(ctx->st, hd, use, ctx->stream));
+    return HJB_OK;
+  };
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, ctx->stream));
+  int rc = run_sharded_loop(ctx, 2, step);  // even body: parity of position k == iteration
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const LoopState& st = *ctx->st_host;
+  ctx->launches += (ns + 1) * (st.iter + 2);
+  res->iterations = st.iter;
+  res->converged = st.converged;
+  res->final_residual = st.last_residual;
+  res->wall_seconds = ms * 1e-3;
+  const long long nh = std::min<long long>(st.iter, res->history_capacity);
+  if (nh > 0 && res->residual_history)
+    CUDA_TRY(cudaMemcpyAsync(res->residual_history, ctx->hist.p, nh * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  if (nh > 0 && res->wall_ms_history)
+    CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  const double* fin = ((st.iter & 1) ? h.buf1 : h.buf0) + h.cbeg * pe;
+  CUDA_TRY(launch_unpad4(fin, value_slab_out, rows_owned, p.g.n[3], h.n3p, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (st.status == HJB_ERR_DIVERGED)
+    return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+  return HJB_OK;
+}
+
+}  // namespace
+}  // namespace hjb
 
 extern "C" {
 
@@ -211,6 +425,68 @@ int hjb_sweep_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* 
   return HJB_OK;
 }
 
+int hjb_ho_stage_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
+                            const hjb_dbounds* db, const double* stage_in, const double* value_n,
+                            const double* constraint, double dt, int32_t order, int32_t kind,
+                            int64_t plane_begin, int64_t plane_end, double* out,
+                            double* max_dv) {
+  int rc;
+  if (!ctx) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: null");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Prepared p;
+  if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
+  if (p.shape < 0)
+    return set_err(HJB_ERR_UNSUPPORTED, "ho_stage_planes: model/grid outside the 4D fast path");
+  if (plane_begin < 0 || plane_end > p.g.n[0] || plane_begin >= plane_end)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "ho_stage_planes: bad plane range");
+  if (order < 1 || order > 3 || kind < 0 || kind > 3)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "ho_stage_planes: bad order/kind");
+  Ho4dArgs h;
+  std::memset(&h, 0, sizeof h);
+  h.order = order;
+  h.cbeg = static_cast<uint32_t>(plane_begin);
+  h.cend = static_cast<uint32_t>(plane_end);
+  ho4d_config(p.g, sm_count(ctx->device), h);
+  const uint64_t rows = static_cast<uint64_t>(p.g.n[0]) * p.g.n[1] * p.g.n[2];
+  const size_t pb = rows * h.n3p * sizeof(double);
+  DevBuf a, vn, cb, o;
+  CUDA_TRY(a.ensure(pb));
+  CUDA_TRY(vn.ensure(pb));
+  CUDA_TRY(cb.ensure(pb));
+  CUDA_TRY(o.ensure(pb));
+  CUDA_TRY(launch_pad4(stage_in, a.d(), rows, p.g.n[3], h.n3p, ctx->stream));
+  CUDA_TRY(launch_pad4(value_n, vn.d(), rows, p.g.n[3], h.n3p, ctx->stream));
+  CUDA_TRY(launch_pad4(constraint, cb.d(), rows, p.g.n[3], h.n3p, ctx->stream));
+  CUDA_TRY(launch_pad4(stage_in, o.d(), rows, p.g.n[3], h.n3p, ctx->stream));
+  h.tab = p.hm.dm.tab;
+  for (int d = 0; d < 4; ++d) {
+    h.off_pos[d] = p.hm.dm.row[d].off_pos;
+    h.off_neg[d] = p.hm.dm.row[d].off_neg;
+    h.off_a[d] = p.hm.dm.row[d].off_a;
+    h.off_b[d] = p.hm.dm.row[d].off_b;
+  }
+  h.c = cb.d();
+  h.xsrc = a.d();
+  h.xvn = vn.d();
+  h.xdst = o.d();
+  h.kind = kind;
+  h.final_stage = 1;
+  h.loop = 0;
+  h.st = ctx->st;
+  h.dt = dt;
+  CUDA_TRY(ho4d_make_maps(h));
+  CUDA_TRY(cudaMemsetAsync(ctx->st, 0, sizeof(LoopState), ctx->stream));
+  CUDA_TRY(launch_ho4d(h, p.shape, ctx->stream));
+  CUDA_TRY(launch_unpad4(o.d(), out, rows, p.g.n[3], h.n3p, ctx->stream));
+  ctx->launches += 6;
+  unsigned long long bits = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bits, &ctx->st->maxdv_bits, sizeof bits, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(max_dv, &bits, sizeof bits);
+  return HJB_OK;
+}
+
 int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
                           const hjb_model* mi, const hjb_dbounds* db, const double* init_slab,
                           const double* c_slab, const hjb_solve_config* cfg,
@@ -223,8 +499,9 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
   if (p.shape < 0)
     return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
-  if (cfg->spatial_order > 1 || cfg->time_order > 1)
-    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: first-order Euler only");
+  const bool high_order = cfg->spatial_order > 1 || cfg->time_order > 1;
+  if (high_order && cfg->scheme != HJB_GODUNOV)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: high-order schemes with Godunov only");
   Nccl* api = nccl();
   if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
   const int P = comm->nranks, r = comm->rank;
@@ -271,6 +548,10 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return HJB_OK;
   }
+
+  if (high_order)
+    return solve_sharded_ho(ctx, comm, api, p, cfg, dt, owned, has_lo, has_hi, init_slab, c_slab,
+                            value_slab_out, res);
 
   // local padded slab arrays: [halo_lo?][owned][halo_hi?]
   DevGrid gloc = p.g;

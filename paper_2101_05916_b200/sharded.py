@@ -37,6 +37,22 @@ def sweep_planes_dev(grid: hj.Grid, model: hj.DynamicsModel, dbounds: hj.Interva
     return mx.value
 
 
+def ho_stage_planes_dev(grid: hj.Grid, model: hj.DynamicsModel, dbounds: hj.IntervalField,
+                        stage_in_ptr: int, value_n_ptr: int, c_ptr: int, dt: float, order: int,
+                        kind: int, plane_begin: int, plane_end: int, out_ptr: int,
+                        ctx: hj.Context | None = None) -> float:
+    """One ENO/TVD-RK stage of planes [plane_begin, plane_end) on a full grid
+    (device pointers); returns the slab's max|out - V_n|."""
+    lib = abi.load()
+    mx = C.c_double()
+    g, m, d = grid.to_c(), model.to_c(), dbounds.to_c()
+    hj._check(lib.hjb_ho_stage_planes_dev(hj._ctx(ctx), C.byref(g), C.byref(m), C.byref(d),
+                                          C.c_void_p(stage_in_ptr), C.c_void_p(value_n_ptr),
+                                          C.c_void_p(c_ptr), dt, order, kind, plane_begin,
+                                          plane_end, C.c_void_p(out_ptr), C.byref(mx)))
+    return mx.value
+
+
 class Comm:
     """NCCL communicator of the library, bootstrapped over torch.distributed."""
 
