@@ -227,3 +227,39 @@ def test_fast4d_slope_shapes(gpu_ctx, oracle, wind):
     assert got.iterations == want.iterations
     assert same(got.residual_history, want.residual_history)
     assert same(got.value.values(), want.value.values())
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 2, 2), (2, 3, 2, 3), (3, 2, 5, 2), (5, 4, 3, 7)])
+@pytest.mark.parametrize("order,rk", [(1, 1), (3, 3), (2, 2)])
+def test_smallest_grids(gpu_ctx, oracle, dims, order, rk):
+    """Two-node axes: every face is an edge face (ghost rule everywhere), the
+    stencil halo exceeds the grid, one-tile / one-plane marches."""
+    n0, n1, n2, n3 = dims
+    g = hj.Grid([(-5.0, 5.0, n0), (-2.0, 2.0, n1), (-0.35, 0.35, n2), (-1.5, 1.5, n3)])
+    model = configs.planar_model()
+    db = hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0) + 0.01 * np.arange(g.size()) / g.size())
+    cfg = hj.SolveConfig(tolerance=1e-6, max_iters=25, spatial_order=order, time_order=rk)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+def test_max_iters_zero_and_time_horizon(gpu_ctx, oracle):
+    case = workload_case(configs.config2(9))
+    init = hj.ScalarField(case.grid, case.c + 0.1)
+    cfg = hj.SolveConfig(tolerance=1e-6, max_iters=0)
+    got = hj.solve(init, case.c_field(), case.model, case.db, cfg, ctx=gpu_ctx)
+    want = oracle.solve(init, case.c_field(), case.model, case.db, cfg)
+    assert got.iterations == want.iterations == 0
+    assert same(got.value.values(), init.values())
+    for order in (1, 2):
+        cfg = hj.SolveConfig(tolerance=1e-9, max_iters=1000, time_horizon=0.05,
+                             spatial_order=order, time_order=order)
+        want = oracle.solve(case.c_field(), case.c_field(), case.model, case.db, cfg)
+        got = hj.solve(case.c_field(), case.c_field(), case.model, case.db, cfg, ctx=gpu_ctx)
+        assert got.iterations == want.iterations < 1000
+        assert got.iterations * got.dt >= 0.05 > (got.iterations - 1) * got.dt
+        assert same(got.value.values(), want.value.values())
