@@ -786,7 +786,7 @@ __device__ __forceinline__ void eno_sel(const double* A, const double* d2, const
 
 template <int R>
 __device__ __forceinline__ void eno_faces(const double* A, double& dm, double& dp) {
-  if (R == 3) {  // named scalars: the register-tight ENO3 kernel allocates them best
+  if constexpr (R == 3) {  // named scalars: the register-tight ENO3 kernel allocates them best
     const double d2m2 = A[1] - A[0], d2m1 = A[2] - A[1], d20 = A[3] - A[2], d21 = A[4] - A[3],
                  d22 = A[5] - A[4];
     const double t1 = d2m1 - d2m2, t2 = d20 - d2m1, t3 = d21 - d20, t4 = d22 - d21;
@@ -804,14 +804,14 @@ __device__ __forceinline__ void eno_faces(const double* A, double& dm, double& d
       const double w = left ? kHoSixthNeg : kHoThird;
       dp = (A[3] + -0.5 * c2) + w * c3;
     }
-    return;
+  } else {
+    double d2[2 * R > 1 ? 2 * R - 1 : 1], t3[2 * R > 2 ? 2 * R - 2 : 1];
+#pragma unroll
+    for (int q = 0; q < 2 * R - 1; ++q) d2[q] = A[q + 1] - A[q];
+#pragma unroll
+    for (int q = 0; q < 2 * R - 2; ++q) t3[q] = d2[q + 1] - d2[q];
+    eno_sel<R>(A, d2, t3, dm, dp);
   }
-  double d2[2 * R > 1 ? 2 * R - 1 : 1], t3[2 * R > 2 ? 2 * R - 2 : 1];
-#pragma unroll
-  for (int q = 0; q < 2 * R - 1; ++q) d2[q] = A[q + 1] - A[q];
-#pragma unroll
-  for (int q = 0; q < 2 * R - 2; ++q) t3[q] = d2[q + 1] - d2[q];
-  eno_sel<R>(A, d2, t3, dm, dp);
 }
 
 // both cells of a 2-cell pencil from the 2R+1 faces of the pencil

@@ -9,6 +9,7 @@
 // body holds the stages of several steps; the last stage of a step runs the
 // solve() epilogue (residual = max|V_{n+1} - V_n| / dt).
 #include <cstring>
+#include <string>
 
 #include <cstdlib>
 
@@ -163,7 +164,21 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   CUDA_TRY(cudaEventCreate(&e1));
   CUDA_TRY(cudaEventRecord(e0, ctx->stream));
   const int body = 4;
-  int rc = run_loop(ctx, launch, body);
+  // small 2D grids: every stage of the whole loop in one cluster launch
+  const char* s2d = std::getenv("HJB_SMALL2D");
+  const bool small2d = shape < 0 && g.nd == 2 && !(s2d && std::strcmp(s2d, "0") == 0) &&
+                       small2d_ho_smem(g, nullptr, nullptr) <= 200 * 1024;
+  int rc = HJB_OK;
+  if (small2d) {
+    StepArgs x = a;
+    x.src = ctx->v0.d();
+    x.dst = out;
+    const cudaError_t e = launch_small2d_ho(x, cfg->time_order < 1 ? 1 : cfg->time_order,
+                                            ctx->stream);
+    if (e != cudaSuccess) rc = set_err(HJB_ERR_CUDA, std::string("small2d_ho: ") + cudaGetErrorString(e));
+  } else {
+    rc = run_loop(ctx, launch, body);
+  }
   if (rc) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -178,7 +193,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   const LoopState& ls = *ctx->st_host;
-  ctx->launches += (ls.iter + body) * ns;
+  ctx->launches += small2d ? 1 : (ls.iter + body) * ns;
   res->iterations = ls.iter;
   res->converged = ls.converged;
   res->final_residual = ls.last_residual;
@@ -191,7 +206,9 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
     CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
   const double* fin = (ls.iter & 1) ? ctx->v1.d() : ctx->v0.d();
-  if (shape >= 0) {
+  if (small2d) {
+    // the cluster kernel wrote V* to `out` itself
+  } else if (shape >= 0) {
     CUDA_TRY(launch_unpad4(fin, out, rows4, g.n[3], n3p, ctx->stream));
     ++ctx->launches;
   } else {

@@ -782,6 +782,181 @@ __global__ void __launch_bounds__(512, 1) k_small2d(const __grid_constant__ Smal
   cluster_sync_all();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
+// High-order (ENO1..3 + TVD-RK1..3) variant of k_small2d: every RK stage of
+// every step in the same single cluster launch (BASELINE config 1 scheme:
+// ENO2 + TVD-RK2 on 101^2).  Per CTA band of rows in shared memory: V_n
+// (double-buffered by parity), stage1, stage2, c.  A stage reads its input
+// rows of any band through DSMEM (mapa), writes its output band, and ends
+// with a cluster barrier; the last stage of a step also reduces max|dV| and
+// applies the solve() loop logic, as k_small2d.  The stencil arithmetic is
+// eno_pair / godunov_flux / lf_hamiltonian, as k_ho_stage.
+template <int SCHEME, bool PERNODE>
+__global__ void __launch_bounds__(512, 1) k_small2d_ho(const __grid_constant__ Small2dArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const StepArgs& p = a.s;
+  const DevGrid& g = p.g;
+  const uint32_t n0 = g.n[0], n1 = g.n[1];
+  const uint32_t RB = a.rows;  // rows per band
+  const uint32_t me = cluster_ctarank(), nct = cluster_nctas();
+  const uint32_t r0 = me * RB;
+  const uint32_t r1 = min(r0 + RB, n0);
+  const uint32_t own = r1 > r0 ? (r1 - r0) * n1 : 0;
+  const uint32_t band = RB * n1;
+  double* bufs[4] = {sm, sm + band, sm + 2 * band, sm + 3 * band};  // V even, V odd, s1, s2
+  double* cl = sm + 4 * band;
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(sm + 5 * band);  // [2][16]
+  __shared__ unsigned long long part[32];
+  __shared__ int s_done;
+  for (uint32_t t = threadIdx.x; t < own; t += blockDim.x) {
+    bufs[0][t] = p.src[r0 * n1 + t];
+    cl[t] = p.c[r0 * n1 + t];
+  }
+  const double inv0 = g.inv_spacing[0], inv1 = g.inv_spacing[1];
+  const int order = p.order;
+  const int rk = p.kind;  // TVD-RK order (1..3), carried in StepArgs.kind for this kernel
+  // stage table (src, dst, kind): buffers 0 = V_n, 1 = stage1, 2 = stage2, 3 = V_{n+1}
+  int ns = 1, ssrc[3] = {0, 0, 0}, sdst[3] = {3, 3, 3}, skind[3] = {0, 0, 0};
+  if (rk == 2) {
+    ns = 2;
+    sdst[0] = 1; ssrc[1] = 1; sdst[1] = 3; skind[1] = 1;
+  } else if (rk >= 3) {
+    ns = 3;
+    sdst[0] = 1; ssrc[1] = 1; sdst[1] = 2; skind[1] = 2; ssrc[2] = 2; sdst[2] = 3; skind[2] = 3;
+  }
+  long long iter = 0;
+  double min_res = __longlong_as_double(0x7ff0000000000000ll), first = 0.0, residual = 0.0;
+  int converged = 0, status = 0;
+  cluster_sync_all();
+  unsigned long long* slots0 = const_cast<unsigned long long*>(
+      reinterpret_cast<const unsigned long long*>(map_rank(reinterpret_cast<const double*>(slots), 0)));
+  const unsigned long long t0 = globaltimer_ns();
+  for (;;) {
+    const int cb = static_cast<int>(iter & 1);
+    double local = 0.0;
+    for (int q = 0; q < ns; ++q) {
+      const int sb = ssrc[q] == 0 ? cb : ssrc[q] + 1;  // smem buffer index of the input
+      const int db = sdst[q] == 3 ? (cb ^ 1) : sdst[q] + 1;
+      const double* in = bufs[sb];
+      const double* vnb = bufs[cb];
+      double* outb = bufs[db];
+      const bool last = q == ns - 1;
+      for (uint32_t t = threadIdx.x; t < own; t += blockDim.x) {
+        const uint32_t lr = t / n1, k1 = t - lr * n1;
+        const uint32_t k0 = r0 + lr;
+        uint32_t idx[2] = {k0, k1};
+        const uint32_t lin = k0 * n1 + k1;
+        // axis-0 column k0-3 .. k0+3 of the stage input (any band, DSMEM)
+        double col[7];
+#pragma unroll
+        for (int o = -3; o <= 3; ++o) {
+          const int j = (int)k0 + o;
+          double x = 0.0;
+          if (j >= 0 && j < (int)n0 && (o >= -order && o <= order)) {
+            const uint32_t owner = (uint32_t)j / RB;
+            const uint32_t off = ((uint32_t)j - owner * RB) * n1 + k1;
+            x = owner == me ? in[off] : map_rank(in, owner)[off];
+          }
+          col[o + 3] = x;
+        }
+        double dm[2], dp[2];
+        eno_pair<SCHEME == kGodunov>(col, 3, 1, (int)k0, (int)n0, inv0, order, dm[0], dp[0]);
+        eno_pair<SCHEME == kGodunov>(in + lr * n1, k1, 1, (int)k1, (int)n1, inv1, order, dm[1],
+                                     dp[1]);
+        double hhat = 0.0;
+        if (SCHEME == kGodunov) {
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            double pos, neg;
+            row_slopes<2, PERNODE>(p.m, p.m.row[d], idx, lin, pos, neg);
+            hhat += godunov_flux(pos, neg, dm[d], dp[d]);
+          }
+        } else {
+          double pq[2] = {0.5 * (dm[0] + dp[0]), 0.5 * (dm[1] + dp[1])};
+          hhat = lf_hamiltonian<2, PERNODE>(p.m, pq, idx, lin);
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const double al = SCHEME == kLfPerNode
+                                  ? row_alpha<2, PERNODE>(p.m, p.m.row[d], idx, lin)
+                                  : p.galpha[d];
+            hhat += al * 0.5 * (dp[d] - dm[d]);
+          }
+        }
+        const double st = in[t] + p.dt * hhat;
+        const double vn = vnb[t];
+        double val;
+        switch (skind[q]) {
+          case 1: val = 0.5 * vn + 0.5 * st; break;
+          case 2: val = 0.75 * vn + 0.25 * st; break;
+          case 3: val = kThird * vn + kTwoThirds * st; break;
+          default: val = st; break;
+        }
+        const double cc = cl[t];
+        const double vnew = val > cc ? val : cc;
+        outb[t] = vnew;
+        if (last) {
+          const double dv = fabs(vnew - vn);
+          if (dv > local) local = dv;
+        }
+      }
+      if (!last) cluster_sync_all();  // the next stage reads this output across bands
+    }
+    unsigned long long bm = warp_max_u64(__double_as_longlong(local));
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = bm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) m = part[w] > m ? part[w] : m;
+      slots0[cb * 16 + me] = m;
+    }
+    cluster_sync_all();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (uint32_t r = 0; r < nct; ++r) {
+        const unsigned long long x = slots0[cb * 16 + r];
+        m = x > m ? x : m;
+      }
+      residual = __longlong_as_double(m) / p.dt;
+      ++iter;
+      LoopState* st = p.st;
+      if (me == 0 && iter - 1 < st->history_cap) {
+        if (st->history) st->history[iter - 1] = residual;
+        if (st->wall_history)
+          st->wall_history[iter - 1] = (double)(globaltimer_ns() - t0) * 1e-6;
+      }
+      bool stop = false;
+      if (residual < p.st->tol) {
+        converged = 1;
+        stop = true;
+      } else {
+        if (iter == 1) first = residual;
+        min_res = residual < min_res ? residual : min_res;
+        const double base = min_res < first ? first : min_res;
+        if (!isfinite(residual) || residual > 10.0 * base) {
+          status = HJB_ERR_DIVERGED;
+          stop = true;
+        }
+      }
+      if (iter >= p.st->max_iters) stop = true;
+      if (p.st->horizon > 0.0 && (double)iter * p.dt >= p.st->horizon) stop = true;
+      s_done = stop ? 1 : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) ++iter;
+    if (s_done) break;
+  }
+  const double* fin = bufs[iter & 1];
+  for (uint32_t t = threadIdx.x; t < own; t += blockDim.x) p.dst[r0 * n1 + t] = fin[t];
+  if (me == 0 && threadIdx.x == 0) {
+    LoopState* st = p.st;
+    st->iter = iter;
+    st->converged = converged;
+    st->status = status;
+    st->last_residual = residual;
+    st->done = 1;
+  }
+  cluster_sync_all();
+}
+
 inline dim3 blocks_for(uint32_t n) { return dim3((n + kThreads - 1) / kThreads); }
 
 // Persistent-style grid: a few CTAs per SM stride over the nodes, so the
@@ -938,6 +1113,48 @@ size_t small2d_smem(const DevGrid& g, uint32_t* rows_out, uint32_t* ctas_out) {
   if (rows_out) *rows_out = R;
   if (ctas_out) *ctas_out = nct;
   return (3ull * R * g.n[1]) * sizeof(double) + 32 * sizeof(unsigned long long);
+}
+
+size_t small2d_ho_smem(const DevGrid& g, uint32_t* rows_out, uint32_t* ctas_out) {
+  if (g.nd != 2) return 0;
+  const uint32_t R = (g.n[0] + 15) / 16;
+  const uint32_t nct = (g.n[0] + R - 1) / R;
+  if (rows_out) *rows_out = R;
+  if (ctas_out) *ctas_out = nct;
+  return (5ull * R * g.n[1]) * sizeof(double) + 32 * sizeof(unsigned long long);
+}
+
+cudaError_t launch_small2d_ho(const StepArgs& s, int rk, cudaStream_t stream) {
+  uint32_t R = 0, nct = 0;
+  const size_t smem = small2d_ho_smem(s.g, &R, &nct);
+  Small2dArgs a;
+  a.s = s;
+  a.s.kind = rk;
+  a.rows = R;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nct);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = nct;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto go = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+  };
+  const bool pn = s.m.per_node != 0;
+  switch (s.scheme) {
+    case kGodunov: return pn ? go(k_small2d_ho<kGodunov, true>) : go(k_small2d_ho<kGodunov, false>);
+    case kLfPerNode:
+      return pn ? go(k_small2d_ho<kLfPerNode, true>) : go(k_small2d_ho<kLfPerNode, false>);
+    default: return pn ? go(k_small2d_ho<kLfGlobal, true>) : go(k_small2d_ho<kLfGlobal, false>);
+  }
 }
 
 cudaError_t launch_small2d(const StepArgs& s, cudaStream_t stream) {

@@ -41,6 +41,10 @@ struct StepArgs {
 // the per-CTA shared memory (0 when the grid is not 2D).
 size_t small2d_smem(const DevGrid& g, uint32_t* rows, uint32_t* ctas);
 cudaError_t launch_small2d(const StepArgs& s, cudaStream_t stream);
+// ENO/TVD-RK variant (s.order = ENO order, rk = TVD-RK order): all stages of
+// the whole loop in one cluster launch; 0 smem when the grid is not 2D
+size_t small2d_ho_smem(const DevGrid& g, uint32_t* rows, uint32_t* ctas);
+cudaError_t launch_small2d_ho(const StepArgs& s, int rk, cudaStream_t stream);
 
 // K6: one ENO/TVD-RK stage (generic rank; see hjb_kernels.cu).
 cudaError_t launch_ho_stage(const StepArgs& a, cudaStream_t s);
