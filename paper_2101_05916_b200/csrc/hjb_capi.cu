@@ -402,6 +402,27 @@ void fill_tables(const Prepared& p, Fast4dArgs& f) {
   }
 }
 
+// Lax-Friedrichs fields of the 4D fast path: per-row drift tables, input
+// coefficients and bounds (constant disturbance bounds only), alpha
+void fill_lf(const DevModel& m, int scheme, const double* galpha, Fast4dArgs& f) {
+  f.lf = scheme == kGodunov ? 0 : (scheme == kLfGlobal ? 2 : 1);
+  for (int d = 0; d < 4; ++d) {
+    const DevRow& r = m.row[d];
+    f.galpha[d] = galpha[d];
+    f.dr_off[d] = r.constant_drift ? -1 : r.off_a;
+    f.dr_const[d] = r.constant_drift ? r.drift_const : 0.0;
+    f.ucoef[d] = r.n_uadd > 0 ? r.ucoef[0] : 0.0;
+    f.dcoef[d] = r.n_dterm > 0 ? r.dcoef[0] : 0.0;
+    f.off_alpha[d] = r.off_alpha;
+  }
+  for (int j = 0; j < 3; ++j) {
+    f.ulo[j] = j < m.m ? m.ulo[j] : 0.0;
+    f.uhi[j] = j < m.m ? m.uhi[j] : 0.0;
+    f.dlo[j] = j < m.p ? m.dlo[j] : 0.0;
+    f.dhi[j] = j < m.p ? m.dhi[j] : 0.0;
+  }
+}
+
 }  // namespace hjb
 
 // Device-resident solve: every pointer is device memory.  Shared by the
@@ -446,6 +467,10 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
   };
   const char* kc = std::getenv("HJB_KCELLS");
   const char* mt = std::getenv("HJB_MAXT");
+  if (f.lf) {  // one Lax-Friedrichs variant (112 registers: no spills)
+    configure(2, 448);
+    return HJB_OK;
+  }
   if (kc || mt) {
     const uint32_t k = (kc && std::atoi(kc) == 4) ? 4u : 2u;
     configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 576u));
@@ -618,6 +643,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     }
     f.st = ctx->st;
     f.dt = dt;
+    fill_lf(hm.dm, scheme_of(cfg), s.max_alpha, f);
     if ((rc = fast4d_choose(ctx, g, shape, init, c, f))) return rc;
     rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
     CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));

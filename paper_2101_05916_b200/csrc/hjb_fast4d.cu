@@ -50,20 +50,28 @@ __device__ __forceinline__ bool sign_clear(double x) { return __double2hiint(x) 
 // Row structure of the model, fixed at compile time: axis of the slope
 // table (A), optional second drift axis (B, pos == neg then), and whether
 // the row is always linear (pos == neg everywhere: no inputs on the row).
+// U(d) / D(d): the control / disturbance channel entering row d (at most one
+// each in these models; -1 none) — the Lax-Friedrichs variant's inputs.
 struct ShapePlanarD0 {  // BASELINE planar 4D, wind on row 0: rows x1 | tan x2 | x2 + x3 | x2
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : 2; }
   __host__ __device__ static constexpr int B(int d) { return d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr bool LIN(int d) { return d == 1 || d == 2; }
+  __host__ __device__ static constexpr int U(int d) { return d == 3 ? 0 : -1; }
+  __host__ __device__ static constexpr int D(int d) { return d == 0 ? 0 : -1; }
 };
 struct ShapePlanarD1 {  // stock NearHoverPlanar4D, wind on row 1
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : 2; }
   __host__ __device__ static constexpr int B(int d) { return d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr bool LIN(int d) { return d == 0 || d == 2; }
+  __host__ __device__ static constexpr int U(int d) { return d == 3 ? 0 : -1; }
+  __host__ __device__ static constexpr int D(int d) { return d == 1 ? 0 : -1; }
 };
 struct ShapeTwin {  // TwinDoubleIntegrator rows: x1 | const | x3 | const
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr int B(int) { return -1; }
   __host__ __device__ static constexpr bool LIN(int d) { return d == 0 || d == 2; }
+  __host__ __device__ static constexpr int U(int d) { return d == 1 ? 0 : d == 3 ? 1 : -1; }
+  __host__ __device__ static constexpr int D(int d) { return d == 1 ? 0 : d == 3 ? 1 : -1; }
 };
 
 template <class S>
@@ -326,7 +334,7 @@ constexpr uint32_t kEndItem = 0xffffffffu;
 // products of faces shared by two cells are formed once: along the march
 // (carried to the next plane) and inside the pencil when the row's slopes do
 // not vary along the contiguous axis.
-template <class S, int kK, int MAXT>
+template <class S, int kK, int MAXT, int SCH>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -542,6 +550,35 @@ __global__ void __launch_bounds__(MAXT, 1)
         o2u[c] = (up[2][c] ? o2p : o2m) + 8u * c;
       }
 
+      // Lax-Friedrichs (SCH 1 per-node alpha, 2 global alpha): row drifts and
+      // dissipation coefficients, loop invariant (rows without inputs have
+      // drift == pos and alpha == |drift|)
+      double lfdr[4][kK], lfal[4][kK];
+      if (SCH != 0) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+            if (S::B(d) >= 0) {  // two-term drift, no inputs: pos == drift
+              lfdr[d][c] = pos_[d][c];
+            } else {
+              lfdr[d][c] = a.dr_off[d] >= 0 ? tabs[a.dr_off[d] + ka] : a.dr_const[d];
+            }
+            if (SCH == 2) {
+              lfal[d][c] = a.galpha[d];
+            } else if (a.off_alpha[d] >= 0) {
+              lfal[d][c] = tabs[a.off_alpha[d] + ka];
+            } else {
+              lfal[d][c] = fabs(lfdr[d][c]);
+            }
+          }
+        }
+      }
+      // LF edge rule (solver.cpp:144,147): the one-sided difference is
+      // replicated at an axis end
+      const bool e1lo = i1 == 0, e1hi = i1 + 1 == n1, e2lo = i2 == 0, e2hi = i2 + 1 == n2;
+
       double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
                    static_cast<uint64_t>(c0) * s0;
       // prologue: V plane c0-1 (first slot of the item when c0 > 0) and c0
@@ -565,7 +602,7 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
         dm0[c] = (v[c] - vp[c]) * inv0;
-        ka0[c] = S::LIN(0) ? 0.0 : pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
+        ka0[c] = (SCH != 0 || S::LIN(0)) ? 0.0 : pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
       }
 
       for (uint32_t i0 = c0; i0 < c1; ++i0) {
@@ -584,7 +621,7 @@ __global__ void __launch_bounds__(MAXT, 1)
         }
         double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
         lds_cells<kK>(csl + cown, cc);
-        if (S::LIN(1)) {  // upwind neighbour only (n1p holds it)
+        if (SCH == 0 && S::LIN(1)) {  // upwind neighbour only (n1p holds it)
           if (pc1) {
 #pragma unroll
             for (int c = 0; c < kK; ++c) n1p[c] = lds1(slot_cur + o1u[c]);
@@ -595,7 +632,7 @@ __global__ void __launch_bounds__(MAXT, 1)
           lds_cells<kK>(slot_cur + o1m, n1m);
           lds_cells<kK>(slot_cur + o1p, n1p);
         }
-        if (S::LIN(2)) {
+        if (SCH == 0 && S::LIN(2)) {
           if (pc2) {
 #pragma unroll
             for (int c = 0; c < kK; ++c) n2p[c] = lds1(slot_cur + o2u[c]);
@@ -621,7 +658,7 @@ __global__ void __launch_bounds__(MAXT, 1)
         // row 3: each face's L product (cell above uses it as A) and R
         // product (cell below uses it as B)
         double k3a[kK + 1], k3b[kK + 1];
-        if (row3_shared && !S::LIN(3)) {
+        if (SCH == 0 && row3_shared && !S::LIN(3)) {
 #pragma unroll
           for (int c = 0; c <= kK; ++c) {
             const uint32_t sb = sign_bit(f3[c]);
@@ -632,6 +669,71 @@ __global__ void __launch_bounds__(MAXT, 1)
         double out[kK];
 #pragma unroll
         for (int c = 0; c < kK; ++c) {
+          if (SCH != 0) {
+            // Lax-Friedrichs: costate p = (D- + D+)/2, bang-bang u*, worst d*,
+            // H = sum_i p_i f_i (extremal_inputs + hamiltonian,
+            // dynamics.cpp:37-83), + alpha_d (D+ - D-)/2 (solver.cpp:161-176)
+            const double dp0r = (vn[c] - v[c]) * inv0;
+            double dmv[4], dpv[4];
+            dmv[0] = i0 == 0 ? dp0r : dm0[c];
+            dpv[0] = i0 + 1 == n0 ? dm0[c] : dp0r;
+            dm0[c] = dp0r;
+            dmv[1] = (v[c] - n1m[c]) * inv1;
+            dpv[1] = (n1p[c] - v[c]) * inv1;
+            if (e1lo) dmv[1] = dpv[1];
+            if (e1hi) dpv[1] = dmv[1];
+            dmv[2] = (v[c] - n2m[c]) * inv2;
+            dpv[2] = (n2p[c] - v[c]) * inv2;
+            if (e2lo) dmv[2] = dpv[2];
+            if (e2hi) dpv[2] = dmv[2];
+            dmv[3] = f3[c];
+            dpv[3] = f3[c + 1];
+            if (i3 + c == 0) dmv[3] = dpv[3];
+            if (i3 + c + 1 == n3) dpv[3] = dmv[3];
+            double pq[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) pq[d] = 0.5 * (dmv[d] + dpv[d]);
+            double u[3] = {0.0, 0.0, 0.0}, dd[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              double coeff = 0.0;
+              bool any = false;
+#pragma unroll
+              for (int d = 0; d < 4; ++d)
+                if (S::U(d) == j) {
+                  coeff += pq[d] * a.ucoef[d];
+                  any = true;
+                }
+              if (any) u[j] = coeff > 0.0 ? a.ulo[j] : (coeff < 0.0 ? a.uhi[j] : a.ulo[j]);
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              double coeff = 0.0;
+              bool any = false;
+#pragma unroll
+              for (int d = 0; d < 4; ++d)
+                if (S::D(d) == k) {
+                  coeff += pq[d] * a.dcoef[d];
+                  any = true;
+                }
+              if (any) dd[k] = coeff > 0.0 ? a.dhi[k] : (coeff < 0.0 ? a.dlo[k] : a.dlo[k]);
+            }
+            double hh = 0.0;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+              double fi = lfdr[d][c];
+              if (S::U(d) >= 0) fi += a.ucoef[d] * u[S::U(d) >= 0 ? S::U(d) : 0];
+              if (S::D(d) >= 0) fi += a.dcoef[d] * dd[S::D(d) >= 0 ? S::D(d) : 0];
+              hh += pq[d] * fi;
+            }
+#pragma unroll
+            for (int d = 0; d < 4; ++d) hh += lfal[d][c] * 0.5 * (dpv[d] - dmv[d]);
+            const double st = v[c] + a.dt * hh;
+            out[c] = st > cc[c] ? st : cc[c];
+            const double dv = fabs(out[c] - v[c]);
+            if (valid[c] && dv > mdv) mdv = dv;
+            continue;
+          }
           // axis 0 (D- carried from the previous plane)
           const double dp0 = (vn[c] - v[c]) * inv0;
           double h0;
@@ -1518,8 +1620,29 @@ __global__ void k_unpad4(const double* __restrict__ in, double* __restrict__ out
 
 }  // namespace
 
+// control / disturbance channel of each row per shape (ShapeX::U / D)
+static const int kShapeU[3][4] = {{-1, -1, -1, 0}, {-1, -1, -1, 0}, {-1, 0, -1, 1}};
+static const int kShapeD[3][4] = {{0, -1, -1, -1}, {-1, 0, -1, -1}, {-1, 0, -1, 1}};
+
+static int fast4d_shape_g(const DevGrid& g, const DevModel& m);
+
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
-  if (g.nd != 4 || scheme != 0 || m.per_node) return -1;
+  const int sh = fast4d_shape_g(g, m);
+  if (sh < 0 || scheme == 0) return sh;
+  // Lax-Friedrichs: each row's inputs must be the shape's (one term each)
+  if (m.m > 3 || m.p > 3) return -1;
+  for (int d = 0; d < 4; ++d) {
+    const DevRow& r = m.row[d];
+    const int u = kShapeU[sh][d], dd = kShapeD[sh][d];
+    if (r.n_uadd != (u >= 0 ? 1 : 0) || (u >= 0 && r.uch[0] != u)) return -1;
+    if (r.n_dterm != (dd >= 0 ? 1 : 0) || (dd >= 0 && r.dch[0] != dd)) return -1;
+    if (u < 0 && dd < 0 && !(r.folded || r.axis_b >= 0)) return -1;
+  }
+  return sh;
+}
+
+static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
+  if (g.nd != 4 || m.per_node) return -1;
   if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   bool lin[4];
@@ -1639,16 +1762,16 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.blocks = std::min<uint32_t>(a.items, static_cast<uint32_t>(sms));
 }
 
-template <class S, int K, int MAXT>
+template <class S, int K, int MAXT, int SCH = 0>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_fast4d<S, K, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_set = true;
   }
   if (a.l2_bytes == 0 && !a.pdl) {
-    k_fast4d<S, K, MAXT><<<a.blocks, a.threads, a.smem, s>>>(a);
+    k_fast4d<S, K, MAXT, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1674,13 +1797,21 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT>, a);
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
 // the autotuner pick among them per grid
 template <class S>
 static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.lf == 1) {  // Lax-Friedrichs variants: one configuration
+    launch_one<S, 2, 448, 1>(a, s);
+    return;
+  }
+  if (a.lf == 2) {
+    launch_one<S, 2, 448, 2>(a, s);
+    return;
+  }
   if (a.kcells == 4)
     launch_one<S, 4, 384>(a, s);
   else if (a.maxthreads == 448)

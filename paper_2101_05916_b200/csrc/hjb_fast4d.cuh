@@ -45,6 +45,16 @@ struct Fast4dArgs {
   // programmatic dependent launch (device loop): the kernel waits on
   // griddepcontrol before touching the loop state or V
   int pdl;
+  // numerical Hamiltonian: 0 Godunov, 1 Lax-Friedrichs with per-node alpha,
+  // 2 Lax-Friedrichs with global alpha (galpha)
+  int lf;
+  double galpha[4];
+  int dr_off[4];        // drift table offset of each row (-1: constant drift)
+  double dr_const[4];
+  double ucoef[4];      // B coefficient of the row's control (shape U(d))
+  double dcoef[4];      // C coefficient of the row's disturbance (shape D(d))
+  double ulo[3], uhi[3], dlo[3], dhi[3];
+  int off_alpha[4];     // LF per-node alpha tables (-1: |drift|)
 };
 
 // One ENO/TVD-RK stage over a padded 4D grid (k_ho4d, hjb_fast4d.cu): the
@@ -90,7 +100,8 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a);
 cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s);
 
 // Model shape id for the fast path, or -1 when the generic kernel must run
-// (rank != 4, LF scheme, per-node bounds, rows depending on x0, ...).
+// (rank != 4, per-node bounds, rows depending on x0, inputs not matching the
+// shape, ...).  scheme: 0 Godunov, 1 LF per-node alpha, 2 LF global alpha.
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);

@@ -71,7 +71,9 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
   // 4D fast-path models (Godunov, constant bounds): padded layout + k_ho4d
   const char* fe = std::getenv("HJB_FAST");
-  const int shape = (fe && std::strcmp(fe, "0") == 0) ? -1 : fast4d_shape(g, m, scheme_id(cfg));
+  const int shape = (fe && std::strcmp(fe, "0") == 0) || scheme_id(cfg) != kGodunov
+                        ? -1
+                        : fast4d_shape(g, m, kGodunov);
   const uint64_t rows4 = g.nd == 4 ? static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2] : 0;
   const uint32_t n3p = g.nd == 4 ? (g.n[3] + 1) / 2 * 2 : 0;
   const size_t pbytes = shape >= 0 ? rows4 * n3p * sizeof(double) : bytes;

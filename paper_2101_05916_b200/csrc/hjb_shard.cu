@@ -502,6 +502,11 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   const bool high_order = cfg->spatial_order > 1 || cfg->time_order > 1;
   if (high_order && cfg->scheme != HJB_GODUNOV)
     return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: high-order schemes with Godunov only");
+  // first order: the scheme's own variant of the fast path
+  const int scheme = scheme_of(cfg);
+  if (!high_order && fast4d_shape(p.g, p.hm.dm, scheme) != p.shape)
+    return set_err(HJB_ERR_UNSUPPORTED,
+                   "solve_sharded: Lax-Friedrichs needs one input term per row of the 4D model");
   Nccl* api = nccl();
   if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
   const int P = comm->nranks, r = comm->rank;
@@ -530,6 +535,7 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
     CUDA_TRY(cudaMemcpyAsync(bits, dbits, sizeof bits, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     std::memcpy(&s.max_speed_sum, bits, sizeof(double));
+    std::memcpy(s.max_alpha, bits + 1, kMaxDims * sizeof(double));
   }
   if (!(s.max_speed_sum > 0.0))
     return set_err(HJB_ERR_RUNTIME, "solve: flow is identically zero on the grid");
@@ -581,6 +587,13 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
                        ctx->stream));
   ctx->launches += 2;
   fill_tables(p, f);
+  fill_lf(p.hm.dm, scheme, s.max_alpha, f);
+  if (f.lf) {  // the Lax-Friedrichs variant's CTA size
+    f.maxthreads = 448;
+    f.cbeg = has_lo ? 1u : 0u;
+    f.cend = f.cbeg + owned;
+    fast4d_config(gloc, sms > 0 ? sms : 148, f);
+  }
   f.c = ctx->pcbuf.d();
   f.buf0 = ctx->v2.d();
   f.buf1 = ctx->v3.d();

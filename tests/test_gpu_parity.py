@@ -263,3 +263,47 @@ def test_max_iters_zero_and_time_horizon(gpu_ctx, oracle):
         assert got.iterations == want.iterations < 1000
         assert got.iterations * got.dt >= 0.05 > (got.iterations - 1) * got.dt
         assert same(got.value.values(), want.value.values())
+
+
+def _lf_models():
+    return [("planar_d0", configs.planar_model(), [hj.Interval(-0.5, 0.5)]),
+            ("planar_d1", hj.NearHoverPlanar4D("x", d_row=1), [hj.Interval(-0.3, 0.7)]),
+            ("twin", hj.TwinDoubleIntegrator(), [hj.Interval(-0.2, 0.2), hj.Interval(-0.1, 0.3)])]
+
+
+@pytest.mark.parametrize("diss", [hj.PER_NODE, hj.GLOBAL], ids=["per_node", "global"])
+@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (7, 9, 5, 12), (17, 21, 19, 23)])
+@pytest.mark.parametrize("which", [0, 1, 2], ids=["planar_d0", "planar_d1", "twin"])
+def test_fast4d_lax_friedrichs(gpu_ctx, oracle, diss, dims, which):
+    """The Lax-Friedrichs variants of the specialised 4D kernel (per-node and
+    global dissipation, every row shape) against the oracle, bitwise."""
+    name, model, ivs = _lf_models()[which]
+    n0, n1, n2, n3 = dims
+    if name == "twin":
+        g = hj.Grid([(-1.0, 1.0, n0), (-1.0, 1.0, n1), (-1.0, 1.0, n2), (-1.0, 1.0, n3)])
+    else:
+        g = hj.Grid([(-5.0, 5.0, n0), (-2.0, 2.0, n1), (-0.35, 0.35, n2), (-1.5, 1.5, n3)])
+    db = hj.IntervalField.constant(g, ivs)
+    c = hj.ScalarField(g, band_np(g, 0, -0.6 * g.dims()[0].max, 0.6 * g.dims()[0].max))
+    cfg = hj.SolveConfig(tolerance=1e-6, max_iters=40, scheme=hj.LAX_FRIEDRICHS, dissipation=diss)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.dt == want.dt
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+@pytest.mark.parametrize("diss", [hj.PER_NODE, hj.GLOBAL], ids=["per_node", "global"])
+def test_fast4d_lax_friedrichs_matches_generic(gpu_ctx, monkeypatch, diss):
+    """Config-2 model on 31^4 with the LF scheme: specialised kernel == generic kernel."""
+    case = with_iters(workload_case(configs.config2(31)), 60)
+    case.cfg.scheme = hj.LAX_FRIEDRICHS
+    case.cfg.dissipation = diss
+    init, c = case.init_field(), case.c_field()
+    fast = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
+    monkeypatch.setenv("HJB_FAST", "0")
+    gen = hj.solve(init, c, case.model, case.db, case.cfg, ctx=gpu_ctx)
+    assert fast.iterations == gen.iterations == 60
+    assert same(fast.value.values(), gen.value.values())
+    assert same(fast.residual_history, gen.residual_history)

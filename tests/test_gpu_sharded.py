@@ -44,10 +44,13 @@ def test_slab_sweeps_compose_to_full_sweep(gpu_ctx, oracle, world):
     assert max(maxes) == float(np.max(np.abs(want - v)))
 
 
-def test_sharded_single_rank_equals_solve(gpu_ctx):
+@pytest.mark.parametrize("scheme,diss", [(hj.GODUNOV, hj.PER_NODE),
+                                         (hj.LAX_FRIEDRICHS, hj.PER_NODE),
+                                         (hj.LAX_FRIEDRICHS, hj.GLOBAL)])
+def test_sharded_single_rank_equals_solve(gpu_ctx, scheme, diss):
     w = configs.config2(21)
     c = band_np(w.grid, 0, -4.0, 4.0)
-    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=150)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=150, scheme=scheme, dissipation=diss)
     ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
                    ctx=gpu_ctx)
     ct = torch.tensor(c, device="cuda")
