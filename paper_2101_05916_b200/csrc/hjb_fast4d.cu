@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(MAXT, 1)
           if (SCH != 0) {
             // Lax-Friedrichs: costate p = (D- + D+)/2, bang-bang u*, worst d*,
             // H = sum_i p_i f_i (extremal_inputs + hamiltonian,
-            // dynamics.cpp:37-83), + alpha_d (D+ - D-)/2 (solver.cpp:161-176)
+            // dynamics.cpp:37-83), + alpha_d (D+ - D-)/2 (solver.cpp:160-174)
             const double dp0r = (vn[c] - v[c]) * inv0;
             double dmv[4], dpv[4];
             dmv[0] = i0 == 0 ? dp0r : dm0[c];
