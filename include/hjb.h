@@ -384,6 +384,73 @@ int hjb_ho_stage_planes_dev(hjb_context* ctx, const hjb_grid* grid, const hjb_mo
                             int32_t order, int32_t kind, int64_t plane_begin, int64_t plane_end,
                             double* out, double* max_dv);
 
+/* ------------------------------------------- GP disturbance bounds */
+/* A fitted GpModel (reference gp.hpp:41-75) over one disturbance channel:
+ * squared-exponential kernel k(a,b) = signal_var * exp(-0.5 * sum_d
+ * ((a_d - b_d) / lengthscales[d])^2) (gp.cpp:22-30) conditioned on n_train
+ * inputs (row-major n_train x input_dim), alpha = (K + noise I)^-1 y and the
+ * lower Cholesky factor chol (row-major n_train x n_train; only the lower
+ * triangle is read) as GpModel::fit stores them (gp.cpp:172-183).
+ * n_train = 0 is GpModel::prior (mean 0, variance signal_var).
+ * input_dims[0 .. n_dims) are the grid axes the channel's GP conditions on
+ * (bounds_on_grid's input_dims[ch]); n_dims must equal input_dim.  All
+ * pointers are host memory. */
+typedef struct hjb_gp_model {
+  int32_t input_dim;
+  int32_t n_dims;
+  int32_t input_dims[HJB_MAX_DIMS];
+  int64_t n_train;
+  double signal_var;
+  double noise_var;
+  double lengthscales[HJB_MAX_DIMS];
+  const double* inputs;
+  const double* alpha;
+  const double* chol;
+} hjb_gp_model;
+
+/* bounds_on_grid (reference gp.cpp:211-249): for every channel and node,
+ * (mean, latent variance) = GpModel::predict at the node's coordinates
+ * along input_dims (gp.cpp:188-208), band = confidence * sqrt(variance +
+ * noise_var), lo = mean - band, hi = mean + band.  lo_out[ch] / hi_out[ch]
+ * are grid.size doubles each: device pointers (_dev) or host pointers.
+ * Errors: "bounds_on_grid: input-dim map does not match GP",
+ * "bounds_on_grid: input dim out of grid range" (gp.cpp:219-227), the GP
+ * hyperparameter checks of GpHyperparams::validate (gp.cpp:14-21). */
+int hjb_gp_bounds_on_grid_dev(hjb_context* ctx, const hjb_grid* grid, int32_t channels,
+                              const hjb_gp_model* models, double confidence,
+                              double* const* lo_out, double* const* hi_out);
+int hjb_gp_bounds_on_grid(hjb_context* ctx, const hjb_grid* grid, int32_t channels,
+                          const hjb_gp_model* models, double confidence, double* const* lo_out,
+                          double* const* hi_out);
+/* GpModel::predict (gp.cpp:188-208) at nq points x[q*input_dim ..] (host):
+ * mean[q] and latent variance[q] (host). */
+int hjb_gp_predict_batch(hjb_context* ctx, const hjb_gp_model* model, int64_t nq,
+                         const double* x, double* mean, double* variance);
+
+/* GpModel::fit (gp.cpp:124-186), host only (O(n^3) once per model update):
+ * uniform subsample to max_training, hyperparameters by log-marginal-
+ * likelihood search over the reference's 48-candidate grid on a
+ * search_subsample subset (HJB_GP_SEARCH) or the prior as given
+ * (HJB_GP_FIXED), jitter 1e-8 signal_var, Cholesky, alpha, LML.
+ * Caller buffers hold min(n, max_training) training points: inputs_out
+ * (x input_dim), alpha_out, chol_out (squared); model_out points at them
+ * (input_dims = 0..input_dim-1; set them for bounds_on_grid).  The
+ * factorisation is a plain LLT, not Eigen's blocked one: factors match the
+ * reference's to rounding, not bitwise. */
+typedef enum hjb_gp_policy { HJB_GP_FIXED = 0, HJB_GP_SEARCH = 1 } hjb_gp_policy;
+typedef struct hjb_gp_fit_config {
+  int32_t policy;               /* hjb_gp_policy, default HJB_GP_SEARCH */
+  int32_t prior_n_lengthscales;
+  int64_t max_training;         /* 500 */
+  int64_t search_subsample;     /* 250 */
+  double prior_signal_var;      /* 0.01 */
+  double prior_noise_var;       /* 0 */
+  double prior_lengthscales[HJB_MAX_DIMS];
+} hjb_gp_fit_config;
+int hjb_gp_fit(int64_t n, int32_t input_dim, const double* x, const double* y,
+               const hjb_gp_fit_config* cfg, double* inputs_out, double* alpha_out,
+               double* chol_out, hjb_gp_model* model_out, double* lml_out);
+
 /* Stream of the context (cudaStream_t as void*) and synchronisation. */
 void* hjb_context_stream(hjb_context* ctx);
 int hjb_context_synchronize(hjb_context* ctx);

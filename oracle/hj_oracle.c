@@ -1259,3 +1259,79 @@ int hjo_ho_solve(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, con
   free(s2);
   return status;
 }
+
+/* ------------------------------------------------------------------- GP */
+/* GpModel::kernel, gp.cpp:22-30 */
+static double gp_kernel(const hjb_gp_model* m, const double* a, const double* b) {
+  double q = 0.0;
+  for (int d = 0; d < m->input_dim; ++d) {
+    const double r = (a[d] - b[d]) / m->lengthscales[d];
+    q += r * r;
+  }
+  return m->signal_var * exp(-0.5 * q);
+}
+
+/* GpModel::predict, gp.cpp:188-208 */
+int hjo_gp_predict(const hjb_gp_model* m, const double* x, double* mean, double* variance) {
+  const int64_t n = m->n_train;
+  if (n == 0) {  /* prior, gp.cpp:190 */
+    *mean = 0.0;
+    *variance = m->signal_var;
+    return 0;
+  }
+  double* v = (double*)malloc((size_t)n * sizeof(double));
+  if (!v) return fail(HJB_ERR_RUNTIME, "GP predict: out of memory");
+  for (int64_t i = 0; i < n; ++i) v[i] = gp_kernel(m, x, m->inputs + i * m->input_dim);
+  double mu = 0.0;
+  for (int64_t i = 0; i < n; ++i) mu += v[i] * m->alpha[i];
+  /* v = L^-1 k*, forward substitution (gp.cpp:196-202) */
+  for (int64_t i = 0; i < n; ++i) {
+    double s = v[i];
+    for (int64_t j = 0; j < i; ++j) s -= m->chol[i * n + j] * v[j];
+    v[i] = s / m->chol[i * n + i];
+  }
+  double var = m->signal_var;
+  for (int64_t i = 0; i < n; ++i) var -= v[i] * v[i];
+  free(v);
+  *mean = mu;
+  *variance = STD_MAX(var, 0.0);
+  return 0;
+}
+
+/* bounds_on_grid, gp.cpp:211-249 */
+int hjo_gp_bounds_on_grid(const hjb_grid* gi, int32_t channels, const hjb_gp_model* models,
+                          double confidence, double* const* lo, double* const* hi) {
+  grid_t g;
+  int rc = grid_init(gi, &g);
+  if (rc) return rc;
+  for (int ch = 0; ch < channels; ++ch) {
+    const hjb_gp_model* m = &models[ch];
+    if (m->n_dims != m->input_dim)
+      return fail(HJB_ERR_INVALID_ARGUMENT, "bounds_on_grid: input-dim map does not match GP");
+    for (int d = 0; d < m->n_dims; ++d)
+      if (m->input_dims[d] < 0 || m->input_dims[d] >= g.nd)
+        return fail(HJB_ERR_INVALID_ARGUMENT, "bounds_on_grid: input dim out of grid range");
+  }
+  for (int ch = 0; ch < channels; ++ch) {
+    const hjb_gp_model* m = &models[ch];
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t lin = 0; lin < g.size; ++lin) {
+      int64_t idx[HJB_MAX_DIMS];
+      double x[HJB_MAX_DIMS];
+      unravel(&g, lin, idx);
+      for (int d = 0; d < m->n_dims; ++d)
+        x[d] = coord(&g, m->input_dims[d], idx[m->input_dims[d]]);
+      double mean, var;
+      if (hjo_gp_predict(m, x, &mean, &var)) {
+        bad = 1;
+        continue;
+      }
+      const double band = confidence * sqrt(var + m->noise_var);
+      lo[ch][lin] = mean - band;
+      hi[ch][lin] = mean + band;
+    }
+    if (bad) return fail(HJB_ERR_RUNTIME, "GP predict: out of memory");
+  }
+  return 0;
+}

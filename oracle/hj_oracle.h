@@ -104,6 +104,14 @@ int hjo_filter_batch(const hjb_grid* g, const hjb_model* m, const hjb_dbounds* d
                      const double* value, int64_t nq, const double* x, const double* u_perf,
                      const hjb_filter_config* cfg, const hjb_filter_out* out);
 
+/* GpModel::predict, gp.cpp:188-208 (kernel gp.cpp:22-30): mean and latent
+ * variance at x[0 .. input_dim).  n_train == 0 is the prior. */
+int hjo_gp_predict(const hjb_gp_model* m, const double* x, double* mean, double* variance);
+/* bounds_on_grid, gp.cpp:211-249: predict at EVERY node (the reference's
+ * per-node evaluation), band = confidence * sqrt(var + noise_var). */
+int hjo_gp_bounds_on_grid(const hjb_grid* g, int32_t channels, const hjb_gp_model* models,
+                          double confidence, double* const* lo, double* const* hi);
+
 #ifdef __cplusplus
 }
 #endif

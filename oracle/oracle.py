@@ -294,6 +294,42 @@ def _restatement_filter_batch(self, v, model, db, x, u_perf=None, mode=abi.FILTE
 Restatement.filter_batch = _restatement_filter_batch
 
 
+def _restatement_gp_predict(self, model, X):
+    """hjo_gp_predict per point (GpModel::predict restated): (mean, var)."""
+    Xa = np.ascontiguousarray(np.asarray(X, dtype=np.float64)).reshape(-1, model.input_dim())
+    cm = model.to_c()
+    mean = np.empty(Xa.shape[0])
+    var = np.empty(Xa.shape[0])
+    fn = self.lib.hjo_gp_predict
+    fn.argtypes = [P(abi.HjbGpModel), _vp, P(_d), P(_d)]
+    for q in range(Xa.shape[0]):
+        m, v = C.c_double(), C.c_double()
+        self._chk(fn(C.byref(cm), _arr(Xa[q]), C.byref(m), C.byref(v)))
+        mean[q], var[q] = m.value, v.value
+    return mean, var
+
+
+def _restatement_gp_bounds_on_grid(self, models, input_dims, grid, confidence=3.0):
+    """hjo_gp_bounds_on_grid (bounds_on_grid restated, per node): (lo[], hi[])."""
+    nch = len(models)
+    arr = (abi.HjbGpModel * max(1, nch))()
+    for ch, (m, dims) in enumerate(zip(models, input_dims)):
+        arr[ch] = m.to_c(dims)
+    lo = [np.empty(grid.size()) for _ in range(nch)]
+    hi = [np.empty(grid.size()) for _ in range(nch)]
+    plo = (_vp * max(1, nch))(*[a.ctypes.data for a in lo])
+    phi = (_vp * max(1, nch))(*[a.ctypes.data for a in hi])
+    fn = self.lib.hjo_gp_bounds_on_grid
+    fn.argtypes = [P(abi.HjbGrid), C.c_int32, P(abi.HjbGpModel), _d, P(_vp), P(_vp)]
+    g = grid.to_c()
+    self._chk(fn(C.byref(g), nch, arr, float(confidence), plo, phi))
+    return lo, hi
+
+
+Restatement.gp_predict = _restatement_gp_predict
+Restatement.gp_bounds_on_grid = _restatement_gp_bounds_on_grid
+
+
 class ModelSpec(C.Structure):
     _fields_ = [("kind", C.c_int32), ("d_row", C.c_int32), ("p", C.c_double * 10)]
 

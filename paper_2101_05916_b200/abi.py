@@ -99,6 +99,25 @@ class HjbFilterOut(C.Structure):
 FILTER_OPTIMAL, FILTER_FILTER = 0, 1
 FILTER_OVERRIDE, FILTER_DEGENERATE, FILTER_OOD = 1, 2, 4
 
+
+class HjbGpModel(C.Structure):
+    _fields_ = [("input_dim", C.c_int32), ("n_dims", C.c_int32),
+                ("input_dims", C.c_int32 * HJB_MAX_DIMS), ("n_train", C.c_int64),
+                ("signal_var", C.c_double), ("noise_var", C.c_double),
+                ("lengthscales", C.c_double * HJB_MAX_DIMS),
+                ("inputs", C.POINTER(C.c_double)), ("alpha", C.POINTER(C.c_double)),
+                ("chol", C.POINTER(C.c_double))]
+
+
+class HjbGpFitConfig(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("prior_n_lengthscales", C.c_int32),
+                ("max_training", C.c_int64), ("search_subsample", C.c_int64),
+                ("prior_signal_var", C.c_double), ("prior_noise_var", C.c_double),
+                ("prior_lengthscales", C.c_double * HJB_MAX_DIMS)]
+
+
+GP_FIXED, GP_SEARCH = 0, 1
+
 P = C.POINTER
 _d = C.c_double
 _dp = P(C.c_double)
@@ -162,6 +181,12 @@ SIGNATURES = [
     ("hjb_copy_d2d", _i, [_vp, _vp, _vp, C.c_uint64]),
     ("hjb_ho_stage_planes_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp, _vp,
                                      _d, _i32, _i32, _i64, _i64, _vp, _dp]),
+    ("hjb_gp_bounds_on_grid_dev", _i, [_vp, P(HjbGrid), _i32, P(HjbGpModel), _d, P(_vp),
+                                       P(_vp)]),
+    ("hjb_gp_bounds_on_grid", _i, [_vp, P(HjbGrid), _i32, P(HjbGpModel), _d, P(_vp), P(_vp)]),
+    ("hjb_gp_predict_batch", _i, [_vp, P(HjbGpModel), _i64, _vp, _vp, _vp]),
+    ("hjb_gp_fit", _i, [_i64, _i32, _vp, _vp, P(HjbGpFitConfig), _vp, _vp, _vp, P(HjbGpModel),
+                        _dp]),
     ("hjb_context_stream", _vp, [_vp]),
     ("hjb_context_synchronize", _i, [_vp]),
     ("hjb_context_launch_count", _i64, [_vp]),

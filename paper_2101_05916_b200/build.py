@@ -15,7 +15,7 @@ CSRC = PKG / "csrc"
 OUT = PKG / "libhjb.so"
 
 SOURCES = ["hjb_capi.cu", "hjb_kernels.cu", "hjb_fast4d.cu", "hjb_shard.cu", "hjb_ho.cu",
-           "hjb_filter.cu"]
+           "hjb_filter.cu", "hjb_gp.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",

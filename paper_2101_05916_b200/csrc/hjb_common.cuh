@@ -55,6 +55,7 @@ struct hjb_context {
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   hjb::DevBuf v0, v1, v2, v3, cbuf, pcbuf, dbbuf, tables, scratch, hist, whist, xbuf;
+  hjb::DevBuf gpa, gpb, gpc;  // GP bounds: k*, factor, per-point tables
   hjb::LoopState* st = nullptr;
   hjb::LoopState* st_host = nullptr;  // pinned mirror
   long long launches = 0;

@@ -14,6 +14,7 @@ Reference map:
   cfl_dt / vi_step / solve ............ solver.hpp:48-65
   solve_coarse_to_fine / resample ..... solver.hpp:70-77, grid.hpp:108-109
   signed_distance_band, field_max/min . levelset.hpp:31-39
+  GpModel / bounds_on_grid ........... gp.hpp:41-97 (gp.py)
 """
 from __future__ import annotations
 
@@ -1037,3 +1038,7 @@ def field_max_dev(n: int, a_ptr: int, b_ptr: int, out_ptr: int, ctx: Context | N
 # safety.py; re-exported here so the reference's names resolve from hjsafe.
 from .safety import (CombinedDecision, Decomposition, FilterDecision, SafetyFilter,  # noqa: E402
                      Subsystem, Violation, project, scatter)
+# GP disturbance bounds (gp.hpp) live in gp.py.
+from . import gp as gp_module  # noqa: E402
+from .gp import (DisturbanceMeasurement, GpConfig, GpHyperparams, GpModel,  # noqa: E402
+                 ViolationCheck, bounds_on_grid, bounds_on_grid_dev, violation_check)
