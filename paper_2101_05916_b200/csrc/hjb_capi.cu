@@ -471,6 +471,10 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
     configure(2, 448);
     return HJB_OK;
   }
+  if (f.pv) {  // one plane-varying-bounds variant
+    configure(2, 576);
+    return HJB_OK;
+  }
   if (kc || mt) {
     const uint32_t k = (kc && std::atoi(kc) == 4) ? 4u : 2u;
     configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 576u));
@@ -568,6 +572,85 @@ static int collapse_dbounds(hjb_context* ctx, const DevGrid& g, const hjb_dbound
   return HJB_OK;
 }
 
+// Per-node bounds that vary along axis 0 only (GP bounds over x, the sim's
+// case) keep the 4D fast path: check separability on the device, then build
+// the plane-varying tables — per row, drift + control terms over its table
+// axis (pos / neg), and per disturbance row the plane's max / min of the
+// disturbance products (row_slopes order, solver.cpp:67-86) — appended to
+// the model table.  Returns 1 when the PV path applies.
+static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
+                      const hjb_dbounds* db, int shape_pv, Fast4dArgs& f, int* ok) {
+  *ok = 0;
+  if (shape_pv < 0 || !db->per_node) return HJB_OK;
+  const uint32_t s0 = g.stride[0];
+  CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
+  unsigned int* flag = reinterpret_cast<unsigned int*>(ctx->scratch.d() + 40);
+  CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(unsigned int), ctx->stream));
+  for (int ch = 0; ch < db->channels; ++ch) {
+    CUDA_TRY(launch_not_axis0(db->lo[ch], g.size, s0, flag, ctx->stream));
+    CUDA_TRY(launch_not_axis0(db->hi[ch], g.size, s0, flag, ctx->stream));
+    ctx->launches += 2;
+  }
+  unsigned int hf = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hf, flag, sizeof hf, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (hf) return HJB_OK;
+  const uint32_t n0 = g.n[0];
+  std::vector<double> plo(static_cast<size_t>(db->channels) * n0),
+      phi(static_cast<size_t>(db->channels) * n0);
+  for (int ch = 0; ch < db->channels; ++ch) {
+    CUDA_TRY(cudaMemcpy2DAsync(plo.data() + ch * n0, sizeof(double), db->lo[ch],
+                               s0 * sizeof(double), sizeof(double), n0,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpy2DAsync(phi.data() + ch * n0, sizeof(double), db->hi[ch],
+                               s0 * sizeof(double), sizeof(double), n0,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::vector<double> t = hm.tab;
+  for (int d = 0; d < 4; ++d) {
+    const DevRow& r = hm.dm.row[d];
+    f.pv_pt[d] = f.pv_nt[d] = -1;
+    if (r.axis_b < 0) {  // drift + controls over the table axis
+      const uint32_t len = r.axis_a >= 0 ? g.n[r.axis_a] : 1u;
+      f.off_pos[d] = static_cast<int>(t.size());
+      for (uint32_t k = 0; k < len; ++k) {
+        double ps = r.constant_drift ? r.drift_const : hm.tab[r.off_a + k];
+        for (int q = 0; q < r.n_uadd; ++q) ps += r.uadd_pos[q];
+        t.push_back(ps);
+      }
+      f.off_neg[d] = static_cast<int>(t.size());
+      for (uint32_t k = 0; k < len; ++k) {
+        double ng = r.constant_drift ? r.drift_const : hm.tab[r.off_a + k];
+        for (int q = 0; q < r.n_uadd; ++q) ng += r.uadd_neg[q];
+        t.push_back(ng);
+      }
+    }
+    if (r.n_dterm == 1) {
+      const int ch = r.dch[0];
+      f.pv_pt[d] = static_cast<int>(t.size());
+      for (uint32_t i = 0; i < n0; ++i) {
+        const double a = r.dcoef[0] * plo[ch * n0 + i], b = r.dcoef[0] * phi[ch * n0 + i];
+        t.push_back(a > b ? a : b);
+      }
+      f.pv_nt[d] = static_cast<int>(t.size());
+      for (uint32_t i = 0; i < n0; ++i) {
+        const double a = r.dcoef[0] * plo[ch * n0 + i], b = r.dcoef[0] * phi[ch * n0 + i];
+        t.push_back(a < b ? a : b);
+      }
+    }
+  }
+  CUDA_TRY(ctx->pvtab.ensure(t.size() * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(ctx->pvtab.p, t.data(), t.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  f.tab = ctx->pvtab.d();
+  f.tab_len = static_cast<uint32_t>(t.size());
+  f.pv = 1;
+  *ok = 1;
+  return HJB_OK;
+}
+
 static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
                       const hjb_dbounds* db_in, const double* init, const double* c,
                       const hjb_solve_config* cfg, double* value_out, hjb_solve_result* res) {
@@ -622,7 +705,11 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   CUDA_TRY(ctx->v0.ensure(bytes));
   CUDA_TRY(ctx->v1.ensure(bytes));
   CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
-  const int shape = fast_enabled() ? fast4d_shape(g, hm.dm, scheme_of(cfg)) : -1;
+  int shape = fast_enabled() ? fast4d_shape(g, hm.dm, scheme_of(cfg)) : -1;
+  const int shape_pv = (shape < 0 && fast_enabled() && db->per_node &&
+                        scheme_of(cfg) == kGodunov)
+                           ? fast4d_shape_pv(g, hm.dm)
+                           : -1;
   StepArgs a = base_args(g, hm.dm, c, dt, scheme_of(cfg), s);
   a.st = ctx->st;
   a.buf0 = ctx->v0.d();
@@ -630,16 +717,27 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   Fast4dArgs f;
   std::memset(&f, 0, sizeof f);
   uint64_t rows = 0;
+  if (shape_pv >= 0) {
+    for (int d = 0; d < 4; ++d) {  // off_a / off_b of the model table stay valid
+      f.off_a[d] = hm.dm.row[d].off_a;
+      f.off_b[d] = hm.dm.row[d].off_b;
+    }
+    int ok = 0;
+    if ((rc = prepare_pv(ctx, g, hm, db, shape_pv, f, &ok))) return rc;
+    if (ok) shape = shape_pv;
+  }
   if (shape >= 0) {
     // padded internal layout for the 4D fast path; kernel variant chosen by
     // the autotuner (cached per grid shape)
-    f.tab = hm.dm.tab;
-    f.tab_len = static_cast<uint32_t>(hm.tab.size());
-    for (int d = 0; d < 4; ++d) {
-      f.off_pos[d] = hm.dm.row[d].off_pos;
-      f.off_neg[d] = hm.dm.row[d].off_neg;
-      f.off_a[d] = hm.dm.row[d].off_a;
-      f.off_b[d] = hm.dm.row[d].off_b;
+    if (!f.pv) {
+      f.tab = hm.dm.tab;
+      f.tab_len = static_cast<uint32_t>(hm.tab.size());
+      for (int d = 0; d < 4; ++d) {
+        f.off_pos[d] = hm.dm.row[d].off_pos;
+        f.off_neg[d] = hm.dm.row[d].off_neg;
+        f.off_a[d] = hm.dm.row[d].off_a;
+        f.off_b[d] = hm.dm.row[d].off_b;
+      }
     }
     f.st = ctx->st;
     f.dt = dt;

@@ -334,7 +334,7 @@ constexpr uint32_t kEndItem = 0xffffffffu;
 // products of faces shared by two cells are formed once: along the march
 // (carried to the next plane) and inside the pencil when the row's slopes do
 // not vary along the contiguous axis.
-template <class S, int kK, int MAXT, int SCH>
+template <class S, int kK, int MAXT, int SCH, bool PV = false>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -606,6 +606,24 @@ __global__ void __launch_bounds__(MAXT, 1)
       }
 
       for (uint32_t i0 = c0; i0 < c1; ++i0) {
+        if (PV) {
+          // plane-varying disturbance bounds: this plane's slopes and shapes
+          // of the disturbance rows (row_slopes order: drift + controls,
+          // then + max / min of the disturbance products, solver.cpp:67-86)
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (S::D(d) < 0) continue;
+            static_assert(!S::LIN(0) || S::D(0) < 0, "PV rows are non-linear");
+            const double pt = tabs[a.pv_pt[d] + i0], nt = tabs[a.pv_nt[d] + i0];
+            const RowShape rs = row_shape(pos_[d][0] + pt, neg_[d][0] + nt);
+#pragma unroll
+            for (int c = 0; c < kK; ++c) shp[d][c] = rs;
+          }
+          if (S::D(0) >= 0) {  // march-axis row: the carried D- face's L product
+#pragma unroll
+            for (int c = 0; c < kK; ++c) ka0[c] = pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
+          }
+        }
         const uint32_t slot_cur = vring + sl * a.vslot_bytes;
         const uint32_t csl = cring + sl * a.cslot_bytes;
         const uint32_t bar_cur = bars + sl * 8;
@@ -1641,6 +1659,37 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   return sh;
 }
 
+int fast4d_shape_pv(const DevGrid& g, const DevModel& m) {
+  if (g.nd != 4) return -1;
+  if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
+  int A[4], B[4];
+  bool lin[4];
+  for (int d = 0; d < 4; ++d) {
+    const DevRow& r = m.row[d];
+    if (r.axis_b >= 0 && (r.n_uadd || r.n_dterm || r.constant_drift)) return -1;
+    A[d] = r.axis_a;
+    B[d] = r.axis_b;
+    if (A[d] == 0 || B[d] == 0) return -1;
+    lin[d] = r.n_uadd == 0 && r.n_dterm == 0;
+    if (r.n_dterm > 1) return -1;
+  }
+  static const int pa[4] = {1, 2, 2, 2}, pb[4] = {-1, -1, 3, -1};
+  static const bool l0[4] = {false, true, true, false}, l1[4] = {true, false, true, false};
+  static const int ta[4] = {1, -1, 3, -1}, tb[4] = {-1, -1, -1, -1};
+  static const bool lt[4] = {true, false, true, false};
+  auto match = [&](const int* a, const int* b, const bool* l, int sh) {
+    for (int d = 0; d < 4; ++d) {
+      if (a[d] != A[d] || b[d] != B[d] || (l[d] && !lin[d])) return false;
+      if ((m.row[d].n_dterm > 0) != (kShapeD[sh][d] >= 0)) return false;
+    }
+    return true;
+  };
+  if (match(pa, pb, l0, 0)) return 0;
+  if (match(pa, pb, l1, 1)) return 1;
+  if (match(ta, tb, lt, 2)) return 2;
+  return -1;
+}
+
 static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
   if (g.nd != 4 || m.per_node) return -1;
   if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
@@ -1762,16 +1811,16 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.blocks = std::min<uint32_t>(a.items, static_cast<uint32_t>(sms));
 }
 
-template <class S, int K, int MAXT, int SCH = 0>
+template <class S, int K, int MAXT, int SCH = 0, bool PV = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH, PV>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   if (a.l2_bytes == 0 && !a.pdl) {
-    k_fast4d<S, K, MAXT, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
+    k_fast4d<S, K, MAXT, SCH, PV><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1797,13 +1846,17 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH>, a);
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
 // the autotuner pick among them per grid
 template <class S>
 static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.pv) {  // plane-varying disturbance bounds: one configuration
+    launch_one<S, 2, 576, 0, true>(a, s);
+    return;
+  }
   if (a.lf == 1) {  // Lax-Friedrichs variants: one configuration
     launch_one<S, 2, 448, 1>(a, s);
     return;

@@ -48,6 +48,12 @@ struct Fast4dArgs {
   // numerical Hamiltonian: 0 Godunov, 1 Lax-Friedrichs with per-node alpha,
   // 2 Lax-Friedrichs with global alpha (galpha)
   int lf;
+  // per-node disturbance bounds that vary along axis 0 only (e.g. GP bounds
+  // over x, gp.cpp:211-249): rows with a disturbance term take
+  // pos = tab[off_pos] + tab[pv_pt + i0], neg = tab[off_neg] + tab[pv_nt + i0]
+  // per plane (Godunov only)
+  int pv;
+  int pv_pt[4], pv_nt[4];
   double galpha[4];
   int dr_off[4];        // drift table offset of each row (-1: constant drift)
   double dr_const[4];
@@ -103,6 +109,11 @@ cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s);
 // (rank != 4, per-node bounds, rows depending on x0, inputs not matching the
 // shape, ...).  scheme: 0 Godunov, 1 LF per-node alpha, 2 LF global alpha.
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
+// Godunov fast-path shape for PER-NODE bounds (rows not folded); -1 if none.
+// Rows with a disturbance term must be exactly the shape's D rows, one
+// term each; their bounds must then vary along axis 0 only (checked on the
+// device by the caller).
+int fast4d_shape_pv(const DevGrid& g, const DevModel& m);
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
 // Encode the three TMA tensor maps for the padded buffers (driver entry point

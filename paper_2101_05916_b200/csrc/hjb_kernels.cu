@@ -1106,6 +1106,28 @@ cudaError_t launch_not_constant(const double* f, uint32_t n, unsigned int* flag,
   return cudaGetLastError();
 }
 
+// flag := 1 if f[lin] differs (bit pattern) from f at the first node of its
+// axis-0 plane, i.e. the field is not a function of i0 alone
+__global__ void k_not_axis0(const double* __restrict__ f, uint32_t n, uint32_t s0,
+                            unsigned int* flag) {
+  for (uint32_t lin = blockIdx.x * blockDim.x + threadIdx.x; lin < n;
+       lin += gridDim.x * blockDim.x) {
+    const uint32_t base = lin - lin % s0;
+    if (__double_as_longlong(f[lin]) != __double_as_longlong(f[base])) {
+      *flag = 1u;
+      return;
+    }
+  }
+}
+
+cudaError_t launch_not_axis0(const double* f, uint32_t n, uint32_t s0, unsigned int* flag,
+                             cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const uint32_t b = (n + kThreads - 1) / kThreads;
+  k_not_axis0<<<b < 148 * 8 ? b : 148 * 8, kThreads, 0, s>>>(f, n, s0, flag);
+  return cudaGetLastError();
+}
+
 size_t small2d_smem(const DevGrid& g, uint32_t* rows_out, uint32_t* ctas_out) {
   if (g.nd != 2) return 0;
   const uint32_t R = (g.n[0] + 15) / 16;

@@ -81,5 +81,7 @@ cudaError_t launch_field_op(long long n, const double* a, const double* b, doubl
 cudaError_t launch_fill(double* out, uint32_t n, double value, cudaStream_t s);
 // *flag |= 1 if any of f[0..n) differs bitwise from f[0] (flag zeroed by caller)
 cudaError_t launch_not_constant(const double* f, uint32_t n, unsigned int* flag, cudaStream_t s);
+cudaError_t launch_not_axis0(const double* f, uint32_t n, uint32_t s0, unsigned int* flag,
+                             cudaStream_t s);
 
 }  // namespace hjb

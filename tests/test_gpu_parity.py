@@ -307,3 +307,53 @@ def test_fast4d_lax_friedrichs_matches_generic(gpu_ctx, monkeypatch, diss):
     assert fast.iterations == gen.iterations == 60
     assert same(fast.value.values(), gen.value.values())
     assert same(fast.residual_history, gen.residual_history)
+
+
+def _axis0_bounds(g, specs, seed=7, break_node=None):
+    """Per-node IntervalField varying along axis 0 only (GP bounds over x):
+    one (center, half-width) profile per channel."""
+    rng = np.random.default_rng(seed)
+    n0 = g.dim(0).n
+    s0 = g.size() // n0
+    lo, hi = [], []
+    for (c, w) in specs:
+        mid = c + 0.3 * np.sin(np.linspace(0.0, 3.0, n0)) + 0.05 * rng.standard_normal(n0)
+        half = w * (1.0 + 0.5 * rng.random(n0))
+        lo.append(np.repeat(mid - half, s0))
+        hi.append(np.repeat(mid + half, s0))
+    if break_node is not None:
+        lo[0][break_node] -= 1e-3
+    return hj.IntervalField(g, len(specs), lo=lo, hi=hi)
+
+
+PV_CASES = [
+    ("planar_d0", lambda: configs.planar_model(), [(0.0, 0.5)],
+     [(-5.0, 5.0, 15), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 11)]),
+    ("planar_d1", lambda: hj.NearHoverPlanar4D("x", d_row=1), [(0.1, 0.4)],
+     [(-5.0, 5.0, 13), (-2.0, 2.0, 8), (-0.35, 0.35, 9), (-1.5, 1.5, 6)]),
+    ("twin", lambda: hj.TwinDoubleIntegrator(), [(0.0, 0.15), (0.05, 0.1)],
+     [(-2.5, 2.5, 11), (-3.0, 3.0, 9), (-2.5, 2.5, 7), (-3.0, 3.0, 13)]),
+]
+
+
+@pytest.mark.parametrize("case", PV_CASES, ids=[c[0] for c in PV_CASES])
+@pytest.mark.parametrize("broken", [False, True], ids=["axis0", "not_axis0"])
+def test_fast4d_axis0_varying_bounds(gpu_ctx, oracle, monkeypatch, case, broken):
+    """Per-node bounds varying along axis 0 only (the sim's GP bounds) run the
+    specialised kernel's plane-varying variant; a field that is not a
+    function of x0 alone falls back to the generic kernel.  Both bitwise equal
+    to the oracle and to HJB_FAST=0."""
+    _, mk, specs, dims = case
+    g = hj.Grid(dims)
+    model = mk()
+    db = _axis0_bounds(g, specs, break_node=(g.size() // 2) if broken else None)
+    c = hj.ScalarField(g, band_np(g, 0, -0.6 * g.dims()[0].max, 0.6 * g.dims()[0].max))
+    cfg = hj.SolveConfig(tolerance=1e-6, max_iters=40)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+    monkeypatch.setenv("HJB_FAST", "0")
+    gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert same(gen.value.values(), got.value.values())
