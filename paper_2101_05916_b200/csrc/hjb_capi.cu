@@ -405,21 +405,25 @@ void fill_tables(const Prepared& p, Fast4dArgs& f) {
 // Lax-Friedrichs fields of the 4D fast path: per-row drift tables, input
 // coefficients and bounds (constant disturbance bounds only), alpha
 void fill_lf(const DevModel& m, int scheme, const double* galpha, Fast4dArgs& f) {
-  f.lf = scheme == kGodunov ? 0 : (scheme == kLfGlobal ? 2 : 1);
+  fill_lf(m, scheme, galpha, f.lf, f.lp);
+}
+
+void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfParams& lp) {
+  lf = scheme == kGodunov ? 0 : (scheme == kLfGlobal ? 2 : 1);
   for (int d = 0; d < 4; ++d) {
     const DevRow& r = m.row[d];
-    f.galpha[d] = galpha[d];
-    f.dr_off[d] = r.constant_drift ? -1 : r.off_a;
-    f.dr_const[d] = r.constant_drift ? r.drift_const : 0.0;
-    f.ucoef[d] = r.n_uadd > 0 ? r.ucoef[0] : 0.0;
-    f.dcoef[d] = r.n_dterm > 0 ? r.dcoef[0] : 0.0;
-    f.off_alpha[d] = r.off_alpha;
+    lp.galpha[d] = galpha[d];
+    lp.dr_off[d] = r.constant_drift ? -1 : r.off_a;
+    lp.dr_const[d] = r.constant_drift ? r.drift_const : 0.0;
+    lp.ucoef[d] = r.n_uadd > 0 ? r.ucoef[0] : 0.0;
+    lp.dcoef[d] = r.n_dterm > 0 ? r.dcoef[0] : 0.0;
+    lp.off_alpha[d] = r.off_alpha;
   }
   for (int j = 0; j < 3; ++j) {
-    f.ulo[j] = j < m.m ? m.ulo[j] : 0.0;
-    f.uhi[j] = j < m.m ? m.uhi[j] : 0.0;
-    f.dlo[j] = j < m.p ? m.dlo[j] : 0.0;
-    f.dhi[j] = j < m.p ? m.dhi[j] : 0.0;
+    lp.ulo[j] = j < m.m ? m.ulo[j] : 0.0;
+    lp.uhi[j] = j < m.m ? m.uhi[j] : 0.0;
+    lp.dlo[j] = j < m.p ? m.dlo[j] : 0.0;
+    lp.dhi[j] = j < m.p ? m.dhi[j] : 0.0;
   }
 }
 

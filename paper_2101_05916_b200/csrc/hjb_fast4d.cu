@@ -334,6 +334,79 @@ constexpr uint32_t kEndItem = 0xffffffffu;
 // products of faces shared by two cells are formed once: along the march
 // (carried to the next plane) and inside the pencil when the row's slopes do
 // not vary along the contiguous axis.
+// Lax-Friedrichs numerical Hamiltonian of one cell from its (D-, D+) per
+// axis: costate p = (D- + D+)/2, bang-bang u* (ties to lo) and worst d*,
+// H = sum_i p_i f_i summed from 0 in row order (extremal_inputs +
+// hamiltonian, dynamics.cpp:37-83), + alpha_i (D+ - D-)/2 (solver.cpp:
+// 160-174).  dr: the rows' drifts at the cell, al: their alphas.
+template <class S>
+__device__ __forceinline__ double lf_hhat(const LfParams& lp, const double* dmv,
+                                          const double* dpv, const double* dr, const double* al) {
+  double pq[4];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) pq[d] = 0.5 * (dmv[d] + dpv[d]);
+  double u[3] = {0.0, 0.0, 0.0}, dd[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    double coeff = 0.0;
+    bool any = false;
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (S::U(d) == j) {
+        coeff += pq[d] * lp.ucoef[d];
+        any = true;
+      }
+    if (any) u[j] = coeff > 0.0 ? lp.ulo[j] : (coeff < 0.0 ? lp.uhi[j] : lp.ulo[j]);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double coeff = 0.0;
+    bool any = false;
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (S::D(d) == k) {
+        coeff += pq[d] * lp.dcoef[d];
+        any = true;
+      }
+    if (any) dd[k] = coeff > 0.0 ? lp.dhi[k] : (coeff < 0.0 ? lp.dlo[k] : lp.dlo[k]);
+  }
+  double hh = 0.0;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    double fi = dr[d];
+    if (S::U(d) >= 0) fi += lp.ucoef[d] * u[S::U(d) >= 0 ? S::U(d) : 0];
+    if (S::D(d) >= 0) fi += lp.dcoef[d] * dd[S::D(d) >= 0 ? S::D(d) : 0];
+    hh += pq[d] * fi;
+  }
+#pragma unroll
+  for (int d = 0; d < 4; ++d) hh += al[d] * 0.5 * (dpv[d] - dmv[d]);
+  return hh;
+}
+
+// Row drifts and LF dissipation coefficients of a cell (loop invariant):
+// rows without inputs have drift == their slope, alpha == |drift| when no
+// flow_bounds table exists; SCH 2 takes the global alpha.
+template <class S, int SCH>
+__device__ __forceinline__ void lf_row_terms(const LfParams& lp, const double* tabs,
+                                             const uint32_t* ka, const double* slope_b,
+                                             double* dr, double* al) {
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    if (S::B(d) >= 0) {  // two-term drift, no inputs: the slope is the drift
+      dr[d] = slope_b[d];
+    } else {
+      dr[d] = lp.dr_off[d] >= 0 ? tabs[lp.dr_off[d] + ka[d]] : lp.dr_const[d];
+    }
+    if (SCH == 2) {
+      al[d] = lp.galpha[d];
+    } else if (lp.off_alpha[d] >= 0) {
+      al[d] = tabs[lp.off_alpha[d] + ka[d]];
+    } else {
+      al[d] = fabs(dr[d]);
+    }
+  }
+}
+
 template <class S, int kK, int MAXT, int SCH, bool PV = false>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
@@ -556,22 +629,20 @@ __global__ void __launch_bounds__(MAXT, 1)
       double lfdr[4][kK], lfal[4][kK];
       if (SCH != 0) {
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
+        for (int c = 0; c < kK; ++c) {
+          uint32_t ka[4];
+          double sb[4];
 #pragma unroll
-          for (int c = 0; c < kK; ++c) {
-            const uint32_t ka = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
-            if (S::B(d) >= 0) {  // two-term drift, no inputs: pos == drift
-              lfdr[d][c] = pos_[d][c];
-            } else {
-              lfdr[d][c] = a.dr_off[d] >= 0 ? tabs[a.dr_off[d] + ka] : a.dr_const[d];
-            }
-            if (SCH == 2) {
-              lfal[d][c] = a.galpha[d];
-            } else if (a.off_alpha[d] >= 0) {
-              lfal[d][c] = tabs[a.off_alpha[d] + ka];
-            } else {
-              lfal[d][c] = fabs(lfdr[d][c]);
-            }
+          for (int d = 0; d < 4; ++d) {
+            ka[d] = active ? pick<S>(S::A(d), i1, i2, min(i3 + c, n3 - 1)) : 0u;
+            sb[d] = pos_[d][c];
+          }
+          double dr[4], al[4];
+          lf_row_terms<S, SCH>(a.lp, tabs, ka, sb, dr, al);
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            lfdr[d][c] = dr[d];
+            lfal[d][c] = al[d];
           }
         }
       }
@@ -708,44 +779,13 @@ __global__ void __launch_bounds__(MAXT, 1)
             dpv[3] = f3[c + 1];
             if (i3 + c == 0) dmv[3] = dpv[3];
             if (i3 + c + 1 == n3) dpv[3] = dmv[3];
-            double pq[4];
-#pragma unroll
-            for (int d = 0; d < 4; ++d) pq[d] = 0.5 * (dmv[d] + dpv[d]);
-            double u[3] = {0.0, 0.0, 0.0}, dd[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              double coeff = 0.0;
-              bool any = false;
-#pragma unroll
-              for (int d = 0; d < 4; ++d)
-                if (S::U(d) == j) {
-                  coeff += pq[d] * a.ucoef[d];
-                  any = true;
-                }
-              if (any) u[j] = coeff > 0.0 ? a.ulo[j] : (coeff < 0.0 ? a.uhi[j] : a.ulo[j]);
-            }
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              double coeff = 0.0;
-              bool any = false;
-#pragma unroll
-              for (int d = 0; d < 4; ++d)
-                if (S::D(d) == k) {
-                  coeff += pq[d] * a.dcoef[d];
-                  any = true;
-                }
-              if (any) dd[k] = coeff > 0.0 ? a.dhi[k] : (coeff < 0.0 ? a.dlo[k] : a.dlo[k]);
-            }
-            double hh = 0.0;
+            double drc[4], alc[4];
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
-              double fi = lfdr[d][c];
-              if (S::U(d) >= 0) fi += a.ucoef[d] * u[S::U(d) >= 0 ? S::U(d) : 0];
-              if (S::D(d) >= 0) fi += a.dcoef[d] * dd[S::D(d) >= 0 ? S::D(d) : 0];
-              hh += pq[d] * fi;
+              drc[d] = lfdr[d][c];
+              alc[d] = lfal[d][c];
             }
-#pragma unroll
-            for (int d = 0; d < 4; ++d) hh += lfal[d][c] * 0.5 * (dpv[d] - dmv[d]);
+            const double hh = lf_hhat<S>(a.lp, dmv, dpv, drc, alc);
             const double st = v[c] + a.dt * hh;
             out[c] = st > cc[c] ? st : cc[c];
             const double dv = fabs(out[c] - v[c]);
@@ -1196,6 +1236,19 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   loop_epilogue(st, a.handle, a.use_handle);
 }
 
+// Lax-Friedrichs ghost faces of a face window (faces f0 .. f0+N-1, valid
+// 0 .. fmax): a face beyond the grid takes the nearest interior face, the
+// reference's replicated one-sided difference (solver.cpp:139-148)
+template <int N>
+__device__ __forceinline__ void lf_ghost(double* A, int f0, int fmax) {
+#pragma unroll
+  for (int q = N - 2; q >= 0; --q)
+    if (f0 + q < 0) A[q] = A[q + 1];
+#pragma unroll
+  for (int q = 1; q < N; ++q)
+    if (f0 + q > fmax) A[q] = A[q - 1];
+}
+
 // TMA-staged variant: a producer thread streams each plane's V box (tile +
 // R-row halo in i1 and i2, full rows) into a shared-memory ring; consumers
 // read the axis-1/2/3 neighbours from shared memory and only their own
@@ -1225,7 +1278,7 @@ __host__ __device__ constexpr int ho4t_maxthreads(int r, int kc) {
   return kc == 1 ? 512 : ho4d_maxthreads(r);
 }
 
-template <class S, int R, int KC>
+template <class S, int R, int KC, int SCH = 0>
 __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
     k_ho4t(const __grid_constant__ Ho4dArgs a) {
   constexpr int kK = KC;
@@ -1327,8 +1380,29 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
         up[d][c] = sign_clear(pos_[d][c]);
-        if (S::LIN(d)) continue;
+        if (S::LIN(d) || SCH != 0) continue;
         shp[d][c] = (c > 0 && !per_cell) ? shp[d][0] : row_shape(pos_[d][c], neg_[d][c]);
+      }
+    }
+    // Lax-Friedrichs: the rows' drifts and alphas (loop invariant)
+    double lfdr[4][kK], lfal[4][kK];
+    if (SCH != 0) {
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        uint32_t ka[4];
+        double sb[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          ka[d] = pick<S>(S::A(d), ci1, ci2, min(i3 + c, n3 - 1));
+          sb[d] = pos_[d][c];
+        }
+        double dr[4], al[4];
+        lf_row_terms<S, SCH>(a.lp, a.tab, ka, sb, dr, al);
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          lfdr[d][c] = dr[d];
+          lfal[d][c] = al[d];
+        }
       }
     }
     // ghost-face masks of axes 1 and 2 are loop invariant
@@ -1404,6 +1478,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
         double A[2 * R];
 #pragma unroll
         for (int q = 0; q < 2 * R; ++q) A[q] = fw[q][c];
+        if (SCH != 0) lf_ghost<2 * R>(A, (int)i0 - R, (int)n0 - 2);
         eno_faces<R>(A, dmv[0][c], dpv[0][c]);
       }
       // axes 3, 1, 2 from this plane's box in shared memory; warps whose
@@ -1431,6 +1506,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
             const double d = (rv[q + 1] - rv[q]) * inv3;
             f3[q] = (kIn || (f >= 0 && f <= (int)n3 - 2)) ? d : 0.0;
           }
+          if (SCH != 0 && !kIn) lf_ghost<NV - 1>(f3, (int)i3 - R, (int)n3 - 2);
           if (R >= 3 || kK != 2) {  // per cell: fewer live registers at the ENO3 register cap
 #pragma unroll
             for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
@@ -1467,6 +1543,8 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
               const double d = (nv[q + 1][c] - nv[q][c]) * inv;
               A[q] = ok ? d : 0.0;
             }
+            if (SCH != 0 && !kIn)
+              lf_ghost<2 * R>(A, (int)(ax == 1 ? ci1 : ci2) - R, (int)(ax == 1 ? n1 : n2) - 2);
             eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
           }
         }
@@ -1496,6 +1574,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
             const int f = (int)i3 - R + q;
             f3[q] = (f >= 0 && f <= (int)n3 - 2) ? (rv[q + 1] - rv[q]) * inv3 : 0.0;
           }
+          if (SCH != 0) lf_ghost<NV - 1>(f3, (int)i3 - R, (int)n3 - 2);
   #pragma unroll
           for (int c = 0; c < kK; ++c) eno_faces<R>(f3 + c, dmv[3][c], dpv[3][c]);
         }
@@ -1521,6 +1600,8 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
               const bool ok = ax == 1 ? ok1[q] : ok2[q];
               A[q] = ok ? (nv[q + 1][c] - nv[q][c]) * inv : 0.0;
             }
+            if (SCH != 0)
+              lf_ghost<2 * R>(A, (int)(ax == 1 ? ci1 : ci2) - R, (int)(ax == 1 ? n1 : n2) - 2);
             eno_faces<R>(A, dmv[ax][c], dpv[ax][c]);
           }
         }
@@ -1535,18 +1616,31 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
       double out[kK];
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
-        double h[4];
+        double hh;
+        if (SCH != 0) {
+          double dm4[4], dp4[4], drc[4], alc[4];
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
-          if (S::LIN(d)) {
-            h[d] = pos_[d][c] * (up[d][c] ? dpv[d][c] : dmv[d][c]);
-          } else {
-            const double ka = pair_kink(shp[d][c].L, dmv[d][c], sign_bit(dmv[d][c]));
-            const double kb = pair_kink(shp[d][c].R, dpv[d][c], sign_bit(dpv[d][c]));
-            h[d] = shape_pick(shp[d][c], ka, kb);
+          for (int d = 0; d < 4; ++d) {
+            dm4[d] = dmv[d][c];
+            dp4[d] = dpv[d][c];
+            drc[d] = lfdr[d][c];
+            alc[d] = lfal[d][c];
           }
+          hh = lf_hhat<S>(a.lp, dm4, dp4, drc, alc);
+        } else {
+          double h[4];
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (S::LIN(d)) {
+              h[d] = pos_[d][c] * (up[d][c] ? dpv[d][c] : dmv[d][c]);
+            } else {
+              const double ka = pair_kink(shp[d][c].L, dmv[d][c], sign_bit(dmv[d][c]));
+              const double kb = pair_kink(shp[d][c].R, dpv[d][c], sign_bit(dpv[d][c]));
+              h[d] = shape_pick(shp[d][c], ka, kb);
+            }
+          }
+          hh = ((h[0] + h[1]) + h[2]) + h[3];
         }
-        const double hh = ((h[0] + h[1]) + h[2]) + h[3];
         const double stv = vw[R][c] + a.dt * hh;
         const double vnc = vnv[c];
         double val;
@@ -1915,7 +2009,7 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   {
     const uint32_t R = (uint32_t)a.order;
     const char* ek = std::getenv("HJB_HO_KC");
-    a.kc = (ek && std::atoi(ek) == 1) ? 1u : 2u;
+    a.kc = (ek && std::atoi(ek) == 1 && a.lf == 0) ? 1u : 2u;  // LF: 2-cell pencils
     const uint32_t maxc = (uint32_t)ho4t_maxthreads(a.order, (int)a.kc) - 32;
     // tiles cover T1 x T2 rows x a T3-cell segment of axis 3; the box adds
     // R rows in i1, i2 and H3 = R rounded up to even cells on each side of
@@ -1991,20 +2085,24 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
 }
 
 namespace {
-template <class S, int R, int KC>
+template <class S, int R, int KC, int SCH = 0>
 void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ho4t<S, R, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_ho4t<S, R, KC, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr = true;
   }
-  k_ho4t<S, R, KC><<<a.blocks, a.threads, a.smem, s>>>(a);
+  k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
 template <class S, int R>
 void ho4t_launch(const Ho4dArgs& a, cudaStream_t s) {
-  if (a.kc == 1)
+  if (a.lf == 1)  // Lax-Friedrichs: 2-cell pencils (ho_solve forces kc = 2)
+    ho4t_launch_k<S, R, 2, 1>(a, s);
+  else if (a.lf == 2)
+    ho4t_launch_k<S, R, 2, 2>(a, s);
+  else if (a.kc == 1)
     ho4t_launch_k<S, R, 1>(a, s);
   else
     ho4t_launch_k<S, R, 2>(a, s);

@@ -10,6 +10,18 @@
 
 namespace hjb {
 
+// Lax-Friedrichs parameters of the 4D model shapes (one input term per
+// row): drift, input coefficients and bounds, dissipation (k_fast4d, k_ho4t)
+struct LfParams {
+  double galpha[4];     // global alpha per axis (scan_alpha)
+  int dr_off[4];        // drift table offset of each row (-1: constant drift)
+  double dr_const[4];
+  double ucoef[4];      // B coefficient of the row's control (shape U(d))
+  double dcoef[4];      // C coefficient of the row's disturbance (shape D(d))
+  double ulo[3], uhi[3], dlo[3], dhi[3];
+  int off_alpha[4];     // LF per-node alpha tables (-1: |drift|)
+};
+
 struct Fast4dArgs {
   CUtensorMap map0;  // V buffer 0 (padded), box = tile + halo rows
   CUtensorMap map1;  // V buffer 1
@@ -54,13 +66,7 @@ struct Fast4dArgs {
   // per plane (Godunov only)
   int pv;
   int pv_pt[4], pv_nt[4];
-  double galpha[4];
-  int dr_off[4];        // drift table offset of each row (-1: constant drift)
-  double dr_const[4];
-  double ucoef[4];      // B coefficient of the row's control (shape U(d))
-  double dcoef[4];      // C coefficient of the row's disturbance (shape D(d))
-  double ulo[3], uhi[3], dlo[3], dhi[3];
-  int off_alpha[4];     // LF per-node alpha tables (-1: |drift|)
+  LfParams lp;
 };
 
 // One ENO/TVD-RK stage over a padded 4D grid (k_ho4d, hjb_fast4d.cu): the
@@ -98,6 +104,10 @@ struct Ho4dArgs {
   uint32_t vbox_bytes, vslot_bytes, ring, smem, tma;
   uint32_t T3, H3, segs;  // axis-3 segment per tile (even), its box halo (even >= R), segments per row
   uint32_t kc;            // cells per thread along axis 3 (1 or 2)
+  // numerical Hamiltonian (k_ho4t): 0 Godunov, 1 / 2 Lax-Friedrichs per-node /
+  // global alpha, ghost faces replicated from the nearest interior face
+  int lf;
+  LfParams lp;
 };
 void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
 // fill mapv[] for the current buffers (k_ho4t); returns cudaErrorNotSupported

@@ -71,9 +71,16 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
   // 4D fast-path models (Godunov, constant bounds): padded layout + k_ho4d
   const char* fe = std::getenv("HJB_FAST");
-  const int shape = (fe && std::strcmp(fe, "0") == 0) || scheme_id(cfg) != kGodunov
-                        ? -1
-                        : fast4d_shape(g, m, kGodunov);
+  int shape = (fe && std::strcmp(fe, "0") == 0) ? -1 : fast4d_shape(g, m, scheme_id(cfg));
+  if (shape >= 0 && scheme_id(cfg) != kGodunov) {
+    // Lax-Friedrichs runs only in the TMA-staged kernel (k_ho4t)
+    Ho4dArgs t;
+    std::memset(&t, 0, sizeof t);
+    t.order = cfg->spatial_order > 3 ? 3 : (cfg->spatial_order < 1 ? 1 : cfg->spatial_order);
+    t.lf = 1;
+    ho4d_config(g, sm_count(ctx->device), t);
+    if (!t.tma) shape = -1;
+  }
   const uint64_t rows4 = g.nd == 4 ? static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2] : 0;
   const uint32_t n3p = g.nd == 4 ? (g.n[3] + 1) / 2 * 2 : 0;
   const size_t pbytes = shape >= 0 ? rows4 * n3p * sizeof(double) : bytes;
@@ -116,6 +123,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   std::memset(&h4, 0, sizeof h4);
   if (shape >= 0) {
     h4.order = a.order > 3 ? 3 : a.order;
+    fill_lf(m, scheme_id(cfg), galpha, h4.lf, h4.lp);
     ho4d_config(g, sm_count(ctx->device), h4);
     h4.tab = m.tab;
     for (int d = 0; d < 4; ++d) {

@@ -40,6 +40,7 @@ void fill_tables(const Prepared& p, Fast4dArgs& f);
 int scheme_of(const hjb_solve_config* cfg);
 // Lax-Friedrichs fields of Fast4dArgs (f.lf = 0 for Godunov)
 void fill_lf(const DevModel& m, int scheme, const double* galpha, Fast4dArgs& f);
+void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfParams& lp);
 // Device iteration loop: WHILE-conditional CUDA graph (or HJB_LOOP=poll);
 // `launch(stream, handle, use_handle)` enqueues one loop-mode sweep.
 using SweepLauncher = std::function<cudaError_t(cudaStream_t, cudaGraphConditionalHandle, int)>;
