@@ -152,10 +152,11 @@ __device__ __forceinline__ void gp_column(uint32_t dst, const double* src, uint3
 // zero) the IEEE division runs.
 __device__ __forceinline__ double gp_div(double s, double d, double y, bool fast_ok) {
   const double as = fabs(s);
-  if (fast_ok && as > 0x1p-900 && as < 0x1p900) {
+  if (fast_ok && as < 0x1p900 && (as > 0x1p-900 || as == 0.0)) {
     const double q = s * y;
     const double r = __fma_rn(-q, d, s);
-    return __fma_rn(r, y, q);
+    const double q2 = __fma_rn(r, y, q);
+    return as == 0.0 ? s : q2;  // 0 / d = 0 with the sign of s (d > 0)
   }
   return s / d;
 }
@@ -166,12 +167,14 @@ __device__ __forceinline__ double gp_div(double s, double d, double y, bool fast
 // gp.cpp:201), every row i > j subtracts L[i][j] v_j (gp.cpp:200) — the
 // reference's j order per row.  mean and the variance accumulate in the same
 // j order (gp.cpp:193-194, 204-205).  L streams through a shared-memory ring
-// in CHUNKS of GpRing::cols columns (one 1D bulk copy and one mbarrier wait
-// per chunk: a per-column wait costs more than the column's arithmetic);
-// thread 0 refills the chunk of `lag` chunks ago, released by every warp.
+// in CHUNKS of C columns (one 1D bulk copy and one mbarrier wait per chunk);
+// thread 0 refills the chunk released one chunk earlier.  The C steps of a
+// chunk are unrolled and branch-free: the columns are padded to a multiple of
+// C with identity steps (L column 0, diagonal 1, k* = alpha = 0, so s, mean
+// and the variance keep their bits), so a chunk never tests j < n.
 template <int RM>
 struct GpRing {
-  static constexpr int cols = RM >= 32 ? 4 : RM >= 16 ? 8 : 16;  // 32 KB chunks at most
+  static constexpr int cols = RM >= 32 ? 4 : 8;  // <= 32 KB chunks
   static constexpr int depth = 4;
   static constexpr int lag = 2;
 };
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(128) k_gp_ring(
   extern __shared__ __align__(16) unsigned char gsm[];
   constexpr int C = GpRing<RM>::cols, D = GpRing<RM>::depth, LAG = GpRing<RM>::lag;
   const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npad = (n + C - 1) / C * C;  // <= ldt
   double* ring = reinterpret_cast<double*>(gsm);  // D chunks of C columns
   double* sal = ring + D * C * ldt;
   double* sdg = sal + ldt;
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(128) k_gp_ring(
   uint64_t* empty = full + D;
   const int64_t p = static_cast<int64_t>(blockIdx.x) * W + w;
   const bool live = p < P;
-  const int nchunks = (n + C - 1) / C;
+  const int nchunks = npad / C;
   if (threadIdx.x == 0) {
     for (int k = 0; k < D; ++k) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gp_smem(full + k)));
@@ -203,62 +207,58 @@ __global__ void __launch_bounds__(128) k_gp_ring(
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    sal[i] = alpha[i];
-    sdg[i] = diag[i];
-    srd[i] = rdiag[i];
+  for (int i = threadIdx.x; i < ldt; i += blockDim.x) {
+    sal[i] = i < n ? alpha[i] : 0.0;
+    sdg[i] = i < n ? diag[i] : 1.0;
+    srd[i] = i < n ? rdiag[i] : 1.0;
   }
   for (int i = lane; i < ldt; i += 32) sks[i] = (live && i < n) ? kstar[p * n + i] : 0.0;
   __syncthreads();
-  // chunk c = columns [cC, cC + C) (the last one shorter), contiguous in lt
-  auto chunk_bytes = [&](int c) {
-    return static_cast<uint32_t>(min(C, n - c * C)) * static_cast<uint32_t>(ldt) * 8u;
-  };
+  const uint32_t chunkb = static_cast<uint32_t>(C) * static_cast<uint32_t>(ldt) * 8u;
   if (threadIdx.x == 0)
     for (int c = 0; c < D && c < nchunks; ++c)
-      gp_column(gp_smem(ring + c * C * ldt), lt + static_cast<size_t>(c) * C * ldt,
-                chunk_bytes(c), gp_smem(full + c));
+      gp_column(gp_smem(ring + c * C * ldt), lt + static_cast<size_t>(c) * C * ldt, chunkb,
+                gp_smem(full + c));
   const bool fok = fast_ok != 0;
   // rows >= n hold 0 and their L entries are 0 (ldt = 32 RM): no row masks
   double s[RM];
 #pragma unroll
   for (int k = 0; k < RM; ++k) s[k] = sks[lane + 32 * k];
   double mean = 0.0, var = signal_var;
-  const double* col = ring;
 #pragma unroll
   for (int kb = 0; kb < RM; ++kb) {
-    for (int lj = 0; lj < 32; ++lj) {
-      const int j = kb * 32 + lj;
-      if (j >= n) break;  // CTA-uniform
-      const int c = j / C, cj = j - c * C;
-      if (cj == 0) {  // chunk start: wait for its columns
-        gp_wait(gp_smem(full + c % D), static_cast<uint32_t>(c / D) & 1u);
-        col = ring + (c % D) * C * ldt + lane;
-      }
-      // every lane divides the owner's s_j (warp-uniform values and branch)
-      const double sj = __shfl_sync(0xffffffffu, s[kb], lj);
-      const double vj = gp_div(sj, sdg[j], srd[j], fok);
-      const double* cc = col + cj * ldt;
-      {
-        const double upd = s[kb] - cc[32 * kb] * vj;
-        s[kb] = lane > lj ? upd : (lane == lj ? vj : s[kb]);
-      }
+    for (int cb = 0; cb < 32 / C; ++cb) {
+      const int j0 = kb * 32 + cb * C;
+      if (j0 >= npad) break;  // CTA-uniform, once per chunk
+      const int c = j0 / C;
+      gp_wait(gp_smem(full + c % D), static_cast<uint32_t>(c / D) & 1u);
+      const double* col = ring + (c % D) * C * ldt + lane;
 #pragma unroll
-      for (int k = kb + 1; k < RM; ++k) s[k] = s[k] - cc[32 * k] * vj;
-      mean += sks[j] * sal[j];
-      var -= vj * vj;
-      if (cj == C - 1 || j == n - 1) {  // chunk done: release, refill an old one
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gp_smem(empty + c % D))
-                       : "memory");
-        const int cr = c - LAG + 1;  // its slot was released LAG - 1 chunks ago
-        if (threadIdx.x == 0 && cr >= 0 && cr + D < nchunks) {
-          gp_wait(gp_smem(empty + cr % D), static_cast<uint32_t>(cr / D) & 1u);
-          gp_column(gp_smem(ring + (cr % D) * C * ldt),
-                    lt + static_cast<size_t>(cr + D) * C * ldt, chunk_bytes(cr + D),
-                    gp_smem(full + cr % D));
+      for (int u = 0; u < C; ++u) {
+        const int lj = cb * C + u, j = j0 + u;
+        // every lane divides the owner's s_j (warp-uniform values and branch)
+        const double sj = __shfl_sync(0xffffffffu, s[kb], lj);
+        const double vj = gp_div(sj, sdg[j], srd[j], fok);
+        const double* cc = col + u * ldt;
+        {
+          const double upd = s[kb] - cc[32 * kb] * vj;
+          s[kb] = lane > lj ? upd : (lane == lj ? vj : s[kb]);
         }
+#pragma unroll
+        for (int k = kb + 1; k < RM; ++k) s[k] = s[k] - cc[32 * k] * vj;
+        mean += sks[j] * sal[j];
+        var -= vj * vj;
+      }
+      // chunk done: release it, refill the one released a chunk earlier
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gp_smem(empty + c % D))
+                     : "memory");
+      const int cr = c - LAG + 1;
+      if (threadIdx.x == 0 && cr >= 0 && cr + D < nchunks) {
+        gp_wait(gp_smem(empty + cr % D), static_cast<uint32_t>(cr / D) & 1u);
+        gp_column(gp_smem(ring + (cr % D) * C * ldt), lt + static_cast<size_t>(cr + D) * C * ldt,
+                  chunkb, gp_smem(full + cr % D));
       }
     }
   }
@@ -277,15 +277,15 @@ __global__ void __launch_bounds__(128) k_gp_ring(
 
 // row-major chol -> column-major strictly-lower part (leading dim ldt,
 // zero-padded) + diagonal
-__global__ void k_gp_prep(const double* __restrict__ chol, int n, int ldt,
+__global__ void k_gp_prep(const double* __restrict__ chol, int n, int ncols, int ldt,
                           double* __restrict__ lt, double* __restrict__ diag,
                           double* __restrict__ rdiag) {
-  const int64_t total = static_cast<int64_t>(n) * ldt;
+  const int64_t total = static_cast<int64_t>(ncols) * ldt;  // columns >= n: zero
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = e / ldt, i = e - j * ldt;  // lt[j*ldt + i] = L[i][j]
-    lt[e] = (i > j && i < n) ? chol[i * n + j] : 0.0;
-    if (i == j) {
+    lt[e] = (i > j && i < n && j < n) ? chol[i * n + j] : 0.0;
+    if (i == j && i < n) {
       diag[i] = chol[i * n + i];
       rdiag[i] = 1.0 / chol[i * n + i];  // IEEE (-prec-div=true): RN(1/d)
     }
@@ -432,7 +432,8 @@ int posterior(hjb_context* ctx, const hjb_gp_model& m, int64_t P, const double* 
   // n rounded to 16 bytes
   const int rm = n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : n <= 256 ? 8 : n <= 512 ? 16 : 32;
   const int ldt = static_cast<int>(n <= 1024 ? 32 * rm : (n + 1) / 2 * 2);
-  const size_t ntl = static_cast<size_t>(n) * ldt;
+  const int ncols = static_cast<int>((n + 7) / 8 * 8);  // chunk padding (zero columns)
+  const size_t ntl = static_cast<size_t>(ncols) * ldt;
   auto al = [](size_t x) { return (x + 31) / 32 * 32; };  // 256-byte sub-buffers
   CUDA_TRY(ctx->gpa.ensure(ks.size() * sizeof(double)));
   CUDA_TRY(ctx->gpb.ensure((al(nn) + al(ntl) + 3 * al(n)) * sizeof(double)));
@@ -450,7 +451,7 @@ int posterior(hjb_context* ctx, const hjb_gp_model& m, int64_t P, const double* 
                            ctx->stream));
   const int sms = sm_count(ctx->device);
   k_gp_prep<<<static_cast<unsigned>(std::min<size_t>((ntl + 255) / 256, 4u * sms)), 256, 0,
-              ctx->stream>>>(draw, static_cast<int>(n), ldt, dlt, ddg, drd);
+              ctx->stream>>>(draw, static_cast<int>(n), ncols, ldt, dlt, ddg, drd);
   CUDA_TRY(cudaGetLastError());
   ++ctx->launches;
   // Markstein division is exact while the diagonal stays in a safe range
