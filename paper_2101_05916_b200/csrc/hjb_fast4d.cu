@@ -471,11 +471,39 @@ __global__ void __launch_bounds__(MAXT, 1)
     if (lane == 0) {
       uint32_t pos = 0;  // ring position (slot = pos % kRing, use = pos / kRing)
       uint32_t w = blockIdx.x;
+      // balanced schedule: this CTA's unit range (tile-major tile-planes)
+      const uint32_t np = a.cend - a.cbeg;
+      const uint64_t units = static_cast<uint64_t>(a.tiles1) * a.tiles2 * np;
+      uint64_t u0 = units * blockIdx.x / gridDim.x;
+      const uint64_t u1 = units * (blockIdx.x + 1) / gridDim.x;
       for (;;) {
-        // next item id fetched ahead (its latency hides behind this item)
-        uint32_t wn = kEndItem;
-        if (w < nitems) wn = gridDim.x + atomicAdd(&a.st->work_next, 1u);
-        if (w >= nitems) {
+        uint32_t t1, t2, c0, c1, wn = kEndItem;
+        bool end;
+        if (a.bal) {
+          end = u0 >= u1;
+          if (!end) {
+            const uint32_t tix = static_cast<uint32_t>(u0 / np);
+            const uint32_t q0 = static_cast<uint32_t>(u0 - static_cast<uint64_t>(tix) * np);
+            const uint64_t qe = q0 + (u1 - u0);
+            const uint32_t q1 = qe < np ? static_cast<uint32_t>(qe) : np;
+            t1 = tix / a.tiles2;
+            t2 = tix - t1 * a.tiles2;
+            c0 = a.cbeg + q0;
+            c1 = a.cbeg + q1;
+            u0 += q1 - q0;
+          }
+        } else {
+          // next item id fetched ahead (its latency hides behind this item)
+          if (w < nitems) wn = gridDim.x + atomicAdd(&a.st->work_next, 1u);
+          end = w >= nitems;
+          if (!end) {
+            uint32_t chunk;
+            item_tile(a, w, t1, t2, chunk);
+            c0 = a.cbeg + chunk * a.L;
+            c1 = min(c0 + a.L, a.cend);
+          }
+        }
+        if (end) {
           const uint32_t sl = pos % kRing, use = pos / kRing;
           mbar_wait(bars + (kRing + sl) * 8, (use & 1u) ^ 1u);
           asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hdr0 + sl * 8), "r"(kEndItem),
@@ -484,19 +512,15 @@ __global__ void __launch_bounds__(MAXT, 1)
           mbar_arrive(bars + sl * 8);
           break;
         }
-        uint32_t t1, t2, chunk;
-        item_tile(a, w, t1, t2, chunk);
-        const uint32_t c0 = a.cbeg + chunk * a.L;
-        const uint32_t c1 = min(c0 + a.L, a.cend);
         const uint32_t pbeg = c0 > 0 ? c0 - 1 : 0;
         const uint32_t pend = c1 < n0 ? c1 : n0 - 1;
         const int base1 = (int)(t1 * T1), base2 = (int)(t2 * T2);
         for (uint32_t p = pbeg; p <= pend; ++p, ++pos) {
           const uint32_t sl = pos % kRing, use = pos / kRing;
           mbar_wait(bars + (kRing + sl) * 8, (use & 1u) ^ 1u);
-          if (p == pbeg)
+          if (p == pbeg)  // item header: tile, plane range (n0 < 65536)
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hdr0 + sl * 8),
-                         "r"(t1 * a.tiles2 + t2), "r"(chunk)
+                         "r"(t1 * a.tiles2 + t2), "r"(c0 | (c1 << 16))
                          : "memory");
           const bool has_c = p >= c0 && p < c1;
           mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes + (has_c ? a.cbox_bytes : 0u));
@@ -536,12 +560,12 @@ __global__ void __launch_bounds__(MAXT, 1)
     for (;;) {
       uint32_t sl = pos % kRing, ph = (pos / kRing) & 1u;
       mbar_wait(bars + sl * 8, ph);
-      uint32_t tix, chunk;
-      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tix), "=r"(chunk) : "r"(hdr0 + sl * 8));
+      uint32_t tix, crange;
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tix), "=r"(crange) : "r"(hdr0 + sl * 8));
       if (tix == kEndItem) break;
       const uint32_t t1 = tix / a.tiles2, t2 = tix - t1 * a.tiles2;
-      const uint32_t c0 = a.cbeg + chunk * a.L;
-      const uint32_t c1 = min(c0 + a.L, a.cend);
+      const uint32_t c0 = crange & 0xffffu;
+      const uint32_t c1 = crange >> 16;
       const uint32_t pend = c1 < n0 ? c1 : n0 - 1;
       const uint32_t i1 = t1 * T1 + r1;
       const uint32_t i2 = t2 * T2 + r2;
@@ -1903,6 +1927,12 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   a.nchunks = (span + L - 1) / L;
   a.items = tiles * a.nchunks;
   a.blocks = std::min<uint32_t>(a.items, static_cast<uint32_t>(sms));
+  // static balanced schedule when tiles are fewer than SMs (51^4: 130 tiles,
+  // 39.3 vs 41.3 us per sweep); with more tiles the dynamic items keep
+  // neighbouring tiles in flight together (71^4: 121 vs 145 us static)
+  const char* eb = std::getenv("HJB_BALANCE");
+  a.bal = eb ? (std::strcmp(eb, "1") == 0 ? 1u : 0u) : (tiles < static_cast<uint32_t>(sms) ? 1u : 0u);
+  if (a.bal) a.blocks = std::min<uint32_t>(static_cast<uint32_t>(sms), tiles * span);
 }
 
 template <class S, int K, int MAXT, int SCH = 0, bool PV = false>

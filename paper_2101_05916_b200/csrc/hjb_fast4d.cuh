@@ -33,6 +33,10 @@ struct Fast4dArgs {
   uint32_t kcells;      // cells per thread along the contiguous axis (2 or 4)
   uint32_t maxthreads;  // CTA thread bound of the variant: (2, 576), (2, 448), (4, 384)
   uint32_t T1, T2, tiles1, tiles2, L, nchunks, items, blocks, threads, consumers, smem;
+  // bal = 1: static balanced schedule — CTA b marches the tile-planes
+  // [b U / G, (b+1) U / G) of the U = tiles x planes units (at most a few
+  // tile pieces each); 0: dynamic items (tile x chunk) off the work counter
+  uint32_t bal;
   uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
   const double* tab;    // slope tables (staged into shared memory per CTA)
   uint32_t tab_len;     // doubles in tab

@@ -357,3 +357,22 @@ def test_fast4d_axis0_varying_bounds(gpu_ctx, oracle, monkeypatch, case, broken)
     monkeypatch.setenv("HJB_FAST", "0")
     gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
     assert same(gen.value.values(), got.value.values())
+
+
+@pytest.mark.parametrize("balance", ["0", "1"], ids=["dynamic_items", "static_balanced"])
+@pytest.mark.parametrize("dims", [(17, 21, 19, 23), (31, 9, 7, 12)])
+def test_fast4d_schedules(gpu_ctx, oracle, monkeypatch, balance, dims):
+    """Both CTA schedules of k_fast4d (dynamic tile x chunk items; static
+    balanced tile-plane ranges, pieces spanning tiles) against the oracle."""
+    monkeypatch.setenv("HJB_BALANCE", balance)
+    n0, n1, n2, n3 = dims
+    g = hj.Grid([(-5.0, 5.0, n0), (-2.0, 2.0, n1), (-0.35, 0.35, n2), (-1.5, 1.5, n3)])
+    model = configs.planar_model()
+    db = hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    cfg = hj.SolveConfig(tolerance=1e-5, max_iters=30)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
