@@ -1778,7 +1778,7 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
 }
 
 int fast4d_shape_pv(const DevGrid& g, const DevModel& m) {
-  if (g.nd != 4) return -1;
+  if (g.nd != 4 || g.n[0] > 65535) return -1;
   if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   bool lin[4];
@@ -1810,6 +1810,7 @@ int fast4d_shape_pv(const DevGrid& g, const DevModel& m) {
 
 static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
   if (g.nd != 4 || m.per_node) return -1;
+  if (g.n[0] > 65535) return -1;  // item headers pack the plane range in 16 bits
   if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   bool lin[4];
