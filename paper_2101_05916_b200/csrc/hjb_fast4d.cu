@@ -1724,11 +1724,390 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   loop_epilogue(st, a.handle, a.use_handle);
 }
 
+// ---- ENO3 Godunov stage with face-shared selections (k_eno3g) ----
+//
+// The ENO3 choice for D+ of cell k and for D- of cell k+1 is made on the
+// same five faces a(k-2) .. a(k+2) with the same comparisons (Osher-Shu: both
+// stencils start at face k); only the final weights differ.  eno3_face makes
+// that choice once per face and returns both one-sided derivatives, each
+// with exactly the operations eno_faces<3> applies per cell (so the results
+// are bitwise the same).  k_eno3g uses it along the axis-0 march (D- of the
+// next plane is carried in a register) and inside the 2-cell pencil (3
+// choices instead of 4); axes 1 and 2 keep the per-cell form.
+//
+// Ghost layout: the stage buffers carry gh = 3 replicated ghost rows on each
+// side of axes 1 and 2 and g3 = 4 ghost cells on each side of axis 3 (rows
+// stay 16-byte aligned), [n0][n1 + 6][n2 + 6][n3p + 8].  Every TMA box is
+// then inside the tensor and its out-of-grid cells hold the nearest edge
+// value, so the Godunov ghost faces come out as (V - V) * inv == +0, the
+// value the masked form writes, with no masks or selects on the consumers.
+// The kernel keeps the ghosts current: threads owning an edge cell also
+// store it into the ghost cells across that edge (face ghosts only: no
+// stencil reads a corner).  Axis 0 loads clamped planes instead.
+__device__ __forceinline__ void eno3_face(double e0, double e1, double e2, double e3, double e4,
+                                          double& dp_left, double& dm_right) {
+  const double g0 = e1 - e0, g1 = e2 - e1, g2 = e3 - e2, g3 = e4 - e3;
+  const double h0 = g1 - g0, h1 = g2 - g1, h2 = g3 - g2;
+  const bool left = fabs(g1) <= fabs(g2);
+  const double c2 = left ? g1 : g2;
+  const double c3 = left ? minabs_d(h0, h1) : minabs_d(h1, h2);
+  const double hc = 0.5 * c2;  // -0.5 * c2 == -(0.5 * c2) exactly
+  dp_left = (e2 - hc) + (left ? kHoSixthNeg : kHoThird) * c3;
+  dm_right = (e2 + hc) + (left ? kHoThird : kHoSixthNeg) * c3;
+}
+
+#ifndef HJB_ENO3G_THREADS
+#define HJB_ENO3G_THREADS 512
+#endif
+constexpr int kEno3gThreads = HJB_ENO3G_THREADS;
+
+// 16-byte read-only load kept in program order (volatile): the compiler
+// would otherwise sink it next to its use at the end of the step
+__device__ __forceinline__ void ldg2_v(const double* p, double* o) {
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(o[0]), "=d"(o[1]) : "l"(p));
+}
+
+template <class S>
+__global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constant__ Ho4dArgs a) {
+  constexpr int R = 3, kK = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  LoopState* st = a.st;
+  if (a.loop != 0 && *(volatile int*)&st->done) return;
+  const long long it = a.loop != 0 ? st->iter : 0;
+  const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
+  double* outp = (it & 1) ? a.buf0 : a.buf1;
+  const double* __restrict__ vs =
+      a.loop == 0 ? a.xsrc : (a.src_sel == 0 ? vn : (a.src_sel == 1 ? a.stage1 : a.stage2));
+  const int msel = a.loop == 0 ? 0 : (a.src_sel == 0 ? (int)(it & 1) : (a.src_sel == 1 ? 2 : 3));
+  double* dst =
+      a.loop == 0 ? a.xdst : (a.dst_sel == 0 ? outp : (a.dst_sel == 1 ? a.stage1 : a.stage2));
+  const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
+  const uint32_t J = a.T3 / kK;
+  const uint32_t B3 = a.T3 + 2 * a.H3;
+  uint32_t b = blockIdx.x;
+  const uint32_t chunk = b % a.nchunks;
+  b /= a.nchunks;
+  const uint32_t seg = b % a.segs;
+  b /= a.segs;
+  const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
+  const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2, base3 = seg * a.T3;
+  const uint32_t c0 = a.cbeg + chunk * a.L;
+  const uint32_t c1 = min(c0 + a.L, a.cend);
+  const uint32_t ncons = a.threads - 32;
+  const uint32_t nwarps_c = ncons >> 5;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ring = a.ring;
+  const uint32_t smem0 = smem_u32(smem_raw);
+  const uint32_t bars = smem0 + ring * a.vslot_bytes;  // full[ring], empty[ring]
+  uint64_t* bar_ptr = reinterpret_cast<uint64_t*>(smem_raw + ring * a.vslot_bytes);
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < ring; ++k) {
+      mbar_init(bar_ptr + k, 1);
+      mbar_init(bar_ptr + ring + k, nwarps_c);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double mdv = 0.0;
+  if (threadIdx.x >= ncons) {
+    // producer: the box of plane q is tile + (R, R, H3) halo, whose ghost-
+    // layout origin is (base1, base2, base3) (gh == R, g3 == H3)
+    if (lane == 0)
+      for (uint32_t q = 0; c0 + q < c1; ++q) {
+        const uint32_t sl = q % ring, use = q / ring;
+        mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
+        mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes);
+        tma_load4(smem0 + sl * a.vslot_bytes, &a.mapv[msel], (int)base3, (int)base2, (int)base1,
+                  (int)(c0 + q), bars + sl * 8);
+      }
+  } else {
+    const uint32_t t = threadIdx.x;
+    const uint32_t rr = t / J, j = t - rr * J;
+    const bool in_tile = rr < a.T1 * a.T2;
+    const uint32_t r = in_tile ? rr : 0u;
+    const uint32_t r1 = r / a.T2, r2 = r - r1 * a.T2;
+    const uint32_t i1 = base1 + r1, i2 = base2 + r2;
+    const uint32_t i3u = base3 + kK * j;
+    const bool active = in_tile && i1 < n1 && i2 < n2 && i3u < n3p;
+    const uint32_t i3 = i3u < n3p ? i3u : n3p - kK;  // clamped for addressing
+    const uint32_t ci1 = active ? i1 : 0u, ci2 = active ? i2 : 0u;
+    const uint64_t s2 = n3p + 2 * a.g3, s1 = (uint64_t)(n2 + 2 * a.gh) * s2,
+                   s0 = (uint64_t)(n1 + 2 * a.gh) * s1;
+    const uint64_t rowo = (uint64_t)(ci1 + a.gh) * s1 + (uint64_t)(ci2 + a.gh) * s2 + i3 + a.g3;
+    const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
+    const uint32_t W2 = a.T2 + 2 * R;
+    const uint32_t rowb = B3 * 8u;
+    const uint32_t own = (((r1 + R) * W2 + (r2 + R)) * B3 + (i3 - base3 + a.H3)) * 8u;
+
+    // loop-invariant flux data (as k_ho4t, Godunov)
+    double pos_[4][kK], neg_[4][kK];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        if (c > 0 && !per_cell) {
+          pos_[d][c] = pos_[d][0];
+          neg_[d][c] = neg_[d][0];
+        } else {
+          const uint32_t ka = pick<S>(S::A(d), ci1, ci2, min(i3 + c, n3 - 1));
+          if (S::B(d) < 0) {
+            pos_[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
+            neg_[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
+          } else {
+            const uint32_t kb = pick<S>(S::B(d), ci1, ci2, min(i3 + c, n3 - 1));
+            const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
+            pos_[d][c] = dr;
+            neg_[d][c] = dr;
+          }
+        }
+      }
+    }
+    RowShape shp[4][kK];
+    bool up[4][kK];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        up[d][c] = sign_clear(pos_[d][c]);
+        if (S::LIN(d)) continue;
+        shp[d][c] = (c > 0 && !per_cell) ? shp[d][0] : row_shape(pos_[d][c], neg_[d][c]);
+      }
+    }
+    auto flux = [&](auto dc, int c, double dm, double dp) -> double {
+      constexpr int d = decltype(dc)::value;
+      if (S::LIN(d)) return pos_[d][c] * (up[d][c] ? dp : dm);
+      const double ka = pair_kink(shp[d][c].L, dm, sign_bit(dm));
+      const double kb = pair_kink(shp[d][c].R, dp, sign_bit(dp));
+      return shape_pick(shp[d][c], ka, kb);
+    };
+
+    // axis-0 window: faces a(i0-2) .. a(i0+2), V(i0+3), and D- of plane i0
+    // (chosen at face a(i0-1) in the previous step); planes clamped to the grid
+    auto plane_at = [&](int p) -> const double* {
+      p = p < 0 ? 0 : (p > (int)n0 - 1 ? (int)n0 - 1 : p);
+      return vs + (uint64_t)p * s0 + rowo;
+    };
+    double F[5][kK], vlast[kK], dmc[kK];
+    {
+      double w[7][kK];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) ldg_k<kK>(plane_at((int)c0 - 3 + q), w[q]);
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        double f6[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) f6[q] = (w[q + 1][c] - w[q][c]) * inv0;
+        double unused;
+        eno3_face(f6[0], f6[1], f6[2], f6[3], f6[4], unused, dmc[c]);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) F[q][c] = f6[q + 1];
+        vlast[c] = w[6][c];
+      }
+    }
+    const bool need_vn = a.kind != 0 || a.final_stage;
+    // ghost stores of this thread's pencil (loop invariant)
+    const bool odd_pad = i3 + 1 == n3;  // the pencil's second cell is axis-3 padding
+    const bool gl3 = i3 == 0, gh3 = i3 + 2 >= n3;
+    const bool gl1 = i1 == 0, gh1 = i1 + 1 == n1, gl2 = i2 == 0, gh2 = i2 + 1 == n2;
+    const bool any_ghost = active && (gl3 || gh3 || gl1 || gh1 || gl2 || gh2);
+    uint32_t sl = 0, ph = 0;
+    for (uint32_t i0 = c0; i0 < c1; ++i0) {
+      const uint64_t po = (uint64_t)i0 * s0;
+      double ccv[kK], vnv[kK], vnx[kK];
+      ldg2_v(a.c + po + rowo, ccv);
+      if (need_vn) {
+        ldg2_v(vn + po + rowo, vnv);
+      } else {
+        vnv[0] = vnv[1] = 0.0;
+      }
+      ldg2_v(plane_at((int)i0 + 4), vnx);
+      const uint32_t slot = smem0 + sl * a.vslot_bytes;
+      mbar_wait_nc(bars + sl * 8, ph);
+      // own row V(i3-3) .. V(i3+4)
+      double rv[8];
+      rv[0] = lds1(slot + own - 24);
+      {
+        const double2 x = lds2(slot + own - 16), y = lds2(slot + own), z = lds2(slot + own + 16);
+        rv[1] = x.x;
+        rv[2] = x.y;
+        rv[3] = y.x;
+        rv[4] = y.y;
+        rv[5] = z.x;
+        rv[6] = z.y;
+      }
+      rv[7] = lds1(slot + own + 32);
+      double hh[kK];
+      // axis 0: choice at face a(i0) -> D+ of i0 and D- of i0+1
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        double dp, dmn;
+        eno3_face(F[0][c], F[1][c], F[2][c], F[3][c], F[4][c], dp, dmn);
+        hh[c] = flux(std::integral_constant<int, 0>{}, c, dmc[c], dp);
+        dmc[c] = dmn;
+      }
+      // axes 1 and 2: per cell, six faces from the box
+#pragma unroll
+      for (int ax = 1; ax <= 2; ++ax) {
+        const int step = ax == 1 ? (int)(W2 * rowb) : (int)rowb;
+        const double inv = ax == 1 ? inv1 : inv2;
+        double nv[7][kK];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+          if (q == 3) {
+            nv[q][0] = rv[3];
+            nv[q][1] = rv[4];
+          } else {
+            lds_k<kK>(slot + own + (q - 3) * step, nv[q]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kK; ++c) {
+          double A[6];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) A[q] = (nv[q + 1][c] - nv[q][c]) * inv;
+          double dm, dp;
+          eno_faces<R>(A, dm, dp);
+          const double h = ax == 1 ? flux(std::integral_constant<int, 1>{}, c, dm, dp)
+                                   : flux(std::integral_constant<int, 2>{}, c, dm, dp);
+          hh[c] = hh[c] + h;
+        }
+      }
+      // axis 3: faces a(i3-3) .. a(i3+3); choices at faces i3-1, i3, i3+1
+      {
+        double f[7];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) f[q] = (rv[q + 1] - rv[q]) * inv3;
+        double x0, dm0, dp0, dm1, dp1, x1;
+        eno3_face(f[0], f[1], f[2], f[3], f[4], x0, dm0);
+        eno3_face(f[1], f[2], f[3], f[4], f[5], dp0, dm1);
+        eno3_face(f[2], f[3], f[4], f[5], f[6], dp1, x1);
+        hh[0] = hh[0] + flux(std::integral_constant<int, 3>{}, 0, dm0, dp0);
+        hh[1] = hh[1] + flux(std::integral_constant<int, 3>{}, 1, dm1, dp1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bars + (ring + sl) * 8);
+      if (++sl == ring) {
+        sl = 0;
+        ph ^= 1u;
+      }
+      double out[kK];
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        const double own_v = c == 0 ? rv[3] : rv[4];
+        const double stv = own_v + a.dt * hh[c];
+        const double vnc = need_vn ? vnv[c] : own_v;
+        double val;
+        switch (a.kind) {
+          case 1: val = 0.5 * vnc + 0.5 * stv; break;
+          case 2: val = 0.75 * vnc + 0.25 * stv; break;
+          case 3: val = kHoThird * vnc + kHoTwoThirds * stv; break;
+          default: val = stv; break;
+        }
+        out[c] = val > ccv[c] ? val : ccv[c];
+        const double dv = fabs(out[c] - vnc);
+        if (active && i3 + c < n3 && dv > mdv) mdv = dv;
+      }
+      if (active) {
+        // an odd n3's padding cell is the first axis-3 ghost: it holds V(n3-1)
+        const double2 o = make_double2(out[0], odd_pad ? out[0] : out[1]);
+        double* p = dst + po + rowo;
+        *reinterpret_cast<double2*>(p) = o;
+        if (any_ghost) {
+          if (gl3) {
+            const double2 e = make_double2(o.x, o.x);
+            *reinterpret_cast<double2*>(p - 2) = e;
+            *reinterpret_cast<double2*>(p - 4) = e;
+          }
+          if (gh3) {
+            const double2 e = make_double2(o.y, o.y);
+            *reinterpret_cast<double2*>(p + 2) = e;
+            *reinterpret_cast<double2*>(p + 4) = e;
+          }
+#pragma unroll
+          for (int k = 1; k <= R; ++k) {
+            if (gl1) *reinterpret_cast<double2*>(p - k * s1) = o;
+            if (gh1) *reinterpret_cast<double2*>(p + k * s1) = o;
+            if (gl2) *reinterpret_cast<double2*>(p - k * s2) = o;
+            if (gh2) *reinterpret_cast<double2*>(p + k * s2) = o;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) F[q][c] = F[q + 1][c];
+        F[4][c] = (vnx[c] - vlast[c]) * inv0;
+        vlast[c] = vnx[c];
+      }
+    }
+  }
+  if (!a.final_stage) return;
+  unsigned long long mbits = (unsigned long long)__double_as_longlong(mdv);
+  __shared__ unsigned long long part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+  if (lane == 0) part[warp] = mbits;
+  __syncthreads();
+  if (warp != 0) return;
+  mbits = lane < (blockDim.x >> 5) ? part[lane] : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+  if (lane != 0) return;
+  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (a.loop != 1) return;
+  __threadfence();
+  const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  loop_epilogue(st, a.handle, a.use_handle);
+}
+
 // Sharded loop: after the residual all-reduce, one thread applies the
 // solve() loop logic to the global max|dV| (every rank decides identically).
 __global__ void k_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
   if (st->done) return;
   loop_epilogue(st, handle, use_handle);
+}
+
+// reference layout <-> ghost layout of the ENO3 stage buffers: every cell of
+// [planes][n1 + 2gh][n2 + 2gh][n3p + 2g3] takes the reference value at the
+// clamped coordinates (ghosts and axis-3 padding replicate the edge)
+__global__ void k_pad4g(const double* __restrict__ in, double* __restrict__ out, uint32_t planes,
+                        uint32_t n1, uint32_t n2, uint32_t n3, uint32_t d1, uint32_t d2,
+                        uint32_t d3, uint32_t gh, uint32_t g3) {
+  const uint64_t total = (uint64_t)planes * d1 * d2 * d3;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t q = k;
+    const int x3 = (int)(q % d3) - (int)g3;
+    q /= d3;
+    const int x2 = (int)(q % d2) - (int)gh;
+    q /= d2;
+    const int x1 = (int)(q % d1) - (int)gh;
+    const uint64_t x0 = q / d1;
+    const uint32_t c3 = (uint32_t)min(max(x3, 0), (int)n3 - 1);
+    const uint32_t c2 = (uint32_t)min(max(x2, 0), (int)n2 - 1);
+    const uint32_t c1 = (uint32_t)min(max(x1, 0), (int)n1 - 1);
+    out[k] = in[((x0 * n1 + c1) * n2 + c2) * n3 + c3];
+  }
+}
+__global__ void k_unpad4g(const double* __restrict__ in, double* __restrict__ out, uint32_t planes,
+                          uint32_t n1, uint32_t n2, uint32_t n3, uint32_t d1, uint32_t d2,
+                          uint32_t d3, uint32_t gh, uint32_t g3) {
+  const uint64_t total = (uint64_t)planes * n1 * n2 * n3;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t q = k;
+    const uint32_t x3 = (uint32_t)(q % n3);
+    q /= n3;
+    const uint32_t x2 = (uint32_t)(q % n2);
+    q /= n2;
+    const uint32_t x1 = (uint32_t)(q % n1);
+    const uint64_t x0 = q / n1;
+    out[k] = in[((x0 * d1 + x1 + gh) * d2 + x2 + gh) * d3 + x3 + g3];
+  }
 }
 
 // padded <-> reference layout
@@ -2041,7 +2420,11 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
     const uint32_t R = (uint32_t)a.order;
     const char* ek = std::getenv("HJB_HO_KC");
     a.kc = (ek && std::atoi(ek) == 1 && a.lf == 0) ? 1u : 2u;  // LF: 2-cell pencils
-    const uint32_t maxc = (uint32_t)ho4t_maxthreads(a.order, (int)a.kc) - 32;
+    const char* eg = std::getenv("HJB_HO_ENO3G");
+    a.eno3g = (R == 3 && a.lf == 0 && a.kc == 2 && !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
+    const uint32_t nbar = 2u;  // mbarriers per ring slot
+    const uint32_t maxc =
+        (uint32_t)(a.eno3g ? kEno3gThreads : ho4t_maxthreads(a.order, (int)a.kc)) - 32;
     // tiles cover T1 x T2 rows x a T3-cell segment of axis 3; the box adds
     // R rows in i1, i2 and H3 = R rounded up to even cells on each side of
     // the segment (16-byte aligned pencils).  Minimise the grid traffic:
@@ -2067,7 +2450,7 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
           const size_t vb = (size_t)(t1 + 2 * R) * (t2 + 2 * R) * B3 * 8;
           const size_t slot = (vb + 127) / 128 * 128;
           uint32_t ring = want_ring;
-          while (ring >= 2 && ring * slot + 2 * ring * 8 > 200 * 1024) --ring;
+          while (ring >= 2 && ring * slot + nbar * ring * 8 > 200 * 1024) --ring;
           if (ring < 2) continue;
           const double useful = double(g.n[1]) * g.n[2] * a.n3p;
           const double boxes = double((g.n[1] + t1 - 1) / t1) * ((g.n[2] + t2 - 1) / t2) * segs;
@@ -2095,13 +2478,18 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
       a.ring = bring;
       a.vbox_bytes = (bt1 + 2 * R) * (bt2 + 2 * R) * (bt3 + 2 * H3) * 8;
       a.vslot_bytes = (a.vbox_bytes + 127) / 128 * 128;
-      a.smem = bring * a.vslot_bytes + 2 * bring * 8;
+      a.smem = bring * a.vslot_bytes + nbar * bring * 8;
+      if (a.eno3g) {  // ghost layout (k_eno3g)
+        a.gh = R;
+        a.g3 = H3;
+      }
       if (std::getenv("HJB_HO_VERBOSE"))
         std::fprintf(stderr, "ho4t R=%u kc=%u tile %ux%ux%u (box %ux%ux%u) ring %u threads %u smem %u\n",
                      R, a.kc, bt1, bt2, bt3, bt1 + 2 * R, bt2 + 2 * R, bt3 + 2 * H3, bring,
                      a.threads, a.smem);
     }
   }
+  if (!a.tma) a.eno3g = 0;
   const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
   if (a.cend == 0) {
     a.cbeg = 0;
@@ -2145,7 +2533,19 @@ cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
     switch (a.order) {
       case 1: ho4t_launch<S, 1>(a, s); break;
       case 2: ho4t_launch<S, 2>(a, s); break;
-      default: ho4t_launch<S, 3>(a, s); break;
+      default:
+        if (a.eno3g) {
+          static bool attr = false;
+          if (!attr) {
+            cudaFuncSetAttribute(k_eno3g<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024);
+            attr = true;
+          }
+          k_eno3g<S><<<a.blocks, a.threads, a.smem, s>>>(a);
+        } else {
+          ho4t_launch<S, 3>(a, s);
+        }
+        break;
     }
     return cudaGetLastError();
   }
@@ -2169,9 +2569,9 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a) {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const uint32_t R = (uint32_t)a.order;
-  const cuuint64_t dims[4] = {a.n3p, a.n[2], a.n[1], a.n[0]};
-  const cuuint64_t strides[3] = {(cuuint64_t)a.n3p * 8, (cuuint64_t)a.n3p * a.n[2] * 8,
-                                 (cuuint64_t)a.n3p * a.n[2] * a.n[1] * 8};
+  const cuuint64_t d3 = a.n3p + 2 * a.g3, d2 = a.n[2] + 2 * a.gh, d1 = a.n[1] + 2 * a.gh;
+  const cuuint64_t dims[4] = {d3, d2, d1, a.n[0]};
+  const cuuint64_t strides[3] = {d3 * 8, d3 * d2 * 8, d3 * d2 * d1 * 8};
   const cuuint32_t box[4] = {a.T3 + 2 * a.H3, a.T2 + 2 * R, a.T1 + 2 * R, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   double* ptrs[4] = {a.buf0, a.buf1, a.stage1, a.stage2};
@@ -2249,6 +2649,30 @@ cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const do
 cudaError_t launch_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
                             cudaStream_t s) {
   k_epilogue<<<1, 1, 0, s>>>(st, handle, use_handle);
+  return cudaGetLastError();
+}
+
+uint64_t ho4d_plane(const Ho4dArgs& a) {
+  return (uint64_t)(a.n[1] + 2 * a.gh) * (a.n[2] + 2 * a.gh) * (a.n3p + 2 * a.g3);
+}
+
+cudaError_t ho4d_pad(const double* in, double* out, uint32_t planes, const Ho4dArgs& a,
+                     cudaStream_t s) {
+  if (planes == 0) return cudaSuccess;
+  const uint64_t total = (uint64_t)planes * ho4d_plane(a);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+  k_pad4g<<<blocks, 256, 0, s>>>(in, out, planes, a.n[1], a.n[2], a.n[3], a.n[1] + 2 * a.gh,
+                                 a.n[2] + 2 * a.gh, a.n3p + 2 * a.g3, a.gh, a.g3);
+  return cudaGetLastError();
+}
+
+cudaError_t ho4d_unpad(const double* in, double* out, uint32_t planes, const Ho4dArgs& a,
+                       cudaStream_t s) {
+  if (planes == 0) return cudaSuccess;
+  const uint64_t total = (uint64_t)planes * a.n[1] * a.n[2] * a.n[3];
+  const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+  k_unpad4g<<<blocks, 256, 0, s>>>(in, out, planes, a.n[1], a.n[2], a.n[3], a.n[1] + 2 * a.gh,
+                                   a.n[2] + 2 * a.gh, a.n3p + 2 * a.g3, a.gh, a.g3);
   return cudaGetLastError();
 }
 

@@ -112,12 +112,25 @@ struct Ho4dArgs {
   // global alpha, ghost faces replicated from the nearest interior face
   int lf;
   LfParams lp;
+  // 1: ENO3 Godunov stage in k_eno3g (face-shared choices, patched boxes,
+  //    three barriers per ring slot); 0: k_ho4t
+  int eno3g;
+  // ghost widths of the stage-buffer layout [n0][n1 + 2gh][n2 + 2gh][n3p + 2g3]
+  // (k_eno3g: 3 and 4; k_ho4t / k_ho4d: 0, the plain padded layout)
+  uint32_t gh, g3;
 };
 void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
 // fill mapv[] for the current buffers (k_ho4t); returns cudaErrorNotSupported
 // when the driver entry point is unavailable
 cudaError_t ho4d_make_maps(Ho4dArgs& a);
 cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s);
+// elements per axis-0 plane of the stage buffers (ghost layout of `a`), and
+// reference layout (planes of n1 * n2 * n3) <-> stage-buffer layout
+uint64_t ho4d_plane(const Ho4dArgs& a);
+cudaError_t ho4d_pad(const double* in, double* out, uint32_t planes, const Ho4dArgs& a,
+                     cudaStream_t s);
+cudaError_t ho4d_unpad(const double* in, double* out, uint32_t planes, const Ho4dArgs& a,
+                       cudaStream_t s);
 
 // Model shape id for the fast path, or -1 when the generic kernel must run
 // (rank != 4, per-node bounds, rows depending on x0, inputs not matching the

@@ -81,17 +81,24 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
     ho4d_config(g, sm_count(ctx->device), t);
     if (!t.tma) shape = -1;
   }
-  const uint64_t rows4 = g.nd == 4 ? static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2] : 0;
-  const uint32_t n3p = g.nd == 4 ? (g.n[3] + 1) / 2 * 2 : 0;
-  const size_t pbytes = shape >= 0 ? rows4 * n3p * sizeof(double) : bytes;
+  // the 4D kernel's configuration fixes the stage-buffer layout (padded, or
+  // with ghost cells for k_eno3g)
+  Ho4dArgs h4;
+  std::memset(&h4, 0, sizeof h4);
+  if (shape >= 0) {
+    h4.order = cfg->spatial_order > 3 ? 3 : (cfg->spatial_order < 1 ? 1 : cfg->spatial_order);
+    fill_lf(m, scheme_id(cfg), galpha, h4.lf, h4.lp);
+    ho4d_config(g, sm_count(ctx->device), h4);
+  }
+  const size_t pbytes = shape >= 0 ? g.n[0] * ho4d_plane(h4) * sizeof(double) : bytes;
   CUDA_TRY(ctx->v0.ensure(pbytes));
   CUDA_TRY(ctx->v1.ensure(pbytes));
   CUDA_TRY(ctx->v2.ensure(pbytes));
   CUDA_TRY(ctx->v3.ensure(pbytes));
   if (shape >= 0) {
     CUDA_TRY(ctx->pcbuf.ensure(pbytes));
-    CUDA_TRY(launch_pad4(init, ctx->v0.d(), rows4, g.n[3], n3p, ctx->stream));
-    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows4, g.n[3], n3p, ctx->stream));
+    CUDA_TRY(ho4d_pad(init, ctx->v0.d(), g.n[0], h4, ctx->stream));
+    CUDA_TRY(ho4d_pad(c, ctx->pcbuf.d(), g.n[0], h4, ctx->stream));
     ctx->launches += 2;
   } else {
     CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -119,12 +126,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   a.loop = 1;
   Stage st[3];
   const int ns = stages_of(cfg->time_order, st);
-  Ho4dArgs h4;
-  std::memset(&h4, 0, sizeof h4);
   if (shape >= 0) {
-    h4.order = a.order > 3 ? 3 : a.order;
-    fill_lf(m, scheme_id(cfg), galpha, h4.lf, h4.lp);
-    ho4d_config(g, sm_count(ctx->device), h4);
     h4.tab = m.tab;
     for (int d = 0; d < 4; ++d) {
       h4.off_pos[d] = m.row[d].off_pos;
@@ -219,7 +221,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   if (small2d) {
     // the cluster kernel wrote V* to `out` itself
   } else if (shape >= 0) {
-    CUDA_TRY(launch_unpad4(fin, out, rows4, g.n[3], n3p, ctx->stream));
+    CUDA_TRY(ho4d_unpad(fin, out, g.n[0], h4, ctx->stream));
     ++ctx->launches;
   } else {
     CUDA_TRY(cudaMemcpyAsync(out, fin, bytes, cudaMemcpyDeviceToDevice, ctx->stream));

@@ -203,8 +203,7 @@ int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared
   h.cbeg = has_lo ? R : 0u;
   h.cend = h.cbeg + owned;
   ho4d_config(gloc, sm_count(ctx->device), h);
-  const uint64_t plane = static_cast<uint64_t>(p.g.n[1]) * p.g.n[2] * h.n3p;
-  const uint64_t rows_owned = static_cast<uint64_t>(owned) * p.g.n[1] * p.g.n[2];
+  const uint64_t plane = ho4d_plane(h);  // stage-buffer plane (ghost layout of h)
   const size_t lbytes = static_cast<size_t>(nloc) * plane * sizeof(double);
   DevBuf* bufs[4] = {&ctx->v0, &ctx->v1, &ctx->v2, &ctx->v3};
   for (DevBuf* b : bufs) {
@@ -213,10 +212,8 @@ int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared
   }
   CUDA_TRY(ctx->pcbuf.ensure(lbytes));
   CUDA_TRY(cudaMemsetAsync(ctx->pcbuf.p, 0, lbytes, ctx->stream));
-  CUDA_TRY(launch_pad4(init_slab, ctx->v0.d() + h.cbeg * plane, rows_owned, p.g.n[3], h.n3p,
-                       ctx->stream));
-  CUDA_TRY(launch_pad4(c_slab, ctx->pcbuf.d() + h.cbeg * plane, rows_owned, p.g.n[3], h.n3p,
-                       ctx->stream));
+  CUDA_TRY(ho4d_pad(init_slab, ctx->v0.d() + h.cbeg * plane, owned, h, ctx->stream));
+  CUDA_TRY(ho4d_pad(c_slab, ctx->pcbuf.d() + h.cbeg * plane, owned, h, ctx->stream));
   ctx->launches += 2;
   h.tab = p.hm.dm.tab;
   for (int d = 0; d < 4; ++d) {
@@ -309,7 +306,7 @@ int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared
     CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
   const double* fin = ((st.iter & 1) ? h.buf1 : h.buf0) + h.cbeg * pe;
-  CUDA_TRY(launch_unpad4(fin, value_slab_out, rows_owned, p.g.n[3], h.n3p, ctx->stream));
+  CUDA_TRY(ho4d_unpad(fin, value_slab_out, owned, h, ctx->stream));
   ++ctx->launches;
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (st.status == HJB_ERR_DIVERGED)
@@ -447,17 +444,17 @@ int hjb_ho_stage_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_mode
   h.cbeg = static_cast<uint32_t>(plane_begin);
   h.cend = static_cast<uint32_t>(plane_end);
   ho4d_config(p.g, sm_count(ctx->device), h);
-  const uint64_t rows = static_cast<uint64_t>(p.g.n[0]) * p.g.n[1] * p.g.n[2];
-  const size_t pb = rows * h.n3p * sizeof(double);
+  const uint32_t n0 = p.g.n[0];
+  const size_t pb = n0 * ho4d_plane(h) * sizeof(double);
   DevBuf a, vn, cb, o;
   CUDA_TRY(a.ensure(pb));
   CUDA_TRY(vn.ensure(pb));
   CUDA_TRY(cb.ensure(pb));
   CUDA_TRY(o.ensure(pb));
-  CUDA_TRY(launch_pad4(stage_in, a.d(), rows, p.g.n[3], h.n3p, ctx->stream));
-  CUDA_TRY(launch_pad4(value_n, vn.d(), rows, p.g.n[3], h.n3p, ctx->stream));
-  CUDA_TRY(launch_pad4(constraint, cb.d(), rows, p.g.n[3], h.n3p, ctx->stream));
-  CUDA_TRY(launch_pad4(stage_in, o.d(), rows, p.g.n[3], h.n3p, ctx->stream));
+  CUDA_TRY(ho4d_pad(stage_in, a.d(), n0, h, ctx->stream));
+  CUDA_TRY(ho4d_pad(value_n, vn.d(), n0, h, ctx->stream));
+  CUDA_TRY(ho4d_pad(constraint, cb.d(), n0, h, ctx->stream));
+  CUDA_TRY(ho4d_pad(stage_in, o.d(), n0, h, ctx->stream));
   h.tab = p.hm.dm.tab;
   for (int d = 0; d < 4; ++d) {
     h.off_pos[d] = p.hm.dm.row[d].off_pos;
@@ -477,7 +474,7 @@ int hjb_ho_stage_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_mode
   CUDA_TRY(ho4d_make_maps(h));
   CUDA_TRY(cudaMemsetAsync(ctx->st, 0, sizeof(LoopState), ctx->stream));
   CUDA_TRY(launch_ho4d(h, p.shape, ctx->stream));
-  CUDA_TRY(launch_unpad4(o.d(), out, rows, p.g.n[3], h.n3p, ctx->stream));
+  CUDA_TRY(ho4d_unpad(o.d(), out, n0, h, ctx->stream));
   ctx->launches += 6;
   unsigned long long bits = 0;
   CUDA_TRY(cudaMemcpyAsync(&bits, &ctx->st->maxdv_bits, sizeof bits, cudaMemcpyDeviceToHost,

@@ -140,3 +140,37 @@ def test_ho4t_lax_friedrichs_matches_generic(gpu_ctx, monkeypatch, diss):
     gen = hj.solve(case.init_field(), case.c_field(), case.model, case.db, cfg, ctx=gpu_ctx)
     assert same(fast.value.values(), gen.value.values())
     assert same(fast.residual_history, gen.residual_history)
+
+
+@pytest.mark.parametrize("model", sorted(_LF_HO_MODELS))
+@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (6, 17, 9, 101), (11, 23, 5, 70)])
+def test_eno3g_godunov_shapes(gpu_ctx, oracle, model, dims):
+    """k_eno3g (ENO3 Godunov, face-shared choices, edge-patched TMA boxes)
+    on every fast-path model shape, multi-segment axis-3 rows and partial
+    tiles, against the restatement."""
+    mk, bounds, box = _LF_HO_MODELS[model]
+    g = hj.Grid([(lo, hi, n) for (lo, hi), n in zip(box, dims)])
+    m = mk()
+    db = hj.IntervalField.constant(g, bounds)
+    rng = np.random.default_rng(sum(dims))
+    c = hj.ScalarField(g, rng.random(g.size()) - 0.6)
+    init = hj.ScalarField(g, c.values() + 0.3 * rng.random(g.size()))
+    cfg = hj.SolveConfig(tolerance=1e-9, max_iters=6, spatial_order=3, time_order=3)
+    want = oracle.solve(init, c, m, db, cfg)
+    got = hj.solve(init, c, m, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+def test_eno3g_matches_ho4t(gpu_ctx, monkeypatch):
+    """The face-shared ENO3 kernel and the per-cell k_ho4t agree bitwise on
+    a config-2 grid large enough for several tiles and plane chunks."""
+    case = with_iters(workload_case(configs.config2(41)), 5)
+    cfg = hj.SolveConfig(**case.cfg.__dict__)
+    cfg.spatial_order, cfg.time_order = 3, 3
+    new = hj.solve(case.init_field(), case.c_field(), case.model, case.db, cfg, ctx=gpu_ctx)
+    monkeypatch.setenv("HJB_HO_ENO3G", "0")
+    old = hj.solve(case.init_field(), case.c_field(), case.model, case.db, cfg, ctx=gpu_ctx)
+    assert same(new.value.values(), old.value.values())
+    assert same(new.residual_history, old.residual_history)
