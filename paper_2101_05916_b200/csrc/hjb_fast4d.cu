@@ -1761,12 +1761,6 @@ __device__ __forceinline__ void eno3_face(double e0, double e1, double e2, doubl
 #endif
 constexpr int kEno3gThreads = HJB_ENO3G_THREADS;
 
-// 16-byte read-only load kept in program order (volatile): the compiler
-// would otherwise sink it next to its use at the end of the step
-__device__ __forceinline__ void ldg2_v(const double* p, double* o) {
-  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(o[0]), "=d"(o[1]) : "l"(p));
-}
-
 template <class S>
 __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constant__ Ho4dArgs a) {
   constexpr int R = 3, kK = 2;
@@ -1812,13 +1806,21 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
   if (threadIdx.x >= ncons) {
     // producer: the box of plane q is tile + (R, R, H3) halo, whose ghost-
     // layout origin is (base1, base2, base3) (gh == R, g3 == H3)
+    const bool need_vn = a.kind != 0 || a.final_stage;
+    const int vsel = a.loop == 0 ? 1 : (int)(it & 1);
+    const uint32_t vbs = (a.vbox_bytes + 127) / 128 * 128;
+    const int x3 = (int)(base3 + a.g3), x2 = (int)(base2 + a.gh), x1 = (int)(base1 + a.gh);
     if (lane == 0)
       for (uint32_t q = 0; c0 + q < c1; ++q) {
         const uint32_t sl = q % ring, use = q / ring;
+        const uint32_t dst0 = smem0 + sl * a.vslot_bytes, bar = bars + sl * 8;
+        const int p = (int)(c0 + q), pa = min(p + 4, (int)n0 - 1);
         mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
-        mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes);
-        tma_load4(smem0 + sl * a.vslot_bytes, &a.mapv[msel], (int)base3, (int)base2, (int)base1,
-                  (int)(c0 + q), bars + sl * 8);
+        mbar_arrive_expect_tx(bar, a.vbox_bytes + (need_vn ? 3u : 2u) * a.tbox_bytes);
+        tma_load4(dst0, &a.mapv[msel], (int)base3, (int)base2, (int)base1, p, bar);
+        tma_load4(dst0 + vbs, &a.mapc, x3, x2, x1, p, bar);
+        if (need_vn) tma_load4(dst0 + vbs + a.tbox_slot, &a.mapt[vsel], x3, x2, x1, p, bar);
+        tma_load4(dst0 + vbs + 2 * a.tbox_slot, &a.mapt[msel], x3, x2, x1, pa, bar);
       }
   } else {
     const uint32_t t = threadIdx.x;
@@ -1838,6 +1840,8 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
     const uint32_t W2 = a.T2 + 2 * R;
     const uint32_t rowb = B3 * 8u;
     const uint32_t own = (((r1 + R) * W2 + (r2 + R)) * B3 + (i3 - base3 + a.H3)) * 8u;
+    // this pencil in the slot's tile boxes (c, V_n, stage input of plane + 4)
+    const uint32_t town = (a.vbox_bytes + 127) / 128 * 128 + ((r * a.T3) + (i3 - base3)) * 8u;
 
     // loop-invariant flux data (as k_ho4t, Godunov)
     double pos_[4][kK], neg_[4][kK];
@@ -1915,14 +1919,6 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
     uint32_t sl = 0, ph = 0;
     for (uint32_t i0 = c0; i0 < c1; ++i0) {
       const uint64_t po = (uint64_t)i0 * s0;
-      double ccv[kK], vnv[kK], vnx[kK];
-      ldg2_v(a.c + po + rowo, ccv);
-      if (need_vn) {
-        ldg2_v(vn + po + rowo, vnv);
-      } else {
-        vnv[0] = vnv[1] = 0.0;
-      }
-      ldg2_v(plane_at((int)i0 + 4), vnx);
       const uint32_t slot = smem0 + sl * a.vslot_bytes;
       mbar_wait_nc(bars + sl * 8, ph);
       // own row V(i3-3) .. V(i3+4)
@@ -1986,6 +1982,14 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
         hh[0] = hh[0] + flux(std::integral_constant<int, 3>{}, 0, dm0, dp0);
         hh[1] = hh[1] + flux(std::integral_constant<int, 3>{}, 1, dm1, dp1);
       }
+      double ccv[kK], vnv[kK], vnx[kK];
+      lds_k<kK>(slot + town, ccv);
+      if (need_vn) {
+        lds_k<kK>(slot + town + a.tbox_slot, vnv);
+      } else {
+        vnv[0] = vnv[1] = 0.0;
+      }
+      lds_k<kK>(slot + town + 2 * a.tbox_slot, vnx);
       __syncwarp();
       if (lane == 0) mbar_arrive(bars + (ring + sl) * 8);
       if (++sl == ring) {
@@ -2448,7 +2452,8 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
         for (uint32_t t2 = 1; t2 <= g.n[2] && t1 * t2 * jj <= maxc; ++t2) {
           if (t1 * t2 * jj < maxc / 2) continue;  // keep the CTA at least half full
           const size_t vb = (size_t)(t1 + 2 * R) * (t2 + 2 * R) * B3 * 8;
-          const size_t slot = (vb + 127) / 128 * 128;
+          const size_t tb = a.eno3g ? ((size_t)t1 * t2 * t3 * 8 + 127) / 128 * 128 : 0;
+          const size_t slot = (vb + 127) / 128 * 128 + 3 * tb;
           uint32_t ring = want_ring;
           while (ring >= 2 && ring * slot + nbar * ring * 8 > 200 * 1024) --ring;
           if (ring < 2) continue;
@@ -2478,6 +2483,11 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
       a.ring = bring;
       a.vbox_bytes = (bt1 + 2 * R) * (bt2 + 2 * R) * (bt3 + 2 * H3) * 8;
       a.vslot_bytes = (a.vbox_bytes + 127) / 128 * 128;
+      if (a.eno3g) {
+        a.tbox_bytes = bt1 * bt2 * bt3 * 8;
+        a.tbox_slot = (a.tbox_bytes + 127) / 128 * 128;
+        a.vslot_bytes += 3 * a.tbox_slot;
+      }
       a.smem = bring * a.vslot_bytes + nbar * bring * 8;
       if (a.eno3g) {  // ghost layout (k_eno3g)
         a.gh = R;
@@ -2497,7 +2507,21 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   }
   const uint32_t span = a.cend - a.cbeg;
   uint32_t nch = 1;
-  while (tiles * nch < 2u * sms && span / (nch + 1) >= 8) ++nch;
+  if (a.eno3g) {
+    // one CTA per SM: pick the chunk count that minimises the wave-quantised
+    // time, waves x (planes per chunk + ~4 planes of window / ring start-up)
+    uint64_t best = ~0ull;
+    for (uint32_t k = 1; k <= 64 && (k == 1 || span / k >= 6); ++k) {
+      const uint64_t waves = ((uint64_t)tiles * k + sms - 1) / sms;
+      const uint64_t est = waves * ((span + k - 1) / k + 4);
+      if (est < best) {
+        best = est;
+        nch = k;
+      }
+    }
+  } else {
+    while (tiles * nch < 2u * sms && span / (nch + 1) >= 8) ++nch;
+  }
   a.L = (span + nch - 1) / nch;
   a.nchunks = (span + a.L - 1) / a.L;
   a.blocks = tiles * a.nchunks;
@@ -2582,6 +2606,19 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a) {
                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  if (a.eno3g) {
+    const cuuint32_t tbox[4] = {a.T3, a.T2, a.T1, 1};
+    double* tp[5] = {ptrs[0], a.loop == 0 ? const_cast<double*>(a.xvn) : a.buf1, a.stage1,
+                     a.stage2, const_cast<double*>(a.c)};
+    for (int k = 0; k < 5; ++k) {
+      if (!tp[k]) continue;
+      CUresult r = encode(k < 4 ? &a.mapt[k] : &a.mapc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, tp[k],
+                          dims, strides, tbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
   }
   return cudaSuccess;
 }

@@ -118,6 +118,13 @@ struct Ho4dArgs {
   // ghost widths of the stage-buffer layout [n0][n1 + 2gh][n2 + 2gh][n3p + 2g3]
   // (k_eno3g: 3 and 4; k_ho4t / k_ho4d: 0, the plain padded layout)
   uint32_t gh, g3;
+  // k_eno3g: tile-only boxes (T1 x T2 x T3, no halo) of the four stage buffers
+  // (loop == 0: [0] the stage input, [1] V_n) and of c; each ring slot holds
+  // the V box of plane q, c and V_n of plane q and the stage input of plane
+  // q + 4 (the axis-0 window's next plane), tbox_slot bytes apart
+  CUtensorMap mapt[4];
+  CUtensorMap mapc;
+  uint32_t tbox_bytes, tbox_slot;
 };
 void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a);
 // fill mapv[] for the current buffers (k_ho4t); returns cudaErrorNotSupported
