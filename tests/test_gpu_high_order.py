@@ -143,7 +143,8 @@ def test_ho4t_lax_friedrichs_matches_generic(gpu_ctx, monkeypatch, diss):
 
 
 @pytest.mark.parametrize("model", sorted(_LF_HO_MODELS))
-@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (6, 17, 9, 101), (11, 23, 5, 70)])
+@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (6, 17, 9, 101), (11, 23, 5, 70), (5, 3, 4, 7),
+                                  (3, 5, 2, 9)])
 def test_eno3g_godunov_shapes(gpu_ctx, oracle, model, dims):
     """k_eno3g (ENO3 Godunov, face-shared choices, edge-patched TMA boxes)
     on every fast-path model shape, multi-segment axis-3 rows and partial
