@@ -57,6 +57,8 @@ def parse():
                     help="skip the full solve to tol 1e-4 (time_to_converged, ~50 s on a B200)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config3", dest="config3", action="store_false",
+                    help="skip the extra config-3 (ENO3 + TVD-RK3, 101^4) step timing")
     return ap.parse_args()
 
 
@@ -221,6 +223,41 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def config3_step(ctx, dev, steps=6):
+    """BASELINE config 3's scheme on its grid: ENO3 + TVD-RK3 Godunov steps of
+    the 101^4 config-2 model (k_eno3g), device time per step from V=c."""
+    import torch
+    from paper_2101_05916_b200 import hjsafe as hj
+    w = configs_mod().config3(101)
+    cells = w.grid.size()
+    c = torch.empty(cells, dtype=torch.float64, device=dev)
+    out = torch.empty_like(c)
+    torch.cuda.synchronize()
+    hj.signed_distance_band_dev(w.grid, 0, -4.0, 4.0, c.data_ptr(), ctx=ctx)
+    cfg = hj.SolveConfig(**w.cfg.__dict__)
+    cfg.spatial_order, cfg.time_order, cfg.max_iters = 3, 3, 2
+    hj.solve_dev(w.grid, w.model, w.dbounds(), c.data_ptr(), c.data_ptr(), out.data_ptr(), cfg,
+                 ctx=ctx)
+    cfg.max_iters = steps
+    r = hj.solve_dev(w.grid, w.model, w.dbounds(), c.data_ptr(), c.data_ptr(), out.data_ptr(), cfg,
+                     ctx=ctx)
+    per = r.wall_seconds / r.iterations
+    peak, _ = measured_peak()
+    gbs = 88 * cells / per / 1e9
+    del c, out
+    torch.cuda.empty_cache()
+    return {"workload": "BASELINE config 3 scheme: ENO3 + TVD-RK3 Godunov, 101^4 config-2 model, "
+                        "one GPU, from V=c", "steps": r.iterations, "ms_per_step": per * 1e3,
+            "cell_steps_per_s": cells / per, "bytes_per_cell_step": 88,
+            "achieved_gbs": gbs, "frac_of_hbm": gbs / peak, "bound": "fp64 issue (see DESIGN §5)",
+            "kernel": "k_eno3g x 3 stages"}
+
+
+def configs_mod():
+    from paper_2101_05916_b200 import configs
+    return configs
+
+
 def run_hjb(args):
     import torch
     rank, world, local = dist_env()
@@ -340,6 +377,8 @@ def run_hjb(args):
                                      "converged": rc.converged, "tolerance": cfgc.tolerance,
                                      "safe_cells": safe, "final_residual": rc.final_residual,
                                      "note": "device time of the whole solve from V=c"}
+    if args.config3:
+        line["config3"] = config3_step(ctx, dev)
     if rank == 0 and not args.no_cpu_baseline:
         try:
             rate, iters, sample, kind = cpu_reference_rate(args.n, args.cpu_seconds)

@@ -598,11 +598,28 @@ static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
   unsigned int hf = 0;
   CUDA_TRY(cudaMemcpyAsync(&hf, flag, sizeof hf, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (hf) return HJB_OK;
+  // bounds varying off axis 0: the per-node variant (padded lo / hi read per
+  // cell); HJB_PN=0 leaves them to the generic kernel
+  const char* epn = std::getenv("HJB_PN");
+  if (hf && epn && std::strcmp(epn, "0") == 0) return HJB_OK;
+  const bool per_node = hf != 0;
   const uint32_t n0 = g.n[0];
+  if (per_node) {
+    const uint32_t n3p = (g.n[3] + 1) / 2 * 2;
+    const uint64_t rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
+    const size_t pb = rows * n3p * sizeof(double);
+    CUDA_TRY(ctx->pnbuf.ensure(2 * db->channels * pb));
+    for (int ch = 0; ch < db->channels; ++ch) {
+      double* lo = ctx->pnbuf.d() + (2 * ch) * rows * n3p;
+      double* hi = ctx->pnbuf.d() + (2 * ch + 1) * rows * n3p;
+      CUDA_TRY(launch_pad4(db->lo[ch], lo, rows, g.n[3], n3p, ctx->stream));
+      CUDA_TRY(launch_pad4(db->hi[ch], hi, rows, g.n[3], n3p, ctx->stream));
+      ctx->launches += 2;
+    }
+  }
   std::vector<double> plo(static_cast<size_t>(db->channels) * n0),
       phi(static_cast<size_t>(db->channels) * n0);
-  for (int ch = 0; ch < db->channels; ++ch) {
+  for (int ch = 0; ch < db->channels && !per_node; ++ch) {
     CUDA_TRY(cudaMemcpy2DAsync(plo.data() + ch * n0, sizeof(double), db->lo[ch],
                                s0 * sizeof(double), sizeof(double), n0,
                                cudaMemcpyDeviceToHost, ctx->stream));
@@ -630,7 +647,13 @@ static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
         t.push_back(ng);
       }
     }
-    if (r.n_dterm == 1) {
+    if (r.n_dterm == 1 && per_node) {
+      const uint32_t n3p = (g.n[3] + 1) / 2 * 2;
+      const uint64_t field = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2] * n3p;
+      f.pn_lo[d] = ctx->pnbuf.d() + (2 * r.dch[0]) * field;
+      f.pn_hi[d] = ctx->pnbuf.d() + (2 * r.dch[0] + 1) * field;
+      f.pn_coef[d] = r.dcoef[0];
+    } else if (r.n_dterm == 1) {
       const int ch = r.dch[0];
       f.pv_pt[d] = static_cast<int>(t.size());
       for (uint32_t i = 0; i < n0; ++i) {
@@ -650,7 +673,7 @@ static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   f.tab = ctx->pvtab.d();
   f.tab_len = static_cast<uint32_t>(t.size());
-  f.pv = 1;
+  f.pv = per_node ? 2 : 1;
   *ok = 1;
   return HJB_OK;
 }

@@ -57,6 +57,7 @@ struct hjb_context {
   hjb::DevBuf v0, v1, v2, v3, cbuf, pcbuf, dbbuf, tables, scratch, hist, whist, xbuf;
   hjb::DevBuf gpa, gpb, gpc;  // GP bounds: k*, factor, per-point tables
   hjb::DevBuf pvtab;          // 4D fast path with axis-0-varying bounds: tables
+  hjb::DevBuf pnbuf;          // 4D fast path with per-node bounds: padded lo / hi
   hjb::LoopState* st = nullptr;
   hjb::LoopState* st_host = nullptr;  // pinned mirror
   long long launches = 0;

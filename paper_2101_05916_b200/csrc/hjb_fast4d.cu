@@ -407,7 +407,18 @@ __device__ __forceinline__ void lf_row_terms(const LfParams& lp, const double* t
   }
 }
 
-template <class S, int kK, int MAXT, int SCH, bool PV = false>
+// a pencil of kK per-node bound values (16-byte global loads)
+template <int K>
+__device__ __forceinline__ void lds_pn(const double* p, double* v) {
+#pragma unroll
+  for (int c = 0; c < K; c += 2) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(p + c));
+    v[c] = x.x;
+    v[c + 1] = x.y;
+  }
+}
+
+template <class S, int kK, int MAXT, int SCH, int PV = 0>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -700,8 +711,43 @@ __global__ void __launch_bounds__(MAXT, 1)
         ka0[c] = (SCH != 0 || S::LIN(0)) ? 0.0 : pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
       }
 
+      // per-node bounds: this pencil's lo / hi of each disturbance row's
+      // channel, plane c0 now and plane i0 + 1 one step ahead
+      const uint64_t pno = active ? static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3
+                                  : 0ull;
+      double pl_c[4][kK], ph_c[4][kK], pl_n[4][kK], ph_n[4][kK];
+      if (PV == 2) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          if (S::D(d) < 0) continue;
+          lds_pn<kK>(a.pn_lo[d] + static_cast<uint64_t>(c0) * s0 + pno, pl_c[d]);
+          lds_pn<kK>(a.pn_hi[d] + static_cast<uint64_t>(c0) * s0 + pno, ph_c[d]);
+        }
+      }
       for (uint32_t i0 = c0; i0 < c1; ++i0) {
-        if (PV) {
+        if (PV == 2) {
+          // per-node disturbance bounds: this cell's slopes and shapes of the
+          // disturbance rows (dim_slopes order: drift + controls, then +
+          // max / min of the disturbance products, solver.cpp:67-86)
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (S::D(d) < 0) continue;
+            if (i0 + 1 < c1) {
+              lds_pn<kK>(a.pn_lo[d] + static_cast<uint64_t>(i0 + 1) * s0 + pno, pl_n[d]);
+              lds_pn<kK>(a.pn_hi[d] + static_cast<uint64_t>(i0 + 1) * s0 + pno, ph_n[d]);
+            }
+#pragma unroll
+            for (int c = 0; c < kK; ++c) {
+              const double x = a.pn_coef[d] * pl_c[d][c], y = a.pn_coef[d] * ph_c[d][c];
+              shp[d][c] = row_shape(pos_[d][c] + (x > y ? x : y), neg_[d][c] + (x < y ? x : y));
+            }
+          }
+          if (S::D(0) >= 0) {  // march-axis row: the carried D- face's L product
+#pragma unroll
+            for (int c = 0; c < kK; ++c) ka0[c] = pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
+          }
+        }
+        if (PV == 1) {
           // plane-varying disturbance bounds: this plane's slopes and shapes
           // of the disturbance rows (row_slopes order: drift + controls,
           // then + max / min of the disturbance products, solver.cpp:67-86)
@@ -767,7 +813,8 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
         for (int c = 1; c < kK; ++c) f3[c] = (v[c] - v[c - 1]) * inv3m[c];
         f3[kK] = (vr - v[kK - 1]) * inv3;
-        constexpr bool row3_shared = !(S::A(3) == 3 || S::B(3) == 3);
+        // (per-node bounds: a disturbance row's slopes vary along x3)
+        constexpr bool row3_shared = !(S::A(3) == 3 || S::B(3) == 3) && !(PV == 2 && S::D(3) >= 0);
         // row 3: each face's L product (cell above uses it as A) and R
         // product (cell below uses it as B)
         double k3a[kK + 1], k3b[kK + 1];
@@ -874,6 +921,17 @@ __global__ void __launch_bounds__(MAXT, 1)
         op += s0;
 #pragma unroll
         for (int c = 0; c < kK; ++c) v[c] = vn[c];
+        if (PV == 2) {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (S::D(d) < 0) continue;
+#pragma unroll
+            for (int c = 0; c < kK; ++c) {
+              pl_c[d][c] = pl_n[d][c];
+              ph_c[d][c] = ph_n[d][c];
+            }
+          }
+        }
         // V plane i0 and c plane i0 are no longer read by this warp
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_cur + kRing * 8);
@@ -2319,7 +2377,7 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   if (a.bal) a.blocks = std::min<uint32_t>(static_cast<uint32_t>(sms), tiles * span);
 }
 
-template <class S, int K, int MAXT, int SCH = 0, bool PV = false>
+template <class S, int K, int MAXT, int SCH = 0, int PV = 0>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -2361,8 +2419,12 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
 // the autotuner pick among them per grid
 template <class S>
 static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
-  if (a.pv) {  // plane-varying disturbance bounds: one configuration
-    launch_one<S, 2, 576, 0, true>(a, s);
+  if (a.pv == 1) {  // plane-varying disturbance bounds: one configuration
+    launch_one<S, 2, 576, 0, 1>(a, s);
+    return;
+  }
+  if (a.pv == 2) {  // per-node disturbance bounds
+    launch_one<S, 2, 576, 0, 2>(a, s);
     return;
   }
   if (a.lf == 1) {  // Lax-Friedrichs variants: one configuration

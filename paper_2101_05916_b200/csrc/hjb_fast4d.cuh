@@ -68,8 +68,14 @@ struct Fast4dArgs {
   // over x, gp.cpp:211-249): rows with a disturbance term take
   // pos = tab[off_pos] + tab[pv_pt + i0], neg = tab[off_neg] + tab[pv_nt + i0]
   // per plane (Godunov only)
-  int pv;
+  int pv;  // 1: plane-varying bounds (pv_pt / pv_nt tables); 2: per-node bounds
   int pv_pt[4], pv_nt[4];
+  // per-node bounds (pv == 2): padded [n0][n1][n2][n3p] lo / hi of each
+  // disturbance row's channel and the row's coefficient; pos / neg =
+  // tab[off_pos / off_neg] (drift + controls) + max / min(coef*lo, coef*hi)
+  const double* pn_lo[4];
+  const double* pn_hi[4];
+  double pn_coef[4];
   LfParams lp;
 };
 
@@ -145,8 +151,9 @@ cudaError_t ho4d_unpad(const double* in, double* out, uint32_t planes, const Ho4
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
 // Godunov fast-path shape for PER-NODE bounds (rows not folded); -1 if none.
 // Rows with a disturbance term must be exactly the shape's D rows, one
-// term each; their bounds must then vary along axis 0 only (checked on the
-// device by the caller).
+// term each.  Bounds varying along axis 0 only run the plane-table variant
+// (pv == 1), any other per-node field the per-node variant (pv == 2); the
+// caller checks which on the device.
 int fast4d_shape_pv(const DevGrid& g, const DevModel& m);
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);

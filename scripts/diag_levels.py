@@ -25,7 +25,11 @@ def main():
         cfg.max_iters, cfg.tolerance = iters, 1e-300
         n = w.grid.size()
         pn = hj.IntervalField(w.grid, 1, lo=[np.full(n, -0.6)], hi=[np.full(n, 0.6)])
-        for label, db in (("constant", w.dbounds()), ("per-node constant", pn)):
+        rng = np.random.default_rng(1)
+        noise = 1e-16 * rng.standard_normal(n)
+        pv = hj.IntervalField(w.grid, 1, lo=[-0.6 + noise], hi=[0.6 + noise])
+        for label, db in (("constant", w.dbounds()), ("per-node constant", pn),
+                          ("per-node noisy", pv)):
             l0 = ctx.launches
             r = hj.solve(c, c, w.model, db, cfg, ctx=ctx)
             print(f"{w.grid.shape} {label}: {r.wall_seconds / r.iterations * 1e6:.1f} us/sweep, "

@@ -376,3 +376,34 @@ def test_fast4d_schedules(gpu_ctx, oracle, monkeypatch, balance, dims):
     assert got.iterations == want.iterations
     assert same(got.residual_history, want.residual_history)
     assert same(got.value.values(), want.value.values())
+
+
+@pytest.mark.parametrize("case", PV_CASES, ids=[c[0] for c in PV_CASES])
+@pytest.mark.parametrize("spread", [0.05, 1.0], ids=["narrow", "sign_mixing"])
+def test_fast4d_per_node_bounds(gpu_ctx, oracle, monkeypatch, case, spread):
+    """Per-node bounds varying in every axis (e.g. a resampled constant field
+    with rounding noise, or GP bounds over several axes) run k_fast4d's
+    per-node variant (slopes and slope shapes of the disturbance rows formed
+    per cell and plane); bitwise equal to the oracle and to HJB_PN=0 (the
+    generic kernel).  `sign_mixing` makes the row shapes differ cell to cell."""
+    _, mk, specs, dims = case
+    g = hj.Grid(dims)
+    model = mk()
+    rng = np.random.default_rng(11)
+    lo, hi = [], []
+    for (cen, w) in specs:
+        a = cen + spread * (rng.random(g.size()) - 0.5)
+        b = a + w * rng.random(g.size())
+        lo.append(a)
+        hi.append(b)
+    db = hj.IntervalField(g, len(specs), lo=lo, hi=hi)
+    c = hj.ScalarField(g, band_np(g, 0, -0.6 * g.dims()[0].max, 0.6 * g.dims()[0].max))
+    cfg = hj.SolveConfig(tolerance=1e-6, max_iters=40)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+    monkeypatch.setenv("HJB_PN", "0")
+    gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert same(gen.value.values(), got.value.values())
