@@ -1818,9 +1818,16 @@ __device__ __forceinline__ void eno3_face(double e0, double e1, double e2, doubl
 #define HJB_ENO3G_THREADS 512
 #endif
 constexpr int kEno3gThreads = HJB_ENO3G_THREADS;
+// Lax-Friedrichs: per-cell drifts / alphas and all four (D-, D+) pairs live
+// at once (lf_hhat couples the axes), so fewer threads with more registers
+constexpr int kEno3gThreadsLF = 384;
+__host__ __device__ constexpr int eno3g_threads(int sch) {
+  return sch ? kEno3gThreadsLF : kEno3gThreads;
+}
 
-template <class S>
-__global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constant__ Ho4dArgs a) {
+template <class S, int SCH = 0>
+__global__ void __launch_bounds__(eno3g_threads(SCH), 1)
+    k_eno3g(const __grid_constant__ Ho4dArgs a) {
   constexpr int R = 3, kK = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
@@ -1937,6 +1944,32 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
         shp[d][c] = (c > 0 && !per_cell) ? shp[d][0] : row_shape(pos_[d][c], neg_[d][c]);
       }
     }
+    // Lax-Friedrichs: the rows' drifts and alphas (loop invariant)
+    double lfdr[4][kK], lfal[4][kK];
+    if (SCH != 0) {
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+        uint32_t ka[4];
+        double sb[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          ka[d] = pick<S>(S::A(d), ci1, ci2, min(i3 + c, n3 - 1));
+          sb[d] = pos_[d][c];
+        }
+        double dr[4], al[4];
+        lf_row_terms<S, SCH>(a.lp, a.tab, ka, sb, dr, al);
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          lfdr[d][c] = dr[d];
+          lfal[d][c] = al[d];
+        }
+      }
+    }
+    // Lax-Friedrichs ghost faces: a face beyond the grid takes the nearest
+    // interior face (lf_ghost); threads whose windows reach past an edge
+    const bool lfe1 = SCH != 0 && (ci1 < 3u || ci1 + 3u > n1 - 1u);
+    const bool lfe2 = SCH != 0 && (ci2 < 3u || ci2 + 3u > n2 - 1u);
+    const bool lfe3 = SCH != 0 && (i3 < 3u || i3 + 4u > n3 - 1u);
     auto flux = [&](auto dc, int c, double dm, double dp) -> double {
       constexpr int d = decltype(dc)::value;
       if (S::LIN(d)) return pos_[d][c] * (up[d][c] ? dp : dm);
@@ -1961,6 +1994,7 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
         double f6[6];
 #pragma unroll
         for (int q = 0; q < 6; ++q) f6[q] = (w[q + 1][c] - w[q][c]) * inv0;
+        if (SCH != 0) lf_ghost<6>(f6, (int)c0 - 3, (int)n0 - 2);
         double unused;
         eno3_face(f6[0], f6[1], f6[2], f6[3], f6[4], unused, dmc[c]);
 #pragma unroll
@@ -1993,12 +2027,18 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
       }
       rv[7] = lds1(slot + own + 32);
       double hh[kK];
+      double dmv[4][kK], dpv[4][kK];  // Lax-Friedrichs: all pairs of the cell
       // axis 0: choice at face a(i0) -> D+ of i0 and D- of i0+1
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
         double dp, dmn;
         eno3_face(F[0][c], F[1][c], F[2][c], F[3][c], F[4][c], dp, dmn);
-        hh[c] = flux(std::integral_constant<int, 0>{}, c, dmc[c], dp);
+        if (SCH == 0) {
+          hh[c] = flux(std::integral_constant<int, 0>{}, c, dmc[c], dp);
+        } else {
+          dmv[0][c] = dmc[c];
+          dpv[0][c] = dp;
+        }
         dmc[c] = dmn;
       }
       // axes 1 and 2: per cell, six faces from the box
@@ -2021,11 +2061,18 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
           double A[6];
 #pragma unroll
           for (int q = 0; q < 6; ++q) A[q] = (nv[q + 1][c] - nv[q][c]) * inv;
+          if (SCH != 0 && (ax == 1 ? lfe1 : lfe2))
+            lf_ghost<6>(A, (int)(ax == 1 ? ci1 : ci2) - 3, (int)(ax == 1 ? n1 : n2) - 2);
           double dm, dp;
           eno_faces<R>(A, dm, dp);
-          const double h = ax == 1 ? flux(std::integral_constant<int, 1>{}, c, dm, dp)
-                                   : flux(std::integral_constant<int, 2>{}, c, dm, dp);
-          hh[c] = hh[c] + h;
+          if (SCH == 0) {
+            const double h = ax == 1 ? flux(std::integral_constant<int, 1>{}, c, dm, dp)
+                                     : flux(std::integral_constant<int, 2>{}, c, dm, dp);
+            hh[c] = hh[c] + h;
+          } else {
+            dmv[ax][c] = dm;
+            dpv[ax][c] = dp;
+          }
         }
       }
       // axis 3: faces a(i3-3) .. a(i3+3); choices at faces i3-1, i3, i3+1
@@ -2033,12 +2080,32 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
         double f[7];
 #pragma unroll
         for (int q = 0; q < 7; ++q) f[q] = (rv[q + 1] - rv[q]) * inv3;
+        if (SCH != 0 && lfe3) lf_ghost<7>(f, (int)i3 - 3, (int)n3 - 2);
         double x0, dm0, dp0, dm1, dp1, x1;
         eno3_face(f[0], f[1], f[2], f[3], f[4], x0, dm0);
         eno3_face(f[1], f[2], f[3], f[4], f[5], dp0, dm1);
         eno3_face(f[2], f[3], f[4], f[5], f[6], dp1, x1);
-        hh[0] = hh[0] + flux(std::integral_constant<int, 3>{}, 0, dm0, dp0);
-        hh[1] = hh[1] + flux(std::integral_constant<int, 3>{}, 1, dm1, dp1);
+        if (SCH == 0) {
+          hh[0] = hh[0] + flux(std::integral_constant<int, 3>{}, 0, dm0, dp0);
+          hh[1] = hh[1] + flux(std::integral_constant<int, 3>{}, 1, dm1, dp1);
+        } else {
+          dmv[3][0] = dm0;
+          dpv[3][0] = dp0;
+          dmv[3][1] = dm1;
+          dpv[3][1] = dp1;
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            double dm4[4], dp4[4], drc[4], alc[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+              dm4[d] = dmv[d][c];
+              dp4[d] = dpv[d][c];
+              drc[d] = lfdr[d][c];
+              alc[d] = lfal[d][c];
+            }
+            hh[c] = lf_hhat<S>(a.lp, dm4, dp4, drc, alc);
+          }
+        }
       }
       double ccv[kK], vnv[kK], vnx[kK];
       lds_k<kK>(slot + town, ccv);
@@ -2101,6 +2168,7 @@ __global__ void __launch_bounds__(kEno3gThreads, 1) k_eno3g(const __grid_constan
 #pragma unroll
         for (int q = 0; q < 4; ++q) F[q][c] = F[q + 1][c];
         F[4][c] = (vnx[c] - vlast[c]) * inv0;
+        if (SCH != 0 && i0 + 3 > n0 - 2) F[4][c] = F[3][c];  // face a(i0+3) past the edge
         vlast[c] = vnx[c];
       }
     }
@@ -2487,10 +2555,10 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
     const char* ek = std::getenv("HJB_HO_KC");
     a.kc = (ek && std::atoi(ek) == 1 && a.lf == 0) ? 1u : 2u;  // LF: 2-cell pencils
     const char* eg = std::getenv("HJB_HO_ENO3G");
-    a.eno3g = (R == 3 && a.lf == 0 && a.kc == 2 && !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
+    a.eno3g = (R == 3 && a.kc == 2 && !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
     const uint32_t nbar = 2u;  // mbarriers per ring slot
     const uint32_t maxc =
-        (uint32_t)(a.eno3g ? kEno3gThreads : ho4t_maxthreads(a.order, (int)a.kc)) - 32;
+        (uint32_t)(a.eno3g ? eno3g_threads(a.lf) : ho4t_maxthreads(a.order, (int)a.kc)) - 32;
     // tiles cover T1 x T2 rows x a T3-cell segment of axis 3; the box adds
     // R rows in i1, i2 and H3 = R rounded up to even cells on each side of
     // the segment (16-byte aligned pencils).  Minimise the grid traffic:
@@ -2601,6 +2669,16 @@ void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
+template <class S, int SCH>
+void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_eno3g<S, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_eno3g<S, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
+}
+
 template <class S, int R>
 void ho4t_launch(const Ho4dArgs& a, cudaStream_t s) {
   if (a.lf == 1)  // Lax-Friedrichs: 2-cell pencils (ho_solve forces kc = 2)
@@ -2621,13 +2699,12 @@ cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
       case 2: ho4t_launch<S, 2>(a, s); break;
       default:
         if (a.eno3g) {
-          static bool attr = false;
-          if (!attr) {
-            cudaFuncSetAttribute(k_eno3g<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024);
-            attr = true;
-          }
-          k_eno3g<S><<<a.blocks, a.threads, a.smem, s>>>(a);
+          if (a.lf == 1)
+            eno3g_launch<S, 1>(a, s);
+          else if (a.lf == 2)
+            eno3g_launch<S, 2>(a, s);
+          else
+            eno3g_launch<S, 0>(a, s);
         } else {
           ho4t_launch<S, 3>(a, s);
         }
