@@ -187,9 +187,9 @@ int ho_stages(int rk, HoStage* st) {
 // exchanged before every stage, k_ho4t/k_ho4d over the owned
 // planes, all-reduce(max) + epilogue after the last stage of a step.
 int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared& p,
-                     const hjb_solve_config* cfg, double dt, uint32_t owned, bool has_lo,
-                     bool has_hi, const double* init_slab, const double* c_slab,
-                     double* value_slab_out, hjb_solve_result* res) {
+                     const hjb_solve_config* cfg, double dt, const double* galpha,
+                     uint32_t owned, bool has_lo, bool has_hi, const double* init_slab,
+                     const double* c_slab, double* value_slab_out, hjb_solve_result* res) {
   const int r = comm->rank;
   const uint32_t R = cfg->spatial_order < 1 ? 1u : (uint32_t)cfg->spatial_order;
   if ((has_lo || has_hi) && owned < R)
@@ -202,7 +202,11 @@ int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared
   h.order = (int)(R > 3 ? 3 : R);
   h.cbeg = has_lo ? R : 0u;
   h.cend = h.cbeg + owned;
+  // Lax-Friedrichs: the global alphas come from the all-reduced scan
+  fill_lf(p.hm.dm, scheme_of(cfg), galpha, h.lf, h.lp);
   ho4d_config(gloc, sm_count(ctx->device), h);
+  if (h.lf && !h.tma)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: Lax-Friedrichs high order needs the TMA kernels");
   const uint64_t plane = ho4d_plane(h);  // stage-buffer plane (ghost layout of h)
   const size_t lbytes = static_cast<size_t>(nloc) * plane * sizeof(double);
   DevBuf* bufs[4] = {&ctx->v0, &ctx->v1, &ctx->v2, &ctx->v3};
@@ -497,11 +501,9 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   if (p.shape < 0)
     return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
   const bool high_order = cfg->spatial_order > 1 || cfg->time_order > 1;
-  if (high_order && cfg->scheme != HJB_GODUNOV)
-    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: high-order schemes with Godunov only");
-  // first order: the scheme's own variant of the fast path
+  // the scheme's own variant of the fast path (first and high order)
   const int scheme = scheme_of(cfg);
-  if (!high_order && fast4d_shape(p.g, p.hm.dm, scheme) != p.shape)
+  if (fast4d_shape(p.g, p.hm.dm, scheme) != p.shape)
     return set_err(HJB_ERR_UNSUPPORTED,
                    "solve_sharded: Lax-Friedrichs needs one input term per row of the 4D model");
   Nccl* api = nccl();
@@ -553,7 +555,8 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   }
 
   if (high_order)
-    return solve_sharded_ho(ctx, comm, api, p, cfg, dt, owned, has_lo, has_hi, init_slab, c_slab,
+    return solve_sharded_ho(ctx, comm, api, p, cfg, dt, s.max_alpha, owned, has_lo, has_hi,
+                            init_slab, c_slab,
                             value_slab_out, res);
 
   // local padded slab arrays: [halo_lo?][owned][halo_hi?]

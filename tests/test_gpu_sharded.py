@@ -97,11 +97,15 @@ def test_ho_slab_stages_compose_to_full_stage(gpu_ctx, oracle, world, order, kin
     assert max(maxes) == want_dv
 
 
+@pytest.mark.parametrize("scheme,diss", [(hj.GODUNOV, hj.PER_NODE), (hj.LAX_FRIEDRICHS, hj.PER_NODE),
+                                         (hj.LAX_FRIEDRICHS, hj.GLOBAL)],
+                         ids=["godunov", "lf_per_node", "lf_global"])
 @pytest.mark.parametrize("order,rk", [(2, 2), (3, 3)])
-def test_sharded_single_rank_high_order_equals_solve(gpu_ctx, order, rk):
+def test_sharded_single_rank_high_order_equals_solve(gpu_ctx, order, rk, scheme, diss):
     w = configs.config2(17)
     c = band_np(w.grid, 0, -4.0, 4.0)
-    cfg = hj.SolveConfig(tolerance=1e-5, max_iters=40, spatial_order=order, time_order=rk)
+    cfg = hj.SolveConfig(tolerance=1e-5, max_iters=40, spatial_order=order, time_order=rk,
+                         scheme=scheme, dissipation=diss)
     ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
                    ctx=gpu_ctx)
     ct = torch.tensor(c, device="cuda")
