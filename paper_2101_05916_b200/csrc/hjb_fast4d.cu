@@ -1970,6 +1970,15 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
     const bool lfe1 = SCH != 0 && (ci1 < 3u || ci1 + 3u > n1 - 1u);
     const bool lfe2 = SCH != 0 && (ci2 < 3u || ci2 + 3u > n2 - 1u);
     const bool lfe3 = SCH != 0 && (i3 < 3u || i3 + 4u > n3 - 1u);
+    // linear rows 1, 2: start of the upwind six-value window (byte offset in
+    // the box; D+ uses V(i-2 .. i+3), D- V(i-3 .. i+2))
+    uint32_t uoff[3][kK];
+#pragma unroll
+    for (int d = 1; d <= 2; ++d) {
+      const int step = d == 1 ? (int)(W2 * rowb) : (int)rowb;
+#pragma unroll
+      for (int c = 0; c < kK; ++c) uoff[d][c] = own + 8u * c + (uint32_t)((up[d][c] ? -2 : -3) * step);
+    }
     auto flux = [&](auto dc, int c, double dm, double dp) -> double {
       constexpr int d = decltype(dc)::value;
       if (S::LIN(d)) return pos_[d][c] * (up[d][c] ? dp : dm);
@@ -2042,39 +2051,65 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
         dmc[c] = dmn;
       }
       // axes 1 and 2: per cell, six faces from the box
-#pragma unroll
-      for (int ax = 1; ax <= 2; ++ax) {
+      auto axis12 = [&](auto axc) {
+        constexpr int ax = decltype(axc)::value;
         const int step = ax == 1 ? (int)(W2 * rowb) : (int)rowb;
         const double inv = ax == 1 ? inv1 : inv2;
-        double nv[7][kK];
+        if constexpr (SCH == 0 && S::LIN(ax)) {
+          // linear row (Godunov flux s * (s >= 0 ? D+ : D-)): only the upwind
+          // derivative is used, so one ENO choice per cell — at face i for D+,
+          // at face i-1 for D- — on the six values from uoff (loop invariant)
+          constexpr bool pc = S::A(ax) == 3 || S::B(ax) == 3;
+          double w6[6][kK];
 #pragma unroll
-        for (int q = 0; q < 7; ++q) {
-          if (q == 3) {
-            nv[q][0] = rv[3];
-            nv[q][1] = rv[4];
-          } else {
-            lds_k<kK>(slot + own + (q - 3) * step, nv[q]);
+          for (int q = 0; q < 6; ++q) {
+            if (pc) {
+#pragma unroll
+              for (int c = 0; c < kK; ++c) w6[q][c] = lds1(slot + uoff[ax][c] + q * step);
+            } else {
+              lds_k<kK>(slot + uoff[ax][0] + q * step, w6[q]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            double e[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) e[q] = (w6[q + 1][c] - w6[q][c]) * inv;
+            double dpl, dmr;
+            eno3_face(e[0], e[1], e[2], e[3], e[4], dpl, dmr);
+            hh[c] = hh[c] + pos_[ax][c] * (up[ax][c] ? dpl : dmr);
+          }
+        } else {
+          double nv[7][kK];
+#pragma unroll
+          for (int q = 0; q < 7; ++q) {
+            if (q == 3) {
+              nv[q][0] = rv[3];
+              nv[q][1] = rv[4];
+            } else {
+              lds_k<kK>(slot + own + (q - 3) * step, nv[q]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            double A[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) A[q] = (nv[q + 1][c] - nv[q][c]) * inv;
+            if (SCH != 0 && (ax == 1 ? lfe1 : lfe2))
+              lf_ghost<6>(A, (int)(ax == 1 ? ci1 : ci2) - 3, (int)(ax == 1 ? n1 : n2) - 2);
+            double dm, dp;
+            eno_faces<R>(A, dm, dp);
+            if (SCH == 0) {
+              hh[c] = hh[c] + flux(axc, c, dm, dp);
+            } else {
+              dmv[ax][c] = dm;
+              dpv[ax][c] = dp;
+            }
           }
         }
-#pragma unroll
-        for (int c = 0; c < kK; ++c) {
-          double A[6];
-#pragma unroll
-          for (int q = 0; q < 6; ++q) A[q] = (nv[q + 1][c] - nv[q][c]) * inv;
-          if (SCH != 0 && (ax == 1 ? lfe1 : lfe2))
-            lf_ghost<6>(A, (int)(ax == 1 ? ci1 : ci2) - 3, (int)(ax == 1 ? n1 : n2) - 2);
-          double dm, dp;
-          eno_faces<R>(A, dm, dp);
-          if (SCH == 0) {
-            const double h = ax == 1 ? flux(std::integral_constant<int, 1>{}, c, dm, dp)
-                                     : flux(std::integral_constant<int, 2>{}, c, dm, dp);
-            hh[c] = hh[c] + h;
-          } else {
-            dmv[ax][c] = dm;
-            dpv[ax][c] = dp;
-          }
-        }
-      }
+      };
+      axis12(std::integral_constant<int, 1>{});
+      axis12(std::integral_constant<int, 2>{});
       // axis 3: faces a(i3-3) .. a(i3+3); choices at faces i3-1, i3, i3+1
       {
         double f[7];
