@@ -678,6 +678,36 @@ static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
   return HJB_OK;
 }
 
+int hjb::constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c,
+                           const double** out) {
+  *out = nullptr;
+  // policy: the table pays where the sweep streams from HBM (working set
+  // V front/back + c beyond twice the L2); measured at 71^4 / 101^4 8-11 %
+  // faster, at 51^4 (working set ~L2) within noise.  HJB_CPLANE=0/1 forces.
+  const char* e = std::getenv("HJB_CPLANE");
+  if ((e && std::strcmp(e, "0") == 0) || g.nd < 2) return HJB_OK;
+  if (!(e && std::strcmp(e, "1") == 0)) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+    if (static_cast<double>(g.size) * 24.0 <= 2.0 * l2) return HJB_OK;
+  }
+  const uint32_t s0 = g.stride[0], n0 = g.n[0];
+  CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
+  unsigned int* flag = reinterpret_cast<unsigned int*>(ctx->scratch.d() + 48);
+  CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(unsigned int), ctx->stream));
+  CUDA_TRY(launch_not_axis0(c, g.size, s0, flag, ctx->stream));
+  ++ctx->launches;
+  unsigned int hf = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hf, flag, sizeof hf, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (hf) return HJB_OK;
+  CUDA_TRY(ctx->cplane.ensure(static_cast<size_t>(n0) * sizeof(double)));
+  CUDA_TRY(cudaMemcpy2DAsync(ctx->cplane.d(), sizeof(double), c, s0 * sizeof(double),
+                             sizeof(double), n0, cudaMemcpyDeviceToDevice, ctx->stream));
+  *out = ctx->cplane.d();
+  return HJB_OK;
+}
+
 static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
                       const hjb_dbounds* db_in, const double* init, const double* c,
                       const hjb_solve_config* cfg, double* value_out, hjb_solve_result* res) {
@@ -772,8 +802,12 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     if ((rc = fast4d_choose(ctx, g, shape, init, c, f))) return rc;
     rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
     CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
-    CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
-    ctx->launches += 2;
+    ++ctx->launches;
+    if ((rc = constraint_planes(ctx, g, c, &f.cplane))) return rc;
+    if (!f.cplane) {
+      CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
+      ++ctx->launches;
+    }
     f.c = ctx->pcbuf.d();
     f.buf0 = ctx->v2.d();
     f.buf1 = ctx->v3.d();

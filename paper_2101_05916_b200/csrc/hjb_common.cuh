@@ -58,6 +58,7 @@ struct hjb_context {
   hjb::DevBuf gpa, gpb, gpc;  // GP bounds: k*, factor, per-point tables
   hjb::DevBuf pvtab;          // 4D fast path with axis-0-varying bounds: tables
   hjb::DevBuf pnbuf;          // 4D fast path with per-node bounds: padded lo / hi
+  hjb::DevBuf cplane;         // constraint varying along axis 0 only: c per plane
   hjb::LoopState* st = nullptr;
   hjb::LoopState* st_host = nullptr;  // pinned mirror
   long long launches = 0;

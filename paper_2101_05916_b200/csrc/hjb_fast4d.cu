@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(MAXT, 1)
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hdr0 + sl * 8),
                          "r"(t1 * a.tiles2 + t2), "r"(c0 | (c1 << 16))
                          : "memory");
-          const bool has_c = p >= c0 && p < c1;
+          const bool has_c = !a.cplane && p >= c0 && p < c1;
           mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes + (has_c ? a.cbox_bytes : 0u));
           tma_load4(vring + sl * a.vslot_bytes, vmap, 0, base2 - 1, base1 - 1, (int)p,
                     bars + sl * 8);
@@ -779,7 +779,13 @@ __global__ void __launch_bounds__(MAXT, 1)
           for (int c = 0; c < kK; ++c) vn[c] = v[c];  // D+ at the i0 = n0-1 edge: +0
         }
         double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
-        lds_cells<kK>(csl + cown, cc);
+        if (a.cplane) {
+          const double cp = __ldg(a.cplane + i0);
+#pragma unroll
+          for (int c = 0; c < kK; ++c) cc[c] = cp;
+        } else {
+          lds_cells<kK>(csl + cown, cc);
+        }
         if (SCH == 0 && S::LIN(1)) {  // upwind neighbour only (n1p holds it)
           if (pc1) {
 #pragma unroll
@@ -1881,9 +1887,10 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
         const uint32_t dst0 = smem0 + sl * a.vslot_bytes, bar = bars + sl * 8;
         const int p = (int)(c0 + q), pa = min(p + 4, (int)n0 - 1);
         mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
-        mbar_arrive_expect_tx(bar, a.vbox_bytes + (need_vn ? 3u : 2u) * a.tbox_bytes);
+        mbar_arrive_expect_tx(
+            bar, a.vbox_bytes + ((need_vn ? 2u : 1u) + (a.cplane ? 0u : 1u)) * a.tbox_bytes);
         tma_load4(dst0, &a.mapv[msel], (int)base3, (int)base2, (int)base1, p, bar);
-        tma_load4(dst0 + vbs, &a.mapc, x3, x2, x1, p, bar);
+        if (!a.cplane) tma_load4(dst0 + vbs, &a.mapc, x3, x2, x1, p, bar);
         if (need_vn) tma_load4(dst0 + vbs + a.tbox_slot, &a.mapt[vsel], x3, x2, x1, p, bar);
         tma_load4(dst0 + vbs + 2 * a.tbox_slot, &a.mapt[msel], x3, x2, x1, pa, bar);
       }
@@ -2143,7 +2150,11 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
         }
       }
       double ccv[kK], vnv[kK], vnx[kK];
-      lds_k<kK>(slot + town, ccv);
+      if (a.cplane) {
+        ccv[0] = ccv[1] = __ldg(a.cplane + i0);
+      } else {
+        lds_k<kK>(slot + town, ccv);
+      }
       if (need_vn) {
         lds_k<kK>(slot + town + a.tbox_slot, vnv);
       } else {

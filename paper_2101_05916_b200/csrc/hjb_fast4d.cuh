@@ -44,6 +44,9 @@ struct Fast4dArgs {
   int tab_staged;       // 1: tables staged in shared memory, 0: read from global
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
   const double* c;  // padded constraint
+  // constraint that varies along axis 0 only (signed distance to a set in
+  // x0, every BASELINE 4D config): c[i0] per plane, the padded field unused
+  const double* cplane;
   double* buf0;
   double* buf1;
   const double* src;
@@ -90,6 +93,7 @@ struct Ho4dArgs {
   const double* tab;
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
   const double* c;
+  const double* cplane;  // as Fast4dArgs::cplane (k_eno3g); null = per-node c
   double* buf0;  // V_n ping-pong (parity = st->iter)
   double* buf1;
   double* stage1;

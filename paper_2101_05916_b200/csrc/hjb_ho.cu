@@ -98,8 +98,13 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   if (shape >= 0) {
     CUDA_TRY(ctx->pcbuf.ensure(pbytes));
     CUDA_TRY(ho4d_pad(init, ctx->v0.d(), g.n[0], h4, ctx->stream));
-    CUDA_TRY(ho4d_pad(c, ctx->pcbuf.d(), g.n[0], h4, ctx->stream));
-    ctx->launches += 2;
+    ++ctx->launches;
+    int rcp;
+    if (h4.eno3g && (rcp = constraint_planes(ctx, g, c, &h4.cplane))) return rcp;
+    if (!h4.cplane) {
+      CUDA_TRY(ho4d_pad(c, ctx->pcbuf.d(), g.n[0], h4, ctx->stream));
+      ++ctx->launches;
+    }
   } else {
     CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   }

@@ -407,3 +407,22 @@ def test_fast4d_per_node_bounds(gpu_ctx, oracle, monkeypatch, case, spread):
     monkeypatch.setenv("HJB_PN", "0")
     gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
     assert same(gen.value.values(), got.value.values())
+
+
+@pytest.mark.parametrize("order,rk", [(1, 1), (3, 3)])
+def test_constraint_plane_table_matches_field(gpu_ctx, oracle, monkeypatch, order, rk):
+    """A constraint that varies along axis 0 only (every BASELINE 4D config)
+    is read from a per-plane table; the result equals the per-node path
+    (HJB_CPLANE=0) and the oracle bitwise."""
+    case = with_iters(workload_case(configs.config2(23)), 12)
+    cfg = hj.SolveConfig(**case.cfg.__dict__)
+    cfg.spatial_order, cfg.time_order = order, rk
+    init, c = case.init_field(), case.c_field()
+    monkeypatch.setenv("HJB_CPLANE", "1")
+    got = hj.solve(init, c, case.model, case.db, cfg, ctx=gpu_ctx)
+    want = oracle.solve(init, c, case.model, case.db, cfg)
+    assert same(got.value.values(), want.value.values())
+    assert same(got.residual_history, want.residual_history)
+    monkeypatch.setenv("HJB_CPLANE", "0")
+    per_node = hj.solve(init, c, case.model, case.db, cfg, ctx=gpu_ctx)
+    assert same(per_node.value.values(), got.value.values())
