@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -2491,14 +2492,20 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   if (a.bal) a.blocks = std::min<uint32_t>(static_cast<uint32_t>(sms), tiles * span);
 }
 
+// Function attributes are per device: set them once per device (thread safe)
+static bool first_on_device(std::atomic<unsigned long long>& done) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  return !(done.fetch_or(bit) & bit);
+}
+
 template <class S, int K, int MAXT, int SCH = 0, int PV = 0>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH, PV>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
   if (a.l2_bytes == 0 && !a.pdl) {
     k_fast4d<S, K, MAXT, SCH, PV><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
@@ -2706,22 +2713,18 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
 namespace {
 template <class S, int R, int KC, int SCH = 0>
 void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k_ho4t<S, R, KC, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr = true;
-  }
   k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
 template <class S, int SCH>
 void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k_eno3g<S, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
   k_eno3g<S, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
