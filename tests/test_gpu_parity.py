@@ -255,7 +255,7 @@ def test_max_iters_zero_and_time_horizon(gpu_ctx, oracle):
     want = oracle.solve(init, case.c_field(), case.model, case.db, cfg)
     assert got.iterations == want.iterations == 0
     assert same(got.value.values(), init.values())
-    for order in (1, 2):
+    for order in (1, 2, 3):
         cfg = hj.SolveConfig(tolerance=1e-9, max_iters=1000, time_horizon=0.05,
                              spatial_order=order, time_order=order)
         want = oracle.solve(case.c_field(), case.c_field(), case.model, case.db, cfg)
