@@ -803,7 +803,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
     CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
     ++ctx->launches;
-    if ((rc = constraint_planes(ctx, g, c, &f.cplane))) return rc;
+    if (!f.lf && !f.pv && (rc = constraint_planes(ctx, g, c, &f.cplane))) return rc;
     if (!f.cplane) {
       CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
       ++ctx->launches;

@@ -419,7 +419,7 @@ __device__ __forceinline__ void lds_pn(const double* p, double* v) {
   }
 }
 
-template <class S, int kK, int MAXT, int SCH, int PV = 0>
+template <class S, int kK, int MAXT, int SCH, int PV = 0, bool CP = false>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(MAXT, 1)
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hdr0 + sl * 8),
                          "r"(t1 * a.tiles2 + t2), "r"(c0 | (c1 << 16))
                          : "memory");
-          const bool has_c = !a.cplane && p >= c0 && p < c1;
+          const bool has_c = !CP && p >= c0 && p < c1;
           mbar_arrive_expect_tx(bars + sl * 8, a.vbox_bytes + (has_c ? a.cbox_bytes : 0u));
           tma_load4(vring + sl * a.vslot_bytes, vmap, 0, base2 - 1, base1 - 1, (int)p,
                     bars + sl * 8);
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(MAXT, 1)
           for (int c = 0; c < kK; ++c) vn[c] = v[c];  // D+ at the i0 = n0-1 edge: +0
         }
         double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
-        if (a.cplane) {
+        if (CP) {  // constraint per plane (Fast4dArgs::cplane)
           const double cp = __ldg(a.cplane + i0);
 #pragma unroll
           for (int c = 0; c < kK; ++c) cc[c] = cp;
@@ -1832,7 +1832,7 @@ __host__ __device__ constexpr int eno3g_threads(int sch) {
   return sch ? kEno3gThreadsLF : kEno3gThreads;
 }
 
-template <class S, int SCH = 0>
+template <class S, int SCH = 0, bool CP = false>
 __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
     k_eno3g(const __grid_constant__ Ho4dArgs a) {
   constexpr int R = 3, kK = 2;
@@ -1889,9 +1889,9 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
         const int p = (int)(c0 + q), pa = min(p + 4, (int)n0 - 1);
         mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
         mbar_arrive_expect_tx(
-            bar, a.vbox_bytes + ((need_vn ? 2u : 1u) + (a.cplane ? 0u : 1u)) * a.tbox_bytes);
+            bar, a.vbox_bytes + ((need_vn ? 2u : 1u) + (CP ? 0u : 1u)) * a.tbox_bytes);
         tma_load4(dst0, &a.mapv[msel], (int)base3, (int)base2, (int)base1, p, bar);
-        if (!a.cplane) tma_load4(dst0 + vbs, &a.mapc, x3, x2, x1, p, bar);
+        if (!CP) tma_load4(dst0 + vbs, &a.mapc, x3, x2, x1, p, bar);
         if (need_vn) tma_load4(dst0 + vbs + a.tbox_slot, &a.mapt[vsel], x3, x2, x1, p, bar);
         tma_load4(dst0 + vbs + 2 * a.tbox_slot, &a.mapt[msel], x3, x2, x1, pa, bar);
       }
@@ -2151,7 +2151,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
         }
       }
       double ccv[kK], vnv[kK], vnx[kK];
-      if (a.cplane) {
+      if (CP) {  // constraint per plane (Ho4dArgs::cplane)
         ccv[0] = ccv[1] = __ldg(a.cplane + i0);
       } else {
         lds_k<kK>(slot + town, ccv);
@@ -2500,14 +2500,14 @@ static bool first_on_device(std::atomic<unsigned long long>& done) {
   return !(done.fetch_or(bit) & bit);
 }
 
-template <class S, int K, int MAXT, int SCH = 0, int PV = 0>
+template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
-    cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH, PV>,
+    cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH, PV, CP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (a.l2_bytes == 0 && !a.pdl) {
-    k_fast4d<S, K, MAXT, SCH, PV><<<a.blocks, a.threads, a.smem, s>>>(a);
+    k_fast4d<S, K, MAXT, SCH, PV, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -2533,7 +2533,7 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV>, a);
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
@@ -2556,12 +2556,15 @@ static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
     launch_one<S, 2, 448, 2>(a, s);
     return;
   }
+  // per-plane constraint (Godunov, constant bounds only): its own instantiation
+  // so the per-node path keeps its code unchanged
+  const bool cp = a.cplane != nullptr;
   if (a.kcells == 4)
-    launch_one<S, 4, 384>(a, s);
+    cp ? launch_one<S, 4, 384, 0, 0, true>(a, s) : launch_one<S, 4, 384>(a, s);
   else if (a.maxthreads == 448)
-    launch_one<S, 2, 448>(a, s);
+    cp ? launch_one<S, 2, 448, 0, 0, true>(a, s) : launch_one<S, 2, 448>(a, s);
   else
-    launch_one<S, 2, 576>(a, s);
+    cp ? launch_one<S, 2, 576, 0, 0, true>(a, s) : launch_one<S, 2, 576>(a, s);
 }
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
@@ -2720,12 +2723,13 @@ void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
-template <class S, int SCH>
+template <class S, int SCH, bool CP = false>
 void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
-    cudaFuncSetAttribute(k_eno3g<S, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_eno3g<S, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
+    cudaFuncSetAttribute(k_eno3g<S, SCH, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+  k_eno3g<S, SCH, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
 template <class S, int R>
@@ -2752,6 +2756,8 @@ cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
             eno3g_launch<S, 1>(a, s);
           else if (a.lf == 2)
             eno3g_launch<S, 2>(a, s);
+          else if (a.cplane)  // per-plane constraint: Godunov only
+            eno3g_launch<S, 0, true>(a, s);
           else
             eno3g_launch<S, 0>(a, s);
         } else {
