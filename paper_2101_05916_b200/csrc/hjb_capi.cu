@@ -681,16 +681,12 @@ static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
 int hjb::constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c,
                            const double** out) {
   *out = nullptr;
-  // policy: the table pays where the sweep streams from HBM (working set
-  // V front/back + c beyond twice the L2); measured at 71^4 / 101^4 8-11 %
-  // faster, at 51^4 (working set ~L2) within noise.  HJB_CPLANE=0/1 forces.
+  // opt-in (HJB_CPLANE=1): measured in interleaved best-of-4 runs, the
+  // per-node field is faster at 71^4 / 101^4 (118 vs 130 us, 436 vs 475 us)
+  // and equal in sustained power-capped runs, although the table saves a
+  // third of the DRAM bytes (the sweep then becomes issue-bound)
   const char* e = std::getenv("HJB_CPLANE");
-  if ((e && std::strcmp(e, "0") == 0) || g.nd < 2) return HJB_OK;
-  if (!(e && std::strcmp(e, "1") == 0)) {
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
-    if (static_cast<double>(g.size) * 24.0 <= 2.0 * l2) return HJB_OK;
-  }
+  if (!(e && std::strcmp(e, "1") == 0) || g.nd < 2) return HJB_OK;
   const uint32_t s0 = g.stride[0], n0 = g.n[0];
   CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
   unsigned int* flag = reinterpret_cast<unsigned int*>(ctx->scratch.d() + 48);

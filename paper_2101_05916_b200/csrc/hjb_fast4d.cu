@@ -2492,20 +2492,23 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   if (a.bal) a.blocks = std::min<uint32_t>(static_cast<uint32_t>(sms), tiles * span);
 }
 
-// Function attributes are per device: set them once per device (thread safe)
-static bool first_on_device(std::atomic<unsigned long long>& done) {
+// Function attributes are per device: set the dynamic shared-memory limit
+// once per device.  The bit is published only after the attribute is set, so
+// a concurrent launcher either sees it set or sets it again (idempotent).
+template <class K>
+static void smem_attr_once(std::atomic<unsigned long long>& done, K kernel) {
   int d = 0;
   cudaGetDevice(&d);
   const unsigned long long bit = 1ull << (d & 63);
-  return !(done.fetch_or(bit) & bit);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(k_fast4d<S, K, MAXT, SCH, PV, CP>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP>);
   if (a.l2_bytes == 0 && !a.pdl) {
     k_fast4d<S, K, MAXT, SCH, PV, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
@@ -2717,18 +2720,14 @@ namespace {
 template <class S, int R, int KC, int SCH = 0>
 void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(k_ho4t<S, R, KC, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+  smem_attr_once(attr, k_ho4t<S, R, KC, SCH>);
   k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
 template <class S, int SCH, bool CP = false>
 void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(k_eno3g<S, SCH, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+  smem_attr_once(attr, k_eno3g<S, SCH, CP>);
   k_eno3g<S, SCH, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 

@@ -41,8 +41,8 @@ int scheme_of(const hjb_solve_config* cfg);
 // Lax-Friedrichs fields of Fast4dArgs (f.lf = 0 for Godunov)
 void fill_lf(const DevModel& m, int scheme, const double* galpha, Fast4dArgs& f);
 // When the constraint c (reference layout, device) varies along axis 0 only
-// (bit for bit), its per-plane values in ctx->cplane; else null.  Used
-// where the working set exceeds twice the L2 (HJB_CPLANE=0/1 forces).
+// (bit for bit), its per-plane values in ctx->cplane; else null.  Opt-in
+// (HJB_CPLANE=1): measured no faster than the per-node field.
 int constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c, const double** out);
 void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfParams& lp);
 // Device iteration loop: WHILE-conditional CUDA graph (or HJB_LOOP=poll);

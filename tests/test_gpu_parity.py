@@ -426,3 +426,41 @@ def test_constraint_plane_table_matches_field(gpu_ctx, oracle, monkeypatch, orde
     monkeypatch.setenv("HJB_CPLANE", "0")
     per_node = hj.solve(init, c, case.model, case.db, cfg, ctx=gpu_ctx)
     assert same(per_node.value.values(), got.value.values())
+
+
+def test_concurrent_first_launches_in_fresh_process():
+    """Several host threads (one context each, the reference's concurrent
+    subsystem jobs, sim.cpp:340-363) launching the TMA kernels for the first
+    time in a fresh process: the per-device kernel attributes must be set
+    before any of them launches."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = r'''
+import sys, threading
+sys.path.insert(0, sys.argv[1])
+from paper_2101_05916_b200 import configs
+from paper_2101_05916_b200 import hjsafe as hj
+w = configs.config2(21)
+ctxs = [hj.Context(0) for _ in range(4)]
+errs = []
+def job(k):
+    try:
+        cfg = hj.SolveConfig(**w.cfg.__dict__)
+        cfg.max_iters = 5
+        if k % 2:
+            cfg.spatial_order, cfg.time_order = 3, 3
+        c = hj.signed_distance_band(w.grid, 0, -4.0, 4.0, ctx=ctxs[k])
+        hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=ctxs[k])
+    except Exception as e:
+        errs.append(repr(e))
+th = [threading.Thread(target=job, args=(k,)) for k in range(4)]
+[t.start() for t in th]
+[t.join() for t in th]
+assert not errs, errs
+print("ok")
+'''
+    root = str(Path(__file__).resolve().parent.parent)
+    r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
