@@ -384,6 +384,10 @@ class Reference:
         L.hjr_solve_coarse_to_fine.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds), _vp,
                                                P(abi.HjbGrid), P(abi.HjbSolveConfig), _vp, _vp,
                                                P(RefResult), _vp, P(RefResult)] + E
+        L.hjr_solve_coarse_to_fine_w.argtypes = [P(abi.HjbGrid), P(ModelSpec), P(abi.HjbDbounds),
+                                                 _vp, P(abi.HjbGrid), P(abi.HjbSolveConfig),
+                                                 C.c_void_p, _vp, _vp, P(RefResult), _vp,
+                                                 P(RefResult)] + E
         L.hjr_resample.argtypes = [P(abi.HjbGrid), _vp, P(abi.HjbGrid), _vp] + E
         L.hjr_max_adjacent_jump.argtypes = [P(abi.HjbGrid), _vp, P(_d)] + E
         L.hjr_signed_distance_band.argtypes = [P(abi.HjbGrid), C.c_int32, _d, _d, _vp] + E
@@ -438,6 +442,10 @@ class Reference:
                               residual_history=hist[:n].copy(), nodes_per_sweep=int(r.nodes_per_sweep))
 
     def solve_coarse_to_fine(self, c_fine, model, db, coarse_grid, cfg, warm=None):
+        """The reference's own ``solve_coarse_to_fine`` (solver.cpp:387-425).
+
+        ``warm`` is a ScalarField on ANY grid (the reference's seed_from
+        resamples from the warm field's own grid, :404-414)."""
         fg = c_fine.grid()
         cap = int(cfg.max_iters)
         res = []
@@ -451,8 +459,11 @@ class Reference:
         fout = np.empty(fg.size())
         g, cg, m, d, k = fg.to_c(), coarse_grid.to_c(), model_spec(model), db.to_c(), cfg.to_c()
         wv = _vals(warm) if warm is not None else None
-        self._call(self.lib.hjr_solve_coarse_to_fine, C.byref(g), C.byref(m), C.byref(d),
-                   _arr(_vals(c_fine)), C.byref(cg), C.byref(k), _arr(wv) if wv is not None else None,
+        wg = warm.grid().to_c() if warm is not None else None
+        self._call(self.lib.hjr_solve_coarse_to_fine_w, C.byref(g), C.byref(m), C.byref(d),
+                   _arr(_vals(c_fine)), C.byref(cg), C.byref(k),
+                   C.cast(C.pointer(wg), C.c_void_p) if wg is not None else None,
+                   _arr(wv) if wv is not None else None,
                    _arr(cout), C.byref(res[0][0]), _arr(fout), C.byref(res[1][0]))
         out = []
         for (r, h), grid, v in ((res[0], coarse_grid, cout), (res[1], fg, fout)):
@@ -462,6 +473,46 @@ class Reference:
                                       wall_seconds=r.wall_seconds, converged=bool(r.converged),
                                       residual_history=h[:n].copy()))
         return hj.CoarseToFineResult(coarse=out[0], fine=out[1])
+
+    def solve_multilevel(self, c_fine, model, db, coarse_grids, cfg, warm=None):
+        """N-level chain composed from the reference's own public pieces
+        (SURVEY §8a row A10): levels 0..N-3 are ``resample`` of the fine
+        constraint / bound fields (solver.cpp:378-385, grid.cpp:215-231) +
+        ``solve``; the last two levels are the reference's own
+        ``solve_coarse_to_fine`` warm-started from level N-3's V* (its private
+        ``seed_from`` does the lowering, solver.cpp:404-414).  Only levels
+        0..N-3 restate ``seed_from`` (max(resample - jump, c), the same
+        expression) because the reference keeps it private."""
+        grids = list(coarse_grids)
+        fg = c_fine.grid()
+        if not grids:
+            return hj.MultiLevelResult([self.solve(c_fine, c_fine, model, db, cfg)])
+        out = []
+        prev = warm
+        for l, g in enumerate(grids[:-1]):
+            cl = hj.ScalarField(g, self.resample(c_fine, g), check=False)
+            dl = self._resample_db(db, fg, g)
+            if prev is None:
+                init = cl
+            else:
+                a = self.resample(prev, g) - self.max_adjacent_jump(prev)
+                init = hj.ScalarField(g, np.where(a < cl.values(), cl.values(), a), check=False)
+            r = self.solve(init, cl, model, dl, cfg)
+            out.append(r)
+            prev = r.value
+        ctf = self.solve_coarse_to_fine(c_fine, model, db, grids[-1], cfg, warm=prev)
+        out += [ctf.coarse, ctf.fine]
+        return hj.MultiLevelResult(out)
+
+    def _resample_db(self, db, fg, g):
+        """resample(IntervalField, Grid) (solver.cpp:378-385), channel by channel."""
+        if db.channels() == 0:
+            return hj.IntervalField.constant(g, [])
+        lo, hi = [], []
+        for ch in range(db.channels()):
+            lo.append(self.resample(db.lo(ch), g))
+            hi.append(self.resample(db.hi(ch), g))
+        return hj.IntervalField(g, db.channels(), lo=lo, hi=hi)
 
     def resample(self, f, target):
         out = np.empty(target.size())

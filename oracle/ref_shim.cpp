@@ -272,6 +272,28 @@ int hjr_solve_coarse_to_fine(const hjb_grid* fine, const hjr_model_spec* m,
   });
 }
 
+int hjr_solve_coarse_to_fine_w(const hjb_grid* fine, const hjr_model_spec* m,
+                               const hjb_dbounds* db_fine, const double* c_fine,
+                               const hjb_grid* coarse, const hjb_solve_config* cfg,
+                               const hjb_grid* warm_grid, const double* warm, double* coarse_out,
+                               hjr_result* coarse_res, double* fine_out, hjr_result* fine_res,
+                               char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Grid fg = make_grid(fine);
+    Grid cg = make_grid(coarse);
+    auto model = make(m);
+    ScalarField w;
+    if (warm) w = make_field(warm_grid ? make_grid(warm_grid) : fg, warm);
+    CoarseToFineResult r =
+        solve_coarse_to_fine(make_field(fg, c_fine), *model, make_db(fg, db_fine), cg,
+                             make_cfg(cfg), warm ? &w : nullptr);
+    std::memcpy(coarse_out, r.coarse.value.values().data(), cg.size() * sizeof(double));
+    std::memcpy(fine_out, r.fine.value.values().data(), fg.size() * sizeof(double));
+    fill_result(r.coarse, coarse_res);
+    fill_result(r.fine, fine_res);
+  });
+}
+
 int hjr_resample(const hjb_grid* src_g, const double* src, const hjb_grid* dst_g, double* dst,
                  char* err, int errlen) {
   return guarded(err, errlen, [&] {

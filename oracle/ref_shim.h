@@ -71,6 +71,16 @@ int hjr_solve_coarse_to_fine(const hjb_grid* fine, const hjr_model_spec* m,
                              const double* warm_init_fine, double* coarse_out,
                              hjr_result* coarse_res, double* fine_out, hjr_result* fine_res,
                              char* err, int errlen);
+/* solve_coarse_to_fine with the warm start on its OWN grid (the reference's
+ * ScalarField carries its grid; seed_from resamples from it,
+ * solver.cpp:404-414).  Used to compose the N-level chain from the
+ * reference's own 2-level driver. warm_grid == NULL means the fine grid. */
+int hjr_solve_coarse_to_fine_w(const hjb_grid* fine, const hjr_model_spec* m,
+                               const hjb_dbounds* db_fine, const double* c_fine,
+                               const hjb_grid* coarse, const hjb_solve_config* cfg,
+                               const hjb_grid* warm_grid, const double* warm, double* coarse_out,
+                               hjr_result* coarse_res, double* fine_out, hjr_result* fine_res,
+                               char* err, int errlen);
 int hjr_resample(const hjb_grid* src_g, const double* src, const hjb_grid* dst_g, double* dst,
                  char* err, int errlen);
 int hjr_max_adjacent_jump(const hjb_grid* g, const double* v, double* out, char* err,

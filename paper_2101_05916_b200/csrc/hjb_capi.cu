@@ -439,7 +439,9 @@ void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfPar
 struct F4Key {
   uint32_t n[4];
   int shape;
+  int device;  // timings (and so the winner) are per device
   bool operator<(const F4Key& o) const {
+    if (device != o.device) return device < o.device;
     for (int d = 0; d < 4; ++d)
       if (n[d] != o.n[d]) return n[d] < o.n[d];
     return shape < o.shape;
@@ -484,7 +486,18 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
     configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 576u));
     return HJB_OK;
   }
-  const F4Key key{{g.n[0], g.n[1], g.n[2], g.n[3]}, shape};
+  const F4Key key{{g.n[0], g.n[1], g.n[2], g.n[3]}, shape, ctx->device};
+  const char* at = std::getenv("HJB_AUTOTUNE");
+  if ((at && std::strcmp(at, "0") == 0) || g.size < (1u << 20)) {
+    configure(2, 576);
+    return HJB_OK;
+  }
+  // Tuning is serialised per device: concurrent contexts on one device (the
+  // decomposed subsystems of config 4) would otherwise time the variants
+  // against each other's load and could pick different winners.  The second
+  // caller finds the first one's entry once it gets the lock.
+  static std::mutex tune_mu[64];
+  std::lock_guard<std::mutex> tune_lk(tune_mu[ctx->device & 63]);
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
@@ -492,11 +505,6 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
       configure(it->second.first, it->second.second);
       return HJB_OK;
     }
-  }
-  const char* at = std::getenv("HJB_AUTOTUNE");
-  if ((at && std::strcmp(at, "0") == 0) || g.size < (1u << 20)) {
-    configure(2, 576);
-    return HJB_OK;
   }
   const uint32_t cands[3][2] = {{2, 576}, {2, 448}, {4, 384}};
   CUDA_TRY(cudaMemsetAsync(ctx->st, 0, sizeof(LoopState), ctx->stream));  // fresh counters
@@ -804,7 +812,9 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
       CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
       ++ctx->launches;
     }
-    f.c = ctx->pcbuf.d();
+    // with the per-plane constraint table the padded field is never filled
+    // for this solve (pcbuf holds stale data): no map, no L2 window on it
+    f.c = f.cplane ? nullptr : ctx->pcbuf.d();
     f.buf0 = ctx->v2.d();
     f.buf1 = ctx->v3.d();
     CUDA_TRY(fast4d_make_maps(f, f.buf0, f.buf1, f.c));
@@ -813,7 +823,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     f.loop = 1;
     // the constraint is read every sweep and never written: keep it in a
     // persisting L2 carve-out when it fits
-    l2_pin(ctx->device, f, f.c, rows * f.n3p * sizeof(double));
+    if (f.c) l2_pin(ctx->device, f, f.c, rows * f.n3p * sizeof(double));
     const char* pd = std::getenv("HJB_PDL");
     f.pdl = (pd && std::strcmp(pd, "0") == 0) ? 0 : 1;
   }

@@ -2493,22 +2493,32 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
 }
 
 // Function attributes are per device: set the dynamic shared-memory limit
-// once per device.  The bit is published only after the attribute is set, so
-// a concurrent launcher either sees it set or sets it again (idempotent).
+// once per device.  The bit is published only after the attribute call
+// SUCCEEDED, so a concurrent launcher either sees it set or sets it again
+// (idempotent), and a failed call is retried on the next launch.  A failure
+// is parked in t_attr_err (the launch is skipped) and returned by
+// launch_fast4d / launch_ho4d instead of surfacing as an opaque launch error.
+static thread_local cudaError_t t_attr_err = cudaSuccess;
 template <class K>
-static void smem_attr_once(std::atomic<unsigned long long>& done, K kernel) {
+static bool smem_attr_once(std::atomic<unsigned long long>& done, K kernel) {
   int d = 0;
   cudaGetDevice(&d);
   const unsigned long long bit = 1ull << (d & 63);
-  if (done.load(std::memory_order_acquire) & bit) return;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (done.load(std::memory_order_acquire) & bit) return true;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) {
+    t_attr_err = e;
+    return false;
+  }
   done.fetch_or(bit, std::memory_order_release);
+  return true;
 }
 
 template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP>);
+  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP>)) return;
   if (a.l2_bytes == 0 && !a.pdl) {
     k_fast4d<S, K, MAXT, SCH, PV, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
@@ -2571,12 +2581,14 @@ static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
+  t_attr_err = cudaSuccess;
   if (shape == 0)
     launch_shape<ShapePlanarD0>(a, s);
   else if (shape == 1)
     launch_shape<ShapePlanarD1>(a, s);
   else
     launch_shape<ShapeTwin>(a, s);
+  if (t_attr_err != cudaSuccess) return t_attr_err;
   return cudaGetLastError();
 }
 
@@ -2720,14 +2732,14 @@ namespace {
 template <class S, int R, int KC, int SCH = 0>
 void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  smem_attr_once(attr, k_ho4t<S, R, KC, SCH>);
+  if (!smem_attr_once(attr, k_ho4t<S, R, KC, SCH>)) return;
   k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
 template <class S, int SCH, bool CP = false>
 void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  smem_attr_once(attr, k_eno3g<S, SCH, CP>);
+  if (!smem_attr_once(attr, k_eno3g<S, SCH, CP>)) return;
   k_eno3g<S, SCH, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
@@ -2817,9 +2829,11 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a) {
 }
 
 cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s) {
-  if (shape == 0) return ho4d_shape<ShapePlanarD0>(a, s);
-  if (shape == 1) return ho4d_shape<ShapePlanarD1>(a, s);
-  return ho4d_shape<ShapeTwin>(a, s);
+  t_attr_err = cudaSuccess;
+  const cudaError_t e = shape == 0   ? ho4d_shape<ShapePlanarD0>(a, s)
+                        : shape == 1 ? ho4d_shape<ShapePlanarD1>(a, s)
+                                     : ho4d_shape<ShapeTwin>(a, s);
+  return t_attr_err != cudaSuccess ? t_attr_err : e;
 }
 
 bool l2_pin(int device, Fast4dArgs& a, const void* base, size_t bytes) {
@@ -2867,6 +2881,10 @@ cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const do
   CUtensorMap* maps[3] = {&a.map0, &a.map1, &a.mapc};
   const void* ptrs[3] = {buf0, buf1, c};
   for (int k = 0; k < 3; ++k) {
+    if (!ptrs[k]) {  // per-plane constraint (CP variants): no constraint field to map
+      std::memset(maps[k], 0, sizeof(CUtensorMap));
+      continue;
+    }
     CUresult r = encode(maps[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(ptrs[k]),
                         dims, strides, k < 2 ? vbox : cbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -513,6 +513,15 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   if ((rc = hjb_slab_partition(p.g.n[0], P, r, &slab_b, &slab_e))) return rc;
   const uint32_t owned = static_cast<uint32_t>(slab_e - slab_b);
   const bool has_lo = r > 0, has_hi = r < P - 1;
+  // Every rank must reject a too-thin partition BEFORE the first collective:
+  // balanced slabs differ by one plane, so a per-rank check would let the
+  // thicker ranks enter NCCL while a thin one returns (a hang, not an error).
+  // The smallest slab is floor(n0 / P) planes on every rank's view.
+  {
+    const int64_t R = high_order ? (cfg->spatial_order < 1 ? 1 : cfg->spatial_order) : 1;
+    if (P > 1 && static_cast<int64_t>(p.g.n[0]) / P < R)
+      return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: slab thinner than the ENO halo");
+  }
   const uint32_t nloc = owned + (has_lo ? 1 : 0) + (has_hi ? 1 : 0);
 
   // CFL scan over the slab + all-reduce(max): rows of the fast path never

@@ -2,6 +2,7 @@
 // the reference itself, in one process.  Built only where /root/reference
 // exists (the reference sources are linked in as the checker); the binary
 // travels to the GPU box.  Exit codes: 0 parity ok, 1 mismatch, 3 no GPU.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -85,6 +86,30 @@ int main() {
     SolveResult g4r = hjb_bridge::solve(c4, c4, planar, db4, cfg4);
     expect(same(r4.value, g4r.value) && r4.iterations == g4r.iterations,
            "NearHoverPlanar4D 9^4: bitwise equal");
+
+    // full config-2 grid size through the drop-in, timed: stock
+    // NearHoverPlanar4D on 51^4, 20 sweeps.  The reference IntervalField is
+    // per node; the bridge detects the uniform channel and ships 2 doubles.
+    {
+      Grid g51({{-5.0, 5.0, 51}, {-2.0, 2.0, 51}, {-0.35, 0.35, 51}, {-1.5, 1.5, 51}});
+      ScalarField c51 = signed_distance_band(g51, 0, -4.0, 4.0);
+      auto db51 = IntervalField::constant(g51, std::vector<Interval>{{-0.5, 0.5}});
+      SolveConfig k20;
+      k20.max_iters = 20;
+      hjb_bridge::solve(c51, c51, planar, db51, k20);  // warm-up (autotuner, context)
+      auto t0 = std::chrono::steady_clock::now();
+      SolveResult rg = hjb_bridge::solve(c51, c51, planar, db51, k20);
+      auto t1 = std::chrono::steady_clock::now();
+      SolveResult rr = solve(c51, c51, planar, db51, k20);
+      auto t2 = std::chrono::steady_clock::now();
+      const double sg = std::chrono::duration<double>(t1 - t0).count();
+      const double sr = std::chrono::duration<double>(t2 - t1).count();
+      std::printf("51^4 x 20 sweeps: bridge %.1f ms (host buffers in and out), reference %.1f ms"
+                  " (%.0fx)\n", sg * 1e3, sr * 1e3, sr / sg);
+      expect(same(rr.value, rg.value) && rr.iterations == rg.iterations &&
+                 rr.residual_history == rg.residual_history,
+             "NearHoverPlanar4D 51^4 x 20: bitwise equal, constant bounds detected");
+    }
 
     // coarse-to-fine (test_solver.cpp:253-278 setup)
     Quad2DVert quad;

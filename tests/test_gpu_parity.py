@@ -444,6 +444,7 @@ from paper_2101_05916_b200 import hjsafe as hj
 w = configs.config2(21)
 ctxs = [hj.Context(0) for _ in range(4)]
 errs = []
+gate = threading.Barrier(4)
 def job(k):
     try:
         cfg = hj.SolveConfig(**w.cfg.__dict__)
@@ -451,6 +452,7 @@ def job(k):
         if k % 2:
             cfg.spatial_order, cfg.time_order = 3, 3
         c = hj.signed_distance_band(w.grid, 0, -4.0, 4.0, ctx=ctxs[k])
+        gate.wait()  # every thread reaches its first TMA-kernel launch together
         hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=ctxs[k])
     except Exception as e:
         errs.append(repr(e))
@@ -461,6 +463,7 @@ assert not errs, errs
 print("ok")
 '''
     root = str(Path(__file__).resolve().parent.parent)
-    r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    for _ in range(3):  # a fresh process each time: the attributes start unset
+        r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
