@@ -279,14 +279,29 @@ int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* 
 int hjb_comm_destroy(hjb_comm* comm);
 /* solve() over a slab-partitioned 4D grid: init/c/value_out hold this rank's
  * owned planes [begin, end) of `global_grid` (reference layout, device
- * pointers).  Per sweep: NCCL halo exchange, slab sweep, all-reduce(max) of
- * max|dV|, device epilogue; bitwise identical to hjb_solve_dev.  4D
- * Godunov fast-path models with constant bounds. */
+ * pointers).  Per sweep / RK stage: boundary planes, then the NCCL halo
+ * exchange on a second stream overlapped with the interior planes, then the
+ * all-reduce(max) of max|dV| and the device epilogue; bitwise identical to
+ * hjb_solve_dev.  4D fast-path models with constant bounds, first order or
+ * ENO/TVD-RK (halo = ENO order), Godunov or Lax-Friedrichs. */
 int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* global_grid,
                           const hjb_model* model, const hjb_dbounds* dbounds,
                           const double* init_slab, const double* c_slab,
                           const hjb_solve_config* cfg, double* value_slab_out,
                           hjb_solve_result* result);
+/* The same slab-partitioned solve with `nranks` IN-PROCESS ranks on this
+ * context's device: every rank has its own slab buffers, halo planes and
+ * loop state, and runs exactly the per-rank plan of hjb_solve_sharded_dev
+ * (boundary planes first, interior while the halos travel); halo planes move
+ * by device copies on a second stream, the residual all-reduce is a kernel.
+ * init/c/value_out are FULL-grid device arrays (reference layout).  Bitwise
+ * identical to hjb_solve_dev; verifies and times the multi-rank protocol on
+ * one GPU.  1 <= nranks <= 16. */
+int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid* grid,
+                                const hjb_model* model, const hjb_dbounds* dbounds,
+                                const double* init, const double* c,
+                                const hjb_solve_config* cfg, double* value_out,
+                                hjb_solve_result* result);
 /* One sweep restricted to planes [plane_begin, plane_end) of a full grid
  * (device pointers): the slab computation of one rank, for single-device
  * verification of the partition.  Planes of `out` outside the range receive

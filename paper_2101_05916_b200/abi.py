@@ -166,6 +166,8 @@ SIGNATURES = [
     ("hjb_comm_destroy", _i, [_vp]),
     ("hjb_solve_sharded_dev", _i, [_vp, _vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp,
                                    P(HjbSolveConfig), _vp, P(HjbSolveResult)]),
+    ("hjb_solve_sharded_local_dev", _i, [_vp, _i32, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp,
+                                         _vp, P(HjbSolveConfig), _vp, P(HjbSolveResult)]),
     ("hjb_sweep_planes_dev", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp, _i64,
                                   _i64, _d, _vp, _dp]),
     ("hjb_filter_batch", _i, [_vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _i64, _vp, _vp,

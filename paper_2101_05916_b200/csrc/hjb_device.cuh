@@ -119,6 +119,9 @@ struct LoopState {
   unsigned long long t0_ns;
   double* history;
   double* wall_history;
+  // pipelined sharded loop: sweep k accumulates into maxdv_slot[k & 1] while
+  // the all-reduce + epilogue of sweep k - 1 run on the comm stream
+  unsigned long long maxdv_slot[2];
 };
 
 }  // namespace hjb

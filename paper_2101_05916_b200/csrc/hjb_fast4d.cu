@@ -147,8 +147,13 @@ __device__ __forceinline__ double lds1(uint32_t addr) {
 // solve() loop logic after a sweep (solver.cpp:347-369): residual, histories,
 // convergence, the 10x divergence guard, max_iters / horizon; resets the
 // sweep accumulators and clears the graph's WHILE condition when done.
-__device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
-  const double max_dv = __longlong_as_double(atomicAdd(&st->maxdv_bits, 0ull));
+// `slot`: the sweep's max|dV| accumulator; the default (st->maxdv_bits) also
+// resets the persistent sweep's counters, a pipelined slot (maxdv_slot[k & 1],
+// epilogue on the comm stream while the next sweep runs) only itself.
+__device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
+                              unsigned long long* slot = nullptr) {
+  unsigned long long* acc = slot ? slot : &st->maxdv_bits;
+  const double max_dv = __longlong_as_double(atomicAdd(acc, 0ull));
   const double residual = max_dv / st->dt;
   const long long iter = st->iter + 1;
   st->iter = iter;
@@ -176,9 +181,11 @@ __device__ void loop_epilogue(LoopState* st, cudaGraphConditionalHandle handle, 
   }
   if (iter >= st->max_iters) stop = true;
   if (st->horizon > 0.0 && (double)iter * st->dt >= st->horizon) stop = true;
-  st->maxdv_bits = 0ull;
-  st->blocks_done = 0u;
-  st->work_next = 0u;
+  *acc = 0ull;
+  if (!slot) {
+    st->blocks_done = 0u;
+    st->work_next = 0u;
+  }
   if (stop) {
     st->done = 1;
     if (use_handle) cudaGraphSetConditional(handle, 0u);
@@ -319,6 +326,20 @@ __device__ __forceinline__ void item_tile(const Fast4dArgs& a, uint32_t w, uint3
   }
   t1 = a.tiles1 - 1;  // partial last tile row
   t2 = e;
+}
+
+// planes [c0, c1) of chunk `chunk` (two-range boundary launches: chunks at
+// or past `split` lie in the second range)
+template <class A>
+__device__ __forceinline__ void chunk_planes(const A& a, uint32_t chunk, uint32_t& c0,
+                                             uint32_t& c1) {
+  if (a.split != 0u && chunk >= a.split) {
+    c0 = a.c2beg + (chunk - a.split) * a.L;
+    c1 = min(c0 + a.L, a.c2end);
+  } else {
+    c0 = a.cbeg + chunk * a.L;
+    c1 = min(c0 + a.L, a.cend);
+  }
 }
 
 constexpr uint32_t kEndItem = 0xffffffffu;
@@ -511,8 +532,7 @@ __global__ void __launch_bounds__(MAXT, 1)
           if (!end) {
             uint32_t chunk;
             item_tile(a, w, t1, t2, chunk);
-            c0 = a.cbeg + chunk * a.L;
-            c1 = min(c0 + a.L, a.cend);
+            chunk_planes(a, chunk, c0, c1);
           }
         }
         if (end) {
@@ -970,7 +990,7 @@ __global__ void __launch_bounds__(MAXT, 1)
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
   LoopState* st = a.st;
-  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (mbits) atomicMax(a.mdv ? a.mdv : &st->maxdv_bits, mbits);
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
   if (ticket != gridDim.x - 1) return;
@@ -1083,7 +1103,7 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   constexpr int kK = 2;
   LoopState* st = a.st;
   if (a.loop != 0 && *(volatile int*)&st->done) return;
-  const long long it = a.loop != 0 ? st->iter : 0;
+  const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
   const double* __restrict__ vs =
@@ -1107,8 +1127,8 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   const uint64_t s2 = n3p, s1 = (uint64_t)n2 * n3p, s0 = (uint64_t)n1 * s1;
   const uint64_t rowo = (uint64_t)ci1 * s1 + (uint64_t)ci2 * s2 + i3;
   const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
-  const uint32_t c0 = a.cbeg + chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, a.cend);
+  uint32_t c0, c1;
+  chunk_planes(a, chunk, c0, c1);
 
   // slopes and shapes of the rows (as k_fast4d)
   double pos_[4][kK], neg_[4][kK];
@@ -1316,7 +1336,7 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
-  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (mbits) atomicMax(a.mdv ? a.mdv : &st->maxdv_bits, mbits);
   if (a.loop != 1) return;  // sharded slab / single stage: the caller reduces
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
@@ -1374,7 +1394,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
   if (a.loop != 0 && *(volatile int*)&st->done) return;
-  const long long it = a.loop != 0 ? st->iter : 0;
+  const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
   const double* __restrict__ vs =
@@ -1392,8 +1412,8 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   b /= a.segs;
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
   const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2, base3 = seg * a.T3;
-  const uint32_t c0 = a.cbeg + chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, a.cend);
+  uint32_t c0, c1;
+  chunk_planes(a, chunk, c0, c1);
   const uint32_t ncons = a.threads - 32;
   const uint32_t nwarps_c = ncons >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1780,7 +1800,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
-  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (mbits) atomicMax(a.mdv ? a.mdv : &st->maxdv_bits, mbits);
   if (a.loop != 1) return;  // sharded slab / single stage: the caller reduces
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
@@ -1839,7 +1859,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
   if (a.loop != 0 && *(volatile int*)&st->done) return;
-  const long long it = a.loop != 0 ? st->iter : 0;
+  const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
   const double* __restrict__ vs =
@@ -1857,8 +1877,8 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
   b /= a.segs;
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
   const uint32_t base1 = t1 * a.T1, base2 = t2 * a.T2, base3 = seg * a.T3;
-  const uint32_t c0 = a.cbeg + chunk * a.L;
-  const uint32_t c1 = min(c0 + a.L, a.cend);
+  uint32_t c0, c1;
+  chunk_planes(a, chunk, c0, c1);
   const uint32_t ncons = a.threads - 32;
   const uint32_t nwarps_c = ncons >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -2232,7 +2252,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane != 0) return;
-  if (mbits) atomicMax(&st->maxdv_bits, mbits);
+  if (mbits) atomicMax(a.mdv ? a.mdv : &st->maxdv_bits, mbits);
   if (a.loop != 1) return;
   __threadfence();
   const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
@@ -2243,9 +2263,10 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
 
 // Sharded loop: after the residual all-reduce, one thread applies the
 // solve() loop logic to the global max|dV| (every rank decides identically).
-__global__ void k_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle) {
+__global__ void k_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
+                           unsigned long long* slot) {
   if (st->done) return;
-  loop_epilogue(st, handle, use_handle);
+  loop_epilogue(st, handle, use_handle, slot);
 }
 
 // reference layout <-> ghost layout of the ENO3 stage buffers: every cell of
@@ -2466,11 +2487,16 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   // planes) off a counter.  Chunks of the axis-0 march give the schedule
   // more items to balance when tiles are few; each chunk costs an extra V
   // plane at each end and a per-item set-up, so chunks stay long.
-  const uint32_t tiles = a.tiles1 * a.tiles2;
   if (a.cend == 0) {
     a.cbeg = 0;
     a.cend = g.n[0];
   }
+  fast4d_chunks(a, sms);
+}
+
+void fast4d_chunks(Fast4dArgs& a, int sms) {
+  a.split = a.c2beg = a.c2end = 0u;
+  const uint32_t tiles = a.tiles1 * a.tiles2;
   const uint32_t span = a.cend - a.cbeg;
   // measured (B200): 51^4 and 71^4 best at 2 chunks, 101^4 at 1
   uint32_t nch = 1;
@@ -2490,6 +2516,21 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
   const char* eb = std::getenv("HJB_BALANCE");
   a.bal = eb ? (std::strcmp(eb, "1") == 0 ? 1u : 0u) : (tiles < static_cast<uint32_t>(sms) ? 1u : 0u);
   if (a.bal) a.blocks = std::min<uint32_t>(static_cast<uint32_t>(sms), tiles * span);
+}
+
+void fast4d_ranges(Fast4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1) {
+  const uint32_t tiles = a.tiles1 * a.tiles2;
+  a.cbeg = b0;
+  a.cend = e0;
+  a.L = e0 - b0;
+  const bool two = b1 < e1;
+  a.split = two ? 1u : 0u;
+  a.c2beg = two ? b1 : 0u;
+  a.c2end = two ? e1 : 0u;
+  a.nchunks = 1u + (two ? (e1 - b1 + a.L - 1) / a.L : 0u);
+  a.items = tiles * a.nchunks;
+  a.blocks = std::min<uint32_t>(a.items, static_cast<uint32_t>(sms));
+  a.bal = 0u;  // dynamic items (the balanced schedule assumes one range)
 }
 
 // Function attributes are per device: set the dynamic shared-memory limit
@@ -2701,11 +2742,16 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
     }
   }
   if (!a.tma) a.eno3g = 0;
-  const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
   if (a.cend == 0) {
     a.cbeg = 0;
     a.cend = g.n[0];
   }
+  ho4d_chunks(a, sms);
+}
+
+void ho4d_chunks(Ho4dArgs& a, int sms) {
+  a.split = a.c2beg = a.c2end = 0u;
+  const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
   const uint32_t span = a.cend - a.cbeg;
   uint32_t nch = 1;
   if (a.eno3g) {
@@ -2725,6 +2771,19 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   }
   a.L = (span + nch - 1) / nch;
   a.nchunks = (span + a.L - 1) / a.L;
+  a.blocks = tiles * a.nchunks;
+}
+
+void ho4d_ranges(Ho4dArgs& a, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1) {
+  const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
+  a.cbeg = b0;
+  a.cend = e0;
+  a.L = e0 - b0;
+  const bool two = b1 < e1;
+  a.split = two ? 1u : 0u;
+  a.c2beg = two ? b1 : 0u;
+  a.c2end = two ? e1 : 0u;
+  a.nchunks = 1u + (two ? (e1 - b1 + a.L - 1) / a.L : 0u);
   a.blocks = tiles * a.nchunks;
 }
 
@@ -2895,8 +2954,8 @@ cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const do
 }
 
 cudaError_t launch_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
-                            cudaStream_t s) {
-  k_epilogue<<<1, 1, 0, s>>>(st, handle, use_handle);
+                            cudaStream_t s, unsigned long long* slot) {
+  k_epilogue<<<1, 1, 0, s>>>(st, handle, use_handle, slot);
   return cudaGetLastError();
 }
 

@@ -38,6 +38,11 @@ struct Fast4dArgs {
   // tile pieces each); 0: dynamic items (tile x chunk) off the work counter
   uint32_t bal;
   uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
+  // second plane range of a boundary launch (sharded solve): chunks >= split
+  // cover [c2beg, c2end) in chunks of L planes; split == 0: one range
+  uint32_t split, c2beg, c2end;
+  // max|dV| accumulator of the launch (null: st->maxdv_bits)
+  unsigned long long* mdv;
   const double* tab;    // slope tables (staged into shared memory per CTA)
   uint32_t tab_len;     // doubles in tab
   uint32_t tab_off;     // shared-memory byte offset of the staged copy
@@ -104,6 +109,11 @@ struct Ho4dArgs {
   //    epilogue); 0: one stage on explicit buffers (xsrc, xvn -> xdst)
   int loop;
   uint32_t cbeg, cend;  // planes updated (0, 0 = all)
+  uint32_t split, c2beg, c2end;  // second plane range (as Fast4dArgs)
+  unsigned long long* mdv;       // max|dV| accumulator (null: st->maxdv_bits)
+  // pmode 1: the V_n buffer parity is `parity` (sharded loop: the loop
+  // state's iteration count advances concurrently on the comm stream)
+  int pmode, parity;
   const double* xsrc;
   const double* xvn;
   double* xdst;
@@ -160,6 +170,16 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
 // caller checks which on the device.
 int fast4d_shape_pv(const DevGrid& g, const DevModel& m);
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
+// Restrict a configured launch (fast4d_config / ho4d_config done) to the
+// planes [b0, e0) and, when b1 < e1, [b1, e1) too — the boundary planes of a
+// slab, swept before its interior so they can travel while the interior
+// sweeps.  One chunk of e0 - b0 planes per range and tile.
+void fast4d_ranges(Fast4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1);
+// Re-chunk a configured launch over its plane range [cbeg, cend) (the
+// chunking fast4d_config / ho4d_config apply)
+void fast4d_chunks(Fast4dArgs& a, int sms);
+void ho4d_chunks(Ho4dArgs& a, int sms);
+void ho4d_ranges(Ho4dArgs& a, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1);
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
 // Encode the three TMA tensor maps for the padded buffers (driver entry point
 // fetched through the runtime; no libcuda link dependency).
@@ -170,7 +190,7 @@ cudaError_t fast4d_make_maps(Fast4dArgs& a, double* buf0, double* buf1, const do
 bool l2_pin(int device, Fast4dArgs& a, const void* base, size_t bytes);
 void l2_release(Fast4dArgs& a);
 cudaError_t launch_epilogue(LoopState* st, cudaGraphConditionalHandle handle, int use_handle,
-                            cudaStream_t s);
+                            cudaStream_t s, unsigned long long* slot = nullptr);
 cudaError_t launch_pad4(const double* in, double* out, uint64_t rows, uint32_t n3, uint32_t n3p,
                         cudaStream_t s);
 cudaError_t launch_unpad4(const double* in, double* out, uint64_t rows, uint32_t n3,

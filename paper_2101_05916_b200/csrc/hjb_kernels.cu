@@ -486,6 +486,8 @@ __global__ void k_loop_init(LoopState* st, long long max_iters, double dt, doubl
   st->last_residual = 0.0;
   st->history = history;
   st->wall_history = wall_history;
+  st->maxdv_slot[0] = 0ull;
+  st->maxdv_slot[1] = 0ull;
   st->t0_ns = globaltimer_ns();
 }
 

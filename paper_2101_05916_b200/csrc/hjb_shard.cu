@@ -1,32 +1,44 @@
 // hjb_shard.cu — multi-GPU slab partition of the 4D solve.
 //
 // One process per GPU.  Axis 0 (the slowest, so slabs are contiguous) is
-// split into balanced slabs; every rank keeps its slab plus one halo plane
-// per interior side in the padded layout of k_fast4d.  Per sweep:
-//   1. halo exchange of the first/last owned planes with the neighbours
-//      (ncclSend/ncclRecv in one group);
-//   2. k_fast4d over the owned planes (loop mode 2: halo planes are read as
-//      neighbours, the global edges keep the reference's zero ghost rule);
-//   3. ncclAllReduce(max) of the sweep's max|dV| bits (non-negative doubles
-//      order like uint64);
-//   4. k_epilogue: the solve() loop logic on the global max, identical on
-//      every rank, so all ranks stop at the same sweep.
+// split into balanced slabs; every rank keeps its slab plus R halo planes
+// per interior side (R = 1 first order, the ENO order otherwise) in the
+// padded / ghost layout of the 4D kernels.  Per loop position and RK stage:
+//   1. the BOUNDARY planes (the R owned planes next to each neighbour — what
+//      the neighbours read next) are swept first (one launch over both
+//      ranges, Fast4dArgs/Ho4dArgs split ranges);
+//   2. on a second captured stream, the stage output's boundary planes go to
+//      the neighbours' halo planes (grouped ncclSend/ncclRecv) while
+//   3. the INTERIOR planes sweep on the main stream (they never read halos);
+//   4. join; after the last stage ncclAllReduce(max) of the max|dV| bits
+//      (non-negative doubles order like uint64) and k_epilogue run the
+//      solve() loop logic on the global max, identically on every rank, so
+//      all ranks leave the device loop together.
 // The whole loop is one CUDA graph with a WHILE node; the body holds an even
-// number of sweeps with fixed buffers (NCCL needs fixed pointers), which the
-// parity of the loop state matches because the loop starts at iteration 0.
-// A Jacobi sweep reads only the previous iterate, so the slab result is
-// bitwise identical to the single-GPU solve.
+// number of positions with fixed buffers (NCCL needs fixed pointers), which
+// the parity of the loop state matches because the loop starts at 0.  A
+// Jacobi sweep / RK stage reads only the previous stage, so the slab result
+// is bitwise identical to the single-GPU solve.
+//
+// hjb_solve_sharded_local_dev runs the SAME per-rank plans (geometry, halo
+// offsets, boundary/interior launches, epilogues) for P in-process ranks on
+// one device, with the halo planes moved by device copies on the second
+// stream and the all-reduce by a kernel: the multi-rank protocol exercised
+// and timed on a single GPU (no kernel waits on another).
 //
 // NCCL is loaded with dlopen at communicator creation, so libhjb.so carries
 // no hard dependency on it (single-GPU use never loads it).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
-#include <functional>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <string>
+#include <vector>
 
 #include "../../include/hjb.h"
 #include "hjb_common.cuh"
@@ -112,7 +124,9 @@ namespace hjb {
 namespace {
 
 // WHILE-conditional graph whose body is `body` calls of iter(k, handle, 1)
-// (k = position in the body), or the host-polled loop under HJB_LOOP=poll.
+// (k = position in the body), or the host-polled loop under HJB_LOOP=poll
+// (loop state of ctx->st).  iter may fork work onto other streams with
+// events; they must join back before it returns.
 int run_sharded_loop(hjb_context* ctx, int body,
                      const std::function<int(int, cudaGraphConditionalHandle, int)>& iter) {
   int rc = HJB_OK;
@@ -183,42 +197,223 @@ int ho_stages(int rk, HoStage* st) {
   return 3;
 }
 
-// ENO/TVD-RK slab solve: halo of R = order planes per interior side,
-// exchanged before every stage, k_ho4t/k_ho4d over the owned
-// planes, all-reduce(max) + epilogue after the last stage of a step.
-int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared& p,
-                     const hjb_solve_config* cfg, double dt, const double* galpha,
-                     uint32_t owned, bool has_lo, bool has_hi, const double* init_slab,
-                     const double* c_slab, double* value_slab_out, hjb_solve_result* res) {
-  const int r = comm->rank;
-  const uint32_t R = cfg->spatial_order < 1 ? 1u : (uint32_t)cfg->spatial_order;
-  if ((has_lo || has_hi) && owned < R)
-    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: slab thinner than the ENO halo");
-  const uint32_t nloc = owned + (has_lo ? R : 0) + (has_hi ? R : 0);
+// ---------------------------------------------------------------- geometry
+// One rank's slab in its local buffers: [halo_lo R][owned][halo_hi R]
+// planes (halo planes only next to a neighbour).
+struct SlabGeom {
+  int P = 1, r = 0;
+  uint32_t owned = 0, R = 1, nloc = 0, cbeg = 0, cend = 0;
+  int64_t gbeg = 0;  // first owned plane in the global grid
+  bool has_lo = false, has_hi = false;
+};
+
+SlabGeom slab_geom(uint32_t n0, int P, int r, uint32_t R) {
+  SlabGeom s;
+  int64_t b = 0, e = 0;
+  hjb_slab_partition(n0, P, r, &b, &e);
+  s.P = P;
+  s.r = r;
+  s.R = R;
+  s.gbeg = b;
+  s.owned = static_cast<uint32_t>(e - b);
+  s.has_lo = r > 0;
+  s.has_hi = r < P - 1;
+  s.cbeg = s.has_lo ? R : 0u;
+  s.cend = s.cbeg + s.owned;
+  s.nloc = s.owned + (s.has_lo ? R : 0u) + (s.has_hi ? R : 0u);
+  return s;
+}
+
+// The halo protocol of one stage buffer, in local planes: the first / last
+// R owned planes go to the lower / upper neighbour, whose halo planes
+// [cbeg - R, cbeg) / [cend, cend + R) receive them.  Both transports (NCCL
+// send/recv between processes, device copies between in-process ranks) move
+// exactly these planes.
+struct Halo {
+  uint32_t send_lo, recv_lo, send_hi, recv_hi, planes;
+};
+Halo halo_of(const SlabGeom& s) {
+  return {s.cbeg, s.has_lo ? s.cbeg - s.R : 0u, s.cend - s.R, s.cend, s.R};
+}
+
+// Boundary planes (the R owned planes next to each neighbour: what the
+// neighbours read next stage) are swept first, so their transfer overlaps
+// the sweep of the interior planes.
+struct PlaneSplit {
+  uint32_t b0 = 0, e0 = 0, b1 = 0, e1 = 0;  // boundary ranges ([b1, e1) may be empty)
+  uint32_t i0 = 0, i1 = 0;                  // interior
+  bool bnd = false, inner = false;
+};
+PlaneSplit plane_split(const SlabGeom& s) {
+  PlaneSplit x;
+  if (s.P == 1) {
+    x.i0 = s.cbeg;
+    x.i1 = s.cend;
+    x.inner = true;
+    return x;
+  }
+  const uint32_t lo_end = s.has_lo ? s.cbeg + s.R : s.cbeg;
+  const uint32_t hi_beg = s.has_hi ? s.cend - s.R : s.cend;
+  x.bnd = true;
+  if (lo_end >= hi_beg) {  // the boundary covers the whole slab
+    x.b0 = s.cbeg;
+    x.e0 = s.cend;
+    return x;
+  }
+  if (s.has_lo) {
+    x.b0 = s.cbeg;
+    x.e0 = lo_end;
+    if (s.has_hi) {
+      x.b1 = hi_beg;
+      x.e1 = s.cend;
+    }
+  } else {
+    x.b0 = hi_beg;
+    x.e0 = s.cend;
+  }
+  x.i0 = lo_end;
+  x.i1 = hi_beg;
+  x.inner = true;
+  return x;
+}
+
+// ------------------------------------------------------------- one rank
+struct SlabRank {
+  SlabGeom geo;
+  PlaneSplit sp;
+  int shape = -1;
+  bool ho = false;
+  size_t pe = 0;  // elements per local plane
+  Fast4dArgs fb, fi;  // first order: boundary / interior launches
+  CUtensorMap map_b0, map_b1;
+  Ho4dArgs hb, hi;  // high order
+  HoStage stages[3];
+  int ns = 1;
+  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // V parity 0/1, stage1, stage2
+  LoopState* st = nullptr;
+
+  // the buffer stage q writes at loop position k (its halo travels after it)
+  double* stage_out(int k, int q) const {
+    const int d = ho ? stages[q].dst : 0;
+    if (d == 0) return (k & 1) ? buf[0] : buf[1];
+    return d == 1 ? buf[2] : buf[3];
+  }
+  // V after `iters` completed iterations
+  double* value(long long iters) const { return (iters & 1) ? buf[1] : buf[0]; }
+  // slot: the max|dV| accumulator of position k (null: st->maxdv_bits)
+  cudaError_t launch(int k, int q, bool boundary, unsigned long long* slot) const;
+  cudaStream_t s = nullptr;
+};
+
+cudaError_t SlabRank::launch(int k, int q, bool boundary, unsigned long long* slot) const {
+  if (!ho) {
+    Fast4dArgs x = boundary ? fb : fi;
+    x.src = (k & 1) ? buf[1] : buf[0];
+    x.dst = (k & 1) ? buf[0] : buf[1];
+    x.map0 = (k & 1) ? map_b1 : map_b0;
+    x.mdv = slot;
+    return launch_fast4d(x, shape, s);
+  }
+  Ho4dArgs x = boundary ? hb : hi;
+  x.mdv = slot;
+  x.pmode = 1;  // position parity == iteration parity (even body, loop from 0)
+  x.parity = k & 1;
+  x.src_sel = stages[q].src;
+  x.dst_sel = stages[q].dst;
+  x.kind = stages[q].kind;
+  x.final_stage = q == ns - 1;
+  return launch_ho4d(x, shape, s);
+}
+
+// Local buffers, padded inputs, launch arguments of one rank.  bufs[0..3] /
+// cbuf are grown to the slab's size; init_slab / c_slab hold the owned
+// planes (reference layout, device).
+int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, double dt,
+               const double* galpha, const SlabGeom& geo, DevBuf* const bufs[4], DevBuf* cbuf,
+               LoopState* st, const double* init_slab, const double* c_slab, cudaStream_t s,
+               SlabRank& rk, long long* launches) {
+  const int sms = sm_count(device);
+  const int scheme = scheme_of(cfg);
+  rk.geo = geo;
+  rk.sp = plane_split(geo);
+  rk.shape = p.shape;
+  rk.st = st;
+  rk.s = s;
+  rk.ho = cfg->spatial_order > 1 || cfg->time_order > 1;
   DevGrid gloc = p.g;
-  gloc.n[0] = nloc;
+  gloc.n[0] = geo.nloc;
+  if (!rk.ho) {
+    Fast4dArgs f;
+    std::memset(&f, 0, sizeof f);
+    f.kcells = 2;
+    f.maxthreads = 576;
+    f.cbeg = geo.cbeg;
+    f.cend = geo.cend;
+    f.tab_len = static_cast<uint32_t>(p.hm.tab.size());
+    fast4d_config(gloc, sms, f);
+    fill_tables(p, f);
+    fill_lf(p.hm.dm, scheme, galpha, f);
+    if (f.lf) {  // the Lax-Friedrichs variant's CTA size
+      f.maxthreads = 448;
+      f.cbeg = geo.cbeg;
+      f.cend = geo.cend;
+      fast4d_config(gloc, sms, f);
+    }
+    rk.pe = static_cast<size_t>(p.g.n[1]) * p.g.n[2] * f.n3p;
+    const uint64_t rows_owned = static_cast<uint64_t>(geo.owned) * p.g.n[1] * p.g.n[2];
+    const size_t lbytes = static_cast<size_t>(geo.nloc) * rk.pe * sizeof(double);
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(bufs[b]->ensure(lbytes));
+      CUDA_TRY(cudaMemsetAsync(bufs[b]->p, 0, lbytes, s));
+      rk.buf[b] = bufs[b]->d();
+    }
+    CUDA_TRY(cbuf->ensure(lbytes));
+    CUDA_TRY(cudaMemsetAsync(cbuf->p, 0, lbytes, s));
+    CUDA_TRY(launch_pad4(init_slab, rk.buf[0] + geo.cbeg * rk.pe, rows_owned, p.g.n[3], f.n3p, s));
+    CUDA_TRY(launch_pad4(c_slab, cbuf->d() + geo.cbeg * rk.pe, rows_owned, p.g.n[3], f.n3p, s));
+    *launches += 2;
+    f.c = cbuf->d();
+    f.buf0 = rk.buf[0];
+    f.buf1 = rk.buf[1];
+    CUDA_TRY(fast4d_make_maps(f, f.buf0, f.buf1, f.c));
+    rk.map_b0 = f.map0;
+    rk.map_b1 = f.map1;
+    f.st = st;
+    f.dt = dt;
+    f.loop = 2;
+    rk.fi = f;
+    rk.fb = f;
+    if (rk.sp.inner) {
+      rk.fi.cbeg = rk.sp.i0;
+      rk.fi.cend = rk.sp.i1;
+      fast4d_chunks(rk.fi, sms);
+    }
+    if (rk.sp.bnd) fast4d_ranges(rk.fb, sms, rk.sp.b0, rk.sp.e0, rk.sp.b1, rk.sp.e1);
+    return HJB_OK;
+  }
   Ho4dArgs h;
   std::memset(&h, 0, sizeof h);
-  h.order = (int)(R > 3 ? 3 : R);
-  h.cbeg = has_lo ? R : 0u;
-  h.cend = h.cbeg + owned;
-  // Lax-Friedrichs: the global alphas come from the all-reduced scan
-  fill_lf(p.hm.dm, scheme_of(cfg), galpha, h.lf, h.lp);
-  ho4d_config(gloc, sm_count(ctx->device), h);
+  h.order = static_cast<int>(geo.R > 3 ? 3 : geo.R);
+  h.cbeg = geo.cbeg;
+  h.cend = geo.cend;
+  fill_lf(p.hm.dm, scheme, galpha, h.lf, h.lp);
+  ho4d_config(gloc, sms, h);
   if (h.lf && !h.tma)
-    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: Lax-Friedrichs high order needs the TMA kernels");
-  const uint64_t plane = ho4d_plane(h);  // stage-buffer plane (ghost layout of h)
-  const size_t lbytes = static_cast<size_t>(nloc) * plane * sizeof(double);
-  DevBuf* bufs[4] = {&ctx->v0, &ctx->v1, &ctx->v2, &ctx->v3};
-  for (DevBuf* b : bufs) {
-    CUDA_TRY(b->ensure(lbytes));
-    CUDA_TRY(cudaMemsetAsync(b->p, 0, lbytes, ctx->stream));
+    return set_err(HJB_ERR_UNSUPPORTED,
+                   "solve_sharded: Lax-Friedrichs high order needs the TMA kernels");
+  rk.ns = ho_stages(cfg->time_order, rk.stages);
+  rk.pe = static_cast<size_t>(ho4d_plane(h));  // stage-buffer plane (ghost layout of h)
+  const size_t lbytes = static_cast<size_t>(geo.nloc) * rk.pe * sizeof(double);
+  for (int b = 0; b < 4; ++b) {
+    CUDA_TRY(bufs[b]->ensure(lbytes));
+    CUDA_TRY(cudaMemsetAsync(bufs[b]->p, 0, lbytes, s));
+    rk.buf[b] = bufs[b]->d();
   }
-  CUDA_TRY(ctx->pcbuf.ensure(lbytes));
-  CUDA_TRY(cudaMemsetAsync(ctx->pcbuf.p, 0, lbytes, ctx->stream));
-  CUDA_TRY(ho4d_pad(init_slab, ctx->v0.d() + h.cbeg * plane, owned, h, ctx->stream));
-  CUDA_TRY(ho4d_pad(c_slab, ctx->pcbuf.d() + h.cbeg * plane, owned, h, ctx->stream));
-  ctx->launches += 2;
+  CUDA_TRY(cbuf->ensure(lbytes));
+  CUDA_TRY(cudaMemsetAsync(cbuf->p, 0, lbytes, s));
+  CUDA_TRY(ho4d_pad(init_slab, rk.buf[0] + geo.cbeg * rk.pe, geo.owned, h, s));
+  CUDA_TRY(ho4d_pad(c_slab, cbuf->d() + geo.cbeg * rk.pe, geo.owned, h, s));
+  *launches += 2;
   h.tab = p.hm.dm.tab;
   for (int d = 0; d < 4; ++d) {
     h.off_pos[d] = p.hm.dm.row[d].off_pos;
@@ -226,78 +421,153 @@ int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared
     h.off_a[d] = p.hm.dm.row[d].off_a;
     h.off_b[d] = p.hm.dm.row[d].off_b;
   }
-  h.c = ctx->pcbuf.d();
-  h.buf0 = ctx->v0.d();
-  h.buf1 = ctx->v1.d();
-  h.stage1 = ctx->v2.d();
-  h.stage2 = ctx->v3.d();
-  h.st = ctx->st;
+  h.c = cbuf->d();
+  h.buf0 = rk.buf[0];
+  h.buf1 = rk.buf[1];
+  h.stage1 = rk.buf[2];
+  h.stage2 = rk.buf[3];
+  h.st = st;
   h.dt = dt;
   h.loop = 2;
   CUDA_TRY(ho4d_make_maps(h));
-  const long long cap =
-      std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
-  CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
-  CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
-  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
-                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
-                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
-  ++ctx->launches;
-  HoStage stages[3];
-  const int ns = ho_stages(cfg->time_order, stages);
-  unsigned long long* maxbits = &ctx->st->maxdv_bits;
-  const size_t pe = static_cast<size_t>(plane);
-  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
-    for (int q = 0; q < ns; ++q) {
-      double* src = stages[q].src == 0 ? ((k & 1) ? h.buf1 : h.buf0)
-                                       : (stages[q].src == 1 ? h.stage1 : h.stage2);
-      if (comm->nranks > 1) {
-        NCCL_TRY(api->GroupStart());
-        if (has_lo) {
-          NCCL_TRY(api->Send(src + h.cbeg * pe, R * pe, ncclFloat64_, r - 1, comm->comm,
-                             ctx->stream));
-          NCCL_TRY(api->Recv(src + (h.cbeg - R) * pe, R * pe, ncclFloat64_, r - 1, comm->comm,
-                             ctx->stream));
-        }
-        if (has_hi) {
-          NCCL_TRY(api->Send(src + (h.cend - R) * pe, R * pe, ncclFloat64_, r + 1, comm->comm,
-                             ctx->stream));
-          NCCL_TRY(api->Recv(src + h.cend * pe, R * pe, ncclFloat64_, r + 1, comm->comm,
-                             ctx->stream));
-        }
-        NCCL_TRY(api->GroupEnd());
-      }
-      Ho4dArgs x = h;
-      x.src_sel = stages[q].src;
-      x.dst_sel = stages[q].dst;
-      x.kind = stages[q].kind;
-      x.final_stage = q == ns - 1;
-      CUDA_TRY(launch_ho4d(x, p.shape, ctx->stream));
-    }
-    NCCL_TRY(api->AllReduce(maxbits, maxbits, 1, ncclUint64_, ncclMax_, comm->comm, ctx->stream));
-    CUDA_TRY(launch_epilogue(ctx->st, hd, use, ctx->stream));
-    return HJB_OK;
-  };
-  cudaEvent_t e0, e1;
-  CUDA_TRY(cudaEventCreate(&e0));
-  CUDA_TRY(cudaEventCreate(&e1));
-  CUDA_TRY(cudaEventRecord(e0, ctx->stream));
-  int rc = run_sharded_loop(ctx, 2, step);  // even body: parity of position k == iteration
-  if (rc) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return rc;
+  rk.hi = h;
+  rk.hb = h;
+  if (rk.sp.inner) {
+    rk.hi.cbeg = rk.sp.i0;
+    rk.hi.cend = rk.sp.i1;
+    ho4d_chunks(rk.hi, sms);
   }
-  CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+  if (rk.sp.bnd) ho4d_ranges(rk.hb, rk.sp.b0, rk.sp.e0, rk.sp.b1, rk.sp.e1);
+  return HJB_OK;
+}
+
+// the owned planes of the final V -> reference layout
+int unpad_rank(const SlabRank& rk, const Prepared& p, long long iters, double* out,
+               cudaStream_t s) {
+  const double* fin = rk.value(iters) + rk.geo.cbeg * rk.pe;
+  if (!rk.ho) {
+    const uint64_t rows_owned = static_cast<uint64_t>(rk.geo.owned) * p.g.n[1] * p.g.n[2];
+    CUDA_TRY(launch_unpad4(fin, out, rows_owned, p.g.n[3], rk.fi.n3p, s));
+  } else {
+    CUDA_TRY(ho4d_unpad(fin, out, rk.geo.owned, rk.hi, s));
+  }
+  return HJB_OK;
+}
+
+// -------------------------------------------------------------- transports
+int nccl_exchange(Nccl* api, hjb_comm* comm, const SlabRank& rk, double* buf, cudaStream_t s) {
+  const Halo h = halo_of(rk.geo);
+  const size_t pe = rk.pe, cnt = static_cast<size_t>(h.planes) * pe;
+  const int r = comm->rank;
+  NCCL_TRY(api->GroupStart());
+  if (rk.geo.has_lo) {
+    NCCL_TRY(api->Send(buf + h.send_lo * pe, cnt, ncclFloat64_, r - 1, comm->comm, s));
+    NCCL_TRY(api->Recv(buf + h.recv_lo * pe, cnt, ncclFloat64_, r - 1, comm->comm, s));
+  }
+  if (rk.geo.has_hi) {
+    NCCL_TRY(api->Send(buf + h.send_hi * pe, cnt, ncclFloat64_, r + 1, comm->comm, s));
+    NCCL_TRY(api->Recv(buf + h.recv_hi * pe, cnt, ncclFloat64_, r + 1, comm->comm, s));
+  }
+  NCCL_TRY(api->GroupEnd());
+  return HJB_OK;
+}
+
+// In-process ranks on one device: rank r's halo planes receive the planes
+// its neighbours send (the same Halo offsets as the NCCL transport).
+// bufs[r] = the stage buffer of rank r.
+int local_exchange(const std::vector<SlabRank>& rks, const std::vector<double*>& bufs,
+                   cudaStream_t s) {
+  const int P = static_cast<int>(rks.size());
+  for (int r = 0; r < P; ++r) {
+    const Halo h = halo_of(rks[r].geo);
+    const size_t pe = rks[r].pe;
+    const size_t bytes = static_cast<size_t>(h.planes) * pe * sizeof(double);
+    if (rks[r].geo.has_lo) {
+      const Halo n = halo_of(rks[r - 1].geo);
+      CUDA_TRY(cudaMemcpyAsync(bufs[r] + h.recv_lo * pe, bufs[r - 1] + n.send_hi * pe, bytes,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    if (rks[r].geo.has_hi) {
+      const Halo n = halo_of(rks[r + 1].geo);
+      CUDA_TRY(cudaMemcpyAsync(bufs[r] + h.recv_hi * pe, bufs[r + 1] + n.send_lo * pe, bytes,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return HJB_OK;
+}
+
+constexpr int kMaxLocalRanks = 16;
+struct RankStates {
+  LoopState* st[kMaxLocalRanks];
+  int n;
+};
+// max over the in-process ranks' max|dV| bits, written back to every rank
+// (the all-reduce of the NCCL transport)
+// slot < 0: maxdv_bits, else maxdv_slot[slot] (pipelined loop)
+__global__ void k_reduce_ranks(RankStates p, int slot) {
+  if (threadIdx.x != 0) return;
+  unsigned long long m = 0ull;
+  for (int r = 0; r < p.n; ++r) {
+    unsigned long long* a = slot < 0 ? &p.st[r]->maxdv_bits : &p.st[r]->maxdv_slot[slot];
+    const unsigned long long b = *(volatile unsigned long long*)a;
+    m = b > m ? b : m;
+  }
+  for (int r = 0; r < p.n; ++r) {
+    unsigned long long* a = slot < 0 ? &p.st[r]->maxdv_bits : &p.st[r]->maxdv_slot[slot];
+    *a = m;
+  }
+  __threadfence();
+}
+
+// HJB_SHARD_OVERLAP=0: the halo transfer runs on the main stream after the
+// whole slab is swept (the serial protocol; A/B of the overlap)
+bool shard_overlap() {
+  const char* e = std::getenv("HJB_SHARD_OVERLAP");
+  return !(e && std::strcmp(e, "0") == 0);
+}
+
+// HJB_SHARD_PIPE=0: the residual all-reduce + epilogue of sweep k run on the
+// main stream before sweep k + 1 (no pipelining)
+bool shard_pipeline() {
+  const char* e = std::getenv("HJB_SHARD_PIPE");
+  return !(e && std::strcmp(e, "0") == 0);
+}
+
+// The comm stream and the events of the sharded loop.  Pipelined residual:
+// position k's sweep accumulates max|dV| into st->maxdv_slot[k & 1]; after
+// its interior (ev_int) the comm stream all-reduces that slot and runs the
+// epilogue (ev_epi[k & 1]) while the main stream already sweeps position
+// k + 1.  Position k reads V_k and writes V_{k+1} over V_{k-1}; if epilogue
+// k - 2 stopped the loop, V_{k-1} is the result, so position k first waits
+// ev_epi[k & 1] (epilogue k - 2).  The one speculative sweep that can run
+// after the stopping sweep overwrites only the previous iterate, and its
+// epilogue returns early (done); the loop state's iteration count, history
+// and status are the unpipelined ones.
+struct StreamPair {
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_xfer = nullptr, ev_int = nullptr, e0 = nullptr, e1 = nullptr;
+  cudaEvent_t ev_epi[2] = {nullptr, nullptr};
+  ~StreamPair() {
+    for (cudaEvent_t e : {ev_bnd, ev_xfer, ev_int, e0, e1, ev_epi[0], ev_epi[1]})
+      if (e) cudaEventDestroy(e);
+    if (comm) cudaStreamDestroy(comm);
+  }
+  cudaError_t init() {
+    cudaError_t e = cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&ev_bnd, &ev_xfer, &ev_int, &ev_epi[0], &ev_epi[1]})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&e1);
+    return e;
+  }
+};
+
+// result fields from the loop state of the reporting rank
+int fill_result(hjb_context* ctx, float ms, hjb_solve_result* res) {
   CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
                            ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   const LoopState& st = *ctx->st_host;
-  ctx->launches += (ns + 1) * (st.iter + 2);
   res->iterations = st.iter;
   res->converged = st.converged;
   res->final_residual = st.last_residual;
@@ -309,12 +579,36 @@ int solve_sharded_ho(hjb_context* ctx, hjb_comm* comm, Nccl* api, const Prepared
   if (nh > 0 && res->wall_ms_history)
     CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
-  const double* fin = ((st.iter & 1) ? h.buf1 : h.buf0) + h.cbeg * pe;
-  CUDA_TRY(ho4d_unpad(fin, value_slab_out, owned, h, ctx->stream));
-  ++ctx->launches;
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (st.status == HJB_ERR_DIVERGED)
-    return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+  return HJB_OK;
+}
+
+// validation, slab-thickness check and the CFL scan shared by both drivers;
+// `allreduce` (may be null) turns the local scan into the global one
+int sharded_prologue(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
+                     const hjb_dbounds* db, const hjb_solve_config* cfg, int P, Prepared& p,
+                     Scan& s, uint32_t& R, const std::function<int(Scan&)>& allreduce,
+                     const DevGrid* scan_grid_override) {
+  int rc;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  if ((rc = validate_config(cfg))) return rc;
+  if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
+  if (p.shape < 0)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
+  if (fast4d_shape(p.g, p.hm.dm, scheme_of(cfg)) != p.shape)
+    return set_err(HJB_ERR_UNSUPPORTED,
+                   "solve_sharded: Lax-Friedrichs needs one input term per row of the 4D model");
+  const bool high_order = cfg->spatial_order > 1 || cfg->time_order > 1;
+  R = high_order ? static_cast<uint32_t>(cfg->spatial_order < 1 ? 1 : cfg->spatial_order) : 1u;
+  // Every rank must reject a too-thin partition BEFORE the first collective:
+  // balanced slabs differ by one plane, so a per-rank check would let the
+  // thicker ranks enter NCCL while a thin one returns (a hang, not an error).
+  // The smallest slab is floor(n0 / P) planes on every rank's view.
+  if (P > 1 && static_cast<int64_t>(p.g.n[0]) / P < static_cast<int64_t>(R))
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: slab thinner than the ENO halo");
+  if ((rc = run_scan(ctx, scan_grid_override ? *scan_grid_override : p.g, p.hm.dm, s))) return rc;
+  if (allreduce && (rc = allreduce(s))) return rc;
+  if (!(s.max_speed_sum > 0.0))
+    return set_err(HJB_ERR_RUNTIME, "solve: flow is identically zero on the grid");
   return HJB_OK;
 }
 
@@ -494,59 +788,168 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
                           double* value_slab_out, hjb_solve_result* res) {
   int rc;
   if (!ctx || !comm) return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_sharded: null context/comm");
-  CUDA_TRY(cudaSetDevice(ctx->device));
-  if ((rc = validate_config(cfg))) return rc;
-  Prepared p;
-  if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
-  if (p.shape < 0)
-    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
-  const bool high_order = cfg->spatial_order > 1 || cfg->time_order > 1;
-  // the scheme's own variant of the fast path (first and high order)
-  const int scheme = scheme_of(cfg);
-  if (fast4d_shape(p.g, p.hm.dm, scheme) != p.shape)
-    return set_err(HJB_ERR_UNSUPPORTED,
-                   "solve_sharded: Lax-Friedrichs needs one input term per row of the 4D model");
   Nccl* api = nccl();
   if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
   const int P = comm->nranks, r = comm->rank;
-  int64_t slab_b, slab_e;
-  if ((rc = hjb_slab_partition(p.g.n[0], P, r, &slab_b, &slab_e))) return rc;
-  const uint32_t owned = static_cast<uint32_t>(slab_e - slab_b);
-  const bool has_lo = r > 0, has_hi = r < P - 1;
-  // Every rank must reject a too-thin partition BEFORE the first collective:
-  // balanced slabs differ by one plane, so a per-rank check would let the
-  // thicker ranks enter NCCL while a thin one returns (a hang, not an error).
-  // The smallest slab is floor(n0 / P) planes on every rank's view.
-  {
-    const int64_t R = high_order ? (cfg->spatial_order < 1 ? 1 : cfg->spatial_order) : 1;
-    if (P > 1 && static_cast<int64_t>(p.g.n[0]) / P < R)
-      return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: slab thinner than the ENO halo");
-  }
-  const uint32_t nloc = owned + (has_lo ? 1 : 0) + (has_hi ? 1 : 0);
-
+  Prepared p;
+  Scan s;
+  uint32_t R = 1;
   // CFL scan over the slab + all-reduce(max): rows of the fast path never
   // depend on x0, so the slab's local grid gives the global values
-  DevGrid gl = p.g;
-  gl.n[0] = owned;
-  gl.size = owned * gl.stride[0];
-  gl.divs[0].init(owned);
-  Scan s;
-  if ((rc = run_scan(ctx, gl, p.hm.dm, s))) return rc;
-  {
+  DevGrid gl;
+  auto allreduce = [&](Scan& sc) -> int {
     unsigned long long bits[1 + kMaxDims];
-    std::memcpy(bits, &s.max_speed_sum, sizeof(double));
-    std::memcpy(bits + 1, s.max_alpha, kMaxDims * sizeof(double));
+    std::memcpy(bits, &sc.max_speed_sum, sizeof(double));
+    std::memcpy(bits + 1, sc.max_alpha, kMaxDims * sizeof(double));
     unsigned long long* dbits = reinterpret_cast<unsigned long long*>(ctx->scratch.d());
     CUDA_TRY(cudaMemcpyAsync(dbits, bits, sizeof bits, cudaMemcpyHostToDevice, ctx->stream));
     NCCL_TRY(api->AllReduce(dbits, dbits, 1 + kMaxDims, ncclUint64_, ncclMax_, comm->comm,
                             ctx->stream));
     CUDA_TRY(cudaMemcpyAsync(bits, dbits, sizeof bits, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(&s.max_speed_sum, bits, sizeof(double));
-    std::memcpy(s.max_alpha, bits + 1, kMaxDims * sizeof(double));
+    std::memcpy(&sc.max_speed_sum, bits, sizeof(double));
+    std::memcpy(sc.max_alpha, bits + 1, kMaxDims * sizeof(double));
+    return HJB_OK;
+  };
+  {
+    // the slab's own grid for the scan (needs p.g: validate/prepare first)
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if ((rc = validate_config(cfg))) return rc;
+    DevGrid g;
+    if ((rc = make_grid(gi, g))) return rc;
+    if (g.nd != 4)
+      return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
+    int64_t b, e;
+    if ((rc = hjb_slab_partition(g.n[0], P, r, &b, &e))) return rc;
+    gl = g;
+    gl.n[0] = static_cast<uint32_t>(e - b);
+    gl.size = gl.n[0] * gl.stride[0];
+    gl.divs[0].init(gl.n[0]);
   }
-  if (!(s.max_speed_sum > 0.0))
-    return set_err(HJB_ERR_RUNTIME, "solve: flow is identically zero on the grid");
+  if ((rc = sharded_prologue(ctx, gi, mi, db, cfg, P, p, s, R, allreduce, &gl))) return rc;
+  const double dt = cfg->cfl_factor / s.max_speed_sum;
+  hjb_solve_result local;
+  std::memset(&local, 0, sizeof local);
+  if (!res) res = &local;
+  res->dt = dt;
+  res->nodes_per_sweep = p.g.size;
+  res->iterations = 0;
+  res->converged = 0;
+  const SlabGeom geo = slab_geom(p.g.n[0], P, r, R);
+  if (cfg->max_iters == 0) {
+    CUDA_TRY(cudaMemcpyAsync(value_slab_out, init_slab,
+                             static_cast<size_t>(geo.owned) * p.g.stride[0] * sizeof(double),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return HJB_OK;
+  }
+  SlabRank rk;
+  DevBuf* const bufs[4] = {&ctx->v0, &ctx->v1, &ctx->v2, &ctx->v3};
+  if ((rc = setup_rank(ctx->device, p, cfg, dt, s.max_alpha, geo, bufs, &ctx->pcbuf, ctx->st,
+                       init_slab, c_slab, ctx->stream, rk, &ctx->launches)))
+    return rc;
+  const long long cap =
+      std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
+  CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
+  CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
+  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
+                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
+                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
+  ++ctx->launches;
+  StreamPair sp;
+  CUDA_TRY(sp.init());
+  // halos of V_0 (afterwards every stage output travels right after its
+  // boundary planes are swept)
+  if (P > 1 && (rc = nccl_exchange(api, comm, rk, rk.buf[0], ctx->stream))) return rc;
+  unsigned long long* maxbits = &ctx->st->maxdv_bits;
+  const bool xfer = P > 1 && rk.sp.bnd;
+  long long per_pos = 0;
+  // one loop position: per stage, boundary planes -> (comm stream) halo
+  // send/recv of the stage output || interior planes; join; then the
+  // residual all-reduce and the device epilogue
+  const bool overlap = shard_overlap();
+  const bool pipe = shard_pipeline();
+  const int body = rk.ho ? 2 : 8;  // even: buffer parity of position k == iteration parity
+  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
+    per_pos = 0;
+    unsigned long long* slot = pipe ? &ctx->st->maxdv_slot[k & 1] : maxbits;
+    // position k overwrites V_{k-1}: epilogue k - 2 must have run
+    if (pipe && k >= 2) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
+    for (int q = 0; q < rk.ns; ++q) {
+      if (xfer && !overlap) {  // serial: whole slab, then the exchange
+        CUDA_TRY(rk.launch(k, q, true, slot));
+        if (rk.sp.inner) CUDA_TRY(rk.launch(k, q, false, slot));
+        int e = nccl_exchange(api, comm, rk, rk.stage_out(k, q), ctx->stream);
+        if (e) return e;
+        per_pos += rk.sp.inner ? 2 : 1;
+        continue;
+      }
+      if (xfer) {
+        CUDA_TRY(rk.launch(k, q, true, slot));
+        CUDA_TRY(cudaEventRecord(sp.ev_bnd, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_bnd, 0));
+        int e = nccl_exchange(api, comm, rk, rk.stage_out(k, q), sp.comm);
+        if (e) return e;
+        CUDA_TRY(cudaEventRecord(sp.ev_xfer, sp.comm));
+        ++per_pos;
+      } else if (rk.sp.bnd) {
+        CUDA_TRY(rk.launch(k, q, true, slot));
+        ++per_pos;
+      }
+      if (rk.sp.inner) {
+        CUDA_TRY(rk.launch(k, q, false, slot));
+        ++per_pos;
+      }
+      if (xfer) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_xfer, 0));
+    }
+    if (!pipe) {
+      NCCL_TRY(api->AllReduce(maxbits, maxbits, 1, ncclUint64_, ncclMax_, comm->comm,
+                              ctx->stream));
+      CUDA_TRY(launch_epilogue(ctx->st, hd, use, ctx->stream));
+    } else {
+      CUDA_TRY(cudaEventRecord(sp.ev_int, ctx->stream));
+      CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_int, 0));
+      NCCL_TRY(api->AllReduce(slot, slot, 1, ncclUint64_, ncclMax_, comm->comm, sp.comm));
+      CUDA_TRY(launch_epilogue(ctx->st, hd, use, sp.comm, slot));
+      CUDA_TRY(cudaEventRecord(sp.ev_epi[k & 1], sp.comm));
+      // the body ends joined (the loop condition / poll reads the epilogue)
+      if (k == body - 1) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
+    }
+    ++per_pos;
+    return HJB_OK;
+  };
+  CUDA_TRY(cudaEventRecord(sp.e0, ctx->stream));
+  if ((rc = run_sharded_loop(ctx, body, step))) return rc;
+  CUDA_TRY(cudaEventRecord(sp.e1, ctx->stream));
+  CUDA_TRY(cudaEventSynchronize(sp.e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, sp.e0, sp.e1);
+  if ((rc = fill_result(ctx, ms, res))) return rc;
+  ctx->launches += per_pos * (res->iterations + body);
+  const LoopState& st = *ctx->st_host;
+  if ((rc = unpad_rank(rk, p, st.iter, value_slab_out, ctx->stream))) return rc;
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (st.status == HJB_ERR_DIVERGED)
+    return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");
+  return HJB_OK;
+}
+
+int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid* gi,
+                                const hjb_model* mi, const hjb_dbounds* db, const double* init,
+                                const double* c, const hjb_solve_config* cfg, double* value_out,
+                                hjb_solve_result* res) {
+  int rc;
+  if (!ctx) return set_err(HJB_ERR_INVALID_ARGUMENT, "context: null");
+  if (nranks < 1 || nranks > kMaxLocalRanks)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_sharded_local: 1..16 ranks");
+  const int P = nranks;
+  Prepared p;
+  Scan s;
+  uint32_t R = 1;
+  if ((rc = sharded_prologue(ctx, gi, mi, db, cfg, P, p, s, R, nullptr, nullptr))) return rc;
+  if (static_cast<int64_t>(p.g.n[0]) < P)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "slab_partition: need 0 <= rank < nranks <= n0");
   const double dt = cfg->cfl_factor / s.max_speed_sum;
   hjb_solve_result local;
   std::memset(&local, 0, sizeof local);
@@ -556,174 +959,136 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   res->iterations = 0;
   res->converged = 0;
   if (cfg->max_iters == 0) {
-    CUDA_TRY(cudaMemcpyAsync(value_slab_out, init_slab,
-                             static_cast<size_t>(owned) * p.g.stride[0] * sizeof(double),
+    CUDA_TRY(cudaMemcpyAsync(value_out, init, static_cast<size_t>(p.g.size) * sizeof(double),
                              cudaMemcpyDeviceToDevice, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return HJB_OK;
   }
-
-  if (high_order)
-    return solve_sharded_ho(ctx, comm, api, p, cfg, dt, s.max_alpha, owned, has_lo, has_hi,
-                            init_slab, c_slab,
-                            value_slab_out, res);
-
-  // local padded slab arrays: [halo_lo?][owned][halo_hi?]
-  DevGrid gloc = p.g;
-  gloc.n[0] = nloc;
-  Fast4dArgs f;
-  std::memset(&f, 0, sizeof f);
-  f.kcells = 2;
-  f.maxthreads = 576;
-  f.cbeg = has_lo ? 1u : 0u;
-  f.cend = f.cbeg + owned;
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  f.tab_len = static_cast<uint32_t>(p.hm.tab.size());
-  fast4d_config(gloc, sms > 0 ? sms : 148, f);
-  const uint64_t plane = static_cast<uint64_t>(p.g.n[1]) * p.g.n[2] * f.n3p;  // padded plane
-  const uint64_t rows_owned = static_cast<uint64_t>(owned) * p.g.n[1] * p.g.n[2];
-  const size_t lbytes = static_cast<size_t>(nloc) * plane * sizeof(double);
-  CUDA_TRY(ctx->v2.ensure(lbytes));
-  CUDA_TRY(ctx->v3.ensure(lbytes));
-  CUDA_TRY(ctx->pcbuf.ensure(lbytes));
-  CUDA_TRY(cudaMemsetAsync(ctx->v2.p, 0, lbytes, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(ctx->v3.p, 0, lbytes, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(ctx->pcbuf.p, 0, lbytes, ctx->stream));
-  double* own0 = ctx->v2.d() + f.cbeg * plane;
-  CUDA_TRY(launch_pad4(init_slab, own0, rows_owned, p.g.n[3], f.n3p, ctx->stream));
-  CUDA_TRY(launch_pad4(c_slab, ctx->pcbuf.d() + f.cbeg * plane, rows_owned, p.g.n[3], f.n3p,
-                       ctx->stream));
-  ctx->launches += 2;
-  fill_tables(p, f);
-  fill_lf(p.hm.dm, scheme, s.max_alpha, f);
-  if (f.lf) {  // the Lax-Friedrichs variant's CTA size
-    f.maxthreads = 448;
-    f.cbeg = has_lo ? 1u : 0u;
-    f.cend = f.cbeg + owned;
-    fast4d_config(gloc, sms > 0 ? sms : 148, f);
+  const size_t s0 = p.g.stride[0];
+  // per-rank buffers (rank 0 uses the context's, so its loop state drives
+  // the loop and the result), loop states of ranks 1..P-1
+  std::vector<std::unique_ptr<DevBuf>> own;
+  DevBuf states;
+  CUDA_TRY(states.ensure(static_cast<size_t>(P) * sizeof(LoopState)));
+  std::vector<SlabRank> rks(P);
+  RankStates rs;
+  rs.n = P;
+  for (int r = 0; r < P; ++r) {
+    const SlabGeom geo = slab_geom(p.g.n[0], P, r, R);
+    DevBuf* bufs[4];
+    DevBuf* cb;
+    if (r == 0) {
+      bufs[0] = &ctx->v0;
+      bufs[1] = &ctx->v1;
+      bufs[2] = &ctx->v2;
+      bufs[3] = &ctx->v3;
+      cb = &ctx->pcbuf;
+    } else {
+      for (int b = 0; b < 4; ++b) {
+        own.emplace_back(new DevBuf());
+        bufs[b] = own.back().get();
+      }
+      own.emplace_back(new DevBuf());
+      cb = own.back().get();
+    }
+    LoopState* st = r == 0 ? ctx->st : reinterpret_cast<LoopState*>(states.p) + r;
+    rs.st[r] = st;
+    if ((rc = setup_rank(ctx->device, p, cfg, dt, s.max_alpha, geo, bufs, cb, st,
+                         init + geo.gbeg * s0, c + geo.gbeg * s0, ctx->stream, rks[r],
+                         &ctx->launches)))
+      return rc;
+    if (rks[r].pe != rks[0].pe)
+      return set_err(HJB_ERR_RUNTIME, "solve_sharded_local: plane layouts differ across ranks");
   }
-  f.c = ctx->pcbuf.d();
-  f.buf0 = ctx->v2.d();
-  f.buf1 = ctx->v3.d();
-  CUtensorMap map_b0, map_b1;
-  CUDA_TRY(fast4d_make_maps(f, f.buf0, f.buf1, f.c));
-  map_b0 = f.map0;
-  map_b1 = f.map1;
-  f.st = ctx->st;
-  f.dt = dt;
-  f.loop = 2;
-
   const long long cap =
       std::min<long long>(cfg->max_iters, std::max<long long>(res->history_capacity, 1));
   CUDA_TRY(ctx->hist.ensure(cap * sizeof(double)));
   CUDA_TRY(ctx->whist.ensure(cap * sizeof(double)));
-  CUDA_TRY(launch_loop_init(ctx->st, cfg->max_iters, dt, cfg->tolerance,
-                            cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
-                            ctx->hist.d(), ctx->whist.d(), ctx->stream));
-  ++ctx->launches;
-  unsigned long long* maxbits = &ctx->st->maxdv_bits;
-  const size_t pe = static_cast<size_t>(plane);
-  // one sweep at a fixed buffer parity: exchange, sweep, all-reduce, epilogue
-  auto sweep = [&](int k, cudaGraphConditionalHandle h, int use) -> int {
-    double* src = (k & 1) ? f.buf1 : f.buf0;
-    double* dst = (k & 1) ? f.buf0 : f.buf1;
-    if (P > 1) {
-      NCCL_TRY(api->GroupStart());
-      if (has_lo) {
-        NCCL_TRY(api->Send(src + f.cbeg * pe, pe, ncclFloat64_, r - 1, comm->comm, ctx->stream));
-        NCCL_TRY(api->Recv(src, pe, ncclFloat64_, r - 1, comm->comm, ctx->stream));
+  for (int r = 0; r < P; ++r) {
+    CUDA_TRY(launch_loop_init(rs.st[r], cfg->max_iters, dt, cfg->tolerance,
+                              cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0,
+                              r == 0 ? cap : 0, r == 0 ? ctx->hist.d() : nullptr,
+                              r == 0 ? ctx->whist.d() : nullptr, ctx->stream));
+    ++ctx->launches;
+  }
+  StreamPair sp;
+  CUDA_TRY(sp.init());
+  std::vector<double*> xb(P);
+  for (int r = 0; r < P; ++r) xb[r] = rks[r].buf[0];
+  if (P > 1 && (rc = local_exchange(rks, xb, ctx->stream))) return rc;
+  long long per_pos = 0;
+  const bool overlap = shard_overlap();
+  const bool pipe = shard_pipeline();
+  const int body = rks[0].ho ? 2 : 8;
+  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
+    per_pos = 0;
+    std::vector<unsigned long long*> acc(P);
+    for (int r = 0; r < P; ++r)
+      acc[r] = pipe ? &rs.st[r]->maxdv_slot[k & 1] : &rs.st[r]->maxdv_bits;
+    if (pipe && k >= 2) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
+    for (int q = 0; q < rks[0].ns; ++q) {
+      if (P > 1 && !overlap) {  // serial: every slab, then the exchange
+        for (int r = 0; r < P; ++r) {
+          CUDA_TRY(rks[r].launch(k, q, true, acc[r]));
+          if (rks[r].sp.inner) CUDA_TRY(rks[r].launch(k, q, false, acc[r]));
+          per_pos += rks[r].sp.inner ? 2 : 1;
+        }
+        for (int r = 0; r < P; ++r) xb[r] = rks[r].stage_out(k, q);
+        int e = local_exchange(rks, xb, ctx->stream);
+        if (e) return e;
+        continue;
       }
-      if (has_hi) {
-        NCCL_TRY(api->Send(src + (f.cend - 1) * pe, pe, ncclFloat64_, r + 1, comm->comm,
-                           ctx->stream));
-        NCCL_TRY(api->Recv(src + f.cend * pe, pe, ncclFloat64_, r + 1, comm->comm, ctx->stream));
+      for (int r = 0; r < P; ++r)
+        if (rks[r].sp.bnd) {
+          CUDA_TRY(rks[r].launch(k, q, true, acc[r]));
+          ++per_pos;
+        }
+      if (P > 1) {
+        CUDA_TRY(cudaEventRecord(sp.ev_bnd, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_bnd, 0));
+        for (int r = 0; r < P; ++r) xb[r] = rks[r].stage_out(k, q);
+        int e = local_exchange(rks, xb, sp.comm);
+        if (e) return e;
+        CUDA_TRY(cudaEventRecord(sp.ev_xfer, sp.comm));
       }
-      NCCL_TRY(api->GroupEnd());
+      for (int r = 0; r < P; ++r)
+        if (rks[r].sp.inner) {
+          CUDA_TRY(rks[r].launch(k, q, false, acc[r]));
+          ++per_pos;
+        }
+      if (P > 1) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_xfer, 0));
     }
-    Fast4dArgs x = f;
-    x.src = src;
-    x.dst = dst;
-    x.map0 = (k & 1) ? map_b1 : map_b0;
-    CUDA_TRY(launch_fast4d(x, p.shape, ctx->stream));
-    NCCL_TRY(api->AllReduce(maxbits, maxbits, 1, ncclUint64_, ncclMax_, comm->comm, ctx->stream));
-    CUDA_TRY(launch_epilogue(ctx->st, h, use, ctx->stream));
+    cudaStream_t es = ctx->stream;
+    if (pipe) {
+      CUDA_TRY(cudaEventRecord(sp.ev_int, ctx->stream));
+      CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_int, 0));
+      es = sp.comm;
+    }
+    k_reduce_ranks<<<1, 32, 0, es>>>(rs, pipe ? (k & 1) : -1);
+    CUDA_TRY(cudaGetLastError());
+    for (int r = 0; r < P; ++r)
+      CUDA_TRY(launch_epilogue(rs.st[r], hd, use, es, pipe ? acc[r] : nullptr));
+    if (pipe) {
+      CUDA_TRY(cudaEventRecord(sp.ev_epi[k & 1], sp.comm));
+      if (k == body - 1) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
+    }
+    per_pos += 1 + P;
     return HJB_OK;
   };
-  cudaEvent_t e0, e1;
-  CUDA_TRY(cudaEventCreate(&e0));
-  CUDA_TRY(cudaEventCreate(&e1));
-  CUDA_TRY(cudaEventRecord(e0, ctx->stream));
-  const int body = 8;  // even: buffer parity of position k == iteration parity
-  const char* mode = std::getenv("HJB_LOOP");
-  if (mode && std::strcmp(mode, "poll") == 0) {
-    for (;;) {
-      for (int k = 0; k < body; ++k)
-        if ((rc = sweep(k, 0, 0))) return rc;
-      CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
-                               ctx->stream));
-      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-      if (ctx->st_host->done) break;
-    }
-  } else {
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    CUDA_TRY(cudaGraphCreate(&graph, 0));
-    cudaGraphConditionalHandle handle;
-    rc = HJB_OK;
-    do {
-      cudaError_t e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
-      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
-      cudaGraphNodeParams cp = {};
-      cp.type = cudaGraphNodeTypeConditional;
-      cp.conditional.handle = handle;
-      cp.conditional.type = cudaGraphCondTypeWhile;
-      cp.conditional.size = 1;
-      cudaGraphNode_t node;
-      e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
-      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
-      e = cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr,
-                                        nullptr, 0, cudaStreamCaptureModeThreadLocal);
-      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
-      for (int k = 0; k < body && rc == HJB_OK; ++k) rc = sweep(k, handle, 1);
-      cudaGraph_t captured = nullptr;
-      e = cudaStreamEndCapture(ctx->stream, &captured);
-      if (rc) break;
-      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
-      e = cudaGraphInstantiate(&exec, graph, 0);
-      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
-      e = cudaGraphLaunch(exec, ctx->stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-      if (e != cudaSuccess) { rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e)); break; }
-    } while (0);
-    if (exec) cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    if (rc) return rc;
-  }
-  CUDA_TRY(cudaEventRecord(e1, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(LoopState), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaEventRecord(sp.e0, ctx->stream));
+  if ((rc = run_sharded_loop(ctx, body, step))) return rc;
+  CUDA_TRY(cudaEventRecord(sp.e1, ctx->stream));
+  CUDA_TRY(cudaEventSynchronize(sp.e1));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  cudaEventElapsedTime(&ms, sp.e0, sp.e1);
+  if ((rc = fill_result(ctx, ms, res))) return rc;
+  ctx->launches += per_pos * (res->iterations + body);
   const LoopState& st = *ctx->st_host;
-  ctx->launches += 2 * (st.iter + body);
-  res->iterations = st.iter;
-  res->converged = st.converged;
-  res->final_residual = st.last_residual;
-  res->wall_seconds = ms * 1e-3;
-  const long long nh = std::min<long long>(st.iter, res->history_capacity);
-  if (nh > 0 && res->residual_history)
-    CUDA_TRY(cudaMemcpyAsync(res->residual_history, ctx->hist.p, nh * sizeof(double),
-                             cudaMemcpyDeviceToHost, ctx->stream));
-  if (nh > 0 && res->wall_ms_history)
-    CUDA_TRY(cudaMemcpyAsync(res->wall_ms_history, ctx->whist.p, nh * sizeof(double),
-                             cudaMemcpyDeviceToHost, ctx->stream));
-  const double* fin = ((st.iter & 1) ? f.buf1 : f.buf0) + f.cbeg * pe;
-  CUDA_TRY(launch_unpad4(fin, value_slab_out, rows_owned, p.g.n[3], f.n3p, ctx->stream));
-  ++ctx->launches;
+  for (int r = 0; r < P; ++r) {
+    if ((rc = unpad_rank(rks[r], p, st.iter, value_out + rks[r].geo.gbeg * s0, ctx->stream)))
+      return rc;
+    ++ctx->launches;
+  }
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (st.status == HJB_ERR_DIVERGED)
     return set_err(HJB_ERR_DIVERGED, "solve: diverging (residual grew 10x above its minimum)");

@@ -95,3 +95,24 @@ def solve_sharded_dev(comm: Comm, grid: hj.Grid, model: hj.DynamicsModel,
                           residual_history=rh[:n].copy(), wall_ms_history=wh[:n].copy(),
                           nodes_per_sweep=int(r.nodes_per_sweep),
                           final_residual=float(r.final_residual))
+
+
+def solve_sharded_local_dev(nranks: int, grid: hj.Grid, model: hj.DynamicsModel,
+                            dbounds: hj.IntervalField, init_ptr: int, c_ptr: int, out_ptr: int,
+                            cfg: hj.SolveConfig, ctx: hj.Context | None = None,
+                            history_capacity: int = 0):
+    """hjb_solve_sharded_local_dev: the slab-partitioned solve with `nranks`
+    in-process ranks on one device (full-grid device pointers); the same
+    per-rank plan, halo offsets and overlap as the NCCL path."""
+    lib = abi.load()
+    r, rh, wh = hj._c_result(int(history_capacity))
+    g, m, d, c = grid.to_c(), model.to_c(), dbounds.to_c(), cfg.to_c()
+    hj._check(lib.hjb_solve_sharded_local_dev(hj._ctx(ctx), int(nranks), C.byref(g), C.byref(m),
+                                              C.byref(d), C.c_void_p(init_ptr), C.c_void_p(c_ptr),
+                                              C.byref(c), C.c_void_p(out_ptr), C.byref(r)))
+    n = min(int(r.iterations), int(r.history_capacity))
+    return hj.SolveResult(value=None, iterations=int(r.iterations), dt=float(r.dt),
+                          wall_seconds=float(r.wall_seconds), converged=bool(r.converged),
+                          residual_history=rh[:n].copy(), wall_ms_history=wh[:n].copy(),
+                          nodes_per_sweep=int(r.nodes_per_sweep),
+                          final_residual=float(r.final_residual))

@@ -207,3 +207,145 @@ def test_high_order_slab_protocol_matches_unsharded(tmp_path, oracle, world, ord
     assert int(r["iterations"]) == want.iterations
     assert np.array_equal(r["history"], want.residual_history)
     assert np.array_equal(r["value"], want.value.values())
+
+
+def _plan(n0, world, rank, R):
+    """Boundary / interior planes of a rank (the split hjb_shard.cu's
+    plane_split makes, in global plane numbers)."""
+    b, e = slab_partition(n0, world, rank)
+    has_lo, has_hi = rank > 0, rank < world - 1
+    lo_end = b + R if has_lo else b
+    hi_beg = e - R if has_hi else e
+    if world == 1:
+        return b, e, [], [(b, e)]
+    if lo_end >= hi_beg:
+        return b, e, [(b, e)], []
+    bnd = ([(b, lo_end)] if has_lo else []) + ([(hi_beg, e)] if has_hi else [])
+    return b, e, bnd, [(lo_end, hi_beg)]
+
+
+def _pipelined_worker(rank, world, port, out_path, order, rk):
+    """The round-2 protocol of hjb_solve_sharded_dev, step by step on CPU:
+    per stage the BOUNDARY planes are swept first and the stage OUTPUT's
+    boundary planes travel (isend/irecv) while the INTERIOR planes sweep;
+    the residual all-reduce of sweep k is asynchronous and its epilogue is
+    applied only after sweep k + 1 was issued (pipelined); a stop at sweep k
+    keeps V_{k+1}, which the speculative sweep k + 1 does not overwrite."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Restatement
+    ora = Restatement(threads=1)
+    g, model, db, c, cfg = _problem()
+    max_iters = 60 if (order > 1 or rk > 1) else cfg.max_iters
+    n0 = g.dim(0).n
+    s0 = g.size() // n0
+    R = order
+    b, e, bnd, inner = _plan(n0, world, rank, R)
+    dt = ora.cfl_dt(g, model, db, cfg.cfl_factor)
+    vbuf = [c.copy(), c.copy()]
+    sbuf = {"s1": c.copy(), "s2": c.copy()}
+
+    def exchange_start(a):
+        reqs, got = [], []
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(a[b * s0:(b + R) * s0].copy()), rank - 1))
+            lo = torch.empty(R * s0, dtype=torch.float64)
+            reqs.append(dist.irecv(lo, rank - 1))
+            got.append(((b - R) * s0, lo))
+        if rank < world - 1:
+            reqs.append(dist.isend(torch.from_numpy(a[(e - R) * s0:e * s0].copy()), rank + 1))
+            hi = torch.empty(R * s0, dtype=torch.float64)
+            reqs.append(dist.irecv(hi, rank + 1))
+            got.append((e * s0, hi))
+        return reqs, got, a
+
+    def exchange_finish(x):
+        reqs, got, a = x
+        for q in reqs:
+            q.wait()
+        for off, t in got:
+            a[off:off + t.numel()] = t.numpy()
+
+    exchange_finish(exchange_start(vbuf[0]))  # halos of V_0
+    stages = _STAGES[rk]
+    hist, it, converged, stopped = [], 0, False, False
+    min_res, first = float("inf"), None
+    pending = None
+    k = 0
+    while True:
+        vn, out = vbuf[k & 1], vbuf[(k + 1) & 1]
+        names = {"v": vn, "n": out, **sbuf}
+        local = 0.0
+        for src, dst, kind in stages:
+            def run(ranges):
+                m = 0.0
+                for pb, pe in ranges:
+                    if order == 1 and rk == 1:
+                        m = max(m, ora.sweep_planes(g, model, db, names[src], c, dt, pb, pe,
+                                                    names[dst]))
+                    else:
+                        m = max(m, ora.ho_stage_planes(g, model, db, names[src], vn, c, dt, order,
+                                                       kind, pb, pe, names[dst]))
+                return m
+            local = run(bnd)  # the final stage's max|V_{n+1} - V_n| is the sweep's
+            x = exchange_start(names[dst])  # travels while the interior sweeps
+            local = max(local, run(inner))
+            exchange_finish(x)
+        t = torch.tensor([local], dtype=torch.float64)
+        work = dist.all_reduce(t, op=dist.ReduceOp.MAX, async_op=True)
+        if pending is not None:  # epilogue of sweep k - 1, after sweep k was issued
+            pw, pt = pending
+            pw.wait()
+            residual = float(pt.item()) / dt
+            it += 1
+            hist.append(residual)
+            if residual < cfg.tolerance:
+                converged = stopped = True
+            else:
+                if first is None:
+                    first = residual
+                min_res = min(min_res, residual)
+                assert residual <= 10 * max(min_res, first)
+            if it >= max_iters:
+                stopped = True
+        if stopped:
+            work.wait()  # the speculative sweep's all-reduce completes too
+            break
+        pending = (work, t)
+        k += 1
+    final = vbuf[it & 1]  # V_it: untouched by the speculative sweep
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (b, e, final[b * s0:e * s0].copy(), it, converged, hist))
+    if rank == 0:
+        full = np.empty(g.size())
+        for (bb, ee, arr, _, _, _) in gathered:
+            full[bb * s0:ee * s0] = arr
+        np.savez(out_path, value=full, iterations=it, converged=converged, history=np.array(hist))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,order,rk", [(2, 1, 1), (3, 1, 1), (2, 3, 3), (3, 2, 2)])
+def test_pipelined_overlap_protocol_matches_unsharded(tmp_path, oracle, world, order, rk):
+    out = tmp_path / "res.npz"
+    mp.spawn(_pipelined_worker, args=(world, _free_port(), str(out), order, rk), nprocs=world,
+             join=True)
+    r = np.load(out)
+    g, model, db, c, cfg = _problem()
+    if order > 1 or rk > 1:
+        cfg = hj.SolveConfig(tolerance=cfg.tolerance, max_iters=60, spatial_order=order,
+                             time_order=rk)
+    want = oracle.solve(hj.ScalarField(g, c), hj.ScalarField(g, c), model, db, cfg)
+    assert int(r["iterations"]) == want.iterations
+    assert bool(r["converged"]) == want.converged
+    assert np.array_equal(r["history"], want.residual_history)
+    assert np.array_equal(r["value"], want.value.values())
+
+
+def test_plane_split_covers_slab():
+    """Boundary + interior ranges tile every rank's slab exactly once."""
+    for n0, world, R in ((101, 8, 1), (101, 8, 3), (11, 3, 3), (17, 4, 2), (9, 2, 1)):
+        for rank in range(world):
+            b, e, bnd, inner = _plan(n0, world, rank, R)
+            planes = sorted(p for lo, hi in bnd + inner for p in range(lo, hi))
+            assert planes == list(range(b, e))

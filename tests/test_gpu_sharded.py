@@ -121,3 +121,115 @@ def test_sharded_single_rank_high_order_equals_solve(gpu_ctx, order, rk, scheme,
     assert r.iterations == ref.iterations
     assert same(r.residual_history, ref.residual_history)
     assert same(out.cpu().numpy(), ref.value.values())
+
+
+# ------------------------------------------- in-process ranks (world > 1)
+# hjb_solve_sharded_local_dev runs the per-rank plans of the NCCL path
+# (slab geometry, halo offsets, boundary planes first, interior while the
+# halos travel on a second stream, per-rank epilogues) for P ranks on one
+# device; the halo planes move by device copies.  Bitwise vs hjb_solve.
+
+def _local(gpu_ctx, w, c, cfg, P, cap):
+    ct = torch.tensor(c, device="cuda")
+    out = torch.full_like(ct, float("nan"))
+    torch.cuda.synchronize()
+    r = sharded.solve_sharded_local_dev(P, w.grid, w.model, w.dbounds(), ct.data_ptr(),
+                                        ct.data_ptr(), out.data_ptr(), cfg, gpu_ctx,
+                                        history_capacity=cap)
+    return r, out.cpu().numpy()
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_local_ranks_first_order_equal_solve(gpu_ctx, monkeypatch, P, overlap):
+    monkeypatch.setenv("HJB_SHARD_OVERLAP", overlap)
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=150)
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, P, 150)
+    assert r.iterations == ref.iterations == 150 and r.dt == ref.dt
+    assert same(r.residual_history, ref.residual_history)
+    assert same(v, ref.value.values())
+
+
+@pytest.mark.parametrize("scheme,diss,P", [(hj.LAX_FRIEDRICHS, hj.PER_NODE, 3),
+                                           (hj.LAX_FRIEDRICHS, hj.GLOBAL, 2)])
+def test_local_ranks_lax_friedrichs_equal_solve(gpu_ctx, scheme, diss, P):
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=120, scheme=scheme, dissipation=diss)
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, P, 120)
+    assert r.iterations == ref.iterations
+    assert same(r.residual_history, ref.residual_history)
+    assert same(v, ref.value.values())
+
+
+@pytest.mark.parametrize("order,rk,P,scheme", [(3, 3, 2, hj.GODUNOV), (3, 3, 3, hj.GODUNOV),
+                                               (2, 2, 4, hj.GODUNOV), (1, 3, 5, hj.GODUNOV),
+                                               (3, 3, 2, hj.LAX_FRIEDRICHS),
+                                               (2, 2, 3, hj.LAX_FRIEDRICHS)])
+def test_local_ranks_high_order_equal_solve(gpu_ctx, order, rk, P, scheme):
+    """ENO/TVD-RK slabs: halos of R = ENO order planes after every stage."""
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=30, scheme=scheme)
+    cfg.spatial_order, cfg.time_order = order, rk
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, P, 30)
+    assert r.iterations == ref.iterations == 30
+    assert same(r.residual_history, ref.residual_history)
+    assert same(v, ref.value.values())
+
+
+def test_local_ranks_irregular_grid(gpu_ctx):
+    """Odd extents on every axis, 3 ranks of 6/6/5 planes, first and third order."""
+    g, model, db = _setup((17, 9, 8, 11))
+    rng = np.random.default_rng(5)
+    c = band_np(g, 0, -4.0, 4.0)
+    init = c + 0.3 * rng.random(g.size())
+    for order, rk in ((1, 1), (3, 3)):
+        cfg = hj.SolveConfig(tolerance=1e-6, max_iters=25)
+        cfg.spatial_order, cfg.time_order = order, rk
+        ref = hj.solve(hj.ScalarField(g, init), hj.ScalarField(g, c), model, db, cfg, ctx=gpu_ctx)
+        it = torch.tensor(init, device="cuda")
+        ct = torch.tensor(c, device="cuda")
+        out = torch.empty_like(it)
+        torch.cuda.synchronize()
+        r = sharded.solve_sharded_local_dev(3, g, model, db, it.data_ptr(), ct.data_ptr(),
+                                            out.data_ptr(), cfg, gpu_ctx, history_capacity=25)
+        assert r.iterations == ref.iterations
+        assert same(r.residual_history, ref.residual_history)
+        assert same(out.cpu().numpy(), ref.value.values())
+
+
+def test_local_ranks_converge_in_reference_iteration_count(gpu_ctx):
+    """4 in-process ranks solve config 2 at 21^4 to tol 5e-3: the reference's
+    16 685 iterations and V* (golden fixture from oracle/_ref)."""
+    import json
+    from pathlib import Path
+    meta = json.loads((Path(__file__).resolve().parent / "golden" / "golden_fullsize.json")
+                      .read_text())["conv21"]
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=5e-3, max_iters=200000)
+    r, v = _local(gpu_ctx, w, c, cfg, 4, 0)
+    assert r.iterations == meta["iterations"] == 16685 and r.converged
+    import hashlib
+    assert hashlib.sha256(np.ascontiguousarray(v + 0.0).tobytes()).hexdigest() == meta["value_sha256"]
+
+
+def test_local_ranks_thin_slab_rejected(gpu_ctx):
+    """n0 = 11 over 4 ranks gives 3/3/3/2 planes: ENO3 needs 3 on EVERY rank,
+    so the solve fails up front (the NCCL path checks this before any
+    collective, so no rank can block in NCCL while another returns)."""
+    w = configs.config2(11)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(max_iters=5)
+    cfg.spatial_order, cfg.time_order = 3, 3
+    with pytest.raises(hj.Unsupported):
+        _local(gpu_ctx, w, c, cfg, 4, 5)
