@@ -139,6 +139,15 @@ typedef struct hjb_solve_config {
   double time_horizon;   /* > 0: also stop once iterations*dt >= horizon */
   int32_t threads;       /* reference CPU knob; accepted and ignored */
   int32_t flags;         /* HJB_FLAG_* (0 by default) */
+  /* Optional target set l(x) (B200 extension, no reference counterpart; the
+   * reference clamps against the avoid set only, solver.cpp:178-179): a field
+   * on the solve's grid, in the memory space of the call's other fields.
+   * Every update (every RK stage) becomes the reach-avoid
+   *   V' = max(c, min(l, stepped))      (std::min / std::max order)
+   * NULL (default) = the reference update V' = max(c, stepped).  Supported
+   * by hjb_solve / hjb_solve_dev / hjb_vi_step[_dev]; the sharded and
+   * multilevel drivers reject it. */
+  const double* target;
 } hjb_solve_config;
 
 /* run the ENO/TVD-RK stage machinery even for order 1 / Euler (verification:
@@ -265,6 +274,10 @@ int hjb_field_max_dev(hjb_context* ctx, int64_t n, const double* a, const double
                       double* out);
 int hjb_field_min_dev(hjb_context* ctx, int64_t n, const double* a, const double* b,
                       double* out);
+/* out = -a: the complement {x : -f(x) <= 0} of a level-set field (an
+ * obstacle band turned into an avoid set, config 5); no reference function
+ * (the reference composes sets by field_max / field_min only). */
+int hjb_field_negate_dev(hjb_context* ctx, int64_t n, const double* a, double* out);
 
 /* ------------------------------------------- multi-GPU slab partition */
 /* Axis-0 slab partition across ranks: one process per GPU,

@@ -358,8 +358,8 @@ int hjo_cfl_dt(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, do
 /* update_chunk, solver.cpp:106-190 */
 static double update_range(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
                            const double* inv, int godunov, const double* global_alpha,
-                           const double* v, const double* c, double* out, double dt, int64_t lo,
-                           int64_t hi) {
+                           const double* v, const double* c, const double* tg, double* out,
+                           double dt, int64_t lo, int64_t hi) {
   const int nd = g->nd;
   int64_t idx[HJB_MAX_DIMS];
   double x[HJB_MAX_STATE], dminus[HJB_MAX_STATE], dplus[HJB_MAX_STATE];
@@ -405,7 +405,10 @@ static double update_range(const grid_t* g, const hjb_model* m, const hjb_dbound
         for (int d = 0; d < nd; ++d) hhat += global_alpha[d] * 0.5 * (dplus[d] - dminus[d]);
       }
     }
-    const double stepped = v[lin] + dt * hhat;
+    double stepped = v[lin] + dt * hhat;
+    /* target set (B200 extension, no reference counterpart; parity
+     * unpinned): reach-avoid V' = max(c, min(l, V + dt*H)), std::min order */
+    if (tg) stepped = tg[lin] < stepped ? tg[lin] : stepped;
     const double vnew = stepped > c[lin] ? stepped : c[lin];
     out[lin] = vnew;
     const double dv = fabs(vnew - v[lin]);
@@ -416,8 +419,8 @@ static double update_range(const grid_t* g, const hjb_model* m, const hjb_dbound
 }
 
 static double sweep(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, const double* v,
-                    const double* c, double dt, int godunov, const double* global_alpha,
-                    double* out) {
+                    const double* c, const double* tg, double dt, int godunov,
+                    const double* global_alpha, double* out) {
   double inv[HJB_MAX_DIMS];
   for (int d = 0; d < g->nd; ++d) inv[d] = 1.0 / g->spacing[d];
   const int64_t nchunks = (g->size + CHUNK - 1) / CHUNK;
@@ -429,7 +432,7 @@ static double sweep(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, 
     for (int64_t ch = 0; ch < nchunks; ++ch) {
       const int64_t lo = ch * CHUNK;
       const int64_t hi = lo + CHUNK < g->size ? lo + CHUNK : g->size;
-      const double r = update_range(g, m, db, inv, godunov, global_alpha, v, c, out, dt, lo, hi);
+      const double r = update_range(g, m, db, inv, godunov, global_alpha, v, c, tg, out, dt, lo, hi);
       lbest = STD_MAX(lbest, r);
     }
 #pragma omp critical
@@ -444,7 +447,7 @@ int hjo_sweep(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, con
   grid_t g;
   int rc = check_ctx(gi, m, db, &g);
   if (rc) return rc;
-  *max_dv = sweep(&g, m, db, v, c, dt, scheme == HJB_GODUNOV, global_alpha, out);
+  *max_dv = sweep(&g, m, db, v, c, NULL, dt, scheme == HJB_GODUNOV, global_alpha, out);
   return 0;
 }
 
@@ -459,7 +462,7 @@ int hjo_sweep_planes(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* 
     return fail(HJB_ERR_INVALID_ARGUMENT, "sweep_planes: bad plane range");
   double inv[HJB_MAX_DIMS];
   for (int d = 0; d < g.nd; ++d) inv[d] = 1.0 / g.spacing[d];
-  *max_dv = update_range(&g, m, db, inv, scheme == HJB_GODUNOV, global_alpha, v, c, out, dt,
+  *max_dv = update_range(&g, m, db, inv, scheme == HJB_GODUNOV, global_alpha, v, c, NULL, out, dt,
                          pb * g.stride[0], pe * g.stride[0]);
   return 0;
 }
@@ -478,7 +481,7 @@ int hjo_vi_step(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, c
     return fail(HJB_ERR_INVALID_ARGUMENT,
                 "vi_step: model inputs are not row-separable, use the Lax-Friedrichs scheme");
   const double* ga = cfg->dissipation == HJB_GLOBAL ? s.max_alpha : NULL;
-  sweep(&g, m, db, v, c, dt, cfg->scheme == HJB_GODUNOV, ga, out);
+  sweep(&g, m, db, v, c, cfg->target, dt, cfg->scheme == HJB_GODUNOV, ga, out);
   return 0;
 }
 
@@ -526,7 +529,7 @@ int hjo_solve(const hjb_grid* gi, const hjb_model* m, const hjb_dbounds* db, con
   double min_residual = INFINITY, first = 0.0, residual = 0.0;
   int status = 0;
   for (int64_t iter = 1; iter <= cfg->max_iters; ++iter) {
-    const double max_dv = sweep(&g, m, db, front, c, dt, godunov, ga, back);
+    const double max_dv = sweep(&g, m, db, front, c, cfg->target, dt, godunov, ga, back);
     residual = max_dv / dt;
     double* t = front;
     front = back;
@@ -1112,7 +1115,8 @@ static inline void eno_pair(const double* v, int64_t lin, int64_t stride, int64_
 static double ho_stage_range(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
                              const double* inv, int godunov, const double* global_alpha,
                              int order, const double* vs, const double* vn, const double* c,
-                             double dt, int kind, double* out, int64_t begin, int64_t end) {
+                             const double* tg, double dt, int kind, double* out, int64_t begin,
+                             int64_t end) {
   const int nd = g->nd;
   const int64_t nchunks = (end - begin + CHUNK - 1) / CHUNK;
   double best = 0.0;
@@ -1159,6 +1163,7 @@ static double ho_stage_range(const grid_t* g, const hjb_model* m, const hjb_dbou
           case 3: val = kThird * vn[lin] + kTwoThirds * st; break;
           default: val = st; break;
         }
+        if (tg) val = tg[lin] < val ? tg[lin] : val; /* target: min(l, .) first */
         const double cl = val > c[lin] ? val : c[lin];
         out[lin] = cl;
         const double dv = fabs(cl - vn[lin]);
@@ -1174,10 +1179,10 @@ static double ho_stage_range(const grid_t* g, const hjb_model* m, const hjb_dbou
 
 static double ho_stage(const grid_t* g, const hjb_model* m, const hjb_dbounds* db,
                        const double* inv, int godunov, const double* global_alpha, int order,
-                       const double* vs, const double* vn, const double* c, double dt, int kind,
-                       double* out) {
-  return ho_stage_range(g, m, db, inv, godunov, global_alpha, order, vs, vn, c, dt, kind, out, 0,
-                        g->size);
+                       const double* vs, const double* vn, const double* c, const double* tg,
+                       double dt, int kind, double* out) {
+  return ho_stage_range(g, m, db, inv, godunov, global_alpha, order, vs, vn, c, tg, dt, kind, out,
+                        0, g->size);
 }
 
 /* one ENO/TVD-RK stage restricted to axis-0 planes [pb, pe) of the full grid
@@ -1193,7 +1198,7 @@ int hjo_ho_stage_planes(const hjb_grid* gi, const hjb_model* m, const hjb_dbound
     return fail(HJB_ERR_INVALID_ARGUMENT, "ho_stage_planes: bad plane range");
   double inv[HJB_MAX_DIMS];
   for (int d = 0; d < g.nd; ++d) inv[d] = 1.0 / g.spacing[d];
-  *max_dv = ho_stage_range(&g, m, db, inv, 1, NULL, order, vs, vn, c, dt, kind, out,
+  *max_dv = ho_stage_range(&g, m, db, inv, 1, NULL, order, vs, vn, c, NULL, dt, kind, out,
                            pb * g.stride[0], pe * g.stride[0]);
   return 0;
 }
@@ -1220,14 +1225,14 @@ int hjo_ho_solve(const grid_t* g, const hjb_model* m, const hjb_dbounds* db, con
   for (int64_t iter = 1; iter <= cfg->max_iters; ++iter) {
     double max_dv;
     if (rk == 1) {
-      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, dt, 0, back);
+      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, cfg->target, dt, 0, back);
     } else if (rk == 2) {
-      ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, dt, 0, s1);
-      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, s1, front, c, dt, 1, back);
+      ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, cfg->target, dt, 0, s1);
+      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, s1, front, c, cfg->target, dt, 1, back);
     } else {
-      ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, dt, 0, s1);
-      ho_stage(g, m, db, inv, godunov, ga, order, s1, front, c, dt, 2, s2);
-      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, s2, front, c, dt, 3, back);
+      ho_stage(g, m, db, inv, godunov, ga, order, front, front, c, cfg->target, dt, 0, s1);
+      ho_stage(g, m, db, inv, godunov, ga, order, s1, front, c, cfg->target, dt, 2, s2);
+      max_dv = ho_stage(g, m, db, inv, godunov, ga, order, s2, front, c, cfg->target, dt, 3, back);
     }
     residual = max_dv / dt;
     double* t = front;

@@ -151,23 +151,31 @@ class Restatement:
                                                _arr(out), C.byref(mx)))
         return mx.value
 
-    def vi_step(self, v, c, model, db, dt, cfg=None):
+    def vi_step(self, v, c, model, db, dt, cfg=None, target=None):
         cfg = cfg or hj.SolveConfig()
         grid = v.grid()
         vv, cc = _vals(v), _vals(c)
         out = np.empty_like(vv)
         g, m, d, k = grid.to_c(), model.to_c(), db.to_c(), cfg.to_c()
+        tv = _vals(target) if target is not None else None
+        if tv is not None:
+            k.target = tv.ctypes.data_as(C.c_void_p)
         self._chk(self.lib.hjo_vi_step(C.byref(g), C.byref(m), C.byref(d), _arr(vv), _arr(cc), dt,
                                        C.byref(k), _arr(out)))
         return out
 
-    def solve(self, init, c, model, db, cfg, history_capacity=None):
+    def solve(self, init, c, model, db, cfg, history_capacity=None, target=None):
+        """hjo_solve; ``target`` (extension, parity unpinned): the reach-avoid
+        update max(c, min(l, stepped)) of every sweep / RK stage."""
         grid = init.grid()
         cap = int(cfg.max_iters if history_capacity is None else history_capacity)
         r, rh, wh = hj._c_result(cap)
         iv, cv = _vals(init), _vals(c)
         out = np.empty_like(iv)
         g, m, d, k = grid.to_c(), model.to_c(), db.to_c(), cfg.to_c()
+        tv = _vals(target) if target is not None else None
+        if tv is not None:
+            k.target = tv.ctypes.data_as(C.c_void_p)
         self._chk(self.lib.hjo_solve(C.byref(g), C.byref(m), C.byref(d), _arr(iv), _arr(cv),
                                      C.byref(k), _arr(out), C.byref(r)))
         return hj._to_result(grid, out, r, rh, wh)
@@ -391,6 +399,8 @@ class Reference:
         L.hjr_resample.argtypes = [P(abi.HjbGrid), _vp, P(abi.HjbGrid), _vp] + E
         L.hjr_max_adjacent_jump.argtypes = [P(abi.HjbGrid), _vp, P(_d)] + E
         L.hjr_signed_distance_band.argtypes = [P(abi.HjbGrid), C.c_int32, _d, _d, _vp] + E
+        L.hjr_field_max.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp] + E
+        L.hjr_field_min.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp] + E
         L.hjr_signed_distance_box.argtypes = [P(abi.HjbGrid), _vp, _vp, _vp] + E
         L.hjr_hamiltonian.argtypes = [P(ModelSpec), _vp, _vp, P(abi.HjbInterval), P(_d)] + E
         L.hjr_flow_bounds.argtypes = [P(ModelSpec), _vp, P(abi.HjbInterval), _vp] + E
@@ -530,6 +540,20 @@ class Reference:
         out = np.empty(grid.size())
         g = grid.to_c()
         self._call(self.lib.hjr_signed_distance_band, C.byref(g), dim, lo, hi, _arr(out))
+        return out
+
+    def field_max(self, a, b):
+        """levelset.cpp:80-82 (std::max per node)."""
+        out = np.empty(a.grid().size())
+        g = a.grid().to_c()
+        self._call(self.lib.hjr_field_max, C.byref(g), _arr(_vals(a)), _arr(_vals(b)), _arr(out))
+        return out
+
+    def field_min(self, a, b):
+        """levelset.cpp:84-86 (std::min per node)."""
+        out = np.empty(a.grid().size())
+        g = a.grid().to_c()
+        self._call(self.lib.hjr_field_min, C.byref(g), _arr(_vals(a)), _arr(_vals(b)), _arr(out))
         return out
 
     def signed_distance_box(self, grid, lo, hi):

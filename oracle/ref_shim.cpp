@@ -162,6 +162,8 @@ IntervalField make_db(const Grid& g, const hjb_dbounds* db) {
 }
 
 SolveConfig make_cfg(const hjb_solve_config* c) {
+  if (c->target)  // the reference clamps against the avoid set only
+    throw std::invalid_argument("ref_shim: the reference has no target set");
   SolveConfig cfg;
   cfg.cfl_factor = c->cfl_factor;
   cfg.tolerance = c->tolerance;
@@ -309,6 +311,24 @@ int hjr_max_adjacent_jump(const hjb_grid* g, const double* v, double* out, char*
   return guarded(err, errlen, [&] {
     Grid grid = make_grid(g);
     *out = max_adjacent_jump(make_field(grid, v));
+  });
+}
+
+int hjr_field_max(const hjb_grid* g, const double* a, const double* b, double* out, char* err,
+                  int errlen) {
+  return guarded(err, errlen, [&] {
+    Grid grid = make_grid(g);
+    ScalarField r = field_max(make_field(grid, a), make_field(grid, b));
+    std::memcpy(out, r.values().data(), grid.size() * sizeof(double));
+  });
+}
+
+int hjr_field_min(const hjb_grid* g, const double* a, const double* b, double* out, char* err,
+                  int errlen) {
+  return guarded(err, errlen, [&] {
+    Grid grid = make_grid(g);
+    ScalarField r = field_min(make_field(grid, a), make_field(grid, b));
+    std::memcpy(out, r.values().data(), grid.size() * sizeof(double));
   });
 }
 

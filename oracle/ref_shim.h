@@ -85,6 +85,11 @@ int hjr_resample(const hjb_grid* src_g, const double* src, const hjb_grid* dst_g
                  char* err, int errlen);
 int hjr_max_adjacent_jump(const hjb_grid* g, const double* v, double* out, char* err,
                           int errlen);
+/* levelset.cpp:80-86 (the reference's own field_max / field_min) */
+int hjr_field_max(const hjb_grid* g, const double* a, const double* b, double* out, char* err,
+                  int errlen);
+int hjr_field_min(const hjb_grid* g, const double* a, const double* b, double* out, char* err,
+                  int errlen);
 int hjr_signed_distance_band(const hjb_grid* g, int32_t dim, double lo, double hi, double* out,
                              char* err, int errlen);
 int hjr_signed_distance_box(const hjb_grid* g, const double* lo, const double* hi, double* out,

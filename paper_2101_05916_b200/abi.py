@@ -73,7 +73,7 @@ class HjbSolveConfig(C.Structure):
                 ("max_iters", C.c_int64), ("scheme", C.c_int32),
                 ("dissipation", C.c_int32), ("spatial_order", C.c_int32),
                 ("time_order", C.c_int32), ("time_horizon", C.c_double),
-                ("threads", C.c_int32), ("flags", C.c_int32)]
+                ("threads", C.c_int32), ("flags", C.c_int32), ("target", C.c_void_p)]
 
 
 class HjbSolveResult(C.Structure):
@@ -160,6 +160,7 @@ SIGNATURES = [
     ("hjb_signed_distance_band_dev", _i, [_vp, P(HjbGrid), _i32, _d, _d, _vp]),
     ("hjb_field_max_dev", _i, [_vp, _i64, _vp, _vp, _vp]),
     ("hjb_field_min_dev", _i, [_vp, _i64, _vp, _vp, _vp]),
+    ("hjb_field_negate_dev", _i, [_vp, _i64, _vp, _vp]),
     ("hjb_slab_partition", _i, [_i64, _i32, _i32, P(_i64), P(_i64)]),
     ("hjb_nccl_unique_id", _i, [_vp]),
     ("hjb_comm_create", _i, [_vp, _i32, _i32, _vp, P(_vp)]),

@@ -98,6 +98,20 @@ class Workload:
         w = self.wind if wind is None else wind
         return hj.IntervalField.constant(self.grid, [hj.Interval(-w, w)])
 
+    def constraint_dev(self, out_ptr: int, scratch_ptr: int, ctx=None) -> None:
+        """c on the device: signed_distance_band per listed band (obstacles
+        negated: their complement), combined with field_max — the reference's
+        set algebra (levelset.cpp:54-66, 80-82) as device kernels.  out /
+        scratch: device buffers of grid size (float64)."""
+        n = self.grid.size()
+        for k, (dim, lo, hi, sign) in enumerate(self.bands):
+            dst = out_ptr if k == 0 else scratch_ptr
+            hj.signed_distance_band_dev(self.grid, dim, lo, hi, dst, ctx=ctx)
+            if sign < 0:
+                hj.field_negate_dev(n, dst, dst, ctx=ctx)
+            if k > 0:
+                hj.field_max_dev(n, out_ptr, scratch_ptr, out_ptr, ctx=ctx)
+
     def constraint(self, band: Callable, fmax: Callable):
         """c = max over the listed signed-distance bands (obstacles negated).
 

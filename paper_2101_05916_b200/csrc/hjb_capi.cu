@@ -477,7 +477,7 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
     configure(2, 448);
     return HJB_OK;
   }
-  if (f.pv) {  // one plane-varying-bounds variant
+  if (f.pv || f.target) {  // one plane-varying-bounds / target-set variant
     configure(2, 576);
     return HJB_OK;
   }
@@ -767,11 +767,15 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   CUDA_TRY(ctx->v1.ensure(bytes));
   CUDA_TRY(cudaMemcpyAsync(ctx->v0.p, init, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   int shape = fast_enabled() ? fast4d_shape(g, hm.dm, scheme_of(cfg)) : -1;
+  // target set: the 4D fast path's TG variant (Godunov, constant bounds);
+  // everything else runs the generic sweep
+  if (cfg->target && scheme_of(cfg) != kGodunov) shape = -1;
   const int shape_pv = (shape < 0 && fast_enabled() && db->per_node &&
-                        scheme_of(cfg) == kGodunov)
+                        scheme_of(cfg) == kGodunov && !cfg->target)
                            ? fast4d_shape_pv(g, hm.dm)
                            : -1;
   StepArgs a = base_args(g, hm.dm, c, dt, scheme_of(cfg), s);
+  a.target = cfg->target;
   a.st = ctx->st;
   a.buf0 = ctx->v0.d();
   a.buf1 = ctx->v1.d();
@@ -803,11 +807,18 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     f.st = ctx->st;
     f.dt = dt;
     fill_lf(hm.dm, scheme_of(cfg), s.max_alpha, f);
+    f.target = cfg->target;  // (non-null: one kernel variant, no autotuning)
     if ((rc = fast4d_choose(ctx, g, shape, init, c, f))) return rc;
     rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
     CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
     ++ctx->launches;
-    if (!f.lf && !f.pv && (rc = constraint_planes(ctx, g, c, &f.cplane))) return rc;
+    if (f.target) {  // padded like V: the kernel reads l per pencil and plane
+      CUDA_TRY(ctx->tgbuf.ensure(rows * f.n3p * sizeof(double)));
+      CUDA_TRY(launch_pad4(cfg->target, ctx->tgbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
+      ++ctx->launches;
+      f.target = ctx->tgbuf.d();
+    }
+    if (!f.lf && !f.pv && !f.target && (rc = constraint_planes(ctx, g, c, &f.cplane))) return rc;
     if (!f.cplane) {
       CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
       ++ctx->launches;
@@ -853,7 +864,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   // small 2D grids: the whole loop in one cluster launch (V in DSMEM)
   const char* s2d = std::getenv("HJB_SMALL2D");
   const bool small2d = shape < 0 && g.nd == 2 && !(s2d && std::strcmp(s2d, "0") == 0) &&
-                       small2d_smem(g, nullptr, nullptr) <= 200 * 1024;
+                       !cfg->target && small2d_smem(g, nullptr, nullptr) <= 200 * 1024;
   if (small2d) {
     StepArgs x = a;
     x.src = ctx->v0.d();
@@ -1077,6 +1088,7 @@ int hjb_vi_step_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   if (cfg->spatial_order > 1 || cfg->time_order > 1 || (cfg->flags & HJB_FLAG_FORCE_HO))
     return ho_vi_step(ctx, g, hm.dm, value, constraint, cfg, dt, s.max_alpha, out);
   StepArgs a = base_args(g, hm.dm, constraint, dt, scheme_of(cfg), s);
+  a.target = cfg->target;
   a.st = ctx->st;
   a.loop = 0;
   a.src = value;
@@ -1111,6 +1123,14 @@ int hjb_vi_step(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const
   CUDA_TRY(cudaMemcpyAsync(sb.c.p, constraint, bytes, cudaMemcpyHostToDevice, ctx->stream));
   hjb_dbounds dbs;
   if ((rc = stage_dbounds(ctx, db, g.size, sb.db, dbs))) return rc;
+  hjb_solve_config cfgd;
+  if (cfg && cfg->target) {  // host target field -> device
+    cfgd = *cfg;
+    CUDA_TRY(ctx->tgx.ensure(bytes));
+    CUDA_TRY(cudaMemcpyAsync(ctx->tgx.p, cfg->target, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    cfgd.target = ctx->tgx.d();
+    cfg = &cfgd;
+  }
   if ((rc = hjb_vi_step_dev(ctx, gi, mi, &dbs, sb.init.d(), sb.c.d(), dt, cfg, sb.out.d())))
     return rc;
   CUDA_TRY(cudaMemcpyAsync(out, sb.out.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1141,6 +1161,14 @@ int hjb_solve(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const h
   CUDA_TRY(cudaMemcpyAsync(ctx->cbuf.p, constraint, bytes, cudaMemcpyHostToDevice, ctx->stream));
   hjb_dbounds dbs;
   if ((rc = stage_dbounds(ctx, db, g.size, ctx->dbbuf, dbs))) return rc;
+  hjb_solve_config cfgd;
+  if (cfg->target) {  // host target field -> device
+    cfgd = *cfg;
+    CUDA_TRY(ctx->tgx.ensure(bytes));
+    CUDA_TRY(cudaMemcpyAsync(ctx->tgx.p, cfg->target, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    cfgd.target = ctx->tgx.d();
+    cfg = &cfgd;
+  }
   rc = solve_impl(ctx, gi, mi, &dbs, ctx->xbuf.d(), ctx->cbuf.d(), cfg, ctx->xbuf.d(), res);
   if (rc && rc != HJB_ERR_DIVERGED) return rc;
   const int status = rc;
@@ -1217,6 +1245,15 @@ int hjb_field_max_dev(hjb_context* ctx, int64_t n, const double* a, const double
   int rc;
   if ((rc = check_ctx(ctx))) return rc;
   CUDA_TRY(launch_field_op(n, a, b, out, 1, ctx->stream));
+  ++ctx->launches;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HJB_OK;
+}
+
+int hjb_field_negate_dev(hjb_context* ctx, int64_t n, const double* a, double* out) {
+  int rc;
+  if ((rc = check_ctx(ctx))) return rc;
+  CUDA_TRY(launch_field_op(n, a, a, out, 2, ctx->stream));
   ++ctx->launches;
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return HJB_OK;
@@ -1303,6 +1340,8 @@ static int multilevel_impl(hjb_context* ctx, int nl, const hjb_grid* grids, cons
   if (nl < 1 || nl > HJB_MAX_LEVELS)
     return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_multilevel: 1..8 levels");
   if ((rc = validate_cfg(cfg))) return rc;
+  if (cfg->target)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_multilevel: no target set (use solve)");
   DevGrid g[HJB_MAX_LEVELS];
   for (int l = 0; l < nl; ++l)
     if ((rc = make_grid(&grids[l], g[l]))) return rc;

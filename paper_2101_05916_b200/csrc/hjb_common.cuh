@@ -59,6 +59,8 @@ struct hjb_context {
   hjb::DevBuf pvtab;          // 4D fast path with axis-0-varying bounds: tables
   hjb::DevBuf pnbuf;          // 4D fast path with per-node bounds: padded lo / hi
   hjb::DevBuf cplane;         // constraint varying along axis 0 only: c per plane
+  hjb::DevBuf tgbuf;          // target set: padded copy for the 4D fast path
+  hjb::DevBuf tgx;            // target set: device copy of a host field
   hjb::LoopState* st = nullptr;
   hjb::LoopState* st_host = nullptr;  // pinned mirror
   long long launches = 0;

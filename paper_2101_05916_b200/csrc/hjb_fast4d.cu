@@ -440,7 +440,7 @@ __device__ __forceinline__ void lds_pn(const double* p, double* v) {
   }
 }
 
-template <class S, int kK, int MAXT, int SCH, int PV = 0, bool CP = false>
+template <class S, int kK, int MAXT, int SCH, int PV = 0, bool CP = false, bool TG = false>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -708,6 +708,12 @@ __global__ void __launch_bounds__(MAXT, 1)
 
       double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
                    static_cast<uint64_t>(c0) * s0;
+      // target set (TG): the pencil's l of each plane, loaded with __ldg
+      const double* tgp =
+          TG ? a.target + (active ? static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3
+                                  : 0ull) +
+                   static_cast<uint64_t>(c0) * s0
+             : nullptr;
       // prologue: V plane c0-1 (first slot of the item when c0 > 0) and c0
       double v[kK], vp[kK];
       if (c0 > 0) {
@@ -799,7 +805,11 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
           for (int c = 0; c < kK; ++c) vn[c] = v[c];  // D+ at the i0 = n0-1 edge: +0
         }
-        double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK];
+        double cc[kK], n1m[kK], n1p[kK], n2m[kK], n2p[kK], tl[kK];
+        if (TG) {
+          lds_pn<kK>(tgp, tl);
+          tgp += s0;
+        }
         if (CP) {  // constraint per plane (Fast4dArgs::cplane)
           const double cp = __ldg(a.cplane + i0);
 #pragma unroll
@@ -884,7 +894,8 @@ __global__ void __launch_bounds__(MAXT, 1)
               alc[d] = lfal[d][c];
             }
             const double hh = lf_hhat<S>(a.lp, dmv, dpv, drc, alc);
-            const double st = v[c] + a.dt * hh;
+            double st = v[c] + a.dt * hh;
+            if (TG) st = tl[c] < st ? tl[c] : st;
             out[c] = st > cc[c] ? st : cc[c];
             const double dv = fabs(out[c] - v[c]);
             if (valid[c] && dv > mdv) mdv = dv;
@@ -933,7 +944,9 @@ __global__ void __launch_bounds__(MAXT, 1)
           }
           // hhat = 0.0 + h0 + h1 + h2 + h3 (0.0 + h0 == h0 in value)
           const double hh = ((h0 + h1) + h2) + h3;
-          const double st = v[c] + a.dt * hh;
+          double st = v[c] + a.dt * hh;
+          // target set: std::min(stepped, l) before the reference clamp
+          if (TG) st = tl[c] < st ? tl[c] : st;
           out[c] = st > cc[c] ? st : cc[c];
           // max |dV| as the reference keeps it: `if (dv > max_dv)`
           // (solver.cpp:181-182), so a NaN never wins
@@ -2556,12 +2569,12 @@ static bool smem_attr_once(std::atomic<unsigned long long>& done, K kernel) {
   return true;
 }
 
-template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false>
+template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false, bool TG = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP>)) return;
+  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP, TG>)) return;
   if (a.l2_bytes == 0 && !a.pdl) {
-    k_fast4d<S, K, MAXT, SCH, PV, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
+    k_fast4d<S, K, MAXT, SCH, PV, CP, TG><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -2587,13 +2600,17 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP>, a);
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
 // the autotuner pick among them per grid
 template <class S>
 static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.target) {  // target set: Godunov, constant bounds, field constraint
+    launch_one<S, 2, 576, 0, 0, false, true>(a, s);
+    return;
+  }
   if (a.pv == 1) {  // plane-varying disturbance bounds: one configuration
     launch_one<S, 2, 576, 0, 1>(a, s);
     return;

@@ -43,6 +43,8 @@ struct Fast4dArgs {
   uint32_t split, c2beg, c2end;
   // max|dV| accumulator of the launch (null: st->maxdv_bits)
   unsigned long long* mdv;
+  // padded target set l (TG variant): out = max(c, min(l, stepped))
+  const double* target;
   const double* tab;    // slope tables (staged into shared memory per CTA)
   uint32_t tab_len;     // doubles in tab
   uint32_t tab_off;     // shared-memory byte offset of the staged copy

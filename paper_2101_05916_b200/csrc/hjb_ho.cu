@@ -38,6 +38,7 @@ StepArgs ho_args(const DevGrid& g, const DevModel& m, const double* c, double dt
   a.scheme = scheme_id(cfg);
   for (int d = 0; d < kMaxDims; ++d) a.galpha[d] = galpha[d];
   a.order = cfg->spatial_order < 1 ? 1 : cfg->spatial_order;
+  a.target = cfg->target;  // reach-avoid: every stage min(l, .) then the clamp
   return a;
 }
 
@@ -72,6 +73,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   // 4D fast-path models (Godunov, constant bounds): padded layout + k_ho4d
   const char* fe = std::getenv("HJB_FAST");
   int shape = (fe && std::strcmp(fe, "0") == 0) ? -1 : fast4d_shape(g, m, scheme_id(cfg));
+  if (cfg->target) shape = -1;  // target sets run the generic stage kernel
   if (shape >= 0 && scheme_id(cfg) != kGodunov) {
     // Lax-Friedrichs runs only in the TMA-staged kernel (k_ho4t)
     Ho4dArgs t;
@@ -184,7 +186,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   // small 2D grids: every stage of the whole loop in one cluster launch
   const char* s2d = std::getenv("HJB_SMALL2D");
   const bool small2d = shape < 0 && g.nd == 2 && !(s2d && std::strcmp(s2d, "0") == 0) &&
-                       small2d_ho_smem(g, nullptr, nullptr) <= 200 * 1024;
+                       !cfg->target && small2d_ho_smem(g, nullptr, nullptr) <= 200 * 1024;
   int rc = HJB_OK;
   if (small2d) {
     StepArgs x = a;

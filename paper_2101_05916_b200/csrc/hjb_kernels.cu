@@ -295,7 +295,11 @@ __global__ void __launch_bounds__(kThreads) k_step(const __grid_constant__ StepA
         for (int d = 0; d < ND; ++d) hhat += a.galpha[d] * 0.5 * (dp[d] - dm[d]);
       }
     }
-    const double stepped = v + a.dt * hhat;
+    double stepped = v + a.dt * hhat;
+    if (a.target) {  // std::min(stepped, l), then the reference clamp
+      const double l = a.target[lin];
+      stepped = l < stepped ? l : stepped;
+    }
     const double cc = a.c[lin];
     const double vnew = stepped > cc ? stepped : cc;
     dst[lin] = vnew;
@@ -424,6 +428,10 @@ __global__ void __launch_bounds__(kThreads) k_ho_stage(const __grid_constant__ S
       case 2: val = 0.75 * vn[lin] + 0.25 * st; break;
       case 3: val = kThird * vn[lin] + kTwoThirds * st; break;
       default: val = st; break;
+    }
+    if (a.target) {  // every RK stage: min against the target, then the clamp
+      const double l = a.target[lin];
+      val = l < val ? l : val;
     }
     const double cc = a.c[lin];
     const double cl = val > cc ? val : cc;
@@ -575,7 +583,13 @@ __global__ void k_field_op(long long n, const double* __restrict__ a,
                            const double* __restrict__ b, double* __restrict__ out, int is_max) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const double x = a[i], y = b[i];
+    const double x = a[i];
+    if (is_max == 2) {  // complement in level-set form: -f (exact)
+      out[i] = -x;
+      continue;
+    }
+    const double y = b[i];
+    // std::max(x, y) / std::min(x, y) (levelset.cpp:80-86): ties keep x
     out[i] = is_max ? (x < y ? y : x) : (y < x ? y : x);
   }
 }

@@ -14,6 +14,9 @@ struct StepArgs {
   DevGrid g;
   DevModel m;
   const double* c;   // constraint
+  // target set l (reach-avoid extension, no reference counterpart): the
+  // update is max(c, min(l, stepped)); null = the reference update
+  const double* target;
   double* buf0;      // loop mode: front/back double buffer, parity = st->iter
   double* buf1;
   const double* src; // single-step mode

@@ -176,6 +176,46 @@ int run_sharded_loop(hjb_context* ctx, int body,
   return rc;
 }
 
+// Host-driven loop for the NCCL transport: the positions are issued eagerly
+// (no graph capture: NCCL's own stream dependencies stay the eager ones it is
+// built for — a captured all-reduce inside the conditional graph, with the
+// sweep kernels on a second captured stream, hung on the B200 pool).  Batch j
+// (= `body` positions) is followed by an async copy of the loop state's done
+// flag; the host waits for batch j - 1's flag only after issuing batch j, so
+// the GPU never idles on the host, and every rank stops after the same batch
+// (done is identical on all ranks at the same iteration), issuing the same
+// NCCL calls.  The extra batch finds done set: its kernels and epilogues
+// return at once.
+int run_eager_loop(hjb_context* ctx, int body,
+                   const std::function<int(int, cudaGraphConditionalHandle, int)>& iter) {
+  int* flags = nullptr;  // pinned: done flag after batch j in flags[j & 1]
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int rc = HJB_OK;
+  cudaError_t e = cudaMallocHost(&flags, 2 * sizeof(int));
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e));
+  for (long long j = 0; rc == HJB_OK; ++j) {
+    for (int k = 0; k < body && rc == HJB_OK; ++k) rc = iter(k, 0, 0);
+    if (rc) break;
+    e = cudaMemcpyAsync(flags + (j & 1), &ctx->st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                        ctx->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[j & 1], ctx->stream);
+    if (e == cudaSuccess && j >= 1) e = cudaEventSynchronize(ev[(j - 1) & 1]);
+    if (e != cudaSuccess) {
+      rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    if (j >= 1 && flags[(j - 1) & 1]) break;
+  }
+  e = cudaStreamSynchronize(ctx->stream);
+  if (rc == HJB_OK && e != cudaSuccess) rc = set_err(HJB_ERR_CUDA, cudaGetErrorString(e));
+  for (cudaEvent_t x : ev)
+    if (x) cudaEventDestroy(x);
+  if (flags) cudaFreeHost(flags);
+  return rc;
+}
+
 // stage table of a TVD-RK step: (input, output, kind); buffers 0 = V_n
 // (parity), 1 = stage1, 2 = stage2
 struct HoStage {
@@ -301,11 +341,12 @@ struct SlabRank {
   // V after `iters` completed iterations
   double* value(long long iters) const { return (iters & 1) ? buf[1] : buf[0]; }
   // slot: the max|dV| accumulator of position k (null: st->maxdv_bits)
-  cudaError_t launch(int k, int q, bool boundary, unsigned long long* slot) const;
-  cudaStream_t s = nullptr;
+  cudaError_t launch(int k, int q, bool boundary, unsigned long long* slot,
+                     cudaStream_t s) const;
 };
 
-cudaError_t SlabRank::launch(int k, int q, bool boundary, unsigned long long* slot) const {
+cudaError_t SlabRank::launch(int k, int q, bool boundary, unsigned long long* slot,
+                             cudaStream_t s) const {
   if (!ho) {
     Fast4dArgs x = boundary ? fb : fi;
     x.src = (k & 1) ? buf[1] : buf[0];
@@ -338,7 +379,6 @@ int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, doubl
   rk.sp = plane_split(geo);
   rk.shape = p.shape;
   rk.st = st;
-  rk.s = s;
   rk.ho = cfg->spatial_order > 1 || cfg->time_order > 1;
   DevGrid gloc = p.g;
   gloc.n[0] = geo.nloc;
@@ -533,34 +573,96 @@ bool shard_pipeline() {
   return !(e && std::strcmp(e, "0") == 0);
 }
 
-// The comm stream and the events of the sharded loop.  Pipelined residual:
-// position k's sweep accumulates max|dV| into st->maxdv_slot[k & 1]; after
-// its interior (ev_int) the comm stream all-reduces that slot and runs the
-// epilogue (ev_epi[k & 1]) while the main stream already sweeps position
-// k + 1.  Position k reads V_k and writes V_{k+1} over V_{k-1}; if epilogue
-// k - 2 stopped the loop, V_{k-1} is the result, so position k first waits
-// ev_epi[k & 1] (epilogue k - 2).  The one speculative sweep that can run
-// after the stopping sweep overwrites only the previous iterate, and its
-// epilogue returns early (done); the loop state's iteration count, history
-// and status are the unpipelined ones.
-struct StreamPair {
-  cudaStream_t comm = nullptr;
-  cudaEvent_t ev_bnd = nullptr, ev_xfer = nullptr, ev_int = nullptr, e0 = nullptr, e1 = nullptr;
-  cudaEvent_t ev_epi[2] = {nullptr, nullptr};
-  ~StreamPair() {
-    for (cudaEvent_t e : {ev_bnd, ev_xfer, ev_int, e0, e1, ev_epi[0], ev_epi[1]})
+// Streams and events of the sharded loop.  The sweep KERNELS run on a work
+// stream W; halo transfers, the residual reduction (NCCL all-reduce or the
+// in-process kernel) and the epilogue run on the capture's origin stream S,
+// so every NCCL call stays on the stream the caller captures (a 1-rank
+// all-reduce issued from a joined side stream hung inside the conditional
+// graph on the B200 pool).
+//
+// Per position k and RK stage q:  W: boundary planes -> S: send/recv of the
+// stage output's boundary planes || W: interior planes; the next stage waits
+// for the transfer.  After the last stage S reduces max|dV| and runs the
+// epilogue.  Pipelined residual (default): position k accumulates into
+// st->maxdv_slot[k & 1] and W starts position k + 1 as soon as its halo is
+// in, while S still reduces position k.  Position k reads V_k and writes
+// V_{k+1} over V_{k-1}; if epilogue k - 2 stopped the loop V_{k-1} is the
+// result, so W waits for epilogue k - 2 first.  The one speculative sweep
+// after the stopping one overwrites only the previous iterate, and its
+// epilogue returns early (done), so iteration count, history and status are
+// the unpipelined ones.
+struct LoopStreams {
+  cudaStream_t work = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_bnd = nullptr, ev_xs = nullptr, ev_int = nullptr;
+  cudaEvent_t ev_xl[2] = {nullptr, nullptr}, ev_epi[2] = {nullptr, nullptr};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ~LoopStreams() {
+    for (cudaEvent_t e : {ev_fork, ev_bnd, ev_xs, ev_int, ev_xl[0], ev_xl[1], ev_epi[0],
+                          ev_epi[1], e0, e1})
       if (e) cudaEventDestroy(e);
-    if (comm) cudaStreamDestroy(comm);
+    if (work) cudaStreamDestroy(work);
   }
   cudaError_t init() {
-    cudaError_t e = cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking);
-    for (cudaEvent_t* ev : {&ev_bnd, &ev_xfer, &ev_int, &ev_epi[0], &ev_epi[1]})
+    cudaError_t e = cudaStreamCreateWithFlags(&work, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&ev_fork, &ev_bnd, &ev_xs, &ev_int, &ev_xl[0], &ev_xl[1], &ev_epi[0],
+                            &ev_epi[1]})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreate(&e0);
     if (e == cudaSuccess) e = cudaEventCreate(&e1);
     return e;
   }
 };
+
+// What one loop position does, per transport (NCCL ranks / in-process ranks)
+struct PositionOps {
+  int ns = 1;                  // RK stages
+  bool bnd = false, inner = true, xfer = false;
+  // sweep kernels of stage q on stream s (accumulator of position k: slot)
+  std::function<int(int k, int q, bool boundary, bool pipe, cudaStream_t s)> sweep;
+  // halo transfer of stage q's output, on s
+  std::function<int(int k, int q, cudaStream_t s)> exchange;
+  // residual reduction + epilogue of position k, on s
+  std::function<int(int k, bool pipe, cudaGraphConditionalHandle h, int use, cudaStream_t s)>
+      finish;
+};
+
+int run_position(LoopStreams& ls, cudaStream_t S, const PositionOps& op, int k, bool overlap,
+                 bool pipe, cudaGraphConditionalHandle h, int use) {
+  int e;
+  if (!overlap) {  // serial: every kernel, then the transfer, on S; no pipelining
+    for (int q = 0; q < op.ns; ++q) {
+      if (op.bnd && (e = op.sweep(k, q, true, false, S))) return e;
+      if (op.inner && (e = op.sweep(k, q, false, false, S))) return e;
+      if (op.xfer && (e = op.exchange(k, q, S))) return e;
+    }
+    return op.finish(k, false, h, use, S);
+  }
+  cudaStream_t W = ls.work;
+  if (k == 0) {  // W joins the capture (position 0 follows everything before)
+    CUDA_TRY(cudaEventRecord(ls.ev_fork, S));
+    CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_fork, 0));
+  } else {
+    if (op.xfer) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_xl[(k - 1) & 1], 0));  // halo of V_k
+    if (!pipe) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_epi[(k - 1) & 1], 0));
+    else if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_epi[k & 1], 0));
+  }
+  for (int q = 0; q < op.ns; ++q) {
+    if (op.bnd && (e = op.sweep(k, q, true, pipe, W))) return e;
+    if (op.xfer) {
+      CUDA_TRY(cudaEventRecord(ls.ev_bnd, W));
+      CUDA_TRY(cudaStreamWaitEvent(S, ls.ev_bnd, 0));
+      if ((e = op.exchange(k, q, S))) return e;
+      CUDA_TRY(cudaEventRecord(q == op.ns - 1 ? ls.ev_xl[k & 1] : ls.ev_xs, S));
+    }
+    if (op.inner && (e = op.sweep(k, q, false, pipe, W))) return e;
+    if (op.xfer && q < op.ns - 1) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_xs, 0));
+  }
+  CUDA_TRY(cudaEventRecord(ls.ev_int, W));
+  CUDA_TRY(cudaStreamWaitEvent(S, ls.ev_int, 0));  // also joins W back into S
+  if ((e = op.finish(k, pipe, h, use, S))) return e;
+  CUDA_TRY(cudaEventRecord(ls.ev_epi[k & 1], S));
+  return HJB_OK;
+}
 
 // result fields from the loop state of the reporting rank
 int fill_result(hjb_context* ctx, float ms, hjb_solve_result* res) {
@@ -591,6 +693,8 @@ int sharded_prologue(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   int rc;
   CUDA_TRY(cudaSetDevice(ctx->device));
   if ((rc = validate_config(cfg))) return rc;
+  if (cfg->target)
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: no target set (use solve)");
   if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
   if (p.shape < 0)
     return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: model/grid outside the 4D fast path");
@@ -856,76 +960,48 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
                             cfg->time_horizon > 0.0 ? cfg->time_horizon : 0.0, cap,
                             ctx->hist.d(), ctx->whist.d(), ctx->stream));
   ++ctx->launches;
-  StreamPair sp;
-  CUDA_TRY(sp.init());
+  LoopStreams ls;
+  CUDA_TRY(ls.init());
   // halos of V_0 (afterwards every stage output travels right after its
   // boundary planes are swept)
   if (P > 1 && (rc = nccl_exchange(api, comm, rk, rk.buf[0], ctx->stream))) return rc;
   unsigned long long* maxbits = &ctx->st->maxdv_bits;
-  const bool xfer = P > 1 && rk.sp.bnd;
-  long long per_pos = 0;
-  // one loop position: per stage, boundary planes -> (comm stream) halo
-  // send/recv of the stage output || interior planes; join; then the
-  // residual all-reduce and the device epilogue
   const bool overlap = shard_overlap();
   const bool pipe = shard_pipeline();
   const int body = rk.ho ? 2 : 8;  // even: buffer parity of position k == iteration parity
-  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
-    per_pos = 0;
-    unsigned long long* slot = pipe ? &ctx->st->maxdv_slot[k & 1] : maxbits;
-    // position k overwrites V_{k-1}: epilogue k - 2 must have run
-    if (pipe && k >= 2) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
-    for (int q = 0; q < rk.ns; ++q) {
-      if (xfer && !overlap) {  // serial: whole slab, then the exchange
-        CUDA_TRY(rk.launch(k, q, true, slot));
-        if (rk.sp.inner) CUDA_TRY(rk.launch(k, q, false, slot));
-        int e = nccl_exchange(api, comm, rk, rk.stage_out(k, q), ctx->stream);
-        if (e) return e;
-        per_pos += rk.sp.inner ? 2 : 1;
-        continue;
-      }
-      if (xfer) {
-        CUDA_TRY(rk.launch(k, q, true, slot));
-        CUDA_TRY(cudaEventRecord(sp.ev_bnd, ctx->stream));
-        CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_bnd, 0));
-        int e = nccl_exchange(api, comm, rk, rk.stage_out(k, q), sp.comm);
-        if (e) return e;
-        CUDA_TRY(cudaEventRecord(sp.ev_xfer, sp.comm));
-        ++per_pos;
-      } else if (rk.sp.bnd) {
-        CUDA_TRY(rk.launch(k, q, true, slot));
-        ++per_pos;
-      }
-      if (rk.sp.inner) {
-        CUDA_TRY(rk.launch(k, q, false, slot));
-        ++per_pos;
-      }
-      if (xfer) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_xfer, 0));
-    }
-    if (!pipe) {
-      NCCL_TRY(api->AllReduce(maxbits, maxbits, 1, ncclUint64_, ncclMax_, comm->comm,
-                              ctx->stream));
-      CUDA_TRY(launch_epilogue(ctx->st, hd, use, ctx->stream));
-    } else {
-      CUDA_TRY(cudaEventRecord(sp.ev_int, ctx->stream));
-      CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_int, 0));
-      NCCL_TRY(api->AllReduce(slot, slot, 1, ncclUint64_, ncclMax_, comm->comm, sp.comm));
-      CUDA_TRY(launch_epilogue(ctx->st, hd, use, sp.comm, slot));
-      CUDA_TRY(cudaEventRecord(sp.ev_epi[k & 1], sp.comm));
-      // the body ends joined (the loop condition / poll reads the epilogue)
-      if (k == body - 1) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
-    }
+  long long per_pos = 0;
+  PositionOps op;
+  op.ns = rk.ns;
+  op.bnd = rk.sp.bnd;
+  op.inner = rk.sp.inner;
+  op.xfer = P > 1;
+  op.sweep = [&](int k, int q, bool boundary, bool pp, cudaStream_t s) -> int {
+    CUDA_TRY(rk.launch(k, q, boundary, pp ? &ctx->st->maxdv_slot[k & 1] : maxbits, s));
     ++per_pos;
     return HJB_OK;
   };
-  CUDA_TRY(cudaEventRecord(sp.e0, ctx->stream));
-  if ((rc = run_sharded_loop(ctx, body, step))) return rc;
-  CUDA_TRY(cudaEventRecord(sp.e1, ctx->stream));
-  CUDA_TRY(cudaEventSynchronize(sp.e1));
+  op.exchange = [&](int k, int q, cudaStream_t s) -> int {
+    return nccl_exchange(api, comm, rk, rk.stage_out(k, q), s);
+  };
+  op.finish = [&](int k, bool pp, cudaGraphConditionalHandle hd, int use, cudaStream_t s) -> int {
+    unsigned long long* slot = pp ? &ctx->st->maxdv_slot[k & 1] : maxbits;
+    NCCL_TRY(api->AllReduce(slot, slot, 1, ncclUint64_, ncclMax_, comm->comm, s));
+    CUDA_TRY(launch_epilogue(ctx->st, hd, use, s, pp ? slot : nullptr));
+    ++per_pos;
+    return HJB_OK;
+  };
+  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
+    per_pos = 0;
+    return run_position(ls, ctx->stream, op, k, overlap, pipe, hd, use);
+  };
+  CUDA_TRY(cudaEventRecord(ls.e0, ctx->stream));
+  if ((rc = run_eager_loop(ctx, body, step))) return rc;
+  CUDA_TRY(cudaEventRecord(ls.e1, ctx->stream));
+  CUDA_TRY(cudaEventSynchronize(ls.e1));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, sp.e0, sp.e1);
+  cudaEventElapsedTime(&ms, ls.e0, ls.e1);
   if ((rc = fill_result(ctx, ms, res))) return rc;
-  ctx->launches += per_pos * (res->iterations + body);
+  ctx->launches += per_pos * (res->iterations + 2 * body);
   const LoopState& st = *ctx->st_host;
   if ((rc = unpad_rank(rk, p, st.iter, value_slab_out, ctx->stream))) return rc;
   ++ctx->launches;
@@ -1011,8 +1087,8 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
                               r == 0 ? ctx->whist.d() : nullptr, ctx->stream));
     ++ctx->launches;
   }
-  StreamPair sp;
-  CUDA_TRY(sp.init());
+  LoopStreams ls;
+  CUDA_TRY(ls.init());
   std::vector<double*> xb(P);
   for (int r = 0; r < P; ++r) xb[r] = rks[r].buf[0];
   if (P > 1 && (rc = local_exchange(rks, xb, ctx->stream))) return rc;
@@ -1020,67 +1096,47 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
   const bool overlap = shard_overlap();
   const bool pipe = shard_pipeline();
   const int body = rks[0].ho ? 2 : 8;
-  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
-    per_pos = 0;
-    std::vector<unsigned long long*> acc(P);
-    for (int r = 0; r < P; ++r)
-      acc[r] = pipe ? &rs.st[r]->maxdv_slot[k & 1] : &rs.st[r]->maxdv_bits;
-    if (pipe && k >= 2) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
-    for (int q = 0; q < rks[0].ns; ++q) {
-      if (P > 1 && !overlap) {  // serial: every slab, then the exchange
-        for (int r = 0; r < P; ++r) {
-          CUDA_TRY(rks[r].launch(k, q, true, acc[r]));
-          if (rks[r].sp.inner) CUDA_TRY(rks[r].launch(k, q, false, acc[r]));
-          per_pos += rks[r].sp.inner ? 2 : 1;
-        }
-        for (int r = 0; r < P; ++r) xb[r] = rks[r].stage_out(k, q);
-        int e = local_exchange(rks, xb, ctx->stream);
-        if (e) return e;
-        continue;
-      }
-      for (int r = 0; r < P; ++r)
-        if (rks[r].sp.bnd) {
-          CUDA_TRY(rks[r].launch(k, q, true, acc[r]));
-          ++per_pos;
-        }
-      if (P > 1) {
-        CUDA_TRY(cudaEventRecord(sp.ev_bnd, ctx->stream));
-        CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_bnd, 0));
-        for (int r = 0; r < P; ++r) xb[r] = rks[r].stage_out(k, q);
-        int e = local_exchange(rks, xb, sp.comm);
-        if (e) return e;
-        CUDA_TRY(cudaEventRecord(sp.ev_xfer, sp.comm));
-      }
-      for (int r = 0; r < P; ++r)
-        if (rks[r].sp.inner) {
-          CUDA_TRY(rks[r].launch(k, q, false, acc[r]));
-          ++per_pos;
-        }
-      if (P > 1) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_xfer, 0));
+  bool any_bnd = false, any_inner = false;
+  for (int r = 0; r < P; ++r) {
+    any_bnd = any_bnd || rks[r].sp.bnd;
+    any_inner = any_inner || rks[r].sp.inner;
+  }
+  PositionOps op;
+  op.ns = rks[0].ns;
+  op.bnd = any_bnd;
+  op.inner = any_inner;
+  op.xfer = P > 1;
+  op.sweep = [&](int k, int q, bool boundary, bool pp, cudaStream_t s) -> int {
+    for (int r = 0; r < P; ++r) {
+      if (!(boundary ? rks[r].sp.bnd : rks[r].sp.inner)) continue;
+      unsigned long long* acc = pp ? &rs.st[r]->maxdv_slot[k & 1] : &rs.st[r]->maxdv_bits;
+      CUDA_TRY(rks[r].launch(k, q, boundary, acc, s));
+      ++per_pos;
     }
-    cudaStream_t es = ctx->stream;
-    if (pipe) {
-      CUDA_TRY(cudaEventRecord(sp.ev_int, ctx->stream));
-      CUDA_TRY(cudaStreamWaitEvent(sp.comm, sp.ev_int, 0));
-      es = sp.comm;
-    }
-    k_reduce_ranks<<<1, 32, 0, es>>>(rs, pipe ? (k & 1) : -1);
+    return HJB_OK;
+  };
+  op.exchange = [&](int k, int q, cudaStream_t s) -> int {
+    for (int r = 0; r < P; ++r) xb[r] = rks[r].stage_out(k, q);
+    return local_exchange(rks, xb, s);
+  };
+  op.finish = [&](int k, bool pp, cudaGraphConditionalHandle hd, int use, cudaStream_t s) -> int {
+    k_reduce_ranks<<<1, 32, 0, s>>>(rs, pp ? (k & 1) : -1);
     CUDA_TRY(cudaGetLastError());
     for (int r = 0; r < P; ++r)
-      CUDA_TRY(launch_epilogue(rs.st[r], hd, use, es, pipe ? acc[r] : nullptr));
-    if (pipe) {
-      CUDA_TRY(cudaEventRecord(sp.ev_epi[k & 1], sp.comm));
-      if (k == body - 1) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, sp.ev_epi[k & 1], 0));
-    }
+      CUDA_TRY(launch_epilogue(rs.st[r], hd, use, s, pp ? &rs.st[r]->maxdv_slot[k & 1] : nullptr));
     per_pos += 1 + P;
     return HJB_OK;
   };
-  CUDA_TRY(cudaEventRecord(sp.e0, ctx->stream));
+  auto step = [&](int k, cudaGraphConditionalHandle hd, int use) -> int {
+    per_pos = 0;
+    return run_position(ls, ctx->stream, op, k, overlap, pipe, hd, use);
+  };
+  CUDA_TRY(cudaEventRecord(ls.e0, ctx->stream));
   if ((rc = run_sharded_loop(ctx, body, step))) return rc;
-  CUDA_TRY(cudaEventRecord(sp.e1, ctx->stream));
-  CUDA_TRY(cudaEventSynchronize(sp.e1));
+  CUDA_TRY(cudaEventRecord(ls.e1, ctx->stream));
+  CUDA_TRY(cudaEventSynchronize(ls.e1));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, sp.e0, sp.e1);
+  cudaEventElapsedTime(&ms, ls.e0, ls.e1);
   if ((rc = fill_result(ctx, ms, res))) return rc;
   ctx->launches += per_pos * (res->iterations + body);
   const LoopState& st = *ctx->st_host;

@@ -817,11 +817,18 @@ def cfl_dt(grid: Grid, model: DynamicsModel, dbounds: IntervalField, cfl_factor:
     return out.value
 
 
+def _target_ok(target, grid):
+    if target is not None and not (target.grid() == grid):
+        raise InvalidArgument("solve: target grid mismatch")
+
+
 def vi_step(value: ScalarField, constraint: ScalarField, model: DynamicsModel,
             dbounds: IntervalField, dt: float, cfg: SolveConfig | None = None,
-            ctx: Context | None = None) -> ScalarField:
-    """solver.hpp:55-57."""
+            ctx: Context | None = None, target: ScalarField | None = None) -> ScalarField:
+    """solver.hpp:55-57.  ``target`` (extension, no reference counterpart):
+    reach-avoid update max(c, min(l, stepped)) against the target field l."""
     cfg = cfg or SolveConfig()
+    _target_ok(target, value.grid())
     if not (value.grid() == constraint.grid()):
         raise InvalidArgument("vi_step: value/constraint grid mismatch")
     if not (dbounds.grid() == value.grid()):
@@ -829,6 +836,8 @@ def vi_step(value: ScalarField, constraint: ScalarField, model: DynamicsModel,
     lib = abi.load()
     out = np.empty(value.size(), dtype=np.float64)
     g, m, d, c = value.grid().to_c(), model.to_c(), dbounds.to_c(), cfg.to_c()
+    if target is not None:
+        c.target = target.ptr()
     _check(lib.hjb_vi_step(_ctx(ctx), C.byref(g), C.byref(m), C.byref(d), value.ptr(),
                            constraint.ptr(), dt, C.byref(c), out.ctypes.data_as(C.c_void_p)))
     return ScalarField(value.grid(), out, check=False)
@@ -837,13 +846,17 @@ def vi_step(value: ScalarField, constraint: ScalarField, model: DynamicsModel,
 def solve(init: ScalarField, constraint: ScalarField, model: DynamicsModel,
           dbounds: IntervalField, cfg: SolveConfig | None = None,
           ctx: Context | None = None, history_capacity: int | None = None,
-          out: np.ndarray | None = None) -> SolveResult:
+          out: np.ndarray | None = None, target: ScalarField | None = None) -> SolveResult:
     """solver.hpp:63-65: iterate vi_step to a fixed point on the GPU.
 
     ``out`` (optional, float64, grid size, C-contiguous) receives V*; pass a
-    page-locked array to make the device->host copy a direct DMA."""
+    page-locked array to make the device->host copy a direct DMA.
+    ``target`` (extension; the reference has the avoid set only,
+    solver.cpp:178-179): every update becomes the reach-avoid
+    max(c, min(l, V + dt*H)) against the target field l."""
     cfg = cfg or SolveConfig()
     cfg.validate()
+    _target_ok(target, init.grid())
     if not (init.grid() == constraint.grid()):
         raise InvalidArgument("solve: init/constraint grid mismatch")
     if not (dbounds.grid() == init.grid()):
@@ -858,6 +871,8 @@ def solve(init: ScalarField, constraint: ScalarField, model: DynamicsModel,
         raise InvalidArgument("solve: out must be a writeable C-contiguous float64 array of grid size")
     out = out.reshape(-1)
     g, m, d, c = init.grid().to_c(), model.to_c(), dbounds.to_c(), cfg.to_c()
+    if target is not None:
+        c.target = target.ptr()
     _check(lib.hjb_solve(_ctx(ctx), C.byref(g), C.byref(m), C.byref(d), init.ptr(),
                          constraint.ptr(), C.byref(c), out.ctypes.data_as(C.c_void_p), C.byref(r)))
     return _to_result(init.grid(), out, r, rh, wh)
@@ -934,6 +949,48 @@ def solve_multilevel(constraint_fine: ScalarField, model: DynamicsModel,
                             wall.value)
 
 
+def solve_multilevel_dev(grids: Sequence[Grid], model: DynamicsModel,
+                         dbounds_fine: IntervalField, c_fine_ptr: int,
+                         cfg: SolveConfig | None = None, out_ptrs: Sequence[int] | None = None,
+                         warm_ptr: int = 0, ctx: Context | None = None,
+                         history_capacity: int = 0) -> MultiLevelResult:
+    """hjb_solve_multilevel_dev: the N-level chain with every field in HBM
+    (grids coarse to fine, the last one c_fine's); out_ptrs[l] (device, may
+    be 0) receive V*_l.  Results carry no host value."""
+    cfg = cfg or SolveConfig()
+    cfg.validate()
+    lib = abi.load()
+    nl = len(grids)
+    cg = (abi.HjbGrid * nl)(*[g.to_c() for g in grids])
+    res = (abi.HjbSolveResult * nl)()
+    keep = []
+    for l in range(nl):
+        rh = np.zeros(int(history_capacity))
+        wh = np.zeros(int(history_capacity))
+        keep.append((rh, wh))
+        res[l].residual_history = rh.ctypes.data_as(C.POINTER(C.c_double))
+        res[l].wall_ms_history = wh.ctypes.data_as(C.POINTER(C.c_double))
+        res[l].history_capacity = int(history_capacity)
+    optr = (C.c_void_p * nl)(*[(out_ptrs[l] if out_ptrs else 0) or None for l in range(nl)])
+    wall = C.c_double()
+    m, d, c = model.to_c(), dbounds_fine.to_c(), cfg.to_c()
+    _check(lib.hjb_solve_multilevel_dev(_ctx(ctx), nl, cg, C.byref(m), C.byref(d),
+                                        C.c_void_p(c_fine_ptr), C.byref(c),
+                                        C.c_void_p(warm_ptr) if warm_ptr else None, optr, res,
+                                        C.byref(wall)))
+    out = []
+    for l in range(nl):
+        r = res[l]
+        n = min(int(r.iterations), int(r.history_capacity))
+        out.append(SolveResult(value=None, iterations=int(r.iterations), dt=float(r.dt),
+                               wall_seconds=float(r.wall_seconds), converged=bool(r.converged),
+                               residual_history=keep[l][0][:n].copy(),
+                               wall_ms_history=keep[l][1][:n].copy(),
+                               nodes_per_sweep=int(r.nodes_per_sweep),
+                               final_residual=float(r.final_residual)))
+    return MultiLevelResult(out, wall.value)
+
+
 def resample(f, target: Grid, ctx: Context | None = None):
     """grid.hpp:108-109 (ScalarField) and solver.hpp:77 (IntervalField)."""
     if isinstance(f, IntervalField):
@@ -1003,7 +1060,8 @@ def field_min(a: ScalarField, b: ScalarField) -> ScalarField:
 # ------------------------------------------------- device-resident entry points
 def solve_dev(grid: Grid, model: DynamicsModel, dbounds: IntervalField, init_ptr: int,
               c_ptr: int, out_ptr: int, cfg: SolveConfig | None = None,
-              ctx: Context | None = None, history_capacity: int = 0) -> SolveResult:
+              ctx: Context | None = None, history_capacity: int = 0,
+              target_ptr: int = 0) -> SolveResult:
     """hjb_solve_dev: init/c/out are device pointers (e.g. torch CUDA tensors'
     data_ptr()); the value stays in HBM.  Returns the result metadata with an
     empty value field."""
@@ -1011,6 +1069,8 @@ def solve_dev(grid: Grid, model: DynamicsModel, dbounds: IntervalField, init_ptr
     lib = abi.load()
     r, rh, wh = _c_result(int(history_capacity))
     g, m, d, c = grid.to_c(), model.to_c(), dbounds.to_c(), cfg.to_c()
+    if target_ptr:
+        c.target = C.c_void_p(target_ptr)
     _check(lib.hjb_solve_dev(_ctx(ctx), C.byref(g), C.byref(m), C.byref(d), C.c_void_p(init_ptr),
                              C.c_void_p(c_ptr), C.byref(c), C.c_void_p(out_ptr), C.byref(r)))
     n = min(int(r.iterations), int(r.history_capacity))
@@ -1032,6 +1092,19 @@ def field_max_dev(n: int, a_ptr: int, b_ptr: int, out_ptr: int, ctx: Context | N
     lib = abi.load()
     _check(lib.hjb_field_max_dev(_ctx(ctx), int(n), C.c_void_p(a_ptr), C.c_void_p(b_ptr),
                                  C.c_void_p(out_ptr)))
+
+
+def field_min_dev(n: int, a_ptr: int, b_ptr: int, out_ptr: int, ctx: Context | None = None) -> None:
+    """field_min (levelset.cpp:84-86) on device pointers."""
+    lib = abi.load()
+    _check(lib.hjb_field_min_dev(_ctx(ctx), int(n), C.c_void_p(a_ptr), C.c_void_p(b_ptr),
+                                 C.c_void_p(out_ptr)))
+
+
+def field_negate_dev(n: int, a_ptr: int, out_ptr: int, ctx: Context | None = None) -> None:
+    """out = -a: the complement of a level-set field (obstacle -> avoid set)."""
+    lib = abi.load()
+    _check(lib.hjb_field_negate_dev(_ctx(ctx), int(n), C.c_void_p(a_ptr), C.c_void_p(out_ptr)))
 
 
 # SafetyFilter / Decomposition (safety.hpp, decomposition.hpp) live in

@@ -1,104 +1,197 @@
 """Run the BASELINE.json workloads end to end on the GPU and report.
 
 usage: python scripts/run_configs.py [cfg ...] [--max-iters N] [--json out.json]
+                                     [--no-cpu]
   cfg in {1, 2, 3, 4, 5}; default: 1 2
 
 Config 1: 2D vertical subsystem 101^2 to convergence (tol 1e-4).
 Config 2: 4D planar 51^4 to convergence (tol 1e-4) or --max-iters.
 Config 3: 4D planar 101^4 (first-order reference scheme) to convergence or cap.
 Config 4: decomposed 10D: 2D 101^2 + x/y 4D 71^4, cold at wind 0.5, warm 0.8,
-          then 10 warm updates with seeded bounds; the three subsystem solves
-          of every update run concurrently (one context + host thread each).
-Config 5: adaptive 26^4 -> 51^4 -> 101^4 (wind 0.6, 3 seeded obstacles).
-All timings are device times reported by the library.
+          then 10 warm updates with seeded bounds, through the device-resident
+          Decomposition chain (sim.cpp:339-363): every subsystem re-solves from
+          its filter's V* in HBM, concurrently (one context + host thread each),
+          and adopt() installs the device results.
+Config 5: adaptive 26^4 -> 51^4 -> 101^4 (wind 0.6, 3 seeded obstacles), the
+          avoid set built on the device (band + negate + field_max kernels),
+          the whole chain device-resident (hjb_solve_multilevel_dev).
+All GPU timings are device times reported by the library.  The reference's
+CPU time (oracle/_ref on this host's cores) is reported per level / update as
+its measured per-sweep cost x the GPU's iteration count — extrapolated, valid
+because the GPU iterates bit for bit like the reference (tests/
+test_golden_fullsize.py pins the counts).
 """
 import argparse
 import json
+import os
 import sys
 import threading
 import time
 from pathlib import Path
 
 import numpy as np
+import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
 
 from paper_2101_05916_b200 import configs  # noqa: E402
 from paper_2101_05916_b200 import hjsafe as hj  # noqa: E402
+from paper_2101_05916_b200 import safety  # noqa: E402
 
 
-def constraint(w, ctx):
-    """c on the device kernels (signed_distance_band + max), then to host."""
-    out = None
-    for dim, lo, hi, sign in w.bands:
-        f = hj.signed_distance_band(w.grid, dim, lo, hi, ctx=ctx).values()
-        f = -f if sign < 0 else f
-        out = f if out is None else np.where(out < f, f, out)
-    return hj.ScalarField(w.grid, out)
+def device_constraint(w, ctx):
+    out = torch.empty(w.grid.size(), dtype=torch.float64, device="cuda")
+    scratch = torch.empty_like(out)
+    torch.cuda.synchronize()
+    w.constraint_dev(out.data_ptr(), scratch.data_ptr(), ctx=ctx)
+    return out
+
+
+_REF_SWEEP = {}
+
+
+def ref_sweep_seconds(w, wind=None):
+    """The reference's loop time per sweep on this host (all cores), from a
+    bounded sample (SolveResult.wall_seconds of the reference's own solve)."""
+    key = (w.grid.shape, w.model.name(), wind)
+    if key in _REF_SWEEP:
+        return _REF_SWEEP[key]
+    from oracle import oracle as o
+    from cases import band_np, fmax_np
+    if not o.reference_available():
+        return None
+    ref = o.Reference()
+    c = hj.ScalarField(w.grid, w.constraint(band_np, fmax_np), check=False)
+    cfg = hj.SolveConfig(**w.cfg.__dict__)
+    cfg.threads = 0
+    cfg.max_iters = 1
+    r = ref.solve(c, c, w.model, w.dbounds(wind), cfg)
+    cfg.max_iters = int(max(2, min(400, 3.0 / max(r.wall_seconds, 1e-6))))
+    cfg.tolerance = 1e-30  # never stop early: the sample is a fixed sweep count
+    r = ref.solve(c, c, w.model, w.dbounds(wind), cfg)
+    _REF_SWEEP[key] = (r.wall_seconds / r.iterations, r.iterations)
+    return _REF_SWEEP[key]
 
 
 def summarize(r, cells):
     return {"iterations": r.iterations, "converged": r.converged, "dt": r.dt,
             "device_seconds": r.wall_seconds, "final_residual": r.final_residual,
-            "cell_updates_per_s": cells * r.iterations / max(r.wall_seconds, 1e-12),
-            "safe_cells": int(np.sum(r.value.values() <= 0)) if r.value is not None else None}
+            "cell_updates_per_s": cells * r.iterations / max(r.wall_seconds, 1e-12)}
 
 
-def run_single(w, max_iters, ctx):
-    c = constraint(w, ctx)
+def run_single(w, max_iters, ctx, cpu):
+    c = device_constraint(w, ctx)
+    out = torch.empty_like(c)
     cfg = hj.SolveConfig(**w.cfg.__dict__)
     cfg.max_iters = max_iters
-    r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=ctx, history_capacity=max_iters)
-    out = summarize(r, w.grid.size())
+    r = hj.solve_dev(w.grid, w.model, w.dbounds(), c.data_ptr(), c.data_ptr(), out.data_ptr(),
+                     cfg, ctx=ctx, history_capacity=max_iters)
+    res = summarize(r, w.grid.size())
+    res["safe_cells"] = int((out <= 0).sum().item())
     h = r.residual_history
     marks = [k for k in (1, 10, 100, 1000, 10000, 100000, 1000000) if k <= len(h)]
-    out["residual_at"] = {str(k): float(h[k - 1]) for k in marks}
-    return out
+    res["residual_at"] = {str(k): float(h[k - 1]) for k in marks}
+    if cpu:
+        per, n = ref_sweep_seconds(w)
+        res["reference_cpu_seconds_extrapolated"] = per * r.iterations
+        res["reference_sample"] = f"{n} sweeps, {os.cpu_count()} host threads"
+    return res
 
 
-def run_config4(max_iters, ctx0, tol):
-    subs = configs.config4_subsystems(tol=tol)
+def run_config4(max_iters, ctx0, tol, cpu):
+    """Decomposed 10D (sim.cpp:316-373 / initial_safety :264-301) with V*
+    never leaving HBM."""
+    ws = configs.config4_subsystems(tol=tol)  # z (2D), x, y (4D)
+    maps = {"z": ([8, 9], [2], [2]), "x": ([0, 1, 2, 3], [0], [0]), "y": ([4, 5, 6, 7], [1], [1])}
+    names = ["z", "x", "y"]
+    subs = [hj.Subsystem(nm, w.model, *maps[nm]) for nm, w in zip(names, ws)]
     bounds = configs.bound_sequence()
-    ctxs = [ctx0] + [hj.Context(0) for _ in subs[1:]]
-    cs = [constraint(w, ctxs[i]) for i, w in enumerate(subs)]
-    values = [c for c in cs]
-    report = []
-    for u, wind in enumerate(bounds):
-        results = [None] * len(subs)
+    ctxs = [ctx0] + [hj.Context(0) for _ in ws[1:]]
+    cdev = []
+    for w, cx in zip(ws, ctxs):
+        buf = safety.DeviceBuffer(cx, w.grid.size() * 8)
+        scratch = safety.DeviceBuffer(cx, w.grid.size() * 8)
+        w.constraint_dev(buf.ptr, scratch.ptr, ctx=cx)
+        scratch.free()
+        cdev.append(buf)
+    cfg = hj.SolveConfig(**ws[0].cfg.__dict__)
+    cfg.tolerance, cfg.max_iters = tol, max_iters
+    # cold solves from V = c, concurrently (initial_safety's solves)
+    cold = [None] * 3
+    db0 = [w.dbounds(bounds[0]) for w in ws]
 
-        def job(i):
-            w = subs[i]
-            cfg = hj.SolveConfig(**w.cfg.__dict__)
-            cfg.max_iters = max_iters
-            results[i] = hj.solve(values[i], cs[i], w.model, w.dbounds(wind), cfg, ctx=ctxs[i],
-                                  history_capacity=0)
+    def cold_job(i):
+        w = ws[i]
+        dst = safety.DeviceBuffer(ctxs[i], w.grid.size() * 8)
+        r = hj.solve_dev(w.grid, w.model, db0[i], cdev[i].ptr, cdev[i].ptr, dst.ptr, cfg,
+                         ctx=ctxs[i])
+        cold[i] = safety.DeviceSolve(grid=w.grid, value=dst, iterations=r.iterations, dt=r.dt,
+                                     wall_seconds=r.wall_seconds, converged=r.converged,
+                                     final_residual=r.final_residual)
 
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=cold_job, args=(i,)) for i in range(3)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    cold_wall = time.perf_counter() - t0
+    dec = hj.Decomposition(subs, 10, 3, 3)
+    dec.attach([hj.SafetyFilter(s.model, r, b, ctx=cx) for s, r, b, cx in zip(subs, cold, db0, ctxs)])
+    report = [{"update": 0, "wind": bounds[0], "kind": "cold", "latency_s": cold_wall,
+               "subsystems": {w.name: {"iterations": r.iterations, "device_seconds": r.wall_seconds,
+                                       "converged": r.converged} for w, r in zip(ws, cold)}}]
+    print(json.dumps(report[-1]), flush=True)
+    for u, wind in enumerate(bounds[1:], start=1):
+        db = [w.dbounds(wind) for w in ws]
         t0 = time.perf_counter()
-        th = [threading.Thread(target=job, args=(i,)) for i in range(len(subs))]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
+        upd = dec.warm_update(cdev, db, cfg, contexts=ctxs)
+        dec.adopt(upd, db)
         wall = time.perf_counter() - t0
-        values = [r.value for r in results]
-        report.append({"update": u, "wind": wind, "latency_s": wall,
-                       "subsystems": {w.name: summarize(r, w.grid.size()) for w, r in zip(subs, results)},
-                       "x_equals_y": bool(np.array_equal(results[1].value.values(),
-                                                         results[2].value.values()))})
-        print(json.dumps(report[-1]), flush=True)
+        xv = upd[1].value.download(np.empty(ws[1].grid.size()))
+        yv = upd[2].value.download(np.empty(ws[2].grid.size()))
+        rec = {"update": u, "wind": wind, "kind": "warm", "latency_s": wall,
+               "subsystems": {w.name: {"iterations": r.iterations, "device_seconds": r.wall_seconds,
+                                       "converged": r.converged} for w, r in zip(ws, upd)},
+               "x_equals_y": bool(np.array_equal(xv, yv))}
+        report.append(rec)
+        print(json.dumps(rec), flush=True)
+    if cpu:
+        per = {w.name: ref_sweep_seconds(w, 0.5)[0] for w in ws}
+        for rec in report:
+            rec["reference_cpu_seconds_extrapolated"] = sum(
+                per[nm] * s["iterations"] for nm, s in rec["subsystems"].items())
+        report.append({"reference_per_sweep_seconds": per,
+                       "note": "extrapolated: reference per-sweep loop time on this host (all "
+                               "cores) x the GPU's bitwise-equal iteration count, subsystems summed"})
     return report
 
 
-def run_config5(max_iters, ctx):
+def run_config5(max_iters, ctx, cpu):
     ws = configs.config5()
     fine = ws[-1]
-    c = constraint(fine, ctx)
+    c = device_constraint(fine, ctx)
+    outs = [torch.empty(w.grid.size(), dtype=torch.float64, device="cuda") for w in ws]
     cfg = hj.SolveConfig(**fine.cfg.__dict__)
     cfg.max_iters = max_iters
-    r = hj.solve_multilevel(c, fine.model, fine.dbounds(), [w.grid for w in ws[:-1]], cfg, ctx=ctx)
-    return {"levels": [dict(grid=str(w.grid.shape), **summarize(x, w.grid.size()))
-                       for w, x in zip(ws, r.levels)], "wall_seconds": r.wall_seconds,
-            "obstacles": configs.obstacles()}
+    torch.cuda.synchronize()
+    r = hj.solve_multilevel_dev([w.grid for w in ws], fine.model, fine.dbounds(), c.data_ptr(), cfg,
+                                out_ptrs=[o.data_ptr() for o in outs], ctx=ctx)
+    levels = []
+    for w, x, o in zip(ws, r.levels, outs):
+        d = dict(grid=str(w.grid.shape), **summarize(x, w.grid.size()))
+        d["safe_cells"] = int((o <= 0).sum().item())
+        if cpu:
+            per, n = ref_sweep_seconds(w, fine.wind)
+            d["reference_cpu_seconds_extrapolated"] = per * x.iterations
+            d["reference_sample"] = f"{n} sweeps of {w.grid.shape}"
+        levels.append(d)
+    out = {"levels": levels, "device_seconds_total": sum(x.wall_seconds for x in r.levels),
+           "wall_seconds": r.wall_seconds, "obstacles": configs.obstacles()}
+    if cpu:
+        out["reference_cpu_seconds_extrapolated_total"] = sum(
+            d["reference_cpu_seconds_extrapolated"] for d in levels)
+    return out
 
 
 def main():
@@ -106,6 +199,7 @@ def main():
     ap.add_argument("cfgs", nargs="*", default=["1", "2"])
     ap.add_argument("--max-iters", type=int, default=200000)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--tol4", type=float, default=5e-3,
                     help="config-4 tolerance (BASELINE leaves it open; the reference's own 10D "
                          "scenario uses 5e-3 for the 4D hover tail, sim.cpp:679)")
@@ -115,15 +209,15 @@ def main():
     for k in a.cfgs:
         t0 = time.perf_counter()
         if k == "1":
-            out["1"] = run_single(configs.config1(), 20000, ctx)
+            out["1"] = run_single(configs.config1(), 20000, ctx, a.cpu)
         elif k == "2":
-            out["2"] = run_single(configs.config2(51), a.max_iters, ctx)
+            out["2"] = run_single(configs.config2(51), a.max_iters, ctx, a.cpu)
         elif k == "3":
-            out["3"] = run_single(configs.config3(101), a.max_iters, ctx)
+            out["3"] = run_single(configs.config3(101), a.max_iters, ctx, a.cpu)
         elif k == "4":
-            out["4"] = run_config4(a.max_iters, ctx, a.tol4)
+            out["4"] = run_config4(a.max_iters, ctx, a.tol4, a.cpu)
         elif k == "5":
-            out["5"] = run_config5(a.max_iters, ctx)
+            out["5"] = run_config5(a.max_iters, ctx, a.cpu)
         print(f"config {k}: {time.perf_counter() - t0:.1f} s wall", flush=True)
         if k != "4":
             print(json.dumps(out[k]), flush=True)
