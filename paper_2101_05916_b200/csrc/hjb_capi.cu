@@ -712,6 +712,10 @@ int hjb::constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c,
   return HJB_OK;
 }
 
+// default size limit of the multi-sweep kernel (cells): 0 = off until
+// measured (HJB_MS=1 opts in)
+constexpr uint32_t kMsDefaultCells = 0u;
+
 static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
                       const hjb_dbounds* db_in, const double* init, const double* c,
                       const hjb_solve_config* cfg, double* value_out, hjb_solve_result* res) {
@@ -865,6 +869,14 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   const char* s2d = std::getenv("HJB_SMALL2D");
   const bool small2d = shape < 0 && g.nd == 2 && !(s2d && std::strcmp(s2d, "0") == 0) &&
                        !cfg->target && small2d_smem(g, nullptr, nullptr) <= 200 * 1024;
+  // multi-sweep persistent kernel (one cooperative launch for the whole
+  // solve, grid barrier + device epilogue between sweeps): the 4D fast path's
+  // Godunov variants on grids whose sweep is short enough that launch and
+  // ramp-up dominate.  HJB_MS=1 / 0 forces it on / off.
+  const char* ems = std::getenv("HJB_MS");
+  const bool multi = shape >= 0 && !f.lf && f.pv != 1 && !f.target && !f.cplane && f.kcells == 2 &&
+                  f.maxthreads == 576 &&
+                  (ems ? std::strcmp(ems, "1") == 0 : g.size <= kMsDefaultCells);
   if (small2d) {
     StepArgs x = a;
     x.src = ctx->v0.d();
@@ -872,6 +884,17 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     cudaError_t e = launch_small2d(x, ctx->stream);
     rc = e == cudaSuccess ? HJB_OK
                           : set_err(HJB_ERR_CUDA, std::string("small2d: ") + cudaGetErrorString(e));
+  } else if (multi) {
+    Fast4dArgs x = f;
+    x.ms = 1;
+    x.pdl = 0;
+    x.loop = 1;
+    x.use_handle = 0;
+    cudaError_t e = launch_fast4d(x, shape, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    rc = e == cudaSuccess ? HJB_OK
+                          : set_err(HJB_ERR_CUDA, std::string("fast4d (multi-sweep): ") +
+                                                      cudaGetErrorString(e));
   } else {
     rc = run_loop(ctx, launch, body);
   }
@@ -890,7 +913,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   const LoopState& st = *ctx->st_host;
-  ctx->launches += small2d ? 1 : st.iter + body;  // sweeps (+ early-exit tail of the body)
+  ctx->launches += (small2d || multi) ? 1 : st.iter + body;  // sweeps (+ early-exit tail of the body)
   res->iterations = st.iter;
   res->converged = st.converged;
   res->final_residual = st.last_residual;

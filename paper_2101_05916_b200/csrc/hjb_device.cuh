@@ -122,6 +122,7 @@ struct LoopState {
   // pipelined sharded loop: sweep k accumulates into maxdv_slot[k & 1] while
   // the all-reduce + epilogue of sweep k - 1 run on the comm stream
   unsigned long long maxdv_slot[2];
+  unsigned int gen;  // grid-barrier generation of the multi-sweep kernel
 };
 
 }  // namespace hjb

@@ -440,7 +440,8 @@ __device__ __forceinline__ void lds_pn(const double* p, double* v) {
   }
 }
 
-template <class S, int kK, int MAXT, int SCH, int PV = 0, bool CP = false, bool TG = false>
+template <class S, int kK, int MAXT, int SCH, int PV = 0, bool CP = false, bool TG = false,
+          bool MS = false>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -485,11 +486,16 @@ __global__ void __launch_bounds__(MAXT, 1)
   // programmatic dependent launch it overlaps that sweep's tail; the loop
   // state and V are read only after the dependency resolves
   if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // MS (multi-sweep persistent mode): the sweeps of the whole solve run in
+  // this one cooperative launch, separated by a grid barrier whose last
+  // arriver runs the solve() epilogue; the ring positions carry over
+  uint32_t ppos = 0, cpos = 0;
+  for (;;) {
   double* dst;
   const CUtensorMap* vmap;
-  if (a.loop == 1) {  // device loop: buffer parity from the loop state
+  if (MS || a.loop == 1) {  // device loop: buffer parity from the loop state
     if (*(volatile int*)&a.st->done) return;
-    const long long it = a.st->iter;
+    const long long it = *(volatile long long*)&a.st->iter;
     dst = (it & 1) ? a.buf0 : a.buf1;
     vmap = (it & 1) ? &a.map1 : &a.map0;
   } else {  // explicit buffers (single step, or a slab sweep of the sharded loop)
@@ -502,8 +508,11 @@ __global__ void __launch_bounds__(MAXT, 1)
   if (threadIdx.x >= ncons) {
     // ---------------- producer thread ----------------
     if (lane == 0) {
-      uint32_t pos = 0;  // ring position (slot = pos % kRing, use = pos / kRing)
+      uint32_t pos = ppos;  // ring position (slot = pos % kRing, use = pos / kRing)
       uint32_t w = blockIdx.x;
+      // MS: V of this sweep was written by other CTAs' generic stores before
+      // the grid barrier; order them before this thread's async-proxy loads
+      if (MS) asm volatile("fence.proxy.async.global;" ::: "memory");
       // balanced schedule: this CTA's unit range (tile-major tile-planes)
       const uint32_t np = a.cend - a.cbeg;
       const uint64_t units = static_cast<uint64_t>(a.tiles1) * a.tiles2 * np;
@@ -542,6 +551,7 @@ __global__ void __launch_bounds__(MAXT, 1)
                        "r"(0u)
                        : "memory");
           mbar_arrive(bars + sl * 8);
+          ppos = pos + 1;  // MS: the end marker used one slot
           break;
         }
         const uint32_t pbeg = c0 > 0 ? c0 - 1 : 0;
@@ -587,14 +597,21 @@ __global__ void __launch_bounds__(MAXT, 1)
     const uint32_t orr = has_r ? own + 8u * kK : own + 8u * (kK - 1);
     const uint32_t cown = (r * n3p + i3) * 8u;
     double mdv = 0.0;
-    uint32_t pos = 0;  // ring position of the item's first plane
+    uint32_t pos = cpos;  // ring position of the item's first plane
 
     for (;;) {
       uint32_t sl = pos % kRing, ph = (pos / kRing) & 1u;
       mbar_wait(bars + sl * 8, ph);
       uint32_t tix, crange;
       asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tix), "=r"(crange) : "r"(hdr0 + sl * 8));
-      if (tix == kEndItem) break;
+      if (tix == kEndItem) {
+        if (MS) {  // release the marker's slot for the next sweep
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bars + (kRing + sl) * 8);
+          cpos = pos + 1;
+        }
+        break;
+      }
       const uint32_t t1 = tix / a.tiles2, t2 = tix - t1 * a.tiles2;
       const uint32_t c0 = crange & 0xffffu;
       const uint32_t c1 = crange >> 16;
@@ -988,11 +1005,38 @@ __global__ void __launch_bounds__(MAXT, 1)
     mbits = (unsigned long long)__double_as_longlong(mdv);
   }
 
+  __shared__ unsigned long long part[32];
+  if constexpr (MS) {
+    // this CTA's stores of V_{k+1} -> visible to the next sweep's TMA loads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
+    if (lane == 0) part[warp] = mbits;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0ull;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) m = umax64(m, part[w]);
+      LoopState* st = a.st;
+      if (m) atomicMax(&st->maxdv_bits, m);
+      __threadfence();
+      const unsigned int gen = *(volatile unsigned int*)&st->gen;
+      const unsigned int ticket = atomicAdd(&st->blocks_done, 1u);
+      if (ticket == gridDim.x - 1) {  // last arriver: the solve() epilogue, then release
+        __threadfence();
+        loop_epilogue(st, a.handle, 0);
+        atomicAdd(&st->gen, 1u);
+      } else {
+        while (*(volatile unsigned int*)&st->gen == gen) __nanosleep(64);
+        __threadfence();
+      }
+    }
+    __syncthreads();
+    continue;
+  }
   // this CTA's planes are done: the next sweep may start its set-up
   if (a.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // CTA max -> global; the last CTA resets the work counter and, in the
   // device loop, runs the sweep epilogue (solver.cpp:347-369)
-  __shared__ unsigned long long part[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mbits = umax64(mbits, __shfl_xor_sync(0xffffffffu, mbits, o));
   if (lane == 0) part[warp] = mbits;
@@ -1015,6 +1059,8 @@ __global__ void __launch_bounds__(MAXT, 1)
     st->work_next = 0u;
     __threadfence();
   }
+  return;
+  }  // sweeps
 }
 
 // ---------------------------------------------------------------- k_ho4d
@@ -2569,10 +2615,26 @@ static bool smem_attr_once(std::atomic<unsigned long long>& done, K kernel) {
   return true;
 }
 
-template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false, bool TG = false>
+template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false, bool TG = false,
+          bool MS = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP, TG>)) return;
+  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS>)) return;
+  if (MS) {  // persistent over sweeps: every CTA must be resident (grid barrier)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.blocks);
+    cfg.blockDim = dim3(a.threads);
+    cfg.dynamicSmemBytes = a.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS>, a);
+    if (e != cudaSuccess) t_attr_err = e;
+    return;
+  }
   if (a.l2_bytes == 0 && !a.pdl) {
     k_fast4d<S, K, MAXT, SCH, PV, CP, TG><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
@@ -2600,13 +2662,20 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG>, a);
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
 // the autotuner pick among them per grid
 template <class S>
 static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.ms) {  // multi-sweep persistent launch (small grids): whole solve
+    if (a.pv == 2)
+      launch_one<S, 2, 576, 0, 2, false, false, true>(a, s);
+    else
+      launch_one<S, 2, 576, 0, 0, false, false, true>(a, s);
+    return;
+  }
   if (a.target) {  // target set: Godunov, constant bounds, field constraint
     launch_one<S, 2, 576, 0, 0, false, true>(a, s);
     return;

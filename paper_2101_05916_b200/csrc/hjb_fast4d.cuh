@@ -45,6 +45,11 @@ struct Fast4dArgs {
   unsigned long long* mdv;
   // padded target set l (TG variant): out = max(c, min(l, stepped))
   const double* target;
+  // 1: multi-sweep persistent launch (k_fast4d MS): one cooperative launch
+  // runs every sweep of the solve with a grid barrier + device epilogue
+  // between sweeps (Godunov, kcells 2 / 576 threads, constant or per-node
+  // bounds)
+  int ms;
   const double* tab;    // slope tables (staged into shared memory per CTA)
   uint32_t tab_len;     // doubles in tab
   uint32_t tab_off;     // shared-memory byte offset of the staged copy

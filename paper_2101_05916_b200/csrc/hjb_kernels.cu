@@ -496,6 +496,7 @@ __global__ void k_loop_init(LoopState* st, long long max_iters, double dt, doubl
   st->wall_history = wall_history;
   st->maxdv_slot[0] = 0ull;
   st->maxdv_slot[1] = 0ull;
+  st->gen = 0u;
   st->t0_ns = globaltimer_ns();
 }
 

@@ -162,3 +162,58 @@ def test_gpu_adaptive_chain_matches_reference(gpu_ctx):
                              ctx=gpu_ctx)
     for lv in range(3):
         _check(f"chain49_l{lv}", "chain49", ml.levels[lv], meta)
+
+
+# ------------------------------------- multi-sweep persistent kernel (MS)
+# One cooperative launch runs every sweep of the solve with a grid barrier
+# and the device epilogue between sweeps (k_fast4d<..., MS>).  Same bits,
+# same iteration counts as the reference fixtures.
+
+@pytest.mark.gpu
+def test_gpu_multisweep_converges_in_reference_iteration_count(gpu_ctx, monkeypatch):
+    monkeypatch.setenv("HJB_MS", "1")
+    w = configs.config2(21)
+    c, cfg = _inputs(w, tol=5e-3, max_iters=200000)
+    r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx)
+    _check("conv21", "conv21", r)
+
+
+@pytest.mark.gpu
+def test_gpu_multisweep_config2_full_grid(gpu_ctx, monkeypatch):
+    monkeypatch.setenv("HJB_MS", "1")
+    w = configs.config2(51)
+    c, cfg = _inputs(w, max_iters=1000)
+    r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx)
+    _check("k51_1000", "k51", r)
+
+
+@pytest.mark.gpu
+def test_gpu_multisweep_adaptive_chain(gpu_ctx, monkeypatch):
+    """Coarse levels carry resampled (per-node) bounds: the MS per-node variant."""
+    monkeypatch.setenv("HJB_MS", "1")
+    meta = _meta()
+    if "chain49_l2" not in meta:
+        pytest.skip("chain49 fixture not generated")
+    ws = configs.config5(levels=(13, 25, 49), tol=5e-3)
+    c, cfg = _inputs(ws[-1], tol=5e-3, max_iters=200000)
+    ml = hj.solve_multilevel(c, ws[-1].model, ws[-1].dbounds(), [x.grid for x in ws[:-1]], cfg,
+                             ctx=gpu_ctx)
+    for lv in range(3):
+        _check(f"chain49_l{lv}", "chain49", ml.levels[lv], meta)
+
+
+@pytest.mark.gpu
+def test_gpu_multisweep_time_horizon_and_max_iters(gpu_ctx, monkeypatch, oracle):
+    """Stops by max_iters / time horizon inside the persistent kernel."""
+    monkeypatch.setenv("HJB_MS", "1")
+    w = configs.config2(13)
+    c, cfg = _inputs(w, tol=1e-12, max_iters=37)
+    r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx)
+    want = oracle.solve(c, c, w.model, w.dbounds(), cfg)
+    assert r.iterations == want.iterations == 37
+    assert np.array_equal(r.value.values(), want.value.values())
+    cfg.max_iters, cfg.time_horizon = 1000, 25.5 * r.dt
+    r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx)
+    want = oracle.solve(c, c, w.model, w.dbounds(), cfg)
+    assert r.iterations == want.iterations == 26
+    assert np.array_equal(r.value.values(), want.value.values())
