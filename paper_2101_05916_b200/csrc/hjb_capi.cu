@@ -712,9 +712,11 @@ int hjb::constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c,
   return HJB_OK;
 }
 
-// default size limit of the multi-sweep kernel (cells): 0 = off until
-// measured (HJB_MS=1 opts in)
-constexpr uint32_t kMsDefaultCells = 0u;
+// default size limit of the multi-sweep kernel (cells).  Measured per sweep
+// (scripts/bench_ms.py, profiles/round2_bench_ms.log): 21^4-41^4 3-10 %
+// faster than one launch per sweep (constant and per-node bounds), 51^4 3 %
+// and 71^4 13 % slower, so it is used up to ~3.1 M cells (41^4).
+constexpr uint32_t kMsDefaultCells = 3u << 20;
 
 static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
                       const hjb_dbounds* db_in, const double* init, const double* c,

@@ -286,7 +286,10 @@ struct PlaneSplit {
 };
 PlaneSplit plane_split(const SlabGeom& s) {
   PlaneSplit x;
-  if (s.P == 1) {
+  // HJB_SHARD_SPLIT=0 (diagnostic, with HJB_SHARD_OVERLAP=0): one launch
+  // over the whole slab, then the exchange
+  const char* e = std::getenv("HJB_SHARD_SPLIT");
+  if (s.P == 1 || (e && std::strcmp(e, "0") == 0)) {
     x.i0 = s.cbeg;
     x.i1 = s.cend;
     x.inner = true;

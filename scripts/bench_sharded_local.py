@@ -55,7 +55,9 @@ def main():
         return best / iters * 1e6
 
     variants = {"overlap+pipe": {}, "serial": {"HJB_SHARD_OVERLAP": "0", "HJB_SHARD_PIPE": "0"},
-                "overlap_only": {"HJB_SHARD_PIPE": "0"}}
+                "overlap_only": {"HJB_SHARD_PIPE": "0"},
+                "serial_one_launch": {"HJB_SHARD_OVERLAP": "0", "HJB_SHARD_PIPE": "0",
+                                      "HJB_SHARD_SPLIT": "0"}}
     ranks = [int(x) for x in a.ranks.split(",")]
     res["first_order"]["unsharded_us"] = run(1, 1, a.sweeps, 0, {})
     for name, env in variants.items():
