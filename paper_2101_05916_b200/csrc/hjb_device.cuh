@@ -123,6 +123,10 @@ struct LoopState {
   // the all-reduce + epilogue of sweep k - 1 run on the comm stream
   unsigned long long maxdv_slot[2];
   unsigned int gen;  // grid-barrier generation of the multi-sweep kernel
+  // sharded slab launches: finished boundary items (per consumer warp) and
+  // the flag the halo transfer waits for (reset by the transfer stream)
+  unsigned int bnd_done;
+  unsigned int bnd_flag;
 };
 
 }  // namespace hjb

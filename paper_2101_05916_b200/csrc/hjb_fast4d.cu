@@ -301,13 +301,25 @@ __device__ __forceinline__ double shape_pick(const RowShape& r, double a, double
   return __fma_rn(a, r.m, r.ca) > b * r.m ? a : b;
 }
 
+// work index w (item or block) -> (chunk, rest): boundary items first
+template <class A>
+__device__ __forceinline__ uint32_t split_index(const A& a, uint32_t w, uint32_t& chunk) {
+  if (w < a.bitems) {
+    chunk = w % a.nb;
+    return w / a.nb;
+  }
+  w -= a.bitems;
+  const uint32_t ni = a.nchunks - a.nb;
+  chunk = a.nb + w % ni;
+  return w / ni;
+}
+
 // Work item w of a sweep: a T1 x T2 tile of (i1, i2) rows and a chunk of
 // axis-0 planes.  Full tiles come first and edge (partial) tiles last, so
 // the dynamic schedule hands out the long items first.
 __device__ __forceinline__ void item_tile(const Fast4dArgs& a, uint32_t w, uint32_t& t1,
                                           uint32_t& t2, uint32_t& chunk) {
-  chunk = w % a.nchunks;
-  const uint32_t u = w / a.nchunks;
+  const uint32_t u = split_index(a, w, chunk);
   const uint32_t f1 = a.n[1] / a.T1, f2 = a.n[2] / a.T2;  // full tiles per axis
   const uint32_t nf = f1 * f2;
   if (u < nf) {
@@ -328,18 +340,38 @@ __device__ __forceinline__ void item_tile(const Fast4dArgs& a, uint32_t w, uint3
   t2 = e;
 }
 
-// planes [c0, c1) of chunk `chunk` (two-range boundary launches: chunks at
-// or past `split` lie in the second range)
+// planes [c0, c1) of chunk `chunk`: the nb boundary chunks first, then the
+// interior chunks of L planes
 template <class A>
 __device__ __forceinline__ void chunk_planes(const A& a, uint32_t chunk, uint32_t& c0,
                                              uint32_t& c1) {
-  if (a.split != 0u && chunk >= a.split) {
-    c0 = a.c2beg + (chunk - a.split) * a.L;
-    c1 = min(c0 + a.L, a.c2end);
+  if (chunk < a.nb) {
+    c0 = chunk ? a.b1 : a.b0;
+    c1 = chunk ? a.e1 : a.e0;
   } else {
-    c0 = a.cbeg + chunk * a.L;
+    c0 = a.cbeg + (chunk - a.nb) * a.L;
     c1 = min(c0 + a.L, a.cend);
   }
+}
+
+// a consumer warp finished an item of planes [c0, ...): count boundary items
+// and raise the flag with the last one (release: the planes' stores first)
+template <class A>
+__device__ __forceinline__ void signal_item(const A& a, LoopState* st, uint32_t c0,
+                                            uint32_t lane) {
+  const bool bnd = (a.nb > 0u && c0 >= a.b0 && c0 < a.e0) ||
+                   (a.nb > 1u && c0 >= a.b1 && c0 < a.e1);
+  if (!bnd) return;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(&st->bnd_done, 1u) + 1u == a.bnd_target) atomicExch(&st->bnd_flag, 1u);
+  }
+}
+// an early-exiting launch (loop done) still releases the transfer stream
+template <class A>
+__device__ __forceinline__ void signal_exit(const A& a, LoopState* st) {
+  if (a.signal && blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&st->bnd_flag, 1u);
 }
 
 constexpr uint32_t kEndItem = 0xffffffffu;
@@ -499,7 +531,10 @@ __global__ void __launch_bounds__(MAXT, 1)
     dst = (it & 1) ? a.buf0 : a.buf1;
     vmap = (it & 1) ? &a.map1 : &a.map0;
   } else {  // explicit buffers (single step, or a slab sweep of the sharded loop)
-    if (a.loop == 2 && *(volatile int*)&a.st->done) return;
+    if (a.loop == 2 && *(volatile int*)&a.st->done) {
+      signal_exit(a, a.st);
+      return;
+    }
     dst = a.dst;
     vmap = &a.map0;
   }
@@ -1001,6 +1036,7 @@ __global__ void __launch_bounds__(MAXT, 1)
         if (lane == 0) mbar_arrive(bars + (kRing + sl) * 8);
         ++pos;
       }
+      if (a.signal) signal_item(a, a.st, c0, lane);
     }
     mbits = (unsigned long long)__double_as_longlong(mdv);
   }
@@ -1161,7 +1197,10 @@ template <class S, int R>
 __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_constant__ Ho4dArgs a) {
   constexpr int kK = 2;
   LoopState* st = a.st;
-  if (a.loop != 0 && *(volatile int*)&st->done) return;
+  if (a.loop != 0 && *(volatile int*)&st->done) {
+    signal_exit(a, st);
+    return;
+  }
   const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
@@ -1172,8 +1211,8 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
   const uint32_t n0 = a.n[0], n1 = a.n[1], n2 = a.n[2], n3 = a.n[3], n3p = a.n3p;
   const uint32_t J = n3p / kK;
   uint32_t b = blockIdx.x;
-  const uint32_t chunk = b % a.nchunks;
-  b /= a.nchunks;
+  uint32_t chunk;
+  b = split_index(a, b, chunk);
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
   const uint32_t t = threadIdx.x;
   const uint32_t rr = t / J, j = t - rr * J;
@@ -1381,6 +1420,7 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
         fw[2 * R - 1][c] = ok ? (vw[2 * R][c] - vw[2 * R - 1][c]) * inv0 : 0.0;
     }
   }
+  if (a.signal) signal_item(a, st, c0, threadIdx.x & 31u);
   if (!a.final_stage) return;
   // max|V_{n+1} - V_n| -> loop state; the last CTA runs the solve() epilogue
   unsigned long long mbits = (unsigned long long)__double_as_longlong(mdv);
@@ -1452,7 +1492,10 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   constexpr int kK = KC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
-  if (a.loop != 0 && *(volatile int*)&st->done) return;
+  if (a.loop != 0 && *(volatile int*)&st->done) {
+    signal_exit(a, st);
+    return;
+  }
   const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
@@ -1465,8 +1508,8 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   const uint32_t J = a.T3 / kK;  // pencil threads per tile row
   const uint32_t B3 = a.T3 + 2 * a.H3;  // box row width (cells)
   uint32_t b = blockIdx.x;
-  const uint32_t chunk = b % a.nchunks;
-  b /= a.nchunks;
+  uint32_t chunk;
+  b = split_index(a, b, chunk);
   const uint32_t seg = b % a.segs;
   b /= a.segs;
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
@@ -1846,6 +1889,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
           fw[2 * R - 1][c] = ok ? (vw[2 * R][c] - vw[2 * R - 1][c]) * inv0 : 0.0;
       }
     }
+    if (a.signal) signal_item(a, st, c0, lane);
   }
   if (!a.final_stage) return;
   unsigned long long mbits = (unsigned long long)__double_as_longlong(mdv);
@@ -1917,7 +1961,10 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
   constexpr int R = 3, kK = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
-  if (a.loop != 0 && *(volatile int*)&st->done) return;
+  if (a.loop != 0 && *(volatile int*)&st->done) {
+    signal_exit(a, st);
+    return;
+  }
   const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
   double* outp = (it & 1) ? a.buf0 : a.buf1;
@@ -1930,8 +1977,8 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
   const uint32_t J = a.T3 / kK;
   const uint32_t B3 = a.T3 + 2 * a.H3;
   uint32_t b = blockIdx.x;
-  const uint32_t chunk = b % a.nchunks;
-  b /= a.nchunks;
+  uint32_t chunk;
+  b = split_index(a, b, chunk);
   const uint32_t seg = b % a.segs;
   b /= a.segs;
   const uint32_t t2 = b % a.tiles2, t1 = b / a.tiles2;
@@ -2298,6 +2345,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
         vlast[c] = vnx[c];
       }
     }
+    if (a.signal) signal_item(a, st, c0, lane);
   }
   if (!a.final_stage) return;
   unsigned long long mbits = (unsigned long long)__double_as_longlong(mdv);
@@ -2554,9 +2602,16 @@ void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a) {
 }
 
 void fast4d_chunks(Fast4dArgs& a, int sms) {
-  a.split = a.c2beg = a.c2end = 0u;
+  a.nb = a.b0 = a.e0 = a.b1 = a.e1 = a.bitems = 0u;
   const uint32_t tiles = a.tiles1 * a.tiles2;
   const uint32_t span = a.cend - a.cbeg;
+  if (span == 0) {
+    a.L = 1;
+    a.nchunks = a.items = 0;
+    a.blocks = 0;
+    a.bal = 0;
+    return;
+  }
   // measured (B200): 51^4 and 71^4 best at 2 chunks, 101^4 at 1
   uint32_t nch = 1;
   if (tiles < 3u * sms)
@@ -2577,19 +2632,23 @@ void fast4d_chunks(Fast4dArgs& a, int sms) {
   if (a.bal) a.blocks = std::min<uint32_t>(static_cast<uint32_t>(sms), tiles * span);
 }
 
-void fast4d_ranges(Fast4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1) {
+void fast4d_bfirst(Fast4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1,
+                   uint32_t i0, uint32_t i1) {
+  a.cbeg = i0;
+  a.cend = i1;
+  fast4d_chunks(a, sms);  // the interior's chunks (none when i0 == i1)
   const uint32_t tiles = a.tiles1 * a.tiles2;
-  a.cbeg = b0;
-  a.cend = e0;
-  a.L = e0 - b0;
-  const bool two = b1 < e1;
-  a.split = two ? 1u : 0u;
-  a.c2beg = two ? b1 : 0u;
-  a.c2end = two ? e1 : 0u;
-  a.nchunks = 1u + (two ? (e1 - b1 + a.L - 1) / a.L : 0u);
+  a.nb = (b0 < e0 ? 1u : 0u) + (b1 < e1 ? 1u : 0u);
+  a.b0 = b0;
+  a.e0 = e0;
+  a.b1 = b1;
+  a.e1 = e1;
+  a.nchunks += a.nb;
+  a.bitems = tiles * a.nb;
   a.items = tiles * a.nchunks;
   a.blocks = std::min<uint32_t>(a.items, static_cast<uint32_t>(sms));
-  a.bal = 0u;  // dynamic items (the balanced schedule assumes one range)
+  a.bal = 0u;  // dynamic items, boundary first
+  a.bnd_target = a.bitems * (a.consumers >> 5);
 }
 
 // Function attributes are per device: set the dynamic shared-memory limit
@@ -2836,9 +2895,15 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
 }
 
 void ho4d_chunks(Ho4dArgs& a, int sms) {
-  a.split = a.c2beg = a.c2end = 0u;
+  a.nb = a.b0 = a.e0 = a.b1 = a.e1 = a.bitems = 0u;
   const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
   const uint32_t span = a.cend - a.cbeg;
+  if (span == 0) {
+    a.L = 1;
+    a.nchunks = 0;
+    a.blocks = 0;
+    return;
+  }
   uint32_t nch = 1;
   if (a.eno3g) {
     // one CTA per SM: pick the chunk count that minimises the wave-quantised
@@ -2860,17 +2925,22 @@ void ho4d_chunks(Ho4dArgs& a, int sms) {
   a.blocks = tiles * a.nchunks;
 }
 
-void ho4d_ranges(Ho4dArgs& a, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1) {
+void ho4d_bfirst(Ho4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1,
+                 uint32_t i0, uint32_t i1) {
+  a.cbeg = i0;
+  a.cend = i1;
+  ho4d_chunks(a, sms);
   const uint32_t tiles = a.tiles1 * a.tiles2 * (a.tma ? a.segs : 1u);
-  a.cbeg = b0;
-  a.cend = e0;
-  a.L = e0 - b0;
-  const bool two = b1 < e1;
-  a.split = two ? 1u : 0u;
-  a.c2beg = two ? b1 : 0u;
-  a.c2end = two ? e1 : 0u;
-  a.nchunks = 1u + (two ? (e1 - b1 + a.L - 1) / a.L : 0u);
+  a.nb = (b0 < e0 ? 1u : 0u) + (b1 < e1 ? 1u : 0u);
+  a.b0 = b0;
+  a.e0 = e0;
+  a.b1 = b1;
+  a.e1 = e1;
+  a.nchunks += a.nb;
+  a.bitems = tiles * a.nb;
   a.blocks = tiles * a.nchunks;
+  // counting warps: the consumers of the TMA kernels, every warp of k_ho4d
+  a.bnd_target = a.bitems * (a.tma ? (a.threads - 32u) >> 5 : a.threads >> 5);
 }
 
 namespace {

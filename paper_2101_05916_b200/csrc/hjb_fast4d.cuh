@@ -38,9 +38,14 @@ struct Fast4dArgs {
   // tile pieces each); 0: dynamic items (tile x chunk) off the work counter
   uint32_t bal;
   uint32_t cbeg, cend;  // planes updated (0, 0 = the whole axis-0 extent)
-  // second plane range of a boundary launch (sharded solve): chunks >= split
-  // cover [c2beg, c2end) in chunks of L planes; split == 0: one range
-  uint32_t split, c2beg, c2end;
+  // sharded slabs: nb (0..2) BOUNDARY chunks [b0, e0), [b1, e1) come first
+  // in the item order (bitems = tiles x nb items), then the interior
+  // [cbeg, cend) in chunks of L planes.  signal: every consumer warp that
+  // finishes a boundary item counts it in st->bnd_done; the count that
+  // reaches bnd_target raises st->bnd_flag (the halo transfer waits for it
+  // on the stream: cuStreamWaitValue32); an early exit raises it too
+  uint32_t nb, b0, e0, b1, e1, bitems, bnd_target;
+  int signal;
   // max|dV| accumulator of the launch (null: st->maxdv_bits)
   unsigned long long* mdv;
   // padded target set l (TG variant): out = max(c, min(l, stepped))
@@ -116,7 +121,8 @@ struct Ho4dArgs {
   //    epilogue); 0: one stage on explicit buffers (xsrc, xvn -> xdst)
   int loop;
   uint32_t cbeg, cend;  // planes updated (0, 0 = all)
-  uint32_t split, c2beg, c2end;  // second plane range (as Fast4dArgs)
+  uint32_t nb, b0, e0, b1, e1, bitems, bnd_target;  // boundary chunks first (as Fast4dArgs)
+  int signal;
   unsigned long long* mdv;       // max|dV| accumulator (null: st->maxdv_bits)
   // pmode 1: the V_n buffer parity is `parity` (sharded loop: the loop
   // state's iteration count advances concurrently on the comm stream)
@@ -177,16 +183,18 @@ int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
 // caller checks which on the device.
 int fast4d_shape_pv(const DevGrid& g, const DevModel& m);
 void fast4d_config(const DevGrid& g, int sms, Fast4dArgs& a);
-// Restrict a configured launch (fast4d_config / ho4d_config done) to the
-// planes [b0, e0) and, when b1 < e1, [b1, e1) too — the boundary planes of a
-// slab, swept before its interior so they can travel while the interior
-// sweeps.  One chunk of e0 - b0 planes per range and tile.
-void fast4d_ranges(Fast4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1);
+// Configure a launch (fast4d_config / ho4d_config done) for a slab: the
+// boundary planes [b0, e0) and, when b1 < e1, [b1, e1) as the FIRST items
+// (one chunk per range and tile), then the interior [i0, i1) chunked as
+// fast4d_chunks / ho4d_chunks would (i0 == i1: boundary only).
+void fast4d_bfirst(Fast4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1,
+                   uint32_t i0, uint32_t i1);
+void ho4d_bfirst(Ho4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1,
+                 uint32_t i0, uint32_t i1);
 // Re-chunk a configured launch over its plane range [cbeg, cend) (the
 // chunking fast4d_config / ho4d_config apply)
 void fast4d_chunks(Fast4dArgs& a, int sms);
 void ho4d_chunks(Ho4dArgs& a, int sms);
-void ho4d_ranges(Ho4dArgs& a, uint32_t b0, uint32_t e0, uint32_t b1, uint32_t e1);
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s);
 // Encode the three TMA tensor maps for the padded buffers (driver entry point
 // fetched through the runtime; no libcuda link dependency).

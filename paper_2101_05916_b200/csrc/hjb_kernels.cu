@@ -497,6 +497,8 @@ __global__ void k_loop_init(LoopState* st, long long max_iters, double dt, doubl
   st->maxdv_slot[0] = 0ull;
   st->maxdv_slot[1] = 0ull;
   st->gen = 0u;
+  st->bnd_done = 0u;
+  st->bnd_flag = 0u;
   st->t0_ns = globaltimer_ns();
 }
 

@@ -37,6 +37,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -321,15 +322,19 @@ PlaneSplit plane_split(const SlabGeom& s) {
 }
 
 // ------------------------------------------------------------- one rank
+enum LaunchMode { kBnd = 0, kInner = 1, kBoth = 2 };
 struct SlabRank {
   SlabGeom geo;
   PlaneSplit sp;
   int shape = -1;
   bool ho = false;
   size_t pe = 0;  // elements per local plane
-  Fast4dArgs fb, fi;  // first order: boundary / interior launches
+  // launches (first order f*, high order h*): boundary planes only,
+  // interior only, and both in one launch with the boundary items first and
+  // the completion signal (bnd_flag) for the transfer stream
+  Fast4dArgs fb, fi, fc;
   CUtensorMap map_b0, map_b1;
-  Ho4dArgs hb, hi;  // high order
+  Ho4dArgs hb, hi, hc;
   HoStage stages[3];
   int ns = 1;
   double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // V parity 0/1, stage1, stage2
@@ -343,22 +348,22 @@ struct SlabRank {
   }
   // V after `iters` completed iterations
   double* value(long long iters) const { return (iters & 1) ? buf[1] : buf[0]; }
-  // slot: the max|dV| accumulator of position k (null: st->maxdv_bits)
-  cudaError_t launch(int k, int q, bool boundary, unsigned long long* slot,
-                     cudaStream_t s) const;
+  // mode: kBnd / kInner / kBoth; slot: the max|dV| accumulator of
+  // position k (null: st->maxdv_bits)
+  cudaError_t launch(int k, int q, int mode, unsigned long long* slot, cudaStream_t s) const;
 };
 
-cudaError_t SlabRank::launch(int k, int q, bool boundary, unsigned long long* slot,
+cudaError_t SlabRank::launch(int k, int q, int mode, unsigned long long* slot,
                              cudaStream_t s) const {
   if (!ho) {
-    Fast4dArgs x = boundary ? fb : fi;
+    Fast4dArgs x = mode == kBnd ? fb : (mode == kInner ? fi : fc);
     x.src = (k & 1) ? buf[1] : buf[0];
     x.dst = (k & 1) ? buf[0] : buf[1];
     x.map0 = (k & 1) ? map_b1 : map_b0;
     x.mdv = slot;
     return launch_fast4d(x, shape, s);
   }
-  Ho4dArgs x = boundary ? hb : hi;
+  Ho4dArgs x = mode == kBnd ? hb : (mode == kInner ? hi : hc);
   x.mdv = slot;
   x.pmode = 1;  // position parity == iteration parity (even body, loop from 0)
   x.parity = k & 1;
@@ -426,12 +431,15 @@ int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, doubl
     f.loop = 2;
     rk.fi = f;
     rk.fb = f;
-    if (rk.sp.inner) {
-      rk.fi.cbeg = rk.sp.i0;
-      rk.fi.cend = rk.sp.i1;
-      fast4d_chunks(rk.fi, sms);
+    rk.fc = f;
+    const PlaneSplit& x = rk.sp;
+    if (x.inner) fast4d_bfirst(rk.fi, sms, 0, 0, 0, 0, x.i0, x.i1);
+    if (x.bnd) {
+      fast4d_bfirst(rk.fb, sms, x.b0, x.e0, x.b1, x.e1, 0, 0);
+      fast4d_bfirst(rk.fc, sms, x.b0, x.e0, x.b1, x.e1, x.inner ? x.i0 : 0,
+                    x.inner ? x.i1 : 0);
+      rk.fc.signal = 1;
     }
-    if (rk.sp.bnd) fast4d_ranges(rk.fb, sms, rk.sp.b0, rk.sp.e0, rk.sp.b1, rk.sp.e1);
     return HJB_OK;
   }
   Ho4dArgs h;
@@ -475,12 +483,14 @@ int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, doubl
   CUDA_TRY(ho4d_make_maps(h));
   rk.hi = h;
   rk.hb = h;
-  if (rk.sp.inner) {
-    rk.hi.cbeg = rk.sp.i0;
-    rk.hi.cend = rk.sp.i1;
-    ho4d_chunks(rk.hi, sms);
+  rk.hc = h;
+  const PlaneSplit& x = rk.sp;
+  if (x.inner) ho4d_bfirst(rk.hi, sms, 0, 0, 0, 0, x.i0, x.i1);
+  if (x.bnd) {
+    ho4d_bfirst(rk.hb, sms, x.b0, x.e0, x.b1, x.e1, 0, 0);
+    ho4d_bfirst(rk.hc, sms, x.b0, x.e0, x.b1, x.e1, x.inner ? x.i0 : 0, x.inner ? x.i1 : 0);
+    rk.hc.signal = 1;
   }
-  if (rk.sp.bnd) ho4d_ranges(rk.hb, rk.sp.b0, rk.sp.e0, rk.sp.b1, rk.sp.e1);
   return HJB_OK;
 }
 
@@ -576,6 +586,51 @@ bool shard_pipeline() {
   return !(e && std::strcmp(e, "0") == 0);
 }
 
+// Stream memory operations (driver API, fetched through the runtime like the
+// tensor-map encoder): the transfer stream waits until a launch raises
+// st->bnd_flag, then re-arms it.  HJB_SHARD_SIGNAL=0 falls back to the
+// boundary launch + interior launch split.
+typedef CUresult (*PfnValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+  PfnValue32 wait = nullptr, write = nullptr;
+};
+const MemOps* memops() {
+  static MemOps m;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      m.wait = reinterpret_cast<PfnValue32>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      m.write = reinterpret_cast<PfnValue32>(fn);
+  });
+  return (m.wait && m.write) ? &m : nullptr;
+}
+bool shard_signal() {
+  const char* e = std::getenv("HJB_SHARD_SIGNAL");
+  return !(e && std::strcmp(e, "0") == 0) && memops() != nullptr;
+}
+// the transfer stream waits for / re-arms one rank's boundary flag
+int wait_flag(LoopState* st, cudaStream_t s) {
+  const CUresult r = memops()->wait(reinterpret_cast<CUstream>(s),
+                                    reinterpret_cast<CUdeviceptr>(&st->bnd_flag), 1u,
+                                    CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? HJB_OK : set_err(HJB_ERR_CUDA, "cuStreamWaitValue32 failed");
+}
+int rearm_flag(LoopState* st, cudaStream_t s) {
+  CUresult r = memops()->write(reinterpret_cast<CUstream>(s),
+                               reinterpret_cast<CUdeviceptr>(&st->bnd_done), 0u,
+                               CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r == CUDA_SUCCESS)
+    r = memops()->write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(&st->bnd_flag),
+                        0u, CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? HJB_OK : set_err(HJB_ERR_CUDA, "cuStreamWriteValue32 failed");
+}
+
 // Streams and events of the sharded loop.  The sweep KERNELS run on a work
 // stream W; halo transfers, the residual reduction (NCCL all-reduce or the
 // in-process kernel) and the epilogue run on the capture's origin stream S,
@@ -620,8 +675,14 @@ struct LoopStreams {
 struct PositionOps {
   int ns = 1;                  // RK stages
   bool bnd = false, inner = true, xfer = false;
-  // sweep kernels of stage q on stream s (accumulator of position k: slot)
-  std::function<int(int k, int q, bool boundary, bool pipe, cudaStream_t s)> sweep;
+  // signal: one launch per stage (boundary items first); the transfer
+  // stream waits on the launch's bnd_flag (wait_bnd), moves the halos and
+  // re-arms the flag (reset_bnd).  Otherwise a boundary launch, then the
+  // transfer (after the launch) || an interior launch.
+  bool signal = false;
+  std::function<int(cudaStream_t s)> wait_bnd, reset_bnd;
+  // sweep kernels of stage q on stream s (mode kBnd / kInner / kBoth)
+  std::function<int(int k, int q, int mode, bool pipe, cudaStream_t s)> sweep;
   // halo transfer of stage q's output, on s
   std::function<int(int k, int q, cudaStream_t s)> exchange;
   // residual reduction + epilogue of position k, on s
@@ -634,8 +695,8 @@ int run_position(LoopStreams& ls, cudaStream_t S, const PositionOps& op, int k, 
   int e;
   if (!overlap) {  // serial: every kernel, then the transfer, on S; no pipelining
     for (int q = 0; q < op.ns; ++q) {
-      if (op.bnd && (e = op.sweep(k, q, true, false, S))) return e;
-      if (op.inner && (e = op.sweep(k, q, false, false, S))) return e;
+      if (op.bnd && (e = op.sweep(k, q, kBnd, false, S))) return e;
+      if (op.inner && (e = op.sweep(k, q, kInner, false, S))) return e;
       if (op.xfer && (e = op.exchange(k, q, S))) return e;
     }
     return op.finish(k, false, h, use, S);
@@ -650,14 +711,23 @@ int run_position(LoopStreams& ls, cudaStream_t S, const PositionOps& op, int k, 
     else if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_epi[k & 1], 0));
   }
   for (int q = 0; q < op.ns; ++q) {
-    if (op.bnd && (e = op.sweep(k, q, true, pipe, W))) return e;
+    if (op.xfer && op.signal) {  // one launch; the transfer starts on its flag
+      if ((e = op.sweep(k, q, kBoth, pipe, W))) return e;
+      if ((e = op.wait_bnd(S))) return e;
+      if ((e = op.exchange(k, q, S))) return e;
+      if ((e = op.reset_bnd(S))) return e;
+      CUDA_TRY(cudaEventRecord(q == op.ns - 1 ? ls.ev_xl[k & 1] : ls.ev_xs, S));
+      if (q < op.ns - 1) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_xs, 0));
+      continue;
+    }
+    if (op.bnd && (e = op.sweep(k, q, kBnd, pipe, W))) return e;
     if (op.xfer) {
       CUDA_TRY(cudaEventRecord(ls.ev_bnd, W));
       CUDA_TRY(cudaStreamWaitEvent(S, ls.ev_bnd, 0));
       if ((e = op.exchange(k, q, S))) return e;
       CUDA_TRY(cudaEventRecord(q == op.ns - 1 ? ls.ev_xl[k & 1] : ls.ev_xs, S));
     }
-    if (op.inner && (e = op.sweep(k, q, false, pipe, W))) return e;
+    if (op.inner && (e = op.sweep(k, q, kInner, pipe, W))) return e;
     if (op.xfer && q < op.ns - 1) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_xs, 0));
   }
   CUDA_TRY(cudaEventRecord(ls.ev_int, W));
@@ -978,8 +1048,11 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   op.bnd = rk.sp.bnd;
   op.inner = rk.sp.inner;
   op.xfer = P > 1;
-  op.sweep = [&](int k, int q, bool boundary, bool pp, cudaStream_t s) -> int {
-    CUDA_TRY(rk.launch(k, q, boundary, pp ? &ctx->st->maxdv_slot[k & 1] : maxbits, s));
+  op.signal = op.xfer && shard_signal();
+  op.wait_bnd = [&](cudaStream_t s) -> int { return wait_flag(ctx->st, s); };
+  op.reset_bnd = [&](cudaStream_t s) -> int { return rearm_flag(ctx->st, s); };
+  op.sweep = [&](int k, int q, int mode, bool pp, cudaStream_t s) -> int {
+    CUDA_TRY(rk.launch(k, q, mode, pp ? &ctx->st->maxdv_slot[k & 1] : maxbits, s));
     ++per_pos;
     return HJB_OK;
   };
@@ -1109,11 +1182,34 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
   op.bnd = any_bnd;
   op.inner = any_inner;
   op.xfer = P > 1;
-  op.sweep = [&](int k, int q, bool boundary, bool pp, cudaStream_t s) -> int {
+  // in-process ranks share one host thread: the signalling protocol's eager
+  // loop would be host-bound there, so it is opt-in (HJB_SHARD_SIGNAL=1)
+  {
+    const char* e = std::getenv("HJB_SHARD_SIGNAL");
+    op.signal = op.xfer && e && std::strcmp(e, "1") == 0 && shard_signal();
+  }
+  op.wait_bnd = [&](cudaStream_t s) -> int {
     for (int r = 0; r < P; ++r) {
-      if (!(boundary ? rks[r].sp.bnd : rks[r].sp.inner)) continue;
+      int e = wait_flag(rs.st[r], s);
+      if (e) return e;
+    }
+    return HJB_OK;
+  };
+  op.reset_bnd = [&](cudaStream_t s) -> int {
+    for (int r = 0; r < P; ++r) {
+      int e = rearm_flag(rs.st[r], s);
+      if (e) return e;
+    }
+    return HJB_OK;
+  };
+  op.sweep = [&](int k, int q, int mode, bool pp, cudaStream_t s) -> int {
+    for (int r = 0; r < P; ++r) {
+      if (mode == kBnd && !rks[r].sp.bnd) continue;
+      if (mode == kInner && !rks[r].sp.inner) continue;
+      // kBoth: ranks without a boundary (P == 1) run their interior
+      const int m = (mode == kBoth && !rks[r].sp.bnd) ? kInner : mode;
       unsigned long long* acc = pp ? &rs.st[r]->maxdv_slot[k & 1] : &rs.st[r]->maxdv_bits;
-      CUDA_TRY(rks[r].launch(k, q, boundary, acc, s));
+      CUDA_TRY(rks[r].launch(k, q, m, acc, s));
       ++per_pos;
     }
     return HJB_OK;
@@ -1135,7 +1231,10 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
     return run_position(ls, ctx->stream, op, k, overlap, pipe, hd, use);
   };
   CUDA_TRY(cudaEventRecord(ls.e0, ctx->stream));
-  if ((rc = run_sharded_loop(ctx, body, step))) return rc;
+  // stream memory operations stay out of graph capture: the signalling
+  // protocol runs the host-driven loop (as the NCCL transport always does)
+  if ((rc = op.signal ? run_eager_loop(ctx, body, step) : run_sharded_loop(ctx, body, step)))
+    return rc;
   CUDA_TRY(cudaEventRecord(ls.e1, ctx->stream));
   CUDA_TRY(cudaEventSynchronize(ls.e1));
   float ms = 0.f;

@@ -233,3 +233,36 @@ def test_local_ranks_thin_slab_rejected(gpu_ctx):
     cfg.spatial_order, cfg.time_order = 3, 3
     with pytest.raises(hj.Unsupported):
         _local(gpu_ctx, w, c, cfg, 4, 5)
+
+
+@pytest.mark.parametrize("order,rk,P", [(1, 1, 2), (1, 1, 8), (3, 3, 3), (2, 2, 4)])
+def test_local_ranks_signal_protocol_equal_solve(gpu_ctx, monkeypatch, order, rk, P):
+    """The NCCL transport's default protocol on in-process ranks: ONE launch
+    per rank and stage with the boundary items first; the transfer stream
+    waits on the launch's boundary flag (cuStreamWaitValue32), moves the
+    halos and re-arms it; host-driven loop with one-batch lookahead."""
+    monkeypatch.setenv("HJB_SHARD_SIGNAL", "1")
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=60)
+    cfg.spatial_order, cfg.time_order = order, rk
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, P, 60)
+    assert r.iterations == ref.iterations == 60
+    assert same(r.residual_history, ref.residual_history)
+    assert same(v, ref.value.values())
+
+
+def test_local_ranks_signal_protocol_converges(gpu_ctx, monkeypatch):
+    """Convergence (the loop stops mid-batch; the extra batch's launches find
+    done set and still release the transfer stream's flag wait)."""
+    monkeypatch.setenv("HJB_SHARD_SIGNAL", "1")
+    w = configs.config2(11)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=5e-3, max_iters=200000)
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, 3, 0)
+    assert r.converged and r.iterations == ref.iterations
+    assert same(v, ref.value.values())
