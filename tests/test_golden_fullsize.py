@@ -217,3 +217,33 @@ def test_gpu_multisweep_time_horizon_and_max_iters(gpu_ctx, monkeypatch, oracle)
     want = oracle.solve(c, c, w.model, w.dbounds(), cfg)
     assert r.iterations == want.iterations == 26
     assert np.array_equal(r.value.values(), want.value.values())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["k51_lf_40", "k51_lfg_40", "k51_pvx_60", "k51_pn_60",
+                                 "k51_stock_60"])
+def test_gpu_config2_grid_variants(gpu_ctx, key):
+    """51^4, reference-generated: Lax-Friedrichs (per-node / global alpha),
+    x-varying and per-node bound fields, the stock model (wind on v)."""
+    meta = _meta()
+    if key not in meta:
+        pytest.skip("k51x fixture not generated")
+    from golden.make_golden_fullsize import k51x_cases
+    w, cases = k51x_cases()
+    model, db, extra, k = cases[key]
+    c, cfg = _inputs(w, max_iters=k)
+    for a, v in extra.items():
+        setattr(cfg, a, v)
+    r = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    _check(key, "k51x", r, meta)
+
+
+@pytest.mark.gpu
+def test_gpu_config4_grid_71(gpu_ctx):
+    meta = _meta()
+    if "k71_20" not in meta:
+        pytest.skip("k71 fixture not generated")
+    w = configs.config2(71)
+    c, cfg = _inputs(w, max_iters=20)
+    r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx)
+    _check("k71_20", "k71", r, meta)
