@@ -154,6 +154,19 @@ typedef struct hjb_solve_config {
  * it must reproduce the reference update bit for bit) */
 #define HJB_FLAG_FORCE_HO 1
 
+/* hjb_solve_result.kernel: which kernel family ran the iterations (a model
+ * or bound field outside the 4D fast path's shapes runs the generic kernel,
+ * ~3.5x slower per cell at 51^4; this reports it instead of falling back
+ * silently) */
+#define HJB_KERNEL_NONE 0          /* max_iters == 0 */
+#define HJB_KERNEL_GENERIC 1       /* k_step, any rank 1..6 */
+#define HJB_KERNEL_FAST4D 2        /* k_fast4d, one launch per sweep */
+#define HJB_KERNEL_FAST4D_MULTI 3  /* k_fast4d multi-sweep persistent launch */
+#define HJB_KERNEL_SMALL2D 4       /* k_small2d, whole loop in one cluster launch */
+#define HJB_KERNEL_HO_GENERIC 5    /* k_ho_stage (ENO / TVD-RK, rank 1..4) */
+#define HJB_KERNEL_HO4D 6          /* k_ho4t / k_eno3g / k_ho4d */
+#define HJB_KERNEL_SMALL2D_HO 7    /* k_small2d_ho */
+
 /* SolveResult, reference solver.hpp:27-36.  The value field is written to
  * the caller's buffer; histories are written to caller buffers of
  * `history_capacity` entries (may be NULL / 0). */
@@ -162,7 +175,7 @@ typedef struct hjb_solve_result {
   double dt;
   double wall_seconds;  /* device time of the iteration loop */
   int32_t converged;
-  int32_t reserved;
+  int32_t kernel;       /* HJB_KERNEL_*: the sweep kernel the solve ran */
   int64_t nodes_per_sweep;
   double final_residual;
   double* residual_history; /* max|dV|/dt per iteration */

@@ -79,7 +79,7 @@ class HjbSolveConfig(C.Structure):
 class HjbSolveResult(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("dt", C.c_double),
                 ("wall_seconds", C.c_double), ("converged", C.c_int32),
-                ("reserved", C.c_int32), ("nodes_per_sweep", C.c_int64),
+                ("kernel", C.c_int32), ("nodes_per_sweep", C.c_int64),
                 ("final_residual", C.c_double),
                 ("residual_history", C.POINTER(C.c_double)),
                 ("wall_ms_history", C.POINTER(C.c_double)),

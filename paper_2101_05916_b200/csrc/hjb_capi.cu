@@ -755,6 +755,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   res->converged = 0;
   res->iterations = 0;
   res->final_residual = 0.0;
+  res->kernel = HJB_KERNEL_NONE;
 
   if (cfg->spatial_order > 1 || cfg->time_order > 1 || (cfg->flags & HJB_FLAG_FORCE_HO))
     return ho_solve(ctx, g, hm.dm, init, c, cfg, dt, s.max_alpha, value_out, res);
@@ -916,6 +917,9 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   cudaEventDestroy(e1);
   const LoopState& st = *ctx->st_host;
   ctx->launches += (small2d || multi) ? 1 : st.iter + body;  // sweeps (+ early-exit tail of the body)
+  res->kernel = small2d ? HJB_KERNEL_SMALL2D
+                        : (multi ? HJB_KERNEL_FAST4D_MULTI
+                                 : (shape >= 0 ? HJB_KERNEL_FAST4D : HJB_KERNEL_GENERIC));
   res->iterations = st.iter;
   res->converged = st.converged;
   res->final_residual = st.last_residual;

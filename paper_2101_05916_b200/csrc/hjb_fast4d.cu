@@ -1134,14 +1134,14 @@ __device__ __forceinline__ void eno_sel(const double* A, const double* d2, const
     {
       const bool left = fabs(d2[1]) <= fabs(d2[2]);
       const double c2 = left ? d2[1] : d2[2];
-      const double c3 = left ? minabs_d(t3[0], t3[1]) : minabs_d(t3[1], t3[2]);
+      const double c3 = minabs_d(left ? t3[0] : t3[1], left ? t3[1] : t3[2]);  // one |.| test: the chosen pair
       const double w = left ? kHoThird : kHoSixthNeg;
       dm = (A[2] + 0.5 * c2) + w * c3;
     }
     {
       const bool left = fabs(d2[2]) <= fabs(d2[3]);
       const double c2 = left ? d2[2] : d2[3];
-      const double c3 = left ? minabs_d(t3[1], t3[2]) : minabs_d(t3[2], t3[3]);
+      const double c3 = minabs_d(left ? t3[1] : t3[2], left ? t3[2] : t3[3]);  // one |.| test: the chosen pair
       const double w = left ? kHoSixthNeg : kHoThird;
       dp = (A[3] + -0.5 * c2) + w * c3;
     }
@@ -1157,14 +1157,14 @@ __device__ __forceinline__ void eno_faces(const double* A, double& dm, double& d
     {
       const bool left = fabs(d2m1) <= fabs(d20);
       const double c2 = left ? d2m1 : d20;
-      const double c3 = left ? minabs_d(t1, t2) : minabs_d(t2, t3);
+      const double c3 = minabs_d(left ? t1 : t2, left ? t2 : t3);  // one |.| test: the chosen pair
       const double w = left ? kHoThird : kHoSixthNeg;
       dm = (A[2] + 0.5 * c2) + w * c3;
     }
     {
       const bool left = fabs(d20) <= fabs(d21);
       const double c2 = left ? d20 : d21;
-      const double c3 = left ? minabs_d(t2, t3) : minabs_d(t3, t4);
+      const double c3 = minabs_d(left ? t2 : t3, left ? t3 : t4);  // one |.| test: the chosen pair
       const double w = left ? kHoSixthNeg : kHoThird;
       dp = (A[3] + -0.5 * c2) + w * c3;
     }
@@ -1938,7 +1938,7 @@ __device__ __forceinline__ void eno3_face(double e0, double e1, double e2, doubl
   const double h0 = g1 - g0, h1 = g2 - g1, h2 = g3 - g2;
   const bool left = fabs(g1) <= fabs(g2);
   const double c2 = left ? g1 : g2;
-  const double c3 = left ? minabs_d(h0, h1) : minabs_d(h1, h2);
+  const double c3 = minabs_d(left ? h0 : h1, left ? h1 : h2);  // one |.| test: the chosen pair
   const double hc = 0.5 * c2;  // -0.5 * c2 == -(0.5 * c2) exactly
   dp_left = (e2 - hc) + (left ? kHoSixthNeg : kHoThird) * c3;
   dm_right = (e2 + hc) + (left ? kHoThird : kHoSixthNeg) * c3;

@@ -213,6 +213,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   cudaEventDestroy(e1);
   const LoopState& ls = *ctx->st_host;
   ctx->launches += small2d ? 1 : (ls.iter + body) * ns;
+  res->kernel = small2d ? HJB_KERNEL_SMALL2D_HO : (shape >= 0 ? HJB_KERNEL_HO4D : HJB_KERNEL_HO_GENERIC);
   res->iterations = ls.iter;
   res->converged = ls.converged;
   res->final_residual = ls.last_residual;

@@ -773,6 +773,11 @@ class SolveResult:
     wall_ms_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
     nodes_per_sweep: int = 0
     final_residual: float = 0.0
+    kernel: str = ""  # the kernel family that ran the sweeps (HJB_KERNEL_*)
+
+
+KERNELS = {0: "none", 1: "generic", 2: "fast4d", 3: "fast4d_multisweep", 4: "small2d",
+           5: "ho_generic", 6: "ho4d", 7: "small2d_ho"}
 
 
 @dataclass
@@ -802,7 +807,8 @@ def _to_result(grid, value, r, rh, wh) -> SolveResult:
                        dt=float(r.dt), wall_seconds=float(r.wall_seconds),
                        converged=bool(r.converged), residual_history=rh[:n].copy(),
                        wall_ms_history=wh[:n].copy(), nodes_per_sweep=int(r.nodes_per_sweep),
-                       final_residual=float(r.final_residual))
+                       final_residual=float(r.final_residual),
+                       kernel=KERNELS.get(int(r.kernel), str(int(r.kernel))))
 
 
 def cfl_dt(grid: Grid, model: DynamicsModel, dbounds: IntervalField, cfl_factor: float,
@@ -1077,7 +1083,8 @@ def solve_dev(grid: Grid, model: DynamicsModel, dbounds: IntervalField, init_ptr
     return SolveResult(value=None, iterations=int(r.iterations), dt=float(r.dt),
                        wall_seconds=float(r.wall_seconds), converged=bool(r.converged),
                        residual_history=rh[:n].copy(), wall_ms_history=wh[:n].copy(),
-                       nodes_per_sweep=int(r.nodes_per_sweep), final_residual=float(r.final_residual))
+                       nodes_per_sweep=int(r.nodes_per_sweep), final_residual=float(r.final_residual),
+                       kernel=KERNELS.get(int(r.kernel), str(int(r.kernel))))
 
 
 def signed_distance_band_dev(grid: Grid, dim: int, lo: float, hi: float, out_ptr: int,

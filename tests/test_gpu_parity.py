@@ -467,3 +467,26 @@ print("ok")
         r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True,
                            timeout=300)
         assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_result_reports_the_kernel_family(gpu_ctx):
+    """A solve says which kernel family ran it (a model outside the 4D fast
+    path's shapes falls to the generic kernel: reported, not silent)."""
+    from paper_2101_05916_b200 import configs
+    w = configs.config2(21)
+    c = hj.signed_distance_band(w.grid, 0, -4.0, 4.0, ctx=gpu_ctx)
+    cfg = hj.SolveConfig(max_iters=3)
+    assert hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx).kernel == "fast4d_multisweep"
+    w5 = configs.config2(61)
+    c5 = hj.signed_distance_band(w5.grid, 0, -4.0, 4.0, ctx=gpu_ctx)
+    assert hj.solve(c5, c5, w5.model, w5.dbounds(), cfg, ctx=gpu_ctx).kernel == "fast4d"
+    w1 = configs.config1()
+    c1 = hj.signed_distance_band(w1.grid, 0, 0.0, 3.0, ctx=gpu_ctx)
+    assert hj.solve(c1, c1, w1.model, w1.dbounds(), cfg, ctx=gpu_ctx).kernel == "small2d"
+    g3 = hj.Grid([(0.0, 1.0, 9), (0.0, 1.0, 9), (0.0, 1.0, 9)])
+    adv = hj.ConstantAdvection([1.0, 0.5, -0.25])
+    c3 = hj.ScalarField(g3, np.zeros(g3.size()))
+    db3 = hj.IntervalField.constant(g3, [])
+    assert hj.solve(c3, c3, adv, db3, cfg, ctx=gpu_ctx).kernel == "generic"
+    cfg.spatial_order, cfg.time_order = 3, 3
+    assert hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=gpu_ctx).kernel == "ho4d"
