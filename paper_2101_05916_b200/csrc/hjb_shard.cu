@@ -439,6 +439,14 @@ int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, doubl
       fast4d_bfirst(rk.fc, sms, x.b0, x.e0, x.b1, x.e1, x.inner ? x.i0 : 0,
                     x.inner ? x.i1 : 0);
       rk.fc.signal = 1;
+      // The persistent sweep fills every SM it runs on (~200 KB of shared
+      // memory, 576 threads), so an NCCL kernel launched while it runs could
+      // not start before it ends: leave a few SMs to the transfer
+      // (HJB_SHARD_COMM_SMS, default 4; dynamic work items rebalance).
+      const char* ce = std::getenv("HJB_SHARD_COMM_SMS");
+      const int comm_sms = ce ? std::max(0, std::atoi(ce)) : 4;
+      const uint32_t cap = static_cast<uint32_t>(std::max(1, sms - comm_sms));
+      for (Fast4dArgs* a : {&rk.fi, &rk.fc}) a->blocks = std::min(a->blocks, cap);
     }
     return HJB_OK;
   }

@@ -116,9 +116,15 @@ def test_restatement_reproduces_reference_chain_level0(oracle):
         pytest.skip("chain49 fixture not generated")
     ws = configs.config5(levels=(13, 25, 49), tol=5e-3)
     c, cfg = _inputs(ws[-1], tol=5e-3, max_iters=200000)
-    ml = oracle.solve_multilevel(c, ws[-1].model, ws[-1].dbounds(), [ws[0].grid], cfg)
-    # a 2-level chain's first level is the 3-level chain's first level
-    _check("chain49_l0", "chain49", ml.levels[0], meta)
+    # level 0 alone: c and the bounds resampled from the fine grid
+    # (solver.cpp:396-397, resample(IntervalField) :378-385), init = c
+    g0, gf = ws[0].grid, ws[-1].grid
+    c0 = hj.ScalarField(g0, oracle.resample(c, g0))
+    db = ws[-1].dbounds()
+    lo = oracle.resample(hj.ScalarField(gf, db.lo(0).values()), g0)
+    hi = oracle.resample(hj.ScalarField(gf, db.hi(0).values()), g0)
+    r = oracle.solve(c0, c0, ws[-1].model, hj.IntervalField(g0, 1, lo=[lo], hi=[hi]), cfg)
+    _check("chain49_l0", "chain49", r, meta)
 
 
 # ------------------------------------------------------------------- GPU
