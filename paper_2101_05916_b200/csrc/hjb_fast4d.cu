@@ -522,16 +522,24 @@ __global__ void __launch_bounds__(MAXT, 1)
   // this one cooperative launch, separated by a grid barrier whose last
   // arriver runs the solve() epilogue; the ring positions carry over
   uint32_t ppos = 0, cpos = 0;
+  // The loop state's done flag is read ONCE per CTA: in the pipelined sharded
+  // loop the epilogue that sets it runs concurrently with this launch, and a
+  // per-thread read could split the CTA (some threads leave, the others wait
+  // on mbarriers for them forever)
+  __shared__ int s_quit;
   for (;;) {
+  if (threadIdx.x == 0) s_quit = (MS || a.loop != 0) ? *(volatile int*)&a.st->done : 0;
+  __syncthreads();
+  const bool quit = s_quit != 0;
   double* dst;
   const CUtensorMap* vmap;
   if (MS || a.loop == 1) {  // device loop: buffer parity from the loop state
-    if (*(volatile int*)&a.st->done) return;
+    if (quit) return;
     const long long it = *(volatile long long*)&a.st->iter;
     dst = (it & 1) ? a.buf0 : a.buf1;
     vmap = (it & 1) ? &a.map1 : &a.map0;
   } else {  // explicit buffers (single step, or a slab sweep of the sharded loop)
-    if (a.loop == 2 && *(volatile int*)&a.st->done) {
+    if (a.loop == 2 && quit) {
       signal_exit(a, a.st);
       return;
     }
@@ -1197,9 +1205,14 @@ template <class S, int R>
 __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_constant__ Ho4dArgs a) {
   constexpr int kK = 2;
   LoopState* st = a.st;
-  if (a.loop != 0 && *(volatile int*)&st->done) {
-    signal_exit(a, st);
-    return;
+  {  // done read once per CTA (see k_fast4d): the CTA leaves together
+    __shared__ int s_quit;
+    if (threadIdx.x == 0) s_quit = a.loop != 0 ? *(volatile int*)&st->done : 0;
+    __syncthreads();
+    if (s_quit) {
+      signal_exit(a, st);
+      return;
+    }
   }
   const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
@@ -1492,9 +1505,14 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
   constexpr int kK = KC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
-  if (a.loop != 0 && *(volatile int*)&st->done) {
-    signal_exit(a, st);
-    return;
+  {  // done read once per CTA (see k_fast4d): the CTA leaves together
+    __shared__ int s_quit;
+    if (threadIdx.x == 0) s_quit = a.loop != 0 ? *(volatile int*)&st->done : 0;
+    __syncthreads();
+    if (s_quit) {
+      signal_exit(a, st);
+      return;
+    }
   }
   const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
@@ -1961,9 +1979,14 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
   constexpr int R = 3, kK = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LoopState* st = a.st;
-  if (a.loop != 0 && *(volatile int*)&st->done) {
-    signal_exit(a, st);
-    return;
+  {  // done read once per CTA (see k_fast4d): the CTA leaves together
+    __shared__ int s_quit;
+    if (threadIdx.x == 0) s_quit = a.loop != 0 ? *(volatile int*)&st->done : 0;
+    __syncthreads();
+    if (s_quit) {
+      signal_exit(a, st);
+      return;
+    }
   }
   const long long it = a.loop == 0 ? 0 : (a.pmode ? (long long)a.parity : st->iter);
   const double* vn = a.loop == 0 ? a.xvn : ((it & 1) ? a.buf1 : a.buf0);
