@@ -345,7 +345,8 @@ class ModelSpec(C.Structure):
 class RefResult(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("dt", C.c_double), ("wall_seconds", C.c_double),
                 ("converged", C.c_int32), ("reserved", C.c_int32), ("nodes_per_sweep", C.c_int64),
-                ("residual_history", P(C.c_double)), ("history_capacity", C.c_int64)]
+                ("residual_history", P(C.c_double)), ("history_capacity", C.c_int64),
+                ("wall_ms_history", P(C.c_double))]
 
 
 def model_spec(model) -> ModelSpec:
@@ -438,8 +439,10 @@ class Reference:
         grid = init.grid()
         cap = int(cfg.max_iters)
         hist = np.zeros(max(cap, 1))
+        whist = np.zeros(max(cap, 1))
         r = RefResult()
         r.residual_history = hist.ctypes.data_as(P(C.c_double))
+        r.wall_ms_history = whist.ctypes.data_as(P(C.c_double))
         r.history_capacity = cap
         iv, cv = _vals(init), _vals(c)
         out = np.empty_like(iv)
@@ -449,7 +452,8 @@ class Reference:
         n = min(int(r.iterations), cap)
         return hj.SolveResult(value=hj.ScalarField(grid, out, check=False), iterations=int(r.iterations),
                               dt=r.dt, wall_seconds=r.wall_seconds, converged=bool(r.converged),
-                              residual_history=hist[:n].copy(), nodes_per_sweep=int(r.nodes_per_sweep))
+                              residual_history=hist[:n].copy(), wall_ms_history=whist[:n].copy(),
+                              nodes_per_sweep=int(r.nodes_per_sweep))
 
     def solve_coarse_to_fine(self, c_fine, model, db, coarse_grid, cfg, warm=None):
         """The reference's own ``solve_coarse_to_fine`` (solver.cpp:387-425).

@@ -188,6 +188,11 @@ void fill_result(const SolveResult& r, hjr_result* out) {
         std::min<std::size_t>(r.residual_history.size(), out->history_capacity);
     std::memcpy(out->residual_history, r.residual_history.data(), n * sizeof(double));
   }
+  if (out->wall_ms_history) {
+    const std::size_t n =
+        std::min<std::size_t>(r.wall_ms_history.size(), out->history_capacity);
+    std::memcpy(out->wall_ms_history, r.wall_ms_history.data(), n * sizeof(double));
+  }
 }
 
 template <typename Fn>

@@ -53,6 +53,7 @@ typedef struct hjr_result {
   int64_t nodes_per_sweep;
   double* residual_history;
   int64_t history_capacity;
+  double* wall_ms_history; /* may be NULL; history_capacity entries */
 } hjr_result;
 
 /* All return 0 on success, 1 std::invalid_argument, 2 std::runtime_error,
