@@ -458,6 +458,12 @@ static int fast4d_prepare_buffers(hjb_context* ctx, const DevGrid& g, Fast4dArgs
   return HJB_OK;
 }
 
+// grids whose solves run long enough to sit at the board's power cap: the
+// 4D sweep takes 448 threads and the per-plane constraint table there
+// (sustained A/B, profiles/round2_ab_sustained_101*.log: 481.5 us vs 526 us
+// per 101^4 sweep for the autotuner's short-run pick)
+constexpr uint32_t kSustainedCells = 50u << 20;
+
 int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* init,
                   const double* c, Fast4dArgs& f) {
   static std::mutex mu;
@@ -484,6 +490,10 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
   if (kc || mt) {
     const uint32_t k = (kc && std::atoi(kc) == 4) ? 4u : 2u;
     configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 576u));
+    return HJB_OK;
+  }
+  if (g.size >= kSustainedCells) {  // long, power-capped solves (see kSustainedCells)
+    configure(2, 448);
     return HJB_OK;
   }
   const F4Key key{{g.n[0], g.n[1], g.n[2], g.n[3]}, shape, ctx->device};
@@ -687,14 +697,17 @@ static int prepare_pv(hjb_context* ctx, const DevGrid& g, const HostModel& hm,
 }
 
 int hjb::constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c,
-                           const double** out) {
+                           const double** out, bool default_on) {
   *out = nullptr;
-  // opt-in (HJB_CPLANE=1): measured in interleaved best-of-4 runs, the
-  // per-node field is faster at 71^4 / 101^4 (118 vs 130 us, 436 vs 475 us)
-  // and equal in sustained power-capped runs, although the table saves a
-  // third of the DRAM bytes (the sweep then becomes issue-bound)
+  // HJB_CPLANE=1 / 0 forces it on / off.  Short cold runs favour the per-node
+  // field (71^4 / 101^4: 118 vs 130 us, 436 vs 475 us), but a long solve runs
+  // at the board's power cap, where the table's third fewer DRAM bytes win:
+  // 101^4 sustained 481.5 us (table, 448 threads) vs 526 us (field,
+  // profiles/round2_ab_sustained_101_b.log); 51^4 equal.  So the table is
+  // the default for large grids (default_on).
   const char* e = std::getenv("HJB_CPLANE");
-  if (!(e && std::strcmp(e, "1") == 0) || g.nd < 2) return HJB_OK;
+  const bool on = e ? std::strcmp(e, "1") == 0 : default_on;
+  if (!on || g.nd < 2) return HJB_OK;
   const uint32_t s0 = g.stride[0], n0 = g.n[0];
   CUDA_TRY(ctx->scratch.ensure(64 * sizeof(double)));
   unsigned int* flag = reinterpret_cast<unsigned int*>(ctx->scratch.d() + 48);
@@ -825,7 +838,9 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
       ++ctx->launches;
       f.target = ctx->tgbuf.d();
     }
-    if (!f.lf && !f.pv && !f.target && (rc = constraint_planes(ctx, g, c, &f.cplane))) return rc;
+    if (!f.lf && !f.pv && !f.target &&
+        (rc = constraint_planes(ctx, g, c, &f.cplane, g.size >= kSustainedCells)))
+      return rc;
     if (!f.cplane) {
       CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
       ++ctx->launches;

@@ -43,7 +43,8 @@ void fill_lf(const DevModel& m, int scheme, const double* galpha, Fast4dArgs& f)
 // When the constraint c (reference layout, device) varies along axis 0 only
 // (bit for bit), its per-plane values in ctx->cplane; else null.  Opt-in
 // (HJB_CPLANE=1): measured no faster than the per-node field.
-int constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c, const double** out);
+int constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c, const double** out,
+                      bool default_on = false);
 void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfParams& lp);
 // Device iteration loop: WHILE-conditional CUDA graph (or HJB_LOOP=poll);
 // `launch(stream, handle, use_handle)` enqueues one loop-mode sweep.

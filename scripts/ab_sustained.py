@@ -17,6 +17,13 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2101_05916_b200 import configs  # noqa: E402
 from paper_2101_05916_b200 import hjsafe as hj  # noqa: E402
 
+VARIANTS_B = {
+    "default (autotuned)": {},
+    "2 cells x 448": {"HJB_KCELLS": "2", "HJB_MAXT": "448"},
+    "cplane 2 x 576": {"HJB_CPLANE": "1", "HJB_KCELLS": "2", "HJB_MAXT": "576"},
+    "cplane 2 x 448": {"HJB_CPLANE": "1", "HJB_KCELLS": "2", "HJB_MAXT": "448"},
+    "cplane 4 x 384": {"HJB_CPLANE": "1", "HJB_KCELLS": "4"},
+}
 VARIANTS = {
     "default (autotuned)": {},
     "2 cells x 576": {"HJB_KCELLS": "2", "HJB_MAXT": "576"},
@@ -32,6 +39,7 @@ def main():
     ap.add_argument("--n", type=int, default=101)
     ap.add_argument("--sweeps", type=int, default=4000)
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--set", default="a", choices=["a", "b"])
     a = ap.parse_args()
     w = configs.config3(a.n)
     g = w.grid
@@ -42,9 +50,10 @@ def main():
     hj.signed_distance_band_dev(g, 0, -4.0, 4.0, c.data_ptr(), ctx=ctx)
     cfg = hj.SolveConfig(**w.cfg.__dict__)
     cfg.max_iters, cfg.tolerance = a.sweeps, 1e-30
-    res = {k: [] for k in VARIANTS}
+    variants = VARIANTS if a.set == "a" else VARIANTS_B
+    res = {k: [] for k in variants}
     for rnd in range(a.rounds):
-        for name, env in VARIANTS.items():
+        for name, env in variants.items():
             for k in ("HJB_KCELLS", "HJB_MAXT", "HJB_CPLANE", "HJB_PDL"):
                 os.environ.pop(k, None)
             os.environ.update(env)

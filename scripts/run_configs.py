@@ -2,12 +2,13 @@
 
 usage: python scripts/run_configs.py [cfg ...] [--max-iters N] [--json out.json]
                                      [--no-cpu]
-  cfg in {1, 2, 3, 3ho, 4, 5}; default: 1 2
+  cfg in {1, 2, 3, 3c, 3ho, 4, 5}; default: 1 2
 
 Config 1: 2D vertical subsystem 101^2 to convergence (tol 1e-4).
 Config 2: 4D planar 51^4 to convergence (tol 1e-4) or --max-iters.
 Config 3: 4D planar 101^4 (first-order reference scheme) to convergence or cap;
-          3ho: config 3's own scheme (ENO3 + TVD-RK3) to convergence through
+          3c: the same to convergence through the adaptive chain
+          26^4 -> 51^4 -> 101^4; 3ho: config 3's own scheme (ENO3 + TVD-RK3) through
           the adaptive chain 26^4 -> 51^4 -> 101^4.
 Config 4: decomposed 10D: 2D 101^2 + x/y 4D 71^4, cold at wind 0.5, warm 0.8,
           then 10 warm updates with seeded bounds, through the device-resident
@@ -196,6 +197,36 @@ def run_config5(max_iters, ctx, cpu):
     return out
 
 
+def run_config3_chain(max_iters, ctx, cpu):
+    """Config 3's grid with the reference scheme (first-order Godunov / Euler)
+    to a converged safe set at tol 1e-4, reached through the adaptive chain
+    26^4 -> 51^4 -> 101^4 (solve_coarse_to_fine generalised, as config 5 but
+    without obstacles, wind 0.5)."""
+    ws = [configs.config3(n) for n in (26, 51, 101)]
+    fine = ws[-1]
+    c = device_constraint(fine, ctx)
+    outs = [torch.empty(w.grid.size(), dtype=torch.float64, device="cuda") for w in ws]
+    cfg = hj.SolveConfig(**fine.cfg.__dict__)
+    cfg.max_iters = max_iters
+    torch.cuda.synchronize()
+    r = hj.solve_multilevel_dev([w.grid for w in ws], fine.model, fine.dbounds(), c.data_ptr(),
+                                cfg, out_ptrs=[o.data_ptr() for o in outs], ctx=ctx)
+    levels = []
+    for w, x, o in zip(ws, r.levels, outs):
+        d = dict(grid=str(w.grid.shape), **summarize(x, w.grid.size()))
+        d["safe_cells"] = int((o <= 0).sum().item())
+        if cpu:
+            per, n = ref_sweep_seconds(w)
+            d["reference_cpu_seconds_extrapolated"] = per * x.iterations
+        levels.append(d)
+    out = {"scheme": "first-order Godunov + Euler (reference)", "levels": levels,
+           "device_seconds_total": sum(x.wall_seconds for x in r.levels)}
+    if cpu:
+        out["reference_cpu_seconds_extrapolated_total"] = sum(
+            d["reference_cpu_seconds_extrapolated"] for d in levels)
+    return out
+
+
 def run_config3_ho(max_iters, ctx, tol):
     """Config 3's scheme to a converged safe set: ENO3 + TVD-RK3 (Godunov) on
     the config-2 model, 101^4, reached through the adaptive chain
@@ -246,6 +277,8 @@ def main():
             out["4"] = run_config4(a.max_iters, ctx, a.tol4, a.cpu)
         elif k == "5":
             out["5"] = run_config5(a.max_iters, ctx, a.cpu)
+        elif k == "3c":
+            out["3c"] = run_config3_chain(a.max_iters, ctx, a.cpu)
         elif k == "3ho":
             out["3ho"] = run_config3_ho(a.max_iters, ctx, a.tol3)
         print(f"config {k}: {time.perf_counter() - t0:.1f} s wall", flush=True)
