@@ -431,6 +431,7 @@ def run_single(args):
     traffic, traffic_src = traffic_for(args.n)
     sweep = statistics.mean(sweep_s)
     achieved = BYTES_PER_CELL * cells / sweep / 1e9
+    dram = traffic / sweep / 1e9 if traffic else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -439,8 +440,13 @@ def run_single(args):
         "sweeps_per_step": args.iters,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "kernel": "k_fast4d sweep (TMA plane ring; average device time per sweep over "
-                               "the timed region, launch gaps included)",
+                     "dram_gbs": dram, "dram_frac": dram / peak if dram else None,
+                     "kernel": ("k_fast4d sweep (TMA plane ring; average device time per sweep over "
+                                "the timed region, launch gaps included)" +
+                                ("; 448 threads, constraint read as one value per axis-0 plane "
+                                 "(it varies along x only, checked on the device), so the DRAM "
+                                 "bytes are ~16 per cell and the 24-byte algorithmic figure "
+                                 "(SURVEY 8d) exceeds them" if cells >= (16 << 20) else "")),
                      "bytes_per_cell": BYTES_PER_CELL, "algorithmic_bytes_per_sweep":
                          BYTES_PER_CELL * cells, "peak_source": peak_src,
                      "sweep_us": sweep * 1e6},

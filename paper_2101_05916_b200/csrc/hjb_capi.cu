@@ -460,9 +460,10 @@ static int fast4d_prepare_buffers(hjb_context* ctx, const DevGrid& g, Fast4dArgs
 
 // grids whose solves run long enough to sit at the board's power cap: the
 // 4D sweep takes 448 threads and the per-plane constraint table there
-// (sustained A/B, profiles/round2_ab_sustained_101*.log: 481.5 us vs 526 us
-// per 101^4 sweep for the autotuner's short-run pick)
-constexpr uint32_t kSustainedCells = 50u << 20;
+// (sustained A/B, profiles/round2_ab_sustained_*_b.log: 101^4 481.5 vs
+// 526 us, 71^4 123.5 vs 136.2 us per sweep for the autotuner's short-run
+// pick; 51^4 equal, so the autotuner keeps grids below ~16.8 M cells)
+constexpr uint32_t kSustainedCells = 16u << 20;
 
 int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* init,
                   const double* c, Fast4dArgs& f) {
@@ -702,9 +703,9 @@ int hjb::constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c,
   // HJB_CPLANE=1 / 0 forces it on / off.  Short cold runs favour the per-node
   // field (71^4 / 101^4: 118 vs 130 us, 436 vs 475 us), but a long solve runs
   // at the board's power cap, where the table's third fewer DRAM bytes win:
-  // 101^4 sustained 481.5 us (table, 448 threads) vs 526 us (field,
-  // profiles/round2_ab_sustained_101_b.log); 51^4 equal.  So the table is
-  // the default for large grids (default_on).
+  // 101^4 sustained 481.5 us (table, 448 threads) vs 526 us (field), 71^4
+  // 123.5 vs 136.2 us (profiles/round2_ab_sustained_*_b.log); 51^4 equal.
+  // So the table is the default for large grids (default_on).
   const char* e = std::getenv("HJB_CPLANE");
   const bool on = e ? std::strcmp(e, "1") == 0 : default_on;
   if (!on || g.nd < 2) return HJB_OK;
