@@ -463,8 +463,6 @@ static int fast4d_prepare_buffers(hjb_context* ctx, const DevGrid& g, Fast4dArgs
 // (sustained A/B, profiles/round2_ab_sustained_*_b.log: 101^4 481.5 vs
 // 526 us, 71^4 123.5 vs 136.2 us per sweep for the autotuner's short-run
 // pick; 51^4 equal, so the autotuner keeps grids below ~16.8 M cells)
-constexpr uint32_t kSustainedCells = 16u << 20;
-
 int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* init,
                   const double* c, Fast4dArgs& f) {
   static std::mutex mu;

@@ -102,7 +102,9 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
     CUDA_TRY(ho4d_pad(init, ctx->v0.d(), g.n[0], h4, ctx->stream));
     ++ctx->launches;
     int rcp;
-    if (h4.eno3g && !h4.lf && (rcp = constraint_planes(ctx, g, c, &h4.cplane))) return rcp;
+    if (h4.eno3g && !h4.lf &&
+        (rcp = constraint_planes(ctx, g, c, &h4.cplane, g.size >= kSustainedCells)))
+      return rcp;
     if (!h4.cplane) {
       CUDA_TRY(ho4d_pad(c, ctx->pcbuf.d(), g.n[0], h4, ctx->stream));
       ++ctx->launches;

@@ -45,6 +45,11 @@ void fill_lf(const DevModel& m, int scheme, const double* galpha, Fast4dArgs& f)
 // (HJB_CPLANE=1): measured no faster than the per-node field.
 int constraint_planes(hjb_context* ctx, const DevGrid& g, const double* c, const double** out,
                       bool default_on = false);
+// Grids whose solves run long enough to sit at the board's power cap (see
+// hjb_capi.cu, constraint_planes): 4D first-order sweeps take 448 threads
+// and, like the ENO3 stage (sustained 4441 vs 4575 us per 101^4 step,
+// profiles/round2_ab_eno3.log), the per-plane constraint table there.
+constexpr uint32_t kSustainedCells = 16u << 20;
 void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfParams& lp);
 // Device iteration loop: WHILE-conditional CUDA graph (or HJB_LOOP=poll);
 // `launch(stream, handle, use_handle)` enqueues one loop-mode sweep.
