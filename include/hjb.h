@@ -297,6 +297,14 @@ int hjb_field_negate_dev(hjb_context* ctx, int64_t n, const double* a, double* o
  * balanced slabs (the first n0 % nranks ranks own one extra plane). */
 typedef struct hjb_comm hjb_comm;
 int hjb_slab_partition(int64_t n0, int32_t nranks, int32_t rank, int64_t* begin, int64_t* end);
+/* The plan one rank runs (host only, no device needed): local geometry and
+ * the halo protocol, in LOCAL plane numbers of the rank's buffers.
+ * out[0..14] = {owned, nloc, cbeg, cend, global_begin,
+ *               send_lo, recv_lo, send_hi, recv_hi, halo_planes (R),
+ *               b0, e0, b1, e1 (boundary planes, swept first; b1 == e1: one
+ *               range), i0, i1 (interior)} -- 16 entries; halo entries are
+ * -1 on a side without a neighbour. */
+int hjb_slab_plan(int64_t n0, int32_t nranks, int32_t rank, int32_t halo, int64_t* out16);
 /* NCCL unique id (128 bytes) created on rank 0 and broadcast by the caller
  * (e.g. over torch.distributed); NCCL is loaded with dlopen. */
 int hjb_nccl_unique_id(void* out128);

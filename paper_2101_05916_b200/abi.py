@@ -162,6 +162,7 @@ SIGNATURES = [
     ("hjb_field_min_dev", _i, [_vp, _i64, _vp, _vp, _vp]),
     ("hjb_field_negate_dev", _i, [_vp, _i64, _vp, _vp]),
     ("hjb_slab_partition", _i, [_i64, _i32, _i32, P(_i64), P(_i64)]),
+    ("hjb_slab_plan", _i, [_i64, _i32, _i32, _i32, P(_i64)]),
     ("hjb_nccl_unique_id", _i, [_vp]),
     ("hjb_comm_create", _i, [_vp, _i32, _i32, _vp, P(_vp)]),
     ("hjb_comm_destroy", _i, [_vp]),

@@ -811,6 +811,22 @@ int hjb_slab_partition(int64_t n0, int32_t nranks, int32_t rank, int64_t* begin,
   return HJB_OK;
 }
 
+int hjb_slab_plan(int64_t n0, int32_t nranks, int32_t rank, int32_t halo, int64_t* o) {
+  if (!o || halo < 1) return set_err(HJB_ERR_INVALID_ARGUMENT, "slab_plan: bad arguments");
+  int64_t b, e;
+  int rc = hjb_slab_partition(n0, nranks, rank, &b, &e);
+  if (rc) return rc;
+  const SlabGeom g = slab_geom(static_cast<uint32_t>(n0), nranks, rank, static_cast<uint32_t>(halo));
+  const Halo h = halo_of(g);
+  const PlaneSplit x = plane_split(g);
+  const int64_t v[16] = {g.owned, g.nloc, g.cbeg, g.cend, g.gbeg,
+                         g.has_lo ? (int64_t)h.send_lo : -1, g.has_lo ? (int64_t)h.recv_lo : -1,
+                         g.has_hi ? (int64_t)h.send_hi : -1, g.has_hi ? (int64_t)h.recv_hi : -1,
+                         h.planes, x.b0, x.e0, x.b1, x.e1, x.i0, x.i1};
+  std::memcpy(o, v, sizeof v);
+  return HJB_OK;
+}
+
 int hjb_nccl_unique_id(void* out) {
   Nccl* api = nccl();
   if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
@@ -1085,6 +1101,7 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ls.e0, ls.e1);
   if ((rc = fill_result(ctx, ms, res))) return rc;
+  res->kernel = rk.ho ? HJB_KERNEL_HO4D : HJB_KERNEL_FAST4D;
   ctx->launches += per_pos * (res->iterations + 2 * body);
   const LoopState& st = *ctx->st_host;
   if ((rc = unpad_rank(rk, p, st.iter, value_slab_out, ctx->stream))) return rc;
@@ -1248,6 +1265,7 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ls.e0, ls.e1);
   if ((rc = fill_result(ctx, ms, res))) return rc;
+  res->kernel = rks[0].ho ? HJB_KERNEL_HO4D : HJB_KERNEL_FAST4D;
   ctx->launches += per_pos * (res->iterations + body);
   const LoopState& st = *ctx->st_host;
   for (int r = 0; r < P; ++r) {

@@ -53,6 +53,17 @@ def ho_stage_planes_dev(grid: hj.Grid, model: hj.DynamicsModel, dbounds: hj.Inte
     return mx.value
 
 
+def slab_plan(n0: int, nranks: int, rank: int, halo: int) -> dict:
+    """The per-rank plan of the sharded solve (hjb_slab_plan, host only):
+    local geometry, halo send/receive planes and the boundary/interior
+    split, in the rank's local plane numbers."""
+    out = (C.c_int64 * 16)()
+    hj._check(abi.load().hjb_slab_plan(n0, nranks, rank, halo, out))
+    keys = ["owned", "nloc", "cbeg", "cend", "global_begin", "send_lo", "recv_lo", "send_hi",
+            "recv_hi", "halo", "b0", "e0", "b1", "e1", "i0", "i1"]
+    return dict(zip(keys, list(out)))
+
+
 class Comm:
     """NCCL communicator of the library, bootstrapped over torch.distributed."""
 

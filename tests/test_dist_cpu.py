@@ -349,3 +349,49 @@ def test_plane_split_covers_slab():
             b, e, bnd, inner = _plan(n0, world, rank, R)
             planes = sorted(p for lo, hi in bnd + inner for p in range(lo, hi))
             assert planes == list(range(b, e))
+
+
+def _cpp_plan(n0, world, rank, R):
+    """hjb_slab_plan (the C++ the sharded drivers run) in global planes."""
+    from paper_2101_05916_b200.sharded import slab_plan
+    p = slab_plan(n0, world, rank, R)
+    gl = lambda x: x - p["cbeg"] + p["global_begin"]  # noqa: E731
+    bnd = [(gl(p["b0"]), gl(p["e0"]))] if p["e0"] > p["b0"] else []
+    if p["e1"] > p["b1"]:
+        bnd.append((gl(p["b1"]), gl(p["e1"])))
+    inner = [(gl(p["i0"]), gl(p["i1"]))] if p["i1"] > p["i0"] else []
+    return p, gl, bnd, inner
+
+
+@pytest.mark.parametrize("n0,world,R", [(101, 8, 1), (101, 8, 3), (11, 3, 3), (17, 4, 2),
+                                        (9, 2, 1), (51, 1, 2), (101, 2, 3), (12, 4, 3)])
+def test_cpp_slab_plan_matches_protocol(n0, world, R):
+    """The native per-rank plan (geometry, halo planes, boundary-first split)
+    is the one the CPU protocol tests above run: owned ranges tile the axis,
+    every halo a rank receives is exactly the planes its neighbour sends, the
+    planes a rank sends lie in its boundary ranges (swept before the
+    exchange starts), and boundary + interior tile the slab once."""
+    plans = [_cpp_plan(n0, world, r, R) for r in range(world)]
+    nxt = 0
+    for r, (p, gl, bnd, inner) in enumerate(plans):
+        b, e = slab_partition(n0, world, r)
+        assert (p["global_begin"], p["owned"]) == (b, e - b) and b == nxt
+        nxt = e
+        assert (p["cbeg"], p["cend"] - p["cbeg"]) == (R if r > 0 else 0, e - b)
+        assert p["nloc"] == p["owned"] + R * ((r > 0) + (r < world - 1)) and p["halo"] == R
+        planes = sorted(q for lo, hi in bnd + inner for q in range(lo, hi))
+        assert planes == list(range(b, e))
+        if world > 1:
+            assert sorted(bnd + inner) == sorted(_plan(n0, world, r, R)[2] + _plan(n0, world, r, R)[3])
+        sends = [p["send_lo"]] if r > 0 else []
+        sends += [p["send_hi"]] if r < world - 1 else []
+        for s in sends:  # the exchanged planes are produced by the boundary pass
+            assert all(any(lo <= gl(s + i) < hi for lo, hi in bnd) for i in range(R))
+        if r < world - 1:
+            q, gq = plans[r + 1][0], plans[r + 1][1]
+            assert [gl(p["send_hi"] + i) for i in range(R)] == [gq(q["recv_lo"] + i) for i in range(R)]
+            assert [gl(p["recv_hi"] + i) for i in range(R)] == [gq(q["send_lo"] + i) for i in range(R)]
+            assert p["recv_hi"] == p["cend"] and q["recv_lo"] == 0
+        else:
+            assert p["send_hi"] == p["recv_hi"] == -1
+    assert nxt == n0
