@@ -641,3 +641,57 @@ Reference.decomposition_batch = _reference_decomposition_batch
 
 def reference_available() -> bool:
     return REF_SO.exists()
+
+
+REF_GP_SO = HERE / "_ref" / "libhjref_gp.so"
+
+
+class ReferenceGp:
+    """oracle/_ref/libhjref_gp.so: the reference's own GpModel::predict and
+    bounds_on_grid (proj/src/gp.cpp:188-249), compiled in place behind
+    oracle/gp_shim.cpp.  The model's factor is pushed into the reference's
+    GpModel as given (its fit needs Eigen, absent here)."""
+
+    def __init__(self, path: os.PathLike | None = None, threads: int = 0):
+        p = Path(path) if path else REF_GP_SO
+        if not p.exists():
+            raise FileNotFoundError(f"{p} missing (build with `make -C oracle ref` where "
+                                    "/root/reference exists)")
+        self.lib = C.CDLL(str(p))
+        self.threads = threads
+        E = [C.c_char_p, C.c_int]
+        self.lib.hjr_gp_predict.argtypes = [P(abi.HjbGpModel), C.c_int64, _vp, _vp, _vp] + E
+        self.lib.hjr_gp_bounds_on_grid.argtypes = [P(abi.HjbGrid), C.c_int32, P(abi.HjbGpModel),
+                                                   _d, C.c_uint, P(_vp), P(_vp)] + E
+
+    @staticmethod
+    def _call(fn, *args):
+        buf = C.create_string_buffer(512)
+        rc = fn(*args, buf, 512)
+        if rc:
+            raise OracleError(rc, buf.value.decode())
+
+    def gp_predict(self, model, X):
+        """GpModel::predict per point: (mean, latent variance)."""
+        Xa = np.ascontiguousarray(np.asarray(X, dtype=np.float64)).reshape(-1, model.input_dim())
+        cm = model.to_c()
+        mean = np.empty(Xa.shape[0])
+        var = np.empty(Xa.shape[0])
+        self._call(self.lib.hjr_gp_predict, C.byref(cm), Xa.shape[0], _arr(Xa), _arr(mean),
+                   _arr(var))
+        return mean, var
+
+    def gp_bounds_on_grid(self, models, input_dims, grid, confidence=3.0):
+        """bounds_on_grid: (lo[ch][], hi[ch][])."""
+        nch = len(models)
+        arr = (abi.HjbGpModel * max(1, nch))()
+        for ch, (m, dims) in enumerate(zip(models, input_dims)):
+            arr[ch] = m.to_c(dims)
+        lo = [np.empty(grid.size()) for _ in range(nch)]
+        hi = [np.empty(grid.size()) for _ in range(nch)]
+        plo = (_vp * max(1, nch))(*[a.ctypes.data for a in lo])
+        phi = (_vp * max(1, nch))(*[a.ctypes.data for a in hi])
+        g = grid.to_c()
+        self._call(self.lib.hjr_gp_bounds_on_grid, C.byref(g), nch, arr, float(confidence),
+                   self.threads, plo, phi)
+        return lo, hi

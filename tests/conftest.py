@@ -36,6 +36,14 @@ def ref():
 
 
 @pytest.fixture(scope="session")
+def ref_gp():
+    from oracle.oracle import ReferenceGp, REF_GP_SO
+    if not REF_GP_SO.exists():
+        pytest.skip("oracle/_ref/libhjref_gp.so not built (needs /root/reference)")
+    return ReferenceGp()
+
+
+@pytest.fixture(scope="session")
 def gpu_ctx():
     from paper_2101_05916_b200 import hjsafe as hj
     return hj.Context(0)

@@ -85,3 +85,30 @@ def numpy_fit(X, y, cfg):
                 best, chosen = lml, hp
     L, alpha, lml = factor(chosen, xs, ys)
     return {"hp": chosen, "L": L, "alpha": alpha, "lml": lml}
+
+
+def fitted(n, seed, hp=None, dims=1):
+    X, y = bump_samples(n, 0.05, seed)
+    if dims > 1:
+        X = np.hstack([X] + [np.random.default_rng(seed + k).uniform(-1, 1, size=(n, 1))
+                             for k in range(dims - 1)])
+    hp = hp or hj.GpHyperparams(0.09, [0.4] * dims, 0.002)
+    return factor_model(hp, X, y)
+
+
+GRID_CASES = [
+    # (name, grid, models, input dims)
+    ("prior_1d", [(0.0, 3.0, 11)], lambda: [hj.GpModel.prior(hj.GpHyperparams(0.01, [1.0], 0.0))],
+     [[0]]),
+    ("one_point", [(0.0, 2.0, 5)],
+     lambda: [factor_model(hj.GpHyperparams(0.04, [0.5], 0.0), [[1.0]], [1.0])], [[0]]),
+    ("bump60_2d", [(-2.0, 2.0, 41), (-1.0, 1.0, 9)], lambda: [fitted(60, 3)], [[0]]),
+    ("bump300_4d_x", [(-2.0, 2.0, 13), (-2.0, 2.0, 7), (-0.35, 0.35, 5), (-1.5, 1.5, 6)],
+     lambda: [fitted(300, 101)], [[0]]),
+    ("two_dims", [(-2.0, 2.0, 9), (-1.0, 1.0, 5), (-1.0, 1.0, 7)], lambda: [fitted(80, 9, dims=2)],
+     [[0, 2]]),
+    ("repeated_axis", [(-2.0, 2.0, 9), (-1.0, 1.0, 5)], lambda: [fitted(50, 5, dims=2)], [[1, 1]]),
+    ("two_channels", [(-2.0, 2.0, 11), (-1.0, 1.0, 6)],
+     lambda: [fitted(40, 1), fitted(70, 2)], [[0], [1]]),
+    ("n1100_R2", [(-2.0, 2.0, 17), (-1.0, 1.0, 3)], lambda: [fitted(1100, 8)], [[0]]),
+]

@@ -10,36 +10,9 @@ from paper_2101_05916_b200 import configs
 from paper_2101_05916_b200 import hjsafe as hj
 
 from cases import band_np, same
-from gp_cases import bump_samples, factor_model
+from gp_cases import GRID_CASES as CASES, bump_samples, factor_model, fitted as _fitted
 
 pytestmark = pytest.mark.gpu
-
-
-def _fitted(n, seed, hp=None, dims=1):
-    X, y = bump_samples(n, 0.05, seed)
-    if dims > 1:
-        X = np.hstack([X] + [np.random.default_rng(seed + k).uniform(-1, 1, size=(n, 1))
-                             for k in range(dims - 1)])
-    hp = hp or hj.GpHyperparams(0.09, [0.4] * dims, 0.002)
-    return factor_model(hp, X, y)
-
-
-CASES = [
-    # (name, grid, models, input dims)
-    ("prior_1d", [(0.0, 3.0, 11)], lambda: [hj.GpModel.prior(hj.GpHyperparams(0.01, [1.0], 0.0))],
-     [[0]]),
-    ("one_point", [(0.0, 2.0, 5)],
-     lambda: [factor_model(hj.GpHyperparams(0.04, [0.5], 0.0), [[1.0]], [1.0])], [[0]]),
-    ("bump60_2d", [(-2.0, 2.0, 41), (-1.0, 1.0, 9)], lambda: [_fitted(60, 3)], [[0]]),
-    ("bump300_4d_x", [(-2.0, 2.0, 13), (-2.0, 2.0, 7), (-0.35, 0.35, 5), (-1.5, 1.5, 6)],
-     lambda: [_fitted(300, 101)], [[0]]),
-    ("two_dims", [(-2.0, 2.0, 9), (-1.0, 1.0, 5), (-1.0, 1.0, 7)], lambda: [_fitted(80, 9, dims=2)],
-     [[0, 2]]),
-    ("repeated_axis", [(-2.0, 2.0, 9), (-1.0, 1.0, 5)], lambda: [_fitted(50, 5, dims=2)], [[1, 1]]),
-    ("two_channels", [(-2.0, 2.0, 11), (-1.0, 1.0, 6)],
-     lambda: [_fitted(40, 1), _fitted(70, 2)], [[0], [1]]),
-    ("n1100_R2", [(-2.0, 2.0, 17), (-1.0, 1.0, 3)], lambda: [_fitted(1100, 8)], [[0]]),
-]
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -52,6 +25,47 @@ def test_bounds_on_grid_matches_oracle(gpu_ctx, oracle, case):
     for ch in range(len(models)):
         assert same(got.lo(ch).values(), want_lo[ch])
         assert same(got.hi(ch).values(), want_hi[ch])
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_bounds_on_grid_matches_reference(gpu_ctx, ref_gp, case):
+    """The device kernels against the REFERENCE's own bounds_on_grid
+    (gp.cpp:211-249 via oracle/_ref/libhjref_gp.so), bitwise."""
+    _, dims, mk, idims = case
+    g = hj.Grid(dims)
+    models = mk()
+    want_lo, want_hi = ref_gp.gp_bounds_on_grid(models, idims, g, confidence=3.0)
+    got = hj.bounds_on_grid(models, idims, g, 3.0, ctx=gpu_ctx)
+    for ch in range(len(models)):
+        assert same(got.lo(ch).values(), want_lo[ch])
+        assert same(got.hi(ch).values(), want_hi[ch])
+
+
+def test_predict_and_fit_through_reference(gpu_ctx, ref_gp):
+    """Product host fit -> device predict_batch / bounds vs the reference's
+    predict and bounds_on_grid on the same factor; hyperparameter errors
+    carry the reference's messages."""
+    X, y = bump_samples(250, 0.05, 33)
+    data = [hj.DisturbanceMeasurement([float(a)], float(b)) for a, b in zip(X[:, 0], y)]
+    m = hj.GpModel.fit(data, hj.GpConfig())
+    Q = np.random.default_rng(4).uniform(-3, 3, size=(300, 1))
+    want = ref_gp.gp_predict(m, Q)
+    got = m.predict_batch(Q, ctx=gpu_ctx)
+    assert same(np.asarray(got[0]), want[0]) and same(np.asarray(got[1]), want[1])
+    g = configs.planar_grid(21)
+    want_lo, want_hi = ref_gp.gp_bounds_on_grid([m], [[0]], g, 3.0)
+    b = hj.bounds_on_grid([m], [[0]], g, 3.0, ctx=gpu_ctx)
+    assert same(b.lo(0).values(), want_lo[0]) and same(b.hi(0).values(), want_hi[0])
+    from oracle.oracle import OracleError
+    for hp, msg in ((hj.GpHyperparams(-1.0, [1.0], 0.0), "GP: signal variance must be > 0"),
+                    (hj.GpHyperparams(1.0, [1.0], -1.0), "GP: noise variance must be >= 0"),
+                    (hj.GpHyperparams(1.0, [0.0], 0.0), "GP: lengthscales must be > 0")):
+        bad = hj.GpModel.prior(hj.GpHyperparams(1.0, [1.0], 0.0))
+        bad._hp = hp
+        with pytest.raises(OracleError, match=msg):
+            ref_gp.gp_bounds_on_grid([bad], [[0]], g)
+        with pytest.raises(hj.InvalidArgument, match=msg):
+            hj.bounds_on_grid([bad], [[0]], g, ctx=gpu_ctx)
 
 
 def test_bounds_on_grid_dev_into_torch(gpu_ctx, oracle):
