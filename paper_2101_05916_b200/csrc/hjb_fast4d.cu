@@ -1962,6 +1962,29 @@ __device__ __forceinline__ void eno3_face(double e0, double e1, double e2, doubl
   dm_right = (e2 + hc) + (left ? kHoThird : kHoSixthNeg) * c3;
 }
 
+// Only the upwind one of eno3_face's two results (a linear row's Godunov flux
+// uses D+ of cell k (up) or D- of cell k+1): sg = 0x80000000 (up) or 0 flips
+// the sign of hc = 0.5 * c2, so e2 + hc' is exactly e2 - hc or e2 + hc
+// (x - y == x + (-y) in IEEE arithmetic), and the weight of c3 is the one
+// eno3_face gives that result.
+__device__ __forceinline__ double eno3_upwind(double e0, double e1, double e2, double e3,
+                                              double e4, bool up, uint32_t sg) {
+  const double g0 = e1 - e0, g1 = e2 - e1, g2 = e3 - e2, g3 = e4 - e3;
+  const double h0 = g1 - g0, h1 = g2 - g1, h2 = g3 - g2;
+  const bool left = fabs(g1) <= fabs(g2);
+  const double c2 = left ? g1 : g2;
+  const double c3 = minabs_d(left ? h0 : h1, left ? h1 : h2);
+  const double hc = 0.5 * c2;
+  const double hcs = __hiloint2double(__double2hiint(hc) ^ (int)sg, __double2loint(hc));
+  return (e2 + hcs) + (left == up ? kHoSixthNeg : kHoThird) * c3;
+}
+
+// k_eno3g's axis-0 march state at plane j (see k_eno3g): V(j+2), a(j),
+// a(j+1), G(j-1), G(j), H(j-1), M(j-2) and D- of plane j
+struct Ax0March {
+  double vl, a0, a1, g0, g1, h, m, dm;
+};
+
 #ifndef HJB_ENO3G_THREADS
 #define HJB_ENO3G_THREADS 512
 #endif
@@ -2035,7 +2058,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
       for (uint32_t q = 0; c0 + q < c1; ++q) {
         const uint32_t sl = q % ring, use = q / ring;
         const uint32_t dst0 = smem0 + sl * a.vslot_bytes, bar = bars + sl * 8;
-        const int p = (int)(c0 + q), pa = min(p + 4, (int)n0 - 1);
+        const int p = (int)(c0 + q), pa = min(p + 3, (int)n0 - 1);
         mbar_wait(bars + (ring + sl) * 8, (use & 1u) ^ 1u);
         mbar_arrive_expect_tx(
             bar, a.vbox_bytes + ((need_vn ? 2u : 1u) + (CP ? 0u : 1u)) * a.tbox_bytes);
@@ -2130,11 +2153,15 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
     // linear rows 1, 2: start of the upwind six-value window (byte offset in
     // the box; D+ uses V(i-2 .. i+3), D- V(i-3 .. i+2))
     uint32_t uoff[3][kK];
+    uint32_t hsg[3][kK];  // eno3_upwind: sign flip of hc for D+
 #pragma unroll
     for (int d = 1; d <= 2; ++d) {
       const int step = d == 1 ? (int)(W2 * rowb) : (int)rowb;
 #pragma unroll
-      for (int c = 0; c < kK; ++c) uoff[d][c] = own + 8u * c + (uint32_t)((up[d][c] ? -2 : -3) * step);
+      for (int c = 0; c < kK; ++c) {
+        uoff[d][c] = own + 8u * c + (uint32_t)((up[d][c] ? -2 : -3) * step);
+        hsg[d][c] = up[d][c] ? 0x80000000u : 0u;
+      }
     }
     auto flux = [&](auto dc, int c, double dm, double dp) -> double {
       constexpr int d = decltype(dc)::value;
@@ -2144,28 +2171,38 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
       return shape_pick(shp[d][c], ka, kb);
     };
 
-    // axis-0 window: faces a(i0-2) .. a(i0+2), V(i0+3), and D- of plane i0
-    // (chosen at face a(i0-1) in the previous step); planes clamped to the grid
+    // axis-0 march state of plane j (Ax0March): with faces a(k) = (V(k+1) -
+    // V(k)) * inv0, G(k) = a(k+1) - a(k), H(k) = G(k+1) - G(k) and M(k) =
+    // minabs(H(k), H(k+1)) — the operands eno3_face forms on a(j-2) .. a(j+2)
+    // — the choice at face j needs a(j), G(j-1), G(j), M(j-2) and M(j-1),
+    // of which only G(j+1), H(j) and M(j-1) are new: every difference and the
+    // pair minimum are formed once per face instead of once per choice.
+    // Planes are clamped to the grid.
     auto plane_at = [&](int p) -> const double* {
       p = p < 0 ? 0 : (p > (int)n0 - 1 ? (int)n0 - 1 : p);
       return vs + (uint64_t)p * s0 + rowo;
     };
-    double F[5][kK], vlast[kK], dmc[kK];
+    Ax0March sa[kK];
     {
-      double w[7][kK];
+      double w[6][kK];
 #pragma unroll
-      for (int q = 0; q < 7; ++q) ldg_k<kK>(plane_at((int)c0 - 3 + q), w[q]);
+      for (int q = 0; q < 6; ++q) ldg_k<kK>(plane_at((int)c0 - 3 + q), w[q]);
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
-        double f6[6];
+        double f[5];  // a(c0-3) .. a(c0+1)
 #pragma unroll
-        for (int q = 0; q < 6; ++q) f6[q] = (w[q + 1][c] - w[q][c]) * inv0;
-        if (SCH != 0) lf_ghost<6>(f6, (int)c0 - 3, (int)n0 - 2);
+        for (int q = 0; q < 5; ++q) f[q] = (w[q + 1][c] - w[q][c]) * inv0;
+        if (SCH != 0) lf_ghost<5>(f, (int)c0 - 3, (int)n0 - 2);
         double unused;
-        eno3_face(f6[0], f6[1], f6[2], f6[3], f6[4], unused, dmc[c]);
-#pragma unroll
-        for (int q = 0; q < 5; ++q) F[q][c] = f6[q + 1];
-        vlast[c] = w[6][c];
+        eno3_face(f[0], f[1], f[2], f[3], f[4], unused, sa[c].dm);
+        const double gm2 = f[2] - f[1], gm1 = f[3] - f[2], g0 = f[4] - f[3];
+        sa[c].vl = w[5][c];
+        sa[c].a0 = f[3];
+        sa[c].a1 = f[4];
+        sa[c].g0 = gm1;
+        sa[c].g1 = g0;
+        sa[c].h = g0 - gm1;
+        sa[c].m = minabs_d(gm1 - gm2, sa[c].h);
       }
     }
     const bool need_vn = a.kind != 0 || a.final_stage;
@@ -2175,10 +2212,14 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
     const bool gl1 = i1 == 0, gh1 = i1 + 1 == n1, gl2 = i2 == 0, gh2 = i2 + 1 == n2;
     const bool any_ghost = active && (gl3 || gh3 || gl1 || gh1 || gl2 || gh2);
     uint32_t sl = 0, ph = 0;
-    for (uint32_t i0 = c0; i0 < c1; ++i0) {
+    // one plane: the march state goes from plane i0 to plane i0 + 1 in place
+    // (every field of a cell's state is read before any is written)
+    auto plane = [&](const uint32_t i0, Ax0March(&ms)[kK]) {
       const uint64_t po = (uint64_t)i0 * s0;
       const uint32_t slot = smem0 + sl * a.vslot_bytes;
       mbar_wait_nc(bars + sl * 8, ph);
+      double vnx[kK];  // stage input of plane i0 + 3 (clamped)
+      lds_k<kK>(slot + town + 2 * a.tbox_slot, vnx);
       // own row V(i3-3) .. V(i3+4)
       double rv[8];
       rv[0] = lds1(slot + own - 24);
@@ -2194,18 +2235,37 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
       rv[7] = lds1(slot + own + 32);
       double hh[kK];
       double dmv[4][kK], dpv[4][kK];  // Lax-Friedrichs: all pairs of the cell
-      // axis 0: choice at face a(i0) -> D+ of i0 and D- of i0+1
+      // axis 0: choice at face a(i0) -> D+ of i0 and D- of i0+1 (the
+      // operations of eno3_face on a(i0-2) .. a(i0+2), see Ax0March)
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
-        double dp, dmn;
-        eno3_face(F[0][c], F[1][c], F[2][c], F[3][c], F[4][c], dp, dmn);
+        const Ax0March s = ms[c];
+        double af = (vnx[c] - s.vl) * inv0;                 // a(i0+2)
+        if (SCH != 0 && i0 + 2 > n0 - 2) af = s.a1;         // LF: face past the edge
+        const double gn = af - s.a1;                         // G(i0+1)
+        const double hn = gn - s.g1;                         // H(i0)
+        const double mn = minabs_d(s.h, hn);                 // M(i0-1)
+        const bool left = fabs(s.g0) <= fabs(s.g1);
+        const double c2 = left ? s.g0 : s.g1;
+        const double c3 = left ? s.m : mn;
+        const double hc = 0.5 * c2;
+        const double dp = (s.a0 - hc) + (left ? kHoSixthNeg : kHoThird) * c3;
+        const double dmn = (s.a0 + hc) + (left ? kHoThird : kHoSixthNeg) * c3;
         if (SCH == 0) {
-          hh[c] = flux(std::integral_constant<int, 0>{}, c, dmc[c], dp);
+          hh[c] = flux(std::integral_constant<int, 0>{}, c, s.dm, dp);
         } else {
-          dmv[0][c] = dmc[c];
+          dmv[0][c] = s.dm;
           dpv[0][c] = dp;
         }
-        dmc[c] = dmn;
+        Ax0March& t = ms[c];
+        t.vl = vnx[c];
+        t.a0 = s.a1;
+        t.a1 = af;
+        t.g0 = s.g1;
+        t.g1 = gn;
+        t.h = hn;
+        t.m = mn;
+        t.dm = dmn;
       }
       // axes 1 and 2: per cell, six faces from the box
       auto axis12 = [&](auto axc) {
@@ -2232,9 +2292,8 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
             double e[5];
 #pragma unroll
             for (int q = 0; q < 5; ++q) e[q] = (w6[q + 1][c] - w6[q][c]) * inv;
-            double dpl, dmr;
-            eno3_face(e[0], e[1], e[2], e[3], e[4], dpl, dmr);
-            hh[c] = hh[c] + pos_[ax][c] * (up[ax][c] ? dpl : dmr);
+            hh[c] = hh[c] + pos_[ax][c] * eno3_upwind(e[0], e[1], e[2], e[3], e[4], up[ax][c],
+                                                      hsg[ax][c]);
           }
         } else {
           double nv[7][kK];
@@ -2299,7 +2358,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
           }
         }
       }
-      double ccv[kK], vnv[kK], vnx[kK];
+      double ccv[kK], vnv[kK];
       if (CP) {  // constraint per plane (Ho4dArgs::cplane)
         ccv[0] = ccv[1] = __ldg(a.cplane + i0);
       } else {
@@ -2310,7 +2369,6 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
       } else {
         vnv[0] = vnv[1] = 0.0;
       }
-      lds_k<kK>(slot + town + 2 * a.tbox_slot, vnx);
       __syncwarp();
       if (lane == 0) mbar_arrive(bars + (ring + sl) * 8);
       if (++sl == ring) {
@@ -2359,15 +2417,8 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
           }
         }
       }
-#pragma unroll
-      for (int c = 0; c < kK; ++c) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) F[q][c] = F[q + 1][c];
-        F[4][c] = (vnx[c] - vlast[c]) * inv0;
-        if (SCH != 0 && i0 + 3 > n0 - 2) F[4][c] = F[3][c];  // face a(i0+3) past the edge
-        vlast[c] = vnx[c];
-      }
-    }
+    };
+    for (uint32_t i0 = c0; i0 < c1; ++i0) plane(i0, sa);
     if (a.signal) signal_item(a, st, c0, lane);
   }
   if (!a.final_stage) return;
