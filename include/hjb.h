@@ -166,6 +166,7 @@ typedef struct hjb_solve_config {
 #define HJB_KERNEL_HO_GENERIC 5    /* k_ho_stage (ENO / TVD-RK, rank 1..4) */
 #define HJB_KERNEL_HO4D 6          /* k_ho4t / k_eno3g / k_ho4d */
 #define HJB_KERNEL_SMALL2D_HO 7    /* k_small2d_ho */
+#define HJB_KERNEL_FAST4D_GEN 8    /* k_fast4d<ShapeGen>: run-time row shapes, one launch per sweep */
 
 /* SolveResult, reference solver.hpp:27-36.  The value field is written to
  * the caller's buffer; histories are written to caller buffers of

@@ -400,6 +400,7 @@ void fill_tables(const Prepared& p, Fast4dArgs& f) {
     f.off_a[d] = p.hm.dm.row[d].off_a;
     f.off_b[d] = p.hm.dm.row[d].off_b;
   }
+  fast4d_gen_rows(p.hm.dm, f);
 }
 
 // Lax-Friedrichs fields of the 4D fast path: per-row drift tables, input
@@ -487,7 +488,7 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
     return HJB_OK;
   }
   if (kc || mt) {
-    const uint32_t k = (kc && std::atoi(kc) == 4) ? 4u : 2u;
+    const uint32_t k = (kc && std::atoi(kc) == 4 && shape != kShapeGen) ? 4u : 2u;
     configure(k, k == 4 ? 384u : ((mt && std::atoi(mt) == 448) ? 448u : 576u));
     return HJB_OK;
   }
@@ -516,6 +517,7 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
     }
   }
   const uint32_t cands[3][2] = {{2, 576}, {2, 448}, {4, 384}};
+  const int ncands = shape == kShapeGen ? 2 : 3;  // run-time shape: 2-cell pencils only
   CUDA_TRY(cudaMemsetAsync(ctx->st, 0, sizeof(LoopState), ctx->stream));  // fresh counters
   float best = 1e30f;
   uint32_t bk = 2, bt = 576;
@@ -523,7 +525,8 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   const uint64_t rows = static_cast<uint64_t>(g.n[0]) * g.n[1] * g.n[2];
-  for (const auto& cd : cands) {
+  for (int ci = 0; ci < ncands; ++ci) {
+    const uint32_t* cd = cands[ci];
     configure(cd[0], cd[1]);
     CUDA_TRY(launch_pad4(init, ctx->v2.d(), rows, g.n[3], f.n3p, ctx->stream));
     CUDA_TRY(launch_pad4(c, ctx->pcbuf.d(), rows, g.n[3], f.n3p, ctx->stream));
@@ -789,6 +792,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   // target set: the 4D fast path's TG variant (Godunov, constant bounds);
   // everything else runs the generic sweep
   if (cfg->target && scheme_of(cfg) != kGodunov) shape = -1;
+  if (cfg->target && shape == kShapeGen) shape = -1;  // no TG variant of the run-time shape
   const int shape_pv = (shape < 0 && fast_enabled() && db->per_node &&
                         scheme_of(cfg) == kGodunov && !cfg->target)
                            ? fast4d_shape_pv(g, hm.dm)
@@ -822,6 +826,7 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
         f.off_a[d] = hm.dm.row[d].off_a;
         f.off_b[d] = hm.dm.row[d].off_b;
       }
+      fast4d_gen_rows(hm.dm, f);
     }
     f.st = ctx->st;
     f.dt = dt;
@@ -933,7 +938,9 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   ctx->launches += (small2d || multi) ? 1 : st.iter + body;  // sweeps (+ early-exit tail of the body)
   res->kernel = small2d ? HJB_KERNEL_SMALL2D
                         : (multi ? HJB_KERNEL_FAST4D_MULTI
-                                 : (shape >= 0 ? HJB_KERNEL_FAST4D : HJB_KERNEL_GENERIC));
+                                 : (shape == kShapeGen ? HJB_KERNEL_FAST4D_GEN
+                                                       : (shape >= 0 ? HJB_KERNEL_FAST4D
+                                                                     : HJB_KERNEL_GENERIC)));
   res->iterations = st.iter;
   res->converged = st.converged;
   res->final_residual = st.last_residual;

@@ -42,6 +42,22 @@ struct FastDiv {
   }
 };
 
+// godunov_flux (solver.cpp:44-63), the reference's Godunov numerical flux of
+// one axis from the row's slopes and the one-sided differences
+__device__ __forceinline__ double godunov_flux(double pos, double neg, double dminus,
+                                               double dplus) {
+  const double ha = dminus > 0.0 ? pos * dminus : neg * dminus;
+  const double hb = dplus > 0.0 ? pos * dplus : neg * dplus;
+  if (dminus <= dplus) {
+    double h = ha > hb ? ha : hb;
+    if (dminus <= 0.0 && 0.0 <= dplus && h < 0.0) h = 0.0;
+    return h;
+  }
+  double h = ha < hb ? ha : hb;
+  if (dplus <= 0.0 && 0.0 <= dminus && h > 0.0) h = 0.0;
+  return h;
+}
+
 // Grid as the kernels see it: reference Grid (grid.hpp:23-48), strides last
 // axis fastest, 1/spacing computed on the host (solver.cpp:208-209).
 struct DevGrid {

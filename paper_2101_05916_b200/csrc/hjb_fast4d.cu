@@ -54,6 +54,7 @@ __device__ __forceinline__ bool sign_clear(double x) { return __double2hiint(x) 
 // U(d) / D(d): the control / disturbance channel entering row d (at most one
 // each in these models; -1 none) — the Lax-Friedrichs variant's inputs.
 struct ShapePlanarD0 {  // BASELINE planar 4D, wind on row 0: rows x1 | tan x2 | x2 + x3 | x2
+  static constexpr bool GEN = false;
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : 2; }
   __host__ __device__ static constexpr int B(int d) { return d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr bool LIN(int d) { return d == 1 || d == 2; }
@@ -61,6 +62,7 @@ struct ShapePlanarD0 {  // BASELINE planar 4D, wind on row 0: rows x1 | tan x2 |
   __host__ __device__ static constexpr int D(int d) { return d == 0 ? 0 : -1; }
 };
 struct ShapePlanarD1 {  // stock NearHoverPlanar4D, wind on row 1
+  static constexpr bool GEN = false;
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : 2; }
   __host__ __device__ static constexpr int B(int d) { return d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr bool LIN(int d) { return d == 0 || d == 2; }
@@ -68,11 +70,26 @@ struct ShapePlanarD1 {  // stock NearHoverPlanar4D, wind on row 1
   __host__ __device__ static constexpr int D(int d) { return d == 1 ? 0 : -1; }
 };
 struct ShapeTwin {  // TwinDoubleIntegrator rows: x1 | const | x3 | const
+  static constexpr bool GEN = false;
   __host__ __device__ static constexpr int A(int d) { return d == 0 ? 1 : d == 2 ? 3 : -1; }
   __host__ __device__ static constexpr int B(int) { return -1; }
   __host__ __device__ static constexpr bool LIN(int d) { return d == 0 || d == 2; }
   __host__ __device__ static constexpr int U(int d) { return d == 1 ? 0 : d == 3 ? 1 : -1; }
   __host__ __device__ static constexpr int D(int d) { return d == 1 ? 0 : d == 3 ? 1 : -1; }
+};
+
+// Run-time row shapes (any other admissible model, kShapeGen): every row is
+// treated as varying per cell (A = 3) and non-linear, its table axes come
+// from Fast4dArgs::gax / gbx, and the flux is the reference's godunov_flux
+// on the row's (pos, neg) — no slope-shape specialisation, both neighbours
+// of every axis read.  Godunov, constant bounds only (no LF / PV / target).
+struct ShapeGen {
+  static constexpr bool GEN = true;
+  __host__ __device__ static constexpr int A(int) { return 3; }
+  __host__ __device__ static constexpr int B(int) { return -1; }
+  __host__ __device__ static constexpr bool LIN(int) { return false; }
+  __host__ __device__ static constexpr int U(int) { return -1; }
+  __host__ __device__ static constexpr int D(int) { return -1; }
 };
 
 template <class S>
@@ -677,6 +694,25 @@ __global__ void __launch_bounds__(MAXT, 1)
       // loop-invariant slopes (row d, cell c); rows that do not vary along x3
       // hold one pair for the whole pencil
       double pos_[4][kK], neg_[4][kK];
+      if constexpr (S::GEN) {  // run-time row axes (Fast4dArgs::gax / gbx)
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            const uint32_t i3c = min(i3 + c, n3 - 1);
+            const uint32_t ka = active ? pick<S>(a.gax[d], i1, i2, i3c) : 0u;
+            if (a.gbx[d] < 0) {
+              pos_[d][c] = tabs[a.off_pos[d] + ka];
+              neg_[d][c] = tabs[a.off_neg[d] + ka];
+            } else {
+              const uint32_t kb = active ? pick<S>(a.gbx[d], i1, i2, i3c) : 0u;
+              const double dr = tabs[a.off_a[d] + ka] + tabs[a.off_b[d] + kb];
+              pos_[d][c] = dr;
+              neg_[d][c] = dr;
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int d = 0; d < 4; ++d) {
         const bool per_cell = S::A(d) == 3 || S::B(d) == 3;
@@ -698,6 +734,7 @@ __global__ void __launch_bounds__(MAXT, 1)
             }
           }
         }
+      }
       }
       // Linear rows (pos == neg == s: no input on the row): the Godunov flux
       // of H(p) = s p is s * D+ for s >= 0 and s * D- otherwise
@@ -795,7 +832,8 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
         dm0[c] = (v[c] - vp[c]) * inv0;
-        ka0[c] = (SCH != 0 || S::LIN(0)) ? 0.0 : pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
+        ka0[c] = (SCH != 0 || S::LIN(0) || S::GEN) ? 0.0
+                                                   : pair_kink(shp[0][c].L, dm0[c], sign_bit(dm0[c]));
       }
 
       // per-node bounds: this pencil's lo / hi of each disturbance row's
@@ -908,7 +946,12 @@ __global__ void __launch_bounds__(MAXT, 1)
         double f3[kK + 1];
         f3[0] = (v[0] - vl) * inv3;
 #pragma unroll
-        for (int c = 1; c < kK; ++c) f3[c] = (v[c] - v[c - 1]) * inv3m[c];
+        for (int c = 1; c < kK; ++c) {
+          if constexpr (S::GEN)  // the reference's ghost D+ of the last cell: +0.0
+            f3[c] = i3 + c < n3 ? (v[c] - v[c - 1]) * inv3 : 0.0;
+          else
+            f3[c] = (v[c] - v[c - 1]) * inv3m[c];
+        }
         f3[kK] = (vr - v[kK - 1]) * inv3;
         // (per-node bounds: a disturbance row's slopes vary along x3)
         constexpr bool row3_shared = !(S::A(3) == 3 || S::B(3) == 3) && !(PV == 2 && S::D(3) >= 0);
@@ -956,6 +999,24 @@ __global__ void __launch_bounds__(MAXT, 1)
             const double hh = lf_hhat<S>(a.lp, dmv, dpv, drc, alc);
             double st = v[c] + a.dt * hh;
             if (TG) st = tl[c] < st ? tl[c] : st;
+            out[c] = st > cc[c] ? st : cc[c];
+            const double dv = fabs(out[c] - v[c]);
+            if (valid[c] && dv > mdv) mdv = dv;
+            continue;
+          }
+          if constexpr (S::GEN) {
+            // update_chunk (solver.cpp:106-190) term by term: hhat = 0.0,
+            // += godunov_flux of each axis in order, stepped = v + dt*hhat
+            const double dp0 = (vn[c] - v[c]) * inv0;
+            const double dm1 = (v[c] - n1m[c]) * inv1, dp1 = (n1p[c] - v[c]) * inv1;
+            const double dm2 = (v[c] - n2m[c]) * inv2, dp2 = (n2p[c] - v[c]) * inv2;
+            double hh = 0.0;
+            hh += godunov_flux(pos_[0][c], neg_[0][c], dm0[c], dp0);
+            hh += godunov_flux(pos_[1][c], neg_[1][c], dm1, dp1);
+            hh += godunov_flux(pos_[2][c], neg_[2][c], dm2, dp2);
+            hh += godunov_flux(pos_[3][c], neg_[3][c], f3[c], f3[c + 1]);
+            dm0[c] = dp0;
+            const double st = v[c] + a.dt * hh;
             out[c] = st > cc[c] ? st : cc[c];
             const double dv = fabs(out[c] - v[c]);
             if (valid[c] && dv > mdv) mdv = dv;
@@ -2523,6 +2584,7 @@ static int fast4d_shape_g(const DevGrid& g, const DevModel& m);
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   const int sh = fast4d_shape_g(g, m);
   if (sh < 0 || scheme == 0) return sh;
+  if (sh == kShapeGen) return -1;  // Lax-Friedrichs: compiled shapes only
   // Lax-Friedrichs: each row's inputs must be the shape's (one term each)
   if (m.m > 3 || m.p > 3) return -1;
   for (int d = 0; d < 4; ++d) {
@@ -2598,7 +2660,15 @@ static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
   if (match(pa, pb, l0)) return 0;
   if (match(pa, pb, l1)) return 1;
   if (match(ta, tb, lt)) return 2;
-  return -1;
+  return kShapeGen;  // admissible rows, run-time shape
+}
+
+void fast4d_gen_rows(const DevModel& m, Fast4dArgs& a) {
+  for (int d = 0; d < 4; ++d) {
+    const DevRow& r = m.row[d];
+    a.gax[d] = r.axis_a;
+    a.gbx[d] = r.folded ? -1 : r.axis_b;
+  }
 }
 
 static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 128 * 128); }
@@ -2840,14 +2910,32 @@ static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
     cp ? launch_one<S, 2, 576, 0, 0, true>(a, s) : launch_one<S, 2, 576>(a, s);
 }
 
+// run-time-shape variant: Godunov, constant bounds, no target set (the host
+// sends the other cases to the generic kernel); kcells 2 only
+static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.ms) {
+    launch_one<ShapeGen, 2, 576, 0, 0, false, false, true>(a, s);
+    return;
+  }
+  const bool cp = a.cplane != nullptr;
+  if (a.maxthreads == 448)
+    cp ? launch_one<ShapeGen, 2, 448, 0, 0, true>(a, s) : launch_one<ShapeGen, 2, 448>(a, s);
+  else
+    cp ? launch_one<ShapeGen, 2, 576, 0, 0, true>(a, s) : launch_one<ShapeGen, 2, 576>(a, s);
+}
+
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   t_attr_err = cudaSuccess;
+  if (shape == kShapeGen && (a.lf || a.pv || a.target || a.kcells != 2))
+    return cudaErrorInvalidValue;  // not a configuration of the run-time-shape variant
   if (shape == 0)
     launch_shape<ShapePlanarD0>(a, s);
   else if (shape == 1)
     launch_shape<ShapePlanarD1>(a, s);
-  else
+  else if (shape == 2)
     launch_shape<ShapeTwin>(a, s);
+  else
+    launch_gen(a, s);
   if (t_attr_err != cudaSuccess) return t_attr_err;
   return cudaGetLastError();
 }

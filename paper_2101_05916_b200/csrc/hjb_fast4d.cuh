@@ -60,6 +60,10 @@ struct Fast4dArgs {
   uint32_t tab_off;     // shared-memory byte offset of the staged copy
   int tab_staged;       // 1: tables staged in shared memory, 0: read from global
   int off_pos[4], off_neg[4], off_a[4], off_b[4];
+  // rows of the run-time-shape variant (ShapeGen): drift-table axes of each
+  // row (gbx < 0: one-axis row, slopes from off_pos / off_neg; else an
+  // input-free two-term row, slope = tab[off_a + k_a] + tab[off_b + k_b])
+  int gax[4], gbx[4];
   const double* c;  // padded constraint
   // constraint that varies along axis 0 only (signed distance to a set in
   // x0, every BASELINE 4D config): c[i0] per plane, the padded field unused
@@ -176,6 +180,14 @@ cudaError_t ho4d_unpad(const double* in, double* out, uint32_t planes, const Ho4
 // (rank != 4, per-node bounds, rows depending on x0, inputs not matching the
 // shape, ...).  scheme: 0 Godunov, 1 LF per-node alpha, 2 LF global alpha.
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
+// Shape id of the run-time-shape Godunov variant (k_fast4d<ShapeGen>): a
+// model whose rows are admissible for the fast path (one-axis rows with any
+// inputs, input-free two-term rows, no row on x0) but match none of the
+// compiled shapes.  First order, Godunov, constant bounds, no target set;
+// the high-order and Lax-Friedrichs paths treat it as -1 (generic kernel).
+constexpr int kShapeGen = 3;
+// Fast4dArgs::gax / gbx of the run-time-shape variant from the model rows
+void fast4d_gen_rows(const DevModel& m, Fast4dArgs& a);
 // Godunov fast-path shape for PER-NODE bounds (rows not folded); -1 if none.
 // Rows with a disturbance term must be exactly the shape's D rows, one
 // term each.  Bounds varying along axis 0 only run the plane-table variant

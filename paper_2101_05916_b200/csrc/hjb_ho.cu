@@ -74,6 +74,7 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   const char* fe = std::getenv("HJB_FAST");
   int shape = (fe && std::strcmp(fe, "0") == 0) ? -1 : fast4d_shape(g, m, scheme_id(cfg));
   if (cfg->target) shape = -1;  // target sets run the generic stage kernel
+  if (shape == kShapeGen) shape = -1;  // ENO/TVD-RK 4D kernels: compiled shapes only
   if (shape >= 0 && scheme_id(cfg) != kGodunov) {
     // Lax-Friedrichs runs only in the TMA-staged kernel (k_ho4t)
     Ho4dArgs t;

@@ -160,20 +160,7 @@ __device__ __forceinline__ void row_slopes(const DevModel& m, const DevRow& r,
   }
 }
 
-// godunov_flux (solver.cpp:44-63)
-__device__ __forceinline__ double godunov_flux(double pos, double neg, double dminus,
-                                               double dplus) {
-  const double ha = dminus > 0.0 ? pos * dminus : neg * dminus;
-  const double hb = dplus > 0.0 ? pos * dplus : neg * dplus;
-  if (dminus <= dplus) {
-    double h = ha > hb ? ha : hb;
-    if (dminus <= 0.0 && 0.0 <= dplus && h < 0.0) h = 0.0;
-    return h;
-  }
-  double h = ha < hb ? ha : hb;
-  if (dplus <= 0.0 && 0.0 <= dminus && h > 0.0) h = 0.0;
-  return h;
-}
+// godunov_flux (solver.cpp:44-63): hjb_device.cuh
 
 // flow_bounds alpha for one row (dynamics.cpp:93-112)
 template <int ND, bool PERNODE>

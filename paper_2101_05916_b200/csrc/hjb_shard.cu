@@ -783,6 +783,9 @@ int sharded_prologue(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     return set_err(HJB_ERR_UNSUPPORTED,
                    "solve_sharded: Lax-Friedrichs needs one input term per row of the 4D model");
   const bool high_order = cfg->spatial_order > 1 || cfg->time_order > 1;
+  if (high_order && p.shape == kShapeGen)
+    return set_err(HJB_ERR_UNSUPPORTED,
+                   "solve_sharded: ENO / TVD-RK slabs need one of the compiled 4D model shapes");
   R = high_order ? static_cast<uint32_t>(cfg->spatial_order < 1 ? 1 : cfg->spatial_order) : 1u;
   // Every rank must reject a too-thin partition BEFORE the first collective:
   // balanced slabs differ by one plane, so a per-rank check would let the
@@ -931,7 +934,7 @@ int hjb_ho_stage_planes_dev(hjb_context* ctx, const hjb_grid* gi, const hjb_mode
   CUDA_TRY(cudaSetDevice(ctx->device));
   Prepared p;
   if ((rc = prepare(ctx, gi, mi, db, p))) return rc;
-  if (p.shape < 0)
+  if (p.shape < 0 || p.shape == kShapeGen)
     return set_err(HJB_ERR_UNSUPPORTED, "ho_stage_planes: model/grid outside the 4D fast path");
   if (plane_begin < 0 || plane_end > p.g.n[0] || plane_begin >= plane_end)
     return set_err(HJB_ERR_INVALID_ARGUMENT, "ho_stage_planes: bad plane range");

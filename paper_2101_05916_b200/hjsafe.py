@@ -656,6 +656,56 @@ class ConstantAdvection(DynamicsModel):
         return [[_term(abi.TERM_CONST, 0, s)] for s in self.speed]
 
 
+class SeparableAffineModel(DynamicsModel):
+    """A user-defined control-affine model in the separable form the C ABI
+    takes (``hjb_model``, include/hjb.h): per row up to two drift terms
+    ``(kind, axis, scale)`` with kind one of ``abi.TERM_COORD`` (scale*x[axis]),
+    ``abi.TERM_TAN`` (scale*tan(x[axis])) or ``abi.TERM_CONST`` (scale), and
+    constant control / disturbance matrices B, C — the structure every
+    reference model has (dynamics.cpp:126-198).  4D models whose rows do not
+    depend on x0 run the fast 4D kernel (compiled shapes or the run-time-shape
+    variant); the rest run the generic kernel."""
+
+    name_ = "separable_affine"
+
+    def __init__(self, drift: Sequence[Sequence[tuple]], control=None, disturbance=None,
+                 control_bounds: Sequence[Interval] = ()):
+        self.drift = [[_term(*t) for t in row] for row in drift]
+        n = len(self.drift)
+        self.B = np.zeros((n, 0)) if control is None else np.asarray(control, dtype=np.float64)
+        self.C = (np.zeros((n, 0)) if disturbance is None
+                  else np.asarray(disturbance, dtype=np.float64))
+        self.ub = list(control_bounds)
+        if self.B.shape[0] != n or self.C.shape[0] != n or len(self.ub) != self.B.shape[1]:
+            raise ValueError("SeparableAffineModel: inconsistent row / input counts")
+        if any(len(row) > 2 for row in self.drift):
+            raise ValueError("SeparableAffineModel: at most two drift terms per row")
+
+    def state_dim(self):
+        return len(self.drift)
+
+    def control_dim(self):
+        return self.B.shape[1]
+
+    def disturbance_dim(self):
+        return self.C.shape[1]
+
+    def control_bounds(self):
+        return list(self.ub)
+
+    def disturbance_rows(self):
+        return [i for i in range(self.state_dim()) if np.any(self.C[i] != 0.0)]
+
+    def drift_terms(self):
+        return [list(row) for row in self.drift]
+
+    def control_matrix(self):
+        return self.B.copy()
+
+    def disturbance_matrix(self):
+        return self.C.copy()
+
+
 class NearHover10D(DynamicsModel):
     """Stacked x/y planar + z vertical model (dynamics.hpp:250-271).  Grids of
     rank 10 exceed the device kernels; it exists for decomposition (the solver
@@ -777,7 +827,7 @@ class SolveResult:
 
 
 KERNELS = {0: "none", 1: "generic", 2: "fast4d", 3: "fast4d_multisweep", 4: "small2d",
-           5: "ho_generic", 6: "ho4d", 7: "small2d_ho"}
+           5: "ho_generic", 6: "ho4d", 7: "small2d_ho", 8: "fast4d_gen"}
 
 
 @dataclass

@@ -1,0 +1,46 @@
+"""Per-sweep device time of user models on the run-time-shape 4D kernel
+(k_fast4d<ShapeGen>) against the generic kernel (HJB_FAST=0), next to the
+compiled-shape kernel on the config-2 model, at one grid size.
+
+usage: python scripts/bench_gen4d.py [n=51] [iters=300]
+Prints one JSON line per (model, kernel).
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+
+from paper_2101_05916_b200 import configs  # noqa: E402
+from paper_2101_05916_b200 import hjsafe as hj  # noqa: E402
+from test_gpu_gen4d import MODELS  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 51
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+    ctx = hj.Context(0)
+    g = hj.Grid([(-5.0, 5.0, n), (-2.0, 2.0, n), (-0.35, 0.35, n), (-1.5, 1.5, n)])
+    c = hj.signed_distance_band(g, 0, -4.0, 4.0, ctx=ctx)
+    cfg = hj.SolveConfig(tolerance=1e-12, max_iters=iters)
+    os.environ["HJB_MS"] = "0"
+    runs = [(name, make(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)] * nd))
+            for name, (make, nd) in sorted(MODELS.items())]
+    w = configs.config2(n)
+    runs.append(("config2 (compiled shape)", w.model, w.dbounds()))
+    for name, model, db in runs:
+        for fast in ("1", "0"):
+            os.environ["HJB_FAST"] = fast
+            hj.solve(c, c, model, db, hj.SolveConfig(max_iters=5), ctx=ctx)  # autotune, warm
+            r = hj.solve(c, c, model, db, cfg, ctx=ctx)
+            us = r.wall_seconds / r.iterations * 1e6
+            print(json.dumps({"model": name, "grid": f"{n}^4", "kernel": r.kernel,
+                              "sweep_us": round(us, 2), "iterations": r.iterations,
+                              "gcell_per_s": round(g.size() / us * 1e-3, 2)}), flush=True)
+    os.environ.pop("HJB_FAST", None)
+
+
+if __name__ == "__main__":
+    main()

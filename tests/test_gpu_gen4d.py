@@ -1,0 +1,147 @@
+"""GPU parity of the run-time-shape 4D sweep (k_fast4d<ShapeGen>) against the
+CPU oracle: user models whose rows fit the fast path's structure (one-axis
+rows with any inputs, input-free two-term rows, nothing on x0) but none of
+the compiled shapes.  Before this variant such models ran the generic
+one-thread-per-node kernel (~3.5x slower per cell).
+
+Bitwise (IEEE ==) values, identical iteration counts and residual histories
+(the update is update_chunk, proj/src/solver.cpp:106-190, term by term).
+"""
+import numpy as np
+import pytest
+
+from paper_2101_05916_b200 import abi
+from paper_2101_05916_b200 import hjsafe as hj
+
+from cases import band_np, same
+
+pytestmark = pytest.mark.gpu
+
+C_, T_, K_ = abi.TERM_COORD, abi.TERM_TAN, abi.TERM_CONST
+
+
+def mixed_model():
+    """Rows: x3 + d | -2 x2 + 0.5 x3 | 9.8 tan x2 | -1.5 x1 + 4 u (a one-axis
+    row with a disturbance, a two-term linear row, a linear tan row and a
+    control row; row axes 3, (2, 3), 2, 1)."""
+    B = np.zeros((4, 1))
+    B[3, 0] = 4.0
+    Cm = np.zeros((4, 1))
+    Cm[0, 0] = 1.0
+    return hj.SeparableAffineModel(
+        [[(C_, 3, 1.0)], [(C_, 2, -2.0), (C_, 3, 0.5)], [(T_, 2, 9.8)], [(C_, 1, -1.5)]],
+        B, Cm, [hj.Interval(-0.4, 0.4)])
+
+
+def inputs_model():
+    """Two controls and two disturbances on rows 1 and 3, drifts over axes
+    2, 3, 1 and a constant row: x2 | x3 + u0 + d0 | -0.7 x1 | -9.8 + u1 - d1."""
+    B = np.zeros((4, 2))
+    B[1, 0] = 1.0
+    B[3, 1] = 2.5
+    Cm = np.zeros((4, 2))
+    Cm[1, 0] = 1.0
+    Cm[3, 1] = -0.5
+    return hj.SeparableAffineModel(
+        [[(C_, 2, 1.0)], [(C_, 3, 1.0)], [(C_, 1, -0.7)], [(K_, 0, -9.8)]],
+        B, Cm, [hj.Interval(-1.0, 1.0), hj.Interval(0.0, 8.0)])
+
+
+def advection_model():
+    """Constant drifts only (every row a table of length one)."""
+    return hj.ConstantAdvection([1.0, -0.5, 0.25, 0.75])
+
+
+MODELS = {"mixed": (mixed_model, 1), "inputs": (inputs_model, 2), "advection": (advection_model, 0)}
+
+
+def _setup(name, dims):
+    make, nd = MODELS[name]
+    n0, n1, n2, n3 = dims
+    g = hj.Grid([(-5.0, 5.0, n0), (-2.0, 2.0, n1), (-0.35, 0.35, n2), (-1.5, 1.5, n3)])
+    db = hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)] * nd)
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    return g, make(), db, c
+
+
+def _check(got, want):
+    assert got.dt == want.dt
+    assert got.iterations == want.iterations
+    assert got.converged == want.converged
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+
+
+@pytest.mark.parametrize("ms", ["0", "1"])
+@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (9, 21, 19, 23), (17, 12, 10, 40),
+                                  (33, 5, 6, 101)])
+@pytest.mark.parametrize("name", sorted(MODELS))
+def test_gen4d_matches_oracle(gpu_ctx, oracle, monkeypatch, name, dims, ms):
+    """Irregular grids (odd / even contiguous extents, partial tiles, chunked
+    marches), per-sweep launches (HJB_MS=0) and the multi-sweep persistent
+    launch, against the oracle."""
+    monkeypatch.setenv("HJB_MS", ms)
+    g, model, db, c = _setup(name, dims)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=40)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.kernel == ("fast4d_multisweep" if ms == "1" else "fast4d_gen")
+    _check(got, want)
+
+
+@pytest.mark.parametrize("name", sorted(MODELS))
+def test_gen4d_to_convergence(gpu_ctx, oracle, monkeypatch, name):
+    """A whole solve to convergence: identical iteration count (north_star)."""
+    monkeypatch.setenv("HJB_MS", "0")
+    g, model, db, c = _setup(name, (15, 13, 11, 17))
+    cfg = hj.SolveConfig(tolerance=5e-3, max_iters=6000)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert want.converged
+    _check(got, want)
+
+
+@pytest.mark.parametrize("name", sorted(MODELS))
+def test_gen4d_matches_generic_kernel(gpu_ctx, monkeypatch, name):
+    """Run-time-shape variant == generic kernel (HJB_FAST=0), bit for bit, on
+    a grid large enough for the autotuned per-sweep path."""
+    monkeypatch.setenv("HJB_MS", "0")
+    g, model, db, c = _setup(name, (41, 41, 41, 41))
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=25)
+    fast = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert fast.kernel == "fast4d_gen"
+    monkeypatch.setenv("HJB_FAST", "0")
+    gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert gen.kernel == "generic"
+    assert same(fast.value.values(), gen.value.values())
+    assert same(fast.residual_history, gen.residual_history)
+
+
+def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
+    """A row on the march axis x0, Lax-Friedrichs, a target set and ENO/TVD-RK
+    stay on the generic kernels (still bitwise against the oracle)."""
+    B = np.zeros((4, 1))
+    B[1, 0] = 1.0
+    x0_model = hj.SeparableAffineModel(
+        [[(C_, 1, 1.0)], [(C_, 0, -0.5)], [(C_, 3, 1.0)], [(C_, 2, -1.0)]], B, None,
+        [hj.Interval(-1.0, 1.0)])
+    g = hj.Grid([(-5.0, 5.0, 11), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 8)])
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=20)
+    db0 = hj.IntervalField.constant(g, [])
+    got = hj.solve(c, c, x0_model, db0, cfg, ctx=gpu_ctx)
+    assert got.kernel == "generic"
+    _check(got, oracle.solve(c, c, x0_model, db0, cfg))
+    model, db = mixed_model(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    lf = hj.SolveConfig(tolerance=1e-4, max_iters=20, scheme=hj.LAX_FRIEDRICHS)
+    got = hj.solve(c, c, model, db, lf, ctx=gpu_ctx)
+    assert got.kernel == "generic"
+    _check(got, oracle.solve(c, c, model, db, lf))
+    ho = hj.SolveConfig(tolerance=1e-4, max_iters=10, spatial_order=3, time_order=3)
+    got = hj.solve(c, c, model, db, ho, ctx=gpu_ctx)
+    assert got.kernel == "ho_generic"
+    _check(got, oracle.solve(c, c, model, db, ho))
+    tl = hj.ScalarField(g, band_np(g, 1, -1.0, 1.0))
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx, target=tl)
+    assert got.kernel == "generic"
+    _check(got, oracle.solve(c, c, model, db, cfg, target=tl))
