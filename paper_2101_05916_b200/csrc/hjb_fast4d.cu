@@ -1010,11 +1010,17 @@ __global__ void __launch_bounds__(MAXT, 1)
             const double dp0 = (vn[c] - v[c]) * inv0;
             const double dm1 = (v[c] - n1m[c]) * inv1, dp1 = (n1p[c] - v[c]) * inv1;
             const double dm2 = (v[c] - n2m[c]) * inv2, dp2 = (n2p[c] - v[c]) * inv2;
+            // rows without inputs (a uniform branch): the upwind product, as
+            // the compiled shapes' LIN rows
+            auto flux = [&](int d, double dm, double dp) -> double {
+              if (a.glin & (1 << d)) return pos_[d][c] * (sign_clear(pos_[d][c]) ? dp : dm);
+              return godunov_flux(pos_[d][c], neg_[d][c], dm, dp);
+            };
             double hh = 0.0;
-            hh += godunov_flux(pos_[0][c], neg_[0][c], dm0[c], dp0);
-            hh += godunov_flux(pos_[1][c], neg_[1][c], dm1, dp1);
-            hh += godunov_flux(pos_[2][c], neg_[2][c], dm2, dp2);
-            hh += godunov_flux(pos_[3][c], neg_[3][c], f3[c], f3[c + 1]);
+            hh += flux(0, dm0[c], dp0);
+            hh += flux(1, dm1, dp1);
+            hh += flux(2, dm2, dp2);
+            hh += flux(3, f3[c], f3[c + 1]);
             dm0[c] = dp0;
             const double st = v[c] + a.dt * hh;
             out[c] = st > cc[c] ? st : cc[c];
@@ -2669,6 +2675,9 @@ void fast4d_gen_rows(const DevModel& m, Fast4dArgs& a) {
     a.gax[d] = r.axis_a;
     a.gbx[d] = r.folded ? -1 : r.axis_b;
   }
+  a.glin = 0;
+  for (int d = 0; d < 4; ++d)
+    if (m.row[d].n_uadd == 0 && m.row[d].n_dterm == 0) a.glin |= 1 << d;
 }
 
 static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 128 * 128); }

@@ -64,6 +64,9 @@ struct Fast4dArgs {
   // row (gbx < 0: one-axis row, slopes from off_pos / off_neg; else an
   // input-free two-term row, slope = tab[off_a + k_a] + tab[off_b + k_b])
   int gax[4], gbx[4];
+  // glin: bit d set when row d has no input (pos == neg == s everywhere):
+  // its Godunov flux is s * D+ (s >= 0) or s * D- (the compiled shapes' LIN)
+  int glin;
   const double* c;  // padded constraint
   // constraint that varies along axis 0 only (signed distance to a set in
   // x0, every BASELINE 4D config): c[i0] per plane, the padded field unused
