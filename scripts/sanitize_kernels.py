@@ -4,7 +4,7 @@ compute-sanitizer (memcheck / racecheck / synccheck, one tool per run):
     compute-sanitizer --tool racecheck --error-exitcode 9 python scripts/sanitize_kernels.py
 
 Covers k_fast4d (Godunov / Lax-Friedrichs / per-node bounds / target set /
-multi-sweep persistent), k_ho4t (ENO2), k_eno3g (ENO3 Godunov and LF),
+multi-sweep persistent / run-time row shapes), k_ho4t (ENO2), k_eno3g (ENO3 Godunov and LF),
 the generic k_step / k_ho_stage, k_small2d / k_small2d_ho (2D cluster
 kernels), the sharded in-process protocol, the resample / seed chain,
 k_gp_ring (GP bounds) and the safety-filter batch.  Every result is also
@@ -53,6 +53,18 @@ def main():
         cfg = hj.SolveConfig(**base, **extra)
         r = hj.solve(c, c, w.model, w.dbounds(), cfg, ctx=ctx)
         check(label, r.value.values(), ora.solve(c, c, w.model, w.dbounds(), cfg).value.values())
+        for k in env:
+            os.environ.pop(k)
+    # run-time row shapes (k_fast4d<ShapeGen>): a user model outside the
+    # compiled shapes, per-sweep and multi-sweep launches
+    from test_gpu_gen4d import mixed_model  # noqa: E402
+    mm, mdb = mixed_model(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    for label, env in (("k_fast4d run-time shape", {"HJB_MS": "0"}),
+                       ("k_fast4d run-time shape multi-sweep", {"HJB_MS": "1"})):
+        os.environ.update(env)
+        cfg = hj.SolveConfig(**base)
+        r = hj.solve(c, c, mm, mdb, cfg, ctx=ctx)
+        check(label, r.value.values(), ora.solve(c, c, mm, mdb, cfg).value.values())
         for k in env:
             os.environ.pop(k)
     # per-node bounds (k_fast4d PV=2), target set (TG)
