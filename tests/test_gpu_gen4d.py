@@ -145,3 +145,25 @@ def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
     got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx, target=tl)
     assert got.kernel == "generic"
     _check(got, oracle.solve(c, c, model, db, cfg, target=tl))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_gen4d_sharded_local_ranks_equal_solve(gpu_ctx, monkeypatch, P):
+    """The slab-partitioned solve (in-process ranks: the NCCL path's per-rank
+    plans, halo offsets and boundary-first launches) with the run-time-shape
+    variant equals the single-GPU solve bit for bit."""
+    import torch
+    from paper_2101_05916_b200 import sharded
+    monkeypatch.setenv("HJB_MS", "0")
+    g, model, db, c = _setup("mixed", (21, 13, 11, 17))
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=60)
+    ref = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert ref.kernel == "fast4d_gen"
+    ct = torch.tensor(c.values(), device="cuda")
+    out = torch.full_like(ct, float("nan"))
+    torch.cuda.synchronize()
+    r = sharded.solve_sharded_local_dev(P, g, model, db, ct.data_ptr(), ct.data_ptr(),
+                                        out.data_ptr(), cfg, gpu_ctx, history_capacity=60)
+    assert r.iterations == ref.iterations and r.dt == ref.dt
+    assert same(r.residual_history, ref.residual_history)
+    assert same(out.cpu().numpy(), ref.value.values())
