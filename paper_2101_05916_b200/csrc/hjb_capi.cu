@@ -426,6 +426,15 @@ void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfPar
     lp.dlo[j] = j < m.p ? m.dlo[j] : 0.0;
     lp.dhi[j] = j < m.p ? m.dhi[j] : 0.0;
   }
+  for (int d = 0; d < 4; ++d) {
+    const DevRow& r = m.row[d];
+    const int uc = r.n_uadd > 0 && r.uch[0] < 3 ? r.uch[0] : -1;
+    const int dc = r.n_dterm > 0 && r.dch[0] < 3 ? r.dch[0] : -1;
+    lp.uprod_lo[d] = uc >= 0 ? lp.ucoef[d] * lp.ulo[uc] : 0.0;
+    lp.uprod_hi[d] = uc >= 0 ? lp.ucoef[d] * lp.uhi[uc] : 0.0;
+    lp.dprod_lo[d] = dc >= 0 ? lp.dcoef[d] * lp.dlo[dc] : 0.0;
+    lp.dprod_hi[d] = dc >= 0 ? lp.dcoef[d] * lp.dhi[dc] : 0.0;
+  }
 }
 
 }  // namespace hjb

@@ -409,58 +409,76 @@ constexpr uint32_t kEndItem = 0xffffffffu;
 // axis: costate p = (D- + D+)/2, bang-bang u* (ties to lo) and worst d*,
 // H = sum_i p_i f_i summed from 0 in row order (extremal_inputs +
 // hamiltonian, dynamics.cpp:37-83), + alpha_i (D+ - D-)/2 (solver.cpp:
-// 160-174).  dr: the rows' drifts at the cell, al: their alphas.
+// 160-174).  dr: the rows' drifts at the cell, alh: alpha_i * 0.5 (the
+// left operand of the reference's alpha * 0.5 * (D+ - D-), loop invariant).
+// A channel entering one row only (every compiled shape) decides its input
+// on the sign of that row's single product: coeff = 0.0 + x compares with 0
+// exactly as x does, and the input term B u* is the host-formed product
+// (LfParams::uprod_*), the same double the reference's B * u* rounds to.
+template <class S>
+__host__ __device__ constexpr int lf_rows_of_u(int j) {
+  int n = 0;
+  for (int d = 0; d < 4; ++d) n += S::U(d) == j ? 1 : 0;
+  return n;
+}
+template <class S>
+__host__ __device__ constexpr int lf_rows_of_d(int k) {
+  int n = 0;
+  for (int d = 0; d < 4; ++d) n += S::D(d) == k ? 1 : 0;
+  return n;
+}
 template <class S>
 __device__ __forceinline__ double lf_hhat(const LfParams& lp, const double* dmv,
-                                          const double* dpv, const double* dr, const double* al) {
+                                          const double* dpv, const double* dr, const double* alh) {
   double pq[4];
 #pragma unroll
   for (int d = 0; d < 4; ++d) pq[d] = 0.5 * (dmv[d] + dpv[d]);
-  double u[3] = {0.0, 0.0, 0.0}, dd[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    double coeff = 0.0;
-    bool any = false;
-#pragma unroll
-    for (int d = 0; d < 4; ++d)
-      if (S::U(d) == j) {
-        coeff += pq[d] * lp.ucoef[d];
-        any = true;
-      }
-    if (any) u[j] = coeff > 0.0 ? lp.ulo[j] : (coeff < 0.0 ? lp.uhi[j] : lp.ulo[j]);
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    double coeff = 0.0;
-    bool any = false;
-#pragma unroll
-    for (int d = 0; d < 4; ++d)
-      if (S::D(d) == k) {
-        coeff += pq[d] * lp.dcoef[d];
-        any = true;
-      }
-    if (any) dd[k] = coeff > 0.0 ? lp.dhi[k] : (coeff < 0.0 ? lp.dlo[k] : lp.dlo[k]);
-  }
   double hh = 0.0;
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
     double fi = dr[d];
-    if (S::U(d) >= 0) fi += lp.ucoef[d] * u[S::U(d) >= 0 ? S::U(d) : 0];
-    if (S::D(d) >= 0) fi += lp.dcoef[d] * dd[S::D(d) >= 0 ? S::D(d) : 0];
+    if (S::U(d) >= 0) {
+      const int j = S::U(d) >= 0 ? S::U(d) : 0;
+      bool hi;  // u* = uhi: the channel's coefficient is < 0 (ties to lo)
+      if (lf_rows_of_u<S>(j) == 1) {
+        hi = pq[d] * lp.ucoef[d] < 0.0;
+      } else {
+        double coeff = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (S::U(e) == j) coeff += pq[e] * lp.ucoef[e];
+        hi = !(coeff > 0.0) && coeff < 0.0;
+      }
+      fi += hi ? lp.uprod_hi[d] : lp.uprod_lo[d];
+    }
+    if (S::D(d) >= 0) {
+      const int k = S::D(d) >= 0 ? S::D(d) : 0;
+      bool hi;  // d* = dhi: the channel's coefficient is > 0
+      if (lf_rows_of_d<S>(k) == 1) {
+        hi = pq[d] * lp.dcoef[d] > 0.0;
+      } else {
+        double coeff = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (S::D(e) == k) coeff += pq[e] * lp.dcoef[e];
+        hi = coeff > 0.0;
+      }
+      fi += hi ? lp.dprod_hi[d] : lp.dprod_lo[d];
+    }
     hh += pq[d] * fi;
   }
 #pragma unroll
-  for (int d = 0; d < 4; ++d) hh += al[d] * 0.5 * (dpv[d] - dmv[d]);
+  for (int d = 0; d < 4; ++d) hh += alh[d] * (dpv[d] - dmv[d]);
   return hh;
 }
 
 // Row drifts and LF dissipation coefficients of a cell (loop invariant):
 // rows without inputs have drift == their slope, alpha == |drift| when no
-// flow_bounds table exists; SCH 2 takes the global alpha.
+// flow_bounds table exists; SCH 2 takes the global alpha.  alh = alpha * 0.5.
 template <class S, int SCH>
 __device__ __forceinline__ void lf_row_terms(const LfParams& lp, const double* tabs,
                                              const uint32_t* ka, const double* slope_b,
-                                             double* dr, double* al) {
+                                             double* dr, double* alh) {
 #pragma unroll
   for (int d = 0; d < 4; ++d) {
     if (S::B(d) >= 0) {  // two-term drift, no inputs: the slope is the drift
@@ -468,13 +486,15 @@ __device__ __forceinline__ void lf_row_terms(const LfParams& lp, const double* t
     } else {
       dr[d] = lp.dr_off[d] >= 0 ? tabs[lp.dr_off[d] + ka[d]] : lp.dr_const[d];
     }
+    double al;
     if (SCH == 2) {
-      al[d] = lp.galpha[d];
+      al = lp.galpha[d];
     } else if (lp.off_alpha[d] >= 0) {
-      al[d] = tabs[lp.off_alpha[d] + ka[d]];
+      al = tabs[lp.off_alpha[d] + ka[d]];
     } else {
-      al[d] = fabs(dr[d]);
+      al = fabs(dr[d]);
     }
+    alh[d] = al * 0.5;  // lf_hhat's alpha * 0.5
   }
 }
 

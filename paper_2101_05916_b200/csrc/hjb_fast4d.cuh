@@ -20,6 +20,9 @@ struct LfParams {
   double dcoef[4];      // C coefficient of the row's disturbance (shape D(d))
   double ulo[3], uhi[3], dlo[3], dhi[3];
   int off_alpha[4];     // LF per-node alpha tables (-1: |drift|)
+  // the row's input products with each bound, formed on the host exactly as
+  // the Hamiltonian forms them (B u* / C d*: ucoef * ulo[ch] etc.)
+  double uprod_lo[4], uprod_hi[4], dprod_lo[4], dprod_hi[4];
 };
 
 struct Fast4dArgs {
