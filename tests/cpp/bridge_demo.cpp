@@ -34,6 +34,27 @@ class ConstantAdvection final : public DynamicsModel {  // test_solver.cpp:14-29
   std::vector<double> s_;
 };
 
+// A user's own 4D model (no reference class, no compiled kernel shape): the
+// bridge probes affine() into one-axis drift tables, and the solve runs the
+// run-time-shape 4D sweep (k_fast4d<ShapeGen>).
+class UserModel4D final : public DynamicsModel {
+ public:
+  std::size_t state_dim() const override { return 4; }
+  std::size_t control_dim() const override { return 1; }
+  std::size_t disturbance_dim() const override { return 1; }
+  std::string name() const override { return "user4d"; }
+  std::vector<Interval> control_bounds() const override { return {{-1.0, 1.0}}; }
+  void affine(std::span<const double> x, AffineFlow& out) const override {
+    out.reset(4, 1, 1);
+    out.drift[0] = x[1];
+    out.drift[1] = -0.2 * x[3] * x[3] * x[3];
+    out.drift[2] = x[3];
+    out.drift[3] = -9.8 * std::sin(x[2]);
+    out.control[3][0] = 2.0;
+    out.disturbance[0][0] = 1.0;
+  }
+};
+
 bool same(const ScalarField& a, const ScalarField& b) {
   if (a.size() != b.size()) return false;
   for (std::size_t i = 0; i < a.size(); ++i)
@@ -109,6 +130,39 @@ int main() {
       expect(same(rr.value, rg.value) && rr.iterations == rg.iterations &&
                  rr.residual_history == rg.residual_history,
              "NearHoverPlanar4D 51^4 x 20: bitwise equal, constant bounds detected");
+    }
+
+    // a user-defined 4D model through the drop-in: probed tables, run-time
+    // row shapes; bitwise on 21^4 x 40 sweeps, then 51^4 x 20 sweeps timed
+    {
+      UserModel4D user;
+      Grid gu({{-5.0, 5.0, 21}, {-2.0, 2.0, 21}, {-0.35, 0.35, 21}, {-1.5, 1.5, 21}});
+      ScalarField cu = signed_distance_band(gu, 0, -4.0, 4.0);
+      auto dbu = IntervalField::constant(gu, std::vector<Interval>{{-0.5, 0.5}});
+      SolveConfig k40;
+      k40.max_iters = 40;
+      SolveResult ru = solve(cu, cu, user, dbu, k40);
+      SolveResult gu40 = hjb_bridge::solve(cu, cu, user, dbu, k40);
+      expect(same(ru.value, gu40.value) && ru.iterations == gu40.iterations &&
+                 ru.residual_history == gu40.residual_history,
+             "user-defined 4D model 21^4 x 40: bitwise equal");
+      Grid g51({{-5.0, 5.0, 51}, {-2.0, 2.0, 51}, {-0.35, 0.35, 51}, {-1.5, 1.5, 51}});
+      ScalarField c51 = signed_distance_band(g51, 0, -4.0, 4.0);
+      auto db51 = IntervalField::constant(g51, std::vector<Interval>{{-0.5, 0.5}});
+      SolveConfig k20;
+      k20.max_iters = 20;
+      hjb_bridge::solve(c51, c51, user, db51, k20);  // warm-up
+      auto t0 = std::chrono::steady_clock::now();
+      SolveResult rg = hjb_bridge::solve(c51, c51, user, db51, k20);
+      auto t1 = std::chrono::steady_clock::now();
+      SolveResult rr = solve(c51, c51, user, db51, k20);
+      auto t2 = std::chrono::steady_clock::now();
+      const double sg = std::chrono::duration<double>(t1 - t0).count();
+      const double sr = std::chrono::duration<double>(t2 - t1).count();
+      std::printf("user 4D model 51^4 x 20 sweeps: bridge %.1f ms (host buffers in and out), "
+                  "reference %.1f ms (%.0fx)\n", sg * 1e3, sr * 1e3, sr / sg);
+      expect(same(rr.value, rg.value) && rr.iterations == rg.iterations,
+             "user-defined 4D model 51^4 x 20: bitwise equal");
     }
 
     // coarse-to-fine (test_solver.cpp:253-278 setup)
