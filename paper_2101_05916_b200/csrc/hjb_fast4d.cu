@@ -714,24 +714,32 @@ __global__ void __launch_bounds__(MAXT, 1)
       // loop-invariant slopes (row d, cell c); rows that do not vary along x3
       // hold one pair for the whole pencil
       double pos_[4][kK], neg_[4][kK];
-      if constexpr (S::GEN) {  // run-time row axes (Fast4dArgs::gax / gbx)
+      // run-time row axes (Fast4dArgs::gax / gbx): the slopes of the rows in
+      // `rows` at plane p (rows on x0 are re-formed every plane, gx0)
+      auto gen_slopes = [&](uint32_t rows, uint32_t p) {
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
+          if (!(rows & (1u << d))) continue;
 #pragma unroll
           for (int c = 0; c < kK; ++c) {
             const uint32_t i3c = min(i3 + c, n3 - 1);
-            const uint32_t ka = active ? pick<S>(a.gax[d], i1, i2, i3c) : 0u;
+            const uint32_t ka =
+                !active ? 0u : (a.gax[d] == 0 ? p : pick<S>(a.gax[d], i1, i2, i3c));
             if (a.gbx[d] < 0) {
               pos_[d][c] = tabs[a.off_pos[d] + ka];
               neg_[d][c] = tabs[a.off_neg[d] + ka];
             } else {
-              const uint32_t kb = active ? pick<S>(a.gbx[d], i1, i2, i3c) : 0u;
+              const uint32_t kb =
+                  !active ? 0u : (a.gbx[d] == 0 ? p : pick<S>(a.gbx[d], i1, i2, i3c));
               const double dr = tabs[a.off_a[d] + ka] + tabs[a.off_b[d] + kb];
               pos_[d][c] = dr;
               neg_[d][c] = dr;
             }
           }
         }
+      };
+      if constexpr (S::GEN) {
+        gen_slopes(0xfu, c0);
       } else {
 #pragma unroll
       for (int d = 0; d < 4; ++d) {
@@ -870,6 +878,9 @@ __global__ void __launch_bounds__(MAXT, 1)
         }
       }
       for (uint32_t i0 = c0; i0 < c1; ++i0) {
+        if constexpr (S::GEN) {
+          if (a.gx0) gen_slopes(a.gx0, i0);  // rows on x0: this plane's slopes
+        }
         if (PV == 2) {
           // per-node disturbance bounds: this cell's slopes and shapes of the
           // disturbance rows (dim_slopes order: drift + controls, then +
@@ -2660,6 +2671,7 @@ static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
   if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   bool lin[4];
+  bool x0 = false;
   for (int d = 0; d < 4; ++d) {
     const DevRow& r = m.row[d];
     if (r.folded) {
@@ -2671,9 +2683,10 @@ static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
     } else {
       return -1;
     }
-    if (A[d] == 0 || B[d] == 0) return -1;
+    if (A[d] == 0 || B[d] == 0) x0 = true;
     lin[d] = r.n_uadd == 0 && r.n_dterm == 0;
   }
+  if (x0) return kShapeGen;  // a row on the march axis: run-time shapes only
   auto match = [&](const int* a, const int* b, const bool* l) {
     for (int d = 0; d < 4; ++d)
       if (a[d] != A[d] || b[d] != B[d] || (l[d] && !lin[d])) return false;
@@ -2696,8 +2709,11 @@ void fast4d_gen_rows(const DevModel& m, Fast4dArgs& a) {
     a.gbx[d] = r.folded ? -1 : r.axis_b;
   }
   a.glin = 0;
-  for (int d = 0; d < 4; ++d)
+  a.gx0 = 0;
+  for (int d = 0; d < 4; ++d) {
     if (m.row[d].n_uadd == 0 && m.row[d].n_dterm == 0) a.glin |= 1 << d;
+    if (a.gax[d] == 0 || a.gbx[d] == 0) a.gx0 |= 1 << d;
+  }
 }
 
 static uint32_t round128(size_t b) { return static_cast<uint32_t>((b + 127) / 128 * 128); }

@@ -70,6 +70,8 @@ struct Fast4dArgs {
   // glin: bit d set when row d has no input (pos == neg == s everywhere):
   // its Godunov flux is s * D+ (s >= 0) or s * D- (the compiled shapes' LIN)
   int glin;
+  // gx0: bit d set when row d's slopes vary along x0 (re-formed every plane)
+  int gx0;
   const double* c;  // padded constraint
   // constraint that varies along axis 0 only (signed distance to a set in
   // x0, every BASELINE 4D config): c[i0] per plane, the padded field unused

@@ -786,6 +786,13 @@ int sharded_prologue(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   if (high_order && p.shape == kShapeGen)
     return set_err(HJB_ERR_UNSUPPORTED,
                    "solve_sharded: ENO / TVD-RK slabs need one of the compiled 4D model shapes");
+  if (p.shape == kShapeGen) {
+    Fast4dArgs probe;
+    std::memset(&probe, 0, sizeof probe);
+    fast4d_gen_rows(p.hm.dm, probe);
+    if (probe.gx0)  // slab-local plane numbers would index the x0 tables
+      return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: a model row depends on x0 (the slab axis)");
+  }
   R = high_order ? static_cast<uint32_t>(cfg->spatial_order < 1 ? 1 : cfg->spatial_order) : 1u;
   // Every rank must reject a too-thin partition BEFORE the first collective:
   // balanced slabs differ by one plane, so a per-rank check would let the

@@ -52,7 +52,22 @@ def advection_model():
     return hj.ConstantAdvection([1.0, -0.5, 0.25, 0.75])
 
 
-MODELS = {"mixed": (mixed_model, 1), "inputs": (inputs_model, 2), "advection": (advection_model, 0)}
+def x0_model():
+    """Rows on the march axis x0 (re-formed every plane): 2 x1 + 0.05 u |
+    x0 + 0.3 x3 | -0.4 x0 + d | x1  (a two-term row on (x0, x3), a one-axis
+    x0 row with a disturbance; no row depends on its own axis, as Godunov
+    requires, solver.cpp:293-295)."""
+    B = np.zeros((4, 1))
+    B[0, 0] = 0.05
+    Cm = np.zeros((4, 1))
+    Cm[2, 0] = 1.0
+    return hj.SeparableAffineModel(
+        [[(C_, 1, 2.0)], [(C_, 0, 1.0), (C_, 3, 0.3)], [(C_, 0, -0.4)], [(C_, 1, 1.0)]],
+        B, Cm, [hj.Interval(-1.0, 1.0)])
+
+
+MODELS = {"mixed": (mixed_model, 1), "inputs": (inputs_model, 2), "advection": (advection_model, 0),
+          "x0rows": (x0_model, 1)}
 
 
 def _setup(name, dims):
@@ -118,20 +133,11 @@ def test_gen4d_matches_generic_kernel(gpu_ctx, monkeypatch, name):
 
 
 def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
-    """A row on the march axis x0, Lax-Friedrichs, a target set and ENO/TVD-RK
-    stay on the generic kernels (still bitwise against the oracle)."""
-    B = np.zeros((4, 1))
-    B[1, 0] = 1.0
-    x0_model = hj.SeparableAffineModel(
-        [[(C_, 1, 1.0)], [(C_, 0, -0.5)], [(C_, 3, 1.0)], [(C_, 2, -1.0)]], B, None,
-        [hj.Interval(-1.0, 1.0)])
+    """Lax-Friedrichs, a target set and ENO/TVD-RK stay on the generic kernels
+    for a run-time-shape model (still bitwise against the oracle)."""
     g = hj.Grid([(-5.0, 5.0, 11), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 8)])
     c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
     cfg = hj.SolveConfig(tolerance=1e-4, max_iters=20)
-    db0 = hj.IntervalField.constant(g, [])
-    got = hj.solve(c, c, x0_model, db0, cfg, ctx=gpu_ctx)
-    assert got.kernel == "generic"
-    _check(got, oracle.solve(c, c, x0_model, db0, cfg))
     model, db = mixed_model(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
     lf = hj.SolveConfig(tolerance=1e-4, max_iters=20, scheme=hj.LAX_FRIEDRICHS)
     got = hj.solve(c, c, model, db, lf, ctx=gpu_ctx)
@@ -167,3 +173,16 @@ def test_gen4d_sharded_local_ranks_equal_solve(gpu_ctx, monkeypatch, P):
     assert r.iterations == ref.iterations and r.dt == ref.dt
     assert same(r.residual_history, ref.residual_history)
     assert same(out.cpu().numpy(), ref.value.values())
+
+
+def test_gen4d_x0_rows_not_sharded(gpu_ctx):
+    """A row on the slab axis x0 is rejected by the slab-partitioned solve
+    (local plane numbers would index the x0 tables) with Unsupported."""
+    import torch
+    from paper_2101_05916_b200 import sharded
+    g, model, db, c = _setup("x0rows", (12, 7, 6, 8))
+    ct = torch.tensor(c.values(), device="cuda")
+    out = torch.empty_like(ct)
+    with pytest.raises(hj.Unsupported):
+        sharded.solve_sharded_local_dev(2, g, model, db, ct.data_ptr(), ct.data_ptr(),
+                                        out.data_ptr(), hj.SolveConfig(max_iters=5), gpu_ctx)
