@@ -184,14 +184,15 @@ cudaError_t ho4d_pad(const double* in, double* out, uint32_t planes, const Ho4dA
 cudaError_t ho4d_unpad(const double* in, double* out, uint32_t planes, const Ho4dArgs& a,
                        cudaStream_t s);
 
-// Model shape id for the fast path, or -1 when the generic kernel must run
-// (rank != 4, per-node bounds, rows depending on x0, inputs not matching the
-// shape, ...).  scheme: 0 Godunov, 1 LF per-node alpha, 2 LF global alpha.
+// Model shape id for the fast path (0..2 compiled shapes, kShapeGen run-time
+// rows), or -1 when the generic kernel must run (rank != 4, per-node bounds,
+// a two-term row with inputs, inputs not matching the shape under LF, ...).
+// scheme: 0 Godunov, 1 LF per-node alpha, 2 LF global alpha.
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme);
 // Shape id of the run-time-shape Godunov variant (k_fast4d<ShapeGen>): a
 // model whose rows are admissible for the fast path (one-axis rows with any
-// inputs, input-free two-term rows, no row on x0) but match none of the
-// compiled shapes.  First order, Godunov, constant bounds, no target set;
+// inputs, input-free two-term rows, on any axes; rows on x0 re-form their
+// slopes every plane) but match none of the compiled shapes.  First order, Godunov, constant bounds, no target set;
 // the high-order and Lax-Friedrichs paths treat it as -1 (generic kernel).
 constexpr int kShapeGen = 3;
 // Fast4dArgs::gax / gbx of the run-time-shape variant from the model rows
