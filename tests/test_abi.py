@@ -74,3 +74,42 @@ def test_no_device_fails_loudly(lib):
 def test_kernels_are_sm100a(lib):
     out = subprocess.run(["cuobjdump", "--list-elf", str(abi.LIB_PATH)], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_kernel_family_ids_match_header():
+    """hjb_solve_result.kernel ids (include/hjb.h) and their names in hjsafe."""
+    import re
+    from pathlib import Path
+    from paper_2101_05916_b200 import hjsafe as hj
+    hdr = (Path(__file__).resolve().parent.parent / "include" / "hjb.h").read_text()
+    ids = {int(v): k for k, v in re.findall(r"#define HJB_KERNEL_(\w+) (\d+)", hdr)}
+    assert set(ids) == set(hj.KERNELS)
+    assert ids[8] == "FAST4D_GEN" and hj.KERNELS[8] == "fast4d_gen"
+
+
+def test_separable_affine_model_descriptor():
+    """SeparableAffineModel -> hjb_model: drift terms, B, C and control bounds
+    as given; inconsistent shapes are rejected on the host."""
+    import numpy as np
+    import pytest
+    from paper_2101_05916_b200 import abi
+    from paper_2101_05916_b200 import hjsafe as hj
+    B = np.zeros((4, 1))
+    B[3, 0] = 4.0
+    C = np.zeros((4, 1))
+    C[0, 0] = 1.0
+    m = hj.SeparableAffineModel(
+        [[(abi.TERM_COORD, 3, 1.0)], [(abi.TERM_COORD, 2, -2.0), (abi.TERM_COORD, 3, 0.5)],
+         [(abi.TERM_TAN, 2, 9.8)], [(abi.TERM_CONST, 0, -1.5)]], B, C, [hj.Interval(-0.4, 0.4)])
+    d = m.to_c()
+    assert (d.state_dim, d.control_dim, d.disturbance_dim) == (4, 1, 1)
+    assert d.drift[1][1].kind == abi.TERM_COORD and d.drift[1][1].axis == 3
+    assert d.drift[1][1].scale == 0.5 and d.drift[2][0].kind == abi.TERM_TAN
+    assert d.control[3][0] == 4.0 and d.disturbance[0][0] == 1.0
+    assert (d.ubounds[0].lo, d.ubounds[0].hi) == (-0.4, 0.4)
+    assert m.disturbance_rows() == [0]
+    assert m.drift_at([0.0, 0.0, 0.0, 2.0])[0] == 2.0
+    with pytest.raises(ValueError):
+        hj.SeparableAffineModel([[(abi.TERM_COORD, 1, 1.0)]] * 4, B, C, [])
+    with pytest.raises(ValueError):
+        hj.SeparableAffineModel([[(abi.TERM_COORD, 1, 1.0)] * 3] + [[]] * 3)
