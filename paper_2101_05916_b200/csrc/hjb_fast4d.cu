@@ -2089,7 +2089,10 @@ struct Ax0March {
 constexpr int kEno3gThreads = HJB_ENO3G_THREADS;
 // Lax-Friedrichs: per-cell drifts / alphas and all four (D-, D+) pairs live
 // at once (lf_hhat couples the axes), so fewer threads with more registers
-constexpr int kEno3gThreadsLF = 384;
+#ifndef HJB_ENO3G_THREADS_LF
+#define HJB_ENO3G_THREADS_LF 384
+#endif
+constexpr int kEno3gThreadsLF = HJB_ENO3G_THREADS_LF;
 __host__ __device__ constexpr int eno3g_threads(int sch) {
   return sch ? kEno3gThreadsLF : kEno3gThreads;
 }
