@@ -434,7 +434,14 @@ void fill_lf(const DevModel& m, int scheme, const double* galpha, int& lf, LfPar
     lp.uprod_hi[d] = uc >= 0 ? lp.ucoef[d] * lp.uhi[uc] : 0.0;
     lp.dprod_lo[d] = dc >= 0 ? lp.dcoef[d] * lp.dlo[dc] : 0.0;
     lp.dprod_hi[d] = dc >= 0 ? lp.dcoef[d] * lp.dhi[dc] : 0.0;
+    lp.uch[d] = uc;
+    lp.dch[d] = dc;
   }
+  lp.single = 1;
+  for (int d = 0; d < 4; ++d)
+    for (int e = d + 1; e < 4; ++e)
+      if ((lp.uch[d] >= 0 && lp.uch[d] == lp.uch[e]) || (lp.dch[d] >= 0 && lp.dch[d] == lp.dch[e]))
+        lp.single = 0;
 }
 
 }  // namespace hjb
@@ -488,8 +495,8 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
   };
   const char* kc = std::getenv("HJB_KCELLS");
   const char* mt = std::getenv("HJB_MAXT");
-  if (f.lf) {  // one Lax-Friedrichs variant (112 registers: no spills)
-    configure(2, 448);
+  if (f.lf) {  // one Lax-Friedrichs variant (no spills; run-time shapes: 384 threads)
+    configure(2, shape == kShapeGen ? 384u : 448u);
     return HJB_OK;
   }
   if (f.pv || f.target) {  // one plane-varying-bounds / target-set variant

@@ -472,6 +472,55 @@ __device__ __forceinline__ double lf_hhat(const LfParams& lp, const double* dmv,
   return hh;
 }
 
+// lf_hhat with the rows' input channels read at run time (LfParams::uch /
+// dch, one input term per row; k_fast4d<ShapeGen>).  A channel entering one
+// row decides on that row's product sign (lp.single, uniform); otherwise
+// its coefficient is summed over its rows in row order, as
+// extremal_inputs does.
+__device__ __forceinline__ double lf_hhat_rt(const LfParams& lp, const double* dmv,
+                                             const double* dpv, const double* dr,
+                                             const double* alh) {
+  double pq[4];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) pq[d] = 0.5 * (dmv[d] + dpv[d]);
+  bool uh[4], dh[4];  // per row: its channel takes the hi bound
+  if (lp.single) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      uh[d] = pq[d] * lp.ucoef[d] < 0.0;
+      dh[d] = pq[d] * lp.dcoef[d] > 0.0;
+    }
+  } else {
+    double cu[3] = {0.0, 0.0, 0.0}, cd[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (lp.uch[d] == j) cu[j] += pq[d] * lp.ucoef[d];
+        if (lp.dch[d] == j) cd[j] += pq[d] * lp.dcoef[d];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const double u = lp.uch[d] == 0 ? cu[0] : (lp.uch[d] == 1 ? cu[1] : cu[2]);
+      const double w = lp.dch[d] == 0 ? cd[0] : (lp.dch[d] == 1 ? cd[1] : cd[2]);
+      uh[d] = !(u > 0.0) && u < 0.0;
+      dh[d] = w > 0.0;
+    }
+  }
+  double hh = 0.0;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    double fi = dr[d];
+    if (lp.uch[d] >= 0) fi += uh[d] ? lp.uprod_hi[d] : lp.uprod_lo[d];
+    if (lp.dch[d] >= 0) fi += dh[d] ? lp.dprod_hi[d] : lp.dprod_lo[d];
+    hh += pq[d] * fi;
+  }
+#pragma unroll
+  for (int d = 0; d < 4; ++d) hh += alh[d] * (dpv[d] - dmv[d]);
+  return hh;
+}
+
 // Row drifts and LF dissipation coefficients of a cell (loop invariant):
 // rows without inputs have drift == their slope, alpha == |drift| when no
 // flow_bounds table exists; SCH 2 takes the global alpha.  alh = alpha * 0.5.
@@ -808,7 +857,36 @@ __global__ void __launch_bounds__(MAXT, 1)
       // dissipation coefficients, loop invariant (rows without inputs have
       // drift == pos and alpha == |drift|)
       double lfdr[4][kK], lfal[4][kK];
-      if (SCH != 0) {
+      // run-time shapes: the drifts and alpha*0.5 of the rows in `rows` at
+      // plane p (two-term rows: the drift is the slope pos_, current for p)
+      auto gen_lf_terms = [&](uint32_t rows, uint32_t p) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          if (!(rows & (1u << d))) continue;
+#pragma unroll
+          for (int c = 0; c < kK; ++c) {
+            const uint32_t i3c = min(i3 + c, n3 - 1);
+            const uint32_t ka =
+                !active ? 0u : (a.gax[d] == 0 ? p : pick<S>(a.gax[d], i1, i2, i3c));
+            double dr;
+            if (a.gbx[d] >= 0)
+              dr = pos_[d][c];
+            else
+              dr = a.lp.dr_off[d] >= 0 ? tabs[a.lp.dr_off[d] + ka] : a.lp.dr_const[d];
+            double al;
+            if (SCH == 2)
+              al = a.lp.galpha[d];
+            else if (a.lp.off_alpha[d] >= 0)
+              al = tabs[a.lp.off_alpha[d] + ka];
+            else
+              al = fabs(dr);
+            lfdr[d][c] = dr;
+            lfal[d][c] = al * 0.5;  // lf_hhat's alpha * 0.5
+          }
+        }
+      };
+      if (S::GEN && SCH != 0) gen_lf_terms(0xfu, c0);
+      if (!S::GEN && SCH != 0) {
 #pragma unroll
         for (int c = 0; c < kK; ++c) {
           uint32_t ka[4];
@@ -879,7 +957,10 @@ __global__ void __launch_bounds__(MAXT, 1)
       }
       for (uint32_t i0 = c0; i0 < c1; ++i0) {
         if constexpr (S::GEN) {
-          if (a.gx0) gen_slopes(a.gx0, i0);  // rows on x0: this plane's slopes
+          if (a.gx0) {  // rows on x0: this plane's slopes (and LF terms)
+            gen_slopes(a.gx0, i0);
+            if (SCH != 0) gen_lf_terms(a.gx0, i0);
+          }
         }
         if (PV == 2) {
           // per-node disturbance bounds: this cell's slopes and shapes of the
@@ -1027,7 +1108,8 @@ __global__ void __launch_bounds__(MAXT, 1)
               drc[d] = lfdr[d][c];
               alc[d] = lfal[d][c];
             }
-            const double hh = lf_hhat<S>(a.lp, dmv, dpv, drc, alc);
+            const double hh = S::GEN ? lf_hhat_rt(a.lp, dmv, dpv, drc, alc)
+                                     : lf_hhat<S>(a.lp, dmv, dpv, drc, alc);
             double st = v[c] + a.dt * hh;
             if (TG) st = tl[c] < st ? tl[c] : st;
             out[c] = st > cc[c] ? st : cc[c];
@@ -2624,7 +2706,15 @@ static int fast4d_shape_g(const DevGrid& g, const DevModel& m);
 int fast4d_shape(const DevGrid& g, const DevModel& m, int scheme) {
   const int sh = fast4d_shape_g(g, m);
   if (sh < 0 || scheme == 0) return sh;
-  if (sh == kShapeGen) return -1;  // Lax-Friedrichs: compiled shapes only
+  if (sh == kShapeGen) {  // Lax-Friedrichs, run-time channels: one input term per row
+    if (m.m > 3 || m.p > 3) return -1;
+    for (int d = 0; d < 4; ++d) {
+      const DevRow& r = m.row[d];
+      if (r.n_uadd > 1 || r.n_dterm > 1) return -1;
+      if ((r.n_uadd && r.uch[0] >= 3) || (r.n_dterm && r.dch[0] >= 3)) return -1;
+    }
+    return sh;
+  }
   // Lax-Friedrichs: each row's inputs must be the shape's (one term each)
   if (m.m > 3 || m.p > 3) return -1;
   for (int d = 0; d < 4; ++d) {
@@ -2961,6 +3051,14 @@ static void launch_shape(const Fast4dArgs& a, cudaStream_t s) {
 // run-time-shape variant: Godunov, constant bounds, no target set (the host
 // sends the other cases to the generic kernel); kcells 2 only
 static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.lf == 1) {  // Lax-Friedrichs: 384 threads (the run-time channels and
+    launch_one<ShapeGen, 2, 384, 1>(a, s);  // per-cell row terms need ~150 registers)
+    return;
+  }
+  if (a.lf == 2) {
+    launch_one<ShapeGen, 2, 384, 2>(a, s);
+    return;
+  }
   if (a.ms) {
     launch_one<ShapeGen, 2, 576, 0, 0, false, false, true>(a, s);
     return;
@@ -2974,7 +3072,7 @@ static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   t_attr_err = cudaSuccess;
-  if (shape == kShapeGen && (a.lf || a.pv || a.target || a.kcells != 2))
+  if (shape == kShapeGen && (a.pv || a.target || a.kcells != 2))
     return cudaErrorInvalidValue;  // not a configuration of the run-time-shape variant
   if (shape == 0)
     launch_shape<ShapePlanarD0>(a, s);

@@ -23,6 +23,11 @@ struct LfParams {
   // the row's input products with each bound, formed on the host exactly as
   // the Hamiltonian forms them (B u* / C d*: ucoef * ulo[ch] etc.)
   double uprod_lo[4], uprod_hi[4], dprod_lo[4], dprod_hi[4];
+  // run-time-shape variant: the control / disturbance channel of each row
+  // (-1 none; one input term per row) and whether every channel enters at
+  // most one row (its input then follows that row's product sign alone)
+  int uch[4], dch[4];
+  int single;
 };
 
 struct Fast4dArgs {

@@ -402,7 +402,7 @@ int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, doubl
     fill_tables(p, f);
     fill_lf(p.hm.dm, scheme, galpha, f);
     if (f.lf) {  // the Lax-Friedrichs variant's CTA size
-      f.maxthreads = 448;
+      f.maxthreads = p.shape == kShapeGen ? 384u : 448u;
       f.cbeg = geo.cbeg;
       f.cend = geo.cend;
       fast4d_config(gloc, sms, f);

@@ -2,7 +2,7 @@
 (k_fast4d<ShapeGen>) against the generic kernel (HJB_FAST=0), next to the
 compiled-shape kernel on the config-2 model, at one grid size.
 
-usage: python scripts/bench_gen4d.py [n=51] [iters=300]
+usage: python scripts/bench_gen4d.py [n=51] [iters=300] [gd|lf]
 Prints one JSON line per (model, kernel).
 """
 import json
@@ -24,7 +24,10 @@ def main():
     ctx = hj.Context(0)
     g = hj.Grid([(-5.0, 5.0, n), (-2.0, 2.0, n), (-0.35, 0.35, n), (-1.5, 1.5, n)])
     c = hj.signed_distance_band(g, 0, -4.0, 4.0, ctx=ctx)
+    scheme = sys.argv[3] if len(sys.argv) > 3 else "gd"
     cfg = hj.SolveConfig(tolerance=1e-12, max_iters=iters)
+    if scheme == "lf":
+        cfg.scheme = hj.LAX_FRIEDRICHS
     os.environ["HJB_MS"] = "0"
     runs = [(name, make(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)] * nd))
             for name, (make, nd) in sorted(MODELS.items())]
@@ -33,10 +36,12 @@ def main():
     for name, model, db in runs:
         for fast in ("1", "0"):
             os.environ["HJB_FAST"] = fast
-            hj.solve(c, c, model, db, hj.SolveConfig(max_iters=5), ctx=ctx)  # autotune, warm
+            warm = hj.SolveConfig(max_iters=5)
+            warm.scheme = cfg.scheme
+            hj.solve(c, c, model, db, warm, ctx=ctx)  # autotune, warm
             r = hj.solve(c, c, model, db, cfg, ctx=ctx)
             us = r.wall_seconds / r.iterations * 1e6
-            print(json.dumps({"model": name, "grid": f"{n}^4", "kernel": r.kernel,
+            print(json.dumps({"model": name, "grid": f"{n}^4", "scheme": scheme, "kernel": r.kernel,
                               "sweep_us": round(us, 2), "iterations": r.iterations,
                               "gcell_per_s": round(g.size() / us * 1e-3, 2)}), flush=True)
     os.environ.pop("HJB_FAST", None)

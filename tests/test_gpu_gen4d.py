@@ -104,6 +104,62 @@ def test_gen4d_matches_oracle(gpu_ctx, oracle, monkeypatch, name, dims, ms):
     _check(got, want)
 
 
+@pytest.mark.parametrize("diss", ["per_node", "global"])
+@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (9, 21, 19, 23), (33, 5, 6, 101)])
+@pytest.mark.parametrize("name", sorted(MODELS))
+def test_gen4d_lax_friedrichs_matches_oracle(gpu_ctx, oracle, name, dims, diss):
+    """Lax-Friedrichs on the run-time-shape variant (per-node / global alpha,
+    the rows' input channels read at run time) against the oracle."""
+    g, model, db, c = _setup(name, dims)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=30, scheme=hj.LAX_FRIEDRICHS,
+                         dissipation=hj.GLOBAL if diss == "global" else hj.PER_NODE)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.kernel == "fast4d_gen"
+    _check(got, want)
+
+
+def test_gen4d_lax_friedrichs_shared_channel(gpu_ctx, oracle):
+    """One disturbance channel entering two rows (LfParams::single = 0): the
+    channel's coefficient is summed over its rows in row order."""
+    B = np.zeros((4, 1))
+    B[3, 0] = 2.0
+    Cm = np.zeros((4, 1))
+    Cm[0, 0] = 1.0
+    Cm[2, 0] = -0.5
+    model = hj.SeparableAffineModel(
+        [[(C_, 1, 1.0)], [(C_, 3, -0.7)], [(C_, 3, 1.0)], [(C_, 1, -1.0)]], B, Cm,
+        [hj.Interval(-1.0, 1.0)])
+    g = hj.Grid([(-5.0, 5.0, 13), (-2.0, 2.0, 11), (-0.35, 0.35, 9), (-1.5, 1.5, 14)])
+    db = hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    for diss in (hj.PER_NODE, hj.GLOBAL):
+        cfg = hj.SolveConfig(tolerance=1e-4, max_iters=30, scheme=hj.LAX_FRIEDRICHS,
+                             dissipation=diss)
+        got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+        assert got.kernel == "fast4d_gen"
+        _check(got, oracle.solve(c, c, model, db, cfg))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_gen4d_lax_friedrichs_sharded(gpu_ctx, P):
+    """The slab-partitioned LF solve (in-process ranks) on the run-time-shape
+    variant equals the single-GPU solve bit for bit."""
+    import torch
+    from paper_2101_05916_b200 import sharded
+    g, model, db, c = _setup("inputs", (21, 13, 11, 17))
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=40, scheme=hj.LAX_FRIEDRICHS)
+    ref = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert ref.kernel == "fast4d_gen"
+    ct = torch.tensor(c.values(), device="cuda")
+    out = torch.full_like(ct, float("nan"))
+    torch.cuda.synchronize()
+    r = sharded.solve_sharded_local_dev(P, g, model, db, ct.data_ptr(), ct.data_ptr(),
+                                        out.data_ptr(), cfg, gpu_ctx, history_capacity=40)
+    assert r.iterations == ref.iterations and r.dt == ref.dt
+    assert same(out.cpu().numpy(), ref.value.values())
+
+
 @pytest.mark.parametrize("name", sorted(MODELS))
 def test_gen4d_to_convergence(gpu_ctx, oracle, monkeypatch, name):
     """A whole solve to convergence: identical iteration count (north_star)."""
@@ -133,16 +189,23 @@ def test_gen4d_matches_generic_kernel(gpu_ctx, monkeypatch, name):
 
 
 def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
-    """Lax-Friedrichs, a target set and ENO/TVD-RK stay on the generic kernels
-    for a run-time-shape model (still bitwise against the oracle)."""
+    """A target set and ENO/TVD-RK stay on the generic kernels for a
+    run-time-shape model, and so does LF for a row with two input terms
+    (still bitwise against the oracle)."""
     g = hj.Grid([(-5.0, 5.0, 11), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 8)])
     c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
     cfg = hj.SolveConfig(tolerance=1e-4, max_iters=20)
     model, db = mixed_model(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    B2 = np.zeros((4, 2))
+    B2[3, 0], B2[3, 1] = 1.0, 0.5
+    two = hj.SeparableAffineModel(
+        [[(C_, 1, 1.0)], [(C_, 3, -0.7)], [(C_, 3, 1.0)], [(C_, 1, -1.0)]], B2, None,
+        [hj.Interval(-1.0, 1.0), hj.Interval(-0.5, 0.5)])
+    db0 = hj.IntervalField.constant(g, [])
     lf = hj.SolveConfig(tolerance=1e-4, max_iters=20, scheme=hj.LAX_FRIEDRICHS)
-    got = hj.solve(c, c, model, db, lf, ctx=gpu_ctx)
+    got = hj.solve(c, c, two, db0, lf, ctx=gpu_ctx)
     assert got.kernel == "generic"
-    _check(got, oracle.solve(c, c, model, db, lf))
+    _check(got, oracle.solve(c, c, two, db0, lf))
     ho = hj.SolveConfig(tolerance=1e-4, max_iters=10, spatial_order=3, time_order=3)
     got = hj.solve(c, c, model, db, ho, ctx=gpu_ctx)
     assert got.kernel == "ho_generic"
