@@ -59,10 +59,11 @@ def main():
     # compiled shapes, per-sweep and multi-sweep launches
     from test_gpu_gen4d import mixed_model  # noqa: E402
     mm, mdb = mixed_model(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
-    for label, env in (("k_fast4d run-time shape", {"HJB_MS": "0"}),
-                       ("k_fast4d run-time shape multi-sweep", {"HJB_MS": "1"})):
+    for label, env, extra in (("k_fast4d run-time shape", {"HJB_MS": "0"}, {}),
+                              ("k_fast4d run-time shape multi-sweep", {"HJB_MS": "1"}, {}),
+                              ("k_fast4d run-time shape lf", {}, {"scheme": hj.LAX_FRIEDRICHS})):
         os.environ.update(env)
-        cfg = hj.SolveConfig(**base)
+        cfg = hj.SolveConfig(**base, **extra)
         r = hj.solve(c, c, mm, mdb, cfg, ctx=ctx)
         check(label, r.value.values(), ora.solve(c, c, mm, mdb, cfg).value.values())
         for k in env:
