@@ -808,7 +808,6 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
   // target set: the 4D fast path's TG variant (Godunov, constant bounds);
   // everything else runs the generic sweep
   if (cfg->target && scheme_of(cfg) != kGodunov) shape = -1;
-  if (cfg->target && shape == kShapeGen) shape = -1;  // no TG variant of the run-time shape
   const int shape_pv = (shape < 0 && fast_enabled() && db->per_node &&
                         scheme_of(cfg) == kGodunov && !cfg->target)
                            ? fast4d_shape_pv(g, hm.dm)

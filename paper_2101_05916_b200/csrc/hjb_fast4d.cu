@@ -1135,7 +1135,8 @@ __global__ void __launch_bounds__(MAXT, 1)
             hh += flux(2, dm2, dp2);
             hh += flux(3, f3[c], f3[c + 1]);
             dm0[c] = dp0;
-            const double st = v[c] + a.dt * hh;
+            double st = v[c] + a.dt * hh;
+            if (TG) st = tl[c] < st ? tl[c] : st;  // target set: std::min(stepped, l)
             out[c] = st > cc[c] ? st : cc[c];
             const double dv = fabs(out[c] - v[c]);
             if (valid[c] && dv > mdv) mdv = dv;
@@ -3063,6 +3064,10 @@ static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
     launch_one<ShapeGen, 2, 576, 0, 0, false, false, true>(a, s);
     return;
   }
+  if (a.target) {  // target set (Godunov, constant bounds, field constraint)
+    launch_one<ShapeGen, 2, 576, 0, 0, false, true>(a, s);
+    return;
+  }
   const bool cp = a.cplane != nullptr;
   if (a.maxthreads == 448)
     cp ? launch_one<ShapeGen, 2, 448, 0, 0, true>(a, s) : launch_one<ShapeGen, 2, 448>(a, s);
@@ -3072,7 +3077,7 @@ static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   t_attr_err = cudaSuccess;
-  if (shape == kShapeGen && (a.pv || a.target || a.kcells != 2))
+  if (shape == kShapeGen && (a.pv || a.kcells != 2 || (a.target && a.lf)))
     return cudaErrorInvalidValue;  // not a configuration of the run-time-shape variant
   if (shape == 0)
     launch_shape<ShapePlanarD0>(a, s);

@@ -189,9 +189,9 @@ def test_gen4d_matches_generic_kernel(gpu_ctx, monkeypatch, name):
 
 
 def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
-    """A target set and ENO/TVD-RK stay on the generic kernels for a
-    run-time-shape model, and so does LF for a row with two input terms
-    (still bitwise against the oracle)."""
+    """ENO/TVD-RK stays on the generic kernels for a run-time-shape model, and
+    so does LF for a row with two input terms (still bitwise against the
+    oracle)."""
     g = hj.Grid([(-5.0, 5.0, 11), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 8)])
     c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
     cfg = hj.SolveConfig(tolerance=1e-4, max_iters=20)
@@ -210,10 +210,7 @@ def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
     got = hj.solve(c, c, model, db, ho, ctx=gpu_ctx)
     assert got.kernel == "ho_generic"
     _check(got, oracle.solve(c, c, model, db, ho))
-    tl = hj.ScalarField(g, band_np(g, 1, -1.0, 1.0))
-    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx, target=tl)
-    assert got.kernel == "generic"
-    _check(got, oracle.solve(c, c, model, db, cfg, target=tl))
+
 
 
 @pytest.mark.parametrize("P", [2, 3])
@@ -249,3 +246,15 @@ def test_gen4d_x0_rows_not_sharded(gpu_ctx):
     with pytest.raises(hj.Unsupported):
         sharded.solve_sharded_local_dev(2, g, model, db, ct.data_ptr(), ct.data_ptr(),
                                         out.data_ptr(), hj.SolveConfig(max_iters=5), gpu_ctx)
+
+
+@pytest.mark.parametrize("name", sorted(MODELS))
+def test_gen4d_target_set(gpu_ctx, oracle, name):
+    """Reach-avoid update max(c, min(l, stepped)) on the run-time-shape
+    variant (the target-set instantiation) against the restatement."""
+    g, model, db, c = _setup(name, (13, 11, 9, 14))
+    tl = hj.ScalarField(g, band_np(g, 1, -1.0, 1.0))
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=30)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx, target=tl)
+    assert got.kernel == "fast4d_gen"
+    _check(got, oracle.solve(c, c, model, db, cfg, target=tl))
