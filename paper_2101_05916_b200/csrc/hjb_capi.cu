@@ -500,7 +500,7 @@ int fast4d_choose(hjb_context* ctx, const DevGrid& g, int shape, const double* i
     return HJB_OK;
   }
   if (f.pv || f.target) {  // one plane-varying-bounds / target-set variant
-    configure(2, 576);
+    configure(2, shape == kShapeGen ? (f.pv == 2 ? 384u : 448u) : 576u);
     return HJB_OK;
   }
   if (kc || mt) {
@@ -827,7 +827,10 @@ static int solve_impl(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi,
     }
     int ok = 0;
     if ((rc = prepare_pv(ctx, g, hm, db, shape_pv, f, &ok))) return rc;
-    if (ok) shape = shape_pv;
+    if (ok) {
+      shape = shape_pv;
+      fast4d_gen_rows(hm.dm, f);  // run-time shapes: row axes, disturbance rows
+    }
   }
   if (shape >= 0) {
     // padded internal layout for the 4D fast path; kernel variant chosen by

@@ -947,6 +947,18 @@ __global__ void __launch_bounds__(MAXT, 1)
       const uint64_t pno = active ? static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3
                                   : 0ull;
       double pl_c[4][kK], ph_c[4][kK], pl_n[4][kK], ph_n[4][kK];
+      // run-time shapes: the disturbance rows' effective slopes per slot
+      // (pos / neg + max / min of the products), formed per plane
+      double gp_[2][kK], gn_[2][kK];
+      if constexpr (S::GEN && PV == 2) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (a.gdrow[q] < 0) continue;
+          const int d = a.gdrow[q];
+          lds_pn<kK>(a.pn_lo[d] + static_cast<uint64_t>(c0) * s0 + pno, pl_c[q]);
+          lds_pn<kK>(a.pn_hi[d] + static_cast<uint64_t>(c0) * s0 + pno, ph_c[q]);
+        }
+      }
       if (PV == 2) {
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
@@ -960,6 +972,40 @@ __global__ void __launch_bounds__(MAXT, 1)
           if (a.gx0) {  // rows on x0: this plane's slopes (and LF terms)
             gen_slopes(a.gx0, i0);
             if (SCH != 0) gen_lf_terms(a.gx0, i0);
+          }
+        }
+        if constexpr (S::GEN && PV != 0) {
+          // dim_slopes order (solver.cpp:67-86): (drift + controls) from the
+          // row's table, then + max / min of the disturbance products
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (a.gdrow[q] < 0) continue;
+            const int d = a.gdrow[q];
+            double bp[kK], bn[kK];
+#pragma unroll
+            for (int c = 0; c < kK; ++c) {  // pos_ / neg_ of row d (unrolled: no local memory)
+              bp[c] = d == 0 ? pos_[0][c] : d == 1 ? pos_[1][c] : d == 2 ? pos_[2][c] : pos_[3][c];
+              bn[c] = d == 0 ? neg_[0][c] : d == 1 ? neg_[1][c] : d == 2 ? neg_[2][c] : neg_[3][c];
+            }
+            if (PV == 1) {
+              const double pt = tabs[a.pv_pt[d] + i0], nt = tabs[a.pv_nt[d] + i0];
+#pragma unroll
+              for (int c = 0; c < kK; ++c) {
+                gp_[q][c] = bp[c] + pt;
+                gn_[q][c] = bn[c] + nt;
+              }
+            } else {
+              if (i0 + 1 < c1) {
+                lds_pn<kK>(a.pn_lo[d] + static_cast<uint64_t>(i0 + 1) * s0 + pno, pl_n[q]);
+                lds_pn<kK>(a.pn_hi[d] + static_cast<uint64_t>(i0 + 1) * s0 + pno, ph_n[q]);
+              }
+#pragma unroll
+              for (int c = 0; c < kK; ++c) {
+                const double x = a.pn_coef[d] * pl_c[q][c], y = a.pn_coef[d] * ph_c[q][c];
+                gp_[q][c] = bp[c] + (x > y ? x : y);
+                gn_[q][c] = bn[c] + (x < y ? x : y);
+              }
+            }
           }
         }
         if (PV == 2) {
@@ -1127,6 +1173,10 @@ __global__ void __launch_bounds__(MAXT, 1)
             // the compiled shapes' LIN rows
             auto flux = [&](int d, double dm, double dp) -> double {
               if (a.glin & (1 << d)) return pos_[d][c] * (sign_clear(pos_[d][c]) ? dp : dm);
+              if (PV != 0) {  // a disturbance row's slopes of this cell and plane
+                if (a.gdrow[0] == d) return godunov_flux(gp_[0][c], gn_[0][c], dm, dp);
+                if (a.gdrow[1] == d) return godunov_flux(gp_[1][c], gn_[1][c], dm, dp);
+              }
               return godunov_flux(pos_[d][c], neg_[d][c], dm, dp);
             };
             double hh = 0.0;
@@ -1205,7 +1255,7 @@ __global__ void __launch_bounds__(MAXT, 1)
         if (PV == 2) {
 #pragma unroll
           for (int d = 0; d < 4; ++d) {
-            if (S::D(d) < 0) continue;
+            if (S::GEN ? (d >= 2 || a.gdrow[d] < 0) : S::D(d) < 0) continue;
 #pragma unroll
             for (int c = 0; c < kK; ++c) {
               pl_c[d][c] = pl_n[d][c];
@@ -2733,15 +2783,20 @@ int fast4d_shape_pv(const DevGrid& g, const DevModel& m) {
   if ((g.n[3] + 3) / 4 * 4 > 256) return -1;  // TMA box extent limit
   int A[4], B[4];
   bool lin[4];
+  bool x0 = false;
+  int ndist = 0;
   for (int d = 0; d < 4; ++d) {
     const DevRow& r = m.row[d];
     if (r.axis_b >= 0 && (r.n_uadd || r.n_dterm || r.constant_drift)) return -1;
     A[d] = r.axis_a;
     B[d] = r.axis_b;
-    if (A[d] == 0 || B[d] == 0) return -1;
+    if (A[d] == 0 || B[d] == 0) x0 = true;
     lin[d] = r.n_uadd == 0 && r.n_dterm == 0;
     if (r.n_dterm > 1) return -1;
+    ndist += r.n_dterm;
   }
+  // run-time shapes: at most two disturbance rows (Fast4dArgs::gdrow)
+  if (x0) return ndist <= 2 ? kShapeGen : -1;
   static const int pa[4] = {1, 2, 2, 2}, pb[4] = {-1, -1, 3, -1};
   static const bool l0[4] = {false, true, true, false}, l1[4] = {true, false, true, false};
   static const int ta[4] = {1, -1, 3, -1}, tb[4] = {-1, -1, -1, -1};
@@ -2756,7 +2811,7 @@ int fast4d_shape_pv(const DevGrid& g, const DevModel& m) {
   if (match(pa, pb, l0, 0)) return 0;
   if (match(pa, pb, l1, 1)) return 1;
   if (match(ta, tb, lt, 2)) return 2;
-  return -1;
+  return ndist <= 2 ? kShapeGen : -1;
 }
 
 static int fast4d_shape_g(const DevGrid& g, const DevModel& m) {
@@ -2804,9 +2859,12 @@ void fast4d_gen_rows(const DevModel& m, Fast4dArgs& a) {
   }
   a.glin = 0;
   a.gx0 = 0;
+  a.gdrow[0] = a.gdrow[1] = -1;
+  int q = 0;
   for (int d = 0; d < 4; ++d) {
     if (m.row[d].n_uadd == 0 && m.row[d].n_dterm == 0) a.glin |= 1 << d;
     if (a.gax[d] == 0 || a.gbx[d] == 0) a.gx0 |= 1 << d;
+    if (m.row[d].n_dterm > 0 && q < 2) a.gdrow[q++] = d;
   }
 }
 
@@ -3064,8 +3122,18 @@ static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
     launch_one<ShapeGen, 2, 576, 0, 0, false, false, true>(a, s);
     return;
   }
+  // plane-varying / per-node disturbance bounds and target sets: 448 threads
+  // (the per-cell slopes of every row do not fit the 576-thread register cap)
+  if (a.pv == 1) {
+    launch_one<ShapeGen, 2, 448, 0, 1>(a, s);
+    return;
+  }
+  if (a.pv == 2) {  // per-node: 384 threads (the pencil's lo / hi windows too)
+    launch_one<ShapeGen, 2, 384, 0, 2>(a, s);
+    return;
+  }
   if (a.target) {  // target set (Godunov, constant bounds, field constraint)
-    launch_one<ShapeGen, 2, 576, 0, 0, false, true>(a, s);
+    launch_one<ShapeGen, 2, 448, 0, 0, false, true>(a, s);
     return;
   }
   const bool cp = a.cplane != nullptr;
@@ -3077,7 +3145,7 @@ static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
 
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   t_attr_err = cudaSuccess;
-  if (shape == kShapeGen && (a.pv || a.kcells != 2 || (a.target && a.lf)))
+  if (shape == kShapeGen && (a.kcells != 2 || (a.target && a.lf) || (a.pv && (a.lf || a.target))))
     return cudaErrorInvalidValue;  // not a configuration of the run-time-shape variant
   if (shape == 0)
     launch_shape<ShapePlanarD0>(a, s);

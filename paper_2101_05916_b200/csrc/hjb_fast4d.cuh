@@ -77,6 +77,9 @@ struct Fast4dArgs {
   int glin;
   // gx0: bit d set when row d's slopes vary along x0 (re-formed every plane)
   int gx0;
+  // run-time shapes with per-node / plane-varying bounds (pv 1 / 2): the rows
+  // with a disturbance term, at most two (slot s -> row gdrow[s], -1 none)
+  int gdrow[2];
   const double* c;  // padded constraint
   // constraint that varies along axis 0 only (signed distance to a set in
   // x0, every BASELINE 4D config): c[i0] per plane, the padded field unused

@@ -258,3 +258,48 @@ def test_gen4d_target_set(gpu_ctx, oracle, name):
     got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx, target=tl)
     assert got.kernel == "fast4d_gen"
     _check(got, oracle.solve(c, c, model, db, cfg, target=tl))
+
+
+def _per_node_db(g, nd, kind, seed=5):
+    """Per-node bounds for nd channels: 'axis0' varies along x0 only (the
+    plane-varying variant), 'mixed' varies at every node with lo / hi of
+    both signs (slopes whose shapes change cell to cell)."""
+    rng = np.random.default_rng(seed)
+    lo, hi = [], []
+    shape = g.shape
+    for _ in range(nd):
+        if kind == "axis0":
+            base = -0.5 + 0.2 * rng.random(shape[0])
+            a = np.broadcast_to(base.reshape(-1, 1, 1, 1), shape).reshape(-1).copy()
+            b = a + 0.3 + 0.4 * np.broadcast_to(rng.random(shape[0]).reshape(-1, 1, 1, 1),
+                                                shape).reshape(-1)
+        else:
+            a = -0.4 + 0.8 * (rng.random(g.size()) - 0.5)
+            b = a + 0.6 * rng.random(g.size())
+        lo.append(a)
+        hi.append(b)
+    return hj.IntervalField(g, nd, lo=lo, hi=hi)
+
+
+@pytest.mark.parametrize("kind", ["axis0", "mixed"])
+@pytest.mark.parametrize("dims", [(13, 8, 11, 6), (9, 21, 19, 23)])
+@pytest.mark.parametrize("name", ["mixed", "inputs", "x0rows"])
+def test_gen4d_per_node_bounds(gpu_ctx, oracle, monkeypatch, name, dims, kind):
+    """Per-node disturbance bounds (plane-varying and every-node) on the
+    run-time-shape variant: a disturbance row's slopes are (drift + controls)
+    + max / min of its products per cell and plane; bitwise vs the oracle and
+    vs the generic kernel (HJB_PN=0)."""
+    make, nd = MODELS[name]
+    n0, n1, n2, n3 = dims
+    g = hj.Grid([(-5.0, 5.0, n0), (-2.0, 2.0, n1), (-0.35, 0.35, n2), (-1.5, 1.5, n3)])
+    model = make()
+    db = _per_node_db(g, nd, kind)
+    c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
+    cfg = hj.SolveConfig(tolerance=1e-6, max_iters=30)
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.kernel == "fast4d_gen"
+    _check(got, want)
+    monkeypatch.setenv("HJB_PN", "0")
+    gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert same(gen.value.values(), got.value.values())
