@@ -2,7 +2,7 @@
 (k_fast4d<ShapeGen>) against the generic kernel (HJB_FAST=0), next to the
 compiled-shape kernel on the config-2 model, at one grid size.
 
-usage: python scripts/bench_gen4d.py [n=51] [iters=300] [gd|lf]
+usage: python scripts/bench_gen4d.py [n=51] [iters=300] [gd|lf] [const|axis0|node]
 Prints one JSON line per (model, kernel).
 """
 import json
@@ -15,7 +15,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
 
 from paper_2101_05916_b200 import configs  # noqa: E402
 from paper_2101_05916_b200 import hjsafe as hj  # noqa: E402
-from test_gpu_gen4d import MODELS  # noqa: E402
+from test_gpu_gen4d import MODELS, _per_node_db  # noqa: E402
 
 
 def main():
@@ -29,10 +29,16 @@ def main():
     if scheme == "lf":
         cfg.scheme = hj.LAX_FRIEDRICHS
     os.environ["HJB_MS"] = "0"
-    runs = [(name, make(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)] * nd))
-            for name, (make, nd) in sorted(MODELS.items())]
+    bounds = sys.argv[4] if len(sys.argv) > 4 else "const"
+
+    def db_of(nd):
+        if bounds == "const" or nd == 0:
+            return hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)] * nd)
+        return _per_node_db(g, nd, bounds)
+    runs = [(name, make(), db_of(nd)) for name, (make, nd) in sorted(MODELS.items())
+            if bounds == "const" or nd > 0]
     w = configs.config2(n)
-    runs.append(("config2 (compiled shape)", w.model, w.dbounds()))
+    runs.append(("config2 (compiled shape)", w.model, w.dbounds() if bounds == "const" else db_of(1)))
     for name, model, db in runs:
         for fast in ("1", "0"):
             os.environ["HJB_FAST"] = fast
@@ -41,7 +47,8 @@ def main():
             hj.solve(c, c, model, db, warm, ctx=ctx)  # autotune, warm
             r = hj.solve(c, c, model, db, cfg, ctx=ctx)
             us = r.wall_seconds / r.iterations * 1e6
-            print(json.dumps({"model": name, "grid": f"{n}^4", "scheme": scheme, "kernel": r.kernel,
+            print(json.dumps({"model": name, "grid": f"{n}^4", "scheme": scheme, "bounds": bounds,
+                              "kernel": r.kernel,
                               "sweep_us": round(us, 2), "iterations": r.iterations,
                               "gcell_per_s": round(g.size() / us * 1e-3, 2)}), flush=True)
     os.environ.pop("HJB_FAST", None)
