@@ -1819,12 +1819,14 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
           pos_[d][c] = pos_[d][0];
           neg_[d][c] = neg_[d][0];
         } else {
-          const uint32_t ka = pick<S>(S::A(d), ci1, ci2, min(i3 + c, n3 - 1));
-          if (S::B(d) < 0) {
+          // (run-time shapes: the row's axes from Ho4dArgs::gax / gbx)
+          const int ax_a = S::GEN ? a.gax[d] : S::A(d), ax_b = S::GEN ? a.gbx[d] : S::B(d);
+          const uint32_t ka = pick<S>(ax_a, ci1, ci2, min(i3 + c, n3 - 1));
+          if (ax_b < 0) {
             pos_[d][c] = __ldg(a.tab + a.off_pos[d] + ka);
             neg_[d][c] = __ldg(a.tab + a.off_neg[d] + ka);
           } else {
-            const uint32_t kb = pick<S>(S::B(d), ci1, ci2, min(i3 + c, n3 - 1));
+            const uint32_t kb = pick<S>(ax_b, ci1, ci2, min(i3 + c, n3 - 1));
             const double dr = __ldg(a.tab + a.off_a[d] + ka) + __ldg(a.tab + a.off_b[d] + kb);
             pos_[d][c] = dr;
             neg_[d][c] = dr;
@@ -1846,7 +1848,28 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
     }
     // Lax-Friedrichs: the rows' drifts and alphas (loop invariant)
     double lfdr[4][kK], lfal[4][kK];
-    if (SCH != 0) {
+    if (SCH != 0 && S::GEN) {  // run-time shapes: drift, alpha * 0.5 per row and cell
+#pragma unroll
+      for (int c = 0; c < kK; ++c) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          const uint32_t ka = pick<S>(a.gax[d], ci1, ci2, min(i3 + c, n3 - 1));
+          const double dr = a.gbx[d] >= 0 ? pos_[d][c]
+                                          : (a.lp.dr_off[d] >= 0 ? __ldg(a.tab + a.lp.dr_off[d] + ka)
+                                                                 : a.lp.dr_const[d]);
+          double al;
+          if (SCH == 2)
+            al = a.lp.galpha[d];
+          else if (a.lp.off_alpha[d] >= 0)
+            al = __ldg(a.tab + a.lp.off_alpha[d] + ka);
+          else
+            al = fabs(dr);
+          lfdr[d][c] = dr;
+          lfal[d][c] = al * 0.5;
+        }
+      }
+    }
+    if (SCH != 0 && !S::GEN) {
 #pragma unroll
       for (int c = 0; c < kK; ++c) {
         uint32_t ka[4];
@@ -2086,7 +2109,16 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
             drc[d] = lfdr[d][c];
             alc[d] = lfal[d][c];
           }
-          hh = lf_hhat<S>(a.lp, dm4, dp4, drc, alc);
+          hh = S::GEN ? lf_hhat_rt(a.lp, dm4, dp4, drc, alc) : lf_hhat<S>(a.lp, dm4, dp4, drc, alc);
+        } else if (S::GEN) {
+          // run-time shapes: hhat = 0.0, += godunov_flux of each axis in order
+          // (input-free rows: the upwind product, as the compiled LIN rows)
+          hh = 0.0;
+#pragma unroll
+          for (int d = 0; d < 4; ++d)
+            hh += (a.glin & (1 << d))
+                      ? pos_[d][c] * (sign_clear(pos_[d][c]) ? dpv[d][c] : dmv[d][c])
+                      : godunov_flux(pos_[d][c], neg_[d][c], dmv[d][c], dpv[d][c]);
         } else {
           double h[4];
 #pragma unroll
@@ -3191,9 +3223,9 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
   {
     const uint32_t R = (uint32_t)a.order;
     const char* ek = std::getenv("HJB_HO_KC");
-    a.kc = (ek && std::atoi(ek) == 1 && a.lf == 0) ? 1u : 2u;  // LF: 2-cell pencils
+    a.kc = (ek && std::atoi(ek) == 1 && a.lf == 0 && !a.gen) ? 1u : 2u;  // LF / run-time shapes: 2 cells
     const char* eg = std::getenv("HJB_HO_ENO3G");
-    a.eno3g = (R == 3 && a.kc == 2 && !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
+    a.eno3g = (R == 3 && a.kc == 2 && !a.gen && !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
     const uint32_t nbar = 2u;  // mbarriers per ring slot
     const uint32_t maxc =
         (uint32_t)(a.eno3g ? eno3g_threads(a.lf) : ho4t_maxthreads(a.order, (int)a.kc)) - 32;
@@ -3424,11 +3456,23 @@ cudaError_t ho4d_make_maps(Ho4dArgs& a) {
   return cudaSuccess;
 }
 
+// run-time-shape stages: the TMA-staged k_ho4t only (2-cell pencils)
+static cudaError_t ho4d_gen(const Ho4dArgs& a, cudaStream_t s) {
+  if (!a.tma || a.kc != 2 || a.eno3g) return cudaErrorInvalidValue;
+  switch (a.order) {
+    case 1: ho4t_launch<ShapeGen, 1>(a, s); break;
+    case 2: ho4t_launch<ShapeGen, 2>(a, s); break;
+    default: ho4t_launch<ShapeGen, 3>(a, s); break;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ho4d(const Ho4dArgs& a, int shape, cudaStream_t s) {
   t_attr_err = cudaSuccess;
   const cudaError_t e = shape == 0   ? ho4d_shape<ShapePlanarD0>(a, s)
                         : shape == 1 ? ho4d_shape<ShapePlanarD1>(a, s)
-                                     : ho4d_shape<ShapeTwin>(a, s);
+                        : shape == 2 ? ho4d_shape<ShapeTwin>(a, s)
+                                     : ho4d_gen(a, s);
   return t_attr_err != cudaSuccess ? t_attr_err : e;
 }
 

@@ -168,6 +168,11 @@ struct Ho4dArgs {
   // 1: ENO3 Godunov stage in k_eno3g (face-shared choices, patched boxes,
   //    three barriers per ring slot); 0: k_ho4t
   int eno3g;
+  // run-time row shapes (k_ho4t<ShapeGen>, set before ho4d_config, which
+  // then keeps k_eno3g off): the rows' table axes (no row on x0) and the
+  // input-free rows, as Fast4dArgs::gax / gbx / glin
+  int gen;
+  int gax[4], gbx[4], glin;
   // ghost widths of the stage-buffer layout [n0][n1 + 2gh][n2 + 2gh][n3p + 2g3]
   // (k_eno3g: 3 and 4; k_ho4t / k_ho4d: 0, the plain padded layout)
   uint32_t gh, g3;

@@ -74,13 +74,21 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   const char* fe = std::getenv("HJB_FAST");
   int shape = (fe && std::strcmp(fe, "0") == 0) ? -1 : fast4d_shape(g, m, scheme_id(cfg));
   if (cfg->target) shape = -1;  // target sets run the generic stage kernel
-  if (shape == kShapeGen) shape = -1;  // ENO/TVD-RK 4D kernels: compiled shapes only
+  // run-time row shapes: k_ho4t<ShapeGen> unless a row depends on x0 (the
+  // march axis of the stage kernels keeps its slopes loop invariant)
+  Fast4dArgs gr;
+  std::memset(&gr, 0, sizeof gr);
+  if (shape == kShapeGen) {
+    fast4d_gen_rows(m, gr);
+    if (gr.gx0) shape = -1;
+  }
   if (shape >= 0 && scheme_id(cfg) != kGodunov) {
     // Lax-Friedrichs runs only in the TMA-staged kernel (k_ho4t)
     Ho4dArgs t;
     std::memset(&t, 0, sizeof t);
     t.order = cfg->spatial_order > 3 ? 3 : (cfg->spatial_order < 1 ? 1 : cfg->spatial_order);
     t.lf = 1;
+    t.gen = shape == kShapeGen ? 1 : 0;
     ho4d_config(g, sm_count(ctx->device), t);
     if (!t.tma) shape = -1;
   }
@@ -91,7 +99,19 @@ int ho_solve(hjb_context* ctx, const DevGrid& g, const DevModel& m, const double
   if (shape >= 0) {
     h4.order = cfg->spatial_order > 3 ? 3 : (cfg->spatial_order < 1 ? 1 : cfg->spatial_order);
     fill_lf(m, scheme_id(cfg), galpha, h4.lf, h4.lp);
+    if (shape == kShapeGen) {
+      h4.gen = 1;
+      for (int d = 0; d < 4; ++d) {
+        h4.gax[d] = gr.gax[d];
+        h4.gbx[d] = gr.gbx[d];
+      }
+      h4.glin = gr.glin;
+    }
     ho4d_config(g, sm_count(ctx->device), h4);
+    if (shape == kShapeGen && !h4.tma) {  // no TMA configuration: the generic stage kernel
+      shape = -1;
+      std::memset(&h4, 0, sizeof h4);
+    }
   }
   const size_t pbytes = shape >= 0 ? g.n[0] * ho4d_plane(h4) * sizeof(double) : bytes;
   CUDA_TRY(ctx->v0.ensure(pbytes));

@@ -2,7 +2,8 @@
 (k_fast4d<ShapeGen>) against the generic kernel (HJB_FAST=0), next to the
 compiled-shape kernel on the config-2 model, at one grid size.
 
-usage: python scripts/bench_gen4d.py [n=51] [iters=300] [gd|lf] [const|axis0|node]
+usage: python scripts/bench_gen4d.py [n=51] [iters=300] [gd|lf] [const|axis0|node] [order=1] [rk=1]
+(order / rk > 1: ENO + TVD-RK, one step = all RK stages)
 Prints one JSON line per (model, kernel).
 """
 import json
@@ -28,6 +29,8 @@ def main():
     cfg = hj.SolveConfig(tolerance=1e-12, max_iters=iters)
     if scheme == "lf":
         cfg.scheme = hj.LAX_FRIEDRICHS
+    cfg.spatial_order = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+    cfg.time_order = int(sys.argv[6]) if len(sys.argv) > 6 else 1
     os.environ["HJB_MS"] = "0"
     bounds = sys.argv[4] if len(sys.argv) > 4 else "const"
 
@@ -43,13 +46,15 @@ def main():
         for fast in ("1", "0"):
             os.environ["HJB_FAST"] = fast
             warm = hj.SolveConfig(max_iters=5)
-            warm.scheme = cfg.scheme
+            warm.scheme, warm.spatial_order, warm.time_order = (cfg.scheme, cfg.spatial_order,
+                                                                cfg.time_order)
             hj.solve(c, c, model, db, warm, ctx=ctx)  # autotune, warm
             r = hj.solve(c, c, model, db, cfg, ctx=ctx)
             us = r.wall_seconds / r.iterations * 1e6
             print(json.dumps({"model": name, "grid": f"{n}^4", "scheme": scheme, "bounds": bounds,
+                              "order": cfg.spatial_order, "rk": cfg.time_order,
                               "kernel": r.kernel,
-                              "sweep_us": round(us, 2), "iterations": r.iterations,
+                              "step_us": round(us, 2), "iterations": r.iterations,
                               "gcell_per_s": round(g.size() / us * 1e-3, 2)}), flush=True)
     os.environ.pop("HJB_FAST", None)
 

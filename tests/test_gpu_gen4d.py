@@ -189,8 +189,8 @@ def test_gen4d_matches_generic_kernel(gpu_ctx, monkeypatch, name):
 
 
 def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
-    """ENO/TVD-RK stays on the generic kernels for a run-time-shape model, and
-    so does LF for a row with two input terms (still bitwise against the
+    """ENO/TVD-RK with rows on x0 stays on the generic stage kernel, and so
+    does LF for a row with two input terms (still bitwise against the
     oracle)."""
     g = hj.Grid([(-5.0, 5.0, 11), (-2.0, 2.0, 9), (-0.35, 0.35, 7), (-1.5, 1.5, 8)])
     c = hj.ScalarField(g, band_np(g, 0, -4.0, 4.0))
@@ -207,9 +207,10 @@ def test_gen4d_outside_scope_falls_back(gpu_ctx, oracle):
     assert got.kernel == "generic"
     _check(got, oracle.solve(c, c, two, db0, lf))
     ho = hj.SolveConfig(tolerance=1e-4, max_iters=10, spatial_order=3, time_order=3)
-    got = hj.solve(c, c, model, db, ho, ctx=gpu_ctx)
-    assert got.kernel == "ho_generic"
-    _check(got, oracle.solve(c, c, model, db, ho))
+    xm, xdb = x0_model(), hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    got = hj.solve(c, c, xm, xdb, ho, ctx=gpu_ctx)
+    assert got.kernel == "ho_generic"  # rows on x0: the stage kernels march x0
+    _check(got, oracle.solve(c, c, xm, xdb, ho))
 
 
 
@@ -303,3 +304,21 @@ def test_gen4d_per_node_bounds(gpu_ctx, oracle, monkeypatch, name, dims, kind):
     monkeypatch.setenv("HJB_PN", "0")
     gen = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
     assert same(gen.value.values(), got.value.values())
+
+
+@pytest.mark.parametrize("scheme", ["gd", "lf"])
+@pytest.mark.parametrize("order,rk", [(1, 2), (2, 2), (3, 3)])
+@pytest.mark.parametrize("dims", [(9, 21, 19, 23), (17, 12, 10, 40)])
+@pytest.mark.parametrize("name", ["mixed", "inputs", "advection"])
+def test_gen4d_high_order_matches_oracle(gpu_ctx, oracle, name, dims, order, rk, scheme):
+    """ENO1-3 + TVD-RK2/3 stages on the run-time-shape k_ho4t (Godunov: the
+    reference flux per axis from hhat = 0.0; LF: run-time channels) against
+    the CPU restatement, bitwise."""
+    g, model, db, c = _setup(name, dims)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=12, spatial_order=order, time_order=rk)
+    if scheme == "lf":
+        cfg.scheme = hj.LAX_FRIEDRICHS
+    want = oracle.solve(c, c, model, db, cfg)
+    got = hj.solve(c, c, model, db, cfg, ctx=gpu_ctx)
+    assert got.kernel == "ho4d"
+    _check(got, want)
