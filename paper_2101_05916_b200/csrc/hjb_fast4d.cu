@@ -371,6 +371,25 @@ __device__ __forceinline__ void chunk_planes(const A& a, uint32_t chunk, uint32_
   }
 }
 
+// publish the peer-store epoch to the neighbours (Fast4dArgs::p2p_*; the
+// stage kernels without peer stores have no such fields)
+template <class A>
+__device__ __forceinline__ void p2p_publish(const A& a) {
+  if constexpr (std::is_same<A, Fast4dArgs>::value) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      if (a.p2p_flag[s])
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.p2p_flag[s]), "r"(a.p2p_epoch)
+                     : "memory");
+  }
+}
+template <class A>
+__device__ __forceinline__ bool p2p_on(const A& a) {
+  if constexpr (std::is_same<A, Fast4dArgs>::value)
+    return a.p2p_flag[0] != nullptr || a.p2p_flag[1] != nullptr;
+  else
+    return false;
+}
 // a consumer warp finished an item of planes [c0, ...): count boundary items
 // and raise the flag with the last one (release: the planes' stores first)
 template <class A>
@@ -381,14 +400,26 @@ __device__ __forceinline__ void signal_item(const A& a, LoopState* st, uint32_t 
   if (!bnd) return;
   __syncwarp();
   if (lane == 0) {
-    __threadfence();
-    if (atomicAdd(&st->bnd_done, 1u) + 1u == a.bnd_target) atomicExch(&st->bnd_flag, 1u);
+    // peer stores: the warp's stores into the neighbours' buffers become
+    // visible system-wide before it is counted
+    if (p2p_on(a))
+      __threadfence_system();
+    else
+      __threadfence();
+    if (atomicAdd(&st->bnd_done, 1u) + 1u == a.bnd_target) {
+      atomicExch(&st->bnd_flag, 1u);
+      p2p_publish(a);
+    }
   }
 }
 // an early-exiting launch (loop done) still releases the transfer stream
+// (and the neighbours waiting on its peer-store epoch)
 template <class A>
 __device__ __forceinline__ void signal_exit(const A& a, LoopState* st) {
-  if (a.signal && blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&st->bnd_flag, 1u);
+  if (a.signal && blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicExch(&st->bnd_flag, 1u);
+    p2p_publish(a);
+  }
 }
 
 constexpr uint32_t kEndItem = 0xffffffffu;
@@ -909,8 +940,8 @@ __global__ void __launch_bounds__(MAXT, 1)
       // replicated at an axis end
       const bool e1lo = i1 == 0, e1hi = i1 + 1 == n1, e2lo = i2 == 0, e2hi = i2 + 1 == n2;
 
-      double* op = dst + static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3 +
-                   static_cast<uint64_t>(c0) * s0;
+      const uint64_t pof = static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3;
+      double* op = dst + pof + static_cast<uint64_t>(c0) * s0;
       // target set (TG): the pencil's l of each plane, loaded with __ldg
       const double* tgp =
           TG ? a.target + (active ? static_cast<uint64_t>(i1) * s1 + static_cast<uint64_t>(i2) * s2 + i3
@@ -1248,6 +1279,18 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
           for (int c = 0; c < kK; c += 2)
             *reinterpret_cast<double2*>(op + c) = make_double2(out[c], out[c + 1]);
+          if (!MS && a.p2p_R) {  // peer-store halos: this plane into a neighbour's halo
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              if (a.p2p_dst[s] && i0 - a.p2p_src0[s] < a.p2p_R) {
+                double* q = a.p2p_dst[s] +
+                            static_cast<uint64_t>(i0 - a.p2p_src0[s] + a.p2p_dst0[s]) * s0 + pof;
+#pragma unroll
+                for (int c = 0; c < kK; c += 2)
+                  *reinterpret_cast<double2*>(q + c) = make_double2(out[c], out[c + 1]);
+              }
+            }
+          }
         }
         op += s0;
 #pragma unroll

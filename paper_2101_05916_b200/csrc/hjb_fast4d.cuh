@@ -54,6 +54,17 @@ struct Fast4dArgs {
   // on the stream: cuStreamWaitValue32); an early exit raises it too
   uint32_t nb, b0, e0, b1, e1, bitems, bnd_target;
   int signal;
+  // peer-store halos (sharded first order, HJB_SHARD_P2P): a boundary plane
+  // i0 in [p2p_src0[s], p2p_src0[s] + p2p_R) is also stored into neighbour
+  // s's output buffer (s = 0 lower, 1 upper; NVLink P2P stores, or a
+  // same-device pointer for in-process ranks) at its plane i0 - p2p_src0[s] +
+  // p2p_dst0[s]; the warp that completes the boundary count then publishes
+  // p2p_epoch to the neighbours' flags (system-scope release), which their
+  // next stage waits on.  Null p2p_dst[s]: no neighbour on that side.
+  double* p2p_dst[2];
+  uint32_t p2p_src0[2], p2p_dst0[2], p2p_R;
+  unsigned int* p2p_flag[2];
+  unsigned int p2p_epoch;
   // max|dV| accumulator of the launch (null: st->maxdv_bits)
   unsigned long long* mdv;
   // padded target set l (TG variant): out = max(c, min(l, stepped))

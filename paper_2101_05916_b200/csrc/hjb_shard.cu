@@ -117,6 +117,11 @@ struct hjb_comm {
   hjb::ncclComm_t comm = nullptr;
   int nranks = 1;
   int rank = 0;
+  // peer-store halos (HJB_SHARD_P2P): this rank's two epoch flags (written
+  // by the lower / upper neighbour over NVLink) and the epoch counter, both
+  // monotonic across solves so no reset can race a neighbour's write
+  unsigned int* p2p_flags = nullptr;
+  unsigned int p2p_seq = 0;
 };
 
 using namespace hjb;
@@ -333,6 +338,18 @@ struct SlabRank {
   // interior only, and both in one launch with the boundary items first and
   // the completion signal (bnd_flag) for the transfer stream
   Fast4dArgs fb, fi, fc;
+  // peer-store halos (first order, HJB_SHARD_P2P): the neighbours' V
+  // buffers (by buffer index 0 / 1), the plane of theirs that receives our
+  // first send plane, their flag we publish to, our flags they publish to,
+  // and the epoch the next launch publishes
+  struct P2PLink {
+    bool on = false;
+    double* peer_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][buffer]
+    uint32_t dst0[2] = {0u, 0u};
+    unsigned int* peer_flag[2] = {nullptr, nullptr};
+    unsigned int* own_flag[2] = {nullptr, nullptr};
+    unsigned int epoch = 0;
+  } p2p;
   CUtensorMap map_b0, map_b1;
   Ho4dArgs hb, hi, hc;
   HoStage stages[3];
@@ -361,6 +378,19 @@ cudaError_t SlabRank::launch(int k, int q, int mode, unsigned long long* slot,
     x.dst = (k & 1) ? buf[0] : buf[1];
     x.map0 = (k & 1) ? map_b1 : map_b0;
     x.mdv = slot;
+    if (p2p.on && mode == kBoth) {  // boundary planes also into the neighbours' halos
+      const Halo h = halo_of(geo);
+      const int ob = (k & 1) ? 0 : 1;  // the output buffer index (theirs is the same)
+      x.p2p_R = h.planes;
+      x.p2p_epoch = p2p.epoch;
+      for (int sd = 0; sd < 2; ++sd) {
+        x.p2p_dst[sd] = p2p.peer_buf[sd][ob];
+        x.p2p_flag[sd] = p2p.peer_flag[sd];
+        x.p2p_dst0[sd] = p2p.dst0[sd];
+      }
+      x.p2p_src0[0] = h.send_lo;
+      x.p2p_src0[1] = h.send_hi;
+    }
     return launch_fast4d(x, shape, s);
   }
   Ho4dArgs x = mode == kBnd ? hb : (mode == kInner ? hi : hc);
@@ -622,6 +652,107 @@ bool shard_signal() {
   const char* e = std::getenv("HJB_SHARD_SIGNAL");
   return !(e && std::strcmp(e, "0") == 0) && memops() != nullptr;
 }
+// peer-store halos (opt-in): HJB_SHARD_P2P=1, first order, stream memory ops
+bool shard_p2p() {
+  const char* e = std::getenv("HJB_SHARD_P2P");
+  return e && std::strcmp(e, "1") == 0 && memops() != nullptr;
+}
+// the work stream waits until a neighbour has published `epoch` into our flag
+int wait_epoch(unsigned int* flag, unsigned int epoch, cudaStream_t s) {
+  const CUresult r = memops()->wait(reinterpret_cast<CUstream>(s),
+                                    reinterpret_cast<CUdeviceptr>(flag), epoch,
+                                    CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? HJB_OK : set_err(HJB_ERR_CUDA, "cuStreamWaitValue32 failed");
+}
+// Peer-store links between processes: each rank sends its neighbours the
+// CUDA IPC handles of its two V buffers and its flag word pair plus the
+// plane numbers where it receives halos, over the NCCL communicator; the
+// neighbours' allocations are mapped with peer access (NVLink).  The opened
+// mappings are closed when the solve returns (IpcPeers).
+struct IpcBlob {
+  cudaIpcMemHandle_t buf[2];
+  cudaIpcMemHandle_t flags;
+  uint32_t recv_lo, recv_hi, pad[2];
+};
+struct IpcPeers {
+  std::vector<void*> opened;
+  ~IpcPeers() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
+};
+int link_ipc_p2p(Nccl* api, hjb_comm* comm, SlabRank& rk, cudaStream_t s, IpcPeers& peers) {
+  IpcBlob mine;
+  std::memset(&mine, 0, sizeof mine);
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[0], rk.buf[0]));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[1], rk.buf[1]));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.flags, comm->p2p_flags));
+  const Halo h = halo_of(rk.geo);
+  mine.recv_lo = h.recv_lo;
+  mine.recv_hi = h.recv_hi;
+  DevBuf stage;
+  CUDA_TRY(stage.ensure(3 * sizeof(IpcBlob)));
+  IpcBlob* d = static_cast<IpcBlob*>(stage.p);
+  CUDA_TRY(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, s));
+  const int r = comm->rank;
+  const size_t nb = sizeof(IpcBlob);
+  NCCL_TRY(api->GroupStart());
+  if (rk.geo.has_lo) {
+    NCCL_TRY(api->Send(d, nb, 0 /* ncclInt8 */, r - 1, comm->comm, s));
+    NCCL_TRY(api->Recv(d + 1, nb, 0, r - 1, comm->comm, s));
+  }
+  if (rk.geo.has_hi) {
+    NCCL_TRY(api->Send(d, nb, 0, r + 1, comm->comm, s));
+    NCCL_TRY(api->Recv(d + 2, nb, 0, r + 1, comm->comm, s));
+  }
+  NCCL_TRY(api->GroupEnd());
+  IpcBlob nbr[2];
+  CUDA_TRY(cudaMemcpyAsync(nbr, d + 1, 2 * nb, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  auto& l = rk.p2p;
+  l = SlabRank::P2PLink();
+  l.on = true;
+  for (int sd = 0; sd < 2; ++sd) {
+    if (!(sd == 0 ? rk.geo.has_lo : rk.geo.has_hi)) continue;
+    for (int b = 0; b < 2; ++b) {
+      void* p = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, nbr[sd].buf[b], cudaIpcMemLazyEnablePeerAccess));
+      peers.opened.push_back(p);
+      l.peer_buf[sd][b] = static_cast<double*>(p);
+    }
+    void* f = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&f, nbr[sd].flags, cudaIpcMemLazyEnablePeerAccess));
+    peers.opened.push_back(f);
+    // our first send plane lands on the lower neighbour's first upper-halo
+    // plane, the upper neighbour's on its first lower-halo plane
+    l.dst0[sd] = sd == 0 ? nbr[sd].recv_hi : nbr[sd].recv_lo;
+    l.peer_flag[sd] = static_cast<unsigned int*>(f) + (sd == 0 ? 1 : 0);
+    l.own_flag[sd] = comm->p2p_flags + sd;
+  }
+  return HJB_OK;
+}
+
+// the peer-store links of in-process ranks (same device: the neighbours'
+// buffers and flags are plain device pointers)
+void link_local_p2p(std::vector<SlabRank>& rks, unsigned int* flags) {
+  const int P = static_cast<int>(rks.size());
+  for (int r = 0; r < P; ++r) {
+    auto& l = rks[r].p2p;
+    l = SlabRank::P2PLink();
+    l.on = true;
+    if (r > 0) {
+      for (int b = 0; b < 2; ++b) l.peer_buf[0][b] = rks[r - 1].buf[b];
+      l.dst0[0] = halo_of(rks[r - 1].geo).recv_hi;
+      l.peer_flag[0] = flags + 2 * (r - 1) + 1;  // the lower rank's "from above"
+      l.own_flag[0] = flags + 2 * r;
+    }
+    if (r < P - 1) {
+      for (int b = 0; b < 2; ++b) l.peer_buf[1][b] = rks[r + 1].buf[b];
+      l.dst0[1] = halo_of(rks[r + 1].geo).recv_lo;
+      l.peer_flag[1] = flags + 2 * (r + 1);  // the upper rank's "from below"
+      l.own_flag[1] = flags + 2 * r + 1;
+    }
+  }
+}
 // the transfer stream waits for / re-arms one rank's boundary flag
 int wait_flag(LoopState* st, cudaStream_t s) {
   const CUresult r = memops()->wait(reinterpret_cast<CUstream>(s),
@@ -689,6 +820,12 @@ struct PositionOps {
   // transfer (after the launch) || an interior launch.
   bool signal = false;
   std::function<int(cudaStream_t s)> wait_bnd, reset_bnd;
+  // peer-store halos: the sweep kernels store the boundary planes into the
+  // neighbours' halos and publish an epoch; before each stage the work
+  // stream waits for the neighbours' epoch of the stage it reads (p2p_wait)
+  // and re-arms the boundary counter (reset_bnd); no transfer on S
+  bool p2p = false;
+  std::function<int(cudaStream_t s)> p2p_wait;
   // sweep kernels of stage q on stream s (mode kBnd / kInner / kBoth)
   std::function<int(int k, int q, int mode, bool pipe, cudaStream_t s)> sweep;
   // halo transfer of stage q's output, on s
@@ -714,11 +851,17 @@ int run_position(LoopStreams& ls, cudaStream_t S, const PositionOps& op, int k, 
     CUDA_TRY(cudaEventRecord(ls.ev_fork, S));
     CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_fork, 0));
   } else {
-    if (op.xfer) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_xl[(k - 1) & 1], 0));  // halo of V_k
+    if (op.xfer && !op.p2p) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_xl[(k - 1) & 1], 0));  // halo of V_k
     if (!pipe) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_epi[(k - 1) & 1], 0));
     else if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(W, ls.ev_epi[k & 1], 0));
   }
   for (int q = 0; q < op.ns; ++q) {
+    if (op.p2p) {  // one launch per stage; its kernels store the halos themselves
+      if ((e = op.p2p_wait(W))) return e;
+      if ((e = op.reset_bnd(W))) return e;
+      if ((e = op.sweep(k, q, kBoth, pipe, W))) return e;
+      continue;
+    }
     if (op.xfer && op.signal) {  // one launch; the transfer starts on its flag
       if ((e = op.sweep(k, q, kBoth, pipe, W))) return e;
       if ((e = op.wait_bnd(S))) return e;
@@ -863,6 +1006,17 @@ int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* 
     return set_err(HJB_ERR_NCCL, std::string("ncclCommInitRank failed: ") +
                                      (api->GetErrorString ? api->GetErrorString(r) : ""));
   }
+  // the flags must be their own cudaMalloc allocation (IPC handles map whole
+  // allocations) and zero before any neighbour can write them: the first
+  // peer write happens after the first halo exchange, which every rank
+  // enters only after this comm_create returned everywhere
+  if (cudaMalloc(&c->p2p_flags, 64) != cudaSuccess ||
+      cudaMemset(c->p2p_flags, 0, 64) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    if (c->p2p_flags) cudaFree(c->p2p_flags);
+    api->CommDestroy(c->comm);
+    delete c;
+    return set_err(HJB_ERR_CUDA, "comm_create: peer-store flag allocation failed");
+  }
   *out = c;
   return HJB_OK;
 }
@@ -870,6 +1024,7 @@ int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* 
 int hjb_comm_destroy(hjb_comm* c) {
   if (!c) return HJB_OK;
   if (c->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(c->comm);
+  if (c->p2p_flags) cudaFree(c->p2p_flags);
   delete c;
   return HJB_OK;
 }
@@ -1085,8 +1240,26 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   op.signal = op.xfer && shard_signal();
   op.wait_bnd = [&](cudaStream_t s) -> int { return wait_flag(ctx->st, s); };
   op.reset_bnd = [&](cudaStream_t s) -> int { return rearm_flag(ctx->st, s); };
+  // peer-store halos (opt-in, first order): the neighbours' buffers and
+  // flags mapped over CUDA IPC; the kernels store the halo planes over NVLink
+  IpcPeers ipc;
+  if (P > 1 && !rk.ho && shard_p2p()) {
+    if ((rc = link_ipc_p2p(api, comm, rk, ctx->stream, ipc))) return rc;
+    op.p2p = true;
+  }
+  op.p2p_wait = [&](cudaStream_t s) -> int {
+    if (comm->p2p_seq == 0) return HJB_OK;  // nothing published yet (V_0 came by NCCL)
+    for (int sd = 0; sd < 2; ++sd)
+      if (rk.p2p.own_flag[sd]) {
+        int e = wait_epoch(rk.p2p.own_flag[sd], comm->p2p_seq, s);
+        if (e) return e;
+      }
+    return HJB_OK;
+  };
   op.sweep = [&](int k, int q, int mode, bool pp, cudaStream_t s) -> int {
+    if (op.p2p) rk.p2p.epoch = comm->p2p_seq + 1;
     CUDA_TRY(rk.launch(k, q, mode, pp ? &ctx->st->maxdv_slot[k & 1] : maxbits, s));
+    if (op.p2p) ++comm->p2p_seq;
     ++per_pos;
     return HJB_OK;
   };
@@ -1237,7 +1410,30 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
     }
     return HJB_OK;
   };
+  // peer-store halos (opt-in, first order): the kernels write the
+  // neighbours' halo planes; one epoch counter for all ranks
+  DevBuf p2p_flags;
+  unsigned int p2p_seq = 0;
+  if (P > 1 && !rks[0].ho && shard_p2p()) {
+    CUDA_TRY(p2p_flags.ensure(2 * static_cast<size_t>(P) * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemsetAsync(p2p_flags.p, 0, 2 * static_cast<size_t>(P) * sizeof(unsigned int),
+                             ctx->stream));
+    link_local_p2p(rks, static_cast<unsigned int*>(p2p_flags.p));
+    op.p2p = true;
+  }
+  op.p2p_wait = [&](cudaStream_t s) -> int {
+    if (p2p_seq == 0) return HJB_OK;  // V_0's halos came with the initial exchange
+    for (int r = 0; r < P; ++r)
+      for (int sd = 0; sd < 2; ++sd)
+        if (rks[r].p2p.own_flag[sd]) {
+          int e = wait_epoch(rks[r].p2p.own_flag[sd], p2p_seq, s);
+          if (e) return e;
+        }
+    return HJB_OK;
+  };
   op.sweep = [&](int k, int q, int mode, bool pp, cudaStream_t s) -> int {
+    if (op.p2p)
+      for (int r = 0; r < P; ++r) rks[r].p2p.epoch = p2p_seq + 1;
     for (int r = 0; r < P; ++r) {
       if (mode == kBnd && !rks[r].sp.bnd) continue;
       if (mode == kInner && !rks[r].sp.inner) continue;
@@ -1247,6 +1443,7 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
       CUDA_TRY(rks[r].launch(k, q, m, acc, s));
       ++per_pos;
     }
+    if (op.p2p) ++p2p_seq;
     return HJB_OK;
   };
   op.exchange = [&](int k, int q, cudaStream_t s) -> int {
@@ -1268,7 +1465,8 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
   CUDA_TRY(cudaEventRecord(ls.e0, ctx->stream));
   // stream memory operations stay out of graph capture: the signalling
   // protocol runs the host-driven loop (as the NCCL transport always does)
-  if ((rc = op.signal ? run_eager_loop(ctx, body, step) : run_sharded_loop(ctx, body, step)))
+  if ((rc = (op.signal || op.p2p) ? run_eager_loop(ctx, body, step)
+                                   : run_sharded_loop(ctx, body, step)))
     return rc;
   CUDA_TRY(cudaEventRecord(ls.e1, ctx->stream));
   CUDA_TRY(cudaEventSynchronize(ls.e1));

@@ -5,7 +5,7 @@ halo copies on a second stream while the interior sweeps, pipelined residual
 reduction + epilogue) on one device, so the ranks' sweeps execute one after
 another: the per-sweep time of P local ranks minus the unsharded sweep time is
 the protocol's own cost on the critical path (extra launches, waits, copies
-that were not hidden).  Variants: HJB_SHARD_OVERLAP / HJB_SHARD_PIPE.
+that were not hidden).  Variants: HJB_SHARD_OVERLAP / HJB_SHARD_PIPE / HJB_SHARD_P2P.
 
     python scripts/bench_sharded_local.py [--n 101] [--sweeps 200] > out.json
 """
@@ -54,7 +54,8 @@ def main():
             os.environ.pop(k, None)
         return best / iters * 1e6
 
-    variants = {"overlap+pipe": {}, "serial": {"HJB_SHARD_OVERLAP": "0", "HJB_SHARD_PIPE": "0"},
+    variants = {"overlap+pipe": {}, "peer_store": {"HJB_SHARD_P2P": "1"},
+                "serial": {"HJB_SHARD_OVERLAP": "0", "HJB_SHARD_PIPE": "0"},
                 "overlap_only": {"HJB_SHARD_PIPE": "0"},
                 "serial_one_launch": {"HJB_SHARD_OVERLAP": "0", "HJB_SHARD_PIPE": "0",
                                       "HJB_SHARD_SPLIT": "0"}}
@@ -64,6 +65,8 @@ def main():
         res["first_order"][name] = {str(P): run(1, 1, a.sweeps, P, env) for P in ranks}
     res["eno3_rk3"]["unsharded_us"] = run(3, 3, a.ho_steps, 0, {})
     for name, env in variants.items():
+        if name == "peer_store":  # first order only
+            continue
         res["eno3_rk3"][name] = {str(P): run(3, 3, a.ho_steps, P, env) for P in ranks if P <= 8}
     print(json.dumps(res, indent=1))
 

@@ -266,3 +266,64 @@ def test_local_ranks_signal_protocol_converges(gpu_ctx, monkeypatch):
     r, v = _local(gpu_ctx, w, c, cfg, 3, 0)
     assert r.converged and r.iterations == ref.iterations
     assert same(v, ref.value.values())
+
+
+# Peer-store halos (HJB_SHARD_P2P=1): the slab sweep kernels store their
+# boundary planes straight into the neighbours' halo planes and publish an
+# epoch to the neighbours' flags; the next stage's stream waits on its own
+# flags.  In-process ranks exercise the same kernels, offsets and flags with
+# same-device pointers (the NCCL driver maps the neighbours' buffers over
+# CUDA IPC instead).
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("scheme", ["godunov", "lf_per_node", "lf_global"])
+def test_local_ranks_peer_store_equal_solve(gpu_ctx, monkeypatch, P, scheme):
+    monkeypatch.setenv("HJB_SHARD_P2P", "1")
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=120)
+    if scheme != "godunov":
+        cfg.scheme = hj.LAX_FRIEDRICHS
+        cfg.dissipation = hj.GLOBAL if scheme == "lf_global" else hj.PER_NODE
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, P, 120)
+    assert r.iterations == ref.iterations == 120 and r.dt == ref.dt
+    assert same(r.residual_history, ref.residual_history)
+    assert same(v, ref.value.values())
+
+
+def test_local_ranks_peer_store_irregular_grid(gpu_ctx, monkeypatch):
+    """Odd extents, 3 ranks with unequal slabs, peer-store halos."""
+    monkeypatch.setenv("HJB_SHARD_P2P", "1")
+    g = hj.Grid([(-5.0, 5.0, 17), (-2.0, 2.0, 9), (-0.35, 0.35, 8), (-1.5, 1.5, 11)])
+    model = configs.planar_model()
+    db = hj.IntervalField.constant(g, [hj.Interval(-0.5, 0.5)])
+    c = band_np(g, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-5, max_iters=60)
+    ref = hj.solve(hj.ScalarField(g, c), hj.ScalarField(g, c), model, db, cfg, ctx=gpu_ctx)
+    ct = torch.tensor(c, device="cuda")
+    out = torch.full_like(ct, float("nan"))
+    torch.cuda.synchronize()
+    r = sharded.solve_sharded_local_dev(3, g, model, db, ct.data_ptr(), ct.data_ptr(),
+                                        out.data_ptr(), cfg, gpu_ctx, history_capacity=60)
+    assert r.iterations == ref.iterations and same(r.residual_history, ref.residual_history)
+    assert same(out.cpu().numpy(), ref.value.values())
+
+
+def test_local_ranks_peer_store_converge_in_reference_iteration_count(gpu_ctx, monkeypatch):
+    """4 in-process ranks with peer-store halos solve config 2 at 21^4 to tol
+    5e-3: the reference's 16 685 iterations and V* (golden fixture), i.e. the
+    epoch protocol holds over every batch, the stop and the extra batch."""
+    import json
+    import hashlib
+    from pathlib import Path
+    monkeypatch.setenv("HJB_SHARD_P2P", "1")
+    meta = json.loads((Path(__file__).resolve().parent / "golden" / "golden_fullsize.json")
+                      .read_text())["conv21"]
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=5e-3, max_iters=200000)
+    r, v = _local(gpu_ctx, w, c, cfg, 4, 0)
+    assert r.iterations == meta["iterations"] == 16685 and r.converged
+    assert hashlib.sha256(np.ascontiguousarray(v + 0.0).tobytes()).hexdigest() == meta["value_sha256"]
