@@ -312,6 +312,19 @@ int hjb_nccl_unique_id(void* out128);
 int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* unique_id128,
                     hjb_comm** out);
 int hjb_comm_destroy(hjb_comm* comm);
+/* Peer-store communicator without NCCL (one process per GPU of one node,
+ * NVLink peer memory): every per-sweep exchange of the slab solve runs on
+ * the devices — the sweep kernels store their boundary planes into the
+ * neighbours' halos and the residual all-reduce goes through system-scope
+ * atomics into every rank's mailbox; the CFL scan all-reduce, the V_0 halos
+ * and the per-solve buffer handles also go through peer memory.  Set up:
+ * create, export this rank's control-block IPC handle (64 bytes), all-gather
+ * the handles on the host (e.g. torch.distributed with gloo), open them.
+ * First-order solves only.  (The NCCL communicator takes the same transport
+ * for its sweeps with HJB_SHARD_P2P=1.) */
+int hjb_p2p_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, hjb_comm** out);
+int hjb_comm_ctl_handle(hjb_comm* comm, void* out64);
+int hjb_comm_open_peers(hjb_comm* comm, const void* handles64xN);
 /* solve() over a slab-partitioned 4D grid: init/c/value_out hold this rank's
  * owned planes [begin, end) of `global_grid` (reference layout, device
  * pointers).  Per sweep / RK stage: boundary planes, then the NCCL halo

@@ -166,6 +166,9 @@ SIGNATURES = [
     ("hjb_nccl_unique_id", _i, [_vp]),
     ("hjb_comm_create", _i, [_vp, _i32, _i32, _vp, P(_vp)]),
     ("hjb_comm_destroy", _i, [_vp]),
+    ("hjb_p2p_comm_create", _i, [_vp, _i32, _i32, P(_vp)]),
+    ("hjb_comm_ctl_handle", _i, [_vp, _vp]),
+    ("hjb_comm_open_peers", _i, [_vp, _vp]),
     ("hjb_solve_sharded_dev", _i, [_vp, _vp, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp, _vp,
                                    P(HjbSolveConfig), _vp, P(HjbSolveResult)]),
     ("hjb_solve_sharded_local_dev", _i, [_vp, _i32, P(HjbGrid), P(HjbModel), P(HjbDbounds), _vp,

@@ -34,7 +34,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -114,15 +116,24 @@ Nccl* nccl() {
 }  // namespace hjb
 
 struct hjb_comm {
-  hjb::ncclComm_t comm = nullptr;
+  hjb::ncclComm_t comm = nullptr;  // null: a peer-store-only communicator (no NCCL)
   int nranks = 1;
   int rank = 0;
-  // peer-store halos (HJB_SHARD_P2P): this rank's two epoch flags (written
-  // by the lower / upper neighbour over NVLink) and the epoch counter, both
-  // monotonic across solves so no reset can race a neighbour's write
+  // peer-store transport (HJB_SHARD_P2P): this rank's control block — two
+  // halo-epoch flags (written by the lower / upper neighbour over NVLink) at
+  // offset 0 and the residual mailbox (P2PMbox) at kMboxOffset — plus the
+  // epoch counters, all monotonic across solves so no reset can race a
+  // neighbour's write; every rank's control block mapped over CUDA IPC
+  // (peer_ctl[q], opened once, closed at destroy)
   unsigned int* p2p_flags = nullptr;
-  unsigned int p2p_seq = 0;
+  unsigned int p2p_seq = 0, res_seq = 0, scan_seq = 0, blob_seq = 0;
+  std::vector<void*> peer_ctl;
+  bool peers_open = false;
 };
+// control-block layout: halo-epoch flags (2 x u32) | blob epoch (u32) |
+// residual mailbox | scan mailbox | the per-solve buffer-handle blob
+constexpr size_t kCtlBytes = 4096, kBlobFlagOffset = 64, kMboxOffset = 256, kScanOffset = 512,
+                 kBlobOffset = 1024;
 
 using namespace hjb;
 
@@ -610,6 +621,76 @@ __global__ void k_reduce_ranks(RankStates p, int slot) {
   __threadfence();
 }
 
+// ---- device-side residual all-reduce of the peer-store transport ----
+// Every rank owns a mailbox; after a position's sweeps each rank atomically
+// max-es its max|dV| bits into slot e % kMboxSlots of EVERY rank's mailbox
+// (system-scope atomics over NVLink, or same-device pointers in-process),
+// fences, and bumps each mailbox's count.  A rank's stream then waits until
+// its own count reaches P * (e / kMboxSlots + 1) (counts are monotonic, never
+// reset), takes the max into the loop state's slot, zeroes the mailbox slot
+// and runs the epilogue.  A contribution for position m implies (through
+// the halo epochs and the epilogue wait of the pipelined loop) that every
+// rank has consumed position m - 4, so 8 slots cannot be overwritten early.
+constexpr int kMboxSlots = 8;
+struct P2PMbox {
+  unsigned long long bits[kMboxSlots];
+  unsigned int count[kMboxSlots];
+};
+struct MboxSet {
+  P2PMbox* m[kMaxLocalRanks];
+  int n;
+};
+// the CFL scan all-reduce of a peer-store-only communicator: 1 + nd
+// non-negative doubles, max-ed as bit patterns (monotonic for values >= +0)
+struct ScanMbox {
+  unsigned long long bits[kMboxSlots][1 + kMaxDims];
+  unsigned int count[kMboxSlots];
+};
+__global__ void k_scan_contribute(const unsigned long long* mine, MboxSet peers, unsigned int e) {
+  if (threadIdx.x != 0) return;
+  const int k = static_cast<int>(e % kMboxSlots);
+  for (int q = 0; q < peers.n; ++q) {
+    ScanMbox* m = reinterpret_cast<ScanMbox*>(peers.m[q]);
+    for (int i = 0; i < 1 + kMaxDims; ++i) atomicMax_system(&m->bits[k][i], mine[i]);
+  }
+  __threadfence_system();
+  for (int q = 0; q < peers.n; ++q)
+    atomicAdd_system(&reinterpret_cast<ScanMbox*>(peers.m[q])->count[k], 1u);
+}
+__global__ void k_scan_take(ScanMbox* own, unsigned long long* out, unsigned int e) {
+  if (threadIdx.x != 0) return;
+  const int k = static_cast<int>(e % kMboxSlots);
+  for (int i = 0; i < 1 + kMaxDims; ++i) out[i] = atomicExch_system(&own->bits[k][i], 0ull);
+}
+// a halo epoch published from the stream (after the V_0 peer copies)
+__global__ void k_publish(unsigned int* f0, unsigned int* f1, unsigned int epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  if (f0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f0), "r"(epoch) : "memory");
+  if (f1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f1), "r"(epoch) : "memory");
+}
+
+// slot < 0: the source is maxdv_bits, else maxdv_slot[slot]
+__global__ void k_p2p_contribute(const LoopState* st, int slot, MboxSet peers, unsigned int e) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long b =
+      slot < 0 ? *(volatile const unsigned long long*)&st->maxdv_bits
+               : *(volatile const unsigned long long*)&st->maxdv_slot[slot];
+  const int k = static_cast<int>(e % kMboxSlots);
+  for (int q = 0; q < peers.n; ++q) atomicMax_system(&peers.m[q]->bits[k], b);
+  __threadfence_system();
+  for (int q = 0; q < peers.n; ++q) atomicAdd_system(&peers.m[q]->count[k], 1u);
+}
+__global__ void k_p2p_take(P2PMbox* own, LoopState* st, int slot, unsigned int e) {
+  if (threadIdx.x != 0) return;
+  const int k = static_cast<int>(e % kMboxSlots);
+  const unsigned long long b = atomicExch_system(&own->bits[k], 0ull);
+  if (slot < 0)
+    st->maxdv_bits = b;
+  else
+    st->maxdv_slot[slot] = b;
+  __threadfence();
+}
 // HJB_SHARD_OVERLAP=0: the halo transfer runs on the main stream after the
 // whole slab is swept (the serial protocol; A/B of the overlap)
 bool shard_overlap() {
@@ -664,6 +745,22 @@ int wait_epoch(unsigned int* flag, unsigned int epoch, cudaStream_t s) {
                                     CU_STREAM_WAIT_VALUE_GEQ);
   return r == CUDA_SUCCESS ? HJB_OK : set_err(HJB_ERR_CUDA, "cuStreamWaitValue32 failed");
 }
+// contribute, wait for all P contributions, take: the all-reduce of one
+// position on stream s; the caller then runs the epilogue
+int p2p_allreduce(const LoopState* st, LoopState* st_w, int slot, const MboxSet& peers,
+                  P2PMbox* own, int P, unsigned int e, cudaStream_t s) {
+  k_p2p_contribute<<<1, 32, 0, s>>>(st, slot, peers, e);
+  CUDA_TRY(cudaGetLastError());
+  const unsigned int need = static_cast<unsigned int>(P) * (e / kMboxSlots + 1u);
+  const CUresult r = memops()->wait(reinterpret_cast<CUstream>(s),
+                                    reinterpret_cast<CUdeviceptr>(&own->count[e % kMboxSlots]),
+                                    need, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return set_err(HJB_ERR_CUDA, "cuStreamWaitValue32 failed");
+  k_p2p_take<<<1, 32, 0, s>>>(own, st_w, slot, e);
+  CUDA_TRY(cudaGetLastError());
+  return HJB_OK;
+}
+
 // Peer-store links between processes: each rank sends its neighbours the
 // CUDA IPC handles of its two V buffers and its flag word pair plus the
 // plane numbers where it receives halos, over the NCCL communicator; the
@@ -671,26 +768,61 @@ int wait_epoch(unsigned int* flag, unsigned int epoch, cudaStream_t s) {
 // mappings are closed when the solve returns (IpcPeers).
 struct IpcBlob {
   cudaIpcMemHandle_t buf[2];
-  cudaIpcMemHandle_t flags;
   uint32_t recv_lo, recv_hi, pad[2];
 };
+static_assert(sizeof(P2PMbox) <= kScanOffset - kMboxOffset, "control block: residual mailbox");
+static_assert(sizeof(ScanMbox) <= kBlobOffset - kScanOffset, "control block: scan mailbox");
+static_assert(kBlobOffset + sizeof(IpcBlob) <= kCtlBytes, "control block: handle blob");
 struct IpcPeers {
   std::vector<void*> opened;
   ~IpcPeers() {
     for (void* p : opened) cudaIpcCloseMemHandle(p);
   }
 };
+// every rank's control block over CUDA IPC, once per communicator: the
+// handles are all-gathered as a byte-wise sum (each rank writes only its own
+// row of a zeroed P x 64-byte array)
+int comm_open_peers(Nccl* api, hjb_comm* comm, cudaStream_t s) {
+  if (comm->peers_open) return HJB_OK;
+  const int P = comm->nranks;
+  if (P > kMaxLocalRanks) return set_err(HJB_ERR_UNSUPPORTED, "peer-store transport: <= 16 ranks");
+  std::vector<cudaIpcMemHandle_t> hs(P);
+  std::memset(hs.data(), 0, P * sizeof(cudaIpcMemHandle_t));
+  CUDA_TRY(cudaIpcGetMemHandle(&hs[comm->rank], comm->p2p_flags));
+  DevBuf d;
+  CUDA_TRY(d.ensure(P * sizeof(cudaIpcMemHandle_t)));
+  CUDA_TRY(cudaMemcpyAsync(d.p, hs.data(), P * sizeof(cudaIpcMemHandle_t), cudaMemcpyHostToDevice, s));
+  NCCL_TRY(api->AllReduce(d.p, d.p, P * sizeof(cudaIpcMemHandle_t), 1 /* ncclUint8 */, 0 /* sum */,
+                          comm->comm, s));
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), d.p, P * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  comm->peer_ctl.assign(P, nullptr);
+  for (int q = 0; q < P; ++q) {
+    if (q == comm->rank) {
+      comm->peer_ctl[q] = comm->p2p_flags;
+      continue;
+    }
+    CUDA_TRY(cudaIpcOpenMemHandle(&comm->peer_ctl[q], hs[q], cudaIpcMemLazyEnablePeerAccess));
+  }
+  comm->peers_open = true;
+  return HJB_OK;
+}
+P2PMbox* ctl_mbox(void* ctl) {
+  return reinterpret_cast<P2PMbox*>(static_cast<char*>(ctl) + kMboxOffset);
+}
+
 int link_ipc_p2p(Nccl* api, hjb_comm* comm, SlabRank& rk, cudaStream_t s, IpcPeers& peers) {
+  int rc;
+  if ((rc = comm_open_peers(api, comm, s))) return rc;
   IpcBlob mine;
   std::memset(&mine, 0, sizeof mine);
   CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[0], rk.buf[0]));
   CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[1], rk.buf[1]));
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.flags, comm->p2p_flags));
   const Halo h = halo_of(rk.geo);
   mine.recv_lo = h.recv_lo;
   mine.recv_hi = h.recv_hi;
   DevBuf stage;
-  CUDA_TRY(stage.ensure(3 * sizeof(IpcBlob)));
+  CUDA_TRY(stage.ensure(3 * sizeof(IpcBlob)));  // mine, from below, from above
   IpcBlob* d = static_cast<IpcBlob*>(stage.p);
   CUDA_TRY(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, s));
   const int r = comm->rank;
@@ -719,13 +851,56 @@ int link_ipc_p2p(Nccl* api, hjb_comm* comm, SlabRank& rk, cudaStream_t s, IpcPee
       peers.opened.push_back(p);
       l.peer_buf[sd][b] = static_cast<double*>(p);
     }
-    void* f = nullptr;
-    CUDA_TRY(cudaIpcOpenMemHandle(&f, nbr[sd].flags, cudaIpcMemLazyEnablePeerAccess));
-    peers.opened.push_back(f);
+    void* f = comm->peer_ctl[sd == 0 ? comm->rank - 1 : comm->rank + 1];
     // our first send plane lands on the lower neighbour's first upper-halo
     // plane, the upper neighbour's on its first lower-halo plane
     l.dst0[sd] = sd == 0 ? nbr[sd].recv_hi : nbr[sd].recv_lo;
     l.peer_flag[sd] = static_cast<unsigned int*>(f) + (sd == 0 ? 1 : 0);
+    l.own_flag[sd] = comm->p2p_flags + sd;
+  }
+  return HJB_OK;
+}
+
+// Per-solve buffer handles of a peer-store-only communicator: each rank
+// writes its blob into its own control block and bumps its blob epoch; the
+// neighbours poll that epoch through their mapping and then read the blob
+// (host-side, bounded wait: an absent neighbour is an error, not a hang).
+int link_blob_p2p(hjb_comm* comm, SlabRank& rk, IpcPeers& peers) {
+  IpcBlob mine;
+  std::memset(&mine, 0, sizeof mine);
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[0], rk.buf[0]));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[1], rk.buf[1]));
+  const Halo h = halo_of(rk.geo);
+  mine.recv_lo = h.recv_lo;
+  mine.recv_hi = h.recv_hi;
+  char* own = reinterpret_cast<char*>(comm->p2p_flags);
+  CUDA_TRY(cudaMemcpy(own + kBlobOffset, &mine, sizeof mine, cudaMemcpyHostToDevice));
+  const unsigned int ep = ++comm->blob_seq;
+  CUDA_TRY(cudaMemcpy(own + kBlobFlagOffset, &ep, sizeof ep, cudaMemcpyHostToDevice));
+  auto& l = rk.p2p;
+  l = SlabRank::P2PLink();
+  l.on = true;
+  for (int sd = 0; sd < 2; ++sd) {
+    if (!(sd == 0 ? rk.geo.has_lo : rk.geo.has_hi)) continue;
+    const int q = sd == 0 ? comm->rank - 1 : comm->rank + 1;
+    char* pc = static_cast<char*>(comm->peer_ctl[q]);
+    unsigned int seen = 0;
+    for (int it = 0; it < 1200000; ++it) {  // ~2 min at 100 us per poll
+      CUDA_TRY(cudaMemcpy(&seen, pc + kBlobFlagOffset, sizeof seen, cudaMemcpyDeviceToHost));
+      if (seen >= ep) break;
+      std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+    if (seen < ep) return set_err(HJB_ERR_RUNTIME, "peer-store link: neighbour did not publish");
+    IpcBlob nb;
+    CUDA_TRY(cudaMemcpy(&nb, pc + kBlobOffset, sizeof nb, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < 2; ++b) {
+      void* p = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, nb.buf[b], cudaIpcMemLazyEnablePeerAccess));
+      peers.opened.push_back(p);
+      l.peer_buf[sd][b] = static_cast<double*>(p);
+    }
+    l.dst0[sd] = sd == 0 ? nb.recv_hi : nb.recv_lo;
+    l.peer_flag[sd] = reinterpret_cast<unsigned int*>(pc) + (sd == 0 ? 1 : 0);
     l.own_flag[sd] = comm->p2p_flags + sd;
   }
   return HJB_OK;
@@ -1010,8 +1185,9 @@ int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* 
   // allocations) and zero before any neighbour can write them: the first
   // peer write happens after the first halo exchange, which every rank
   // enters only after this comm_create returned everywhere
-  if (cudaMalloc(&c->p2p_flags, 64) != cudaSuccess ||
-      cudaMemset(c->p2p_flags, 0, 64) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+  if (cudaMalloc(&c->p2p_flags, kCtlBytes) != cudaSuccess ||
+      cudaMemset(c->p2p_flags, 0, kCtlBytes) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
     if (c->p2p_flags) cudaFree(c->p2p_flags);
     api->CommDestroy(c->comm);
     delete c;
@@ -1021,8 +1197,53 @@ int hjb_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, const void* 
   return HJB_OK;
 }
 
+int hjb_p2p_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, hjb_comm** out) {
+  if (!ctx || !out) return set_err(HJB_ERR_INVALID_ARGUMENT, "p2p_comm_create: null");
+  if (nranks < 1 || nranks > kMaxLocalRanks || rank < 0 || rank >= nranks)
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "p2p_comm_create: 1 <= nranks <= 16, 0 <= rank < nranks");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  hjb_comm* c = new hjb_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  if (cudaMalloc(&c->p2p_flags, kCtlBytes) != cudaSuccess ||
+      cudaMemset(c->p2p_flags, 0, kCtlBytes) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    if (c->p2p_flags) cudaFree(c->p2p_flags);
+    delete c;
+    return set_err(HJB_ERR_CUDA, "p2p_comm_create: control block allocation failed");
+  }
+  *out = c;
+  return HJB_OK;
+}
+
+int hjb_comm_ctl_handle(hjb_comm* c, void* out64) {
+  if (!c || !out64) return set_err(HJB_ERR_INVALID_ARGUMENT, "comm_ctl_handle: null");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->p2p_flags));
+  std::memcpy(out64, &h, sizeof h);
+  return HJB_OK;
+}
+
+int hjb_comm_open_peers(hjb_comm* c, const void* handles) {
+  if (!c || !handles) return set_err(HJB_ERR_INVALID_ARGUMENT, "comm_open_peers: null");
+  if (c->peers_open) return HJB_OK;
+  const cudaIpcMemHandle_t* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  c->peer_ctl.assign(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      c->peer_ctl[q] = c->p2p_flags;
+      continue;
+    }
+    CUDA_TRY(cudaIpcOpenMemHandle(&c->peer_ctl[q], hs[q], cudaIpcMemLazyEnablePeerAccess));
+  }
+  c->peers_open = true;
+  return HJB_OK;
+}
+
 int hjb_comm_destroy(hjb_comm* c) {
   if (!c) return HJB_OK;
+  for (int q = 0; q < static_cast<int>(c->peer_ctl.size()); ++q)
+    if (q != c->rank && c->peer_ctl[q]) cudaIpcCloseMemHandle(c->peer_ctl[q]);
   if (c->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(c->comm);
   if (c->p2p_flags) cudaFree(c->p2p_flags);
   delete c;
@@ -1154,8 +1375,18 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
                           double* value_slab_out, hjb_solve_result* res) {
   int rc;
   if (!ctx || !comm) return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_sharded: null context/comm");
-  Nccl* api = nccl();
-  if (!api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
+  // peer-store-only communicator: no NCCL anywhere (first order)
+  const bool p2p_only = comm->comm == nullptr;
+  Nccl* api = p2p_only ? nullptr : nccl();
+  if (!p2p_only && !api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
+  if (p2p_only && cfg && (cfg->spatial_order > 1 || cfg->time_order > 1))
+    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: the peer-store communicator runs first order");
+  if (p2p_only && comm->nranks == 1 && !comm->peers_open) {  // a single rank is its own peer
+    comm->peer_ctl.assign(1, comm->p2p_flags);
+    comm->peers_open = true;
+  }
+  if (p2p_only && (!comm->peers_open || !memops()))
+    return set_err(HJB_ERR_INVALID_ARGUMENT, "solve_sharded: open the peers first (hjb_comm_open_peers)");
   const int P = comm->nranks, r = comm->rank;
   Prepared p;
   Scan s;
@@ -1169,8 +1400,24 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
     std::memcpy(bits + 1, sc.max_alpha, kMaxDims * sizeof(double));
     unsigned long long* dbits = reinterpret_cast<unsigned long long*>(ctx->scratch.d());
     CUDA_TRY(cudaMemcpyAsync(dbits, bits, sizeof bits, cudaMemcpyHostToDevice, ctx->stream));
-    NCCL_TRY(api->AllReduce(dbits, dbits, 1 + kMaxDims, ncclUint64_, ncclMax_, comm->comm,
-                            ctx->stream));
+    if (p2p_only) {  // through every rank's scan mailbox
+      MboxSet ms;
+      ms.n = P;
+      for (int q = 0; q < P; ++q)
+        ms.m[q] = reinterpret_cast<P2PMbox*>(static_cast<char*>(comm->peer_ctl[q]) + kScanOffset);
+      const unsigned int e = comm->scan_seq++;
+      k_scan_contribute<<<1, 32, 0, ctx->stream>>>(dbits, ms, e);
+      CUDA_TRY(cudaGetLastError());
+      ScanMbox* own = reinterpret_cast<ScanMbox*>(reinterpret_cast<char*>(comm->p2p_flags) + kScanOffset);
+      int we = wait_epoch(&own->count[e % kMboxSlots],
+                          static_cast<unsigned int>(P) * (e / kMboxSlots + 1u), ctx->stream);
+      if (we) return we;
+      k_scan_take<<<1, 32, 0, ctx->stream>>>(own, dbits, e);
+      CUDA_TRY(cudaGetLastError());
+    } else {
+      NCCL_TRY(api->AllReduce(dbits, dbits, 1 + kMaxDims, ncclUint64_, ncclMax_, comm->comm,
+                              ctx->stream));
+    }
     CUDA_TRY(cudaMemcpyAsync(bits, dbits, sizeof bits, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     std::memcpy(&sc.max_speed_sum, bits, sizeof(double));
@@ -1226,7 +1473,27 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   CUDA_TRY(ls.init());
   // halos of V_0 (afterwards every stage output travels right after its
   // boundary planes are swept)
-  if (P > 1 && (rc = nccl_exchange(api, comm, rk, rk.buf[0], ctx->stream))) return rc;
+  IpcPeers ipc;
+  if (P > 1 && p2p_only) {
+    // buffer handles through the control blocks, then V_0's boundary planes
+    // copied into the neighbours' halos and published as one epoch
+    if ((rc = link_blob_p2p(comm, rk, ipc))) return rc;
+    const Halo h = halo_of(rk.geo);
+    const size_t bytes = static_cast<size_t>(h.planes) * rk.pe * sizeof(double);
+    if (rk.geo.has_lo)
+      CUDA_TRY(cudaMemcpyAsync(rk.p2p.peer_buf[0][0] + rk.p2p.dst0[0] * rk.pe,
+                               rk.buf[0] + h.send_lo * rk.pe, bytes, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    if (rk.geo.has_hi)
+      CUDA_TRY(cudaMemcpyAsync(rk.p2p.peer_buf[1][0] + rk.p2p.dst0[1] * rk.pe,
+                               rk.buf[0] + h.send_hi * rk.pe, bytes, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    k_publish<<<1, 32, 0, ctx->stream>>>(rk.p2p.peer_flag[0], rk.p2p.peer_flag[1],
+                                         ++comm->p2p_seq);
+    CUDA_TRY(cudaGetLastError());
+  } else if (P > 1 && (rc = nccl_exchange(api, comm, rk, rk.buf[0], ctx->stream))) {
+    return rc;
+  }
   unsigned long long* maxbits = &ctx->st->maxdv_bits;
   const bool overlap = shard_overlap();
   const bool pipe = shard_pipeline();
@@ -1240,10 +1507,12 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   op.signal = op.xfer && shard_signal();
   op.wait_bnd = [&](cudaStream_t s) -> int { return wait_flag(ctx->st, s); };
   op.reset_bnd = [&](cudaStream_t s) -> int { return rearm_flag(ctx->st, s); };
-  // peer-store halos (opt-in, first order): the neighbours' buffers and
-  // flags mapped over CUDA IPC; the kernels store the halo planes over NVLink
-  IpcPeers ipc;
-  if (P > 1 && !rk.ho && shard_p2p()) {
+  // peer-store halos (opt-in with NCCL, always without it; first order): the
+  // neighbours' buffers and flags mapped over CUDA IPC; the kernels store
+  // the halo planes over NVLink
+  if (P > 1 && p2p_only) {
+    op.p2p = true;
+  } else if (P > 1 && !rk.ho && shard_p2p()) {
     if ((rc = link_ipc_p2p(api, comm, rk, ctx->stream, ipc))) return rc;
     op.p2p = true;
   }
@@ -1268,6 +1537,17 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   };
   op.finish = [&](int k, bool pp, cudaGraphConditionalHandle hd, int use, cudaStream_t s) -> int {
     unsigned long long* slot = pp ? &ctx->st->maxdv_slot[k & 1] : maxbits;
+    if (op.p2p) {  // device-side all-reduce over the ranks' mailboxes (NVLink atomics)
+      MboxSet ms;
+      ms.n = P;
+      for (int q = 0; q < P; ++q) ms.m[q] = ctl_mbox(comm->peer_ctl[q]);
+      int e = p2p_allreduce(ctx->st, ctx->st, pp ? (k & 1) : -1, ms, ctl_mbox(comm->p2p_flags), P,
+                            comm->res_seq++, s);
+      if (e) return e;
+      CUDA_TRY(launch_epilogue(ctx->st, hd, use, s, pp ? slot : nullptr));
+      per_pos += 3;
+      return HJB_OK;
+    }
     NCCL_TRY(api->AllReduce(slot, slot, 1, ncclUint64_, ncclMax_, comm->comm, s));
     CUDA_TRY(launch_epilogue(ctx->st, hd, use, s, pp ? slot : nullptr));
     ++per_pos;
@@ -1450,7 +1730,35 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
     for (int r = 0; r < P; ++r) xb[r] = rks[r].stage_out(k, q);
     return local_exchange(rks, xb, s);
   };
+  // peer-store transport: the residual all-reduce through the ranks'
+  // mailboxes as well (every contribution first: the ranks share a stream)
+  DevBuf mbox_buf;
+  unsigned int res_seq = 0;
+  MboxSet mset;
+  std::memset(&mset, 0, sizeof mset);
+  if (op.p2p) {
+    CUDA_TRY(mbox_buf.ensure(static_cast<size_t>(P) * sizeof(P2PMbox)));
+    CUDA_TRY(cudaMemsetAsync(mbox_buf.p, 0, static_cast<size_t>(P) * sizeof(P2PMbox), ctx->stream));
+    mset.n = P;
+    for (int q = 0; q < P; ++q) mset.m[q] = static_cast<P2PMbox*>(mbox_buf.p) + q;
+  }
   op.finish = [&](int k, bool pp, cudaGraphConditionalHandle hd, int use, cudaStream_t s) -> int {
+    if (op.p2p) {
+      const int sl = pp ? (k & 1) : -1;
+      for (int r = 0; r < P; ++r) k_p2p_contribute<<<1, 32, 0, s>>>(rs.st[r], sl, mset, res_seq);
+      CUDA_TRY(cudaGetLastError());
+      const unsigned int need = static_cast<unsigned int>(P) * (res_seq / kMboxSlots + 1u);
+      for (int r = 0; r < P; ++r) {
+        int e = wait_epoch(&mset.m[r]->count[res_seq % kMboxSlots], need, s);
+        if (e) return e;
+        k_p2p_take<<<1, 32, 0, s>>>(mset.m[r], rs.st[r], sl, res_seq);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(launch_epilogue(rs.st[r], hd, use, s, pp ? &rs.st[r]->maxdv_slot[k & 1] : nullptr));
+      }
+      ++res_seq;
+      per_pos += 3 * P;
+      return HJB_OK;
+    }
     k_reduce_ranks<<<1, 32, 0, s>>>(rs, pp ? (k & 1) : -1);
     CUDA_TRY(cudaGetLastError());
     for (int r = 0; r < P; ++r)

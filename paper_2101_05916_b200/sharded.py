@@ -65,12 +65,31 @@ def slab_plan(n0: int, nranks: int, rank: int, halo: int) -> dict:
 
 
 class Comm:
-    """NCCL communicator of the library, bootstrapped over torch.distributed."""
+    """Communicator of the library, bootstrapped over torch.distributed.
 
-    def __init__(self, ctx: hj.Context, rank: int, world: int, device):
+    p2p=False: NCCL (the unique id is broadcast by torch.distributed).
+    p2p=True: the peer-store communicator, no NCCL: the ranks' control blocks
+    are mapped over CUDA IPC (handles all-gathered by torch.distributed, any
+    backend, e.g. gloo); every per-sweep exchange runs on the devices."""
+
+    def __init__(self, ctx: hj.Context, rank: int, world: int, device, p2p: bool = False):
         import torch
         import torch.distributed as dist
         lib = abi.load()
+        self.rank, self.world = rank, world
+        if p2p:
+            h = C.c_void_p()
+            hj._check(lib.hjb_p2p_comm_create(ctx.handle, world, rank, C.byref(h)))
+            self.handle = h
+            mine = (C.c_uint8 * 64)()
+            hj._check(lib.hjb_comm_ctl_handle(h, mine))
+            allh = [bytes(mine)]
+            if world > 1:
+                allh = [None] * world
+                dist.all_gather_object(allh, bytes(mine))
+            buf = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(allh))
+            hj._check(lib.hjb_comm_open_peers(h, buf))
+            return
         uid = (C.c_uint8 * 128)()
         if rank == 0:
             hj._check(lib.hjb_nccl_unique_id(uid))
@@ -82,7 +101,6 @@ class Comm:
         h = C.c_void_p()
         hj._check(lib.hjb_comm_create(ctx.handle, world, rank, buf, C.byref(h)))
         self.handle = h
-        self.rank, self.world = rank, world
 
     def close(self):
         if self.handle:

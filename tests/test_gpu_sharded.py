@@ -327,3 +327,47 @@ def test_local_ranks_peer_store_converge_in_reference_iteration_count(gpu_ctx, m
     r, v = _local(gpu_ctx, w, c, cfg, 4, 0)
     assert r.iterations == meta["iterations"] == 16685 and r.converged
     assert hashlib.sha256(np.ascontiguousarray(v + 0.0).tobytes()).hexdigest() == meta["value_sha256"]
+
+
+def _mp_probe(np_, n, iters, tol=0.0):
+    """Run scripts/p2p_same_gpu_probe.py in np_ processes on this one GPU with
+    the peer-store communicator; one JSON report per rank."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, P2P_COMM="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={np_}",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(root / "scripts" / "p2p_same_gpu_probe.py"), str(n), str(iters), str(tol)]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    reps = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert out.returncode == 0 and len(reps) == np_, out.stdout[-2000:] + out.stderr[-2000:]
+    return reps
+
+
+@pytest.mark.parametrize("np_", [2, 3])
+def test_peer_store_comm_multiprocess_equal_solve(np_):
+    """The NCCL-free peer-store communicator between PROCESSES (CUDA IPC
+    control blocks and V buffers, halos stored by the sweep kernels, residual
+    and CFL-scan all-reduces through the ranks' mailboxes), here with all
+    ranks on this one GPU: every rank's slab and residual history equal the
+    single-process solve bit for bit."""
+    for rep in _mp_probe(np_, 21, 60):
+        assert rep["ok"] and rep["bitwise"] and rep["history_equal"], rep
+        assert rep["iterations"] == rep["ref_iterations"] == 60
+
+
+def test_peer_store_comm_multiprocess_converges():
+    """Two processes to convergence (config 2 at 21^4, tol 5e-3): the
+    reference's 16 685 iterations, V bitwise (epochs, mailbox slots and the
+    stop across thousands of positions)."""
+    for rep in _mp_probe(2, 21, 200000, 5e-3):
+        assert rep["ok"] and rep["bitwise"] and rep["converged"], rep
+        assert rep["iterations"] == rep["ref_iterations"] == 16685
