@@ -74,6 +74,12 @@ def parse():
                     help="run the slab-partitioned solve even at N = 1")
     ap.add_argument("--order", type=int, default=1, help="sharded: ENO order")
     ap.add_argument("--rk", type=int, default=1, help="sharded: TVD-RK order")
+    ap.add_argument("--comm", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="sharded transport: p2p = the NCCL-free peer-store communicator "
+                         "(halos stored by the sweep kernels over NVLink, device-side "
+                         "all-reduces; first order), nccl = NCCL send/recv + all-reduce; "
+                         "auto = p2p for first order, falling back to NCCL (all ranks "
+                         "together) if its set-up fails on any rank")
     return ap.parse_args()
 
 
@@ -515,7 +521,29 @@ def run_sharded(args):
         c.copy_(torch.tensor(np.repeat(band, s0)))
     cfg = hj.SolveConfig(**w.cfg.__dict__)
     cfg.max_iters, cfg.spatial_order, cfg.time_order = args.iters, args.order, args.rk
-    comm = sharded.Comm(ctx, rank, world, dev)
+    # transport: the peer-store communicator for first order (set-up checked on
+    # every rank; any failure sends all ranks to NCCL together), else NCCL
+    use_p2p = args.comm == "p2p" or (args.comm == "auto" and args.order == 1 and args.rk == 1)
+    comm, comm_kind = None, "nccl"
+    if use_p2p:
+        try:
+            comm = sharded.Comm(ctx, rank, world, dev, p2p=True)
+            ok = 1
+        except Exception as ex:  # e.g. no peer access between the GPUs
+            print(f"rank {rank}: peer-store communicator unavailable ({ex}); using NCCL",
+                  file=sys.stderr)
+            ok = 0
+        if world > 1:
+            t_ok = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+            ok = int(t_ok.item())
+        if ok:
+            comm_kind = "p2p"
+        elif comm is not None:
+            comm.close()
+            comm = None
+    if comm is None:
+        comm = sharded.Comm(ctx, rank, world, dev)
     try:
         for _ in range(max(3, args.warmup)):
             sharded.solve_sharded_dev(comm, g, w.model, w.dbounds(), c.data_ptr(), c.data_ptr(),
@@ -578,6 +606,9 @@ def run_sharded(args):
                          "peak_source": peak_src, "bytes_per_cell": bpc, "sweep_us": sweep * 1e6,
                          "kernel": "k_fast4d slab sweeps (boundary planes + interior) with the "
                                    "halo exchange and the residual all-reduce inside the loop"},
+            "transport": ("peer-store (sweep kernels store halos over NVLink, device-side "
+                          "all-reduces, no NCCL)" if comm_kind == "p2p" else
+                          "NCCL send/recv halos + all-reduce"),
             "e2e": {"value": cells * args.iters / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": cells * 8, "d2h_bytes_per_step": cells * 8,
                     "ms_per_step": e2e_s * 1e3,

@@ -1537,7 +1537,7 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   };
   op.finish = [&](int k, bool pp, cudaGraphConditionalHandle hd, int use, cudaStream_t s) -> int {
     unsigned long long* slot = pp ? &ctx->st->maxdv_slot[k & 1] : maxbits;
-    if (op.p2p) {  // device-side all-reduce over the ranks' mailboxes (NVLink atomics)
+    if (op.p2p || p2p_only) {  // device-side all-reduce over the ranks' mailboxes (NVLink atomics)
       MboxSet ms;
       ms.n = P;
       for (int q = 0; q < P; ++q) ms.m[q] = ctl_mbox(comm->peer_ctl[q]);
