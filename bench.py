@@ -76,10 +76,10 @@ def parse():
     ap.add_argument("--rk", type=int, default=1, help="sharded: TVD-RK order")
     ap.add_argument("--comm", default="auto", choices=["auto", "p2p", "nccl"],
                     help="sharded transport: p2p = the NCCL-free peer-store communicator "
-                         "(halos stored by the sweep kernels over NVLink, device-side "
-                         "all-reduces; first order), nccl = NCCL send/recv + all-reduce; "
-                         "auto = p2p for first order, falling back to NCCL (all ranks "
-                         "together) if its set-up fails on any rank")
+                         "(halos stored by the sweep / stage kernels over NVLink, device-side "
+                         "all-reduces), nccl = NCCL send/recv + all-reduce; auto = p2p, "
+                         "falling back to NCCL (all ranks together) if its set-up fails on "
+                         "any rank")
     return ap.parse_args()
 
 
@@ -521,9 +521,9 @@ def run_sharded(args):
         c.copy_(torch.tensor(np.repeat(band, s0)))
     cfg = hj.SolveConfig(**w.cfg.__dict__)
     cfg.max_iters, cfg.spatial_order, cfg.time_order = args.iters, args.order, args.rk
-    # transport: the peer-store communicator for first order (set-up checked on
-    # every rank; any failure sends all ranks to NCCL together), else NCCL
-    use_p2p = args.comm == "p2p" or (args.comm == "auto" and args.order == 1 and args.rk == 1)
+    # transport: the peer-store communicator (set-up checked on every rank;
+    # any failure sends all ranks to NCCL together)
+    use_p2p = args.comm in ("p2p", "auto")
     comm, comm_kind = None, "nccl"
     if use_p2p:
         try:

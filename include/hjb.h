@@ -320,8 +320,8 @@ int hjb_comm_destroy(hjb_comm* comm);
  * and the per-solve buffer handles also go through peer memory.  Set up:
  * create, export this rank's control-block IPC handle (64 bytes), all-gather
  * the handles on the host (e.g. torch.distributed with gloo), open them.
- * First-order solves only.  (The NCCL communicator takes the same transport
- * for its sweeps with HJB_SHARD_P2P=1.) */
+ * First order and ENO / TVD-RK stages.  (The NCCL communicator takes the
+ * same transport for its sweeps with HJB_SHARD_P2P=1.) */
 int hjb_p2p_comm_create(hjb_context* ctx, int32_t nranks, int32_t rank, hjb_comm** out);
 int hjb_comm_ctl_handle(hjb_comm* comm, void* out64);
 int hjb_comm_open_peers(hjb_comm* comm, const void* handles64xN);

@@ -371,11 +371,20 @@ __device__ __forceinline__ void chunk_planes(const A& a, uint32_t chunk, uint32_
   }
 }
 
-// publish the peer-store epoch to the neighbours (Fast4dArgs::p2p_*; the
-// stage kernels without peer stores have no such fields)
+// publish the peer-store epoch to the neighbours (Fast4dArgs / Ho4dArgs
+// p2p_* fields)
+// the neighbour-s address of a boundary plane's element (null: not a send
+// plane of side s, or no neighbour there)
+template <class A>
+__device__ __forceinline__ double* p2p_peer(const A& a, int s, uint32_t i0, uint64_t s0,
+                                           uint64_t off) {
+  return (a.p2p_dst[s] && i0 - a.p2p_src0[s] < a.p2p_R)
+             ? a.p2p_dst[s] + static_cast<uint64_t>(i0 - a.p2p_src0[s] + a.p2p_dst0[s]) * s0 + off
+             : nullptr;
+}
 template <class A>
 __device__ __forceinline__ void p2p_publish(const A& a) {
-  if constexpr (std::is_same<A, Fast4dArgs>::value) {
+  if constexpr (std::is_same<A, Fast4dArgs>::value || std::is_same<A, Ho4dArgs>::value) {
 #pragma unroll
     for (int s = 0; s < 2; ++s)
       if (a.p2p_flag[s])
@@ -385,7 +394,7 @@ __device__ __forceinline__ void p2p_publish(const A& a) {
 }
 template <class A>
 __device__ __forceinline__ bool p2p_on(const A& a) {
-  if constexpr (std::is_same<A, Fast4dArgs>::value)
+  if constexpr (std::is_same<A, Fast4dArgs>::value || std::is_same<A, Ho4dArgs>::value)
     return a.p2p_flag[0] != nullptr || a.p2p_flag[1] != nullptr;
   else
     return false;
@@ -1687,6 +1696,12 @@ __global__ void __launch_bounds__(ho4d_maxthreads(R)) k_ho4d(const __grid_consta
     }
     if (active)
       *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[1]);
+      if (a.p2p_R) {  // peer-store halos: a boundary plane into the neighbours' stage buffer
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd)
+          if (double* q = p2p_peer(a, sd, i0, s0, rowo))
+            *reinterpret_cast<double2*>(q) = make_double2(out[0], out[1]);
+      }
     // slide the axis-0 window
 #pragma unroll
     for (int q = 0; q < 2 * R; ++q) {
@@ -2194,6 +2209,16 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
           *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[kK - 1]);
         else
           dst[po + rowo] = out[0];
+        if (a.p2p_R) {  // peer-store halos: a boundary plane into the neighbours' stage buffer
+#pragma unroll
+          for (int sd = 0; sd < 2; ++sd)
+            if (double* q = p2p_peer(a, sd, i0, s0, rowo)) {
+              if (kK == 2)
+                *reinterpret_cast<double2*>(q) = make_double2(out[0], out[kK - 1]);
+              else
+                *q = out[0];
+            }
+        }
       }
 #pragma unroll
       for (int q = 0; q < 2 * R; ++q)
@@ -2704,26 +2729,34 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
       if (active) {
         // an odd n3's padding cell is the first axis-3 ghost: it holds V(n3-1)
         const double2 o = make_double2(out[0], odd_pad ? out[0] : out[1]);
-        double* p = dst + po + rowo;
-        *reinterpret_cast<double2*>(p) = o;
-        if (any_ghost) {
-          if (gl3) {
-            const double2 e = make_double2(o.x, o.x);
-            *reinterpret_cast<double2*>(p - 2) = e;
-            *reinterpret_cast<double2*>(p - 4) = e;
-          }
-          if (gh3) {
-            const double2 e = make_double2(o.y, o.y);
-            *reinterpret_cast<double2*>(p + 2) = e;
-            *reinterpret_cast<double2*>(p + 4) = e;
-          }
+        // the pencil and its ghost copies, at p (own buffer or a neighbour's)
+        auto put = [&](double* p) {
+          *reinterpret_cast<double2*>(p) = o;
+          if (any_ghost) {
+            if (gl3) {
+              const double2 e = make_double2(o.x, o.x);
+              *reinterpret_cast<double2*>(p - 2) = e;
+              *reinterpret_cast<double2*>(p - 4) = e;
+            }
+            if (gh3) {
+              const double2 e = make_double2(o.y, o.y);
+              *reinterpret_cast<double2*>(p + 2) = e;
+              *reinterpret_cast<double2*>(p + 4) = e;
+            }
 #pragma unroll
-          for (int k = 1; k <= R; ++k) {
-            if (gl1) *reinterpret_cast<double2*>(p - k * s1) = o;
-            if (gh1) *reinterpret_cast<double2*>(p + k * s1) = o;
-            if (gl2) *reinterpret_cast<double2*>(p - k * s2) = o;
-            if (gh2) *reinterpret_cast<double2*>(p + k * s2) = o;
+            for (int k = 1; k <= R; ++k) {
+              if (gl1) *reinterpret_cast<double2*>(p - k * s1) = o;
+              if (gh1) *reinterpret_cast<double2*>(p + k * s1) = o;
+              if (gl2) *reinterpret_cast<double2*>(p - k * s2) = o;
+              if (gh2) *reinterpret_cast<double2*>(p + k * s2) = o;
+            }
           }
+        };
+        put(dst + po + rowo);
+        if (a.p2p_R) {  // peer-store halos: a boundary plane (ghosts too) into the neighbours
+#pragma unroll
+          for (int sd = 0; sd < 2; ++sd)
+            if (double* q = p2p_peer(a, sd, i0, s0, rowo)) put(q);
         }
       }
     };

@@ -184,6 +184,13 @@ struct Ho4dArgs {
   // input-free rows, as Fast4dArgs::gax / gbx / glin
   int gen;
   int gax[4], gbx[4], glin;
+  // peer-store halos of the sharded stages (as Fast4dArgs::p2p_*): a
+  // boundary plane's stores (ghost cells included) also go into the
+  // neighbour's same stage buffer
+  double* p2p_dst[2];
+  uint32_t p2p_src0[2], p2p_dst0[2], p2p_R;
+  unsigned int* p2p_flag[2];
+  unsigned int p2p_epoch;
   // ghost widths of the stage-buffer layout [n0][n1 + 2gh][n2 + 2gh][n3p + 2g3]
   // (k_eno3g: 3 and 4; k_ho4t / k_ho4d: 0, the plain padded layout)
   uint32_t gh, g3;

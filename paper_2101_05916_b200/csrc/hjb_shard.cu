@@ -355,7 +355,7 @@ struct SlabRank {
   // and the epoch the next launch publishes
   struct P2PLink {
     bool on = false;
-    double* peer_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][buffer]
+    double* peer_buf[2][4] = {};  // [side][buffer: V parity 0 / 1, stage1, stage2]
     uint32_t dst0[2] = {0u, 0u};
     unsigned int* peer_flag[2] = {nullptr, nullptr};
     unsigned int* own_flag[2] = {nullptr, nullptr};
@@ -406,6 +406,20 @@ cudaError_t SlabRank::launch(int k, int q, int mode, unsigned long long* slot,
   }
   Ho4dArgs x = mode == kBnd ? hb : (mode == kInner ? hi : hc);
   x.mdv = slot;
+  if (p2p.on && mode == kBoth) {  // stage output's boundary planes into the neighbours
+    const Halo h = halo_of(geo);
+    const int d = stages[q].dst;
+    const int ob = d == 0 ? ((k & 1) ? 0 : 1) : (d == 1 ? 2 : 3);
+    x.p2p_R = h.planes;
+    x.p2p_epoch = p2p.epoch;
+    for (int sd = 0; sd < 2; ++sd) {
+      x.p2p_dst[sd] = p2p.peer_buf[sd][ob];
+      x.p2p_flag[sd] = p2p.peer_flag[sd];
+      x.p2p_dst0[sd] = p2p.dst0[sd];
+    }
+    x.p2p_src0[0] = h.send_lo;
+    x.p2p_src0[1] = h.send_hi;
+  }
   x.pmode = 1;  // position parity == iteration parity (even body, loop from 0)
   x.parity = k & 1;
   x.src_sel = stages[q].src;
@@ -767,8 +781,8 @@ int p2p_allreduce(const LoopState* st, LoopState* st_w, int slot, const MboxSet&
 // neighbours' allocations are mapped with peer access (NVLink).  The opened
 // mappings are closed when the solve returns (IpcPeers).
 struct IpcBlob {
-  cudaIpcMemHandle_t buf[2];
-  uint32_t recv_lo, recv_hi, pad[2];
+  cudaIpcMemHandle_t buf[4];  // V parity 0 / 1, stage1, stage2 (ENO / TVD-RK)
+  uint32_t nbuf, recv_lo, recv_hi, pad;
 };
 static_assert(sizeof(P2PMbox) <= kScanOffset - kMboxOffset, "control block: residual mailbox");
 static_assert(sizeof(ScanMbox) <= kBlobOffset - kScanOffset, "control block: scan mailbox");
@@ -816,8 +830,8 @@ int link_ipc_p2p(Nccl* api, hjb_comm* comm, SlabRank& rk, cudaStream_t s, IpcPee
   if ((rc = comm_open_peers(api, comm, s))) return rc;
   IpcBlob mine;
   std::memset(&mine, 0, sizeof mine);
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[0], rk.buf[0]));
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[1], rk.buf[1]));
+  mine.nbuf = rk.ho ? 4u : 2u;
+  for (uint32_t b = 0; b < mine.nbuf; ++b) CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[b], rk.buf[b]));
   const Halo h = halo_of(rk.geo);
   mine.recv_lo = h.recv_lo;
   mine.recv_hi = h.recv_hi;
@@ -845,7 +859,7 @@ int link_ipc_p2p(Nccl* api, hjb_comm* comm, SlabRank& rk, cudaStream_t s, IpcPee
   l.on = true;
   for (int sd = 0; sd < 2; ++sd) {
     if (!(sd == 0 ? rk.geo.has_lo : rk.geo.has_hi)) continue;
-    for (int b = 0; b < 2; ++b) {
+    for (uint32_t b = 0; b < nbr[sd].nbuf; ++b) {
       void* p = nullptr;
       CUDA_TRY(cudaIpcOpenMemHandle(&p, nbr[sd].buf[b], cudaIpcMemLazyEnablePeerAccess));
       peers.opened.push_back(p);
@@ -868,8 +882,8 @@ int link_ipc_p2p(Nccl* api, hjb_comm* comm, SlabRank& rk, cudaStream_t s, IpcPee
 int link_blob_p2p(hjb_comm* comm, SlabRank& rk, IpcPeers& peers) {
   IpcBlob mine;
   std::memset(&mine, 0, sizeof mine);
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[0], rk.buf[0]));
-  CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[1], rk.buf[1]));
+  mine.nbuf = rk.ho ? 4u : 2u;
+  for (uint32_t b = 0; b < mine.nbuf; ++b) CUDA_TRY(cudaIpcGetMemHandle(&mine.buf[b], rk.buf[b]));
   const Halo h = halo_of(rk.geo);
   mine.recv_lo = h.recv_lo;
   mine.recv_hi = h.recv_hi;
@@ -893,7 +907,7 @@ int link_blob_p2p(hjb_comm* comm, SlabRank& rk, IpcPeers& peers) {
     if (seen < ep) return set_err(HJB_ERR_RUNTIME, "peer-store link: neighbour did not publish");
     IpcBlob nb;
     CUDA_TRY(cudaMemcpy(&nb, pc + kBlobOffset, sizeof nb, cudaMemcpyDeviceToHost));
-    for (int b = 0; b < 2; ++b) {
+    for (uint32_t b = 0; b < nb.nbuf; ++b) {
       void* p = nullptr;
       CUDA_TRY(cudaIpcOpenMemHandle(&p, nb.buf[b], cudaIpcMemLazyEnablePeerAccess));
       peers.opened.push_back(p);
@@ -915,13 +929,13 @@ void link_local_p2p(std::vector<SlabRank>& rks, unsigned int* flags) {
     l = SlabRank::P2PLink();
     l.on = true;
     if (r > 0) {
-      for (int b = 0; b < 2; ++b) l.peer_buf[0][b] = rks[r - 1].buf[b];
+      for (int b = 0; b < 4; ++b) l.peer_buf[0][b] = rks[r - 1].buf[b];
       l.dst0[0] = halo_of(rks[r - 1].geo).recv_hi;
       l.peer_flag[0] = flags + 2 * (r - 1) + 1;  // the lower rank's "from above"
       l.own_flag[0] = flags + 2 * r;
     }
     if (r < P - 1) {
-      for (int b = 0; b < 2; ++b) l.peer_buf[1][b] = rks[r + 1].buf[b];
+      for (int b = 0; b < 4; ++b) l.peer_buf[1][b] = rks[r + 1].buf[b];
       l.dst0[1] = halo_of(rks[r + 1].geo).recv_lo;
       l.peer_flag[1] = flags + 2 * (r + 1);  // the upper rank's "from below"
       l.own_flag[1] = flags + 2 * r + 1;
@@ -1379,8 +1393,6 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   const bool p2p_only = comm->comm == nullptr;
   Nccl* api = p2p_only ? nullptr : nccl();
   if (!p2p_only && !api) return set_err(HJB_ERR_NCCL, "libnccl.so.2 not loadable");
-  if (p2p_only && cfg && (cfg->spatial_order > 1 || cfg->time_order > 1))
-    return set_err(HJB_ERR_UNSUPPORTED, "solve_sharded: the peer-store communicator runs first order");
   if (p2p_only && comm->nranks == 1 && !comm->peers_open) {  // a single rank is its own peer
     comm->peer_ctl.assign(1, comm->p2p_flags);
     comm->peers_open = true;
@@ -1512,7 +1524,7 @@ int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* gi,
   // the halo planes over NVLink
   if (P > 1 && p2p_only) {
     op.p2p = true;
-  } else if (P > 1 && !rk.ho && shard_p2p()) {
+  } else if (P > 1 && shard_p2p()) {
     if ((rc = link_ipc_p2p(api, comm, rk, ctx->stream, ipc))) return rc;
     op.p2p = true;
   }
@@ -1694,7 +1706,7 @@ int hjb_solve_sharded_local_dev(hjb_context* ctx, int32_t nranks, const hjb_grid
   // neighbours' halo planes; one epoch counter for all ranks
   DevBuf p2p_flags;
   unsigned int p2p_seq = 0;
-  if (P > 1 && !rks[0].ho && shard_p2p()) {
+  if (P > 1 && shard_p2p()) {
     CUDA_TRY(p2p_flags.ensure(2 * static_cast<size_t>(P) * sizeof(unsigned int)));
     CUDA_TRY(cudaMemsetAsync(p2p_flags.p, 0, 2 * static_cast<size_t>(P) * sizeof(unsigned int),
                              ctx->stream));

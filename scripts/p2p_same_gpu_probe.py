@@ -10,7 +10,7 @@ prints one JSON line: ok, iterations, and bitwise equality of its slab with
 the single-process solve.
 
     P2P_COMM=1 python -m torch.distributed.run --nproc-per-node 2 \
-        --master-addr 127.0.0.1 scripts/p2p_same_gpu_probe.py [n=21] [iters=60] [tol=0]
+        --master-addr 127.0.0.1 scripts/p2p_same_gpu_probe.py [n=21] [iters=60] [tol=0] [order=1]
 """
 import json
 import os
@@ -33,6 +33,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 21
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 60
     tol = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+    order = int(sys.argv[4]) if len(sys.argv) > 4 else 1  # ENO order = TVD-RK order
     p2p = os.environ.get("P2P_COMM", "0") == "1"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
@@ -46,7 +47,8 @@ def main():
     c_full = band_np(g, 0, -4.0, 4.0)
     c = torch.tensor(c_full[b * s0:e * s0], device=dev)
     out = torch.empty_like(c)
-    cfg = hj.SolveConfig(tolerance=tol if tol > 0 else 1e-12, max_iters=iters)
+    cfg = hj.SolveConfig(tolerance=tol if tol > 0 else 1e-12, max_iters=iters,
+                         spatial_order=order, time_order=order)
     rep = {"rank": rank, "p2p_comm": p2p, "shard_p2p": os.environ.get("HJB_SHARD_P2P", "0")}
     try:
         comm = sharded.Comm(ctx, rank, world, dev, p2p=p2p)

@@ -329,7 +329,7 @@ def test_local_ranks_peer_store_converge_in_reference_iteration_count(gpu_ctx, m
     assert hashlib.sha256(np.ascontiguousarray(v + 0.0).tobytes()).hexdigest() == meta["value_sha256"]
 
 
-def _mp_probe(np_, n, iters, tol=0.0):
+def _mp_probe(np_, n, iters, tol=0.0, order=1):
     """Run scripts/p2p_same_gpu_probe.py in np_ processes on this one GPU with
     the peer-store communicator; one JSON report per rank."""
     import json
@@ -345,7 +345,7 @@ def _mp_probe(np_, n, iters, tol=0.0):
     env = dict(os.environ, P2P_COMM="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={np_}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
-           str(root / "scripts" / "p2p_same_gpu_probe.py"), str(n), str(iters), str(tol)]
+           str(root / "scripts" / "p2p_same_gpu_probe.py"), str(n), str(iters), str(tol), str(order)]
     out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     reps = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert out.returncode == 0 and len(reps) == np_, out.stdout[-2000:] + out.stderr[-2000:]
@@ -371,3 +371,31 @@ def test_peer_store_comm_multiprocess_converges():
     for rep in _mp_probe(2, 21, 200000, 5e-3):
         assert rep["ok"] and rep["bitwise"] and rep["converged"], rep
         assert rep["iterations"] == rep["ref_iterations"] == 16685
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("order,rk,scheme", [(2, 2, "godunov"), (3, 3, "godunov"), (3, 3, "lf")])
+def test_local_ranks_peer_store_high_order_equal_solve(gpu_ctx, monkeypatch, P, order, rk, scheme):
+    """Peer-store halos for ENO / TVD-RK slabs: every stage's boundary planes
+    (ghost cells of the ENO3 layout included) go straight into the
+    neighbours' stage buffers; bitwise vs the single-GPU solve."""
+    monkeypatch.setenv("HJB_SHARD_P2P", "1")
+    w = configs.config2(21)
+    c = band_np(w.grid, 0, -4.0, 4.0)
+    cfg = hj.SolveConfig(tolerance=1e-4, max_iters=20, spatial_order=order, time_order=rk)
+    if scheme == "lf":
+        cfg.scheme = hj.LAX_FRIEDRICHS
+    ref = hj.solve(hj.ScalarField(w.grid, c), hj.ScalarField(w.grid, c), w.model, w.dbounds(), cfg,
+                   ctx=gpu_ctx)
+    r, v = _local(gpu_ctx, w, c, cfg, P, 20)
+    assert r.iterations == ref.iterations == 20 and r.dt == ref.dt
+    assert same(r.residual_history, ref.residual_history)
+    assert same(v, ref.value.values())
+
+
+def test_peer_store_comm_multiprocess_eno3_rk3():
+    """ENO3 + TVD-RK3 slabs (config 3's scheme) between 3 processes on the
+    NCCL-free communicator: bitwise vs the single-process solve."""
+    for rep in _mp_probe(3, 21, 10, 0.0, 3):
+        assert rep["ok"] and rep["bitwise"] and rep["history_equal"], rep
+        assert rep["iterations"] == rep["ref_iterations"] == 10
