@@ -327,11 +327,15 @@ int hjb_comm_ctl_handle(hjb_comm* comm, void* out64);
 int hjb_comm_open_peers(hjb_comm* comm, const void* handles64xN);
 /* solve() over a slab-partitioned 4D grid: init/c/value_out hold this rank's
  * owned planes [begin, end) of `global_grid` (reference layout, device
- * pointers).  Per sweep / RK stage: boundary planes, then the NCCL halo
- * exchange on a second stream overlapped with the interior planes, then the
- * all-reduce(max) of max|dV| and the device epilogue; bitwise identical to
- * hjb_solve_dev.  4D fast-path models with constant bounds, first order or
- * ENO/TVD-RK (halo = ENO order), Godunov or Lax-Friedrichs. */
+ * pointers).  Per sweep / RK stage: one launch with the boundary planes
+ * first; with an NCCL communicator the halos then travel by NCCL send/recv on
+ * a second stream while the interior planes sweep (HJB_SHARD_P2P=1: stored
+ * by the kernel into the neighbours, as below); with a peer-store
+ * communicator (hjb_p2p_comm_create) the kernel itself stores the boundary
+ * planes into the neighbours' halos and the all-reduces run on the devices.
+ * Then the all-reduce(max) of max|dV| and the device epilogue; bitwise
+ * identical to hjb_solve_dev.  4D fast-path models with constant bounds,
+ * first order or ENO/TVD-RK (halo = ENO order), Godunov or Lax-Friedrichs. */
 int hjb_solve_sharded_dev(hjb_context* ctx, hjb_comm* comm, const hjb_grid* global_grid,
                           const hjb_model* model, const hjb_dbounds* dbounds,
                           const double* init_slab, const double* c_slab,
