@@ -598,8 +598,10 @@ __device__ __forceinline__ void lds_pn(const double* p, double* v) {
   }
 }
 
+// PS: peer-store halos (sharded slabs: Fast4dArgs::p2p_*); its own
+// instantiation, so the single-GPU sweep carries no peer-store code
 template <class S, int kK, int MAXT, int SCH, int PV = 0, bool CP = false, bool TG = false,
-          bool MS = false>
+          bool MS = false, bool PS = false>
 __global__ void __launch_bounds__(MAXT, 1)
     k_fast4d(const __grid_constant__ Fast4dArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1288,7 +1290,7 @@ __global__ void __launch_bounds__(MAXT, 1)
 #pragma unroll
           for (int c = 0; c < kK; c += 2)
             *reinterpret_cast<double2*>(op + c) = make_double2(out[c], out[c + 1]);
-          if (!MS && a.p2p_R) {  // peer-store halos: this plane into a neighbour's halo
+          if constexpr (PS) {  // peer-store halos: this plane into a neighbour's halo
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
               if (a.p2p_dst[s] && i0 - a.p2p_src0[s] < a.p2p_R) {
@@ -3124,10 +3126,10 @@ static bool smem_attr_once(std::atomic<unsigned long long>& done, K kernel) {
 }
 
 template <class S, int K, int MAXT, int SCH = 0, int PV = 0, bool CP = false, bool TG = false,
-          bool MS = false>
+          bool MS = false, bool PS = false>
 static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS>)) return;
+  if (!smem_attr_once(attr, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS, PS>)) return;
   if (MS) {  // persistent over sweeps: every CTA must be resident (grid barrier)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.blocks);
@@ -3139,12 +3141,13 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS>, a);
+    const cudaError_t e =
+        cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS, PS>, a);
     if (e != cudaSuccess) t_attr_err = e;
     return;
   }
   if (a.l2_bytes == 0 && !a.pdl) {
-    k_fast4d<S, K, MAXT, SCH, PV, CP, TG><<<a.blocks, a.threads, a.smem, s>>>(a);
+    k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS, PS><<<a.blocks, a.threads, a.smem, s>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -3170,7 +3173,7 @@ static void launch_one(const Fast4dArgs& a, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS>, a);
+  cudaLaunchKernelEx(&cfg, k_fast4d<S, K, MAXT, SCH, PV, CP, TG, MS, PS>, a);
 }
 
 // kernel variants (cells per thread, CTA thread bound): the tile search and
@@ -3251,8 +3254,37 @@ static void launch_gen(const Fast4dArgs& a, cudaStream_t s) {
     cp ? launch_one<ShapeGen, 2, 576, 0, 0, true>(a, s) : launch_one<ShapeGen, 2, 576>(a, s);
 }
 
+// peer-store slab sweeps (Fast4dArgs::p2p_R != 0): the sharded
+// configurations only — 2-cell pencils, 576 threads Godunov / 448 LF (384
+// for the run-time-shape LF), field constraint, constant bounds
+template <class S>
+static cudaError_t launch_ps(const Fast4dArgs& a, cudaStream_t s) {
+  if (a.kcells != 2 || a.pv || a.target || a.ms || a.cplane) return cudaErrorInvalidValue;
+  if (a.lf == 1) {
+    if (S::GEN) launch_one<S, 2, 384, 1, 0, false, false, false, true>(a, s);
+    else launch_one<S, 2, 448, 1, 0, false, false, false, true>(a, s);
+  } else if (a.lf == 2) {
+    if (S::GEN) launch_one<S, 2, 384, 2, 0, false, false, false, true>(a, s);
+    else launch_one<S, 2, 448, 2, 0, false, false, false, true>(a, s);
+  } else if (a.maxthreads == 448) {
+    launch_one<S, 2, 448, 0, 0, false, false, false, true>(a, s);
+  } else {
+    launch_one<S, 2, 576, 0, 0, false, false, false, true>(a, s);
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_fast4d(const Fast4dArgs& a, int shape, cudaStream_t s) {
   t_attr_err = cudaSuccess;
+  if (a.p2p_R) {
+    const cudaError_t e = shape == 0   ? launch_ps<ShapePlanarD0>(a, s)
+                          : shape == 1 ? launch_ps<ShapePlanarD1>(a, s)
+                          : shape == 2 ? launch_ps<ShapeTwin>(a, s)
+                                       : launch_ps<ShapeGen>(a, s);
+    if (e != cudaSuccess) return e;
+    if (t_attr_err != cudaSuccess) return t_attr_err;
+    return cudaGetLastError();
+  }
   if (shape == kShapeGen && (a.kcells != 2 || (a.target && a.lf) || (a.pv && (a.lf || a.target))))
     return cudaErrorInvalidValue;  // not a configuration of the run-time-shape variant
   if (shape == 0)
