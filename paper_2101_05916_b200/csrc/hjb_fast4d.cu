@@ -1790,7 +1790,7 @@ __host__ __device__ constexpr int ho4t_maxthreads(int r, int kc) {
   return kc == 1 ? 512 : ho4d_maxthreads(r);
 }
 
-template <class S, int R, int KC, int SCH = 0>
+template <class S, int R, int KC, int SCH = 0, bool PS = false>  // PS: peer-store slabs
 __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
     k_ho4t(const __grid_constant__ Ho4dArgs a) {
   constexpr int kK = KC;
@@ -2211,7 +2211,7 @@ __global__ void __launch_bounds__(ho4t_maxthreads(R, KC))
           *reinterpret_cast<double2*>(dst + po + rowo) = make_double2(out[0], out[kK - 1]);
         else
           dst[po + rowo] = out[0];
-        if (a.p2p_R) {  // peer-store halos: a boundary plane into the neighbours' stage buffer
+        if constexpr (PS) {  // peer-store halos: a boundary plane into the neighbours' stage buffer
 #pragma unroll
           for (int sd = 0; sd < 2; ++sd)
             if (double* q = p2p_peer(a, sd, i0, s0, rowo)) {
@@ -2332,7 +2332,7 @@ __host__ __device__ constexpr int eno3g_threads(int sch) {
   return sch ? kEno3gThreadsLF : kEno3gThreads;
 }
 
-template <class S, int SCH = 0, bool CP = false>
+template <class S, int SCH = 0, bool CP = false, bool PS = false>  // PS: peer-store slabs
 __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
     k_eno3g(const __grid_constant__ Ho4dArgs a) {
   constexpr int R = 3, kK = 2;
@@ -2755,7 +2755,7 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
           }
         };
         put(dst + po + rowo);
-        if (a.p2p_R) {  // peer-store halos: a boundary plane (ghosts too) into the neighbours
+        if constexpr (PS) {  // peer-store halos: a boundary plane (ghosts too) into the neighbours
 #pragma unroll
           for (int sd = 0; sd < 2; ++sd)
             if (double* q = p2p_peer(a, sd, i0, s0, rowo)) put(q);
@@ -3465,22 +3465,38 @@ void ho4d_bfirst(Ho4dArgs& a, int sms, uint32_t b0, uint32_t e0, uint32_t b1, ui
 }
 
 namespace {
-template <class S, int R, int KC, int SCH = 0>
+template <class S, int R, int KC, int SCH = 0, bool PS = false>
 void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (!smem_attr_once(attr, k_ho4t<S, R, KC, SCH>)) return;
-  k_ho4t<S, R, KC, SCH><<<a.blocks, a.threads, a.smem, s>>>(a);
+  if (!smem_attr_once(attr, k_ho4t<S, R, KC, SCH, PS>)) return;
+  k_ho4t<S, R, KC, SCH, PS><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
-template <class S, int SCH, bool CP = false>
+template <class S, int SCH, bool CP = false, bool PS = false>
 void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (!smem_attr_once(attr, k_eno3g<S, SCH, CP>)) return;
-  k_eno3g<S, SCH, CP><<<a.blocks, a.threads, a.smem, s>>>(a);
+  if (!smem_attr_once(attr, k_eno3g<S, SCH, CP, PS>)) return;
+  k_eno3g<S, SCH, CP, PS><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
+// peer-store slab sweeps (Ho4dArgs::p2p_R != 0) run their own instantiations
+// so the single-GPU kernels carry no peer-store code (compiled shapes only:
+// the sharded solve rejects run-time shapes at high order)
 template <class S, int R>
 void ho4t_launch(const Ho4dArgs& a, cudaStream_t s) {
+  if constexpr (!S::GEN) {
+    if (a.p2p_R) {
+      if (a.lf == 1)
+        ho4t_launch_k<S, R, 2, 1, true>(a, s);
+      else if (a.lf == 2)
+        ho4t_launch_k<S, R, 2, 2, true>(a, s);
+      else if (a.kc == 1)
+        ho4t_launch_k<S, R, 1, 0, true>(a, s);
+      else
+        ho4t_launch_k<S, R, 2, 0, true>(a, s);
+      return;
+    }
+  }
   if (a.lf == 1)  // Lax-Friedrichs: 2-cell pencils (ho_solve forces kc = 2)
     ho4t_launch_k<S, R, 2, 1>(a, s);
   else if (a.lf == 2)
@@ -3498,7 +3514,16 @@ cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
       case 1: ho4t_launch<S, 1>(a, s); break;
       case 2: ho4t_launch<S, 2>(a, s); break;
       default:
-        if (a.eno3g) {
+        if (a.eno3g && a.p2p_R) {
+          if constexpr (!S::GEN) {
+            if (a.lf == 1)
+              eno3g_launch<S, 1, false, true>(a, s);
+            else if (a.lf == 2)
+              eno3g_launch<S, 2, false, true>(a, s);
+            else
+              eno3g_launch<S, 0, false, true>(a, s);
+          }
+        } else if (a.eno3g) {
           if (a.lf == 1)
             eno3g_launch<S, 1>(a, s);
           else if (a.lf == 2)
