@@ -2,9 +2,10 @@
 
 usage: python scripts/run_configs.py [cfg ...] [--max-iters N] [--json out.json]
                                      [--no-cpu]
-  cfg in {1, 2, 3, 3c, 3ho, 4, 5}; default: 1 2
+  cfg in {1, 1ho, 2, 3, 3c, 3ho, 4, 5}; default: 1 2
 
-Config 1: 2D vertical subsystem 101^2 to convergence (tol 1e-4).
+Config 1: 2D vertical subsystem 101^2 to convergence (tol 1e-4); 1ho: with
+          BASELINE's scheme for it (ENO2 + TVD-RK2) next to first order.
 Config 2: 4D planar 51^4 to convergence (tol 1e-4) or --max-iters.
 Config 3: 4D planar 101^4 (first-order reference scheme) to convergence or cap;
           3c: the same to convergence through the adaptive chain
@@ -252,6 +253,34 @@ def run_config3_ho(max_iters, ctx, tol):
             "device_seconds_total": sum(x.wall_seconds for x in r.levels)}
 
 
+def run_config1_ho(ctx):
+    """Config 1 with BASELINE's own scheme: ENO2 + TVD-RK2 (Godunov), CFL
+    0.8, tol 1e-4, to convergence (k_small2d_ho); the safe set next to the
+    first-order reference scheme's.  No reference exists for the scheme (the
+    restatement pins it, tests/test_gpu_high_order.py::test_config1_eno2_rk2)."""
+    w = configs.config1()
+    c = device_constraint(w, ctx)
+    outs = {}
+    res = {}
+    for name, (order, rk) in (("eno2_rk2", (2, 2)), ("first_order", (1, 1))):
+        out = torch.empty_like(c)
+        cfg = hj.SolveConfig(**w.cfg.__dict__)
+        cfg.max_iters = 20000
+        cfg.spatial_order, cfg.time_order = order, rk
+        hj.solve_dev(w.grid, w.model, w.dbounds(), c.data_ptr(), c.data_ptr(), out.data_ptr(),
+                     cfg, ctx=ctx)  # warm (module load, graph build)
+        r = hj.solve_dev(w.grid, w.model, w.dbounds(), c.data_ptr(), c.data_ptr(),
+                         out.data_ptr(), cfg, ctx=ctx)
+        d = summarize(r, w.grid.size())
+        d["safe_cells"] = int((out <= 0).sum().item())
+        d["kernel"] = r.kernel
+        res[name] = d
+        outs[name] = out
+    a, b = outs["eno2_rk2"] <= 0, outs["first_order"] <= 0
+    res["safe_set_cells_differing"] = int((a != b).sum().item())
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cfgs", nargs="*", default=["1", "2"])
@@ -281,6 +310,8 @@ def main():
             out["3c"] = run_config3_chain(a.max_iters, ctx, a.cpu)
         elif k == "3ho":
             out["3ho"] = run_config3_ho(a.max_iters, ctx, a.tol3)
+        elif k == "1ho":
+            out["1ho"] = run_config1_ho(ctx)
         print(f"config {k}: {time.perf_counter() - t0:.1f} s wall", flush=True)
         if k != "4":
             print(json.dumps(out[k]), flush=True)
