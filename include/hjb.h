@@ -204,7 +204,9 @@ int hjb_vi_step(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
                 const hjb_dbounds* dbounds, const double* value, const double* constraint,
                 double dt, const hjb_solve_config* cfg, double* out);
 
-/* solve, reference solver.hpp:63-65 / solver.cpp:310-376. */
+/* solve, reference solver.hpp:63-65 / solver.cpp:310-376.  init may be the
+ * constraint pointer itself (the reference's cold solve, solve(c, c, ...),
+ * sim.cpp:282): the field is then copied to the device once. */
 int hjb_solve(hjb_context* ctx, const hjb_grid* grid, const hjb_model* model,
               const hjb_dbounds* dbounds, const double* init, const double* constraint,
               const hjb_solve_config* cfg, double* value_out, hjb_solve_result* result);

@@ -1225,7 +1225,11 @@ int hjb_solve(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const h
   const size_t bytes = static_cast<size_t>(g.size) * sizeof(double);
   CUDA_TRY(ctx->xbuf.ensure(bytes));
   CUDA_TRY(ctx->cbuf.ensure(bytes));
-  CUDA_TRY(cudaMemcpyAsync(ctx->xbuf.p, init, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  // the reference's cold solve passes one field as both (solve(c, c, ...),
+  // sim.cpp:282): it crosses the bus once and serves as init and constraint
+  const bool same = init == constraint;
+  if (!same)
+    CUDA_TRY(cudaMemcpyAsync(ctx->xbuf.p, init, bytes, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(cudaMemcpyAsync(ctx->cbuf.p, constraint, bytes, cudaMemcpyHostToDevice, ctx->stream));
   hjb_dbounds dbs;
   if ((rc = stage_dbounds(ctx, db, g.size, ctx->dbbuf, dbs))) return rc;
@@ -1237,7 +1241,8 @@ int hjb_solve(hjb_context* ctx, const hjb_grid* gi, const hjb_model* mi, const h
     cfgd.target = ctx->tgx.d();
     cfg = &cfgd;
   }
-  rc = solve_impl(ctx, gi, mi, &dbs, ctx->xbuf.d(), ctx->cbuf.d(), cfg, ctx->xbuf.d(), res);
+  rc = solve_impl(ctx, gi, mi, &dbs, same ? ctx->cbuf.d() : ctx->xbuf.d(), ctx->cbuf.d(), cfg,
+                  ctx->xbuf.d(), res);
   if (rc && rc != HJB_ERR_DIVERGED) return rc;
   const int status = rc;
   const std::string msg = g_err;

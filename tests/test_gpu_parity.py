@@ -36,6 +36,24 @@ def test_config1_converges_like_reference(gpu_ctx):
     assert int(np.sum(r.value.values() <= 0)) == 4544
 
 
+@pytest.mark.parametrize("order", [1, 3])
+def test_solve_with_one_field_as_init_and_constraint(gpu_ctx, oracle, order):
+    """hjb_solve copies an aliased init/constraint (the reference's cold
+    solve(c, c, ...), sim.cpp:282) once; the result is the two-buffer one,
+    and the host field is left untouched."""
+    case = with_iters(workload_case(configs.config2(13)), 40)
+    cfg = hj.SolveConfig(**case.cfg.__dict__)
+    cfg.spatial_order = cfg.time_order = order
+    c = case.c_field()
+    before = c.values().copy()
+    want = oracle.solve(case.init_field(), case.c_field(), case.model, case.db, cfg)
+    got = hj.solve(c, c, case.model, case.db, cfg, ctx=gpu_ctx)
+    assert got.iterations == want.iterations == 40
+    assert same(got.residual_history, want.residual_history)
+    assert same(got.value.values(), want.value.values())
+    assert np.array_equal(c.values(), before)
+
+
 @pytest.mark.parametrize("n,iters", [(21, 200), (51, 10)])
 def test_config2_k_iterations(gpu_ctx, oracle, n, iters):
     case = with_iters(workload_case(configs.config2(n)), iters)
