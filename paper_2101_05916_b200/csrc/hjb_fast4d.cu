@@ -2414,8 +2414,8 @@ __global__ void __launch_bounds__(eno3g_threads(SCH), 1)
     const bool active = in_tile && i1 < n1 && i2 < n2 && i3u < n3p;
     const uint32_t i3 = i3u < n3p ? i3u : n3p - kK;  // clamped for addressing
     const uint32_t ci1 = active ? i1 : 0u, ci2 = active ? i2 : 0u;
-    const uint64_t s2 = n3p + 2 * a.g3, s1 = (uint64_t)(n2 + 2 * a.gh) * s2,
-                   s0 = (uint64_t)(n1 + 2 * a.gh) * s1;
+    // ghost-layout strides in 32 bits (ho4d_config: a plane < 2^28 cells)
+    const uint32_t s2 = n3p + 2 * a.g3, s1 = (n2 + 2 * a.gh) * s2, s0 = (n1 + 2 * a.gh) * s1;
     const uint64_t rowo = (uint64_t)(ci1 + a.gh) * s1 + (uint64_t)(ci2 + a.gh) * s2 + i3 + a.g3;
     const double inv0 = a.inv[0], inv1 = a.inv[1], inv2 = a.inv[2], inv3 = a.inv[3];
     const uint32_t W2 = a.T2 + 2 * R;
@@ -3333,7 +3333,10 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
     const char* ek = std::getenv("HJB_HO_KC");
     a.kc = (ek && std::atoi(ek) == 1 && a.lf == 0 && !a.gen) ? 1u : 2u;  // LF / run-time shapes: 2 cells
     const char* eg = std::getenv("HJB_HO_ENO3G");
-    a.eno3g = (R == 3 && a.kc == 2 && !a.gen && !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
+    // k_eno3g keeps its ghost-layout strides in 32 bits (a plane < 2^28 cells)
+    const bool small_plane = (uint64_t)(g.n[1] + 6) * (g.n[2] + 6) * (g.n[3] + 10) < (1ull << 28);
+    a.eno3g = (R == 3 && a.kc == 2 && !a.gen && small_plane &&
+               !(eg && std::strcmp(eg, "0") == 0)) ? 1 : 0;
     const uint32_t nbar = 2u;  // mbarriers per ring slot
     const uint32_t maxc =
         (uint32_t)(a.eno3g ? eno3g_threads(a.lf) : ho4t_maxthreads(a.order, (int)a.kc)) - 32;
