@@ -620,6 +620,24 @@ def run_sharded(args):
         dist.destroy_process_group()
 
 
+def arm_watchdog(rank):
+    """Multi-rank runs wait on their neighbours (stream waits on peer epochs,
+    NCCL); if a peer never arrives the job would block forever.  After
+    HJB_BENCH_WATCHDOG_S seconds (default 900) each rank reports and exits
+    non-zero instead, which tears its context (and the waits) down."""
+    limit = float(os.environ.get("HJB_BENCH_WATCHDOG_S", "900"))
+
+    def fire():
+        print(json.dumps({"error": f"rank {rank}: multi-GPU run exceeded {limit:.0f} s "
+                                   "(watchdog); exiting"}), flush=True)
+        os._exit(3)
+
+    t = threading.Timer(limit, fire)
+    t.daemon = True
+    t.start()
+    return t
+
+
 def main():
     args = parse()
     rank, world, _ = dist_env()
@@ -628,6 +646,8 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     elif world > 1 or args.sharded:
+        if world > 1:
+            arm_watchdog(rank)
         run_sharded(args)
     else:
         run_single(args)
