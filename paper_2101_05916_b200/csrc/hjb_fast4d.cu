@@ -2328,12 +2328,16 @@ constexpr int kEno3gThreads = HJB_ENO3G_THREADS;
 #define HJB_ENO3G_THREADS_LF 384
 #endif
 constexpr int kEno3gThreadsLF = HJB_ENO3G_THREADS_LF;
+// Godunov's second thread bound (see k_eno3g's TB)
+constexpr int kEno3gThreadsSmall = 384;
 __host__ __device__ constexpr int eno3g_threads(int sch) {
   return sch ? kEno3gThreadsLF : kEno3gThreads;
 }
 
-template <class S, int SCH = 0, bool CP = false, bool PS = false>  // PS: peer-store slabs
-__global__ void __launch_bounds__(eno3g_threads(SCH), 1)
+// TB: a smaller thread bound (384: 166 registers, no spills) for the grids
+// whose tiling loses little to the smaller tile (ho4d_config picks it)
+template <class S, int SCH = 0, bool CP = false, bool PS = false, int TB = 0>  // PS: peer-store slabs
+__global__ void __launch_bounds__(TB ? TB : eno3g_threads(SCH), 1)
     k_eno3g(const __grid_constant__ Ho4dArgs a) {
   constexpr int R = 3, kK = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -3348,6 +3352,9 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
     uint32_t bt1 = 0, bt2 = 0, bt3 = 0, bring = 0;
     double bcost = 1e30;
     const uint32_t want_ring = 4;
+    auto search = [&](const uint32_t maxc) {
+    bt1 = bt2 = bt3 = bring = 0;
+    bcost = 1e30;
     const char* ft3 = std::getenv("HJB_HO_T3");  // experiment override of the segment width
     const uint32_t only_t3 = ft3 ? (uint32_t)std::atoi(ft3) : 0u;
     // segment width: full rows up to 64 cells, else 24..40 (measured on
@@ -3379,6 +3386,32 @@ void ho4d_config(const DevGrid& g, int sms, Ho4dArgs& a) {
             bring = ring;
           }
         }
+    }
+    };
+    search(maxc);
+    // k_eno3g Godunov, single GPU: the 384-thread bound (166 registers, no
+    // spills) is picked where the 512-thread tiling cannot fill its CTA (at
+    // most 88 % of the consumer threads busy) and the smaller tile's box
+    // cells per useful cell stay within 1.2x: 51^4 426 -> 374 us, 81^4 2152
+    // -> 1993 us per RK3 step; every other measured size (26..121^4, whose
+    // 512-thread tiles are >= 90 % full) keeps the 512-thread kernel, which is
+    // faster there (profiles/round2_ab_eno3g_tb.log)
+    if (a.eno3g && a.lf == 0 && !a.tb_fixed && bt1) {
+      const char* etb = std::getenv("HJB_ENO3G_TB");  // 384 / 512: force; else the rule
+      const int force = etb ? std::atoi(etb) : 0;
+      if (force != kEno3gThreads) {
+        const uint32_t w1 = bt1, w2 = bt2, w3 = bt3, wr = bring;
+        const double wc = bcost;
+        const bool unfilled = 100u * (w1 * w2 * (w3 / a.kc)) <= 88u * maxc;
+        search((uint32_t)kEno3gThreadsSmall - 32);
+        if (!bt1 || (force != kEno3gThreadsSmall && (!unfilled || bcost > 1.2 * wc))) {
+          bt1 = w1;
+          bt2 = w2;
+          bt3 = w3;
+          bring = wr;
+          bcost = wc;
+        }
+      }
     }
     const char* e = std::getenv("HJB_HO_TMA");
     if (bt1 && !(e && std::strcmp(e, "0") == 0)) {
@@ -3475,11 +3508,11 @@ void ho4t_launch_k(const Ho4dArgs& a, cudaStream_t s) {
   k_ho4t<S, R, KC, SCH, PS><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
-template <class S, int SCH, bool CP = false, bool PS = false>
+template <class S, int SCH, bool CP = false, bool PS = false, int TB = 0>
 void eno3g_launch(const Ho4dArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (!smem_attr_once(attr, k_eno3g<S, SCH, CP, PS>)) return;
-  k_eno3g<S, SCH, CP, PS><<<a.blocks, a.threads, a.smem, s>>>(a);
+  if (!smem_attr_once(attr, k_eno3g<S, SCH, CP, PS, TB>)) return;
+  k_eno3g<S, SCH, CP, PS, TB><<<a.blocks, a.threads, a.smem, s>>>(a);
 }
 
 // peer-store slab sweeps (Ho4dArgs::p2p_R != 0) run their own instantiations
@@ -3531,8 +3564,12 @@ cudaError_t ho4d_shape(const Ho4dArgs& a, cudaStream_t s) {
             eno3g_launch<S, 1>(a, s);
           else if (a.lf == 2)
             eno3g_launch<S, 2>(a, s);
-          else if (a.cplane)  // per-plane constraint: Godunov only
+          else if (a.cplane && a.threads <= kEno3gThreadsSmall)  // per-plane constraint: Godunov only
+            eno3g_launch<S, 0, true, false, kEno3gThreadsSmall>(a, s);
+          else if (a.cplane)
             eno3g_launch<S, 0, true>(a, s);
+          else if (a.threads <= kEno3gThreadsSmall)
+            eno3g_launch<S, 0, false, false, kEno3gThreadsSmall>(a, s);
           else
             eno3g_launch<S, 0>(a, s);
         } else {

@@ -179,6 +179,9 @@ struct Ho4dArgs {
   // 1: ENO3 Godunov stage in k_eno3g (face-shared choices, patched boxes,
   //    three barriers per ring slot); 0: k_ho4t
   int eno3g;
+  // set before ho4d_config: keep k_eno3g's 512-thread tiling (the slab
+  // solves, whose peer-store instantiations have that bound only)
+  int tb_fixed;
   // run-time row shapes (k_ho4t<ShapeGen>, set before ho4d_config, which
   // then keeps k_eno3g off): the rows' table axes (no row on x0) and the
   // input-free rows, as Fast4dArgs::gax / gbx / glin

@@ -511,6 +511,7 @@ int setup_rank(int device, const Prepared& p, const hjb_solve_config* cfg, doubl
   h.cbeg = geo.cbeg;
   h.cend = geo.cend;
   fill_lf(p.hm.dm, scheme, galpha, h.lf, h.lp);
+  h.tb_fixed = 1;
   ho4d_config(gloc, sms, h);
   if (h.lf && !h.tma)
     return set_err(HJB_ERR_UNSUPPORTED,

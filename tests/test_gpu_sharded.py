@@ -347,7 +347,14 @@ def _mp_probe(np_, n, iters, tol=0.0, order=1):
            "--master-addr=127.0.0.1", f"--master-port={port}",
            str(root / "scripts" / "p2p_same_gpu_probe.py"), str(n), str(iters), str(tol), str(order)]
     out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    reps = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    # the ranks share one stdout pipe: two reports can land on one line
+    reps, dec = [], json.JSONDecoder()
+    for ln in out.stdout.splitlines():
+        pos = ln.find("{")
+        while pos >= 0:
+            obj, end = dec.raw_decode(ln, pos)
+            reps.append(obj)
+            pos = ln.find("{", end)
     assert out.returncode == 0 and len(reps) == np_, out.stdout[-2000:] + out.stderr[-2000:]
     return reps
 
